@@ -1,0 +1,384 @@
+/*
+ * oracle.c — CPU ORACLE (test infrastructure only; see oracle.h for who may call it).
+ *
+ * A plain, slow, obviously-correct, single-threaded restatement of the Genome-on-Diet hot path
+ * (arXiv 2211.08157, PAPER.md).  No blocking, no fusion, no rolling state: every k-mer value is
+ * recomputed from its bases, every window minimum is recomputed by a scan of the window, the index
+ * is qsort + a linear scan, lookups are binary searches.  Readings where the paper is silent or
+ * garbled are SURVEY.md §8(c) O1-O9 (listed in DESIGN.md §2).
+ */
+#include "oracle.h"
+#include <stdlib.h>
+#include <string.h>
+
+/* ------------------------------------------------------------------------------------------ */
+/* O1 — alphabet and 2-bit encoding.  P:282 (alphabet ACGT + N), P:368/P:370 (2-bit encoding).  */
+int or_code(uint8_t b) {
+    switch (b) {
+        case 'A': case 'a': return 0;
+        case 'C': case 'c': return 1;
+        case 'G': case 'g': return 2;
+        case 'T': case 't': return 3;
+        default: return OR_N;
+    }
+}
+
+/* O2 — the diet pattern P[0..p-1] over {0,1}, weight x = #ones, beta = p/x.  P:282, P:286 (1). */
+int or_parse_pattern(const char* text, or_pattern* out) {
+    if (!text || !out) return -1;
+    size_t p = strlen(text);
+    if (p == 0 || p > 64) return -1;
+    uint32_t x = 0;
+    for (size_t i = 0; i < p; i++) {
+        if (text[i] == '1') { out->bit[i] = 1; x++; }
+        else if (text[i] == '0') out->bit[i] = 0;
+        else return -1;
+    }
+    if (x == 0) return -1;
+    out->p = (uint32_t)p;
+    out->x = x;
+    return 0;
+}
+
+/* O3 — patterned sequence PQ_s (PQ_s ⊆ {Q[i+s]·P[i mod p]}; P:308 with s = a; P:282 PR
+ * with s = 0).  Keep original position i iff i >= s and P[(i - s) mod p] = 1, in increasing i. */
+int64_t or_sparsify(const uint8_t* seq, uint64_t L, const or_pattern* P, uint32_t s, uint8_t* codes, uint64_t* orig) {
+    if (s >= P->p) return -1;
+    int64_t n = 0;
+    for (uint64_t i = 0; i < L; i++) {
+        if (i < s) continue;
+        if (P->bit[(i - s) % P->p] != 1) continue;
+        if (codes) codes[n] = (uint8_t)or_code(seq[i]);
+        if (orig) orig[n] = i;
+        n++;
+    }
+    return n;
+}
+
+/* O5 — Thomas Wang's invertible 64-bit integer hash (ref. 120), each step mod m = 4^k.  */
+uint64_t or_hash(uint64_t key, int k) {
+    uint64_t m = (k >= 32) ? ~0ull : ((1ull << (2 * k)) - 1);   /* mask = m - 1 */
+    key = (~key + (key << 21)) & m;      /* x1 = 2^21 x - x - 1 */
+    key = key ^ (key >> 24);             /* x2 */
+    key = (key + (key << 3) + (key << 8)) & m;  /* x3 = 265 x2 */
+    key = key ^ (key >> 14);             /* x4 */
+    key = (key + (key << 2) + (key << 4)) & m;  /* x5 = 21 x4 */
+    key = key ^ (key >> 28);             /* x6 */
+    key = (key + (key << 31)) & m;       /* H = (2^31 + 1) x6 */
+    return key;
+}
+
+void or_hash_batch(const uint64_t* x, uint64_t n, int k, uint64_t* out) {
+    for (uint64_t i = 0; i < n; i++) out[i] = or_hash(x[i], k);
+}
+
+/* ------------------------------------------------------------------------------------------ */
+/* O4 + O6 — double-strand (w,k)-minimizers of the patterned sequence.
+ *  P:286 (3): "computes minimizers of the patterned genome sequence ... the start location of each
+ *             minimizer in the original unpatterned reference genome".
+ *  P:294:     "the double-strand (w,k)-minimizer of a string is the smallest k-mer in a surrounding
+ *             window of w consecutive k-mers".
+ *  P:370:     an N terminates the current computation; restart after it.
+ * Step 1: t = Sparsify(seq, P, s) with orig[].
+ * Step 2: for each k-mer start j with t[j..j+k-1] free of N: fwd, rev, canonical, strand, hash;
+ *         palindromes (fwd == rev) are marked and never take part in a window minimum.
+ * Step 3: runs of consecutive valid starts (N-free segments).  Windows: every w consecutive
+ *         starts of a run, or the whole run if it has fewer than w starts.
+ * Step 4: in every window, every non-palindromic start whose hash equals the window minimum is
+ *         selected (all ties kept).  Output selected starts in increasing j.                  */
+int64_t or_minimizers(const uint8_t* seq, uint64_t L, const or_pattern* P, uint32_t s, int k, int w,
+                      uint64_t pos_base, or_mz* out, uint64_t cap) {
+    if (s >= P->p || k < 1 || k > 28 || w < 1) return -1;
+    int64_t n = or_sparsify(seq, L, P, s, NULL, NULL);
+    if (n < k) return 0;
+    uint8_t* t = (uint8_t*)malloc((size_t)n);
+    uint64_t* orig = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)n);
+    or_sparsify(seq, L, P, s, t, orig);
+    int64_t nk = n - k + 1;                       /* k-mer start positions 0..nk-1 */
+    uint8_t* valid = (uint8_t*)calloc((size_t)nk, 1);
+    uint8_t* pal = (uint8_t*)calloc((size_t)nk, 1);
+    uint8_t* z = (uint8_t*)calloc((size_t)nk, 1);
+    uint64_t* h = (uint64_t*)calloc((size_t)nk, sizeof(uint64_t));
+    uint8_t* sel = (uint8_t*)calloc((size_t)nk, 1);
+    /* step 2 */
+    for (int64_t j = 0; j < nk; j++) {
+        int ok = 1;
+        for (int i = 0; i < k; i++) if (t[j + i] == OR_N) { ok = 0; break; }
+        if (!ok) continue;
+        uint64_t fwd = 0, rev = 0;
+        for (int i = 0; i < k; i++) fwd = fwd * 4 + t[j + i];                     /* first base most significant */
+        for (int i = 0; i < k; i++) rev = rev * 4 + (uint64_t)(3 - t[j + k - 1 - i]); /* reverse complement */
+        valid[j] = 1;
+        if (fwd == rev) { pal[j] = 1; continue; }
+        uint64_t canon = fwd < rev ? fwd : rev;
+        z[j] = fwd > rev;
+        h[j] = or_hash(canon, k);
+    }
+    /* steps 3-4 */
+    int64_t j = 0;
+    while (j < nk) {
+        if (!valid[j]) { j++; continue; }
+        int64_t rs = j;
+        while (j < nk && valid[j]) j++;
+        int64_t re = j;                          /* run [rs, re) */
+        int64_t nrun = re - rs;
+        int64_t win = nrun >= w ? w : nrun;
+        for (int64_t a = rs; a + win <= re; a++) {
+            int have = 0; uint64_t mn = 0;
+            for (int64_t i = a; i < a + win; i++) {
+                if (pal[i]) continue;
+                if (!have || h[i] < mn) { mn = h[i]; have = 1; }
+            }
+            if (!have) continue;
+            for (int64_t i = a; i < a + win; i++) if (!pal[i] && h[i] == mn) sel[i] = 1;
+        }
+    }
+    int64_t cnt = 0;
+    for (int64_t q = 0; q < nk; q++) {
+        if (!sel[q]) continue;
+        if ((uint64_t)cnt < cap && out) { out[cnt].hash = h[q]; out[cnt].pos = pos_base + orig[q]; out[cnt].strand = z[q]; }
+        cnt++;
+    }
+    free(t); free(orig); free(valid); free(pal); free(z); free(h); free(sel);
+    return cnt;
+}
+
+int64_t or_minimizers_batch(const uint8_t* seq, const uint64_t* offsets, uint32_t n, const uint8_t* phases,
+                            const char* pattern, int k, int w, int global_pos, or_mz* out, uint64_t cap,
+                            uint64_t* out_offsets) {
+    or_pattern P;
+    if (or_parse_pattern(pattern, &P)) return -1;
+    uint64_t tot = 0;
+    for (uint32_t r = 0; r < n; r++) {
+        uint32_t s = phases ? phases[r] : 0;
+        if (out_offsets) out_offsets[r] = tot;
+        uint64_t room = tot < cap ? cap - tot : 0;
+        int64_t c = or_minimizers(seq + offsets[r], offsets[r + 1] - offsets[r], &P, s, k, w,
+                                  global_pos ? offsets[r] : 0, out ? out + (tot < cap ? tot : cap) : NULL, room);
+        if (c < 0) return -1;
+        tot += (uint64_t)c;
+    }
+    if (out_offsets) out_offsets[n] = tot;
+    return tot > cap && out ? -1 : (int64_t)tot;
+}
+
+/* ------------------------------------------------------------------------------------------ */
+/* O7 — the seed index.  P:286 (3) key = hash, value = list of start locations (original coords);
+ * P:294 "append the minimizer information to an array and sort the array after collecting ...
+ * then add it to the hash table"; P:302 discard minimizers occurring >= a user threshold.
+ * Cutoff (reading O7): n distinct hashes with counts a_0 <= ... <= a_{n-1}, m = floor(n*num/den),
+ * tau = a_{n-m-1}; keep h iff c(h) <= tau.  max_occ >= 0 overrides: keep iff c(h) <= max_occ.   */
+struct or_index {
+    or_pattern P; int k, w;
+    uint64_t n_kept;
+    uint64_t* hash; uint64_t* pos; uint8_t* strand;     /* kept entries, (hash,pos) order */
+    uint64_t n_keys; uint64_t* key; uint64_t* key_first; uint32_t* key_count;  /* distinct kept hashes */
+    or_index_stats st;
+};
+
+static int cmp_mz(const void* a, const void* b) {
+    const or_mz* x = (const or_mz*)a; const or_mz* y = (const or_mz*)b;
+    if (x->hash != y->hash) return x->hash < y->hash ? -1 : 1;
+    if (x->pos != y->pos) return x->pos < y->pos ? -1 : 1;
+    return 0;
+}
+static int cmp_u64(const void* a, const void* b) {
+    uint64_t x = *(const uint64_t*)a, y = *(const uint64_t*)b;
+    return x < y ? -1 : x > y;
+}
+
+/* Cutoff (reading O7 of SURVEY §8(c); "discard the most frequently (>= a user-defined
+ * threshold) occurring minimizers"): sort the n distinct-hash counts ascending a_0..a_{n-1},
+ * m = floor(n*num/den); tau = a_{n-m-1} (m = 0 gives tau = max count: keep all). */
+uint64_t or_cutoff_tau(const uint64_t* counts, uint64_t n, uint32_t num, uint32_t den, uint64_t* m_out) {
+    uint64_t m = den ? (uint64_t)(((unsigned __int128)n * num) / den) : 0;
+    if (m_out) *m_out = m;
+    if (n == 0 || m >= n) return 0;
+    uint64_t* a = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)n);
+    memcpy(a, counts, sizeof(uint64_t) * (size_t)n);
+    qsort(a, (size_t)n, sizeof(uint64_t), cmp_u64);
+    uint64_t tau = a[n - m - 1];
+    free(a);
+    return tau;
+}
+
+or_index* or_build_index(const uint8_t* ref, const uint64_t* offsets, uint32_t n, const char* pattern, int k, int w,
+                         uint32_t frac_num, uint32_t frac_den, int64_t max_occ) {
+    or_pattern P;
+    if (or_parse_pattern(pattern, &P) || k < 1 || k > 28 || w < 1 || (max_occ < 0 && frac_den == 0)) return NULL;
+    /* collect: E = multiset of (h, global pos, z) over every reference sequence, phase 0 */
+    int64_t tot = or_minimizers_batch(ref, offsets, n, NULL, pattern, k, w, 1, NULL, 0, NULL);
+    if (tot < 0) return NULL;
+    or_mz* E = (or_mz*)malloc(sizeof(or_mz) * (size_t)(tot ? tot : 1));
+    or_minimizers_batch(ref, offsets, n, NULL, pattern, k, w, 1, E, (uint64_t)tot, NULL);
+    /* sort */
+    qsort(E, (size_t)tot, sizeof(or_mz), cmp_mz);
+    /* count per distinct hash */
+    uint64_t nd = 0;
+    for (int64_t i = 0; i < tot; i++) if (i == 0 || E[i].hash != E[i - 1].hash) nd++;
+    uint64_t* cnt = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)(nd ? nd : 1));
+    uint64_t d = 0;
+    for (int64_t i = 0; i < tot; ) {
+        int64_t j = i;
+        while (j < tot && E[j].hash == E[i].hash) j++;
+        cnt[d++] = (uint64_t)(j - i);
+        i = j;
+    }
+    /* cutoff: fraction rule, or the absolute override (keep iff count <= max_occ) */
+    uint64_t m = 0, tau;
+    if (max_occ >= 0) tau = (uint64_t)max_occ;
+    else tau = or_cutoff_tau(cnt, nd, frac_num, frac_den, &m);
+    or_index* ix = (or_index*)calloc(1, sizeof(or_index));
+    ix->P = P; ix->k = k; ix->w = w;
+    ix->st.n_entries_all = (uint64_t)tot; ix->st.n_distinct_all = nd; ix->st.m = m; ix->st.tau = tau;
+    /* table: keep hashes with count <= tau */
+    ix->hash = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)(tot ? tot : 1));
+    ix->pos = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)(tot ? tot : 1));
+    ix->strand = (uint8_t*)malloc((size_t)(tot ? tot : 1));
+    ix->key = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)(nd ? nd : 1));
+    ix->key_first = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)(nd ? nd : 1));
+    ix->key_count = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)(nd ? nd : 1));
+    d = 0;
+    for (int64_t i = 0; i < tot; ) {
+        uint64_t c = cnt[d++];
+        if (c <= tau) {
+            ix->key[ix->n_keys] = E[i].hash;
+            ix->key_first[ix->n_keys] = ix->n_kept;
+            ix->key_count[ix->n_keys] = (uint32_t)c;
+            ix->n_keys++;
+            for (uint64_t q = 0; q < c; q++) {
+                ix->hash[ix->n_kept] = E[i + q].hash;
+                ix->pos[ix->n_kept] = E[i + q].pos;
+                ix->strand[ix->n_kept] = E[i + q].strand;
+                ix->n_kept++;
+            }
+            ix->st.kept_distinct++;
+            ix->st.kept_entries += c;
+        } else {
+            ix->st.dropped_distinct++;
+            ix->st.dropped_entries += c;
+        }
+        i += (int64_t)c;
+    }
+    free(cnt); free(E);
+    return ix;
+}
+
+void or_index_free(or_index* ix) {
+    if (!ix) return;
+    free(ix->hash); free(ix->pos); free(ix->strand); free(ix->key); free(ix->key_first); free(ix->key_count);
+    free(ix);
+}
+
+void or_index_stats_get(const or_index* ix, or_index_stats* st) { *st = ix->st; }
+
+uint64_t or_index_dump(const or_index* ix, uint64_t* hash, uint64_t* pos, uint8_t* strand, uint64_t cap) {
+    for (uint64_t i = 0; i < ix->n_kept && i < cap; i++) {
+        if (hash) hash[i] = ix->hash[i];
+        if (pos) pos[i] = ix->pos[i];
+        if (strand) strand[i] = ix->strand[i];
+    }
+    return ix->n_kept;
+}
+
+/* binary search over the sorted distinct kept keys; returns key index or -1 */
+static int64_t find_key(const or_index* ix, uint64_t h) {
+    int64_t lo = 0, hi = (int64_t)ix->n_keys - 1;
+    while (lo <= hi) {
+        int64_t mid = lo + (hi - lo) / 2;
+        if (ix->key[mid] == h) return mid;
+        if (ix->key[mid] < h) lo = mid + 1; else hi = mid - 1;
+    }
+    return -1;
+}
+
+uint32_t or_index_occ(const or_index* ix, uint64_t h) {
+    int64_t q = find_key(ix, h);
+    return q < 0 ? 0 : ix->key_count[q];
+}
+
+/* ------------------------------------------------------------------------------------------ */
+/* O8 — pattern alignment.  For s = 0..p-1: M_s = minimizers of PQ_s (position order).
+ * "the same number of minimizer seeds from each PQ_s" and "limit the number of calculated
+ * minimizers in each PQ_s to a user-defined threshold" t  =>  c = min(t, min_s |M_s|);
+ * score_s = sum over the first c records of M_s of occ(hash);  a = argmax_s score_s, ties -> smallest s. */
+int or_select_phase(const or_index* ix, const uint8_t* read, uint64_t L, uint32_t t, uint64_t* scores) {
+    uint32_t p = ix->P.p;
+    if (p == 1) { if (scores) scores[0] = 0; return 0; }
+    or_mz* M[64]; int64_t cntM[64];
+    int64_t cmin = -1;
+    for (uint32_t s = 0; s < p; s++) {
+        int64_t c = or_minimizers(read, L, &ix->P, s, ix->k, ix->w, 0, NULL, 0);
+        M[s] = (or_mz*)malloc(sizeof(or_mz) * (size_t)(c ? c : 1));
+        or_minimizers(read, L, &ix->P, s, ix->k, ix->w, 0, M[s], (uint64_t)c);
+        cntM[s] = c;
+        if (cmin < 0 || c < cmin) cmin = c;
+    }
+    int64_t c = cmin < (int64_t)t ? cmin : (int64_t)t;
+    int best = 0; uint64_t best_score = 0;
+    for (uint32_t s = 0; s < p; s++) {
+        uint64_t sc = 0;
+        for (int64_t i = 0; i < c; i++) sc += or_index_occ(ix, M[s][i].hash);
+        if (scores) scores[s] = sc;
+        if (s == 0 || sc > best_score) { best_score = sc; best = (int)s; }
+        free(M[s]);
+    }
+    (void)cntM;
+    return best;
+}
+
+static int cmp_anchor(const void* a, const void* b) {
+    const or_anchor* x = (const or_anchor*)a; const or_anchor* y = (const or_anchor*)b;
+    if (x->read_id != y->read_id) return x->read_id < y->read_id ? -1 : 1;
+    if (x->ref_pos != y->ref_pos) return x->ref_pos < y->ref_pos ? -1 : 1;
+    if (x->read_pos != y->read_pos) return x->read_pos < y->read_pos ? -1 : 1;
+    if (x->strand != y->strand) return x->strand < y->strand ? -1 : 1;
+    return 0;
+}
+
+/* O9 — compressed seeding: minimizers of PQ_a, every kept index entry with the same
+ * hash is a match -> anchor (read_id, ref_pos, read_pos, ref strand XOR read strand). */
+int64_t or_seed_read(const or_index* ix, const uint8_t* read, uint64_t L, uint32_t a, uint32_t read_id,
+                     or_anchor* out, uint64_t cap) {
+    int64_t c = or_minimizers(read, L, &ix->P, a, ix->k, ix->w, 0, NULL, 0);
+    if (c < 0) return -1;
+    or_mz* M = (or_mz*)malloc(sizeof(or_mz) * (size_t)(c ? c : 1));
+    or_minimizers(read, L, &ix->P, a, ix->k, ix->w, 0, M, (uint64_t)c);
+    uint64_t tot = 0;
+    for (int64_t i = 0; i < c; i++) {
+        int64_t q = find_key(ix, M[i].hash);
+        if (q < 0) continue;
+        for (uint64_t e = ix->key_first[q]; e < ix->key_first[q] + ix->key_count[q]; e++) {
+            if (out && tot < cap) {
+                out[tot].read_id = read_id;
+                out[tot].ref_pos = (uint32_t)ix->pos[e];
+                out[tot].read_pos = (uint32_t)M[i].pos;
+                out[tot].strand = (uint32_t)(ix->strand[e] ^ M[i].strand);
+            }
+            tot++;
+        }
+    }
+    if (out) qsort(out, (size_t)(tot < cap ? tot : cap), sizeof(or_anchor), cmp_anchor);
+    free(M);
+    return (int64_t)tot;
+}
+
+int64_t or_seed_reads_batch(const or_index* ix, const uint8_t* reads, const uint64_t* offsets, uint32_t n,
+                            int mode, uint8_t* phases, uint32_t t, or_anchor* out, uint64_t cap,
+                            uint64_t* anchor_offsets) {
+    uint64_t tot = 0;
+    for (uint32_t r = 0; r < n; r++) {
+        const uint8_t* q = reads + offsets[r];
+        uint64_t L = offsets[r + 1] - offsets[r];
+        uint32_t a;
+        if (mode == 0) { a = (uint32_t)or_select_phase(ix, q, L, t, NULL); if (phases) phases[r] = (uint8_t)a; }
+        else { a = phases ? phases[r] : 0; if (a >= ix->P.p) return -1; }
+        if (anchor_offsets) anchor_offsets[r] = tot;
+        uint64_t room = tot < cap ? cap - tot : 0;
+        int64_t c = or_seed_read(ix, q, L, a, r, out ? out + (tot < cap ? tot : cap) : NULL, room);
+        if (c < 0) return -1;
+        tot += (uint64_t)c;
+    }
+    if (anchor_offsets) anchor_offsets[n] = tot;
+    return tot > cap && out ? -1 : (int64_t)tot;
+}
