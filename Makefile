@@ -16,7 +16,7 @@ all: $(PKG)/lib/libgod.so oracle/liboracle.so synth/libsynth.so
 
 build/%.o: $(PKG)/csrc/%.cu $(CU_HDRS)
 	@mkdir -p build
-	$(NVCC) $(NVFLAGS) -dc $< -o $@ 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; exit 1)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; exit 1)
 
 $(PKG)/lib/libgod.so: $(CU_OBJS)
 	@mkdir -p $(PKG)/lib

@@ -1,0 +1,414 @@
+#!/usr/bin/env python
+"""Benchmark of the Genome-on-Diet hot path on B200 (BASELINE.json metric).
+
+A STEP is one pass of the whole hot path over one batch of synthetic input, all in libgod's CUDA
+kernels through the C ABI: build the seed index of the reference (sparsify + minimizers + sort +
+cutoff + table), then pattern alignment (phase selection) and compressed
+seeding of every read.  Default workload = BASELINE configs[4] "human-scale" with the
+paper's pattern '10': 3.1 Gbp repeat-rich synthetic reference + 10,000,000 x 150 bp reads,
+k=21, w=11, cutoff top 0.02%.  Inputs (3.1 GB + 1.5 GB) are larger than L2 (126 MB), so no flush
+is needed between steps.
+
+value = reads seeded per second over the whole step (index build included), summed over ranks.
+e2e   = the same through the C ABI with pinned HOST buffers (H2D of the inputs and D2H of the
+        anchors inside the timed region).
+--impl reference: the CPU oracle (oracle/, plain single-threaded C) on a bounded sample of the
+same workload, extrapolated to the metric's unit (see cpu_baseline.sample).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "seeded reads/s and index-build Gbp/s on 1 B200; % of HBM roofline"
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+
+WORKLOADS = {
+    # name: (config, pattern, k, w)
+    "human": ("human", "10", 21, 11),
+    "human-110": ("human", "110", 21, 11),
+    "human-1110": ("human", "1110", 21, 11),
+    "human-1": ("human", "1", 21, 11),
+    "illumina": ("illumina", "10", 21, 11),
+    "hifi": ("hifi", "10", 19, 19),
+    "hifi-110": ("hifi", "110", 19, 19),
+    "ont": ("ont", "10", 15, 10),
+    "tiny": ("tiny", "10", 21, 11),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="human", choices=sorted(WORKLOADS))
+    ap.add_argument("--scale", type=float, default=1.0, help="size multiplier (1.0 = the BASELINE config)")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-bp", type=int, default=40_000_000)
+    ap.add_argument("--cpu-sample-reads", type=int, default=40_000)
+    return ap.parse_args()
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ------------------------------------------------------------------------------------------ data
+def make_inputs(workload: str, scale: float, rank: int):
+    import synth
+    cfg_name, pattern, k, w = WORKLOADS[workload]
+    t0 = time.time()
+    cfg = synth.make_config(cfg_name, scale=scale, read_seed_offset=7919 * rank)
+    log(f"[bench] rank {rank}: generated {cfg_name} x{scale}: ref {cfg.ref.size/1e9:.3f} Gbp, "
+        f"{cfg.reads.n} reads ({cfg.reads.seq.size/1e9:.3f} Gbp) in {time.time()-t0:.1f}s")
+    return cfg, pattern, k, w
+
+
+# ------------------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={','.join(self.FIELDS)}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        med = float(np.median(sm)) if sm else None
+        return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------------ roofline
+def algorithmic_bytes(name: str, ctx: dict):
+    """Algorithmic bytes per LAUNCH of the named kernel (DESIGN.md §5 table): what the method must
+    move, not what a kernel happens to touch."""
+    n_ref_mz = ctx["n_entries_all"]
+    if name == "extract_ref":      # read every reference byte once; write 12 B per minimizer (u64 hash|strand, u32 pos)
+        return ctx["ref_bytes"] + 12 * n_ref_mz
+    if name == "k_rs_scatter":     # read + write one 12-B record per pass
+        return 24 * n_ref_mz
+    if name == "k_rs_hist":
+        return 8 * n_ref_mz
+    if name == "extract_seed":     # read bytes once; write hz, pos, read id per read minimizer
+        return ctx["read_bytes"] + 16 * ctx["n_read_mz"]
+    if name == "extract_phase":
+        return ctx["read_bytes"] + 12 * ctx["n_phase_mz"]
+    return None
+
+
+def pick_roofline(prof: dict, steps: int, ctx: dict, peak_gbs: float):
+    # dominant kernel = largest share of device time in the timed region
+    items = sorted(prof.items(), key=lambda kv: -kv[1][0])
+    total_ms = sum(v[0] for v in prof.values())
+    for name, (ms, n) in items:
+        b = algorithmic_bytes(name, ctx)
+        if b is None:
+            continue
+        avg_s = ms / n / 1e3
+        ach = b / avg_s / 1e9
+        return {"kernel": name, "bound": "hbm", "achieved": round(ach, 1), "peak": peak_gbs, "unit": "GB/s",
+                "frac": round(ach / peak_gbs, 4), "traffic": None, "share_of_step": round(ms / total_ms, 4),
+                "avg_launch_ms": round(avg_s * 1e3, 4), "algorithmic_bytes_per_launch": int(b),
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, measured)"}
+    return None
+
+
+# ------------------------------------------------------------------------------------------ CPU oracle
+def oracle_sample(cfg, pattern, k, w, sample_bp: int, sample_reads: int):
+    """Time the CPU oracle on a bounded sample: index over a reference prefix of sample_bp bases and
+    seeding of sample_reads reads simulated from that prefix (same error model).  Returns
+    (seconds for the full workload extrapolated linearly, description)."""
+    import oracle
+    import synth
+    L = min(sample_bp, cfg.ref.size)
+    pref = np.ascontiguousarray(cfg.ref[:L])
+    off = np.array([0, L], np.uint64)
+    t0 = time.perf_counter()
+    ix = oracle.Index(pref, off, pattern, k, w)
+    t_idx = time.perf_counter() - t0
+    rd = cfg.reads
+    nr = min(sample_reads, rd.n)
+    lens = np.diff(rd.offsets.astype(np.int64))
+    mean_len = float(lens.mean()) if lens.size else 150.0
+    sim = synth.simulate_reads(pref, nr, 9001, length=int(round(mean_len)), start_margin=int(mean_len * 1.3) + 64,
+                               p_sub=0.001, p_ins=0.00005, p_del=0.00005)
+    t0 = time.perf_counter()
+    ix.seed_reads(sim.seq, sim.offsets)
+    t_seed = time.perf_counter() - t0
+    full = t_idx * (cfg.ref.size / L) + t_seed * (rd.n / max(1, nr))
+    desc = (f"oracle index over a {L/1e6:.0f} Mbp prefix of the reference ({t_idx:.1f}s) + SELECT-mode seeding of "
+            f"{nr} reads simulated from that prefix ({t_seed:.1f}s), each scaled linearly to the full workload "
+            f"({cfg.ref.size/1e9:.2f} Gbp, {rd.n} reads)")
+    return full, desc, t_idx + t_seed
+
+
+# ------------------------------------------------------------------------------------------ main
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, world, rank)
+    import torch
+    import paper_2211_08157_b200 as god
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl")
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    cfg, pattern, k, w = make_inputs(args.workload, args.scale, rank)
+    n_reads = cfg.reads.n
+    dref = torch.from_numpy(cfg.ref).to(dev)
+    droff = torch.from_numpy(cfg.ref_offsets).to(dev)
+    dreads = torch.from_numpy(cfg.reads.seq).to(dev)
+    droffs = torch.from_numpy(cfg.reads.offsets).to(dev)
+    torch.cuda.synchronize()
+
+    def step(cap=None, ev=None):
+        if ev:
+            ev[0].record()
+        ix = god.god_build_index(dref, droff, pattern, k, w, cutoff=cfg.cutoff)
+        if ev:
+            ev[1].record()
+        an, ao, ph = god.god_seed_reads(ix, dreads, droffs, cap=cap)
+        if ev:
+            ev[2].record()
+        return ix, an
+
+    # warm-up (also sizes the anchor output)
+    cap = None
+    keep = []
+    for i in range(max(args.warmup, 1)):
+        ix, an = step(cap)
+        cap = max(int(an.shape[0]), 1)
+        st = ix.stats()
+        keep.append(ix)
+    n_anchors = cap
+    for ix in keep:
+        ix.free()
+    keep.clear()
+    torch.cuda.synchronize()
+
+    # timed region
+    god.profile_reset()
+    god.profile_enable(True)
+    launches0 = god.launch_count()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clk = ClockSampler(torch.cuda.current_device())
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk.start()
+    start.record()
+    for i in range(args.steps):
+        ix, an = step(cap, evs[i])
+        keep.append(ix)
+    end.record()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clocks = clk.stop()
+    god.profile_enable(False)
+    launches = god.launch_count() - launches0
+    prof = god.profile_query()
+    elapsed_ms = start.elapsed_time(end)
+    build_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in evs]))
+    seed_ms = float(np.mean([e[1].elapsed_time(e[2]) for e in evs]))
+    for ix in keep:
+        ix.free()
+    keep.clear()
+    if dist:
+        t = torch.tensor([elapsed_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(t.item())
+    ms_per_step = elapsed_ms / args.steps
+    value = world * n_reads / (ms_per_step / 1e3)
+
+    # records counts for the byte model (one extra untimed pass)
+    hz, _, _, _ = god.god_minimizers(dreads, droffs, pattern, k, w, phases=None)  # phase-0 read minimizers (approx.)
+    n_read_mz = int(hz.shape[0])
+    del hz
+    peaks = json.load(open(PEAKS)) if os.path.exists(PEAKS) else {"hbm_gbs": 6650.0}
+    peak_gbs = float(peaks.get("hbm_gbs", 6650.0))
+    ctx = {"ref_bytes": int(cfg.ref.size), "read_bytes": int(cfg.reads.seq.size), "n_entries_all": st["n_entries_all"],
+           "n_read_mz": n_read_mz, "n_phase_mz": n_read_mz * 2}
+    roof = pick_roofline(prof, args.steps, ctx, peak_gbs)
+    kernels = {kname: {"ms_per_step": round(ms / args.steps, 4), "launches_per_step": n // args.steps}
+               for kname, (ms, n) in sorted(prof.items(), key=lambda kv: -kv[1][0])}
+
+    # e2e through the C ABI with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(god, torch, cfg, pattern, k, w, n_anchors, args.e2e_steps, dist, world, dev)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        full_s, desc, spent = oracle_sample(cfg, pattern, k, w, int(args.cpu_sample_bp * args.scale) or 1_000_000,
+                                            max(1000, int(args.cpu_sample_reads * args.scale)))
+        cpu = {"value": round(n_reads / full_s, 2), "unit": "reads/s", "cores": 1, "kind": "oracle",
+               "sample": desc, "cpu_seconds_spent": round(spent, 1)}
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": round(value, 1), "unit": "reads/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": f"{args.workload}: BASELINE configs[{list(WORKLOADS).index(args.workload) if args.workload.startswith('human') else 0}] "
+                       f"{cfg.ref.size/1e9:.2f} Gbp ref + {n_reads} reads, pattern '{pattern}', k={k}, w={w}, "
+                       f"cutoff top {cfg.cutoff[0]}/{cfg.cutoff[1]}",
+                       "ref_bp": int(cfg.ref.size), "n_reads": n_reads, "read_bp": int(cfg.reads.seq.size),
+                       "pattern": pattern, "k": k, "w": w, "scale": args.scale,
+                       "l2_policy": "inputs larger than L2 (no flush needed)", "parallelism": f"replicas x{world} (weak)"},
+            "index_build_gbps": round(cfg.ref.size / (build_ms / 1e3) / 1e9, 3),
+            "seed_reads_per_s": round(n_reads / (seed_ms / 1e3), 1),
+            "anchors_per_s": round(n_anchors / (seed_ms / 1e3), 1),
+            "stage_ms": {"index_build": round(build_ms, 3), "phase_select_and_seed": round(seed_ms, 3)},
+            "index": {kk: st[kk] for kk in ("n_entries_all", "n_distinct_all", "m", "tau", "kept_entries", "dir_bits")},
+            "n_anchors_per_step": n_anchors,
+            "roofline": roof, "kernels": kernels,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
+        }
+        print(json.dumps(out), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def run_e2e(god, torch, cfg, pattern, k, w, n_anchors, steps, dist, world, dev):
+    href = torch.from_numpy(cfg.ref).pin_memory()
+    hroff = torch.from_numpy(cfg.ref_offsets).pin_memory()
+    hreads = torch.from_numpy(cfg.reads.seq).pin_memory()
+    hroffs = torch.from_numpy(cfg.reads.offsets).pin_memory()
+    n = cfg.reads.n
+    n_anchors = int(n_anchors * 1.02) + 1024  # slack; the path is deterministic
+    an_host = torch.empty(n_anchors * 4 + 4, dtype=torch.uint32).pin_memory()
+    ao_host = torch.empty(n + 1, dtype=torch.uint64).pin_memory()
+    ph_host = torch.empty(max(1, n), dtype=torch.uint8).pin_memory()
+    import ctypes
+    from paper_2211_08157_b200 import _lib
+    L = _lib.load()
+    prm = _lib.GodParams(pattern.encode(), k, w)
+    cut = _lib.GodCutoff(0, cfg.cutoff[0], cfg.cutoff[1], 0)
+    stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    need = ctypes.c_uint64(0)
+    vp = ctypes.c_void_p
+
+    def one():
+        h = ctypes.c_void_p(0)
+        _lib.check(L.god_build_index(ctypes.byref(prm), vp(href.data_ptr()), vp(hroff.data_ptr()), 1,
+                                     ctypes.byref(cut), ctypes.byref(h), stream))
+        _lib.check(L.god_seed_reads(h, vp(hreads.data_ptr()), vp(hroffs.data_ptr()), n, _lib.PHASE_SELECT,
+                                    vp(ph_host.data_ptr()), 16, vp(an_host.data_ptr()), vp(ao_host.data_ptr()),
+                                    n_anchors, ctypes.byref(need), stream))
+        return h
+
+    L.god_index_free(one())  # warm-up
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    hs = []
+    s.record()
+    for _ in range(steps):
+        hs.append(one())
+    e.record()
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e)
+    for h in hs:
+        L.god_index_free(h)
+    if dist:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    h2d = cfg.ref.size + cfg.ref_offsets.nbytes + cfg.reads.seq.size + cfg.reads.offsets.nbytes
+    d2h = int(need.value) * 16 + (n + 1) * 8 + n
+    return {"value": round(world * n / (ms / steps / 1e3), 1), "unit": "reads/s", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "steps": steps, "ms_per_step": round(ms / steps, 3)}
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the CPU oracle, as it stands, on bounded samples of the same workload."""
+    if world > 1 and rank != 0:
+        return
+    cfg, pattern, k, w = make_inputs(args.workload, args.scale, 0)
+    times = []
+    desc = ""
+    spent = 0.0
+    sbp = max(1_000_000, int(4_000_000 * args.scale))
+    srd = max(500, int(4_000 * args.scale))
+    for i in range(args.warmup + args.steps):
+        full_s, desc, sp = oracle_sample(cfg, pattern, k, w, sbp, srd)
+        if i >= args.warmup:
+            times.append(full_s)
+            spent += sp
+    full = float(np.mean(times))
+    v = cfg.reads.n / full
+    out = {"impl": "reference", "metric": METRIC, "value": round(v, 2), "unit": "reads/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(full * 1e3, 1), "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+           "config": {"workload": args.workload, "ref_bp": int(cfg.ref.size), "n_reads": cfg.reads.n,
+                      "pattern": pattern, "k": k, "w": w, "scale": args.scale},
+           "cpu_baseline": {"value": round(v, 2), "unit": "reads/s", "cores": 1, "kind": "oracle", "sample": desc},
+           "e2e": {"value": round(v, 2), "unit": "reads/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,169 @@
+/*
+ * god.h — C ABI of the B200-native Genome-on-Diet hot path (libgod.so).
+ *
+ * Implements the data-parallel hot path of arXiv 2211.08157 ("Genome-on-Diet", PAPER.md; P:n =
+ * line n): (1) pattern sparsification, (2) double-strand (w,k)-minimizer extraction, (3) seed
+ * index build with an occurrence cutoff, (4) pattern alignment (phase selection) and compressed
+ * seeding into anchors.  Every step runs in hand-written CUDA kernels for sm_100a; there is no
+ * CPU fallback.  Readings of the paper (tie rule, position convention, cutoff quantile, phase
+ * rules) are DESIGN.md §2 (= SURVEY.md §8(c) O1-O9).
+ *
+ * CONVENTIONS (all entry points)
+ *  - Pointers may be DEVICE or HOST memory: each pointer is classified with
+ *    cudaPointerGetAttributes; host inputs are staged to the device inside the call and host
+ *    outputs are copied back before it returns (such calls synchronize `stream`).  Device-only
+ *    calls are asynchronous on `stream` except where a host-visible size is returned
+ *    (`*_needed` out-params, god_build_index, god_index_get_stats): those synchronize `stream`.
+ *  - Sequences are CSR: `seq` holds the concatenated ASCII bases of n sequences, `offsets[n+1]`
+ *    (u64) delimits them.  Bytes A/C/G/T (either case) are bases; every other byte is an
+ *    ambiguous base N (reading O1).
+ *  - Inputs are caller-owned and read-only; outputs are caller-allocated with an explicit
+ *    capacity.  If the capacity is too small the call returns GOD_ETRUNC, writes the required
+ *    size to `*needed` (host u64) and writes nothing else.
+ *  - Index memory is library-owned (stream-ordered allocations) and released by god_index_free.
+ *    An index is immutable after build; concurrent god_seed_reads calls on one index are safe.
+ *  - Errors: GOD_EINVAL is detected on the host before any device work; god_last_error() returns
+ *    a thread-local message for the last failing call.  The library never exits or throws.
+ *  - Limits: pattern length 1..64 with at least one '1'; 1 <= k <= 28; 1 <= w <= 255;
+ *    total reference length < 2^32 (positions are u32); each read < 2^32 bases; phases < p.
+ */
+#ifndef GOD_H
+#define GOD_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define GOD_API __attribute__((visibility("default")))
+#else
+#define GOD_API
+#endif
+
+typedef int32_t god_status;
+#define GOD_OK 0
+#define GOD_EINVAL 1  /* contract violation, detected on the host before any launch */
+#define GOD_ENOMEM 2  /* device allocation failed */
+#define GOD_ECUDA 3   /* CUDA runtime / launch error */
+#define GOD_ETRUNC 4  /* output capacity too small; required size in *needed */
+
+typedef void* god_stream;   /* a cudaStream_t (0 = legacy default stream) */
+
+/* The user's diet pattern P ("a binary pattern sequence P[0..p-1] ... weight x"),
+ * the k-mer length k and minimizer window w ("(w,k)-minimizer"). */
+typedef struct {
+    const char* pattern;   /* NUL-terminated '0'/'1' string, 1 <= p <= 64, >= one '1' */
+    int32_t k;             /* 1..28 */
+    int32_t w;             /* 1..255 */
+} god_params;
+
+/* Occurrence cutoff ("we discard the most frequently (>= a user-defined threshold)
+ * occurring minimizers").  mode 0: drop the top frac_num/frac_den of distinct hashes by count
+ * (reading O7: m = floor(n*num/den), tau = a_{n-m-1} of the ascending counts, keep count <= tau;
+ * BASELINE "top 0.02%" = 1/5000).  mode 1: absolute, keep iff count <= max_occ. */
+typedef struct {
+    uint32_t mode;
+    uint32_t frac_num, frac_den;
+    uint32_t max_occ;
+} god_cutoff;
+
+typedef struct {
+    uint64_t n_entries_all;    /* |E|: minimizer occurrences collected from the reference */
+    uint64_t n_distinct_all;   /* n: distinct hashes */
+    uint64_t m;                /* floor(n * frac) (0 in mode 1) */
+    uint64_t tau;              /* keep iff count <= tau */
+    uint64_t kept_entries, dropped_entries, kept_distinct, dropped_distinct;
+    uint32_t k, w, p, x;       /* parameters the index was built with */
+    uint32_t dir_bits;         /* B: directory = top B bits of the 2k-bit hash */
+    uint32_t reserved;
+} god_index_stats;
+
+/* One seed match ("finds exact matches of minimizers in the reference genome by querying
+ * the seed index"; P:312 anchors): reference start position (global, original coordinates),
+ * read start position (original read coordinates, read as supplied), read index, and
+ * strand = reference-minimizer strand XOR read-minimizer strand. */
+typedef struct {
+    uint32_t ref_pos;
+    uint32_t read_pos;
+    uint32_t read_id;
+    uint32_t strand;
+} god_anchor;
+
+typedef enum { GOD_PHASE_SELECT = 0, GOD_PHASE_GIVEN = 1 } god_phase_mode;
+
+typedef struct god_index god_index;
+
+GOD_API const char* god_last_error(void);
+GOD_API const char* god_version(void);
+
+/* ---- stage 1: sparsification (P:282 PR/PQ; P:286 steps (1)-(2); P:300 PQ_s) ----
+ * For sequence i with phase s_i (phases == NULL: all 0, the reference convention of P:286) keep
+ * original base j iff j >= s_i and P[(j - s_i) mod p] = 1, in order (reading O3).
+ * Output per sequence, starting on a fresh word: `packed` 2 bits per kept base, 32 bases per u64
+ * word, LSB-first (kept base q -> word q>>5, bits 2(q&31)..+1; A0 C1 G2 T3; N stored as 0);
+ * `nmask` parallel to `packed` (same word index), bit (q&31) set iff kept base q is N.  Pad bits 0.
+ * out_offsets[n+1]: word offsets per sequence; counts[n]: kept bases per sequence.
+ * Needs packed_cap_words >= out_offsets[n]; else GOD_ETRUNC with *packed_needed.  Synchronizes. */
+GOD_API god_status god_sparsify(const god_params* prm, const uint8_t* seq, const uint64_t* offsets, uint32_t n_seqs,
+                                const uint8_t* phases, uint64_t* packed, uint64_t* nmask, uint64_t* out_offsets,
+                                uint64_t* counts, uint64_t packed_cap_words, uint64_t* packed_needed,
+                                god_stream stream);
+
+/* ---- stage 2: (w,k)-minimizers (P:286 (3); P:370 N handling) ----
+ * Canonical k-mers over each N-free run of the sparsified sequence, Thomas Wang's hash masked to
+ * 2k bits (ref. 120), every position attaining a window minimum (all ties; windows of w
+ * consecutive k-mers, or the whole run if shorter; palindromes never selected).
+ * Records per sequence in position order: hash[], pos[] (u32 start in original coordinates;
+ * + the sequence's global offset if global_pos != 0), strand[] (1 = reverse is canonical).
+ * out_offsets[n+1].  cap = record capacity; GOD_ETRUNC + *needed if too small.  Synchronizes. */
+GOD_API god_status god_minimizers(const god_params* prm, const uint8_t* seq, const uint64_t* offsets, uint32_t n_seqs,
+                                  const uint8_t* phases, int32_t global_pos, uint64_t* hash, uint32_t* pos,
+                                  uint8_t* strand, uint64_t* out_offsets, uint64_t cap, uint64_t* needed,
+                                  god_stream stream);
+
+/* ---- stage 3: the seed index (P:286 (3), P:294 collect-then-sort, P:302 cutoff) ----
+ * Minimizers of every reference sequence (phase 0, global positions), sorted by (hash, pos),
+ * counted per distinct hash, filtered by the cutoff, stored as a bucketed table: a directory over
+ * the top B bits of the hash and, per kept entry, the remaining hash bits + strand and the
+ * position.  *out receives a library-owned handle.  Synchronizes `stream`. */
+GOD_API god_status god_build_index(const god_params* prm, const uint8_t* ref, const uint64_t* ref_offsets,
+                                   uint32_t n_refs, const god_cutoff* cutoff, god_index** out, god_stream stream);
+GOD_API god_status god_index_get_stats(const god_index* idx, god_index_stats* out_host);
+/* Kept entries in (hash, pos) order.  cap = entry capacity (>= kept_entries else GOD_ETRUNC). */
+GOD_API god_status god_index_dump(const god_index* idx, uint64_t* hash, uint32_t* pos, uint8_t* strand, uint64_t cap,
+                                  uint64_t* needed, god_stream stream);
+/* occ(h) for n query hashes ("their sum of occurrence frequencies"): kept count, 0 if absent/dropped. */
+GOD_API god_status god_index_count(const god_index* idx, const uint64_t* hashes, uint64_t n, uint32_t* counts,
+                                   god_stream stream);
+GOD_API void god_index_free(god_index* idx);
+
+/* ---- stage 4: pattern alignment + compressed seeding ----
+ * mode GOD_PHASE_SELECT: for each read and s = 0..p-1 take the minimizers of PQ_s, c = min(t,
+ * min_s |M_s|), score_s = sum of occ over the first c, a = argmax (smallest s on ties; p = 1 ->
+ * 0); phases[n] (u8) receives a.  mode GOD_PHASE_GIVEN: phases[n] is an input (each < p).
+ * Then every minimizer of PQ_a is looked up and every kept entry with the same hash yields one
+ * anchor (no deduplication).  Anchors of read r occupy [anchor_offsets[r], anchor_offsets[r+1]),
+ * ordered by read minimizer position then reference position.  t >= 1 (default 16).
+ * cap = anchor capacity; GOD_ETRUNC + *needed (phases are still written).  Synchronizes. */
+GOD_API god_status god_seed_reads(const god_index* idx, const uint8_t* reads, const uint64_t* read_offsets,
+                                  uint32_t n_reads, god_phase_mode mode, uint8_t* phases, uint32_t t,
+                                  god_anchor* anchors, uint64_t* anchor_offsets, uint64_t cap, uint64_t* needed,
+                                  god_stream stream);
+
+/* ---- tracing: per-kernel device time by CUDA events on the launching stream ----
+ * Off by default.  When on, every kernel launch is bracketed by two events; god_profile_query
+ * synchronizes on the pending events and returns, per kernel name (in first-launch order), the
+ * accumulated milliseconds and launch count: names are written NUL-separated into `names`
+ * (capacity names_len bytes), ms[i] and launches[i] for i < return value (<= max_entries).
+ * god_launch_count() counts every kernel launch of the library since load (always on). */
+GOD_API void god_profile_enable(int on);
+GOD_API void god_profile_reset(void);
+GOD_API int god_profile_query(char* names, size_t names_len, double* ms, uint64_t* launches, int max_entries);
+GOD_API uint64_t god_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GOD_H */

@@ -1,0 +1,256 @@
+"""B200-native Genome-on-Diet hot path (arXiv 2211.08157): sparsify -> minimizers -> index -> seeds.
+
+Thin Python binding over libgod.so (include/god.h).  Argument marshalling only: every step of the
+path runs in the CUDA kernels behind the C ABI; there is no CPU or PyTorch fallback, and the
+functions raise if the library is missing.  Names follow the C ABI.
+
+Arrays may be CUDA torch tensors (device path, asynchronous on the current torch stream until a
+size is needed) or host numpy arrays / CPU tensors (staged by the library; outputs come back as
+numpy).  PyTorch is used only for device memory and streams.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from ._lib import GodError, PHASE_GIVEN, PHASE_SELECT  # noqa: F401
+
+try:
+    import torch
+except Exception:  # pragma: no cover - torch is in the image
+    torch = None
+
+ANCHOR_DTYPE = np.dtype([("ref_pos", "<u4"), ("read_pos", "<u4"), ("read_id", "<u4"), ("strand", "<u4")])
+
+
+# ---------------------------------------------------------------------------------------- helpers
+def _is_cuda(x) -> bool:
+    return torch is not None and isinstance(x, torch.Tensor) and x.is_cuda
+
+
+def _ptr(x):
+    if x is None:
+        return None
+    if torch is not None and isinstance(x, torch.Tensor):
+        return ctypes.c_void_p(x.data_ptr()) if x.numel() else ctypes.c_void_p(0)
+    return ctypes.c_void_p(x.ctypes.data) if x.size else ctypes.c_void_p(0)
+
+
+def _host(x, dtype):
+    if torch is not None and isinstance(x, torch.Tensor):
+        x = x.numpy()
+    return np.ascontiguousarray(x, dtype=dtype)
+
+
+def _prep(x, dtype):
+    """CUDA tensors pass through (must be contiguous, right dtype); everything else -> numpy."""
+    if x is None:
+        return None
+    if _is_cuda(x):
+        tdt = {np.uint8: torch.uint8, np.uint64: torch.uint64, np.uint32: torch.uint32}[dtype]
+        if x.dtype != tdt:
+            raise TypeError(f"expected {tdt}, got {x.dtype}")
+        return x.contiguous()
+    return _host(x, dtype)
+
+
+def _empty(n, dtype, like_cuda: bool, device=None):
+    if like_cuda:
+        tdt = {np.uint8: torch.uint8, np.uint64: torch.uint64, np.uint32: torch.uint32}[dtype]
+        return torch.empty(int(n), dtype=tdt, device=device)
+    return np.empty(int(n), dtype=dtype)
+
+
+def _stream(device_path: bool):
+    if device_path and torch is not None:
+        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    return ctypes.c_void_p(0)
+
+
+def _params(pattern: str, k: int, w: int) -> _lib.GodParams:
+    return _lib.GodParams(pattern.encode(), int(k), int(w))
+
+
+def version() -> str:
+    return _lib.load().god_version().decode()
+
+
+# ---------------------------------------------------------------------------------------- stage 1
+def god_sparsify(seq, offsets, pattern: str, k: int = 1, w: int = 1, phases=None):
+    """-> (packed u64, nmask u64, out_offsets u64[n+1], counts u64[n])  (god.h stage 1)."""
+    L = _lib.load()
+    dev = _is_cuda(seq)
+    seq, offsets, phases = _prep(seq, np.uint8), _prep(offsets, np.uint64), _prep(phases, np.uint8)
+    n = int(offsets.shape[0]) - 1
+    dv = seq.device if dev else None
+    prm = _params(pattern, k, w)
+    oo = _empty(n + 1, np.uint64, dev, dv)
+    cnt = _empty(n, np.uint64, dev, dv)
+    need = ctypes.c_uint64(0)
+    st = _stream(dev)
+    rc = L.god_sparsify(ctypes.byref(prm), _ptr(seq), _ptr(offsets), n, _ptr(phases), None, None, _ptr(oo),
+                        _ptr(cnt), 0, ctypes.byref(need), st)
+    _lib.check(rc, allow=(_lib.GOD_ETRUNC,))
+    packed = _empty(max(1, need.value), np.uint64, dev, dv)
+    nmask = _empty(max(1, need.value), np.uint64, dev, dv)
+    rc = L.god_sparsify(ctypes.byref(prm), _ptr(seq), _ptr(offsets), n, _ptr(phases), _ptr(packed), _ptr(nmask),
+                        _ptr(oo), _ptr(cnt), need.value, ctypes.byref(need), st)
+    _lib.check(rc)
+    return packed[: need.value], nmask[: need.value], oo, cnt
+
+
+# ---------------------------------------------------------------------------------------- stage 2
+def god_minimizers(seq, offsets, pattern: str, k: int, w: int, phases=None, global_pos: bool = False,
+                   cap: int | None = None):
+    """-> (hash u64, pos u32, strand u8, out_offsets u64[n+1])  (god.h stage 2), position order."""
+    L = _lib.load()
+    dev = _is_cuda(seq)
+    seq, offsets, phases = _prep(seq, np.uint8), _prep(offsets, np.uint64), _prep(phases, np.uint8)
+    n = int(offsets.shape[0]) - 1
+    dv = seq.device if dev else None
+    prm = _params(pattern, k, w)
+    total = int(seq.shape[0])
+    if cap is None:
+        cap = total * 2 // (w + 1) + total // 8 + 1024
+    oo = _empty(n + 1, np.uint64, dev, dv)
+    need = ctypes.c_uint64(0)
+    st = _stream(dev)
+    for _ in range(2):
+        h = _empty(max(1, cap), np.uint64, dev, dv)
+        p = _empty(max(1, cap), np.uint32, dev, dv)
+        z = _empty(max(1, cap), np.uint8, dev, dv)
+        rc = L.god_minimizers(ctypes.byref(prm), _ptr(seq), _ptr(offsets), n, _ptr(phases), int(global_pos),
+                              _ptr(h), _ptr(p), _ptr(z), _ptr(oo), cap, ctypes.byref(need), st)
+        if rc == _lib.GOD_ETRUNC:
+            cap = need.value
+            continue
+        _lib.check(rc)
+        m = need.value
+        return h[:m], p[:m], z[:m], oo
+    raise GodError(_lib.GOD_ETRUNC, "minimizer capacity retry failed")
+
+
+# ---------------------------------------------------------------------------------------- stage 3
+class GodIndex:
+    """Library-owned seed index (god.h stage 3).  Free with .free() or by garbage collection."""
+
+    def __init__(self, handle, pattern, k, w):
+        self._h = handle
+        self.pattern, self.k, self.w = pattern, k, w
+
+    @property
+    def handle(self):
+        return self._h
+
+    def stats(self) -> dict:
+        st = _lib.GodIndexStats()
+        _lib.check(_lib.load().god_index_get_stats(self._h, ctypes.byref(st)))
+        return {f: int(getattr(st, f)) for f, _ in _lib.GodIndexStats._fields_ if f != "reserved"}
+
+    def dump(self, device: bool = False):
+        """Kept entries in (hash, pos) order -> (hash u64, pos u32, strand u8)."""
+        n = self.stats()["kept_entries"]
+        dv = torch.device("cuda") if device else None
+        h = _empty(max(1, n), np.uint64, device, dv)
+        p = _empty(max(1, n), np.uint32, device, dv)
+        z = _empty(max(1, n), np.uint8, device, dv)
+        need = ctypes.c_uint64(0)
+        _lib.check(_lib.load().god_index_dump(self._h, _ptr(h), _ptr(p), _ptr(z), n, ctypes.byref(need),
+                                              _stream(device)))
+        return h[:n], p[:n], z[:n]
+
+    def count(self, hashes):
+        dev = _is_cuda(hashes)
+        hashes = _prep(hashes, np.uint64)
+        n = int(hashes.shape[0])
+        out = _empty(max(1, n), np.uint32, dev, hashes.device if dev else None)
+        _lib.check(_lib.load().god_index_count(self._h, _ptr(hashes), n, _ptr(out), _stream(dev)))
+        return out[:n]
+
+    def free(self):
+        if self._h:
+            _lib.load().god_index_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def god_build_index(ref, ref_offsets, pattern: str, k: int, w: int, cutoff=(1, 5000), max_occ=None) -> GodIndex:
+    """Build the seed index.  cutoff = (num, den): drop the top num/den distinct hashes by count
+    (BASELINE "top 0.02%" = (1, 5000)); max_occ = int: keep iff count <= max_occ instead."""
+    L = _lib.load()
+    dev = _is_cuda(ref)
+    ref, ref_offsets = _prep(ref, np.uint8), _prep(ref_offsets, np.uint64)
+    n = int(ref_offsets.shape[0]) - 1
+    prm = _params(pattern, k, w)
+    cut = _lib.GodCutoff(1, 0, 1, int(max_occ)) if max_occ is not None else _lib.GodCutoff(0, cutoff[0], cutoff[1], 0)
+    h = ctypes.c_void_p(0)
+    _lib.check(L.god_build_index(ctypes.byref(prm), _ptr(ref), _ptr(ref_offsets), n, ctypes.byref(cut),
+                                 ctypes.byref(h), _stream(dev)))
+    return GodIndex(h, pattern, k, w)
+
+
+# ---------------------------------------------------------------------------------------- stage 4
+def god_seed_reads(index: GodIndex, reads, read_offsets, phases=None, t: int = 16, cap: int | None = None):
+    """SELECT mode if phases is None (phase per read computed), else GIVEN.
+    -> (anchors, anchor_offsets u64[n+1], phases u8[n]).  Device path: anchors is a CUDA u32 tensor
+    of shape (n_anchors, 4) = (ref_pos, read_pos, read_id, strand); host path: structured numpy."""
+    L = _lib.load()
+    dev = _is_cuda(reads)
+    reads, read_offsets = _prep(reads, np.uint8), _prep(read_offsets, np.uint64)
+    n = int(read_offsets.shape[0]) - 1
+    dv = reads.device if dev else None
+    mode = _lib.PHASE_SELECT if phases is None else _lib.PHASE_GIVEN
+    ph = _empty(max(1, n), np.uint8, dev, dv) if phases is None else _prep(phases, np.uint8).clone() if dev \
+        else _prep(phases, np.uint8).copy()
+    ao = _empty(n + 1, np.uint64, dev, dv)
+    if cap is None:
+        cap = int(reads.shape[0]) // 4 + 1024
+    need = ctypes.c_uint64(0)
+    st = _stream(dev)
+    for _ in range(2):
+        an = torch.empty((max(1, cap), 4), dtype=torch.uint32, device=dv) if dev else np.zeros(max(1, cap), ANCHOR_DTYPE)
+        rc = L.god_seed_reads(index.handle, _ptr(reads), _ptr(read_offsets), n, mode, _ptr(ph), int(t), _ptr(an),
+                              _ptr(ao), cap, ctypes.byref(need), st)
+        if rc == _lib.GOD_ETRUNC:
+            cap = need.value
+            mode = _lib.PHASE_GIVEN  # phases were written by the first call
+            continue
+        _lib.check(rc)
+        return an[: need.value], ao, ph[:n]
+    raise GodError(_lib.GOD_ETRUNC, "anchor capacity retry failed")
+
+
+# ---------------------------------------------------------------------------------------- tracing
+def profile_enable(on: bool = True):
+    _lib.load().god_profile_enable(int(on))
+
+
+def profile_reset():
+    _lib.load().god_profile_reset()
+
+
+def profile_query() -> dict:
+    """{kernel name: (total ms, launches)} accumulated since the last reset (synchronizes)."""
+    L = _lib.load()
+    cap = 128
+    buf = ctypes.create_string_buffer(cap * 64)
+    ms = (ctypes.c_double * cap)()
+    ln = (ctypes.c_uint64 * cap)()
+    n = L.god_profile_query(buf, len(buf), ms, ln, cap)
+    names = buf.raw.split(b"\0")[:n]
+    return {nm.decode(): (ms[i], int(ln[i])) for i, nm in enumerate(names)}
+
+
+def launch_count() -> int:
+    return int(_lib.load().god_launch_count())
+
+
+__all__ = ["god_sparsify", "god_minimizers", "god_build_index", "god_seed_reads", "GodIndex", "GodError",
+           "ANCHOR_DTYPE", "version"]

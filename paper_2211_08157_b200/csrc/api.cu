@@ -1,0 +1,430 @@
+// api.cu — the C ABI (include/god.h): validation, host/device staging, dispatch to the kernels.
+#include <atomic>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+#include "internal.cuh"
+
+namespace god {
+
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+// ---------------------------------------------------------------------------------- tracing
+namespace {
+struct ProfPending { const char* name; cudaEvent_t a, b; };
+struct ProfAcc { double ms = 0; uint64_t n = 0; };
+std::mutex g_prof_mu;
+bool g_prof_on = false;
+std::atomic<uint64_t> g_launches{0};
+std::vector<ProfPending> g_pending;
+std::map<std::string, ProfAcc> g_acc;
+std::vector<std::string> g_order;
+std::vector<cudaEvent_t> g_pool;
+
+cudaEvent_t get_event() {
+  if (!g_pool.empty()) {
+    cudaEvent_t e = g_pool.back();
+    g_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+void prof_flush_locked() {
+  for (auto& p : g_pending) {
+    cudaEventSynchronize(p.b);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, p.a, p.b);
+    auto it = g_acc.find(p.name);
+    if (it == g_acc.end()) {
+      g_order.push_back(p.name);
+      it = g_acc.emplace(p.name, ProfAcc{}).first;
+    }
+    it->second.ms += ms;
+    it->second.n += 1;
+    g_pool.push_back(p.a);
+    g_pool.push_back(p.b);
+  }
+  g_pending.clear();
+}
+}  // namespace
+
+ProfScope::ProfScope(const char* n, cudaStream_t s) : name(n), st(s) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (!g_prof_on) return;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  a = get_event();
+  cudaEventRecord(a, st);
+}
+ProfScope::~ProfScope() {
+  if (!a) return;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  cudaEvent_t b = get_event();
+  cudaEventRecord(b, st);
+  g_pending.push_back({name, a, b});
+}
+
+bool is_device_ptr(const void* p) {
+  if (!p) return true;
+  cudaPointerAttributes a;
+  cudaError_t e = cudaPointerGetAttributes(&a, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+Params make_params(const god_params* prm) {
+  GOD_REQUIRE(prm != nullptr, "params is NULL");
+  GOD_REQUIRE(prm->pattern != nullptr, "pattern is NULL");
+  const size_t p = strlen(prm->pattern);
+  GOD_REQUIRE(p >= 1 && p <= 64, "pattern length must be 1..64");
+  GOD_REQUIRE(prm->k >= 1 && prm->k <= 28, "k must be 1..28 (P:368)");
+  GOD_REQUIRE(prm->w >= 1 && prm->w <= 255, "w must be 1..255");
+  Params P;
+  memset(&P, 0, sizeof(P));
+  P.pat.p = (uint32_t)p;
+  uint32_t x = 0;
+  for (size_t i = 0; i < p; i++) {
+    const char c = prm->pattern[i];
+    GOD_REQUIRE(c == '0' || c == '1', "pattern must be over {0,1}");
+    if (c == '1') {
+      P.pat.bits |= 1ull << i;
+      P.pat.one[x++] = (uint8_t)i;
+    }
+  }
+  GOD_REQUIRE(x >= 1, "pattern must contain at least one '1' (weight >= 1)");
+  P.pat.x = x;
+  for (uint32_t r = 0; r < x; r++)
+    P.pat.gap[r] = (uint8_t)(r + 1 < x ? P.pat.one[r + 1] - P.pat.one[r] : p - P.pat.one[x - 1] + P.pat.one[0]);
+  uint32_t acc = 0;
+  for (size_t i = 0; i <= p; i++) {
+    P.pat.ones_before[i] = (uint8_t)acc;
+    if (i < p && prm->pattern[i] == '1') ++acc;
+  }
+  P.k = prm->k;
+  P.w = prm->w;
+  P.kmask = (prm->k >= 32) ? ~0ull : ((1ull << (2 * prm->k)) - 1);
+  return P;
+}
+
+// ---------------------------------------------------------------------------------- staging
+struct Stage {
+  cudaStream_t st;
+  Scratch& scr;
+  struct Back { void* user; void* dev; size_t bytes; };
+  std::vector<Back> backs;
+  bool synced_any = false;
+  Stage(cudaStream_t s, Scratch& sc) : st(s), scr(sc) {}
+  template <class T>
+  const T* in(const T* p, size_t count) {
+    if (!p || is_device_ptr(p)) return p;
+    T* d = scr.alloc<T>(count);
+    if (count) GOD_CUDA(cudaMemcpyAsync(d, p, count * sizeof(T), cudaMemcpyHostToDevice, st));
+    synced_any = true;
+    return d;
+  }
+  template <class T>
+  T* out(T* p, size_t count) {
+    if (!p || is_device_ptr(p)) return p;
+    T* d = scr.alloc<T>(count);
+    backs.push_back({p, d, count * sizeof(T)});
+    return d;
+  }
+  template <class T>
+  T* inout(T* p, size_t count) {
+    if (!p || is_device_ptr(p)) return p;
+    T* d = scr.alloc<T>(count);
+    if (count) GOD_CUDA(cudaMemcpyAsync(d, p, count * sizeof(T), cudaMemcpyHostToDevice, st));
+    backs.push_back({p, d, count * sizeof(T)});
+    return d;
+  }
+  void finish() {
+    for (auto& b : backs)
+      if (b.bytes) GOD_CUDA(cudaMemcpyAsync(b.user, b.dev, b.bytes, cudaMemcpyDeviceToHost, st));
+    GOD_CUDA(cudaStreamSynchronize(st));
+  }
+};
+
+// offsets[n] (total bytes) readable from host or device
+static uint64_t total_len(const uint64_t* offsets, uint32_t n, cudaStream_t st) {
+  if (!offsets) return 0;
+  if (!is_device_ptr(offsets)) return offsets[n];
+  return d2h_scalar(offsets + n, st);
+}
+
+template <class F>
+static god_status guarded(F&& f) {
+  try {
+    f();
+    return GOD_OK;
+  } catch (const Fail& e) {
+    return e.code;
+  } catch (const std::exception& e) {
+    set_error(std::string("exception: ") + e.what());
+    return GOD_ECUDA;
+  } catch (...) {
+    set_error("unknown exception");
+    return GOD_ECUDA;
+  }
+}
+
+namespace {
+__global__ void k_split_records(const uint64_t* __restrict__ hz, const uint32_t* __restrict__ pos, uint64_t n,
+                                uint64_t* hash, uint32_t* opos, uint8_t* strand) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t v = hz[i];
+    if (hash) hash[i] = v & ((1ull << 63) - 1);
+    if (opos) opos[i] = pos[i];
+    if (strand) strand[i] = (uint8_t)(v >> 63);
+  }
+}
+__global__ void k_check_phases(const uint8_t* ph, uint32_t n, uint32_t p, uint32_t* bad) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    if (ph[i] >= p) atomicAdd(bad, 1u);
+}
+}  // namespace
+
+}  // namespace god
+
+using namespace god;
+
+extern "C" {
+
+GOD_API const char* god_last_error(void) { return g_err.c_str(); }
+GOD_API const char* god_version(void) { return "god-b200 0.1 (sm_100a)"; }
+
+GOD_API void god_profile_enable(int on) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_prof_on = on != 0;
+}
+GOD_API void god_profile_reset(void) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  prof_flush_locked();
+  g_acc.clear();
+  g_order.clear();
+}
+GOD_API int god_profile_query(char* names, size_t names_len, double* ms, uint64_t* launches, int max_entries) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  prof_flush_locked();
+  int n = 0;
+  size_t off = 0;
+  for (const auto& nm : g_order) {
+    if (n >= max_entries) break;
+    const auto& a = g_acc[nm];
+    if (names && off + nm.size() + 1 <= names_len) {
+      memcpy(names + off, nm.c_str(), nm.size() + 1);
+      off += nm.size() + 1;
+    }
+    if (ms) ms[n] = a.ms;
+    if (launches) launches[n] = a.n;
+    ++n;
+  }
+  return n;
+}
+GOD_API uint64_t god_launch_count(void) { return g_launches.load(); }
+
+GOD_API god_status god_sparsify(const god_params* prm, const uint8_t* seq, const uint64_t* offsets, uint32_t n_seqs,
+                                const uint8_t* phases, uint64_t* packed, uint64_t* nmask, uint64_t* out_offsets,
+                                uint64_t* counts, uint64_t packed_cap_words, uint64_t* packed_needed,
+                                god_stream stream) {
+  return guarded([&] {
+    Params P = make_params(prm);
+    GOD_REQUIRE(offsets && out_offsets && counts && packed_needed, "NULL argument");
+    GOD_REQUIRE(packed_cap_words == 0 || (packed && nmask), "NULL packed/nmask with nonzero capacity");
+    if (phases && !is_device_ptr(phases))
+      for (uint32_t i = 0; i < n_seqs; i++) GOD_REQUIRE(phases[i] < P.pat.p, "phase >= p");
+    cudaStream_t st = (cudaStream_t)stream;
+    Scratch scr(st);
+    Stage sg(st, scr);
+    const uint64_t L = total_len(offsets, n_seqs, st);
+    const uint8_t* dseq = sg.in(seq, L);
+    const uint64_t* doff = sg.in(offsets, (size_t)n_seqs + 1);
+    const uint8_t* dph = sg.in(phases, n_seqs);
+    uint64_t* doo = sg.out(out_offsets, (size_t)n_seqs + 1);
+    uint64_t* dcnt = sg.out(counts, n_seqs);
+    uint64_t* dpk = sg.out(packed, packed_cap_words);
+    uint64_t* dnm = sg.out(nmask, packed_cap_words);
+    god::sparsify(P, dseq, doff, n_seqs, dph, dpk, dnm, doo, dcnt, packed_cap_words, packed_needed, st);
+    sg.finish();
+  });
+}
+
+GOD_API god_status god_minimizers(const god_params* prm, const uint8_t* seq, const uint64_t* offsets, uint32_t n_seqs,
+                                  const uint8_t* phases, int32_t global_pos, uint64_t* hash, uint32_t* pos,
+                                  uint8_t* strand, uint64_t* out_offsets, uint64_t cap, uint64_t* needed,
+                                  god_stream stream) {
+  return guarded([&] {
+    Params P = make_params(prm);
+    GOD_REQUIRE(offsets && out_offsets && needed, "NULL argument");
+    if (phases && !is_device_ptr(phases))
+      for (uint32_t i = 0; i < n_seqs; i++) GOD_REQUIRE(phases[i] < P.pat.p, "phase >= p");
+    cudaStream_t st = (cudaStream_t)stream;
+    Scratch scr(st);
+    Stage sg(st, scr);
+    const uint64_t L = total_len(offsets, n_seqs, st);
+    GOD_REQUIRE(!global_pos || L < (1ull << 32), "global positions need total length < 2^32");
+    const uint8_t* dseq = sg.in(seq, L);
+    const uint64_t* doff = sg.in(offsets, (size_t)n_seqs + 1);
+    const uint8_t* dph = sg.in(phases, n_seqs);
+    if (dph && is_device_ptr(phases)) {
+      uint32_t* bad = scr.alloc<uint32_t>(1);
+      GOD_CUDA(cudaMemsetAsync(bad, 0, 4, st));
+      if (n_seqs) GOD_LAUNCH("k_check_phases", k_check_phases, grid_for(n_seqs, 256), 256, 0, st, dph, n_seqs, P.pat.p, bad);
+      GOD_REQUIRE(d2h_scalar(bad, st) == 0, "phase >= p");
+    }
+    JobSet js = make_jobs(P, doff, n_seqs, dph, 0, 0, global_pos != 0, st, scr);
+    Records rec;
+    run_extract(P, dseq, js.jobs, js.kb, js.n, js.total_pos, false, true, rec, st, scr,
+                js.total_pos / (uint64_t)(P.w + 1) * 2 + js.total_pos / 8 + 4096, "extract_mz");
+    *needed = rec.n;
+    uint64_t* doo = sg.out(out_offsets, (size_t)n_seqs + 1);
+    GOD_CUDA(cudaMemcpyAsync(doo, rec.job_off, ((size_t)n_seqs + 1) * sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
+    if (rec.n > cap) {
+      sg.finish();
+      throw Fail{GOD_ETRUNC};
+    }
+    uint64_t* dh = sg.out(hash, rec.n);
+    uint32_t* dp = sg.out(pos, rec.n);
+    uint8_t* dz = sg.out(strand, rec.n);
+    if (rec.n) {
+      GOD_LAUNCH("k_split_records", k_split_records, grid_for(rec.n, 256), 256, 0, st, rec.hz, rec.pos, rec.n, dh, dp, dz);
+    }
+    sg.finish();
+  });
+}
+
+GOD_API god_status god_build_index(const god_params* prm, const uint8_t* ref, const uint64_t* ref_offsets,
+                                   uint32_t n_refs, const god_cutoff* cutoff, god_index** out, god_stream stream) {
+  return guarded([&] {
+    Params P = make_params(prm);
+    GOD_REQUIRE(ref_offsets && out && cutoff, "NULL argument");
+    GOD_REQUIRE(cutoff->mode <= 1, "cutoff mode must be 0 (fraction) or 1 (max_occ)");
+    GOD_REQUIRE(cutoff->mode == 1 || cutoff->frac_den > 0, "cutoff frac_den must be > 0");
+    *out = nullptr;
+    cudaStream_t st = (cudaStream_t)stream;
+    Scratch scr(st);
+    Stage sg(st, scr);
+    const uint64_t L = total_len(ref_offsets, n_refs, st);
+    GOD_REQUIRE(L < (1ull << 32), "total reference length must be < 2^32 (u32 positions)");
+    const uint8_t* dref = sg.in(ref, L);
+    const uint64_t* doff = sg.in(ref_offsets, (size_t)n_refs + 1);
+    god_index* ix = new god_index();
+    try {
+      god::build_index(P, dref, doff, n_refs, *cutoff, ix, st);
+    } catch (...) {
+      god_index_free(ix);
+      throw;
+    }
+    sg.finish();
+    *out = ix;
+  });
+}
+
+GOD_API god_status god_index_get_stats(const god_index* idx, god_index_stats* out_host) {
+  return guarded([&] {
+    GOD_REQUIRE(idx && out_host, "NULL argument");
+    *out_host = idx->st;
+  });
+}
+
+GOD_API god_status god_index_dump(const god_index* idx, uint64_t* hash, uint32_t* pos, uint8_t* strand, uint64_t cap,
+                                  uint64_t* needed, god_stream stream) {
+  return guarded([&] {
+    GOD_REQUIRE(idx && needed, "NULL argument");
+    const uint64_t n = idx->st.kept_entries;
+    *needed = n;
+    if (n > cap) throw Fail{GOD_ETRUNC};
+    cudaStream_t st = (cudaStream_t)stream;
+    Scratch scr(st);
+    Stage sg(st, scr);
+    uint64_t* dh = sg.out(hash, n);
+    uint32_t* dp = sg.out(pos, n);
+    uint8_t* dz = sg.out(strand, n);
+    god::index_dump(idx, dh, dp, dz, st);
+    sg.finish();
+  });
+}
+
+GOD_API god_status god_index_count(const god_index* idx, const uint64_t* hashes, uint64_t n, uint32_t* counts,
+                                   god_stream stream) {
+  return guarded([&] {
+    GOD_REQUIRE(idx && (n == 0 || (hashes && counts)), "NULL argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    Scratch scr(st);
+    Stage sg(st, scr);
+    const uint64_t* dh = sg.in(hashes, n);
+    uint32_t* dc = sg.out(counts, n);
+    // hashes must be < 4^k (a 2k-bit hash); larger values cannot be present
+    god::index_count(idx, dh, n, dc, st);
+    sg.finish();
+  });
+}
+
+GOD_API void god_index_free(god_index* idx) {
+  if (!idx) return;
+  // the arrays come from the stream-ordered pool: wait for all users, then return them in order
+  cudaDeviceSynchronize();
+  if (idx->dir) cudaFreeAsync(idx->dir, 0);
+  if (idx->ent_key) cudaFreeAsync(idx->ent_key, 0);
+  if (idx->ent_pos) cudaFreeAsync(idx->ent_pos, 0);
+  cudaStreamSynchronize(0);
+  delete idx;
+}
+
+GOD_API god_status god_seed_reads(const god_index* idx, const uint8_t* reads, const uint64_t* read_offsets,
+                                  uint32_t n_reads, god_phase_mode mode, uint8_t* phases, uint32_t t,
+                                  god_anchor* anchors, uint64_t* anchor_offsets, uint64_t cap, uint64_t* needed,
+                                  god_stream stream) {
+  return guarded([&] {
+    GOD_REQUIRE(idx && read_offsets && phases && anchor_offsets && needed, "NULL argument");
+    GOD_REQUIRE(mode == GOD_PHASE_SELECT || mode == GOD_PHASE_GIVEN, "mode must be SELECT or GIVEN");
+    GOD_REQUIRE(t >= 1, "t must be >= 1");
+    GOD_REQUIRE(cap == 0 || anchors, "NULL anchors with nonzero capacity");
+    if (mode == GOD_PHASE_GIVEN && !is_device_ptr(phases))
+      for (uint32_t i = 0; i < n_reads; i++) GOD_REQUIRE(phases[i] < idx->P.pat.p, "phase >= p");
+    cudaStream_t st = (cudaStream_t)stream;
+    Scratch scr(st);
+    Stage sg(st, scr);
+    const uint64_t L = total_len(read_offsets, n_reads, st);
+    const uint8_t* dreads = sg.in(reads, L);
+    const uint64_t* doff = sg.in(read_offsets, (size_t)n_reads + 1);
+    uint8_t* dph = mode == GOD_PHASE_GIVEN ? sg.inout(phases, n_reads) : sg.out(phases, n_reads);
+    if (mode == GOD_PHASE_GIVEN && is_device_ptr(phases) && n_reads) {
+      uint32_t* bad = scr.alloc<uint32_t>(1);
+      GOD_CUDA(cudaMemsetAsync(bad, 0, 4, st));
+      GOD_LAUNCH("k_check_phases", k_check_phases, grid_for(n_reads, 256), 256, 0, st, dph, n_reads, idx->P.pat.p, bad);
+      GOD_REQUIRE(d2h_scalar(bad, st) == 0, "phase >= p");
+    }
+    uint64_t* dao = sg.out(anchor_offsets, (size_t)n_reads + 1);
+    // anchors: if host, stage at full capacity only when it fits
+    god_anchor* dan = anchors;
+    const bool host_anchors = anchors && !is_device_ptr(anchors);
+    if (host_anchors) dan = scr.alloc<god_anchor>(cap);
+    const uint64_t tot = god::seed_reads(idx, dreads, doff, n_reads, mode, dph, t, dan, dao, cap, st);
+    *needed = tot;
+    if (host_anchors && tot <= cap && tot)
+      GOD_CUDA(cudaMemcpyAsync(anchors, dan, tot * sizeof(god_anchor), cudaMemcpyDeviceToHost, st));
+    sg.finish();
+    if (tot > cap) throw Fail{GOD_ETRUNC};
+  });
+}
+
+}  // extern "C"

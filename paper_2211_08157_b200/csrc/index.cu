@@ -1,0 +1,434 @@
+// index.cu — stage 3: the seed index (P:286 (3)).
+//
+// "We do not directly insert minimizer information ... Instead, we append the minimizer
+// information to an array and sort the array after collecting information on all minimizers and
+// then add it to the hash table".  B200 version (kernels K2-K6):
+//   K1  fused sparsify+minimizer extraction of the reference (extract.cu) -> records in position order
+//   K2  stable LSD radix sort of (hash | strand<<63, pos) on the 2k hash bits, 8-bit digits:
+//       per pass: tile histograms -> exclusive scan (digit-major) -> stable scatter staged in SMEM
+//       (position order within equal hashes is preserved, so the result is (hash, pos) order)
+//   K3  run heads -> distinct index (scan) -> per-distinct start / count
+//   K4  cutoff tau on device (reading O7): count histogram (small counts) + radix select
+//       over the rare large counts; tau = (m+1)-th largest count, m = floor(n*num/den)
+//   K5  kept-entry offsets (scan), entry write: key = low (2k-B) hash bits << 1 | strand, pos
+//   K6  directory over the top B hash bits (gap fill over the kept entries' slots)
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <utility>
+#include <vector>
+#include "internal.cuh"
+
+namespace god {
+
+namespace {
+constexpr int RS_NT = 256;
+constexpr int RS_IPT = 16;
+constexpr int RS_TILE = RS_NT * RS_IPT;
+constexpr int RS_BITS = 8;
+constexpr int RS_BINS = 1 << RS_BITS;
+constexpr uint64_t HASH_BITS_MASK = (1ull << 63) - 1;
+constexpr int RS_DYN_SMEM = RS_TILE * (sizeof(uint64_t) + sizeof(uint32_t));
+
+__global__ void __launch_bounds__(RS_NT) k_rs_hist(const uint64_t* __restrict__ keys, uint64_t n, int shift,
+                                                   uint32_t dmask, uint32_t* hist, uint32_t ntiles) {
+  __shared__ uint32_t h[RS_BINS];
+  for (int i = threadIdx.x; i < RS_BINS; i += RS_NT) h[i] = 0;
+  __syncthreads();
+  const uint64_t base = (uint64_t)blockIdx.x * RS_TILE;
+#pragma unroll 4
+  for (int r = 0; r < RS_IPT; r++) {
+    uint64_t i = base + (uint64_t)r * RS_NT + threadIdx.x;
+    if (i < n) atomicAdd(&h[(uint32_t)((keys[i] & HASH_BITS_MASK) >> shift) & dmask], 1u);
+  }
+  __syncthreads();
+  for (int d = threadIdx.x; d < RS_BINS; d += RS_NT) hist[(uint64_t)d * ntiles + blockIdx.x] = h[d];
+}
+
+__global__ void __launch_bounds__(RS_NT) k_rs_scatter(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin,
+                                                      uint64_t* __restrict__ kout, uint32_t* __restrict__ vout,
+                                                      uint64_t n, int shift, uint32_t dmask,
+                                                      const uint64_t* __restrict__ goff, uint32_t ntiles) {
+  __shared__ uint32_t wcnt[RS_NT / 32][RS_BINS];
+  __shared__ uint32_t run[RS_BINS];
+  __shared__ uint32_t dstart[RS_BINS];
+  extern __shared__ __align__(16) unsigned char rs_dyn[];
+  uint64_t* sk = reinterpret_cast<uint64_t*>(rs_dyn);
+  uint32_t* sv = reinterpret_cast<uint32_t*>(sk + RS_TILE);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint64_t base = (uint64_t)blockIdx.x * RS_TILE;
+  for (int i = tid; i < RS_BINS; i += RS_NT) run[i] = 0;
+  for (int i = tid; i < (RS_NT / 32) * RS_BINS; i += RS_NT) (&wcnt[0][0])[i] = 0;
+  __syncthreads();
+  uint64_t key[RS_IPT];
+  uint32_t val[RS_IPT];
+  uint32_t rank[RS_IPT];
+  const uint32_t lt = (1u << lane) - 1;
+#pragma unroll
+  for (int r = 0; r < RS_IPT; r++) {
+    const uint64_t i = base + (uint64_t)r * RS_NT + tid;
+    const bool ok = i < n;
+    key[r] = ok ? kin[i] : 0;
+    val[r] = ok ? vin[i] : 0;
+    const uint32_t d = ok ? ((uint32_t)((key[r] & HASH_BITS_MASK) >> shift) & dmask) : RS_BINS;  // sentinel
+    const uint32_t peers = __match_any_sync(0xffffffffu, d);
+    const uint32_t rw = __popc(peers & lt);
+    if (ok && rw == 0) wcnt[wid][d] = __popc(peers);
+    __syncthreads();
+    {  // digit tid: exclusive prefix over warps, continuing the running count of earlier rounds
+      uint32_t acc = run[tid];
+#pragma unroll
+      for (int q = 0; q < RS_NT / 32; q++) {
+        uint32_t c = wcnt[q][tid];
+        wcnt[q][tid] = acc;
+        acc += c;
+      }
+      run[tid] = acc;
+    }
+    __syncthreads();
+    rank[r] = ok ? wcnt[wid][d] + rw : 0;
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < RS_NT / 32; q++) wcnt[q][tid] = 0;
+    __syncthreads();
+  }
+  // tile-local digit starts (exclusive scan of run[] over 256 digits by warp 0..7)
+  if (tid < 32) {
+    uint32_t v[RS_BINS / 32];
+    uint32_t s = 0;
+#pragma unroll
+    for (int q = 0; q < RS_BINS / 32; q++) { v[q] = run[tid * (RS_BINS / 32) + q]; s += v[q]; }
+    uint32_t incl = s;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += y;
+    }
+    uint32_t acc = incl - s;
+#pragma unroll
+    for (int q = 0; q < RS_BINS / 32; q++) { dstart[tid * (RS_BINS / 32) + q] = acc; acc += v[q]; }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < RS_IPT; r++) {
+    const uint64_t i = base + (uint64_t)r * RS_NT + tid;
+    if (i < n) {
+      const uint32_t d = (uint32_t)((key[r] & HASH_BITS_MASK) >> shift) & dmask;
+      const uint32_t slot = dstart[d] + rank[r];
+      sk[slot] = key[r];
+      sv[slot] = val[r];
+    }
+  }
+  __syncthreads();
+  const uint32_t cnt = (uint32_t)min((uint64_t)RS_TILE, n - base);
+  for (uint32_t s = tid; s < cnt; s += RS_NT) {
+    const uint64_t kk = sk[s];
+    const uint32_t d = (uint32_t)((kk & HASH_BITS_MASK) >> shift) & dmask;
+    const uint64_t dst = goff[(uint64_t)d * ntiles + blockIdx.x] + (s - dstart[d]);
+    kout[dst] = kk;
+    vout[dst] = sv[s];
+  }
+}
+
+__global__ void k_heads(const uint64_t* __restrict__ hz, uint64_t n, uint32_t* flag) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    flag[i] = (i == 0 || ((hz[i] ^ hz[i - 1]) & HASH_BITS_MASK)) ? 1u : 0u;
+}
+
+__global__ void k_dstart(const uint32_t* __restrict__ flag, const uint64_t* __restrict__ dix, uint64_t n, uint64_t* dstart,
+                         const uint64_t* nd) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    if (flag[i]) dstart[dix[i]] = i;
+  if (blockIdx.x == 0 && threadIdx.x == 0) dstart[*nd] = n;
+}
+
+constexpr uint32_t SMALL_BINS = 4096;
+
+// counts per distinct hash + small-count histogram + list of large counts
+__global__ void k_counts(const uint64_t* __restrict__ dstart, uint64_t nd, uint32_t* count, uint32_t* hist_small,
+                         uint32_t* large, uint32_t* n_large) {
+  __shared__ uint32_t h[SMALL_BINS];
+  for (int i = threadIdx.x; i < (int)SMALL_BINS; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  for (uint64_t d = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; d < nd; d += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t c = (uint32_t)(dstart[d + 1] - dstart[d]);
+    count[d] = c;
+    if (c < SMALL_BINS) atomicAdd(&h[c], 1u);
+    else large[atomicAdd(n_large, 1u)] = c;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < (int)SMALL_BINS; i += blockDim.x)
+    if (h[i]) atomicAdd(&hist_small[i], h[i]);
+}
+
+struct CutState {
+  uint64_t n_entries, n_distinct, m, tau;
+  uint64_t kept_entries, kept_distinct;
+};
+
+// tau = (m+1)-th largest count (reading O7: tau = a_{n-m-1}); one block.
+__global__ void __launch_bounds__(1024) k_tau(const uint32_t* hist_small, const uint32_t* large, const uint32_t* n_large_p,
+                                              const uint64_t* nd_p, uint64_t n_entries, uint32_t mode, uint32_t num,
+                                              uint32_t den, uint32_t max_occ, CutState* cs) {
+  __shared__ uint32_t bins[256];
+  __shared__ uint32_t s_prefix, s_mask;
+  __shared__ uint64_t s_need;
+  const uint64_t nd = *nd_p;
+  const uint32_t nl = *n_large_p;
+  uint64_t m = 0, tau = 0;
+  if (mode == 1) {
+    tau = max_occ;
+  } else {
+    m = den ? (uint64_t)(((unsigned __int128)nd * num) / den) : 0;
+    if (nd == 0 || m >= nd) {
+      tau = 0;
+    } else if (m + 1 <= nl) {
+      // radix select the (m+1)-th largest among the large counts (32-bit, 4 x 8-bit digits)
+      if (threadIdx.x == 0) { s_prefix = 0; s_mask = 0; s_need = m + 1; }
+      __syncthreads();
+      for (int sh = 24; sh >= 0; sh -= 8) {
+        for (int i = threadIdx.x; i < 256; i += blockDim.x) bins[i] = 0;
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < nl; i += blockDim.x) {
+          const uint32_t v = large[i];
+          if ((v & s_mask) == s_prefix) atomicAdd(&bins[(v >> sh) & 255u], 1u);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          uint64_t need = s_need;
+          for (int d = 255; d >= 0; d--) {
+            if (bins[d] >= need) { s_prefix |= (uint32_t)d << sh; break; }
+            need -= bins[d];
+          }
+          s_need = need;
+          s_mask |= 255u << sh;
+        }
+        __syncthreads();
+      }
+      tau = s_prefix;
+    } else {
+      if (threadIdx.x == 0) {
+        uint64_t cum = nl;  // counts >= SMALL_BINS
+        uint64_t v = SMALL_BINS;
+        while (v > 0) {
+          --v;
+          cum += hist_small[v];
+          if (cum >= m + 1) break;
+        }
+        s_need = v;
+      }
+      __syncthreads();
+      tau = s_need;
+    }
+  }
+  if (threadIdx.x == 0) {
+    cs->n_entries = n_entries;
+    cs->n_distinct = nd;
+    cs->m = m;
+    cs->tau = tau;
+    cs->kept_entries = 0;
+    cs->kept_distinct = 0;
+  }
+}
+
+__global__ void k_kept(const uint32_t* __restrict__ count, uint64_t nd, CutState* cs, uint64_t* kept_val) {
+  const uint64_t tau = cs->tau;
+  uint32_t local = 0;
+  for (uint64_t d = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; d < nd; d += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t c = count[d];
+    const bool keep = c <= tau;
+    kept_val[d] = keep ? c : 0;
+    local += keep;
+  }
+  for (int o = 16; o; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+  if ((threadIdx.x & 31) == 0 && local) atomicAdd((unsigned long long*)&cs->kept_distinct, (unsigned long long)local);
+}
+
+__global__ void k_write_entries(const uint64_t* __restrict__ hz, const uint32_t* __restrict__ pos, uint64_t n, const uint32_t* __restrict__ flag,
+                                const uint64_t* __restrict__ dix, const uint64_t* __restrict__ dstart,
+                                const uint32_t* __restrict__ count, const uint64_t* __restrict__ kept_off,
+                                const CutState* cs, uint32_t low_bits, uint32_t* ent_key, uint32_t* ent_pos,
+                                uint32_t* kslot) {
+  const uint64_t tau = cs->tau;
+  const uint64_t lowmask = (1ull << low_bits) - 1;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t d = dix[i] + flag[i] - 1;  // run index: exclusive scan of heads counts its own head for non-heads
+    if (count[d] > tau) continue;
+    const uint64_t e = kept_off[d] + (i - dstart[d]);
+    const uint64_t v = hz[i];
+    const uint64_t h = v & HASH_BITS_MASK;
+    ent_key[e] = (uint32_t)(((h & lowmask) << 1) | (v >> 63));
+    ent_pos[e] = pos[i];
+    kslot[e] = (uint32_t)(h >> low_bits);
+  }
+}
+
+__global__ void k_dir_fill(const uint32_t* __restrict__ kslot, uint64_t n_kept, uint32_t dir_bits, uint32_t* dir) {
+  const uint64_t nslots = 1ull << dir_bits;
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e <= n_kept; e += (uint64_t)gridDim.x * blockDim.x) {
+    const int64_t sp = e ? (int64_t)kslot[e - 1] : -1;
+    const int64_t se = e < n_kept ? (int64_t)kslot[e] : (int64_t)nslots;
+    for (int64_t s = sp + 1; s <= se; s++) dir[s] = (uint32_t)e;
+  }
+}
+
+}  // namespace
+
+namespace {
+__global__ void k_count_queries(god::IndexView v, const uint64_t* __restrict__ hashes, uint64_t n, uint32_t* out) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint2 r = probe_range(v, hashes[i]);
+    out[i] = r.y - r.x;
+  }
+}
+
+__global__ void k_dump(god::IndexView v, uint64_t* hash, uint32_t* pos, uint8_t* strand) {
+  const uint64_t nslots = 1ull << v.dir_bits;
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < v.n_kept; e += (uint64_t)gridDim.x * blockDim.x) {
+    // slot = largest s with dir[s] <= e
+    uint64_t lo = 0, hi = nslots - 1;
+    while (lo < hi) {
+      uint64_t mid = (lo + hi + 1) >> 1;
+      if (v.dir[mid] <= e) lo = mid;
+      else hi = mid - 1;
+    }
+    const uint32_t kk = v.ent_key[e];
+    if (hash) hash[e] = (lo << v.low_bits) | (kk >> 1);
+    if (pos) pos[e] = v.ent_pos[e];
+    if (strand) strand[e] = kk & 1u;
+  }
+}
+
+inline uint32_t floor_log2(uint64_t v) { return v ? 63u - (uint32_t)__builtin_clzll(v) : 0u; }
+}  // namespace
+
+
+void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offsets, uint32_t n_refs,
+                 const god_cutoff& cut, god_index* ix, cudaStream_t st) {
+  Scratch scr(st);
+  ix->P = P;
+  memset(&ix->st, 0, sizeof(ix->st));
+  ix->st.k = P.k; ix->st.w = P.w; ix->st.p = P.pat.p; ix->st.x = P.pat.x;
+  // K1: reference minimizers, position order (phase 0, global positions)
+  JobSet js = make_jobs(P, ref_offsets, n_refs, nullptr, 0, 0, true, st, scr);
+  Records rec;
+  const uint64_t est = js.total_pos / (uint64_t)(P.w + 1) * 2 + js.total_pos / 8 + 4096;
+  run_extract(P, ref, js.jobs, js.kb, js.n, js.total_pos, false, false, rec, st, scr, est, "extract_ref");
+  const uint64_t n = rec.n;
+  // K2: stable LSD radix sort on the 2k hash bits
+  uint64_t* k0 = rec.hz;
+  uint32_t* v0 = rec.pos;
+  if (n > 1) {
+    uint64_t* k1 = scr.alloc<uint64_t>(n);
+    uint32_t* v1 = scr.alloc<uint32_t>(n);
+    const uint32_t ntiles = (uint32_t)((n + RS_TILE - 1) / RS_TILE);
+    uint32_t* hist = scr.alloc<uint32_t>((uint64_t)RS_BINS * ntiles);
+    uint64_t* goff = scr.alloc<uint64_t>((uint64_t)RS_BINS * ntiles);
+    static bool attr = false;
+    if (!attr) {
+      GOD_CUDA(cudaFuncSetAttribute(k_rs_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, RS_DYN_SMEM));
+      attr = true;
+    }
+    const int hbits = 2 * P.k;
+    for (int shift = 0; shift < hbits; shift += RS_BITS) {
+      const int bits = min(RS_BITS, hbits - shift);
+      const uint32_t dmask = (1u << bits) - 1;
+      GOD_LAUNCH("k_rs_hist", k_rs_hist, ntiles, RS_NT, 0, st, k0, n, shift, dmask, hist, ntiles);
+      scan_exclusive_u32_to_u64(hist, goff, (uint64_t)RS_BINS * ntiles, nullptr, st, scr);
+      GOD_LAUNCH("k_rs_scatter", k_rs_scatter, ntiles, RS_NT, RS_DYN_SMEM, st, k0, v0, k1, v1, n, shift, dmask, goff, ntiles);
+      std::swap(k0, k1);
+      std::swap(v0, v1);
+    }
+  }
+  // K3: distinct hashes
+  uint32_t* flag = scr.alloc<uint32_t>(n);
+  uint64_t* dix = scr.alloc<uint64_t>(n);
+  uint64_t* nd_d = scr.alloc<uint64_t>(1);
+  if (n) {
+    GOD_LAUNCH("k_heads", k_heads, grid_for(n, 256), 256, 0, st, k0, n, flag);
+  }
+  scan_exclusive_u32_to_u64(flag, dix, n, nd_d, st, scr);
+  const uint64_t nd_bound = n;  // distinct <= n
+  uint64_t* dstart = scr.alloc<uint64_t>(nd_bound + 1);
+  GOD_LAUNCH("k_dstart", k_dstart, grid_for(n, 256), 256, 0, st, flag, dix, n, dstart, nd_d);
+  const uint64_t nd = d2h_scalar(nd_d, st);
+  // K4: counts, tau
+  uint32_t* count = scr.alloc<uint32_t>(nd);
+  uint32_t* hist_small = scr.alloc<uint32_t>(SMALL_BINS);
+  const uint64_t large_cap = n / SMALL_BINS + 1;
+  uint32_t* large = scr.alloc<uint32_t>(large_cap);
+  uint32_t* n_large = scr.alloc<uint32_t>(1);
+  CutState* cs = scr.alloc<CutState>(1);
+  GOD_CUDA(cudaMemsetAsync(hist_small, 0, SMALL_BINS * sizeof(uint32_t), st));
+  GOD_CUDA(cudaMemsetAsync(n_large, 0, sizeof(uint32_t), st));
+  if (nd) {
+    GOD_LAUNCH("k_counts", k_counts, min(grid_for(nd, 512), 4u * num_sms()), 512, 0, st, dstart, nd, count, hist_small, large, n_large);
+  }
+  GOD_LAUNCH("k_tau", k_tau, 1, 1024, 0, st, hist_small, large, n_large, nd_d, n, cut.mode, cut.frac_num, cut.frac_den, cut.max_occ, cs);
+  // K5: kept offsets + entries
+  uint64_t* kept_off = scr.alloc<uint64_t>(nd + 1);
+  uint64_t* kept_tot = scr.alloc<uint64_t>(1);
+  if (nd) {
+    GOD_LAUNCH("k_kept", k_kept, min(grid_for(nd, 256), 8u * num_sms()), 256, 0, st, count, nd, cs, kept_off);
+  }
+  scan_exclusive_u64(kept_off, kept_off, nd, kept_tot, st, scr);
+  CutState hcs;
+  GOD_CUDA(cudaMemcpyAsync(&hcs, cs, sizeof(CutState), cudaMemcpyDeviceToHost, st));
+  uint64_t n_kept = 0;
+  GOD_CUDA(cudaMemcpyAsync(&n_kept, kept_tot, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+  GOD_CUDA(cudaStreamSynchronize(st));
+  GOD_REQUIRE(n_kept < 0xFFFFFFFFull, "index has >= 2^32 kept entries");
+  // directory bits: ~1-2 entries per slot; low bits must fit 31 bits next to the strand bit
+  const uint32_t hb = 2 * P.k;
+  uint32_t B = floor_log2(n_kept ? n_kept : 1);
+  const uint32_t Bmin = hb > 31 ? hb - 31 : 0;
+  const uint32_t Bmax = hb < 28 ? hb : 28;
+  B = B < Bmin ? Bmin : (B > Bmax ? Bmax : B);
+  const uint32_t low_bits = hb - B;
+  ix->st.n_entries_all = n;
+  ix->st.n_distinct_all = nd;
+  ix->st.m = hcs.m;
+  ix->st.tau = hcs.tau;
+  ix->st.kept_entries = n_kept;
+  ix->st.dropped_entries = n - n_kept;
+  ix->st.kept_distinct = hcs.kept_distinct;
+  ix->st.dropped_distinct = nd - hcs.kept_distinct;
+  ix->st.dir_bits = B;
+  ix->st_alloc = st;
+  GOD_CUDA(cudaMallocAsync((void**)&ix->dir, ((1ull << B) + 1) * sizeof(uint32_t), st));
+  GOD_CUDA(cudaMallocAsync((void**)&ix->ent_key, (n_kept ? n_kept : 1) * sizeof(uint32_t), st));
+  GOD_CUDA(cudaMallocAsync((void**)&ix->ent_pos, (n_kept ? n_kept : 1) * sizeof(uint32_t), st));
+  uint32_t* kslot = scr.alloc<uint32_t>(n_kept);
+  if (n) {
+    GOD_LAUNCH("k_write_entries", k_write_entries, grid_for(n, 256), 256, 0, st, k0, v0, n, flag, dix, dstart, count, kept_off, cs, low_bits, ix->ent_key,
+                                                     ix->ent_pos, kslot);
+  }
+  GOD_LAUNCH("k_dir_fill", k_dir_fill, grid_for(n_kept + 1, 256), 256, 0, st, kslot, n_kept, B, ix->dir);
+  GOD_CUDA(cudaStreamSynchronize(st));
+  if (const char* dd = getenv("GOD_DEBUG_DIR")) {  // developer aid: dump the intermediates
+    auto dump = [&](const char* name, const void* p, size_t bytes) {
+      std::vector<char> h(bytes);
+      cudaMemcpy(h.data(), p, bytes, cudaMemcpyDeviceToHost);
+      std::string f = std::string(dd) + "/" + name + ".bin";
+      FILE* fp = fopen(f.c_str(), "wb");
+      if (fp) { fwrite(h.data(), 1, bytes, fp); fclose(fp); }
+    };
+    dump("rec_hz", rec.hz, n * 8); dump("sorted_hz", k0, n * 8); dump("sorted_pos", v0, n * 4);
+    dump("flag", flag, n * 4); dump("dix", dix, n * 8); dump("dstart", dstart, (nd + 1) * 8);
+    dump("count", count, nd * 4); dump("kept_off", kept_off, nd * 8); dump("kslot", kslot, n_kept * 4);
+    dump("ent_key", ix->ent_key, n_kept * 4); dump("dir", ix->dir, ((1ull << B) + 1) * 4);
+  }
+}
+
+void index_count(const god_index* ix, const uint64_t* hashes, uint64_t n, uint32_t* counts, cudaStream_t st) {
+  if (!n) return;
+  GOD_LAUNCH("k_count_queries", k_count_queries, grid_for(n, 256), 256, 0, st, ix->view(), hashes, n, counts);
+}
+
+void index_dump(const god_index* ix, uint64_t* hash, uint32_t* pos, uint8_t* strand, cudaStream_t st) {
+  if (!ix->st.kept_entries) return;
+  GOD_LAUNCH("k_dump", k_dump, grid_for(ix->st.kept_entries, 256), 256, 0, st, ix->view(), hash, pos, strand);
+}
+
+}  // namespace god

@@ -1,0 +1,84 @@
+// scan.cu — device-wide exclusive prefix sums (single pass, decoupled look-back) and small utilities.
+#include "common.cuh"
+
+namespace god {
+
+namespace {
+constexpr int SCAN_NT = 256;
+constexpr int SCAN_IPT = 8;
+constexpr int SCAN_TILE = SCAN_NT * SCAN_IPT;
+
+template <class TIn>
+__global__ void __launch_bounds__(SCAN_NT) k_scan(const TIn* in, uint64_t* out, uint64_t n,
+                                                  uint64_t* status, uint32_t* tile_ctr, uint64_t* total) {
+  __shared__ uint64_t warp_sum[SCAN_NT / 32];
+  __shared__ uint64_t s_excl;
+  __shared__ uint32_t s_tile;
+  if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
+  __syncthreads();
+  const uint64_t tile = s_tile;
+  const uint64_t base = tile * SCAN_TILE + (uint64_t)threadIdx.x * SCAN_IPT;
+  uint64_t v[SCAN_IPT];
+  uint64_t sum = 0;
+#pragma unroll
+  for (int i = 0; i < SCAN_IPT; i++) {
+    uint64_t idx = base + i;
+    v[i] = idx < n ? (uint64_t)in[idx] : 0;
+    sum += v[i];
+  }
+  // block exclusive scan of per-thread sums
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint64_t x = sum;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    uint64_t y = __shfl_up_sync(0xffffffffu, x, d);
+    if (lane >= d) x += y;
+  }
+  if (lane == 31) warp_sum[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    uint64_t ws = lane < SCAN_NT / 32 ? warp_sum[lane] : 0;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      uint64_t y = __shfl_up_sync(0xffffffffu, ws, d);
+      if (lane >= d) ws += y;
+    }
+    if (lane < SCAN_NT / 32) warp_sum[lane] = ws;  // inclusive
+    if (lane == SCAN_NT / 32 - 1) s_excl = lb_exclusive(status, tile, ws);
+  }
+  __syncthreads();
+  uint64_t run = s_excl + (wid ? warp_sum[wid - 1] : 0) + x - sum;
+#pragma unroll
+  for (int i = 0; i < SCAN_IPT; i++) {
+    uint64_t idx = base + i;
+    if (idx < n) out[idx] = run;
+    run += v[i];
+  }
+  if (total && tile == (n + SCAN_TILE - 1) / SCAN_TILE - 1 && threadIdx.x == SCAN_NT - 1) *total = run;
+}
+
+template <class TIn>
+void scan_impl(const TIn* in, uint64_t* out, uint64_t n, uint64_t* total, cudaStream_t st, Scratch& scr) {
+  if (n == 0) {
+    if (total) GOD_CUDA(cudaMemsetAsync(total, 0, sizeof(uint64_t), st));
+    return;
+  }
+  uint64_t tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
+  uint64_t* status = scr.alloc<uint64_t>(tiles);
+  uint32_t* ctr = scr.alloc<uint32_t>(1);
+  GOD_CUDA(cudaMemsetAsync(status, 0, tiles * sizeof(uint64_t), st));
+  GOD_CUDA(cudaMemsetAsync(ctr, 0, sizeof(uint32_t), st));
+  GOD_LAUNCH("k_scan", k_scan<TIn>, (unsigned)tiles, SCAN_NT, 0, st, in, out, n, status, ctr, total);
+}
+}  // namespace
+
+void scan_exclusive_u64(const uint64_t* in, uint64_t* out, uint64_t n, uint64_t* total, cudaStream_t st,
+                        Scratch& scr) {
+  scan_impl<uint64_t>(in, out, n, total, st, scr);
+}
+void scan_exclusive_u32_to_u64(const uint32_t* in, uint64_t* out, uint64_t n, uint64_t* total, cudaStream_t st,
+                               Scratch& scr) {
+  scan_impl<uint32_t>(in, out, n, total, st, scr);
+}
+
+}  // namespace god

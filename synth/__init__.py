@@ -176,30 +176,32 @@ def reference_for(name: str, scale: float = 1.0) -> np.ndarray:
     return ref
 
 
-def make_config(name: str, scale: float = 1.0, read_scale: float | None = None) -> Config:
-    """Build config `name` (BASELINE.json configs[i]); sizes × `scale` (1.0 = the real config)."""
+def make_config(name: str, scale: float = 1.0, read_scale: float | None = None, read_seed_offset: int = 0) -> Config:
+    """Build config `name` (BASELINE.json configs[i]); sizes × `scale` (1.0 = the real config).
+    read_seed_offset shifts the read-simulation seed (independent read batches per rank)."""
     rs = scale if read_scale is None else read_scale
+    so = int(read_seed_offset)
     ref = reference_for(name, scale)
     offs = np.array([0, ref.size], dtype=np.uint64)
     if name == "tiny":
-        reads = simulate_reads(ref, max(1, int(10_000 * rs)), 102, length=150, start_margin=200, p_sub=0.001)
+        reads = simulate_reads(ref, max(1, int(10_000 * rs)), 102 + so, length=150, start_margin=200, p_sub=0.001)
         cfg = Config("tiny", ["10"], 21, 11)
     elif name == "illumina":
-        reads = simulate_reads(ref, max(1, int(1_000_000 * rs)), 202, length=150, start_margin=200,
+        reads = simulate_reads(ref, max(1, int(1_000_000 * rs)), 202 + so, length=150, start_margin=200,
                                p_sub=0.001, p_ins=0.00005, p_del=0.00005)
         cfg = Config("illumina", ["10"], 21, 11)
     elif name == "hifi":
         mu, sg = _lognormal_params(15000, 3000)
-        reads = simulate_reads(ref, max(1, int(100_000 * rs)), 302, mu=mu, sigma=sg, lmin=1000, lmax=100000,
+        reads = simulate_reads(ref, max(1, int(100_000 * rs)), 302 + so, mu=mu, sigma=sg, lmin=1000, lmax=100000,
                                p_sub=0.0005, p_ins=0.00025, p_del=0.00025)
         cfg = Config("hifi", ["10", "110"], 19, 19)
     elif name == "ont":
         mu, sg = _lognormal_params(10000, 8000)
-        reads = simulate_reads(ref, max(1, int(50_000 * rs)), 402, mu=mu, sigma=sg, lmin=200, lmax=100000,
+        reads = simulate_reads(ref, max(1, int(50_000 * rs)), 402 + so, mu=mu, sigma=sg, lmin=200, lmax=100000,
                                p_sub=0.028, p_ins=0.021, p_del=0.021, homopolymer_factor=3.0)
         cfg = Config("ont", ["10"], 15, 10)
     elif name == "human":
-        reads = simulate_reads(ref, max(1, int(10_000_000 * rs)), 502, length=150, start_margin=200,
+        reads = simulate_reads(ref, max(1, int(10_000_000 * rs)), 502 + so, length=150, start_margin=200,
                                p_sub=0.001, p_ins=0.00005, p_del=0.00005)
         cfg = Config("human", ["10", "110", "1110", "1"], 21, 11)
     else:

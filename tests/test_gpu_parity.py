@@ -1,0 +1,264 @@
+"""GPU parity (-m gpu): the CUDA path, called through the C ABI (libgod.so), against the CPU oracle,
+element by element on the same seeded inputs.  Integer work -> bit-exact.  Sizes span many tiles
+(a tile = 2048 k-mer starts) and ragged tails; edge cases: empty / short / all-N sequences, even k
+(palindromes), homopolymers (ties), k = 1, k = 28, w = 1, w = 255, p = 1, long patterns."""
+import zlib
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2211_08157_b200 as god  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu(built):
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA GPU required for -m gpu tests")
+    return True
+
+
+def cu(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def np_(t):
+    return t.cpu().numpy()
+
+
+def pack_oracle(seq, offs, pattern, phases):
+    """Oracle sparsify output in god_sparsify's documented packing (god.h stage 1)."""
+    words, nms, oo, cnts = [], [], [0], []
+    for i in range(len(offs) - 1):
+        s = int(phases[i]) if phases is not None else 0
+        codes, _ = oracle.sparsify(seq[int(offs[i]):int(offs[i + 1])], pattern, s)
+        n = codes.size
+        cnts.append(n)
+        nw = (n + 31) // 32
+        for wi in range(nw):
+            word, nm = 0, 0
+            for b in range(32):
+                q = wi * 32 + b
+                if q >= n:
+                    break
+                c = int(codes[q])
+                if c == 4:
+                    nm |= 1 << b
+                else:
+                    word |= c << (2 * b)
+            words.append(word)
+            nms.append(nm)
+        oo.append(oo[-1] + nw)
+    return (np.array(words, np.uint64), np.array(nms, np.uint64), np.array(oo, np.uint64), np.array(cnts, np.uint64))
+
+
+def random_seqs(rng, n, lo, hi, n_frac=0.0, lowcomp=False):
+    seqs = []
+    for i in range(n):
+        L = int(rng.integers(lo, hi + 1))
+        if lowcomp and i % 3 == 0:
+            s = np.frombuffer(b"AAAAAAAACA", np.uint8)[rng.integers(0, 10, size=L)].copy()
+        else:
+            s = synth.random_acgt(rng, L, n_frac)
+        seqs.append(s)
+    return synth.concat(seqs)
+
+
+# ------------------------------------------------------------------------------------ stage 1
+@pytest.mark.parametrize("pattern", ["10", "110", "1110", "1", "0110100101", "1" + "0" * 62 + "1"])
+def test_sparsify_parity(pattern):
+    rng = np.random.default_rng(1)
+    seq, offs = random_seqs(rng, 300, 0, 700, 0.03)
+    p = len(pattern)
+    phases = rng.integers(0, p, size=len(offs) - 1).astype(np.uint8)
+    for ph in (None, phases):
+        want = pack_oracle(seq, offs, pattern, ph)
+        for dev in (True, False):
+            args = (cu(seq), cu(offs)) if dev else (seq, offs)
+            pk, nm, oo, cnt = god.god_sparsify(*args, pattern, phases=None if ph is None else (cu(ph) if dev else ph))
+            got = [np_(x) if dev else x for x in (pk, nm, oo, cnt)]
+            for g, w_ in zip(got, want):
+                assert np.array_equal(g, w_)
+
+
+# ------------------------------------------------------------------------------------ stage 2
+MZ_CASES = [
+    # (pattern, k, w, nseq, lo, hi, nfrac, lowcomp)
+    ("10", 21, 11, 40, 0, 30000, 0.0, False),
+    ("10", 21, 11, 200, 0, 400, 0.02, True),
+    ("110", 19, 19, 60, 0, 5000, 0.01, True),
+    ("1110", 15, 10, 60, 0, 5000, 0.0, False),
+    ("1", 15, 10, 30, 0, 20000, 0.005, True),
+    ("10", 4, 3, 100, 0, 600, 0.05, True),        # even k: palindromes
+    ("1", 1, 1, 50, 0, 300, 0.1, True),
+    ("101", 28, 40, 30, 0, 4000, 0.0, False),
+    ("1", 12, 255, 20, 0, 6000, 0.002, True),
+    ("11", 6, 2, 80, 0, 200, 0.2, True),
+    ("1" + "0" * 20, 5, 4, 20, 0, 3000, 0.0, False),
+]
+
+
+@pytest.mark.parametrize("case", MZ_CASES, ids=[f"{c[0]}-k{c[1]}-w{c[2]}" for c in MZ_CASES])
+def test_minimizer_parity(case):
+    pattern, k, w, nseq, lo, hi, nf, lc = case
+    rng = np.random.default_rng(zlib.crc32(repr(case).encode()))
+    seq, offs = random_seqs(rng, nseq, lo, hi, nf, lc)
+    p = len(pattern)
+    phases = rng.integers(0, p, size=len(offs) - 1).astype(np.uint8)
+    for gp in (False, True):
+        want, wo = oracle.minimizers_batch(seq, offs, pattern, k, w, phases=phases, global_pos=gp)
+        h, ps, z, oo = god.god_minimizers(cu(seq), cu(offs), pattern, k, w, phases=cu(phases), global_pos=gp)
+        assert np.array_equal(np_(oo), wo)
+        assert np.array_equal(np_(h), want["hash"])
+        assert np.array_equal(np_(ps).astype(np.uint64), want["pos"])
+        assert np.array_equal(np_(z), want["strand"])
+    # host-pointer path through the same ABI
+    h2, p2, z2, oo2 = god.god_minimizers(seq, offs, pattern, k, w, phases=phases)
+    want, wo = oracle.minimizers_batch(seq, offs, pattern, k, w, phases=phases)
+    assert np.array_equal(h2, want["hash"]) and np.array_equal(oo2, wo)
+
+
+def test_minimizer_edge_inputs():
+    # no sequences; only empty sequences; all-N; shorter than k
+    for seqs in ([], [np.zeros(0, np.uint8)] * 5, [np.frombuffer(b"N" * 500, np.uint8)],
+                 [np.frombuffer(b"ACGTAC", np.uint8), np.frombuffer(b"A", np.uint8)]):
+        seq, offs = synth.concat(seqs)
+        want, wo = oracle.minimizers_batch(seq, offs, "10", 5, 3)
+        h, ps, z, oo = god.god_minimizers(seq, offs, "10", 5, 3)
+        assert np.array_equal(oo, wo)
+        assert np.array_equal(h, want["hash"]) and np.array_equal(ps.astype(np.uint64), want["pos"])
+
+
+# ------------------------------------------------------------------------------------ stage 3
+def _index_parity(ref, offs, pattern, k, w, cutoff=(1, 5000), max_occ=None):
+    ix = god.god_build_index(cu(ref), cu(offs), pattern, k, w, cutoff=cutoff, max_occ=max_occ)
+    ox = oracle.Index(ref, offs, pattern, k, w, cutoff=cutoff, max_occ=-1 if max_occ is None else max_occ)
+    st, ost = ix.stats(), ox.stats()
+    for f in oracle.STATS_FIELDS:
+        assert st[f] == ost[f], (f, st[f], ost[f])
+    h, p, z = ix.dump()
+    oh, op, oz = ox.dump()
+    assert np.array_equal(h, oh)
+    assert np.array_equal(p.astype(np.uint64), op)
+    assert np.array_equal(z, oz)
+    # occ() probes, present and absent hashes
+    q = np.concatenate([oh[:: max(1, oh.size // 2000)], np.arange(0, 3000, dtype=np.uint64) * 7919 % (4 ** k)])
+    got = np_(ix.count(cu(q)))
+    want = np.array([ox.occ(int(v)) for v in q], np.uint32)
+    assert np.array_equal(got, want)
+    return ix, ox
+
+
+def test_index_parity_tiny_config():
+    cfg = synth.make_config("tiny")
+    ix, ox = _index_parity(cfg.ref, cfg.ref_offsets, "10", 21, 11)
+    assert ix.stats()["kept_entries"] > 50000
+
+
+@pytest.mark.parametrize("pattern,k,w", [("10", 15, 10), ("110", 13, 7), ("1", 11, 5), ("1110", 9, 4)])
+def test_index_parity_repeats_and_cutoff(pattern, k, w):
+    rng = np.random.default_rng(7)
+    rep = synth.random_acgt(rng, 700)
+    parts = []
+    for i in range(60):
+        parts += [synth.random_acgt(rng, int(rng.integers(500, 5000)), 0.001), rep]
+    seqs = [np.concatenate(parts[i:i + 10]) for i in range(0, len(parts), 10)] + [np.zeros(0, np.uint8)]
+    ref, offs = synth.concat(seqs)
+    for cut in [(1, 5000), (1, 200), (1, 20)]:
+        _index_parity(ref, offs, pattern, k, w, cutoff=cut)
+    for mo in [0, 1, 3, 60]:
+        _index_parity(ref, offs, pattern, k, w, max_occ=mo)
+
+
+def test_index_parity_homopolymer_heavy():
+    # all-ties runs make single hashes with very large counts (exercises the large-count select)
+    rng = np.random.default_rng(3)
+    parts = []
+    for i in range(40):
+        parts += [synth.random_acgt(rng, 3000), np.frombuffer(b"A" * int(rng.integers(100, 9000)), np.uint8)]
+    ref, offs = synth.concat([np.concatenate(parts)])
+    for cut in [(1, 5000), (1, 3), (1, 2)]:
+        _index_parity(ref, offs, "1", 7, 5, cutoff=cut)
+
+
+# ------------------------------------------------------------------------------------ stage 4
+def canon(an):
+    """anchors -> array sorted by (read_id, ref_pos, read_pos, strand)"""
+    a = np.asarray(an)
+    if a.dtype.names is None:
+        a = a.reshape(-1, 4)
+        rec = np.zeros(a.shape[0], oracle.ANCHOR_DTYPE)
+        rec["ref_pos"], rec["read_pos"], rec["read_id"], rec["strand"] = a[:, 0], a[:, 1], a[:, 2], a[:, 3]
+        a = rec
+    else:
+        rec = np.zeros(a.size, oracle.ANCHOR_DTYPE)
+        for f in ("ref_pos", "read_pos", "read_id", "strand"):
+            rec[f] = a[f]
+        a = rec
+    return np.sort(a, order=["read_id", "ref_pos", "read_pos", "strand"])
+
+
+def _seed_parity(ix, ox, reads, roffs, phases=None, t=16, sample=None):
+    an, ao, ph = god.god_seed_reads(ix, cu(reads), cu(roffs), phases=None if phases is None else cu(phases), t=t)
+    an, ao, ph = np_(an), np_(ao), np_(ph)
+    ids = np.arange(len(roffs) - 1) if sample is None else sample
+    sub_seqs = [reads[int(roffs[i]):int(roffs[i + 1])] for i in ids]
+    sub, soffs = synth.concat(sub_seqs)
+    sph = None if phases is None else phases[ids]
+    oan, oao, oph = ox.seed_reads(sub, soffs, phases=sph, t=t)
+    assert np.array_equal(ph[ids], oph)
+    # per-read anchor counts and canonical anchor lists
+    assert np.array_equal((ao[ids + 1] - ao[ids]), np.diff(oao))
+    g = np.concatenate([an[int(ao[i]):int(ao[i + 1])] for i in ids]) if len(ids) else an[:0]
+    g = canon(g)
+    remap = np.zeros(len(roffs), np.uint32)
+    remap[ids] = np.arange(len(ids), dtype=np.uint32)
+    g["read_id"] = remap[g["read_id"]]
+    g = np.sort(g, order=["read_id", "ref_pos", "read_pos", "strand"])
+    assert np.array_equal(g, canon(oan))
+    return an, ao, ph
+
+
+def test_seed_parity_tiny_config():
+    cfg = synth.make_config("tiny")
+    ix = god.god_build_index(cu(cfg.ref), cu(cfg.ref_offsets), "10", 21, 11)
+    ox = oracle.Index(cfg.ref, cfg.ref_offsets, "10", 21, 11)
+    an, ao, ph = _seed_parity(ix, ox, cfg.reads.seq, cfg.reads.offsets)
+    assert an.shape[0] > 50000
+    # GIVEN mode with the selected phases and with flipped phases
+    _seed_parity(ix, ox, cfg.reads.seq, cfg.reads.offsets, phases=ph)
+    _seed_parity(ix, ox, cfg.reads.seq, cfg.reads.offsets, phases=(1 - ph).astype(np.uint8))
+
+
+@pytest.mark.parametrize("pattern,k,w,t", [("110", 15, 10, 16), ("1110", 13, 6, 4), ("1", 15, 10, 16),
+                                           ("10", 9, 5, 1), ("0101", 11, 8, 40)])
+def test_seed_parity_mixed_reads(pattern, k, w, t):
+    rng = np.random.default_rng(17)
+    ref = synth.dup_genome(400_000, 9, dup_frac=0.2, lmin=300, lmax=2000)
+    roffs_ref = np.array([0, ref.size], np.uint64)
+    reads = synth.simulate_reads(ref, 700, 5, mu=6.5, sigma=1.0, lmin=1, lmax=6000, p_sub=0.01, p_ins=0.005,
+                                 p_del=0.005)
+    seqs = [reads.seq[int(reads.offsets[i]):int(reads.offsets[i + 1])] for i in range(reads.n)]
+    seqs += [np.zeros(0, np.uint8), np.frombuffer(b"N" * 400, np.uint8), synth.random_acgt(rng, 3000, 0.3),
+             np.frombuffer(b"ACGTTGCAAC", np.uint8)]
+    rs, ro = synth.concat(seqs)
+    ix = god.god_build_index(cu(ref), cu(roffs_ref), pattern, k, w, cutoff=(1, 500))
+    ox = oracle.Index(ref, roffs_ref, pattern, k, w, cutoff=(1, 500))
+    _seed_parity(ix, ox, rs, ro, t=t)
+    ph = rng.integers(0, len(pattern), size=len(ro) - 1).astype(np.uint8)
+    _seed_parity(ix, ox, rs, ro, phases=ph, t=t)
+
+
+def test_seed_host_pointer_path():
+    cfg = synth.make_config("tiny", read_scale=0.1)
+    ix = god.god_build_index(cfg.ref, cfg.ref_offsets, "10", 21, 11)
+    ox = oracle.Index(cfg.ref, cfg.ref_offsets, "10", 21, 11)
+    an, ao, ph = god.god_seed_reads(ix, cfg.reads.seq, cfg.reads.offsets)
+    oan, oao, oph = ox.seed_reads(cfg.reads.seq, cfg.reads.offsets)
+    assert np.array_equal(ph, oph) and np.array_equal(ao, oao)
+    assert np.array_equal(canon(an), canon(oan))
