@@ -275,14 +275,20 @@ JobSet make_jobs(const Params& P, const uint64_t* offsets, uint32_t n_seqs, cons
   }
   scan_exclusive_u64(js.kb, js.kb, nj, tot, st, scr);
   GOD_CUDA(cudaMemcpyAsync(js.kb + nj, tot, sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
-  js.total_pos = d2h_scalar(tot, st);
+  uint64_t h[2] = {0, 0};
+  GOD_CUDA(cudaMemcpyAsync(&h[0], tot, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+  GOD_CUDA(cudaMemcpyAsync(&h[1], offsets + n_seqs, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+  GOD_CUDA(cudaStreamSynchronize(st));
+  js.total_pos = h[0];
+  js.seq_bytes = h[1];
   return js;
 }
 
-void run_extract(const Params& P, const uint8_t* seq, const Job* jobs, const uint64_t* kb, uint32_t n_jobs,
-                 uint64_t total_pos, bool want_job, bool want_job_off, Records& rec, cudaStream_t st, Scratch& scr,
-                 uint64_t cap_hint, const char* tag) {
+void run_extract(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const Job* jobs, const uint64_t* kb,
+                 uint32_t n_jobs, uint64_t total_pos, bool want_job, bool want_job_off, Records& rec, cudaStream_t st,
+                 Scratch& scr, uint64_t cap_hint, const char* tag) {
   rec.n = 0;
+  if (run_extract2(P, seq, seq_bytes, jobs, n_jobs, want_job, want_job_off, rec, st, scr, cap_hint, tag)) return;
   if (n_jobs == 0 || total_pos == 0) {
     rec.cap = 1;
     rec.hz = scr.alloc<uint64_t>(1);

@@ -264,13 +264,86 @@ __global__ void k_write_entries(const uint64_t* __restrict__ hz, const uint32_t*
   }
 }
 
-__global__ void k_dir_fill(const uint32_t* __restrict__ kslot, uint64_t n_kept, uint32_t dir_bits, uint32_t* dir) {
-  const uint64_t nslots = 1ull << dir_bits;
-  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e <= n_kept; e += (uint64_t)gridDim.x * blockDim.x) {
-    const int64_t sp = e ? (int64_t)kslot[e - 1] : -1;
-    const int64_t se = e < n_kept ? (int64_t)kslot[e] : (int64_t)nslots;
-    for (int64_t s = sp + 1; s <= se; s++) dir[s] = (uint32_t)e;
+// K6a: dir[slot] = first kept entry of each non-empty slot (dir pre-filled with ~0; dir[2^B] = n_kept)
+__global__ void k_dir_mark(const uint32_t* __restrict__ kslot, uint64_t n_kept, uint32_t dir_bits, uint32_t* dir) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < n_kept; e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t s = kslot[e];
+    if (e == 0 || kslot[e - 1] != s) dir[s] = (uint32_t)e;
   }
+  if (blockIdx.x == 0 && threadIdx.x == 0) dir[1ull << dir_bits] = (uint32_t)n_kept;
+}
+
+// K6b: empty slots take the next non-empty slot's first entry: a suffix-min over dir[0 .. 2^B],
+// single pass, tiles processed right to left with a decoupled look-back on the running minimum.
+constexpr int DF_NT = 256, DF_IPT = 16, DF_TILE = DF_NT * DF_IPT;
+__global__ void __launch_bounds__(DF_NT) k_dir_suffix_min(uint32_t* dir, uint64_t n, uint64_t* status, uint32_t* ctr) {
+  __shared__ uint32_t s_tile;
+  __shared__ uint32_t warp_min[DF_NT / 32];
+  __shared__ uint32_t s_carry;
+  if (threadIdx.x == 0) s_tile = atomicAdd(ctr, 1u);
+  __syncthreads();
+  const uint64_t ntiles = (n + DF_TILE - 1) / DF_TILE;
+  const uint64_t rt = s_tile;                 // look-back order: right to left
+  const uint64_t t = ntiles - 1 - rt;         // tile position
+  const uint64_t base = t * DF_TILE + (uint64_t)threadIdx.x * DF_IPT;
+  uint32_t v[DF_IPT];
+#pragma unroll
+  for (int i = 0; i < DF_IPT; i++) v[i] = base + i < n ? dir[base + i] : 0xFFFFFFFFu;
+  // thread-local suffix minima
+#pragma unroll
+  for (int i = DF_IPT - 2; i >= 0; i--) v[i] = min(v[i], v[i + 1]);
+  // block suffix-min of the per-thread minima (v[0]); reverse inclusive scan over threads
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t x = v[0];
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t y = __shfl_down_sync(0xffffffffu, x, d);
+    if (lane + d < 32) x = min(x, y);
+  }
+  if (lane == 0) warp_min[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    uint32_t ws = lane < DF_NT / 32 ? warp_min[lane] : 0xFFFFFFFFu;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_down_sync(0xffffffffu, ws, d);
+      if (lane + d < 32) ws = min(ws, y);
+    }
+    if (lane < DF_NT / 32) warp_min[lane] = ws;  // inclusive suffix min over warps >= lane
+    if (lane == 0) {  // look-back over the tiles to the right (running min in the value field)
+      const uint64_t agg = ws;
+      uint64_t carry = 0xFFFFFFFFull;
+      if (rt == 0) {
+        lb_store(&status[0], LB_INC | agg);
+      } else {
+        lb_store(&status[rt], LB_AGG | agg);
+        int64_t j = (int64_t)rt - 1;
+        while (true) {
+          const uint64_t s = lb_load(&status[j]);
+          const uint64_t f = s & ~LB_VAL;
+          if (f == 0) continue;
+          carry = min(carry, s & LB_VAL);
+          if (f == LB_INC) break;
+          --j;
+        }
+        lb_store(&status[rt], LB_INC | min(carry, agg));
+      }
+      s_carry = (uint32_t)carry;
+    }
+  }
+  __syncthreads();
+  // suffix min of the threads after me within the block, then of the tiles to the right
+  uint32_t after = 0xFFFFFFFFu;
+  {
+    const uint32_t in_warp = __shfl_down_sync(0xffffffffu, x, 1);
+    if (lane < 31) after = in_warp;
+    if (lane == 31 && wid + 1 < DF_NT / 32) after = warp_min[wid + 1];
+    else if (lane < 31 && wid + 1 < DF_NT / 32) after = min(after, warp_min[wid + 1]);
+  }
+  after = min(after, s_carry);
+#pragma unroll
+  for (int i = 0; i < DF_IPT; i++)
+    if (base + i < n) dir[base + i] = min(v[i], after);
 }
 
 }  // namespace
@@ -314,7 +387,7 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
   JobSet js = make_jobs(P, ref_offsets, n_refs, nullptr, 0, 0, true, st, scr);
   Records rec;
   const uint64_t est = js.total_pos / (uint64_t)(P.w + 1) * 2 + js.total_pos / 8 + 4096;
-  run_extract(P, ref, js.jobs, js.kb, js.n, js.total_pos, false, false, rec, st, scr, est, "extract_ref");
+  run_extract(P, ref, js.seq_bytes, js.jobs, js.kb, js.n, js.total_pos, false, false, rec, st, scr, est, "extract_ref");
   const uint64_t n = rec.n;
   // K2: stable LSD radix sort on the 2k hash bits
   uint64_t* k0 = rec.hz;
@@ -404,7 +477,18 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
     GOD_LAUNCH("k_write_entries", k_write_entries, grid_for(n, 256), 256, 0, st, k0, v0, n, flag, dix, dstart, count, kept_off, cs, low_bits, ix->ent_key,
                                                      ix->ent_pos, kslot);
   }
-  GOD_LAUNCH("k_dir_fill", k_dir_fill, grid_for(n_kept + 1, 256), 256, 0, st, kslot, n_kept, B, ix->dir);
+  {
+    const uint64_t nd1 = (1ull << B) + 1;
+    GOD_CUDA(cudaMemsetAsync(ix->dir, 0xFF, nd1 * sizeof(uint32_t), st));
+    GOD_LAUNCH("k_dir_mark", k_dir_mark, min(grid_for(n_kept ? n_kept : 1, 256), 16u * num_sms()), 256, 0, st, kslot,
+               n_kept, B, ix->dir);
+    const uint64_t nt = (nd1 + DF_TILE - 1) / DF_TILE;
+    uint64_t* dst = scr.alloc<uint64_t>(nt);
+    uint32_t* dctr = scr.alloc<uint32_t>(1);
+    GOD_CUDA(cudaMemsetAsync(dst, 0, nt * sizeof(uint64_t), st));
+    GOD_CUDA(cudaMemsetAsync(dctr, 0, sizeof(uint32_t), st));
+    GOD_LAUNCH("k_dir_suffix_min", k_dir_suffix_min, (unsigned)nt, DF_NT, 0, st, ix->dir, nd1, dst, dctr);
+  }
   GOD_CUDA(cudaStreamSynchronize(st));
   if (const char* dd = getenv("GOD_DEBUG_DIR")) {  // developer aid: dump the intermediates
     auto dump = [&](const char* name, const void* p, size_t bytes) {

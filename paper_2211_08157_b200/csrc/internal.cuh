@@ -29,9 +29,14 @@ struct Records {
 // Run the fused sparsify + minimizer kernel over device jobs (kb = exclusive scan of nk + 1,
 // total_pos = kb[n_jobs]).  Allocates rec arrays from `scr` (capacity grown on demand), fills
 // rec.n (synchronizes once to read the count).
-void run_extract(const Params& P, const uint8_t* seq, const Job* jobs, const uint64_t* kb, uint32_t n_jobs,
-                 uint64_t total_pos, bool want_job, bool want_job_off, Records& rec, cudaStream_t st, Scratch& scr,
-                 uint64_t cap_hint, const char* tag = "k_extract");
+void run_extract(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const Job* jobs, const uint64_t* kb,
+                 uint32_t n_jobs, uint64_t total_pos, bool want_job, bool want_job_off, Records& rec, cudaStream_t st,
+                 Scratch& scr, uint64_t cap_hint, const char* tag = "k_extract");
+// Specialised register-resident kernel (extract2.cu) for x == 1 patterns of period 1 or 2 and
+// (k, w) in {(21,11), (19,19), (15,10)}; returns false if not applicable.
+bool run_extract2(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const Job* jobs, uint32_t n_jobs,
+                  bool want_job, bool want_job_off, Records& rec, cudaStream_t st, Scratch& scr,
+                  uint64_t cap_hint, const char* tag);
 
 // Build jobs for n sequences: phase from `phases` (nullable -> 0) or, if p_all != 0, one job per
 // (sequence, s) for s < p_all (job index = seq * p_all + s).  nk capped at kcap (0 = no cap).
@@ -41,6 +46,7 @@ struct JobSet {
   uint64_t* kb = nullptr;
   uint32_t n = 0;
   uint64_t total_pos = 0;
+  uint64_t seq_bytes = 0;   // offsets[n_seqs]: bytes of the sequence buffer
 };
 JobSet make_jobs(const Params& P, const uint64_t* offsets, uint32_t n_seqs, const uint8_t* phases, uint32_t p_all,
                  uint32_t kcap, bool global_pos, cudaStream_t st, Scratch& scr);

@@ -141,8 +141,9 @@ uint64_t seed_reads(const god_index* ix, const uint8_t* reads, const uint64_t* o
     } else {
       const uint32_t kcap = (t + 1) * (uint32_t)P.w + (uint32_t)P.w;
       JobSet js = make_jobs(P, offsets, n_reads, nullptr, p, kcap, false, st, scr);
+      const uint64_t js_bytes = js.seq_bytes;
       Records rec;
-      run_extract(P, reads, js.jobs, js.kb, js.n, js.total_pos, false, true, rec, st, scr,
+      run_extract(P, reads, js.seq_bytes, js.jobs, js.kb, js.n, js.total_pos, false, true, rec, st, scr,
                   js.total_pos / (uint64_t)(P.w + 1) * 2 + js.total_pos / 8 + 4096, "extract_phase");
       uint32_t* redo = scr.alloc<uint32_t>(n_reads);
       uint32_t* n_redo = scr.alloc<uint32_t>(1);
@@ -159,7 +160,7 @@ uint64_t seed_reads(const god_index* ix, const uint8_t* reads, const uint64_t* o
         GOD_CUDA(cudaMemcpyAsync(kb2 + (uint64_t)nr * p, tot2, sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
         const uint64_t tp2 = d2h_scalar(tot2, st);
         Records rec2;
-        run_extract(P, reads, jobs2, kb2, nr * p, tp2, false, true, rec2, st, scr, tp2 / 4 + 4096, "extract_phase_redo");
+        run_extract(P, reads, js_bytes, jobs2, kb2, nr * p, tp2, false, true, rec2, st, scr, tp2 / 4 + 4096, "extract_phase_redo");
         uint32_t* n_redo2 = scr.alloc<uint32_t>(1);
         GOD_CUDA(cudaMemsetAsync(n_redo2, 0, sizeof(uint32_t), st));
         GOD_LAUNCH("k_phase", k_phase, grid_for(nr, 128), 128, 0, st, v, jobs2, rec2.job_off, rec2.hz, rec2.pos, redo, nr, p, t, P.w, 0,
@@ -170,7 +171,7 @@ uint64_t seed_reads(const god_index* ix, const uint8_t* reads, const uint64_t* o
   // ---------------- S3: minimizers of PQ_a
   JobSet js = make_jobs(P, offsets, n_reads, phases, 0, 0, false, st, scr);
   Records rec;
-  run_extract(P, reads, js.jobs, js.kb, js.n, js.total_pos, true, true, rec, st, scr,
+  run_extract(P, reads, js.seq_bytes, js.jobs, js.kb, js.n, js.total_pos, true, true, rec, st, scr,
               js.total_pos / (uint64_t)(P.w + 1) * 2 + js.total_pos / 8 + 4096, "extract_seed");
   // ---------------- S4: probes -> anchors
   const uint64_t n = rec.n;

@@ -262,3 +262,43 @@ def test_seed_host_pointer_path():
     oan, oao, oph = ox.seed_reads(cfg.reads.seq, cfg.reads.offsets)
     assert np.array_equal(ph, oph) and np.array_equal(ao, oao)
     assert np.array_equal(canon(an), canon(oan))
+
+
+# ------------------------------------------------------------------------------------ K1 v2 (specialised)
+X2_COMBOS = [("10", 21, 11), ("01", 21, 11), ("1", 21, 11), ("10", 19, 19), ("1", 19, 19), ("10", 15, 10),
+             ("1", 15, 10)]
+
+
+@pytest.mark.parametrize("combo", X2_COMBOS, ids=[f"{c[0]}-k{c[1]}-w{c[2]}" for c in X2_COMBOS])
+@pytest.mark.parametrize("keybits", [None, "9"])
+def test_x2_specialised_kernel_parity(combo, keybits, monkeypatch):
+    """The register-resident kernel (extract2.cu) on long N-free sequences (fast path), sequences
+    with N runs and short sequences (exact slow path); keybits=9 makes 31-bit key ties frequent so
+    the exactness check + slow path run on most tiles."""
+    pattern, k, w = combo
+    if keybits:
+        monkeypatch.setenv("GOD_DEBUG_KEYBITS", keybits)
+    rng = np.random.default_rng(zlib.crc32(repr(combo).encode()))
+    seqs = [synth.random_acgt(rng, int(rng.integers(20000, 60000))) for _ in range(3)]
+    seqs += [synth.sprinkle_n(synth.random_acgt(rng, 30000), 5, 6, 40)]
+    seqs += [synth.random_acgt(rng, int(rng.integers(0, 200)), 0.01) for _ in range(60)]
+    seqs += [np.frombuffer(b"ACGT" * 3000, np.uint8).copy(), np.frombuffer(b"A" * 5000, np.uint8).copy()]
+    seq, offs = synth.concat(seqs)
+    phases = rng.integers(0, len(pattern), size=len(offs) - 1).astype(np.uint8)
+    for gp, ph in ((True, None), (False, phases)):
+        want, wo = oracle.minimizers_batch(seq, offs, pattern, k, w, phases=ph, global_pos=gp)
+        h, ps, z, oo = god.god_minimizers(cu(seq), cu(offs), pattern, k, w,
+                                          phases=None if ph is None else cu(ph), global_pos=gp)
+        assert np.array_equal(np_(oo), wo)
+        assert np.array_equal(np_(h), want["hash"])
+        assert np.array_equal(np_(ps).astype(np.uint64), want["pos"])
+        assert np.array_equal(np_(z), want["strand"])
+
+
+def test_x2_matches_generic_kernel(monkeypatch):
+    cfg = synth.make_config("tiny", read_scale=0.2)
+    a = god.god_minimizers(cu(cfg.ref), cu(cfg.ref_offsets), "10", 21, 11, global_pos=True)
+    monkeypatch.setenv("GOD_DISABLE_X2", "1")
+    b = god.god_minimizers(cu(cfg.ref), cu(cfg.ref_offsets), "10", 21, 11, global_pos=True)
+    for x, y in zip(a, b):
+        assert torch.equal(x, y)
