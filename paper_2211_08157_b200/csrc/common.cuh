@@ -96,13 +96,15 @@ constexpr uint64_t LB_AGG = 1ull << 62;
 constexpr uint64_t LB_INC = 2ull << 62;
 constexpr uint64_t LB_VAL = (1ull << 62) - 1;
 
+// The status word is the only datum exchanged (no payload is published through it), so relaxed
+// accesses suffice; acquire/release here would add an L1 invalidate + fence to every spin.
 __device__ __forceinline__ void lb_store(uint64_t* p, uint64_t v) {
-  cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> a(*reinterpret_cast<unsigned long long*>(p));
-  a.store(v, cuda::memory_order_release);
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ uint64_t lb_load(uint64_t* p) {
-  cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> a(*reinterpret_cast<unsigned long long*>(p));
-  return a.load(cuda::memory_order_acquire);
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
 }
 
 // Called by ONE thread of tile `tile` with the tile's local total; returns the exclusive prefix.
@@ -123,6 +125,34 @@ __device__ inline uint64_t lb_exclusive(uint64_t* status, uint64_t tile, uint64_
     --j;
   }
   lb_store(&status[tile], LB_INC | (excl + local));
+  return excl;
+}
+
+// Warp-cooperative variant (call with a whole warp): each round inspects 32 predecessors at once.
+__device__ inline uint64_t lb_exclusive_warp(uint64_t* status, uint64_t tile, uint64_t local) {
+  const int lane = threadIdx.x & 31;
+  if (tile == 0) {
+    if (lane == 0) lb_store(&status[0], LB_INC | local);
+    return 0;
+  }
+  if (lane == 0) lb_store(&status[tile], LB_AGG | local);
+  uint64_t excl = 0;
+  int64_t j = (int64_t)tile - 1 - lane;
+  while (true) {
+    uint64_t s = j >= 0 ? lb_load(&status[j]) : (LB_INC | 0ull);
+    while (__any_sync(0xffffffffu, (s & ~LB_VAL) == 0)) {
+      if ((s & ~LB_VAL) == 0) s = lb_load(&status[j]);
+    }
+    const uint32_t inc = __ballot_sync(0xffffffffu, (s & ~LB_VAL) == LB_INC);
+    const int first = inc ? __ffs(inc) - 1 : 32;  // closest predecessor with an inclusive prefix
+    uint64_t v = lane <= first ? (s & LB_VAL) : 0ull;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    excl += v;
+    if (inc) break;
+    j -= 32;
+  }
+  if (lane == 0) lb_store(&status[tile], LB_INC | (excl + local));
   return excl;
 }
 

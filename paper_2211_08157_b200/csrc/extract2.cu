@@ -24,6 +24,8 @@
 //   D. exact slow path for the whole tile (64-bit hashes in SMEM, direct window rule incl. partial
 //      windows) when the tile has an N, a run shorter than w, or such a key tie.
 //   E. ordered compaction: staged in SMEM, tile offset by decoupled look-back, coalesced copy.
+#include <cstdio>
+#include <cstdlib>
 #include "internal.cuh"
 
 namespace god {
@@ -32,6 +34,9 @@ namespace {
 
 constexpr int X2_NT = 256;
 constexpr int X2_OUT_BLOCKS = X2_NT - 2;
+#ifndef X2_MINB
+#define X2_MINB 4
+#endif
 
 struct X2Args {
   const uint8_t* seq;
@@ -51,6 +56,8 @@ struct X2Args {
   uint64_t* job_off;
   uint64_t cap;
   uint64_t* total_out;
+  uint32_t dbg_flags;      // developer toggles (GOD_X2_DBG): 1 = unordered output, 2 = no tie check
+  uint32_t* dbg_counts;    // [0] tiles on the slow path, [1] tiles with a key tie
 };
 
 __device__ __forceinline__ uint32_t find_job_le(const uint64_t* arr, uint32_t lo, uint32_t hi, uint64_t g) {
@@ -99,7 +106,7 @@ __device__ __forceinline__ uint64_t wang_hash_k(uint64_t key) {
 struct X2Shared {
   uint32_t j0, j1;
   uint64_t cw_lo, cw_hi;
-  uint32_t any_n, slow, tie;
+  uint32_t any_n, slow, simple;
   uint64_t base;
   uint32_t warp_cnt[X2_NT / 32];
   uint32_t tile;
@@ -113,161 +120,174 @@ struct X2Cfg {
   static constexpr int POS = X2_NT * W;                 // positions per tile (incl. halo blocks)
   // code words the tile can touch: every block's window, plus one partial word per job (<= 256 jobs)
   static constexpr int MAXWORDS = (POS + X2_NT * (K - 1) + 15) / 16 + X2_NT + 8;
+  static constexpr size_t SMEM = (size_t)(256 + 2 * MAXWORDS + 2 * 8 * W + 2) * 4  // lut, codes, nmask, xchg
+                                 + (size_t)POS * 8                                   // HZ (or H64 on the slow path)
+                                 + (size_t)POS * 4                                   // selected list + keys
+                                 + (size_t)X2_NT * 8 + 16;                           // per-block (job, l0)
 };
+
+// 16 patterned bases (MSB-first 2-bit codes) from the ASCII bytes at A (a PS-strided gather);
+// *nm gets the N bits (bit 15 - b for base b).  nb = bases that exist (<= 16).
+template <int PS, bool CHECKED>
+__device__ __forceinline__ uint32_t pack16(const uint8_t* seq, uint64_t seq_bytes, uint64_t A, int nb,
+                                           const uint32_t* lut, uint32_t* nm) {
+  const uint64_t Aa = A & ~3ull;
+  const uint32_t d8 = (uint32_t)(A - Aa) * 8;
+  constexpr int NL = 4 * PS + 1;
+  uint32_t w[NL];
+  const uint32_t* src = reinterpret_cast<const uint32_t*>(seq + Aa);
+#pragma unroll
+  for (int i = 0; i < NL; i++) {
+    if constexpr (CHECKED) {
+      const uint64_t ad = Aa + 4ull * i;
+      uint32_t v = 0;
+      if (ad + 4 <= seq_bytes) v = __ldg(src + i);
+      else
+        for (uint64_t q = ad; q < seq_bytes; q++) v |= (uint32_t)seq[q] << (8 * (q - ad));
+      w[i] = v;
+    } else {
+      w[i] = __ldg(src + i);
+    }
+  }
+  uint32_t t4[4];
+  uint32_t bad_any = 0, badw[4];
+#pragma unroll
+  for (int g = 0; g < 4; g++) {
+    uint32_t x;
+    if constexpr (PS == 1) {
+      x = __funnelshift_r(w[g], w[g + 1], d8);
+    } else {
+      const uint32_t lo = __funnelshift_r(w[2 * g], w[2 * g + 1], d8);
+      const uint32_t hi = __funnelshift_r(w[2 * g + 1], w[2 * g + 2], d8);
+      x = __byte_perm(lo, hi, 0x6420);
+    }
+    const uint32_t c = ((x >> 1) ^ (x >> 2)) & 0x03030303u;  // A0 C1 G2 T3 (either case)
+    const uint32_t t = c * 0x40100401u;                       // top byte = the 4 codes, MSB-first
+    badw[g] = (x & 0xDFDFDFDFu) ^ lut[t >> 24];              // nonzero byte <=> not A/C/G/T
+    bad_any |= badw[g];
+    t4[g] = t;
+  }
+  uint32_t word = __byte_perm(__byte_perm(t4[1], t4[0], 0x7300), __byte_perm(t4[3], t4[2], 0x0073), 0x3254);
+  if (nb < 16) word &= 0xFFFFFFFFu << (32 - 2 * nb);
+  uint32_t n = 0;
+  if (bad_any) {
+#pragma unroll
+    for (int g = 0; g < 4; g++)
+#pragma unroll
+      for (int i = 0; i < 4; i++)
+        if (((badw[g] >> (8 * i)) & 0xFFu) && 4 * g + i < nb) n |= 1u << (15 - (4 * g + i));
+  }
+  *nm = n;
+  return word;
+}
 
 // ---------------------------------------------------------------------------------------------
 template <int K, int W, int PS>
-__global__ void __launch_bounds__(X2_NT, 1) k_extract2(X2Args a) {
+__global__ void __launch_bounds__(X2_NT, X2_MINB) k_extract2(X2Args a) {
   using C = X2Cfg<K, W, PS>;
   constexpr int NB = C::NB, NWIN = C::NWIN, NLOAD = C::NLOAD, POS = C::POS;
   extern __shared__ __align__(16) unsigned char x2_smem[];
-  // layout: lut[256] | codes[MAXWORDS] | nmask[MAXWORDS] | xchg[2][8][W] | stage (12 B x POS, or 8 B x POS H64)
   uint32_t* lut = reinterpret_cast<uint32_t*>(x2_smem);
   uint32_t* codes = lut + 256;
   uint32_t* nmask = codes + C::MAXWORDS;
-  uint32_t* xchg = nmask + C::MAXWORDS;                     // [2][8][W]
-  uint64_t* st_hz = reinterpret_cast<uint64_t*>(xchg + 2 * 8 * W + 2);  // 8-aligned (W*16 even)
-  uint32_t* st_pos = reinterpret_cast<uint32_t*>(st_hz + POS);
-  uint16_t* st_e = reinterpret_cast<uint16_t*>(st_pos + POS);
-  uint64_t* H64 = st_hz;  // slow path alias (POS entries)
+  uint32_t* xchg = nmask + C::MAXWORDS;                                  // [2][8][W]
+  uint64_t* HZ = reinterpret_cast<uint64_t*>(xchg + 2 * 8 * W + 2);       // [POS] hash | strand<<63 (slow: H64)
+  uint16_t* sel_e = reinterpret_cast<uint16_t*>(HZ + POS);               // [POS] selected tile positions
+  uint16_t* sel_k = sel_e + POS;                                         // [POS] low 16 key bits (tie check)
+  uint32_t* blk_j = reinterpret_cast<uint32_t*>(sel_k + POS);             // [256] job of each block
+  uint32_t* blk_l = blk_j + X2_NT;                                       // [256] first k-mer index of each block
   __shared__ X2Shared sh;
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  // ---- tile id (dynamic, in launch order -> look-back safe) and job range
   if (tid == 0) {
     const uint32_t t = atomicAdd(a.tile_ctr, 1u);
     sh.tile = t;
     const int64_t b_first = (int64_t)t * X2_OUT_BLOCKS - 1;
     const int64_t b_last = (int64_t)t * X2_OUT_BLOCKS + X2_NT - 2;
+    const uint64_t gmax = a.total_blocks * W - 1;
     const uint64_t gfirst = b_first < 0 ? 0 : (uint64_t)b_first * W;
     uint64_t glast = (uint64_t)(b_last < 0 ? 0 : b_last) * W;
-    const uint64_t gmax = a.total_blocks * W - 1;
     if (glast > gmax) glast = gmax;
-    sh.j0 = find_job_le(a.kb, 0, a.n_jobs - 1, gfirst);
-    sh.j1 = find_job_le(a.kb, sh.j0, a.n_jobs - 1, glast);
-    sh.any_n = 0; sh.slow = 0; sh.tie = 0;
+    const uint32_t j0 = find_job_le(a.kb, 0, a.n_jobs - 1, gfirst);
+    const uint32_t j1 = find_job_le(a.kb, j0, a.n_jobs - 1, glast);
+    sh.j0 = j0; sh.j1 = j1;
+    const uint64_t lo = b_first < 0 ? a.cw[0] : a.cw[j0] + (gfirst - a.kb[j0]) / 16;
+    uint64_t hi = a.cw[j1] + (glast - a.kb[j1] + NB + 15) / 16 + 1;
+    if (hi > a.cw[j1 + 1]) hi = a.cw[j1 + 1];
+    if (hi < lo) hi = lo;
+    if (hi > lo + C::MAXWORDS) hi = lo + C::MAXWORDS;  // cannot happen for 256 blocks; guard
+    sh.cw_lo = lo; sh.cw_hi = hi;
+    // "simple" tile: one job and every byte of its words inside the buffer -> no per-word checks
+    const Job jb = a.jobs[j0];
+    const uint64_t last_byte = jb.seq_off + jb.phase + a.one0 + (uint64_t)PS * 16 * (hi - a.cw[j0]) + 4 * PS + 8;
+    sh.simple = (j0 == j1) && last_byte <= a.seq_bytes;
+    sh.any_n = 0; sh.slow = 0;
   }
-  // expected-letter table: for 4 MSB-first codes pk, bytes "ACGT"[c_i], base 0 in byte 0
-  {
-    const uint32_t pk = tid;
-    const uint32_t L4 = 0x54474341u;  // 'A','C','G','T'
+  {  // expected-letter table: for 4 MSB-first codes pk, bytes "ACGT"[c_i], base 0 in byte 0
+    const uint32_t L4 = 0x54474341u;
     uint32_t e = 0;
 #pragma unroll
-    for (int i = 0; i < 4; i++) {
-      const uint32_t c = (pk >> (6 - 2 * i)) & 3u;
-      e |= ((L4 >> (8 * c)) & 0xFFu) << (8 * i);
-    }
+    for (int i = 0; i < 4; i++) e |= ((L4 >> (8 * ((tid >> (6 - 2 * i)) & 3u))) & 0xFFu) << (8 * i);
     lut[tid] = e;
   }
   __syncthreads();
   const uint32_t tile = sh.tile;
   const uint32_t j0 = sh.j0, j1 = sh.j1;
+  const uint64_t cw_lo = sh.cw_lo;
+  const int nwords = (int)(sh.cw_hi - cw_lo);
 
-  // ---- my block
+  // ---- my block: job J, first k-mer index l0 (32-bit: nk < 2^32)
   const int64_t myb = (int64_t)tile * X2_OUT_BLOCKS - 1 + tid;
   const bool blk_in = myb >= 0 && (uint64_t)myb < a.total_blocks;
-  uint32_t J = j0;
-  uint64_t l0 = 0;
-  uint32_t nk = 0;
+  uint32_t J = j0, l0 = 0, nk = 0;
   if (blk_in) {
     const uint64_t g = (uint64_t)myb * W;
-    J = find_job_le(a.kb, j0, j1, g);
-    l0 = g - a.kb[J];
+    J = (j0 == j1) ? j0 : find_job_le(a.kb, j0, j1, g);
+    l0 = (uint32_t)(g - a.kb[J]);
     nk = a.jobs[J].nk;
   }
-  // tile code-word range (from the first and last blocks' jobs)
-  if (tid == 0) {
-    uint64_t lo;
-    const int64_t bf = (int64_t)tile * X2_OUT_BLOCKS - 1;
-    if (bf < 0) lo = a.cw[0];
-    else {
-      const uint64_t g = (uint64_t)bf * W;
-      lo = a.cw[j0] + (g - a.kb[j0]) / 16;
-    }
-    sh.cw_lo = lo;
-    // end: the last block's window, within its job
-    const int64_t bl = (int64_t)tile * X2_OUT_BLOCKS + X2_NT - 2;
-    uint64_t gl = (uint64_t)(bl < 0 ? 0 : bl) * W;
-    const uint64_t gmax = a.total_blocks * W - 1;
-    if (gl > gmax) gl = gmax;
-    const uint64_t ll = gl - a.kb[j1];
-    uint64_t hi = a.cw[j1] + (ll + NB + 15) / 16 + 1;
-    if (hi > a.cw[j1 + 1]) hi = a.cw[j1 + 1];
-    sh.cw_hi = hi < lo ? lo : hi;
-  }
-  __syncthreads();
-  const uint64_t cw_lo = sh.cw_lo;
-  uint64_t cw_hi = sh.cw_hi;
-  if (cw_hi > cw_lo + C::MAXWORDS) cw_hi = cw_lo + C::MAXWORDS;  // cannot happen for 256 blocks; guard
-  const int nwords = (int)(cw_hi - cw_lo);
+  blk_j[tid] = J;
+  blk_l[tid] = l0;
 
   // ---------------------------------------------------------------- A. sparsify into SMEM
   {
     uint32_t my_n = 0;
-    uint32_t Jw = j0;
-    for (int wi = tid; wi < nwords; wi += X2_NT) {
-      uint32_t word = 0, nm = 0;
-      {
+    if (sh.simple) {
+      const Job jb = a.jobs[j0];
+      const uint64_t w0 = cw_lo - a.cw[j0];  // first word of the tile inside the job
+      const uint32_t ncode = jb.nk ? jb.nk + K - 1 : 0;
+      const uint64_t A0 = jb.seq_off + jb.phase + a.one0;
+      for (int wi = tid; wi < nwords; wi += X2_NT) {
+        const uint64_t q0 = (w0 + wi) * 16;
+        uint32_t nm = 0, word = 0;
+        if (q0 < ncode) {
+          const int nb = (int)min((uint64_t)16, ncode - q0);
+          word = pack16<PS, false>(a.seq, a.seq_bytes, A0 + (uint64_t)PS * q0, nb, lut, &nm);
+        }
+        codes[wi] = word;
+        nmask[wi] = nm;
+        my_n |= nm;
+      }
+    } else {
+      uint32_t Jw = j0;
+      for (int wi = tid; wi < nwords; wi += X2_NT) {
         const uint64_t gw = cw_lo + wi;
         Jw = find_job_le(a.cw, Jw, j1, gw);
-        while (Jw < j1 && a.cw[Jw + 1] <= gw) ++Jw;
         const Job jb = a.jobs[Jw];
         const uint64_t ncode = jb.nk ? (uint64_t)jb.nk + K - 1 : 0;
         const uint64_t q0 = (gw - a.cw[Jw]) * 16;
+        uint32_t nm = 0, word = 0;
         if (q0 < ncode) {
           const int nb = (int)min((uint64_t)16, ncode - q0);
-          const uint64_t A = jb.seq_off + jb.phase + a.one0 + (uint64_t)PS * q0;
-          const uint64_t Aa = A & ~3ull;
-          const uint32_t d8 = (uint32_t)(A - Aa) * 8;
-          constexpr int NL = 4 * PS + 1;
-          uint32_t w[NL];
-#pragma unroll
-          for (int i = 0; i < NL; i++) {
-            const uint64_t ad = Aa + 4ull * i;
-            w[i] = ad + 4 <= a.seq_bytes ? __ldg(reinterpret_cast<const uint32_t*>(a.seq + ad))
-                                         : 0u;
-            if (ad + 4 > a.seq_bytes && ad < a.seq_bytes) {  // ragged tail of the buffer
-              uint32_t v = 0;
-              for (uint64_t q = ad; q < a.seq_bytes; q++) v |= (uint32_t)a.seq[q] << (8 * (q - ad));
-              w[i] = v;
-            }
-          }
-          uint32_t t4[4];
-#pragma unroll
-          for (int g = 0; g < 4; g++) {
-            uint32_t x;
-            if constexpr (PS == 1) {
-              x = __funnelshift_r(w[g], w[g + 1], d8);
-            } else {
-              const uint32_t lo = __funnelshift_r(w[2 * g], w[2 * g + 1], d8);
-              const uint32_t hi = __funnelshift_r(w[2 * g + 1], w[2 * g + 2], d8);
-              x = __byte_perm(lo, hi, 0x6420);
-            }
-            const uint32_t c = ((x >> 1) ^ (x >> 2)) & 0x03030303u;
-            const uint32_t t = c * 0x40100401u;  // top byte = the 4 codes, MSB-first
-            uint32_t bad = (x & 0xDFDFDFDFu) ^ lut[t >> 24];
-            const int valid_here = nb - 4 * g;  // bases of this group that exist
-            if (valid_here < 4) bad = valid_here <= 0 ? 0u : (bad & (0xFFFFFFFFu >> (8 * (4 - valid_here))));
-            if (bad) {
-#pragma unroll
-              for (int i = 0; i < 4; i++)
-                if ((bad >> (8 * i)) & 0xFFu) nm |= 1u << (15 - (4 * g + i));
-            }
-            t4[g] = t;
-          }
-          const uint32_t u = __byte_perm(t4[1], t4[0], 0x7300);
-          const uint32_t v = __byte_perm(t4[3], t4[2], 0x0073);
-          word = __byte_perm(u, v, 0x3254);
-          if (nb < 16) word &= 0xFFFFFFFFu << (32 - 2 * nb);
+          word = pack16<PS, true>(a.seq, a.seq_bytes, jb.seq_off + jb.phase + a.one0 + (uint64_t)PS * q0, nb,
+                                  lut, &nm);
         }
+        codes[wi] = word;
+        nmask[wi] = nm;
+        my_n |= nm;
       }
-      codes[wi] = word;
-      nmask[wi] = nm;
-      my_n |= nm;
     }
-    if (__syncthreads_or(my_n != 0)) {
-      if (tid == 0) sh.any_n = 1;
-    }
+    if (__syncthreads_or(my_n != 0) && tid == 0) sh.any_n = 1;
   }
   __syncthreads();
 
@@ -275,14 +295,13 @@ __global__ void __launch_bounds__(X2_NT, 1) k_extract2(X2Args a) {
   const bool blk_has_kmers = blk_in && l0 < nk;
   uint32_t win[NWIN];
   {
-    const uint64_t gwb = a.cw[J] + l0 / 16;
-    const int wbase = (int)(gwb - cw_lo);
-    const uint32_t off = (uint32_t)(l0 % 16) * 2;
+    const int wbase = (int)(a.cw[J] + l0 / 16 - cw_lo);
+    const uint32_t off = (l0 % 16) * 2;
     uint32_t raw[NLOAD + 1];
 #pragma unroll
     for (int i = 0; i <= NLOAD; i++) {
       const int idx = wbase + i;
-      raw[i] = (blk_has_kmers && idx >= 0 && idx < C::MAXWORDS) ? codes[idx] : 0u;
+      raw[i] = (blk_has_kmers && idx < C::MAXWORDS) ? codes[idx] : 0u;
     }
 #pragma unroll
     for (int i = 0; i < NWIN; i++) win[i] = __funnelshift_l(raw[i + 1], raw[i], off);
@@ -292,28 +311,28 @@ __global__ void __launch_bounds__(X2_NT, 1) k_extract2(X2Args a) {
   for (int i = 0; i < NWIN; i++) rcw[i] = ~rev2(win[NWIN - 1 - i]);
   constexpr int PADB = 32 * NWIN - 2 * NB;
 
-  uint64_t hz[W];     // hash | strand << 63
+  const uint32_t ks = a.key_shift;
   uint32_t key[W];
   uint32_t palmask = 0;
-  const uint32_t ks = a.key_shift;
+  const uint32_t nvalid = blk_has_kmers ? min((uint32_t)W, nk - l0) : 0u;  // k-mer starts in this block
 #pragma unroll
   for (int i = 0; i < W; i++) {
     const uint64_t fwd = ext_bits(win, 2 * i, 2 * K);
     const uint64_t rev = ext_bits(rcw, PADB + 2 * (NB - i - K), 2 * K);
     const bool z = fwd > rev;
     const uint64_t h = wang_hash_k<K>(z ? rev : fwd);
-    hz[i] = h | ((uint64_t)z << 63);
+    HZ[tid * W + i] = h | ((uint64_t)z << 63);
     uint32_t kk = (uint32_t)(h >> ks) + 1u;
     if constexpr ((K & 1) == 0) {
       if (fwd == rev) { kk = 0xFFFFFFFFu; palmask |= 1u << i; }
     }
-    key[i] = (blk_has_kmers && l0 + i < nk) ? kk : 0u;
+    key[i] = (uint32_t)i < nvalid ? kk : 0u;
   }
 
   // ---------------------------------------------------------------- C. selection on keys
   uint32_t selmask = 0;
-  bool need_slow = false;
   if (!sh.any_n) {
+    bool need_slow = false;
     uint32_t PF[W], SF[W];
     PF[0] = key[0];
 #pragma unroll
@@ -321,9 +340,8 @@ __global__ void __launch_bounds__(X2_NT, 1) k_extract2(X2Args a) {
     SF[W - 1] = key[W - 1];
 #pragma unroll
     for (int i = W - 2; i >= 0; i--) SF[i] = min(SF[i + 1], key[i]);
-    // next block's prefix minima
-    uint32_t* xpf = xchg;            // [8][W]
-    uint32_t* xsf = xchg + 8 * W;    // [8][W]
+    uint32_t* xpf = xchg;
+    uint32_t* xsf = xchg + 8 * W;
     if (lane == 0) {
 #pragma unroll
       for (int i = 0; i < W; i++) xpf[wid * W + i] = PF[i];
@@ -331,10 +349,10 @@ __global__ void __launch_bounds__(X2_NT, 1) k_extract2(X2Args a) {
     __syncthreads();
     uint32_t nPF[W];
 #pragma unroll
-    for (int i = 0; i < W; i++) {
-      uint32_t v = __shfl_down_sync(0xffffffffu, PF[i], 1);
-      if (lane == 31) v = (wid < 7) ? xpf[(wid + 1) * W + i] : 0u;
-      nPF[i] = v;
+    for (int i = 0; i < W; i++) nPF[i] = __shfl_down_sync(0xffffffffu, PF[i], 1);
+    if (lane == 31) {
+#pragma unroll
+      for (int i = 0; i < W; i++) nPF[i] = (wid < 7) ? xpf[(wid + 1) * W + i] : 0u;
     }
     uint32_t WM[W];
     WM[0] = SF[0];
@@ -354,10 +372,10 @@ __global__ void __launch_bounds__(X2_NT, 1) k_extract2(X2Args a) {
     __syncthreads();
     uint32_t pSX[W];
 #pragma unroll
-    for (int i = 0; i < W; i++) {
-      uint32_t v = __shfl_up_sync(0xffffffffu, SX[i], 1);
-      if (lane == 0) v = (wid > 0) ? xsf[(wid - 1) * W + i] : 0u;
-      pSX[i] = v;
+    for (int i = 0; i < W; i++) pSX[i] = __shfl_up_sync(0xffffffffu, SX[i], 1);
+    if (lane == 0) {
+#pragma unroll
+      for (int i = 0; i < W; i++) pSX[i] = (wid > 0) ? xsf[(wid - 1) * W + i] : 0u;
     }
 #pragma unroll
     for (int o = 0; o < W; o++) {
@@ -365,35 +383,30 @@ __global__ void __launch_bounds__(X2_NT, 1) k_extract2(X2Args a) {
       const uint32_t k = key[o];
       bool s = (k == mm) && k != 0u;
       if constexpr ((K & 1) == 0) s = s && k != 0xFFFFFFFFu;
-      if (k != 0u && mm == 0u) need_slow = true;  // run shorter than w: partial-window rule
+      need_slow |= (k != 0u) & (mm == 0u);  // a run shorter than w: partial-window rule
       if (s) selmask |= 1u << o;
     }
     if (tid == 0 || tid == X2_NT - 1) need_slow = false;  // halo blocks are not emitted
-  }
-  if (__syncthreads_or(need_slow)) {
-    if (tid == 0) sh.slow = 1;
+    if (__syncthreads_or(need_slow) && tid == 0) sh.slow = 1;
   }
   __syncthreads();
 
-  // ---------------------------------------------------------------- D. exact slow path
+  // ---------------------------------------------------------------- D. exact slow path (whole tile)
   auto slow_path = [&]() {
-    // 64-bit H (hash+1; 0 barrier; ~0 palindrome) for every position of the tile, exact N handling
+    uint64_t* H64 = HZ;  // hash+1, 0 barrier, ~0 palindrome; HZ is rebuilt afterwards
 #pragma unroll
     for (int i = 0; i < W; i++) {
       uint64_t hv = 0;
-      if (blk_has_kmers && l0 + i < nk) {
-        const uint64_t q = l0 + i;  // k-mer start (patterned index) in job J
-        // N bits for bases q .. q+K-1
-        const uint64_t gwq = a.cw[J] + q / 16;
-        const int wb = (int)(gwq - cw_lo);
-        const uint32_t o = (uint32_t)(q % 16);
+      if ((uint32_t)i < nvalid) {
+        const uint32_t q = l0 + i;
+        const int wb = (int)(a.cw[J] + q / 16 - cw_lo);
+        const uint32_t o = q % 16;
         bool anyn = false;
         for (int b = 0; b < K; b++) {
           const int wi2 = wb + (int)((o + b) / 16);
-          const uint32_t bit = 15 - ((o + b) % 16);
-          if (wi2 >= 0 && wi2 < C::MAXWORDS && ((nmask[wi2] >> bit) & 1u)) anyn = true;
+          if (wi2 < C::MAXWORDS && ((nmask[wi2] >> (15 - ((o + b) % 16))) & 1u)) anyn = true;
         }
-        if (!anyn) hv = ((palmask >> i) & 1u) ? ~0ull : (hz[i] & ~(1ull << 63)) + 1;
+        if (!anyn) hv = ((palmask >> i) & 1u) ? ~0ull : (HZ[tid * W + i] & ~(1ull << 63)) + 1;
       }
       H64[tid * W + i] = hv;
     }
@@ -425,14 +438,27 @@ __global__ void __launch_bounds__(X2_NT, 1) k_extract2(X2Args a) {
         if (s) m |= 1u << i;
       }
     }
-    selmask = m;
     __syncthreads();
+    selmask = m;
   };
-  if (sh.any_n || sh.slow) slow_path();
+
+  // the slow path overwrites HZ with H64; keep the strand bits in a register mask to rebuild it
+  uint32_t zmask = 0;
+  if (sh.any_n || sh.slow) {
+    if (tid == 0 && a.dbg_counts) atomicAdd(&a.dbg_counts[0], 1u);
+#pragma unroll
+    for (int i = 0; i < W; i++) zmask |= (uint32_t)(HZ[tid * W + i] >> 63) << i;
+    slow_path();
+#pragma unroll
+    for (int i = 0; i < W; i++) {
+      const uint64_t hv = HZ[tid * W + i];
+      HZ[tid * W + i] = (hv - 1) | ((uint64_t)((zmask >> i) & 1u) << 63);  // back to hash|strand (selected only matter)
+    }
+  }
   if (tid == 0 || tid == X2_NT - 1 || !blk_in) selmask = 0;
 
-  // ---------------------------------------------------------------- E. compaction (staged)
-  auto stage_records = [&]() -> uint32_t {
+  // ---------------------------------------------------------------- E. compaction
+  auto compact = [&]() -> uint32_t {
     const uint32_t cnt = __popc(selmask);
     uint32_t incl = cnt;
 #pragma unroll
@@ -454,49 +480,59 @@ __global__ void __launch_bounds__(X2_NT, 1) k_extract2(X2Args a) {
     __syncthreads();
     uint32_t idx = (wid ? sh.warp_cnt[wid - 1] : 0u) + incl - cnt;
     const uint32_t first = idx;
-    const Job jb = a.jobs[J];
-#pragma unroll
-    for (int i = 0; i < W; i++) {
-      if (selmask & (1u << i)) {
-        st_hz[idx] = hz[i];
-        st_pos[idx] = (uint32_t)(jb.pos_base + jb.phase + a.one0 + (uint64_t)PS * (l0 + i));
-        st_e[idx] = (uint16_t)(tid * W + i);
-        ++idx;
-      }
+    uint32_t m = selmask;
+    while (m) {
+      const int i = __ffs(m) - 1;
+      m &= m - 1;
+      sel_e[idx] = (uint16_t)(tid * W + i);
+      sel_k[idx] = (uint16_t)(HZ[tid * W + i] >> ks);
+      ++idx;
     }
+    __syncthreads();
     return first;
   };
-  uint32_t my_first = stage_records();
-  __syncthreads();
+  uint32_t my_first = compact();
   uint32_t tile_cnt = sh.warp_cnt[X2_NT / 32 - 1];
-  // exactness check of the 31-bit keys: candidates closer than w with equal keys and different hashes
-  if (!sh.any_n && !sh.slow && a.key_shift > 0) {
+  // exactness of the 31-bit keys: candidates closer than w with equal keys but different hashes
+  if (!sh.any_n && !sh.slow && ks > 0 && !(a.dbg_flags & 2u)) {
     bool tie = false;
     for (uint32_t r = tid; r < tile_cnt; r += X2_NT) {
-      const uint64_t hr = st_hz[r] & ~(1ull << 63);
-      const uint32_t kr = (uint32_t)(hr >> ks);
-      const int er = st_e[r];
+      const int er = sel_e[r];
+      const uint16_t kr = sel_k[r];
       for (uint32_t q = r + 1; q < tile_cnt; q++) {
-        if (st_e[q] - er >= W) break;
-        const uint64_t hq = st_hz[q] & ~(1ull << 63);
-        if ((uint32_t)(hq >> ks) == kr && hq != hr) tie = true;
+        const int eq = sel_e[q];
+        if (eq - er >= W) break;
+        if (sel_k[q] == kr) {
+          const uint64_t hr = HZ[er] & ~(1ull << 63), hq = HZ[eq] & ~(1ull << 63);
+          if ((hr >> ks) == (hq >> ks) && hr != hq) tie = true;
+        }
       }
     }
     if (__syncthreads_or(tie)) {
-      // recompute exactly (the H64 alias overwrites the staging area)
+      if (tid == 0 && a.dbg_counts) atomicAdd(&a.dbg_counts[1], 1u);
+#pragma unroll
+      for (int i = 0; i < W; i++) zmask |= (uint32_t)(HZ[tid * W + i] >> 63) << i;
       slow_path();
+#pragma unroll
+      for (int i = 0; i < W; i++) {
+        const uint64_t hv = HZ[tid * W + i];
+        HZ[tid * W + i] = (hv - 1) | ((uint64_t)((zmask >> i) & 1u) << 63);
+      }
       if (tid == 0 || tid == X2_NT - 1 || !blk_in) selmask = 0;
-      my_first = stage_records();
-      __syncthreads();
+      my_first = compact();
       tile_cnt = sh.warp_cnt[X2_NT / 32 - 1];
     }
   }
-  // tile offset (decoupled look-back in tile order)
-  if (tid == 0) {
-    const uint64_t base = lb_exclusive(a.status, tile, tile_cnt);
-    sh.base = base;
-    const uint64_t ntiles = (a.total_blocks + X2_OUT_BLOCKS - 1) / X2_OUT_BLOCKS;
-    if (tile == ntiles - 1) *a.total_out = base + tile_cnt;
+  // ---------------------------------------------------------------- F. tile offset + output
+  if (wid == 0) {
+    uint64_t base;
+    if (a.dbg_flags & 1u) base = lane == 0 ? atomicAdd((unsigned long long*)&a.status[0], (unsigned long long)tile_cnt) : 0;
+    else base = lb_exclusive_warp(a.status, tile, tile_cnt);
+    if (lane == 0) {
+      sh.base = base;
+      const uint64_t ntiles = (a.total_blocks + X2_OUT_BLOCKS - 1) / X2_OUT_BLOCKS;
+      if (tile == ntiles - 1) *a.total_out = base + tile_cnt;
+    }
   }
   __syncthreads();
   const uint64_t base = sh.base;
@@ -504,19 +540,13 @@ __global__ void __launch_bounds__(X2_NT, 1) k_extract2(X2Args a) {
   for (uint32_t r = tid; r < tile_cnt; r += X2_NT) {
     const uint64_t gi = base + r;
     if (gi < a.cap) {
-      a.out_hz[gi] = st_hz[r];
-      a.out_pos[gi] = st_pos[r];
-    }
-  }
-  if (a.out_job) {
-    // job of each staged record: recover from its tile position (block -> job), rare enough per record
-    for (uint32_t r = tid; r < tile_cnt; r += X2_NT) {
-      const uint64_t gi = base + r;
-      if (gi < a.cap) {
-        const int e = st_e[r];
-        const uint64_t g = ((uint64_t)tile * X2_OUT_BLOCKS - 1) * W + e;
-        a.out_job[gi] = find_job_le(a.kb, j0, j1, g);
-      }
+      const int e = sel_e[r];
+      const int b = e / W;
+      const uint32_t Jr = blk_j[b];
+      const Job& jb = a.jobs[Jr];
+      a.out_hz[gi] = HZ[e];
+      a.out_pos[gi] = (uint32_t)(jb.pos_base + jb.phase + a.one0 + (uint64_t)PS * (blk_l[b] + (uint32_t)(e - b * W)));
+      if (a.out_job) a.out_job[gi] = Jr;
     }
   }
 }
@@ -533,8 +563,7 @@ __global__ void k_x2_sizes(const Job* __restrict__ jobs, uint32_t n, int K, int 
 
 template <int K, int W, int PS>
 size_t x2_smem_bytes() {
-  using C = X2Cfg<K, W, PS>;
-  return (size_t)(256 + 2 * C::MAXWORDS + 2 * 8 * W + 2) * 4 + (size_t)C::POS * (8 + 4 + 2) + 16;
+  return X2Cfg<K, W, PS>::SMEM;
 }
 
 template <int K, int W, int PS>
@@ -584,6 +613,13 @@ bool run_extract2(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const
   uint32_t* ctr = scr.alloc<uint32_t>(1);
   uint64_t* dtotal = scr.alloc<uint64_t>(1);
   if (want_job_off) rec.job_off = scr.alloc<uint64_t>(n_jobs + 1);
+  const char* dflag = getenv("GOD_X2_DBG");
+  const uint32_t dbg_flags = dflag ? (uint32_t)atoi(dflag) : 0u;
+  uint32_t* dbg_counts = nullptr;
+  if (dflag) {
+    dbg_counts = scr.alloc<uint32_t>(2);
+    GOD_CUDA(cudaMemsetAsync(dbg_counts, 0, 8, st));
+  }
   const char* dbg = getenv("GOD_DEBUG_KEYBITS");  // test hook: coarser keys force the exact tie path
   uint32_t key_shift = 2 * K > 31 ? 2 * K - 31 : 0;
   if (dbg) {
@@ -598,7 +634,7 @@ bool run_extract2(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const
     GOD_CUDA(cudaMemsetAsync(status, 0, ntiles * sizeof(uint64_t), st));
     GOD_CUDA(cudaMemsetAsync(ctr, 0, sizeof(uint32_t), st));
     X2Args a{seq, seq_bytes, jobs, kb, cw, n_jobs, total_blocks, P.pat.one[0], key_shift, status, ctr,
-             rec.hz, rec.pos, rec.job, rec.job_off, cap, dtotal};
+             rec.hz, rec.pos, rec.job, rec.job_off, cap, dtotal, dbg_flags, dbg_counts};
     if (ntiles) {
       if (K == 21 && W == 11) {
         if (PS == 2) launch_x2<21, 11, 2>(a, ntiles, st, tag);
@@ -614,6 +650,11 @@ bool run_extract2(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const
       GOD_CUDA(cudaMemsetAsync(dtotal, 0, sizeof(uint64_t), st));
     }
     const uint64_t n = d2h_scalar(dtotal, st);
+    if (dbg_counts) {
+      uint32_t hc[2];
+      GOD_CUDA(cudaMemcpy(hc, dbg_counts, 8, cudaMemcpyDeviceToHost));
+      fprintf(stderr, "[x2] %s tiles=%llu slow=%u tie=%u\n", tag, (unsigned long long)ntiles, hc[0], hc[1]);
+    }
     if (n <= cap) {
       rec.n = n;
       if (want_job_off)
