@@ -32,10 +32,10 @@ namespace god {
 
 namespace {
 
-constexpr int X2_NT = 256;
+constexpr int X2_NT = 128;
 constexpr int X2_OUT_BLOCKS = X2_NT - 2;
 #ifndef X2_MINB
-#define X2_MINB 4
+#define X2_MINB 6
 #endif
 
 struct X2Args {
@@ -103,13 +103,9 @@ __device__ __forceinline__ uint64_t wang_hash_k(uint64_t key) {
   return key;
 }
 
-struct X2Shared {
-  uint32_t j0, j1;
+struct X2Tile {  // per-tile scalars, in SMEM
+  uint32_t tile, j0, j1, simple, any_n, slow, cnt;
   uint64_t cw_lo, cw_hi;
-  uint32_t any_n, slow, simple;
-  uint64_t base;
-  uint32_t warp_cnt[X2_NT / 32];
-  uint32_t tile;
 };
 
 template <int K, int W, int PS>
@@ -117,13 +113,17 @@ struct X2Cfg {
   static constexpr int NB = W + K - 1;                 // bases in a thread's window
   static constexpr int NWIN = (2 * NB + 31) / 32;       // aligned window words
   static constexpr int NLOAD = (30 + 2 * NB + 31) / 32; // words loaded before alignment
-  static constexpr int POS = X2_NT * W;                 // positions per tile (incl. halo blocks)
-  // code words the tile can touch: every block's window, plus one partial word per job (<= 256 jobs)
+  static constexpr int POS = X2_NT * W;                 // positions per tile (incl. the two halo blocks)
   static constexpr int MAXWORDS = (POS + X2_NT * (K - 1) + 15) / 16 + X2_NT + 8;
-  static constexpr size_t SMEM = (size_t)(256 + 2 * MAXWORDS + 2 * 8 * W + 2) * 4  // lut, codes, nmask, xchg
-                                 + (size_t)POS * 8                                   // HZ (or H64 on the slow path)
-                                 + (size_t)POS * 4                                   // selected list + keys
-                                 + (size_t)X2_NT * 8 + 16;                           // per-block (job, l0)
+  // SMEM layout (bytes)
+  static constexpr size_t O_LUT = 0;
+  static constexpr size_t O_CODES = O_LUT + 256 * 4;
+  static constexpr size_t O_NMASK = O_CODES + (size_t)MAXWORDS * 4;
+  static constexpr size_t O_XCHG = O_NMASK + (size_t)MAXWORDS * 4;
+  static constexpr size_t O_HZ = (O_XCHG + 2 * (X2_NT / 32) * W * 4 + 15) / 16 * 16;  // [2][POS] hz
+  static constexpr size_t O_SE = O_HZ + 2 * (size_t)POS * 8;      // [2][POS] selected: e | key16 << 16
+  static constexpr size_t O_BI = O_SE + 2 * (size_t)POS * 4;      // block info [2][4][NT]
+  static constexpr size_t SMEM = (O_BI + 2 * 4 * X2_NT * 4 + 15) / 16 * 16;
 };
 
 // 16 patterned bases (MSB-first 2-bit codes) from the ASCII bytes at A (a PS-strided gather);
@@ -181,374 +181,412 @@ __device__ __forceinline__ uint32_t pack16(const uint8_t* seq, uint64_t seq_byte
   return word;
 }
 
+// deferred decoupled look-back: publish the aggregate as soon as it is known ...
+__device__ __forceinline__ void lb_publish(uint64_t* status, uint64_t tile, uint64_t local) {
+  lb_store(&status[tile], (tile == 0 ? LB_INC : LB_AGG) | local);
+}
+// ... and resolve the exclusive prefix later (whole warp), publishing the inclusive prefix
+__device__ inline uint64_t lb_resolve_warp(uint64_t* status, uint64_t tile, uint64_t local) {
+  const int lane = threadIdx.x & 31;
+  if (tile == 0) return 0;
+  uint64_t excl = 0;
+  int64_t j = (int64_t)tile - 1 - lane;
+  while (true) {
+    uint64_t s = j >= 0 ? lb_load(&status[j]) : (LB_INC | 0ull);
+    while (__any_sync(0xffffffffu, (s & ~LB_VAL) == 0)) {
+      if ((s & ~LB_VAL) == 0) s = lb_load(&status[j]);
+    }
+    const uint32_t inc = __ballot_sync(0xffffffffu, (s & ~LB_VAL) == LB_INC);
+    const int first = inc ? __ffs(inc) - 1 : 32;
+    uint64_t v = lane <= first ? (s & LB_VAL) : 0ull;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    excl += v;
+    if (inc) break;
+    j -= 32;
+  }
+  if (lane == 0) lb_store(&status[tile], LB_INC | (excl + local));
+  return excl;
+}
+
 // ---------------------------------------------------------------------------------------------
+// Persistent CTAs: each grabs tiles in order (atomic counter), computes a tile, publishes its
+// record count, and only then resolves the PREVIOUS tile's output offset and writes its records,
+// so the look-back never stalls the CTA on a tile that other CTAs are still computing.
 template <int K, int W, int PS>
 __global__ void __launch_bounds__(X2_NT, X2_MINB) k_extract2(X2Args a) {
   using C = X2Cfg<K, W, PS>;
   constexpr int NB = C::NB, NWIN = C::NWIN, NLOAD = C::NLOAD, POS = C::POS;
+  constexpr int NWARP = X2_NT / 32;
   extern __shared__ __align__(16) unsigned char x2_smem[];
-  uint32_t* lut = reinterpret_cast<uint32_t*>(x2_smem);
-  uint32_t* codes = lut + 256;
-  uint32_t* nmask = codes + C::MAXWORDS;
-  uint32_t* xchg = nmask + C::MAXWORDS;                                  // [2][8][W]
-  uint64_t* HZ = reinterpret_cast<uint64_t*>(xchg + 2 * 8 * W + 2);       // [POS] hash | strand<<63 (slow: H64)
-  uint16_t* sel_e = reinterpret_cast<uint16_t*>(HZ + POS);               // [POS] selected tile positions
-  uint16_t* sel_k = sel_e + POS;                                         // [POS] low 16 key bits (tie check)
-  uint32_t* blk_j = reinterpret_cast<uint32_t*>(sel_k + POS);             // [256] job of each block
-  uint32_t* blk_l = blk_j + X2_NT;                                       // [256] first k-mer index of each block
-  __shared__ X2Shared sh;
+  uint32_t* lut = reinterpret_cast<uint32_t*>(x2_smem + C::O_LUT);
+  uint32_t* codes = reinterpret_cast<uint32_t*>(x2_smem + C::O_CODES);
+  uint32_t* nmask = reinterpret_cast<uint32_t*>(x2_smem + C::O_NMASK);
+  uint32_t* xpf = reinterpret_cast<uint32_t*>(x2_smem + C::O_XCHG);
+  uint32_t* xsf = xpf + NWARP * W;
+  uint64_t* HZ2 = reinterpret_cast<uint64_t*>(x2_smem + C::O_HZ);    // [2][POS]
+  uint32_t* SE = reinterpret_cast<uint32_t*>(x2_smem + C::O_SE);     // [2][POS]
+  uint32_t* BI = reinterpret_cast<uint32_t*>(x2_smem + C::O_BI);     // [2][4][NT]: job, pos base, first, start
+  __shared__ X2Tile T;
+  __shared__ uint32_t warp_cnt[NWARP];
+  __shared__ uint64_t s_base;
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  if (tid == 0) {
-    const uint32_t t = atomicAdd(a.tile_ctr, 1u);
-    sh.tile = t;
-    const int64_t b_first = (int64_t)t * X2_OUT_BLOCKS - 1;
-    const int64_t b_last = (int64_t)t * X2_OUT_BLOCKS + X2_NT - 2;
-    const uint64_t gmax = a.total_blocks * W - 1;
-    const uint64_t gfirst = b_first < 0 ? 0 : (uint64_t)b_first * W;
-    uint64_t glast = (uint64_t)(b_last < 0 ? 0 : b_last) * W;
-    if (glast > gmax) glast = gmax;
-    const uint32_t j0 = find_job_le(a.kb, 0, a.n_jobs - 1, gfirst);
-    const uint32_t j1 = find_job_le(a.kb, j0, a.n_jobs - 1, glast);
-    sh.j0 = j0; sh.j1 = j1;
-    const uint64_t lo = b_first < 0 ? a.cw[0] : a.cw[j0] + (gfirst - a.kb[j0]) / 16;
-    uint64_t hi = a.cw[j1] + (glast - a.kb[j1] + NB + 15) / 16 + 1;
-    if (hi > a.cw[j1 + 1]) hi = a.cw[j1 + 1];
-    if (hi < lo) hi = lo;
-    if (hi > lo + C::MAXWORDS) hi = lo + C::MAXWORDS;  // cannot happen for 256 blocks; guard
-    sh.cw_lo = lo; sh.cw_hi = hi;
-    // "simple" tile: one job and every byte of its words inside the buffer -> no per-word checks
-    const Job jb = a.jobs[j0];
-    const uint64_t last_byte = jb.seq_off + jb.phase + a.one0 + (uint64_t)PS * 16 * (hi - a.cw[j0]) + 4 * PS + 8;
-    sh.simple = (j0 == j1) && last_byte <= a.seq_bytes;
-    sh.any_n = 0; sh.slow = 0;
-  }
+  const uint64_t ntiles = (a.total_blocks + X2_OUT_BLOCKS - 1) / X2_OUT_BLOCKS;
   {  // expected-letter table: for 4 MSB-first codes pk, bytes "ACGT"[c_i], base 0 in byte 0
     const uint32_t L4 = 0x54474341u;
-    uint32_t e = 0;
+    for (int pk = tid; pk < 256; pk += X2_NT) {
+      uint32_t e = 0;
 #pragma unroll
-    for (int i = 0; i < 4; i++) e |= ((L4 >> (8 * ((tid >> (6 - 2 * i)) & 3u))) & 0xFFu) << (8 * i);
-    lut[tid] = e;
-  }
-  __syncthreads();
-  const uint32_t tile = sh.tile;
-  const uint32_t j0 = sh.j0, j1 = sh.j1;
-  const uint64_t cw_lo = sh.cw_lo;
-  const int nwords = (int)(sh.cw_hi - cw_lo);
-
-  // ---- my block: job J, first k-mer index l0 (32-bit: nk < 2^32)
-  const int64_t myb = (int64_t)tile * X2_OUT_BLOCKS - 1 + tid;
-  const bool blk_in = myb >= 0 && (uint64_t)myb < a.total_blocks;
-  uint32_t J = j0, l0 = 0, nk = 0;
-  if (blk_in) {
-    const uint64_t g = (uint64_t)myb * W;
-    J = (j0 == j1) ? j0 : find_job_le(a.kb, j0, j1, g);
-    l0 = (uint32_t)(g - a.kb[J]);
-    nk = a.jobs[J].nk;
-  }
-  blk_j[tid] = J;
-  blk_l[tid] = l0;
-
-  // ---------------------------------------------------------------- A. sparsify into SMEM
-  {
-    uint32_t my_n = 0;
-    if (sh.simple) {
-      const Job jb = a.jobs[j0];
-      const uint64_t w0 = cw_lo - a.cw[j0];  // first word of the tile inside the job
-      const uint32_t ncode = jb.nk ? jb.nk + K - 1 : 0;
-      const uint64_t A0 = jb.seq_off + jb.phase + a.one0;
-      for (int wi = tid; wi < nwords; wi += X2_NT) {
-        const uint64_t q0 = (w0 + wi) * 16;
-        uint32_t nm = 0, word = 0;
-        if (q0 < ncode) {
-          const int nb = (int)min((uint64_t)16, ncode - q0);
-          word = pack16<PS, false>(a.seq, a.seq_bytes, A0 + (uint64_t)PS * q0, nb, lut, &nm);
-        }
-        codes[wi] = word;
-        nmask[wi] = nm;
-        my_n |= nm;
-      }
-    } else {
-      uint32_t Jw = j0;
-      for (int wi = tid; wi < nwords; wi += X2_NT) {
-        const uint64_t gw = cw_lo + wi;
-        Jw = find_job_le(a.cw, Jw, j1, gw);
-        const Job jb = a.jobs[Jw];
-        const uint64_t ncode = jb.nk ? (uint64_t)jb.nk + K - 1 : 0;
-        const uint64_t q0 = (gw - a.cw[Jw]) * 16;
-        uint32_t nm = 0, word = 0;
-        if (q0 < ncode) {
-          const int nb = (int)min((uint64_t)16, ncode - q0);
-          word = pack16<PS, true>(a.seq, a.seq_bytes, jb.seq_off + jb.phase + a.one0 + (uint64_t)PS * q0, nb,
-                                  lut, &nm);
-        }
-        codes[wi] = word;
-        nmask[wi] = nm;
-        my_n |= nm;
-      }
+      for (int i = 0; i < 4; i++) e |= ((L4 >> (8 * ((pk >> (6 - 2 * i)) & 3u))) & 0xFFu) << (8 * i);
+      lut[pk] = e;
     }
-    if (__syncthreads_or(my_n != 0) && tid == 0) sh.any_n = 1;
   }
-  __syncthreads();
-
-  // ---------------------------------------------------------------- B. k-mers and hashes
-  const bool blk_has_kmers = blk_in && l0 < nk;
-  uint32_t win[NWIN];
-  {
-    const int wbase = (int)(a.cw[J] + l0 / 16 - cw_lo);
-    const uint32_t off = (l0 % 16) * 2;
-    uint32_t raw[NLOAD + 1];
-#pragma unroll
-    for (int i = 0; i <= NLOAD; i++) {
-      const int idx = wbase + i;
-      raw[i] = (blk_has_kmers && idx < C::MAXWORDS) ? codes[idx] : 0u;
-    }
-#pragma unroll
-    for (int i = 0; i < NWIN; i++) win[i] = __funnelshift_l(raw[i + 1], raw[i], off);
-  }
-  uint32_t rcw[NWIN];
-#pragma unroll
-  for (int i = 0; i < NWIN; i++) rcw[i] = ~rev2(win[NWIN - 1 - i]);
-  constexpr int PADB = 32 * NWIN - 2 * NB;
-
   const uint32_t ks = a.key_shift;
-  uint32_t key[W];
-  uint32_t palmask = 0;
-  const uint32_t nvalid = blk_has_kmers ? min((uint32_t)W, nk - l0) : 0u;  // k-mer starts in this block
-#pragma unroll
-  for (int i = 0; i < W; i++) {
-    const uint64_t fwd = ext_bits(win, 2 * i, 2 * K);
-    const uint64_t rev = ext_bits(rcw, PADB + 2 * (NB - i - K), 2 * K);
-    const bool z = fwd > rev;
-    const uint64_t h = wang_hash_k<K>(z ? rev : fwd);
-    HZ[tid * W + i] = h | ((uint64_t)z << 63);
-    uint32_t kk = (uint32_t)(h >> ks) + 1u;
-    if constexpr ((K & 1) == 0) {
-      if (fwd == rev) { kk = 0xFFFFFFFFu; palmask |= 1u << i; }
-    }
-    key[i] = (uint32_t)i < nvalid ? kk : 0u;
-  }
+  int64_t pend_tile = -1;
+  uint32_t pend_cnt = 0;
+  int buf = 0;
 
-  // ---------------------------------------------------------------- C. selection on keys
-  uint32_t selmask = 0;
-  if (!sh.any_n) {
-    bool need_slow = false;
-    uint32_t PF[W], SF[W];
-    PF[0] = key[0];
-#pragma unroll
-    for (int i = 1; i < W; i++) PF[i] = min(PF[i - 1], key[i]);
-    SF[W - 1] = key[W - 1];
-#pragma unroll
-    for (int i = W - 2; i >= 0; i--) SF[i] = min(SF[i + 1], key[i]);
-    uint32_t* xpf = xchg;
-    uint32_t* xsf = xchg + 8 * W;
-    if (lane == 0) {
-#pragma unroll
-      for (int i = 0; i < W; i++) xpf[wid * W + i] = PF[i];
-    }
-    __syncthreads();
-    uint32_t nPF[W];
-#pragma unroll
-    for (int i = 0; i < W; i++) nPF[i] = __shfl_down_sync(0xffffffffu, PF[i], 1);
-    if (lane == 31) {
-#pragma unroll
-      for (int i = 0; i < W; i++) nPF[i] = (wid < 7) ? xpf[(wid + 1) * W + i] : 0u;
-    }
-    uint32_t WM[W];
-    WM[0] = SF[0];
-#pragma unroll
-    for (int i = 1; i < W; i++) WM[i] = min(SF[i], nPF[i - 1]);
-    uint32_t PX[W], SX[W];
-    PX[0] = WM[0];
-#pragma unroll
-    for (int i = 1; i < W; i++) PX[i] = max(PX[i - 1], WM[i]);
-    SX[W - 1] = WM[W - 1];
-#pragma unroll
-    for (int i = W - 2; i >= 0; i--) SX[i] = max(SX[i + 1], WM[i]);
-    if (lane == 31) {
-#pragma unroll
-      for (int i = 0; i < W; i++) xsf[wid * W + i] = SX[i];
-    }
-    __syncthreads();
-    uint32_t pSX[W];
-#pragma unroll
-    for (int i = 0; i < W; i++) pSX[i] = __shfl_up_sync(0xffffffffu, SX[i], 1);
-    if (lane == 0) {
-#pragma unroll
-      for (int i = 0; i < W; i++) pSX[i] = (wid > 0) ? xsf[(wid - 1) * W + i] : 0u;
-    }
-#pragma unroll
-    for (int o = 0; o < W; o++) {
-      const uint32_t mm = (o == W - 1) ? PX[W - 1] : max(pSX[o + 1], PX[o]);
-      const uint32_t k = key[o];
-      bool s = (k == mm) && k != 0u;
-      if constexpr ((K & 1) == 0) s = s && k != 0xFFFFFFFFu;
-      need_slow |= (k != 0u) & (mm == 0u);  // a run shorter than w: partial-window rule
-      if (s) selmask |= 1u << o;
-    }
-    if (tid == 0 || tid == X2_NT - 1) need_slow = false;  // halo blocks are not emitted
-    if (__syncthreads_or(need_slow) && tid == 0) sh.slow = 1;
-  }
-  __syncthreads();
-
-  // ---------------------------------------------------------------- D. exact slow path (whole tile)
-  auto slow_path = [&]() {
-    uint64_t* H64 = HZ;  // hash+1, 0 barrier, ~0 palindrome; HZ is rebuilt afterwards
-#pragma unroll
-    for (int i = 0; i < W; i++) {
-      uint64_t hv = 0;
-      if ((uint32_t)i < nvalid) {
-        const uint32_t q = l0 + i;
-        const int wb = (int)(a.cw[J] + q / 16 - cw_lo);
-        const uint32_t o = q % 16;
-        bool anyn = false;
-        for (int b = 0; b < K; b++) {
-          const int wi2 = wb + (int)((o + b) / 16);
-          if (wi2 < C::MAXWORDS && ((nmask[wi2] >> (15 - ((o + b) % 16))) & 1u)) anyn = true;
-        }
-        if (!anyn) hv = ((palmask >> i) & 1u) ? ~0ull : (HZ[tid * W + i] & ~(1ull << 63)) + 1;
-      }
-      H64[tid * W + i] = hv;
-    }
-    __syncthreads();
-    uint32_t m = 0;
-    if (tid > 0 && tid < X2_NT - 1) {
-      for (int i = 0; i < W; i++) {
-        const int j = tid * W + i;
-        const uint64_t hj = H64[j];
-        if (hj == 0 || hj == ~0ull) continue;
-        int lo = j, hi = j;
-        while (lo > j - (W - 1) && H64[lo - 1] != 0) --lo;
-        while (hi < j + (W - 1) && H64[hi + 1] != 0) ++hi;
-        bool s = false;
-        if (hi - lo + 1 < W) {  // the whole run is one partial window
-          uint64_t mn = ~0ull;
-          for (int q = lo; q <= hi; q++)
-            if (H64[q] != ~0ull) mn = min(mn, H64[q]);
-          s = (hj == mn);
-        } else {
-          const int a0 = max(lo, j - (W - 1)), a1 = min(j, hi - (W - 1));
-          for (int st = a0; st <= a1 && !s; st++) {
-            uint64_t mn = ~0ull;
-            for (int q = st; q < st + W; q++)
-              if (H64[q] != ~0ull) mn = min(mn, H64[q]);
-            s = (hj == mn);
-          }
-        }
-        if (s) m |= 1u << i;
-      }
-    }
-    __syncthreads();
-    selmask = m;
-  };
-
-  // the slow path overwrites HZ with H64; keep the strand bits in a register mask to rebuild it
-  uint32_t zmask = 0;
-  if (sh.any_n || sh.slow) {
-    if (tid == 0 && a.dbg_counts) atomicAdd(&a.dbg_counts[0], 1u);
-#pragma unroll
-    for (int i = 0; i < W; i++) zmask |= (uint32_t)(HZ[tid * W + i] >> 63) << i;
-    slow_path();
-#pragma unroll
-    for (int i = 0; i < W; i++) {
-      const uint64_t hv = HZ[tid * W + i];
-      HZ[tid * W + i] = (hv - 1) | ((uint64_t)((zmask >> i) & 1u) << 63);  // back to hash|strand (selected only matter)
-    }
-  }
-  if (tid == 0 || tid == X2_NT - 1 || !blk_in) selmask = 0;
-
-  // ---------------------------------------------------------------- E. compaction
-  auto compact = [&]() -> uint32_t {
-    const uint32_t cnt = __popc(selmask);
-    uint32_t incl = cnt;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
-      if (lane >= d) incl += y;
-    }
-    if (lane == 31) sh.warp_cnt[wid] = incl;
-    __syncthreads();
+  // write the staged records of a finished tile (whole CTA); warp 0 resolves its offset first
+  auto flush = [&](uint64_t tile, uint32_t cnt, int b) {
     if (wid == 0) {
-      uint32_t ws = lane < X2_NT / 32 ? sh.warp_cnt[lane] : 0u;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, ws, d);
-        if (lane >= d) ws += y;
+      uint64_t base;
+      if (a.dbg_flags & 1u) base = lane == 0 ? atomicAdd((unsigned long long*)&a.status[ntiles], (unsigned long long)cnt) : 0;
+      else base = lb_resolve_warp(a.status, tile, cnt);
+      if (lane == 0) {
+        s_base = base;
+        if (tile == ntiles - 1) *a.total_out = base + cnt;
       }
-      if (lane < X2_NT / 32) sh.warp_cnt[lane] = ws;
     }
     __syncthreads();
-    uint32_t idx = (wid ? sh.warp_cnt[wid - 1] : 0u) + incl - cnt;
-    const uint32_t first = idx;
-    uint32_t m = selmask;
-    while (m) {
-      const int i = __ffs(m) - 1;
-      m &= m - 1;
-      sel_e[idx] = (uint16_t)(tid * W + i);
-      sel_k[idx] = (uint16_t)(HZ[tid * W + i] >> ks);
-      ++idx;
+    const uint64_t base = s_base;
+    const uint64_t* hzb = HZ2 + (size_t)b * POS;
+    const uint32_t* se = SE + (size_t)b * POS;
+    const uint32_t* bj = BI + (size_t)b * 4 * X2_NT;
+    const uint32_t* bpb = bj + X2_NT;
+    const uint32_t* bfirst = bpb + X2_NT;
+    const uint32_t* bstart = bfirst + X2_NT;
+    if (a.job_off && bstart[tid]) a.job_off[bj[tid]] = base + bfirst[tid];
+    for (uint32_t r = tid; r < cnt; r += X2_NT) {
+      const uint64_t gi = base + r;
+      if (gi < a.cap) {
+        const int e = se[r] & 0xFFFFu;
+        const int blk = e / W;
+        a.out_hz[gi] = hzb[e];
+        a.out_pos[gi] = bpb[blk] + (uint32_t)PS * (uint32_t)(e - blk * W);
+        if (a.out_job) a.out_job[gi] = bj[blk];
+      }
     }
-    __syncthreads();
-    return first;
   };
-  uint32_t my_first = compact();
-  uint32_t tile_cnt = sh.warp_cnt[X2_NT / 32 - 1];
-  // exactness of the 31-bit keys: candidates closer than w with equal keys but different hashes
-  if (!sh.any_n && !sh.slow && ks > 0 && !(a.dbg_flags & 2u)) {
-    bool tie = false;
-    for (uint32_t r = tid; r < tile_cnt; r += X2_NT) {
-      const int er = sel_e[r];
-      const uint16_t kr = sel_k[r];
-      for (uint32_t q = r + 1; q < tile_cnt; q++) {
-        const int eq = sel_e[q];
-        if (eq - er >= W) break;
-        if (sel_k[q] == kr) {
-          const uint64_t hr = HZ[er] & ~(1ull << 63), hq = HZ[eq] & ~(1ull << 63);
-          if ((hr >> ks) == (hq >> ks) && hr != hq) tie = true;
+
+  while (true) {
+    if (tid == 0) {
+      const uint32_t t = atomicAdd(a.tile_ctr, 1u);
+      T.tile = t;
+      if (t < ntiles) {
+        const int64_t b_first = (int64_t)t * X2_OUT_BLOCKS - 1;
+        const int64_t b_last = (int64_t)t * X2_OUT_BLOCKS + X2_NT - 2;
+        const uint64_t gmax = a.total_blocks * W - 1;
+        const uint64_t gfirst = b_first < 0 ? 0 : (uint64_t)b_first * W;
+        uint64_t glast = (uint64_t)(b_last < 0 ? 0 : b_last) * W;
+        if (glast > gmax) glast = gmax;
+        const uint32_t j0 = find_job_le(a.kb, 0, a.n_jobs - 1, gfirst);
+        const uint32_t j1 = find_job_le(a.kb, j0, a.n_jobs - 1, glast);
+        T.j0 = j0; T.j1 = j1;
+        const uint64_t lo = b_first < 0 ? a.cw[0] : a.cw[j0] + (gfirst - a.kb[j0]) / 16;
+        uint64_t hi = a.cw[j1] + (glast - a.kb[j1] + NB + 15) / 16 + 1;
+        if (hi > a.cw[j1 + 1]) hi = a.cw[j1 + 1];
+        if (hi < lo) hi = lo;
+        if (hi > lo + C::MAXWORDS) hi = lo + C::MAXWORDS;
+        T.cw_lo = lo; T.cw_hi = hi;
+        const Job jb = a.jobs[j0];
+        const uint64_t last_byte = jb.seq_off + jb.phase + a.one0 + (uint64_t)PS * 16 * (hi - a.cw[j0]) + 4 * PS + 8;
+        T.simple = (j0 == j1) && last_byte <= a.seq_bytes;
+        T.any_n = 0; T.slow = 0;
+      }
+    }
+    __syncthreads();
+    const uint32_t tile = T.tile;
+    if (tile >= ntiles) break;
+    uint64_t* HZ = HZ2 + (size_t)buf * POS;
+    const uint32_t j0 = T.j0, j1 = T.j1;
+    const uint64_t cw_lo = T.cw_lo;
+    const int nwords = (int)(T.cw_hi - cw_lo);
+
+    // ---- my block: job J, first k-mer index l0
+    const int64_t myb = (int64_t)tile * X2_OUT_BLOCKS - 1 + tid;
+    const bool blk_in = myb >= 0 && (uint64_t)myb < a.total_blocks;
+    uint32_t J = j0, l0 = 0, nk = 0;
+    if (blk_in) {
+      const uint64_t g = (uint64_t)myb * W;
+      J = (j0 == j1) ? j0 : find_job_le(a.kb, j0, j1, g);
+      l0 = (uint32_t)(g - a.kb[J]);
+      nk = a.jobs[J].nk;
+    }
+
+    // ------------------------------------------------------------ A. sparsify into SMEM
+    {
+      uint32_t my_n = 0;
+      if (T.simple) {
+        const Job jb = a.jobs[j0];
+        const uint64_t w0 = cw_lo - a.cw[j0];
+        const uint32_t ncode = jb.nk ? jb.nk + K - 1 : 0;
+        const uint64_t A0 = jb.seq_off + jb.phase + a.one0;
+        for (int wi = tid; wi < nwords; wi += X2_NT) {
+          const uint64_t q0 = (w0 + wi) * 16;
+          uint32_t nm = 0, word = 0;
+          if (q0 < ncode) word = pack16<PS, false>(a.seq, a.seq_bytes, A0 + (uint64_t)PS * q0,
+                                                   (int)min((uint64_t)16, ncode - q0), lut, &nm);
+          codes[wi] = word;
+          nmask[wi] = nm;
+          my_n |= nm;
+        }
+      } else {
+        uint32_t Jw = j0;
+        for (int wi = tid; wi < nwords; wi += X2_NT) {
+          const uint64_t gw = cw_lo + wi;
+          Jw = find_job_le(a.cw, Jw, j1, gw);
+          const Job jb = a.jobs[Jw];
+          const uint64_t ncode = jb.nk ? (uint64_t)jb.nk + K - 1 : 0;
+          const uint64_t q0 = (gw - a.cw[Jw]) * 16;
+          uint32_t nm = 0, word = 0;
+          if (q0 < ncode)
+            word = pack16<PS, true>(a.seq, a.seq_bytes, jb.seq_off + jb.phase + a.one0 + (uint64_t)PS * q0,
+                                    (int)min((uint64_t)16, ncode - q0), lut, &nm);
+          codes[wi] = word;
+          nmask[wi] = nm;
+          my_n |= nm;
         }
       }
+      if (__syncthreads_or(my_n != 0) && tid == 0) T.any_n = 1;
     }
-    if (__syncthreads_or(tie)) {
-      if (tid == 0 && a.dbg_counts) atomicAdd(&a.dbg_counts[1], 1u);
+    __syncthreads();
+
+    // ------------------------------------------------------------ B. k-mers and hashes
+    const bool blk_has_kmers = blk_in && l0 < nk;
+    uint32_t win[NWIN];
+    {
+      const int wbase = (int)(a.cw[J] + l0 / 16 - cw_lo);
+      const uint32_t off = (l0 % 16) * 2;
+      uint32_t raw[NLOAD + 1];
+#pragma unroll
+      for (int i = 0; i <= NLOAD; i++) {
+        const int idx = wbase + i;
+        raw[i] = (blk_has_kmers && idx < C::MAXWORDS) ? codes[idx] : 0u;
+      }
+#pragma unroll
+      for (int i = 0; i < NWIN; i++) win[i] = __funnelshift_l(raw[i + 1], raw[i], off);
+    }
+    uint32_t rcw[NWIN];
+#pragma unroll
+    for (int i = 0; i < NWIN; i++) rcw[i] = ~rev2(win[NWIN - 1 - i]);
+    constexpr int PADB = 32 * NWIN - 2 * NB;
+    uint32_t key[W];
+    uint32_t palmask = 0;
+    const uint32_t nvalid = blk_has_kmers ? min((uint32_t)W, nk - l0) : 0u;
+#pragma unroll
+    for (int i = 0; i < W; i++) {
+      const uint64_t fwd = ext_bits(win, 2 * i, 2 * K);
+      const uint64_t rev = ext_bits(rcw, PADB + 2 * (NB - i - K), 2 * K);
+      const bool z = fwd > rev;
+      const uint64_t h = wang_hash_k<K>(z ? rev : fwd);
+      HZ[tid * W + i] = h | ((uint64_t)z << 63);
+      uint32_t kk = (uint32_t)(h >> ks) + 1u;
+      if constexpr ((K & 1) == 0) {
+        if (fwd == rev) { kk = 0xFFFFFFFFu; palmask |= 1u << i; }
+      }
+      key[i] = (uint32_t)i < nvalid ? kk : 0u;
+    }
+
+    // ------------------------------------------------------------ C. selection on keys
+    uint32_t selmask = 0;
+    if (!T.any_n) {
+      bool need_slow = false;
+      uint32_t PF[W], SF[W];
+      PF[0] = key[0];
+#pragma unroll
+      for (int i = 1; i < W; i++) PF[i] = min(PF[i - 1], key[i]);
+      SF[W - 1] = key[W - 1];
+#pragma unroll
+      for (int i = W - 2; i >= 0; i--) SF[i] = min(SF[i + 1], key[i]);
+      if (lane == 0) {
+#pragma unroll
+        for (int i = 0; i < W; i++) xpf[wid * W + i] = PF[i];
+      }
+      __syncthreads();
+      uint32_t nPF[W];
+#pragma unroll
+      for (int i = 0; i < W; i++) nPF[i] = __shfl_down_sync(0xffffffffu, PF[i], 1);
+      if (lane == 31) {
+#pragma unroll
+        for (int i = 0; i < W; i++) nPF[i] = (wid < NWARP - 1) ? xpf[(wid + 1) * W + i] : 0u;
+      }
+      uint32_t WM[W];
+      WM[0] = SF[0];
+#pragma unroll
+      for (int i = 1; i < W; i++) WM[i] = min(SF[i], nPF[i - 1]);
+      uint32_t PX[W], SX[W];
+      PX[0] = WM[0];
+#pragma unroll
+      for (int i = 1; i < W; i++) PX[i] = max(PX[i - 1], WM[i]);
+      SX[W - 1] = WM[W - 1];
+#pragma unroll
+      for (int i = W - 2; i >= 0; i--) SX[i] = max(SX[i + 1], WM[i]);
+      if (lane == 31) {
+#pragma unroll
+        for (int i = 0; i < W; i++) xsf[wid * W + i] = SX[i];
+      }
+      __syncthreads();
+      uint32_t pSX[W];
+#pragma unroll
+      for (int i = 0; i < W; i++) pSX[i] = __shfl_up_sync(0xffffffffu, SX[i], 1);
+      if (lane == 0) {
+#pragma unroll
+        for (int i = 0; i < W; i++) pSX[i] = (wid > 0) ? xsf[(wid - 1) * W + i] : 0u;
+      }
+#pragma unroll
+      for (int o = 0; o < W; o++) {
+        const uint32_t mm = (o == W - 1) ? PX[W - 1] : max(pSX[o + 1], PX[o]);
+        const uint32_t k = key[o];
+        bool s = (k == mm) && k != 0u;
+        if constexpr ((K & 1) == 0) s = s && k != 0xFFFFFFFFu;
+        need_slow |= (k != 0u) & (mm == 0u);  // a run shorter than w: partial-window rule
+        if (s) selmask |= 1u << o;
+      }
+      if (tid == 0 || tid == X2_NT - 1) need_slow = false;  // halo blocks are not emitted
+      if (__syncthreads_or(need_slow) && tid == 0) T.slow = 1;
+    }
+    __syncthreads();
+
+    // ------------------------------------------------------------ D. exact slow path (whole tile)
+    auto slow_path = [&]() {
+      uint32_t zmask = 0;
 #pragma unroll
       for (int i = 0; i < W; i++) zmask |= (uint32_t)(HZ[tid * W + i] >> 63) << i;
-      slow_path();
+      uint64_t* H64 = HZ;  // hash+1, 0 barrier, ~0 palindrome
 #pragma unroll
       for (int i = 0; i < W; i++) {
-        const uint64_t hv = HZ[tid * W + i];
-        HZ[tid * W + i] = (hv - 1) | ((uint64_t)((zmask >> i) & 1u) << 63);
+        uint64_t hv = 0;
+        if ((uint32_t)i < nvalid) {
+          const uint32_t q = l0 + i;
+          const int wb = (int)(a.cw[J] + q / 16 - cw_lo);
+          const uint32_t o = q % 16;
+          bool anyn = false;
+          for (int bb = 0; bb < K; bb++) {
+            const int wi2 = wb + (int)((o + bb) / 16);
+            if (wi2 < C::MAXWORDS && ((nmask[wi2] >> (15 - ((o + bb) % 16))) & 1u)) anyn = true;
+          }
+          if (!anyn) hv = ((palmask >> i) & 1u) ? ~0ull : (HZ[tid * W + i] & ~(1ull << 63)) + 1;
+        }
+        H64[tid * W + i] = hv;
       }
-      if (tid == 0 || tid == X2_NT - 1 || !blk_in) selmask = 0;
-      my_first = compact();
-      tile_cnt = sh.warp_cnt[X2_NT / 32 - 1];
+      __syncthreads();
+      uint32_t m = 0;
+      if (tid > 0 && tid < X2_NT - 1) {
+        for (int i = 0; i < W; i++) {
+          const int j = tid * W + i;
+          const uint64_t hj = H64[j];
+          if (hj == 0 || hj == ~0ull) continue;
+          int lo = j, hi = j;
+          while (lo > j - (W - 1) && H64[lo - 1] != 0) --lo;
+          while (hi < j + (W - 1) && H64[hi + 1] != 0) ++hi;
+          bool s = false;
+          if (hi - lo + 1 < W) {
+            uint64_t mn = ~0ull;
+            for (int q = lo; q <= hi; q++)
+              if (H64[q] != ~0ull) mn = min(mn, H64[q]);
+            s = (hj == mn);
+          } else {
+            const int a0 = max(lo, j - (W - 1)), a1 = min(j, hi - (W - 1));
+            for (int st = a0; st <= a1 && !s; st++) {
+              uint64_t mn = ~0ull;
+              for (int q = st; q < st + W; q++)
+                if (H64[q] != ~0ull) mn = min(mn, H64[q]);
+              s = (hj == mn);
+            }
+          }
+          if (s) m |= 1u << i;
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < W; i++)  // back to hash | strand (only selected entries matter)
+        HZ[tid * W + i] = (H64[tid * W + i] - 1) | ((uint64_t)((zmask >> i) & 1u) << 63);
+      selmask = m;
+    };
+    if (T.any_n || T.slow) {
+      if (tid == 0 && a.dbg_counts) atomicAdd(&a.dbg_counts[0], 1u);
+      slow_path();
     }
-  }
-  // ---------------------------------------------------------------- F. tile offset + output
-  if (wid == 0) {
-    uint64_t base;
-    if (a.dbg_flags & 1u) base = lane == 0 ? atomicAdd((unsigned long long*)&a.status[0], (unsigned long long)tile_cnt) : 0;
-    else base = lb_exclusive_warp(a.status, tile, tile_cnt);
-    if (lane == 0) {
-      sh.base = base;
-      const uint64_t ntiles = (a.total_blocks + X2_OUT_BLOCKS - 1) / X2_OUT_BLOCKS;
-      if (tile == ntiles - 1) *a.total_out = base + tile_cnt;
+    if (tid == 0 || tid == X2_NT - 1 || !blk_in) selmask = 0;
+
+    // ------------------------------------------------------------ E. compaction into staging[buf]
+    uint32_t* se = SE + (size_t)buf * POS;
+    uint32_t* bi = BI + (size_t)buf * 4 * X2_NT;
+    auto compact = [&]() -> uint32_t {
+      const uint32_t cnt = __popc(selmask);
+      uint32_t incl = cnt;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += y;
+      }
+      if (lane == 31) warp_cnt[wid] = incl;
+      __syncthreads();
+      uint32_t before = 0, total = 0;
+#pragma unroll
+      for (int q = 0; q < NWARP; q++) {
+        const uint32_t c = warp_cnt[q];
+        before += q < wid ? c : 0u;
+        total += c;
+      }
+      uint32_t idx = before + incl - cnt;
+      bi[tid] = J;
+      bi[X2_NT + tid] = (uint32_t)(a.jobs[J].pos_base + a.jobs[J].phase + a.one0) + (uint32_t)PS * l0;
+      bi[2 * X2_NT + tid] = idx;
+      bi[3 * X2_NT + tid] = (blk_in && tid > 0 && tid < X2_NT - 1 && l0 == 0) ? 1u : 0u;
+      uint32_t m = selmask;
+      while (m) {
+        const int i = __ffs(m) - 1;
+        m &= m - 1;
+        se[idx] = (uint32_t)(tid * W + i) | ((uint32_t)(HZ[tid * W + i] >> ks) << 16);
+        ++idx;
+      }
+      __syncthreads();
+      return total;
+    };
+    uint32_t cnt = compact();
+    // exactness of the 31-bit keys: candidates closer than w with equal keys but different hashes
+    if (!T.any_n && !T.slow && ks > 0 && !(a.dbg_flags & 2u)) {
+      bool tie = false;
+      for (uint32_t r = tid; r < cnt; r += X2_NT) {
+        const uint32_t vr = se[r];
+        const int er = vr & 0xFFFFu;
+        for (uint32_t q = r + 1; q < cnt; q++) {
+          const uint32_t vq = se[q];
+          if ((int)(vq & 0xFFFFu) - er >= W) break;
+          if ((vq >> 16) == (vr >> 16)) {  // 16 key bits agree: compare the full keys and hashes
+            const uint64_t hr = HZ[er] & ~(1ull << 63), hq = HZ[vq & 0xFFFFu] & ~(1ull << 63);
+            tie |= ((hq >> ks) == (hr >> ks)) & (hq != hr);
+          }
+        }
+      }
+      if (__syncthreads_or(tie)) {
+        if (tid == 0 && a.dbg_counts) atomicAdd(&a.dbg_counts[1], 1u);
+        slow_path();
+        if (tid == 0 || tid == X2_NT - 1 || !blk_in) selmask = 0;
+        cnt = compact();
+      }
     }
+    // publish this tile's count, then finish the previous tile (its predecessors are done by now)
+    if (tid == 0 && !(a.dbg_flags & 1u)) lb_publish(a.status, tile, cnt);
+    if (pend_tile >= 0) flush((uint64_t)pend_tile, pend_cnt, buf ^ 1);
+    pend_tile = tile;
+    pend_cnt = cnt;
+    buf ^= 1;
+    __syncthreads();
   }
-  __syncthreads();
-  const uint64_t base = sh.base;
-  if (a.job_off && blk_in && tid > 0 && tid < X2_NT - 1 && l0 == 0) a.job_off[J] = base + my_first;
-  for (uint32_t r = tid; r < tile_cnt; r += X2_NT) {
-    const uint64_t gi = base + r;
-    if (gi < a.cap) {
-      const int e = sel_e[r];
-      const int b = e / W;
-      const uint32_t Jr = blk_j[b];
-      const Job& jb = a.jobs[Jr];
-      a.out_hz[gi] = HZ[e];
-      a.out_pos[gi] = (uint32_t)(jb.pos_base + jb.phase + a.one0 + (uint64_t)PS * (blk_l[b] + (uint32_t)(e - b * W)));
-      if (a.out_job) a.out_job[gi] = Jr;
-    }
-  }
+  if (pend_tile >= 0) flush((uint64_t)pend_tile, pend_cnt, buf ^ 1);
 }
 
 // padded position bases (multiple of W) and code-word bases per job
@@ -568,13 +606,16 @@ size_t x2_smem_bytes() {
 
 template <int K, int W, int PS>
 void launch_x2(const X2Args& a, uint64_t ntiles, cudaStream_t st, const char* tag) {
-  static bool attr = false;
+  static int grid = 0;
   const size_t smem = x2_smem_bytes<K, W, PS>();
-  if (!attr) {
+  if (!grid) {
     GOD_CUDA(cudaFuncSetAttribute(k_extract2<K, W, PS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
+    int per_sm = 0;
+    GOD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_extract2<K, W, PS>, X2_NT, smem));
+    grid = (per_sm > 0 ? per_sm : 1) * num_sms();
   }
-  GOD_LAUNCH(tag, (k_extract2<K, W, PS>), (unsigned)ntiles, X2_NT, smem, st, a);
+  const unsigned g = (unsigned)(ntiles < (uint64_t)grid ? ntiles : (uint64_t)grid);
+  GOD_LAUNCH(tag, (k_extract2<K, W, PS>), g, X2_NT, smem, st, a);
 }
 
 }  // namespace
@@ -609,7 +650,7 @@ bool run_extract2(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const
   uint64_t cap = cap_hint ? cap_hint : total_pos;
   if (cap > total_pos) cap = total_pos;
   if (cap == 0) cap = 1;
-  uint64_t* status = scr.alloc<uint64_t>(ntiles);
+  uint64_t* status = scr.alloc<uint64_t>(ntiles + 1);
   uint32_t* ctr = scr.alloc<uint32_t>(1);
   uint64_t* dtotal = scr.alloc<uint64_t>(1);
   if (want_job_off) rec.job_off = scr.alloc<uint64_t>(n_jobs + 1);
@@ -631,7 +672,7 @@ bool run_extract2(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const
     rec.hz = scr.alloc<uint64_t>(cap);
     rec.pos = scr.alloc<uint32_t>(cap);
     rec.job = want_job ? scr.alloc<uint32_t>(cap) : nullptr;
-    GOD_CUDA(cudaMemsetAsync(status, 0, ntiles * sizeof(uint64_t), st));
+    GOD_CUDA(cudaMemsetAsync(status, 0, (ntiles + 1) * sizeof(uint64_t), st));
     GOD_CUDA(cudaMemsetAsync(ctr, 0, sizeof(uint32_t), st));
     X2Args a{seq, seq_bytes, jobs, kb, cw, n_jobs, total_blocks, P.pat.one[0], key_shift, status, ctr,
              rec.hz, rec.pos, rec.job, rec.job_off, cap, dtotal, dbg_flags, dbg_counts};
