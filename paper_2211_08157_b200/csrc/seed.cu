@@ -13,6 +13,12 @@
 
 namespace god {
 
+struct SeedSources {
+  const uint64_t* hz[3];
+  const uint32_t* pos[3];
+  const uint64_t* off[3];
+};
+
 namespace {
 
 __global__ void k_phase(IndexView v, const Job* __restrict__ jobs, const uint64_t* __restrict__ job_off,
@@ -62,14 +68,6 @@ __global__ void k_phase(IndexView v, const Job* __restrict__ jobs, const uint64_
   }
 }
 
-__global__ void k_gather_offsets(const uint64_t* __restrict__ offsets, const uint32_t* __restrict__ ids, uint32_t n,
-                                 uint64_t* seq_off, uint64_t* seq_len) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    seq_off[i] = offsets[ids[i]];
-    seq_len[i] = offsets[ids[i] + 1] - offsets[ids[i]];
-  }
-}
-
 // jobs for an explicit read list: (ids[i], s) for s < p
 __global__ void k_make_jobs_ids(Params P, const uint64_t* __restrict__ offsets, const uint32_t* __restrict__ ids,
                                 uint32_t n, uint32_t p, Job* jobs, uint64_t* nkp1) {
@@ -88,28 +86,116 @@ __global__ void k_make_jobs_ids(Params P, const uint64_t* __restrict__ offsets, 
   }
 }
 
-__global__ void k_anchor_count(IndexView v, const uint64_t* __restrict__ hz, uint64_t n, uint32_t* cnt) {
+__global__ void k_anchor_count(IndexView v, const uint64_t* __restrict__ hz, uint64_t n, uint32_t* cnt,
+                               uint32_t* beg) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint2 rg = probe_range(v, hz[i] & ((1ull << 63) - 1));
     cnt[i] = rg.y - rg.x;
+    beg[i] = rg.x;
   }
 }
 
-__global__ void k_anchor_write(IndexView v, const uint64_t* __restrict__ hz, const uint32_t* __restrict__ pos,
-                               const uint32_t* __restrict__ job, uint64_t n, const uint64_t* __restrict__ aoff,
-                               god_anchor* out) {
+// one thread per read minimizer: its anchors are the kept entries [beg, beg + cnt)
+__global__ void k_anchor_write(IndexView v, const uint32_t* __restrict__ pos, const uint32_t* __restrict__ rid,
+                               const uint64_t* __restrict__ hz, uint64_t n, const uint64_t* __restrict__ aoff,
+                               const uint32_t* __restrict__ cnt, const uint32_t* __restrict__ beg, god_anchor* out) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t h = hz[i];
-    const uint2 rg = probe_range(v, h & ((1ull << 63) - 1));
+    const uint32_t c = cnt[i];
+    if (!c) continue;
+    const uint32_t qz = (uint32_t)(hz[i] >> 63), qpos = pos[i], r = rid[i], b = beg[i];
     uint64_t o = aoff[i];
-    const uint32_t qz = (uint32_t)(h >> 63), qpos = pos[i], rid = job[i];
-    for (uint32_t e = rg.x; e < rg.y; e++, o++) {
+    for (uint32_t e = b; e < b + c; e++, o++) {
       god_anchor an;
       an.ref_pos = __ldg(v.ent_pos + e);
       an.read_pos = qpos;
-      an.read_id = rid;
+      an.read_id = r;
       an.strand = (__ldg(v.ent_key + e) & 1u) ^ qz;
       out[o] = an;
+    }
+  }
+}
+
+// source of each read's PQ_a minimizers (see seed_reads); reads with src == 2 are already set
+__global__ void k_seed_plan(Pattern pat, int k, uint32_t n_reads, uint32_t p, const uint8_t* __restrict__ phases,
+                            const Job* __restrict__ jobs1, const uint64_t* __restrict__ offsets, uint8_t* src,
+                            uint32_t* srcj, uint32_t* list3, uint32_t* n3) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n_reads; r += gridDim.x * blockDim.x) {
+    if (src[r] == 2) continue;
+    if (jobs1) {
+      const uint32_t a = phases[r];
+      const uint64_t j = (uint64_t)r * p + a;
+      const uint64_t len = offsets[r + 1] - offsets[r];
+      const uint64_t ninc = included_count(pat, len, a);
+      const uint64_t nk_full = ninc >= (uint64_t)k ? ninc - k + 1 : 0;
+      if (jobs1[j].nk == nk_full) {
+        src[r] = 1;
+        srcj[r] = (uint32_t)j;
+        continue;
+      }
+    }
+    list3[atomicAdd(n3, 1u)] = r;
+  }
+}
+
+__global__ void k_redo_src(uint32_t nr, uint32_t p, const uint32_t* __restrict__ redo, const uint8_t* __restrict__ phases,
+                           uint8_t* src, uint32_t* srcj) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nr; i += gridDim.x * blockDim.x) {
+    const uint32_t r = redo[i];
+    src[r] = 2;
+    srcj[r] = i * p + phases[r];
+  }
+}
+
+__global__ void k_iota_src3(uint32_t n, uint8_t* src, uint32_t* srcj) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    src[r] = 3;
+    srcj[r] = r;
+  }
+}
+
+// jobs (list3[i], phase a) for the reads that need a dedicated extraction
+__global__ void k_make_jobs_sel(Params P, const uint64_t* __restrict__ offsets, const uint32_t* __restrict__ list3,
+                                uint32_t n3, const uint8_t* __restrict__ phases, Job* jobs, uint64_t* nkp1, uint8_t* src,
+                                uint32_t* srcj) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n3; i += gridDim.x * blockDim.x) {
+    const uint32_t r = list3[i];
+    Job jb;
+    jb.seq_off = offsets[r];
+    jb.len = offsets[r + 1] - offsets[r];
+    jb.pos_base = 0;
+    jb.phase = phases[r];
+    const uint64_t ninc = included_count(P.pat, jb.len, jb.phase);
+    jb.nk = (uint32_t)(ninc >= (uint64_t)P.k ? ninc - P.k + 1 : 0);
+    jobs[i] = jb;
+    nkp1[i] = (uint64_t)jb.nk + 1;
+    src[r] = 3;
+    srcj[r] = i;
+  }
+}
+
+__global__ void k_seed_counts(SeedSources S, uint32_t n_reads, const uint8_t* __restrict__ src,
+                              const uint32_t* __restrict__ srcj, uint64_t* cntr) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n_reads; r += gridDim.x * blockDim.x) {
+    const int s = src[r] - 1;
+    const uint32_t j = srcj[r];
+    cntr[r] = s >= 0 ? S.off[s][j + 1] - S.off[s][j] : 0;
+  }
+}
+
+// 8 threads per read copy its records into the read-ordered arrays
+__global__ void k_seed_gather(SeedSources S, uint32_t n_reads, const uint8_t* __restrict__ src,
+                              const uint32_t* __restrict__ srcj, const uint64_t* __restrict__ roff, uint64_t* hz,
+                              uint32_t* qpos, uint32_t* rid) {
+  for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < (uint64_t)n_reads * 8;
+       g += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t r = (uint32_t)(g >> 3), l = (uint32_t)(g & 7);
+    const int s = src[r] - 1;
+    if (s < 0) continue;
+    const uint64_t b = S.off[s][srcj[r]], o = roff[r], c = roff[r + 1] - o;
+    for (uint64_t q = l; q < c; q += 8) {
+      hz[o + q] = S.hz[s][b + q];
+      qpos[o + q] = S.pos[s][b + q];
+      rid[o + q] = r;
     }
   }
 }
@@ -134,60 +220,107 @@ uint64_t seed_reads(const god_index* ix, const uint8_t* reads, const uint64_t* o
     GOD_CUDA(cudaMemsetAsync(anchor_offsets, 0, sizeof(uint64_t), st));
     return 0;
   }
+  // Where each read's PQ_a minimizers come from: 1 = the capped phase extraction (its phase-a job
+  // was not truncated, so it holds all of PQ_a's minimizers), 2 = the uncapped phase re-extraction
+  // (fallback reads), 3 = a dedicated extraction of PQ_a (long reads, GIVEN mode, p = 1).
+  uint8_t* src = scr.alloc<uint8_t>(n_reads);
+  uint32_t* srcj = scr.alloc<uint32_t>(n_reads);
+  GOD_CUDA(cudaMemsetAsync(src, 0, n_reads, st));
   // ---------------- S1/S2: pattern alignment
+  bool have_phase_records = false;
+  Records rec1, rec2, rec3;
+  JobSet js1;
   if (mode == GOD_PHASE_SELECT) {
     if (p == 1) {
       GOD_CUDA(cudaMemsetAsync(phases, 0, n_reads, st));
     } else {
       const uint32_t kcap = (t + 1) * (uint32_t)P.w + (uint32_t)P.w;
-      JobSet js = make_jobs(P, offsets, n_reads, nullptr, p, kcap, false, st, scr);
-      const uint64_t js_bytes = js.seq_bytes;
-      Records rec;
-      run_extract(P, reads, js.seq_bytes, js.jobs, js.kb, js.n, js.total_pos, false, true, rec, st, scr,
-                  js.total_pos / (uint64_t)(P.w + 1) * 2 + js.total_pos / 8 + 4096, "extract_phase");
+      js1 = make_jobs(P, offsets, n_reads, nullptr, p, kcap, false, st, scr);
+      run_extract(P, reads, js1.seq_bytes, js1.jobs, js1.kb, js1.n, js1.total_pos, false, true, rec1, st, scr,
+                  js1.total_pos / (uint64_t)(P.w + 1) * 2 + js1.total_pos / 8 + 4096, "extract_phase");
       uint32_t* redo = scr.alloc<uint32_t>(n_reads);
       uint32_t* n_redo = scr.alloc<uint32_t>(1);
       GOD_CUDA(cudaMemsetAsync(n_redo, 0, sizeof(uint32_t), st));
-      GOD_LAUNCH("k_phase", k_phase, grid_for(n_reads, 128), 128, 0, st, v, js.jobs, rec.job_off, rec.hz, rec.pos, nullptr, n_reads, p, t,
-                                                      P.w, kcap, P.pat, P.k, phases, redo, n_redo);
+      GOD_LAUNCH("k_phase", k_phase, grid_for(n_reads, 128), 128, 0, st, v, js1.jobs, rec1.job_off, rec1.hz, rec1.pos,
+                 nullptr, n_reads, p, t, P.w, kcap, P.pat, P.k, phases, redo, n_redo);
       const uint32_t nr = d2h_scalar(n_redo, st);
       if (nr) {  // uncapped phase selection for reads whose capped prefix was not enough
         Job* jobs2 = scr.alloc<Job>((uint64_t)nr * p);
         uint64_t* kb2 = scr.alloc<uint64_t>((uint64_t)nr * p + 1);
         uint64_t* tot2 = scr.alloc<uint64_t>(1);
-        GOD_LAUNCH("k_make_jobs_ids", k_make_jobs_ids, grid_for((uint64_t)nr * p, 256), 256, 0, st, P, offsets, redo, nr, p, jobs2, kb2);
+        GOD_LAUNCH("k_make_jobs_ids", k_make_jobs_ids, grid_for((uint64_t)nr * p, 256), 256, 0, st, P, offsets, redo,
+                   nr, p, jobs2, kb2);
         scan_exclusive_u64(kb2, kb2, (uint64_t)nr * p, tot2, st, scr);
         GOD_CUDA(cudaMemcpyAsync(kb2 + (uint64_t)nr * p, tot2, sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
         const uint64_t tp2 = d2h_scalar(tot2, st);
-        Records rec2;
-        run_extract(P, reads, js_bytes, jobs2, kb2, nr * p, tp2, false, true, rec2, st, scr, tp2 / 4 + 4096, "extract_phase_redo");
+        run_extract(P, reads, js1.seq_bytes, jobs2, kb2, nr * p, tp2, false, true, rec2, st, scr, tp2 / 4 + 4096,
+                    "extract_phase_redo");
         uint32_t* n_redo2 = scr.alloc<uint32_t>(1);
         GOD_CUDA(cudaMemsetAsync(n_redo2, 0, sizeof(uint32_t), st));
-        GOD_LAUNCH("k_phase", k_phase, grid_for(nr, 128), 128, 0, st, v, jobs2, rec2.job_off, rec2.hz, rec2.pos, redo, nr, p, t, P.w, 0,
-                                                   P.pat, P.k, phases, redo, n_redo2);
+        GOD_LAUNCH("k_phase", k_phase, grid_for(nr, 128), 128, 0, st, v, jobs2, rec2.job_off, rec2.hz, rec2.pos, redo,
+                   nr, p, t, P.w, 0, P.pat, P.k, phases, redo, n_redo2);
+        GOD_LAUNCH("k_redo_src", k_redo_src, grid_for(nr, 256), 256, 0, st, nr, p, redo, phases, src, srcj);
       }
+      have_phase_records = true;
     }
   }
-  // ---------------- S3: minimizers of PQ_a
-  JobSet js = make_jobs(P, offsets, n_reads, phases, 0, 0, false, st, scr);
-  Records rec;
-  run_extract(P, reads, js.seq_bytes, js.jobs, js.kb, js.n, js.total_pos, true, true, rec, st, scr,
-              js.total_pos / (uint64_t)(P.w + 1) * 2 + js.total_pos / 8 + 4096, "extract_seed");
-  // ---------------- S4: probes -> anchors
-  const uint64_t n = rec.n;
+  // ---------------- S3: minimizers of PQ_a (reused from the phase extraction when complete)
+  uint32_t* list3 = scr.alloc<uint32_t>(n_reads);
+  uint32_t* n3 = scr.alloc<uint32_t>(1);
+  GOD_CUDA(cudaMemsetAsync(n3, 0, sizeof(uint32_t), st));
+  GOD_LAUNCH("k_seed_plan", k_seed_plan, grid_for(n_reads, 256), 256, 0, st, P.pat, P.k, n_reads, p, phases,
+             have_phase_records ? js1.jobs : nullptr, offsets, src, srcj, list3, n3);
+  const uint32_t h3 = d2h_scalar(n3, st);
+  if (h3) {
+    if (h3 == n_reads) {  // every read: phase-a jobs in read order
+      JobSet js3 = make_jobs(P, offsets, n_reads, phases, 0, 0, false, st, scr);
+      run_extract(P, reads, js3.seq_bytes, js3.jobs, js3.kb, js3.n, js3.total_pos, false, true, rec3, st, scr,
+                  js3.total_pos / (uint64_t)(P.w + 1) * 2 + js3.total_pos / 8 + 4096, "extract_seed");
+      GOD_LAUNCH("k_iota_src3", k_iota_src3, grid_for(n_reads, 256), 256, 0, st, n_reads, src, srcj);
+    } else {
+      Job* jobs3 = scr.alloc<Job>(h3);
+      uint64_t* kb3 = scr.alloc<uint64_t>((uint64_t)h3 + 1);
+      uint64_t* tot3 = scr.alloc<uint64_t>(1);
+      GOD_LAUNCH("k_make_jobs_sel", k_make_jobs_sel, grid_for(h3, 256), 256, 0, st, P, offsets, list3, h3, phases,
+                 jobs3, kb3, src, srcj);
+      scan_exclusive_u64(kb3, kb3, h3, tot3, st, scr);
+      GOD_CUDA(cudaMemcpyAsync(kb3 + h3, tot3, sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
+      const uint64_t tp3 = d2h_scalar(tot3, st);
+      uint64_t bytes = 0;
+      GOD_CUDA(cudaMemcpyAsync(&bytes, offsets + n_reads, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+      GOD_CUDA(cudaStreamSynchronize(st));
+      run_extract(P, reads, bytes, jobs3, kb3, h3, tp3, false, true, rec3, st, scr, tp3 / 4 + 4096, "extract_seed");
+    }
+  }
+  SeedSources S{};
+  S.hz[0] = rec1.hz; S.pos[0] = rec1.pos; S.off[0] = rec1.job_off;
+  S.hz[1] = rec2.hz; S.pos[1] = rec2.pos; S.off[1] = rec2.job_off;
+  S.hz[2] = rec3.hz; S.pos[2] = rec3.pos; S.off[2] = rec3.job_off;
+  // per-read record counts -> offsets -> one contiguous record array in read order
+  uint64_t* roff = scr.alloc<uint64_t>((uint64_t)n_reads + 1);
+  uint64_t* rtot = scr.alloc<uint64_t>(1);
+  GOD_LAUNCH("k_seed_counts", k_seed_counts, grid_for(n_reads, 256), 256, 0, st, S, n_reads, src, srcj, roff);
+  scan_exclusive_u64(roff, roff, n_reads, rtot, st, scr);
+  GOD_CUDA(cudaMemcpyAsync(roff + n_reads, rtot, sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
+  const uint64_t n = d2h_scalar(rtot, st);
+  uint64_t* hz = scr.alloc<uint64_t>(n);
+  uint32_t* qpos = scr.alloc<uint32_t>(n);
+  uint32_t* rid = scr.alloc<uint32_t>(n);
+  GOD_LAUNCH("k_seed_gather", k_seed_gather, grid_for((uint64_t)n_reads * 8, 256), 256, 0, st, S, n_reads, src, srcj,
+             roff, hz, qpos, rid);
+  // ---------------- S4: probes -> anchors (one probe per read minimizer; its range is kept for the write)
   uint32_t* cnt = scr.alloc<uint32_t>(n);
+  uint32_t* beg = scr.alloc<uint32_t>(n);
   uint64_t* aoff = scr.alloc<uint64_t>(n);
   uint64_t* total = scr.alloc<uint64_t>(1);
-  if (n) {
-    GOD_LAUNCH("k_anchor_count", k_anchor_count, grid_for(n, 256), 256, 0, st, v, rec.hz, n, cnt);
-  }
+  if (n) GOD_LAUNCH("k_anchor_count", k_anchor_count, grid_for(n, 256), 256, 0, st, v, hz, n, cnt, beg);
   scan_exclusive_u32_to_u64(cnt, aoff, n, total, st, scr);
-  GOD_LAUNCH("k_read_anchor_offsets", k_read_anchor_offsets, grid_for((uint64_t)n_reads + 1, 256), 256, 0, st, rec.job_off, aoff, n, total, n_reads,
-                                                                             anchor_offsets);
+  GOD_LAUNCH("k_read_anchor_offsets", k_read_anchor_offsets, grid_for((uint64_t)n_reads + 1, 256), 256, 0, st, roff,
+             aoff, n, total, n_reads, anchor_offsets);
   const uint64_t tot = d2h_scalar(total, st);
-  if (tot <= cap && n) {
-    GOD_LAUNCH("k_anchor_write", k_anchor_write, grid_for(n, 256), 256, 0, st, v, rec.hz, rec.pos, rec.job, n, aoff, anchors);
-  }
+  if (tot <= cap && n)
+    GOD_LAUNCH("k_anchor_write", k_anchor_write, grid_for(n, 256), 256, 0, st, v, qpos, rid, hz, n, aoff, cnt, beg,
+               anchors);
   return tot;
 }
 
