@@ -58,6 +58,7 @@ struct X2Args {
   uint64_t* total_out;
   uint32_t dbg_flags;      // developer toggles (GOD_X2_DBG): 1 = unordered output, 2 = no tie check
   uint32_t* dbg_counts;    // [0] tiles on the slow path, [1] tiles with a key tie
+  const uint32_t* tile_j;  // [2 * ntiles]: first and last job of each tile
 };
 
 __device__ __forceinline__ uint32_t find_job_le(const uint64_t* arr, uint32_t lo, uint32_t hi, uint64_t g) {
@@ -228,6 +229,8 @@ __global__ void __launch_bounds__(X2_NT, X2_MINB) k_extract2(X2Args a) {
   uint32_t* SE = reinterpret_cast<uint32_t*>(x2_smem + C::O_SE);     // [2][POS]
   uint32_t* BI = reinterpret_cast<uint32_t*>(x2_smem + C::O_BI);     // [2][4][NT]: job, pos base, first, start
   __shared__ X2Tile T;
+  __shared__ uint64_t skb[X2_NT + 2], scw[X2_NT + 2];
+  __shared__ uint32_t sjob[X2_NT];
   __shared__ uint32_t warp_cnt[NWARP];
   __shared__ uint64_t s_base;
 
@@ -290,8 +293,7 @@ __global__ void __launch_bounds__(X2_NT, X2_MINB) k_extract2(X2Args a) {
         const uint64_t gfirst = b_first < 0 ? 0 : (uint64_t)b_first * W;
         uint64_t glast = (uint64_t)(b_last < 0 ? 0 : b_last) * W;
         if (glast > gmax) glast = gmax;
-        const uint32_t j0 = find_job_le(a.kb, 0, a.n_jobs - 1, gfirst);
-        const uint32_t j1 = find_job_le(a.kb, j0, a.n_jobs - 1, glast);
+        const uint32_t j0 = a.tile_j[2 * t], j1 = a.tile_j[2 * t + 1];  // precomputed (k_x2_tile_jobs)
         T.j0 = j0; T.j1 = j1;
         const uint64_t lo = b_first < 0 ? a.cw[0] : a.cw[j0] + (gfirst - a.kb[j0]) / 16;
         uint64_t hi = a.cw[j1] + (glast - a.kb[j1] + NB + 15) / 16 + 1;
@@ -311,6 +313,13 @@ __global__ void __launch_bounds__(X2_NT, X2_MINB) k_extract2(X2Args a) {
     uint64_t* HZ = HZ2 + (size_t)buf * POS;
     const uint32_t j0 = T.j0, j1 = T.j1;
     const uint64_t cw_lo = T.cw_lo;
+    // the tile's job bases in SMEM (a tile spans <= NT + 1 jobs: every job owns >= 1 block)
+    const uint32_t nj = j1 - j0 + 1;
+    for (uint32_t q = tid; q <= nj; q += X2_NT) {
+      skb[q] = a.kb[j0 + q];
+      scw[q] = a.cw[j0 + q];
+    }
+    __syncthreads();
     const int nwords = (int)(T.cw_hi - cw_lo);
 
     // ---- my block: job J, first k-mer index l0
@@ -319,10 +328,11 @@ __global__ void __launch_bounds__(X2_NT, X2_MINB) k_extract2(X2Args a) {
     uint32_t J = j0, l0 = 0, nk = 0;
     if (blk_in) {
       const uint64_t g = (uint64_t)myb * W;
-      J = (j0 == j1) ? j0 : find_job_le(a.kb, j0, j1, g);
-      l0 = (uint32_t)(g - a.kb[J]);
+      J = (j0 == j1) ? j0 : j0 + find_job_le(skb, 0, nj - 1, g);
+      l0 = (uint32_t)(g - skb[J - j0]);
       nk = a.jobs[J].nk;
     }
+    sjob[tid] = blk_in ? J : 0xFFFFFFFFu;  // block -> job (job boundaries are window barriers)
 
     // ------------------------------------------------------------ A. sparsify into SMEM
     {
@@ -342,13 +352,13 @@ __global__ void __launch_bounds__(X2_NT, X2_MINB) k_extract2(X2Args a) {
           my_n |= nm;
         }
       } else {
-        uint32_t Jw = j0;
+        uint32_t Jw = 0;
         for (int wi = tid; wi < nwords; wi += X2_NT) {
           const uint64_t gw = cw_lo + wi;
-          Jw = find_job_le(a.cw, Jw, j1, gw);
-          const Job jb = a.jobs[Jw];
+          Jw = find_job_le(scw, Jw, nj - 1, gw);
+          const Job jb = a.jobs[j0 + Jw];
           const uint64_t ncode = jb.nk ? (uint64_t)jb.nk + K - 1 : 0;
-          const uint64_t q0 = (gw - a.cw[Jw]) * 16;
+          const uint64_t q0 = (gw - scw[Jw]) * 16;
           uint32_t nm = 0, word = 0;
           if (q0 < ncode)
             word = pack16<PS, true>(a.seq, a.seq_bytes, jb.seq_off + jb.phase + a.one0 + (uint64_t)PS * q0,
@@ -366,7 +376,7 @@ __global__ void __launch_bounds__(X2_NT, X2_MINB) k_extract2(X2Args a) {
     const bool blk_has_kmers = blk_in && l0 < nk;
     uint32_t win[NWIN];
     {
-      const int wbase = (int)(a.cw[J] + l0 / 16 - cw_lo);
+      const int wbase = (int)(scw[J - j0] + l0 / 16 - cw_lo);
       const uint32_t off = (l0 % 16) * 2;
       uint32_t raw[NLOAD + 1];
 #pragma unroll
@@ -421,6 +431,11 @@ __global__ void __launch_bounds__(X2_NT, X2_MINB) k_extract2(X2Args a) {
 #pragma unroll
         for (int i = 0; i < W; i++) nPF[i] = (wid < NWARP - 1) ? xpf[(wid + 1) * W + i] : 0u;
       }
+      // the next block starting another job: no window crosses into it (a job boundary is a barrier)
+      if (tid + 1 < X2_NT && sjob[tid + 1] != J) {
+#pragma unroll
+        for (int i = 0; i < W; i++) nPF[i] = 0u;
+      }
       uint32_t WM[W];
       WM[0] = SF[0];
 #pragma unroll
@@ -469,7 +484,7 @@ __global__ void __launch_bounds__(X2_NT, X2_MINB) k_extract2(X2Args a) {
         uint64_t hv = 0;
         if ((uint32_t)i < nvalid) {
           const uint32_t q = l0 + i;
-          const int wb = (int)(a.cw[J] + q / 16 - cw_lo);
+          const int wb = (int)(scw[J - j0] + q / 16 - cw_lo);
           const uint32_t o = q % 16;
           bool anyn = false;
           for (int bb = 0; bb < K; bb++) {
@@ -488,8 +503,8 @@ __global__ void __launch_bounds__(X2_NT, X2_MINB) k_extract2(X2Args a) {
           const uint64_t hj = H64[j];
           if (hj == 0 || hj == ~0ull) continue;
           int lo = j, hi = j;
-          while (lo > j - (W - 1) && H64[lo - 1] != 0) --lo;
-          while (hi < j + (W - 1) && H64[hi + 1] != 0) ++hi;
+          while (lo > j - (W - 1) && H64[lo - 1] != 0 && sjob[(lo - 1) / W] == J) --lo;
+          while (hi < j + (W - 1) && H64[hi + 1] != 0 && sjob[(hi + 1) / W] == J) ++hi;
           bool s = false;
           if (hi - lo + 1 < W) {
             uint64_t mn = ~0ull;
@@ -589,11 +604,27 @@ __global__ void __launch_bounds__(X2_NT, X2_MINB) k_extract2(X2Args a) {
   if (pend_tile >= 0) flush((uint64_t)pend_tile, pend_cnt, buf ^ 1);
 }
 
+// first and last job of every tile (binary searches over the padded bases, one thread per tile)
+__global__ void k_x2_tile_jobs(const uint64_t* __restrict__ kb, uint32_t n_jobs, uint64_t total_blocks, int W,
+                               uint64_t ntiles, uint32_t* tile_j) {
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < ntiles; t += (uint64_t)gridDim.x * blockDim.x) {
+    const int64_t b_first = (int64_t)t * X2_OUT_BLOCKS - 1;
+    const int64_t b_last = (int64_t)t * X2_OUT_BLOCKS + X2_NT - 2;
+    const uint64_t gmax = total_blocks * W - 1;
+    const uint64_t gfirst = b_first < 0 ? 0 : (uint64_t)b_first * W;
+    uint64_t glast = (uint64_t)(b_last < 0 ? 0 : b_last) * W;
+    if (glast > gmax) glast = gmax;
+    const uint32_t j0 = find_job_le(kb, 0, n_jobs - 1, gfirst);
+    tile_j[2 * t] = j0;
+    tile_j[2 * t + 1] = find_job_le(kb, j0, n_jobs - 1, glast);
+  }
+}
+
 // padded position bases (multiple of W) and code-word bases per job
 __global__ void k_x2_sizes(const Job* __restrict__ jobs, uint32_t n, int K, int W, uint64_t* kb, uint64_t* cw) {
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
     const uint64_t nk = jobs[j].nk;
-    kb[j] = (nk + 1 + W - 1) / W * W;
+    kb[j] = (nk ? (nk + W - 1) / W : 1) * W;  // no separator: job boundaries are handled in-kernel
     const uint64_t ncode = nk ? nk + K - 1 : 0;
     cw[j] = (ncode + 15) / 16;
   }
@@ -651,6 +682,10 @@ bool run_extract2(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const
   if (cap > total_pos) cap = total_pos;
   if (cap == 0) cap = 1;
   uint64_t* status = scr.alloc<uint64_t>(ntiles + 1);
+  uint32_t* tile_j = scr.alloc<uint32_t>(2 * ntiles + 2);
+  if (ntiles)
+    GOD_LAUNCH("k_x2_tile_jobs", k_x2_tile_jobs, grid_for(ntiles, 256), 256, 0, st, kb, n_jobs, total_blocks, W, ntiles,
+               tile_j);
   uint32_t* ctr = scr.alloc<uint32_t>(1);
   uint64_t* dtotal = scr.alloc<uint64_t>(1);
   if (want_job_off) rec.job_off = scr.alloc<uint64_t>(n_jobs + 1);
@@ -675,7 +710,7 @@ bool run_extract2(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const
     GOD_CUDA(cudaMemsetAsync(status, 0, (ntiles + 1) * sizeof(uint64_t), st));
     GOD_CUDA(cudaMemsetAsync(ctr, 0, sizeof(uint32_t), st));
     X2Args a{seq, seq_bytes, jobs, kb, cw, n_jobs, total_blocks, P.pat.one[0], key_shift, status, ctr,
-             rec.hz, rec.pos, rec.job, rec.job_off, cap, dtotal, dbg_flags, dbg_counts};
+             rec.hz, rec.pos, rec.job, rec.job_off, cap, dtotal, dbg_flags, dbg_counts, tile_j};
     if (ntiles) {
       if (K == 21 && W == 11) {
         if (PS == 2) launch_x2<21, 11, 2>(a, ntiles, st, tag);

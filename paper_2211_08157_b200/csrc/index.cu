@@ -30,6 +30,7 @@ constexpr int RS_BITS = 8;
 constexpr int RS_BINS = 1 << RS_BITS;
 constexpr uint64_t HASH_BITS_MASK = (1ull << 63) - 1;
 constexpr int RS_DYN_SMEM = RS_TILE * (sizeof(uint64_t) + sizeof(uint32_t));
+constexpr int RS2_NT = 512, RS2_IPT = RS_TILE / RS2_NT;  // scatter: 16 warps, 8 items per thread
 
 __global__ void __launch_bounds__(RS_NT) k_rs_hist(const uint64_t* __restrict__ keys, uint64_t n, int shift,
                                                    uint32_t dmask, uint32_t* hist, uint32_t ntiles) {
@@ -128,6 +129,141 @@ __global__ void __launch_bounds__(RS_NT) k_rs_scatter(const uint64_t* __restrict
     const uint64_t dst = goff[(uint64_t)d * ntiles + blockIdx.x] + (s - dstart[d]);
     kout[dst] = kk;
     vout[dst] = sv[s];
+  }
+}
+
+// Stable scatter, warp-striped ranking: warp w owns items [w*256, w*256+256) of the tile, item j of
+// lane l is w*256 + 32 j + l, so (warp, j, lane) order is index order.  Ranks come from match_any
+// plus per-warp digit counters (no block barrier per item round).
+__global__ void __launch_bounds__(RS2_NT) k_rs_scatter2(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin,
+                                                       uint64_t* __restrict__ kout, uint32_t* __restrict__ vout,
+                                                       uint64_t n, int shift, uint32_t dmask,
+                                                       const uint64_t* __restrict__ goff, uint32_t ntiles) {
+  __shared__ uint32_t wcnt[RS2_NT / 32][RS_BINS];
+  __shared__ uint32_t dstart[RS_BINS];
+  __shared__ uint32_t wsum[RS_BINS / 32];
+  extern __shared__ __align__(16) unsigned char rs_dyn[];
+  uint64_t* sk = reinterpret_cast<uint64_t*>(rs_dyn);
+  uint32_t* sv = reinterpret_cast<uint32_t*>(sk + RS_TILE);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  for (int i = tid; i < (RS2_NT / 32) * RS_BINS; i += RS2_NT) (&wcnt[0][0])[i] = 0;
+  __syncthreads();
+  const uint64_t base = (uint64_t)blockIdx.x * RS_TILE + (uint64_t)wid * (32 * RS2_IPT);
+  const uint32_t lt = (1u << lane) - 1;
+  uint64_t key[RS2_IPT];
+  uint32_t val[RS2_IPT];
+  uint32_t rk[RS2_IPT];
+#pragma unroll
+  for (int j = 0; j < RS2_IPT; j++) {
+    const uint64_t i = base + (uint64_t)j * 32 + lane;
+    const bool ok = i < n;
+    key[j] = ok ? kin[i] : 0;
+    val[j] = ok ? vin[i] : 0;
+    const uint32_t d = ok ? ((uint32_t)((key[j] & HASH_BITS_MASK) >> shift) & dmask) : RS_BINS;
+    const uint32_t peers = __match_any_sync(0xffffffffu, d);
+    const int leader = __ffs(peers) - 1;
+    uint32_t old = 0;
+    if (lane == leader && ok) {
+      old = wcnt[wid][d];
+      wcnt[wid][d] = old + __popc(peers);
+    }
+    old = __shfl_sync(0xffffffffu, old, leader);
+    rk[j] = old + __popc(peers & lt);
+  }
+  __syncthreads();
+  // digit tid (< 256): exclusive prefix over warps, tile total
+  uint32_t acc = 0;
+  if (tid < RS_BINS) {
+#pragma unroll
+    for (int q = 0; q < RS2_NT / 32; q++) {
+      const uint32_t c = wcnt[q][tid];
+      wcnt[q][tid] = acc;
+      acc += c;
+    }
+  }
+  // exclusive scan of the tile totals over the 256 digits (warps 0..7)
+  uint32_t incl = acc;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += y;
+  }
+  if (lane == 31 && tid < RS_BINS) wsum[wid] = incl;
+  __syncthreads();
+  if (tid < RS_BINS) {
+    uint32_t before = 0;
+#pragma unroll
+    for (int q = 0; q < RS_BINS / 32; q++) before += q < wid ? wsum[q] : 0u;
+    dstart[tid] = before + incl - acc;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < RS2_IPT; j++) {
+    const uint64_t i = base + (uint64_t)j * 32 + lane;
+    if (i < n) {
+      const uint32_t d = (uint32_t)((key[j] & HASH_BITS_MASK) >> shift) & dmask;
+      const uint32_t slot = dstart[d] + wcnt[wid][d] + rk[j];
+      sk[slot] = key[j];
+      sv[slot] = val[j];
+    }
+  }
+  __syncthreads();
+  const uint32_t cnt = (uint32_t)min((uint64_t)RS_TILE, n - (uint64_t)blockIdx.x * RS_TILE);
+  for (uint32_t s = tid; s < cnt; s += RS2_NT) {
+    const uint64_t kk = sk[s];
+    const uint32_t d = (uint32_t)((kk & HASH_BITS_MASK) >> shift) & dmask;
+    const uint64_t dst = goff[(uint64_t)d * ntiles + blockIdx.x] + (s - dstart[d]);
+    kout[dst] = kk;
+    vout[dst] = sv[s];
+  }
+}
+
+// After sorting by the top 32 hash bits, order each group of equal top bits by the remaining low
+// bits, stably.  Only "mixed" groups (two different hashes sharing the top 32 bits, ~n^2/2^33 of
+// them; identical-hash runs are already in position order) need work: (a) the first hash change
+// inside a group marks it, (b) the marked group is insertion-sorted (a handful of entries).
+__global__ void k_rs_fix_mark(const uint64_t* __restrict__ k, uint64_t n, int lo_bits, uint8_t* mark) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x + 1; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t a = k[i - 1] & HASH_BITS_MASK, b = k[i] & HASH_BITS_MASK;
+    if ((a >> lo_bits) != (b >> lo_bits) || a == b) continue;  // not a hash change inside a group
+    uint64_t g = i - 1;
+    bool first = true;
+    while (g > 0) {
+      const uint64_t c = k[g - 1] & HASH_BITS_MASK;
+      if ((c >> lo_bits) != (b >> lo_bits)) break;
+      if (c != (k[g] & HASH_BITS_MASK)) { first = false; break; }
+      --g;
+    }
+    if (first) mark[i] = 1;
+  }
+}
+
+__global__ void k_rs_fix_sort(uint64_t* __restrict__ k, uint32_t* __restrict__ v, uint64_t n, int lo_bits,
+                              const uint8_t* __restrict__ mark, uint64_t* __restrict__ tk, uint32_t* __restrict__ tv) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x + 1; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    if (!mark[i]) continue;
+    const uint64_t top = (k[i] & HASH_BITS_MASK) >> lo_bits;
+    uint64_t g = i - 1;
+    while (g > 0 && ((k[g - 1] & HASH_BITS_MASK) >> lo_bits) == top) --g;
+    uint64_t e = i + 1;
+    while (e < n && ((k[e] & HASH_BITS_MASK) >> lo_bits) == top) ++e;
+    // stable: emit the entries of each distinct hash in ascending hash order, each run in place order
+    // (O(group x distinct hashes); a group holds 2-3 distinct hashes)
+    uint64_t out = g;
+    bool have_prev = false;
+    uint64_t prev = 0;
+    while (out < e) {
+      uint64_t nxt = ~0ull;
+      for (uint64_t q = g; q < e; q++) {
+        const uint64_t h = k[q] & HASH_BITS_MASK;
+        if ((!have_prev || h > prev) && h < nxt) nxt = h;
+      }
+      for (uint64_t q = g; q < e; q++)
+        if ((k[q] & HASH_BITS_MASK) == nxt) { tk[out] = k[q]; tv[out] = v[q]; ++out; }
+      prev = nxt;
+      have_prev = true;
+    }
+    for (uint64_t q = g; q < e; q++) { k[q] = tk[q]; v[q] = tv[q]; }
   }
 }
 
@@ -400,18 +536,27 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
     uint64_t* goff = scr.alloc<uint64_t>((uint64_t)RS_BINS * ntiles);
     static bool attr = false;
     if (!attr) {
-      GOD_CUDA(cudaFuncSetAttribute(k_rs_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, RS_DYN_SMEM));
+      GOD_CUDA(cudaFuncSetAttribute(k_rs_scatter2, cudaFuncAttributeMaxDynamicSharedMemorySize, RS_DYN_SMEM));
       attr = true;
     }
+    // LSD passes over the top min(2k, 32) hash bits, then a finishing pass for the low bits
     const int hbits = 2 * P.k;
-    for (int shift = 0; shift < hbits; shift += RS_BITS) {
+    const int lo = hbits > 32 ? hbits - 32 : 0;
+    for (int shift = lo; shift < hbits; shift += RS_BITS) {
       const int bits = min(RS_BITS, hbits - shift);
       const uint32_t dmask = (1u << bits) - 1;
       GOD_LAUNCH("k_rs_hist", k_rs_hist, ntiles, RS_NT, 0, st, k0, n, shift, dmask, hist, ntiles);
       scan_exclusive_u32_to_u64(hist, goff, (uint64_t)RS_BINS * ntiles, nullptr, st, scr);
-      GOD_LAUNCH("k_rs_scatter", k_rs_scatter, ntiles, RS_NT, RS_DYN_SMEM, st, k0, v0, k1, v1, n, shift, dmask, goff, ntiles);
+      GOD_LAUNCH("k_rs_scatter2", k_rs_scatter2, ntiles, RS2_NT, RS_DYN_SMEM, st, k0, v0, k1, v1, n, shift, dmask, goff,
+                 ntiles);
       std::swap(k0, k1);
       std::swap(v0, v1);
+    }
+    if (lo > 0) {
+      uint8_t* mark = scr.alloc<uint8_t>(n);
+      GOD_CUDA(cudaMemsetAsync(mark, 0, n, st));
+      GOD_LAUNCH("k_rs_fix_mark", k_rs_fix_mark, grid_for(n, 256), 256, 0, st, k0, n, lo, mark);
+      GOD_LAUNCH("k_rs_fix_sort", k_rs_fix_sort, grid_for(n, 256), 256, 0, st, k0, v0, n, lo, mark, k1, v1);
     }
   }
   // K3: distinct hashes

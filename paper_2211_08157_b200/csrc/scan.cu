@@ -5,7 +5,7 @@ namespace god {
 
 namespace {
 constexpr int SCAN_NT = 256;
-constexpr int SCAN_IPT = 8;
+constexpr int SCAN_IPT = 16;
 constexpr int SCAN_TILE = SCAN_NT * SCAN_IPT;
 
 template <class TIn>
@@ -44,7 +44,9 @@ __global__ void __launch_bounds__(SCAN_NT) k_scan(const TIn* in, uint64_t* out, 
       if (lane >= d) ws += y;
     }
     if (lane < SCAN_NT / 32) warp_sum[lane] = ws;  // inclusive
-    if (lane == SCAN_NT / 32 - 1) s_excl = lb_exclusive(status, tile, ws);
+    const uint64_t tile_total = __shfl_sync(0xffffffffu, ws, SCAN_NT / 32 - 1);
+    const uint64_t ex = lb_exclusive_warp(status, tile, tile_total);
+    if (lane == 0) s_excl = ex;
   }
   __syncthreads();
   uint64_t run = s_excl + (wid ? warp_sum[wid - 1] : 0) + x - sum;
