@@ -541,7 +541,7 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
     }
     // LSD passes over the top min(2k, 32) hash bits, then a finishing pass for the low bits
     const int hbits = 2 * P.k;
-    const int lo = hbits > 32 ? hbits - 32 : 0;
+    const int lo = (hbits > 32 && getenv("GOD_SORT_FIXUP")) ? hbits - 32 : 0;  // default: full LSD
     for (int shift = lo; shift < hbits; shift += RS_BITS) {
       const int bits = min(RS_BITS, hbits - shift);
       const uint32_t dmask = (1u << bits) - 1;
@@ -597,9 +597,13 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
   GOD_CUDA(cudaMemcpyAsync(&n_kept, kept_tot, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
   GOD_CUDA(cudaStreamSynchronize(st));
   GOD_REQUIRE(n_kept < 0xFFFFFFFFull, "index has >= 2^32 kept entries");
-  // directory bits: ~1-2 entries per slot; low bits must fit 31 bits next to the strand bit
+  // directory bits: ~1-2 kept entries per slot (measured best for the probe kernels: a probe is one
+  // directory sector + one key sector); the low hash bits must fit 31 bits next to the strand bit
   const uint32_t hb = 2 * P.k;
-  uint32_t B = floor_log2(n_kept ? n_kept : 1);
+  const uint32_t lg = floor_log2(n_kept ? n_kept : 1);
+  const char* bdbg = getenv("GOD_DIR_SLACK");
+  const uint32_t slack = bdbg ? (uint32_t)atoi(bdbg) : 0u;
+  uint32_t B = lg > slack ? lg - slack : 0;
   const uint32_t Bmin = hb > 31 ? hb - 31 : 0;
   const uint32_t Bmax = hb < 28 ? hb : 28;
   B = B < Bmin ? Bmin : (B > Bmax ? Bmax : B);

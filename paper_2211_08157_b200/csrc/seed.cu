@@ -17,11 +17,13 @@ struct SeedSources {
   const uint64_t* hz[3];
   const uint32_t* pos[3];
   const uint64_t* off[3];
+  const uint32_t* cnt[3];   // probe result per record: number of kept entries with its hash
+  const uint32_t* beg[3];   // ... and the first of them
 };
 
 namespace {
 
-__global__ void k_phase(IndexView v, const Job* __restrict__ jobs, const uint64_t* __restrict__ job_off,
+__global__ void k_phase(const uint32_t* __restrict__ occ, const Job* __restrict__ jobs, const uint64_t* __restrict__ job_off,
                         const uint64_t* __restrict__ hz, const uint32_t* __restrict__ pos, const uint32_t* __restrict__ ids,
                         uint32_t n_reads, uint32_t p, uint32_t t, uint32_t w, uint32_t kcap, Pattern pat, int k,
                         uint8_t* phases, uint32_t* redo, uint32_t* n_redo) {
@@ -58,10 +60,7 @@ __global__ void k_phase(IndexView v, const Job* __restrict__ jobs, const uint64_
     for (uint32_t s = 0; s < p; s++) {
       const uint64_t j = (uint64_t)i * p + s;
       uint64_t sc = 0;
-      for (uint64_t q = 0; q < c; q++) {
-        const uint2 rg = probe_range(v, hz[job_off[j] + q] & ((1ull << 63) - 1));
-        sc += rg.y - rg.x;
-      }
+      for (uint64_t q = 0; q < c; q++) sc += occ[job_off[j] + q];  // occ(h) of the q-th minimizer
       if (s == 0 || sc > best) { best = sc; a = s; }
     }
     phases[r] = (uint8_t)a;
@@ -185,7 +184,7 @@ __global__ void k_seed_counts(SeedSources S, uint32_t n_reads, const uint8_t* __
 // 8 threads per read copy its records into the read-ordered arrays
 __global__ void k_seed_gather(SeedSources S, uint32_t n_reads, const uint8_t* __restrict__ src,
                               const uint32_t* __restrict__ srcj, const uint64_t* __restrict__ roff, uint64_t* hz,
-                              uint32_t* qpos, uint32_t* rid) {
+                              uint32_t* qpos, uint32_t* rid, uint32_t* cnt, uint32_t* beg) {
   for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < (uint64_t)n_reads * 8;
        g += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t r = (uint32_t)(g >> 3), l = (uint32_t)(g & 7);
@@ -196,6 +195,8 @@ __global__ void k_seed_gather(SeedSources S, uint32_t n_reads, const uint8_t* __
       hz[o + q] = S.hz[s][b + q];
       qpos[o + q] = S.pos[s][b + q];
       rid[o + q] = r;
+      cnt[o + q] = S.cnt[s][b + q];
+      beg[o + q] = S.beg[s][b + q];
     }
   }
 }
@@ -208,6 +209,13 @@ __global__ void k_read_anchor_offsets(const uint64_t* __restrict__ job_off, cons
   }
 }
 }  // namespace
+
+// probe every record once: (count, first) of the kept entries with its hash
+static void probe_all(const IndexView& v, Records& rec, cudaStream_t st, Scratch& scr) {
+  rec.cnt = scr.alloc<uint32_t>(rec.n);
+  rec.beg = scr.alloc<uint32_t>(rec.n);
+  if (rec.n) GOD_LAUNCH("k_probe", k_anchor_count, grid_for(rec.n, 256), 256, 0, st, v, rec.hz, rec.n, rec.cnt, rec.beg);
+}
 
 uint64_t seed_reads(const god_index* ix, const uint8_t* reads, const uint64_t* offsets, uint32_t n_reads,
                     god_phase_mode mode, uint8_t* phases, uint32_t t, god_anchor* anchors, uint64_t* anchor_offsets,
@@ -241,8 +249,9 @@ uint64_t seed_reads(const god_index* ix, const uint8_t* reads, const uint64_t* o
       uint32_t* redo = scr.alloc<uint32_t>(n_reads);
       uint32_t* n_redo = scr.alloc<uint32_t>(1);
       GOD_CUDA(cudaMemsetAsync(n_redo, 0, sizeof(uint32_t), st));
-      GOD_LAUNCH("k_phase", k_phase, grid_for(n_reads, 128), 128, 0, st, v, js1.jobs, rec1.job_off, rec1.hz, rec1.pos,
-                 nullptr, n_reads, p, t, P.w, kcap, P.pat, P.k, phases, redo, n_redo);
+      probe_all(v, rec1, st, scr);
+      GOD_LAUNCH("k_phase", k_phase, grid_for(n_reads, 128), 128, 0, st, rec1.cnt, js1.jobs, rec1.job_off, rec1.hz,
+                 rec1.pos, nullptr, n_reads, p, t, P.w, kcap, P.pat, P.k, phases, redo, n_redo);
       const uint32_t nr = d2h_scalar(n_redo, st);
       if (nr) {  // uncapped phase selection for reads whose capped prefix was not enough
         Job* jobs2 = scr.alloc<Job>((uint64_t)nr * p);
@@ -257,8 +266,9 @@ uint64_t seed_reads(const god_index* ix, const uint8_t* reads, const uint64_t* o
                     "extract_phase_redo");
         uint32_t* n_redo2 = scr.alloc<uint32_t>(1);
         GOD_CUDA(cudaMemsetAsync(n_redo2, 0, sizeof(uint32_t), st));
-        GOD_LAUNCH("k_phase", k_phase, grid_for(nr, 128), 128, 0, st, v, jobs2, rec2.job_off, rec2.hz, rec2.pos, redo,
-                   nr, p, t, P.w, 0, P.pat, P.k, phases, redo, n_redo2);
+        probe_all(v, rec2, st, scr);
+        GOD_LAUNCH("k_phase", k_phase, grid_for(nr, 128), 128, 0, st, rec2.cnt, jobs2, rec2.job_off, rec2.hz, rec2.pos,
+                   redo, nr, p, t, P.w, 0, P.pat, P.k, phases, redo, n_redo2);
         GOD_LAUNCH("k_redo_src", k_redo_src, grid_for(nr, 256), 256, 0, st, nr, p, redo, phases, src, srcj);
       }
       have_phase_records = true;
@@ -292,10 +302,11 @@ uint64_t seed_reads(const god_index* ix, const uint8_t* reads, const uint64_t* o
       run_extract(P, reads, bytes, jobs3, kb3, h3, tp3, false, true, rec3, st, scr, tp3 / 4 + 4096, "extract_seed");
     }
   }
+  if (h3) probe_all(v, rec3, st, scr);
   SeedSources S{};
-  S.hz[0] = rec1.hz; S.pos[0] = rec1.pos; S.off[0] = rec1.job_off;
-  S.hz[1] = rec2.hz; S.pos[1] = rec2.pos; S.off[1] = rec2.job_off;
-  S.hz[2] = rec3.hz; S.pos[2] = rec3.pos; S.off[2] = rec3.job_off;
+  S.hz[0] = rec1.hz; S.pos[0] = rec1.pos; S.off[0] = rec1.job_off; S.cnt[0] = rec1.cnt; S.beg[0] = rec1.beg;
+  S.hz[1] = rec2.hz; S.pos[1] = rec2.pos; S.off[1] = rec2.job_off; S.cnt[1] = rec2.cnt; S.beg[1] = rec2.beg;
+  S.hz[2] = rec3.hz; S.pos[2] = rec3.pos; S.off[2] = rec3.job_off; S.cnt[2] = rec3.cnt; S.beg[2] = rec3.beg;
   // per-read record counts -> offsets -> one contiguous record array in read order
   uint64_t* roff = scr.alloc<uint64_t>((uint64_t)n_reads + 1);
   uint64_t* rtot = scr.alloc<uint64_t>(1);
@@ -306,14 +317,13 @@ uint64_t seed_reads(const god_index* ix, const uint8_t* reads, const uint64_t* o
   uint64_t* hz = scr.alloc<uint64_t>(n);
   uint32_t* qpos = scr.alloc<uint32_t>(n);
   uint32_t* rid = scr.alloc<uint32_t>(n);
-  GOD_LAUNCH("k_seed_gather", k_seed_gather, grid_for((uint64_t)n_reads * 8, 256), 256, 0, st, S, n_reads, src, srcj,
-             roff, hz, qpos, rid);
-  // ---------------- S4: probes -> anchors (one probe per read minimizer; its range is kept for the write)
   uint32_t* cnt = scr.alloc<uint32_t>(n);
   uint32_t* beg = scr.alloc<uint32_t>(n);
+  GOD_LAUNCH("k_seed_gather", k_seed_gather, grid_for((uint64_t)n_reads * 8, 256), 256, 0, st, S, n_reads, src, srcj,
+             roff, hz, qpos, rid, cnt, beg);
+  // ---------------- S4: anchors (every read minimizer was probed once, right after its extraction)
   uint64_t* aoff = scr.alloc<uint64_t>(n);
   uint64_t* total = scr.alloc<uint64_t>(1);
-  if (n) GOD_LAUNCH("k_anchor_count", k_anchor_count, grid_for(n, 256), 256, 0, st, v, hz, n, cnt, beg);
   scan_exclusive_u32_to_u64(cnt, aoff, n, total, st, scr);
   GOD_LAUNCH("k_read_anchor_offsets", k_read_anchor_offsets, grid_for((uint64_t)n_reads + 1, 256), 256, 0, st, roff,
              aoff, n, total, n_reads, anchor_offsets);
