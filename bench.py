@@ -230,20 +230,17 @@ def main():
         an, ao, ph = god.god_seed_reads(ix, dreads, droffs, cap=cap)
         if ev:
             ev[2].record()
-        return ix, an
+        st = ix.stats()
+        ix.free()  # a step builds, uses and releases its index (the pool keeps the memory mapped)
+        return st, an
 
     # warm-up (also sizes the anchor output)
     cap = None
-    keep = []
     for i in range(max(args.warmup, 1)):
-        ix, an = step(cap)
+        st, an = step(cap)
         cap = max(int(an.shape[0]), 1)
-        st = ix.stats()
-        keep.append(ix)
+        del an
     n_anchors = cap
-    for ix in keep:
-        ix.free()
-    keep.clear()
     torch.cuda.synchronize()
 
     # timed region
@@ -259,8 +256,7 @@ def main():
     clk.start()
     start.record()
     for i in range(args.steps):
-        ix, an = step(cap, evs[i])
-        keep.append(ix)
+        st, an = step(cap, evs[i])
     end.record()
     torch.cuda.synchronize()
     if dist:
@@ -272,9 +268,6 @@ def main():
     elapsed_ms = start.elapsed_time(end)
     build_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in evs]))
     seed_ms = float(np.mean([e[1].elapsed_time(e[2]) for e in evs]))
-    for ix in keep:
-        ix.free()
-    keep.clear()
     if dist:
         t = torch.tensor([elapsed_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -364,15 +357,12 @@ def run_e2e(god, torch, cfg, pattern, k, w, n_anchors, steps, dist, world, dev):
     if dist:
         dist.barrier()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    hs = []
     s.record()
     for _ in range(steps):
-        hs.append(one())
+        L.god_index_free(one())
     e.record()
     torch.cuda.synchronize()
     ms = s.elapsed_time(e)
-    for h in hs:
-        L.god_index_free(h)
     if dist:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
