@@ -78,6 +78,34 @@ def make_inputs(workload: str, scale: float, rank: int):
     return cfg, pattern, k, w
 
 
+# ------------------------------------------------------------------------------------------ multi-GPU plumbing
+# Replicas: every rank builds the index of the same reference and seeds its OWN batch
+# of reads (read seed offset by rank) -> weak scaling, no data-path collective.  The only collective
+# is the max-over-ranks of the device-timed region.
+def max_over_ranks(x: float, dist=None, device=None) -> float:
+    if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
+        return float(x)
+    import torch
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def aggregate_rate(units_per_rank: int, world: int, ms_per_step_max: float) -> float:
+    """Whole-job throughput: the units all ranks processed / the slowest rank's time."""
+    return world * units_per_rank / (ms_per_step_max / 1e3)
+
+
+def workload_config(args, cfg, pattern, k, w, world):
+    idx = {"tiny": 0, "illumina": 1, "hifi": 2, "hifi-110": 2, "ont": 3}.get(args.workload, 4)
+    return {"workload": f"{args.workload}: BASELINE.json configs[{idx}] ({cfg.ref.size/1e9:.2f} Gbp reference, "
+                        f"{cfg.reads.n} reads/rank, pattern '{pattern}', k={k}, w={w}, cutoff top "
+                        f"{cfg.cutoff[0]}/{cfg.cutoff[1]})",
+            "ref_bp": int(cfg.ref.size), "n_reads": cfg.reads.n, "read_bp": int(cfg.reads.seq.size),
+            "pattern": pattern, "k": k, "w": w, "scale": args.scale,
+            "l2_policy": "inputs larger than L2 (no flush needed)", "parallelism": f"replicas x{world} (weak)"}
+
+
 # ------------------------------------------------------------------------------------------ clocks
 class ClockSampler:
     FIELDS = ("clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.hw_slowdown",
@@ -268,12 +296,9 @@ def main():
     elapsed_ms = start.elapsed_time(end)
     build_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in evs]))
     seed_ms = float(np.mean([e[1].elapsed_time(e[2]) for e in evs]))
-    if dist:
-        t = torch.tensor([elapsed_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed_ms = float(t.item())
+    elapsed_ms = max_over_ranks(elapsed_ms, dist, dev)
     ms_per_step = elapsed_ms / args.steps
-    value = world * n_reads / (ms_per_step / 1e3)
+    value = aggregate_rate(n_reads, world, ms_per_step)
 
     # records counts for the byte model (one extra untimed pass)
     hz, _, _, _ = god.god_minimizers(dreads, droffs, pattern, k, w, phases=None)  # phase-0 read minimizers (approx.)
@@ -304,12 +329,7 @@ def main():
             "metric": METRIC, "value": round(value, 1), "unit": "reads/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-            "config": {"workload": f"{args.workload}: BASELINE configs[{list(WORKLOADS).index(args.workload) if args.workload.startswith('human') else 0}] "
-                       f"{cfg.ref.size/1e9:.2f} Gbp ref + {n_reads} reads, pattern '{pattern}', k={k}, w={w}, "
-                       f"cutoff top {cfg.cutoff[0]}/{cfg.cutoff[1]}",
-                       "ref_bp": int(cfg.ref.size), "n_reads": n_reads, "read_bp": int(cfg.reads.seq.size),
-                       "pattern": pattern, "k": k, "w": w, "scale": args.scale,
-                       "l2_policy": "inputs larger than L2 (no flush needed)", "parallelism": f"replicas x{world} (weak)"},
+            "config": workload_config(args, cfg, pattern, k, w, world),
             "index_build_gbps": round(cfg.ref.size / (build_ms / 1e3) / 1e9, 3),
             "seed_reads_per_s": round(n_reads / (seed_ms / 1e3), 1),
             "anchors_per_s": round(n_anchors / (seed_ms / 1e3), 1),
@@ -363,10 +383,7 @@ def run_e2e(god, torch, cfg, pattern, k, w, n_anchors, steps, dist, world, dev):
     e.record()
     torch.cuda.synchronize()
     ms = s.elapsed_time(e)
-    if dist:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(ms, dist, dev)
     h2d = cfg.ref.size + cfg.ref_offsets.nbytes + cfg.reads.seq.size + cfg.reads.offsets.nbytes
     d2h = int(need.value) * 16 + (n + 1) * 8 + n
     return {"value": round(world * n / (ms / steps / 1e3), 1), "unit": "reads/s", "h2d_bytes_per_step": int(h2d),
@@ -393,8 +410,7 @@ def run_reference(args, world, rank):
     out = {"impl": "reference", "metric": METRIC, "value": round(v, 2), "unit": "reads/s", "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(full * 1e3, 1), "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-           "config": {"workload": args.workload, "ref_bp": int(cfg.ref.size), "n_reads": cfg.reads.n,
-                      "pattern": pattern, "k": k, "w": w, "scale": args.scale},
+           "config": workload_config(args, cfg, pattern, k, w, world),
            "cpu_baseline": {"value": round(v, 2), "unit": "reads/s", "cores": 1, "kind": "oracle", "sample": desc},
            "e2e": {"value": round(v, 2), "unit": "reads/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
