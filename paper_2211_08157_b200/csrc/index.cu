@@ -1,3 +1,4 @@
+#include <algorithm>
 // index.cu — stage 3: the seed index (P:286 (3)).
 //
 // "We do not directly insert minimizer information ... Instead, we append the minimizer
@@ -16,6 +17,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <type_traits>
 #include <utility>
 #include <vector>
 #include "internal.cuh"
@@ -32,10 +34,26 @@ constexpr uint64_t HASH_BITS_MASK = (1ull << 63) - 1;
 constexpr int RS_DYN_SMEM = RS_TILE * (sizeof(uint64_t) + sizeof(uint32_t));
 constexpr int RS2_NT = 512, RS2_IPT = RS_TILE / RS2_NT;  // scatter: 16 warps, 8 items per thread
 
+// Lanes of the warp holding the same digit as this lane (digit < 2^NBITS; invalid lanes carry
+// d = 2^NBITS and only match each other): one ballot per digit bit.  Measured much cheaper than
+// __match_any_sync, whose long latency stalled the ranking loops.
+template <int NBITS>
+__device__ __forceinline__ uint32_t warp_peers(uint32_t d) {
+  uint32_t peers = 0xFFFFFFFFu;
+#pragma unroll
+  for (int b = 0; b <= NBITS; b++) {
+    const bool bit = (d >> b) & 1u;
+    const uint32_t m = __ballot_sync(0xFFFFFFFFu, bit);
+    peers &= bit ? m : ~m;
+  }
+  return peers;
+}
+
+template <int RB>
 __global__ void __launch_bounds__(RS_NT) k_rs_hist(const uint64_t* __restrict__ keys, uint64_t n, int shift,
                                                    uint32_t dmask, uint32_t* hist, uint32_t ntiles) {
-  __shared__ uint32_t h[RS_BINS];
-  for (int i = threadIdx.x; i < RS_BINS; i += RS_NT) h[i] = 0;
+  __shared__ uint32_t h[(1 << RB)];
+  for (int i = threadIdx.x; i < (1 << RB); i += RS_NT) h[i] = 0;
   __syncthreads();
   const uint64_t base = (uint64_t)blockIdx.x * RS_TILE;
 #pragma unroll 4
@@ -44,109 +62,25 @@ __global__ void __launch_bounds__(RS_NT) k_rs_hist(const uint64_t* __restrict__ 
     if (i < n) atomicAdd(&h[(uint32_t)((keys[i] & HASH_BITS_MASK) >> shift) & dmask], 1u);
   }
   __syncthreads();
-  for (int d = threadIdx.x; d < RS_BINS; d += RS_NT) hist[(uint64_t)d * ntiles + blockIdx.x] = h[d];
-}
-
-__global__ void __launch_bounds__(RS_NT) k_rs_scatter(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin,
-                                                      uint64_t* __restrict__ kout, uint32_t* __restrict__ vout,
-                                                      uint64_t n, int shift, uint32_t dmask,
-                                                      const uint64_t* __restrict__ goff, uint32_t ntiles) {
-  __shared__ uint32_t wcnt[RS_NT / 32][RS_BINS];
-  __shared__ uint32_t run[RS_BINS];
-  __shared__ uint32_t dstart[RS_BINS];
-  extern __shared__ __align__(16) unsigned char rs_dyn[];
-  uint64_t* sk = reinterpret_cast<uint64_t*>(rs_dyn);
-  uint32_t* sv = reinterpret_cast<uint32_t*>(sk + RS_TILE);
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const uint64_t base = (uint64_t)blockIdx.x * RS_TILE;
-  for (int i = tid; i < RS_BINS; i += RS_NT) run[i] = 0;
-  for (int i = tid; i < (RS_NT / 32) * RS_BINS; i += RS_NT) (&wcnt[0][0])[i] = 0;
-  __syncthreads();
-  uint64_t key[RS_IPT];
-  uint32_t val[RS_IPT];
-  uint32_t rank[RS_IPT];
-  const uint32_t lt = (1u << lane) - 1;
-#pragma unroll
-  for (int r = 0; r < RS_IPT; r++) {
-    const uint64_t i = base + (uint64_t)r * RS_NT + tid;
-    const bool ok = i < n;
-    key[r] = ok ? kin[i] : 0;
-    val[r] = ok ? vin[i] : 0;
-    const uint32_t d = ok ? ((uint32_t)((key[r] & HASH_BITS_MASK) >> shift) & dmask) : RS_BINS;  // sentinel
-    const uint32_t peers = __match_any_sync(0xffffffffu, d);
-    const uint32_t rw = __popc(peers & lt);
-    if (ok && rw == 0) wcnt[wid][d] = __popc(peers);
-    __syncthreads();
-    {  // digit tid: exclusive prefix over warps, continuing the running count of earlier rounds
-      uint32_t acc = run[tid];
-#pragma unroll
-      for (int q = 0; q < RS_NT / 32; q++) {
-        uint32_t c = wcnt[q][tid];
-        wcnt[q][tid] = acc;
-        acc += c;
-      }
-      run[tid] = acc;
-    }
-    __syncthreads();
-    rank[r] = ok ? wcnt[wid][d] + rw : 0;
-    __syncthreads();
-#pragma unroll
-    for (int q = 0; q < RS_NT / 32; q++) wcnt[q][tid] = 0;
-    __syncthreads();
-  }
-  // tile-local digit starts (exclusive scan of run[] over 256 digits by warp 0..7)
-  if (tid < 32) {
-    uint32_t v[RS_BINS / 32];
-    uint32_t s = 0;
-#pragma unroll
-    for (int q = 0; q < RS_BINS / 32; q++) { v[q] = run[tid * (RS_BINS / 32) + q]; s += v[q]; }
-    uint32_t incl = s;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
-      if (lane >= d) incl += y;
-    }
-    uint32_t acc = incl - s;
-#pragma unroll
-    for (int q = 0; q < RS_BINS / 32; q++) { dstart[tid * (RS_BINS / 32) + q] = acc; acc += v[q]; }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int r = 0; r < RS_IPT; r++) {
-    const uint64_t i = base + (uint64_t)r * RS_NT + tid;
-    if (i < n) {
-      const uint32_t d = (uint32_t)((key[r] & HASH_BITS_MASK) >> shift) & dmask;
-      const uint32_t slot = dstart[d] + rank[r];
-      sk[slot] = key[r];
-      sv[slot] = val[r];
-    }
-  }
-  __syncthreads();
-  const uint32_t cnt = (uint32_t)min((uint64_t)RS_TILE, n - base);
-  for (uint32_t s = tid; s < cnt; s += RS_NT) {
-    const uint64_t kk = sk[s];
-    const uint32_t d = (uint32_t)((kk & HASH_BITS_MASK) >> shift) & dmask;
-    const uint64_t dst = goff[(uint64_t)d * ntiles + blockIdx.x] + (s - dstart[d]);
-    kout[dst] = kk;
-    vout[dst] = sv[s];
-  }
+  for (int d = threadIdx.x; d < (1 << RB); d += RS_NT) hist[(uint64_t)d * ntiles + blockIdx.x] = h[d];
 }
 
 // Stable scatter, warp-striped ranking: warp w owns items [w*256, w*256+256) of the tile, item j of
 // lane l is w*256 + 32 j + l, so (warp, j, lane) order is index order.  Ranks come from match_any
 // plus per-warp digit counters (no block barrier per item round).
+template <int RB>
 __global__ void __launch_bounds__(RS2_NT) k_rs_scatter2(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin,
                                                        uint64_t* __restrict__ kout, uint32_t* __restrict__ vout,
                                                        uint64_t n, int shift, uint32_t dmask,
                                                        const uint64_t* __restrict__ goff, uint32_t ntiles) {
-  __shared__ uint32_t wcnt[RS2_NT / 32][RS_BINS];
-  __shared__ uint32_t dstart[RS_BINS];
-  __shared__ uint32_t wsum[RS_BINS / 32];
+  __shared__ uint32_t wcnt[RS2_NT / 32][(1 << RB)];
+  __shared__ uint32_t dstart[(1 << RB)];
+  __shared__ uint32_t wsum[(1 << RB) / 32];
   extern __shared__ __align__(16) unsigned char rs_dyn[];
   uint64_t* sk = reinterpret_cast<uint64_t*>(rs_dyn);
   uint32_t* sv = reinterpret_cast<uint32_t*>(sk + RS_TILE);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  for (int i = tid; i < (RS2_NT / 32) * RS_BINS; i += RS2_NT) (&wcnt[0][0])[i] = 0;
+  for (int i = tid; i < (RS2_NT / 32) * (1 << RB); i += RS2_NT) (&wcnt[0][0])[i] = 0;
   __syncthreads();
   const uint64_t base = (uint64_t)blockIdx.x * RS_TILE + (uint64_t)wid * (32 * RS2_IPT);
   const uint32_t lt = (1u << lane) - 1;
@@ -159,8 +93,8 @@ __global__ void __launch_bounds__(RS2_NT) k_rs_scatter2(const uint64_t* __restri
     const bool ok = i < n;
     key[j] = ok ? kin[i] : 0;
     val[j] = ok ? vin[i] : 0;
-    const uint32_t d = ok ? ((uint32_t)((key[j] & HASH_BITS_MASK) >> shift) & dmask) : RS_BINS;
-    const uint32_t peers = __match_any_sync(0xffffffffu, d);
+    const uint32_t d = ok ? ((uint32_t)((key[j] & HASH_BITS_MASK) >> shift) & dmask) : (1 << RB);
+    const uint32_t peers = warp_peers<RB>(d);
     const int leader = __ffs(peers) - 1;
     uint32_t old = 0;
     if (lane == leader && ok) {
@@ -173,7 +107,7 @@ __global__ void __launch_bounds__(RS2_NT) k_rs_scatter2(const uint64_t* __restri
   __syncthreads();
   // digit tid (< 256): exclusive prefix over warps, tile total
   uint32_t acc = 0;
-  if (tid < RS_BINS) {
+  if (tid < (1 << RB)) {
 #pragma unroll
     for (int q = 0; q < RS2_NT / 32; q++) {
       const uint32_t c = wcnt[q][tid];
@@ -188,12 +122,12 @@ __global__ void __launch_bounds__(RS2_NT) k_rs_scatter2(const uint64_t* __restri
     const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
     if (lane >= d) incl += y;
   }
-  if (lane == 31 && tid < RS_BINS) wsum[wid] = incl;
+  if (lane == 31 && tid < (1 << RB)) wsum[wid] = incl;
   __syncthreads();
-  if (tid < RS_BINS) {
+  if (tid < (1 << RB)) {
     uint32_t before = 0;
 #pragma unroll
-    for (int q = 0; q < RS_BINS / 32; q++) before += q < wid ? wsum[q] : 0u;
+    for (int q = 0; q < (1 << RB) / 32; q++) before += q < wid ? wsum[q] : 0u;
     dstart[tid] = before + incl - acc;
   }
   __syncthreads();
@@ -218,52 +152,421 @@ __global__ void __launch_bounds__(RS2_NT) k_rs_scatter2(const uint64_t* __restri
   }
 }
 
-// After sorting by the top 32 hash bits, order each group of equal top bits by the remaining low
-// bits, stably.  Only "mixed" groups (two different hashes sharing the top 32 bits, ~n^2/2^33 of
-// them; identical-hash runs are already in position order) need work: (a) the first hash change
-// inside a group marks it, (b) the marked group is insertion-sorted (a handful of entries).
-__global__ void k_rs_fix_mark(const uint64_t* __restrict__ k, uint64_t n, int lo_bits, uint8_t* mark) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x + 1; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t a = k[i - 1] & HASH_BITS_MASK, b = k[i] & HASH_BITS_MASK;
-    if ((a >> lo_bits) != (b >> lo_bits) || a == b) continue;  // not a hash change inside a group
-    uint64_t g = i - 1;
-    bool first = true;
-    while (g > 0) {
-      const uint64_t c = k[g - 1] & HASH_BITS_MASK;
-      if ((c >> lo_bits) != (b >> lo_bits)) break;
-      if (c != (k[g] & HASH_BITS_MASK)) { first = false; break; }
-      --g;
-    }
-    if (first) mark[i] = 1;
+// ---- bin sort (2k >= 36).  Minimizer hashes are skewed toward small values (each is the minimum
+// of a window: density ~ (w+1)(1-u)^w at u = h / 4^k), so fixed-width hash buckets differ ~10x in
+// size.  Instead each record gets a monotone bin number b(h) sized from the data: the top SEG_BITS
+// hash bits select a segment t, which is cut into bins_t = ceil(c_t / BIN_TARGET) equal-width bins,
+//   b(h) = base_t + floor(low(h) * bins_t / 2^L),   L = 2k - SEG_BITS, base = exclusive scan of bins_t,
+// so bins hold ~BIN_TARGET records, b is non-decreasing in h, and a bin never spans two segments.
+// b is stored in the free key bits above the hash; two stable 9-bit LSD passes order the records by
+// b, then one CTA per bin sorts it in SMEM on the packed u64
+//   v = low(h) << 33 | pos << 1 | strand       (integer order = (hash, pos) order; L <= 30),
+// skipping digits that are constant across the bin.  Bins above BS_CAP (hashes with thousands of
+// occurrences) go to a chunked global-memory kernel.
+constexpr int BS_NT = 512;
+constexpr int BS_NW = BS_NT / 32;
+constexpr int BS_CAP = 4096;                      // records of a bin held in SMEM (x2 buffers)
+constexpr int BS_IPT = BS_CAP / BS_NT;            // 8
+constexpr int BS_SMEM = 2 * BS_CAP * 8;
+constexpr int SEG_BITS = 12;
+constexpr uint32_t BIN_TARGET = 3584;
+constexpr int BIN_DIGIT = 9;                      // LSD digit over b
+constexpr int BIN_INS_MAX = 4;                    // buckets up to this size: insertion sort by one thread
+static_assert(RS_BINS * BS_NW == BS_NT * 8, "block scan assumes 8 counters per thread");
+
+__global__ void k_seg_hist(const uint64_t* __restrict__ k, uint64_t n, int L, uint32_t* segc) {
+  __shared__ uint32_t h[1 << SEG_BITS];
+  for (int i = threadIdx.x; i < (1 << SEG_BITS); i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    atomicAdd(&h[(uint32_t)((k[i] & HASH_BITS_MASK) >> L)], 1u);
+  __syncthreads();
+  for (int i = threadIdx.x; i < (1 << SEG_BITS); i += blockDim.x)
+    if (h[i]) atomicAdd(&segc[i], h[i]);
+}
+
+// one CTA of 1024 threads: bins_t, base_t (exclusive scan) and the total bin count
+__global__ void __launch_bounds__(1024) k_seg_table(const uint32_t* __restrict__ segc, uint32_t target, uint2* table,
+                                                    uint32_t* n_bins) {
+  constexpr int PER = (1 << SEG_BITS) / 1024;
+  __shared__ uint32_t wsum[32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  uint32_t nb[PER], tsum = 0;
+#pragma unroll
+  for (int q = 0; q < PER; q++) {
+    const uint32_t c = segc[tid * PER + q];
+    nb[q] = (c + target - 1) / target;
+    tsum += nb[q];
+  }
+  uint32_t incl = tsum;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += y;
+  }
+  if (lane == 31) wsum[wid] = incl;
+  __syncthreads();
+  uint32_t before = incl - tsum;
+  for (int q = 0; q < wid; q++) before += wsum[q];
+#pragma unroll
+  for (int q = 0; q < PER; q++) {
+    table[tid * PER + q] = make_uint2(before, nb[q]);
+    before += nb[q];
+  }
+  if (tid == 1023) *n_bins = before;
+}
+
+__global__ void k_seg_assign(uint64_t* __restrict__ k, uint64_t n, int L, int hbits, const uint2* __restrict__ table) {
+  const uint64_t lmask = (1ull << L) - 1;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t kk = k[i];
+    const uint64_t h = kk & HASH_BITS_MASK;
+    const uint2 t = __ldg(table + (h >> L));
+    const uint64_t b = t.x + (((h & lmask) * t.y) >> L);
+    k[i] = kk | (b << hbits);
   }
 }
 
-__global__ void k_rs_fix_sort(uint64_t* __restrict__ k, uint32_t* __restrict__ v, uint64_t n, int lo_bits,
-                              const uint8_t* __restrict__ mark, uint64_t* __restrict__ tk, uint32_t* __restrict__ tv) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x + 1; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    if (!mark[i]) continue;
-    const uint64_t top = (k[i] & HASH_BITS_MASK) >> lo_bits;
-    uint64_t g = i - 1;
-    while (g > 0 && ((k[g - 1] & HASH_BITS_MASK) >> lo_bits) == top) --g;
-    uint64_t e = i + 1;
-    while (e < n && ((k[e] & HASH_BITS_MASK) >> lo_bits) == top) ++e;
-    // stable: emit the entries of each distinct hash in ascending hash order, each run in place order
-    // (O(group x distinct hashes); a group holds 2-3 distinct hashes)
-    uint64_t out = g;
-    bool have_prev = false;
-    uint64_t prev = 0;
-    while (out < e) {
-      uint64_t nxt = ~0ull;
-      for (uint64_t q = g; q < e; q++) {
-        const uint64_t h = k[q] & HASH_BITS_MASK;
-        if ((!have_prev || h > prev) && h < nxt) nxt = h;
-      }
-      for (uint64_t q = g; q < e; q++)
-        if ((k[q] & HASH_BITS_MASK) == nxt) { tk[out] = k[q]; tv[out] = v[q]; ++out; }
-      prev = nxt;
-      have_prev = true;
+__global__ void k_bucket_bounds(const uint64_t* __restrict__ k, uint64_t n, int lo_bits, uint32_t nb, uint64_t* bstart) {
+  for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b <= nb; b += gridDim.x * blockDim.x) {
+    uint64_t lo = 0, hi = n;  // first record whose bits above lo_bits are >= b
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if (((k[mid] & HASH_BITS_MASK) >> lo_bits) < b) lo = mid + 1;
+      else hi = mid;
     }
-    for (uint64_t q = g; q < e; q++) { k[q] = tk[q]; v[q] = tv[q]; }
+    bstart[b] = lo;
+  }
+}
+
+// One CTA-wide LSD pass: the n <= BS_CAP values v[] (thread item j = warp-striped index
+// wid * 32 * BS_IPT + j * 32 + lane) are scattered into dst stably by bits [shift, shift + bits).
+// cnt is digit-major with a padded row (cnt[d * CNT_LD + w], CNT_LD = BS_NW + 1, so that the lanes of
+// a warp touching different digits hit different banks); on return cnt[d * CNT_LD] is the start of
+// digit d in dst.  Ends with a barrier (dst complete, cnt readable).
+constexpr int CNT_LD = BS_NW + 1;
+constexpr int CNT_WORDS = RS_BINS * CNT_LD;
+__device__ __forceinline__ void cta_rank_scatter(const uint64_t (&v)[BS_IPT], int n, int shift, uint32_t dmask,
+                                                 uint64_t* dst, uint32_t* cnt, uint32_t* wsum) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  for (int i = tid; i < CNT_WORDS; i += BS_NT) cnt[i] = 0;
+  __syncthreads();
+  const uint32_t lt = (1u << lane) - 1;
+  uint32_t rk[BS_IPT];
+#pragma unroll
+  for (int j = 0; j < BS_IPT; j++) {
+    const int i = wid * (32 * BS_IPT) + j * 32 + lane;
+    const bool ok = i < n;
+    const uint32_t d = ok ? (uint32_t)(v[j] >> shift) & dmask : RS_BINS;
+    const uint32_t peers = warp_peers<RS_BITS>(d);
+    const int leader = __ffs(peers) - 1;
+    uint32_t old = 0;
+    if (lane == leader && ok) {
+      old = cnt[d * CNT_LD + wid];
+      cnt[d * CNT_LD + wid] = old + __popc(peers);
+    }
+    rk[j] = __shfl_sync(0xffffffffu, old, leader) + __popc(peers & lt);
+  }
+  __syncthreads();
+  // block-wide exclusive scan of the 4096 counters in (digit, warp) order, 8 per thread
+  uint32_t* row = cnt + (tid >> 1) * CNT_LD + (tid & 1) * 8;
+  uint32_t x[8];
+  uint32_t tsum = 0;
+#pragma unroll
+  for (int q = 0; q < 8; q++) { const uint32_t c = row[q]; x[q] = tsum; tsum += c; }
+  uint32_t incl = tsum;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += y;
+  }
+  if (lane == 31) wsum[wid] = incl;
+  __syncthreads();
+  uint32_t before = incl - tsum;
+#pragma unroll
+  for (int q = 0; q < BS_NW; q++) before += q < wid ? wsum[q] : 0u;
+#pragma unroll
+  for (int q = 0; q < 8; q++) row[q] = x[q] + before;
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < BS_IPT; j++) {
+    const int i = wid * (32 * BS_IPT) + j * 32 + lane;
+    if (i < n) {
+      const uint32_t d = (uint32_t)(v[j] >> shift) & dmask;
+      dst[cnt[d * CNT_LD + wid] + rk[j]] = v[j];
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void cta_load_striped(const uint64_t* src, int n, uint64_t (&v)[BS_IPT]) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int j = 0; j < BS_IPT; j++) {
+    const int i = wid * (32 * BS_IPT) + j * 32 + lane;
+    v[j] = i < n ? src[i] : 0;
+  }
+}
+
+__global__ void __launch_bounds__(BS_NT, 2) k_bin_sort(uint64_t* __restrict__ k, uint32_t* __restrict__ v,
+                                                       const uint64_t* __restrict__ bstart,
+                                                       const uint32_t* __restrict__ n_bins, int L, int hbits,
+                                                       uint32_t* big, uint32_t* n_big) {
+  extern __shared__ __align__(16) unsigned char bs_smem[];
+  uint64_t* A = reinterpret_cast<uint64_t*>(bs_smem);
+  uint64_t* Bf = A + BS_CAP;
+  __shared__ __align__(16) uint32_t cnt[CNT_WORDS];
+  __shared__ uint32_t wsum[BS_NW];
+  __shared__ uint32_t s_or[BS_NW], s_and[BS_NW];
+  __shared__ uint32_t s_big[BS_CAP / (BIN_INS_MAX + 1) + 1];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint64_t lmask = (1ull << L) - 1, hmask = (1ull << hbits) - 1;
+  const uint32_t nb = *n_bins;
+  for (uint32_t c = blockIdx.x; c < nb; c += gridDim.x) {
+    const uint64_t s = bstart[c], e = bstart[c + 1];
+    const int n = (int)(e - s);
+    if (n <= 1) {
+      if (n == 1 && threadIdx.x == 0) k[s] &= ~(hmask ^ HASH_BITS_MASK);  // strip b
+      continue;
+    }
+    if (n > BS_CAP) {
+      if (threadIdx.x == 0) big[atomicAdd(n_big, 1u)] = c;
+      continue;
+    }
+    uint64_t x[BS_IPT];
+    uint32_t lmin = 0xFFFFFFFFu, lmax = 0;
+    uint64_t seg = 0;
+#pragma unroll
+    for (int j = 0; j < BS_IPT; j++) {  // all loads of the bin in flight at once
+      const int i = wid * (32 * BS_IPT) + j * 32 + lane;
+      uint64_t kk = 0;
+      uint32_t pp = 0;
+      if (i < n) {
+        kk = __ldcs(k + s + i);
+        pp = __ldcs(v + s + i);
+        const uint32_t lo = (uint32_t)(kk & lmask);
+        lmin = min(lmin, lo);
+        lmax = max(lmax, lo);
+        seg = (kk & hmask) >> L;
+      }
+      x[j] = ((kk & lmask) << 33) | ((uint64_t)pp << 1) | (kk >> 63);
+    }
+#pragma unroll
+    for (int d = 16; d; d >>= 1) {
+      lmin = min(lmin, __shfl_xor_sync(0xffffffffu, lmin, d));
+      lmax = max(lmax, __shfl_xor_sync(0xffffffffu, lmax, d));
+    }
+    if (lane == 0) { s_or[wid] = lmin; s_and[wid] = lmax; }
+    if (wid == 0 && lane == 0) wsum[0] = (uint32_t)seg;  // every record of a bin has the same segment
+    __syncthreads();
+    uint32_t mn = 0xFFFFFFFFu, mx = 0;
+#pragma unroll
+    for (int q = 0; q < BS_NW; q++) { mn = min(mn, s_or[q]); mx = max(mx, s_and[q]); }
+    const uint64_t segv = wsum[0];
+    __syncthreads();
+    if (mn == mx) {  // one hash: position order already (the stable passes over b kept it)
+      for (int i = threadIdx.x; i < n; i += BS_NT) k[s + i] &= ~(hmask ^ HASH_BITS_MASK);
+      __syncthreads();
+      continue;
+    }
+    // (1) MSD placement by the top 12 bits of low(h) - mn (4096 buckets, ~1 record each), then an
+    //     insertion sort of each bucket on the full packed value (unique: it contains pos)
+    const int rbits = 32 - __clz(mx - mn);
+    const int shb = rbits > 12 ? rbits - 12 : 0;
+    {
+      uint4* c4 = reinterpret_cast<uint4*>(cnt);
+      c4[2 * threadIdx.x] = make_uint4(0, 0, 0, 0);
+      c4[2 * threadIdx.x + 1] = make_uint4(0, 0, 0, 0);
+    }
+    __syncthreads();
+    uint32_t bk[BS_IPT];
+#pragma unroll
+    for (int j = 0; j < BS_IPT; j++) {
+      const int i = wid * (32 * BS_IPT) + j * 32 + lane;
+      bk[j] = ((uint32_t)(x[j] >> 33) - mn) >> shb;
+      if (i < n) atomicAdd(&cnt[bk[j]], 1u);
+    }
+    __syncthreads();
+    uint32_t cmax;
+    {
+      uint4* c4 = reinterpret_cast<uint4*>(cnt);
+      const uint4 p0 = c4[2 * threadIdx.x], p1 = c4[2 * threadIdx.x + 1];
+      uint32_t y[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+      uint32_t tsum = 0, tmax = 0;
+#pragma unroll
+      for (int q = 0; q < 8; q++) { const uint32_t c2 = y[q]; y[q] = tsum; tsum += c2; tmax = max(tmax, c2); }
+      uint32_t incl = tsum;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t t2 = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += t2;
+      }
+#pragma unroll
+      for (int d = 16; d; d >>= 1) tmax = max(tmax, __shfl_xor_sync(0xffffffffu, tmax, d));
+      if (lane == 31) wsum[wid] = incl;
+      if (lane == 0) s_or[wid] = tmax;
+      __syncthreads();
+      uint32_t before = incl - tsum;
+      cmax = 0;
+#pragma unroll
+      for (int q = 0; q < BS_NW; q++) { before += q < wid ? wsum[q] : 0u; cmax = max(cmax, s_or[q]); }
+      c4[2 * threadIdx.x] = make_uint4(y[0] + before, y[1] + before, y[2] + before, y[3] + before);
+      c4[2 * threadIdx.x + 1] = make_uint4(y[4] + before, y[5] + before, y[6] + before, y[7] + before);
+    }
+    __syncthreads();
+    const uint64_t* res;
+    if (cmax <= 1024) {
+#pragma unroll
+      for (int j = 0; j < BS_IPT; j++) {
+        const int i = wid * (32 * BS_IPT) + j * 32 + lane;
+        if (i < n) A[atomicAdd(&cnt[bk[j]], 1u)] = x[j];
+      }
+      if (threadIdx.x == 0) wsum[0] = 0;
+      __syncthreads();
+      // cnt[b] is now the end of bucket b.  Buckets of <= BIN_INS_MAX records: insertion sort by the owning
+      // thread; larger ones: listed for the warps below
+      uint32_t* biglist = s_big;  // buckets of more than BIN_INS_MAX records
+#pragma unroll 1
+      for (int q = 0; q < 8; q++) {
+        const int b2 = threadIdx.x * 8 + q;
+        const int st = b2 ? (int)cnt[b2 - 1] : 0, en = (int)cnt[b2];
+        if (en - st > BIN_INS_MAX) {
+          biglist[atomicAdd(&wsum[0], 1u)] = (uint32_t)b2;
+          continue;
+        }
+        for (int i = st + 1; i < en; i++) {
+          const uint64_t t2 = A[i];
+          int j2 = i - 1;
+          while (j2 >= st && A[j2] > t2) { A[j2 + 1] = A[j2]; --j2; }
+          A[j2 + 1] = t2;
+        }
+      }
+      __syncthreads();
+      const uint32_t nbig_b = wsum[0];
+      if (nbig_b) {
+        // one warp per large bucket: bitonic sort in place, in the all-ascending form (each merge
+        // starts by comparing i with its mirror), so pairs reaching past the bucket end are no-ops
+        for (uint32_t q = wid; q < nbig_b; q += BS_NW) {
+          const uint32_t b2 = biglist[q];
+          const int st = b2 ? (int)cnt[b2 - 1] : 0, sz = (int)cnt[b2] - st;
+          uint64_t* a2 = A + st;
+          const int P2 = 1 << (32 - __clz(sz - 1));
+          for (int kk = 2; kk <= P2; kk <<= 1) {
+            const int hk = kk >> 1;
+            for (int t = lane; t < (P2 >> 1); t += 32) {
+              const int blk = t >> (__ffs(hk) - 1), off = t & (hk - 1);
+              const int i = blk * kk + off, j = blk * kk + kk - 1 - off;
+              if (j < sz) {
+                const uint64_t x0 = a2[i], x1 = a2[j];
+                if (x0 > x1) { a2[i] = x1; a2[j] = x0; }
+              }
+            }
+            __syncwarp();
+            for (int j2 = hk >> 1; j2 >= 1; j2 >>= 1) {
+              for (int t = lane; t < (P2 >> 1); t += 32) {
+                const int blk = t >> (__ffs(j2) - 1), off = t & (j2 - 1);
+                const int i = blk * 2 * j2 + off, j = i + j2;
+                if (j < sz) {
+                  const uint64_t x0 = a2[i], x1 = a2[j];
+                  if (x0 > x1) { a2[i] = x1; a2[j] = x0; }
+                }
+              }
+              __syncwarp();
+            }
+          }
+        }
+        __syncthreads();
+      }
+      res = A;
+    } else {
+      // (2) a bucket with > 1024 records (a very frequent hash): stable LSD over the low(h) digits below
+      //     the highest bit where mn and mx differ (bits above it are constant in the bin)
+      if (threadIdx.x == 0) atomicAdd(n_big + 1, 1u);  // statistics: bins sorted this way
+      const int hib = 32 - __clz(mn ^ mx);
+      uint64_t* dst = A;
+      for (int sh = 0; sh < hib; sh += RS_BITS) {
+        const int bits = min(RS_BITS, hib - sh);
+        if (sh) cta_load_striped(dst == A ? Bf : A, n, x);
+        cta_rank_scatter(x, n, 33 + sh, (1u << bits) - 1, dst, cnt, wsum);
+        dst = dst == A ? Bf : A;
+      }
+      res = dst == A ? Bf : A;
+    }
+    const uint64_t topv = segv << L;
+    for (int i = threadIdx.x; i < n; i += BS_NT) {
+      const uint64_t pv = res[i];
+      __stcs(k + s + i, (topv | (pv >> 33)) | ((pv & 1ull) << 63));
+      __stcs(v + s + i, (uint32_t)(pv >> 1));
+    }
+    __syncthreads();
+  }
+}
+
+// oversized bins (repeat-heavy hashes): the same LSD over the low bits, chunk by chunk through
+// global memory (stable across chunks: chunks are taken in order, each digit's run appended)
+__global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort_big(uint64_t* __restrict__ k, uint32_t* __restrict__ v,
+                                                              uint64_t* __restrict__ t0, uint64_t* __restrict__ t1,
+                                                              const uint64_t* __restrict__ bstart, const uint32_t* big,
+                                                              const uint32_t* n_big, int lo_bits, int hbits) {
+  extern __shared__ __align__(16) unsigned char bs_smem[];
+  uint64_t* Bf = reinterpret_cast<uint64_t*>(bs_smem);
+  __shared__ __align__(16) uint32_t cnt[CNT_WORDS];
+  __shared__ uint32_t wsum[BS_NW];
+  __shared__ uint64_t dbase[RS_BINS];
+  __shared__ uint32_t hist[RS_BINS];
+  const uint64_t lowmask = (1ull << lo_bits) - 1;
+  const uint32_t nbig = *n_big;
+  for (uint32_t q = blockIdx.x; q < nbig; q += gridDim.x) {
+    const uint32_t b = big[q];
+    const uint64_t s = bstart[b], e = bstart[b + 1], n = e - s;
+    const uint64_t top = ((k[s] & ((1ull << hbits) - 1)) >> lo_bits) << lo_bits;  // the bin's segment
+    for (uint64_t i = threadIdx.x; i < n; i += BS_NT) {
+      const uint64_t kk = k[s + i];
+      t0[s + i] = ((kk & lowmask) << 33) | ((uint64_t)v[s + i] << 1) | (kk >> 63);
+    }
+    __syncthreads();
+    uint64_t* src = t0 + s;
+    uint64_t* dst = t1 + s;
+    for (int sh = 0; sh < lo_bits; sh += RS_BITS) {
+      const int bits = min(RS_BITS, lo_bits - sh);
+      const uint32_t dmask = (1u << bits) - 1;
+      const int shift = 33 + sh;
+      for (int i = threadIdx.x; i < RS_BINS; i += BS_NT) hist[i] = 0;
+      __syncthreads();
+      for (uint64_t i = threadIdx.x; i < n; i += BS_NT) atomicAdd(&hist[(uint32_t)(src[i] >> shift) & dmask], 1u);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        uint64_t acc = 0;
+        for (int d = 0; d < RS_BINS; d++) { dbase[d] = acc; acc += hist[d]; }
+      }
+      __syncthreads();
+      for (uint64_t c0 = 0; c0 < n; c0 += BS_CAP) {
+        const int cn = (int)min((uint64_t)BS_CAP, n - c0);
+        uint64_t x[BS_IPT];
+        cta_load_striped(src + c0, cn, x);
+        cta_rank_scatter(x, cn, shift, dmask, Bf, cnt, wsum);
+        // Bf: the chunk sorted by digit; digit d's run starts at cnt[d * CNT_LD], its slot is dbase[d]
+        for (int i = threadIdx.x; i < cn; i += BS_NT) {
+          const uint64_t pv = Bf[i];
+          const uint32_t d = (uint32_t)(pv >> shift) & dmask;
+          dst[dbase[d] + (i - cnt[d * CNT_LD])] = pv;
+        }
+        __syncthreads();
+        if (threadIdx.x < RS_BINS) {  // advance by this chunk's count of digit threadIdx.x
+          const uint32_t d = threadIdx.x;
+          const uint32_t nxt = d + 1 < RS_BINS ? cnt[(d + 1) * CNT_LD] : (uint32_t)cn;
+          dbase[d] += nxt - cnt[d * CNT_LD];
+        }
+        __syncthreads();
+      }
+      uint64_t* t = src; src = dst; dst = t;
+    }
+    for (uint64_t i = threadIdx.x; i < n; i += BS_NT) {
+      const uint64_t pv = src[i];
+      k[s + i] = (top | (pv >> 33)) | ((pv & 1ull) << 63);
+      v[s + i] = (uint32_t)(pv >> 1);
+    }
+    __syncthreads();
   }
 }
 
@@ -532,31 +835,60 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
     uint64_t* k1 = scr.alloc<uint64_t>(n);
     uint32_t* v1 = scr.alloc<uint32_t>(n);
     const uint32_t ntiles = (uint32_t)((n + RS_TILE - 1) / RS_TILE);
-    uint32_t* hist = scr.alloc<uint32_t>((uint64_t)RS_BINS * ntiles);
-    uint64_t* goff = scr.alloc<uint64_t>((uint64_t)RS_BINS * ntiles);
+    uint32_t* hist = scr.alloc<uint32_t>((uint64_t)(1u << BIN_DIGIT) * ntiles);
+    uint64_t* goff = scr.alloc<uint64_t>((uint64_t)(1u << BIN_DIGIT) * ntiles);
     static bool attr = false;
     if (!attr) {
-      GOD_CUDA(cudaFuncSetAttribute(k_rs_scatter2, cudaFuncAttributeMaxDynamicSharedMemorySize, RS_DYN_SMEM));
+      GOD_CUDA(cudaFuncSetAttribute(k_rs_scatter2<RS_BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize, RS_DYN_SMEM));
+      GOD_CUDA(cudaFuncSetAttribute(k_rs_scatter2<BIN_DIGIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, RS_DYN_SMEM));
+      GOD_CUDA(cudaFuncSetAttribute(k_bin_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, BS_SMEM));
+      GOD_CUDA(cudaFuncSetAttribute(k_bucket_sort_big, cudaFuncAttributeMaxDynamicSharedMemorySize, BS_SMEM));
       attr = true;
     }
-    // LSD passes over the top min(2k, 32) hash bits, then a finishing pass for the low bits
     const int hbits = 2 * P.k;
-    const int lo = (hbits > 32 && getenv("GOD_SORT_FIXUP")) ? hbits - 32 : 0;  // default: full LSD
-    for (int shift = lo; shift < hbits; shift += RS_BITS) {
-      const int bits = min(RS_BITS, hbits - shift);
+    auto lsd_pass = [&](auto rb, int shift, int bits) {
+      constexpr int RB = decltype(rb)::value;
       const uint32_t dmask = (1u << bits) - 1;
-      GOD_LAUNCH("k_rs_hist", k_rs_hist, ntiles, RS_NT, 0, st, k0, n, shift, dmask, hist, ntiles);
-      scan_exclusive_u32_to_u64(hist, goff, (uint64_t)RS_BINS * ntiles, nullptr, st, scr);
-      GOD_LAUNCH("k_rs_scatter2", k_rs_scatter2, ntiles, RS2_NT, RS_DYN_SMEM, st, k0, v0, k1, v1, n, shift, dmask, goff,
-                 ntiles);
+      GOD_LAUNCH("k_rs_hist", k_rs_hist<RB>, ntiles, RS_NT, 0, st, k0, n, shift, dmask, hist, ntiles);
+      scan_exclusive_u32_to_u64(hist, goff, (uint64_t)(1u << RB) * ntiles, nullptr, st, scr);
+      GOD_LAUNCH("k_rs_scatter2", k_rs_scatter2<RB>, ntiles, RS2_NT, RS_DYN_SMEM, st, k0, v0, k1, v1, n, shift, dmask,
+                 goff, ntiles);
       std::swap(k0, k1);
       std::swap(v0, v1);
-    }
-    if (lo > 0) {
-      uint8_t* mark = scr.alloc<uint8_t>(n);
-      GOD_CUDA(cudaMemsetAsync(mark, 0, n, st));
-      GOD_LAUNCH("k_rs_fix_mark", k_rs_fix_mark, grid_for(n, 256), 256, 0, st, k0, n, lo, mark);
-      GOD_LAUNCH("k_rs_fix_sort", k_rs_fix_sort, grid_for(n, 256), 256, 0, st, k0, v0, n, lo, mark, k1, v1);
+    };
+    if (hbits >= 36 && hbits - SEG_BITS <= 30 && !getenv("GOD_SORT_FULL")) {
+      // K2 bin sort (see the comment above k_seg_hist)
+      const int L = hbits - SEG_BITS;
+      uint32_t* segc = scr.alloc<uint32_t>(1u << SEG_BITS);
+      uint2* table = scr.alloc<uint2>(1u << SEG_BITS);
+      uint32_t* n_bins_d = scr.alloc<uint32_t>(1);
+      GOD_CUDA(cudaMemsetAsync(segc, 0, (1u << SEG_BITS) * sizeof(uint32_t), st));
+      GOD_LAUNCH("k_seg_hist", k_seg_hist, 4u * num_sms(), 512, 0, st, k0, n, L, segc);
+      const uint32_t target = (uint32_t)std::max<uint64_t>(BIN_TARGET, n / ((1u << (2 * BIN_DIGIT)) - (1u << SEG_BITS)) + 1);
+      GOD_LAUNCH("k_seg_table", k_seg_table, 1, 1024, 0, st, segc, target, table, n_bins_d);
+      GOD_LAUNCH("k_seg_assign", k_seg_assign, grid_for(n, 256), 256, 0, st, k0, n, L, hbits, table);
+      lsd_pass(std::integral_constant<int, BIN_DIGIT>(), hbits, BIN_DIGIT);
+      lsd_pass(std::integral_constant<int, BIN_DIGIT>(), hbits + BIN_DIGIT, BIN_DIGIT);
+      const uint32_t nb = d2h_scalar(n_bins_d, st);
+      uint64_t* bstart = scr.alloc<uint64_t>((uint64_t)nb + 1);
+      uint32_t* big = scr.alloc<uint32_t>(nb ? nb : 1);
+      uint32_t* n_big = scr.alloc<uint32_t>(2);
+      GOD_CUDA(cudaMemsetAsync(n_big, 0, 2 * sizeof(uint32_t), st));
+      GOD_LAUNCH("k_bucket_bounds", k_bucket_bounds, grid_for((uint64_t)nb + 1, 256), 256, 0, st, k0, n, hbits, nb,
+                 bstart);
+      GOD_LAUNCH("k_bin_sort", k_bin_sort, 2u * num_sms(), BS_NT, BS_SMEM, st, k0, v0, bstart, n_bins_d, L, hbits, big,
+                 n_big);
+      const uint32_t hb_big = d2h_scalar(n_big, st);
+      if (getenv("GOD_DEBUG_BUCKETS"))
+        fprintf(stderr, "[bins] n=%llu bins=%u target=%u big=%u lsd=%u\n", (unsigned long long)n, nb, target, hb_big,
+                d2h_scalar(n_big + 1, st));
+      if (hb_big)
+        GOD_LAUNCH("k_bucket_sort_big", k_bucket_sort_big, std::min(hb_big, (uint32_t)num_sms()), BS_NT, BS_SMEM, st, k0,
+                   v0, /*t0=*/k1, /*t1=*/k0, bstart, big, n_big, L, hbits);
+    } else {
+      // K2 full stable LSD over the 2k hash bits (position order kept within equal hashes)
+      for (int shift = 0; shift < hbits; shift += RS_BITS)
+        lsd_pass(std::integral_constant<int, RS_BITS>(), shift, std::min(RS_BITS, hbits - shift));
     }
   }
   // K3: distinct hashes
