@@ -160,13 +160,29 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------------ roofline
+# Algorithmic integer operations per k-mer start position of the fused extraction:
+# the oracle's arithmetic (oracle.c or_minimizers / or_hash) mapped onto a 32-bit ALU, one op per
+# 32-bit instruction: base code 1, forward k-mer update 6, reverse-complement update 7, canonical
+# compare + select 4, strand/palindrome test 1, masked Wang hash 23 x 2 = 46, window minimum
+# (van Herk: prefix min, suffix min, combine on 64-bit keys) 12 -> 77.
+ALU_OPS_PER_POS = 77
+EXTRACT_KERNELS = ("extract_ref", "extract_phase", "extract_seed")
+
+
+def alu_peak_tops(peaks: dict) -> float:
+    """Integer-op issue peak: 148 SMs x 4 SMSPs x 32 lanes (one warp instruction per SMSP per clock;
+    alu pipe 16 lanes/clk + fma pipe (IMAD) 16 lanes/clk per SMSP) x the max SM clock."""
+    mhz = float(peaks.get("sm_max_mhz", 1965.0))
+    return 148 * 4 * 32 * mhz * 1e6 / 1e12
+
+
 def algorithmic_bytes(name: str, ctx: dict):
     """Algorithmic bytes per LAUNCH of the named kernel (DESIGN.md §5 table): what the method must
     move, not what a kernel happens to touch."""
     n_ref_mz = ctx["n_entries_all"]
     if name == "extract_ref":      # read every reference byte once; write 12 B per minimizer (u64 hash|strand, u32 pos)
         return ctx["ref_bytes"] + 12 * n_ref_mz
-    if name == "k_rs_scatter":     # read + write one 12-B record per pass
+    if name in ("k_rs_scatter2", "k_bin_sort"):  # read + write one 12-B record per pass / per bin sort
         return 24 * n_ref_mz
     if name == "k_rs_hist":
         return 8 * n_ref_mz
@@ -177,19 +193,48 @@ def algorithmic_bytes(name: str, ctx: dict):
     return None
 
 
-def pick_roofline(prof: dict, steps: int, ctx: dict, peak_gbs: float):
-    # dominant kernel = largest share of device time in the timed region
+def load_traffic():
+    """ncu-measured DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum from one
+    `ncu --set full` capture) of the kernels profiled this round, written by tools/ncu_traffic.py."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic_r01.json")
+    if not os.path.exists(p):
+        return {}
+    try:
+        return json.load(open(p))
+    except Exception:
+        return {}
+
+
+def pick_roofline(prof: dict, ctx: dict, peaks: dict, units: dict):
+    """Roofline of the dominant kernel (largest share of device time in the timed region)."""
     items = sorted(prof.items(), key=lambda kv: -kv[1][0])
     total_ms = sum(v[0] for v in prof.values())
+    peak_gbs = float(peaks.get("hbm_gbs", 6650.0))
+    traffic = load_traffic()
     for name, (ms, n) in items:
+        avg_s = ms / n / 1e3
         b = algorithmic_bytes(name, ctx)
+        tr = traffic.get(name, {})
+        common = {"kernel": name, "share_of_step": round(ms / total_ms, 4), "avg_launch_ms": round(avg_s * 1e3, 4),
+                  "traffic": tr.get("dram_bytes_per_launch"), "traffic_source": tr.get("source")}
+        if name in EXTRACT_KERNELS and units.get(name):
+            pos = units[name] / n
+            ops = ALU_OPS_PER_POS * pos
+            ach = ops / avg_s / 1e12
+            pk = alu_peak_tops(peaks)
+            out = {"bound": "alu", "achieved": round(ach, 3), "peak": round(pk, 2), "unit": "Tops/s",
+                   "frac": round(ach / pk, 4), **common, "positions_per_launch": int(pos),
+                   "algorithmic_ops_per_position": ALU_OPS_PER_POS,
+                   "peak_source": "DESIGN.md §5: 148 SM x 128 int32 lanes/clk x sm_max_mhz (G0 measured 31.35 Tops/s)"}
+            if b is not None:
+                out["hbm_view"] = {"achieved_gbs": round(b / avg_s / 1e9, 1), "peak_gbs": peak_gbs,
+                                   "frac": round(b / avg_s / 1e9 / peak_gbs, 4), "algorithmic_bytes_per_launch": int(b)}
+            return out
         if b is None:
             continue
-        avg_s = ms / n / 1e3
         ach = b / avg_s / 1e9
-        return {"kernel": name, "bound": "hbm", "achieved": round(ach, 1), "peak": peak_gbs, "unit": "GB/s",
-                "frac": round(ach / peak_gbs, 4), "traffic": None, "share_of_step": round(ms / total_ms, 4),
-                "avg_launch_ms": round(avg_s * 1e3, 4), "algorithmic_bytes_per_launch": int(b),
+        return {"bound": "hbm", "achieved": round(ach, 1), "peak": peak_gbs, "unit": "GB/s",
+                "frac": round(ach / peak_gbs, 4), **common, "algorithmic_bytes_per_launch": int(b),
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, measured)"}
     return None
 
@@ -293,6 +338,7 @@ def main():
     god.profile_enable(False)
     launches = god.launch_count() - launches0
     prof = god.profile_query()
+    units = {kname: god.profile_units(kname) for kname in EXTRACT_KERNELS}
     elapsed_ms = start.elapsed_time(end)
     build_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in evs]))
     seed_ms = float(np.mean([e[1].elapsed_time(e[2]) for e in evs]))
@@ -304,11 +350,10 @@ def main():
     hz, _, _, _ = god.god_minimizers(dreads, droffs, pattern, k, w, phases=None)  # phase-0 read minimizers (approx.)
     n_read_mz = int(hz.shape[0])
     del hz
-    peaks = json.load(open(PEAKS)) if os.path.exists(PEAKS) else {"hbm_gbs": 6650.0}
-    peak_gbs = float(peaks.get("hbm_gbs", 6650.0))
+    peaks = json.load(open(PEAKS)) if os.path.exists(PEAKS) else {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}
     ctx = {"ref_bytes": int(cfg.ref.size), "read_bytes": int(cfg.reads.seq.size), "n_entries_all": st["n_entries_all"],
            "n_read_mz": n_read_mz, "n_phase_mz": n_read_mz * 2}
-    roof = pick_roofline(prof, args.steps, ctx, peak_gbs)
+    roof = pick_roofline(prof, ctx, peaks, units)
     kernels = {kname: {"ms_per_step": round(ms / args.steps, 4), "launches_per_step": n // args.steps}
                for kname, (ms, n) in sorted(prof.items(), key=lambda kv: -kv[1][0])}
 

@@ -157,11 +157,15 @@ GOD_API god_status god_seed_reads(const god_index* idx, const uint8_t* reads, co
  * synchronizes on the pending events and returns, per kernel name (in first-launch order), the
  * accumulated milliseconds and launch count: names are written NUL-separated into `names`
  * (capacity names_len bytes), ms[i] and launches[i] for i < return value (<= max_entries).
- * god_launch_count() counts every kernel launch of the library since load (always on). */
+ * god_launch_count() counts every kernel launch of the library since load (always on).
+ * god_profile_units(name) returns the work units recorded for the launches named `name` while
+ * profiling was on: for the extraction launches ("extract_ref", "extract_phase", "extract_seed")
+ * the number of k-mer start positions processed (sum of n_k over the jobs); 0 for other names. */
 GOD_API void god_profile_enable(int on);
 GOD_API void god_profile_reset(void);
 GOD_API int god_profile_query(char* names, size_t names_len, double* ms, uint64_t* launches, int max_entries);
 GOD_API uint64_t god_launch_count(void);
+GOD_API uint64_t god_profile_units(const char* name);
 
 #ifdef __cplusplus
 }

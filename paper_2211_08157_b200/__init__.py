@@ -248,6 +248,12 @@ def profile_query() -> dict:
     return {nm.decode(): (ms[i], int(ln[i])) for i, nm in enumerate(names)}
 
 
+def profile_units(name: str) -> int:
+    """Work units recorded for the launches named `name` since the last reset (extraction launches:
+    k-mer start positions processed)."""
+    return int(_lib.load().god_profile_units(name.encode()))
+
+
 def launch_count() -> int:
     return int(_lib.load().god_launch_count())
 

@@ -35,7 +35,8 @@ class GodIndexStats(ctypes.Structure):
 # every symbol include/god.h declares (tests/test_abi.py checks header <-> library agreement)
 EXPORTS = ("god_last_error", "god_version", "god_sparsify", "god_minimizers", "god_build_index",
            "god_index_get_stats", "god_index_dump", "god_index_count", "god_index_free", "god_seed_reads",
-           "god_profile_enable", "god_profile_reset", "god_profile_query", "god_launch_count")
+           "god_profile_enable", "god_profile_reset", "god_profile_query", "god_launch_count",
+           "god_profile_units")
 
 _lib = None
 
@@ -67,6 +68,8 @@ def load():
     L.god_profile_reset.restype = None
     L.god_profile_query.argtypes = [vp, ctypes.c_size_t, vp, vp, ctypes.c_int]
     L.god_profile_query.restype = ctypes.c_int
+    L.god_profile_units.argtypes = [ctypes.c_char_p]
+    L.god_profile_units.restype = ctypes.c_uint64
     L.god_launch_count.argtypes = []
     L.god_launch_count.restype = u64
     for name in ("god_sparsify", "god_minimizers", "god_build_index", "god_index_get_stats", "god_index_dump",

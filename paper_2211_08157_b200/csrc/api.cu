@@ -26,7 +26,7 @@ int num_sms() {
 // ---------------------------------------------------------------------------------- tracing
 namespace {
 struct ProfPending { const char* name; cudaEvent_t a, b; };
-struct ProfAcc { double ms = 0; uint64_t n = 0; };
+struct ProfAcc { double ms = 0; uint64_t n = 0; uint64_t units = 0; };
 std::mutex g_prof_mu;
 bool g_prof_on = false;
 std::atomic<uint64_t> g_launches{0};
@@ -64,6 +64,18 @@ void prof_flush_locked() {
   g_pending.clear();
 }
 }  // namespace
+
+void prof_add_units(const char* name, uint64_t units) {
+  if (!g_prof_on) return;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  prof_flush_locked();
+  auto it = g_acc.find(name);
+  if (it == g_acc.end()) {
+    g_order.push_back(name);
+    it = g_acc.emplace(name, ProfAcc{}).first;
+  }
+  it->second.units += units;
+}
 
 ProfScope::ProfScope(const char* n, cudaStream_t s) : name(n), st(s) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -240,6 +252,11 @@ GOD_API int god_profile_query(char* names, size_t names_len, double* ms, uint64_
   return n;
 }
 GOD_API uint64_t god_launch_count(void) { return g_launches.load(); }
+GOD_API uint64_t god_profile_units(const char* name) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  auto it = g_acc.find(name ? name : "");
+  return it == g_acc.end() ? 0 : it->second.units;
+}
 
 GOD_API god_status god_sparsify(const god_params* prm, const uint8_t* seq, const uint64_t* offsets, uint32_t n_seqs,
                                 const uint8_t* phases, uint64_t* packed, uint64_t* nmask, uint64_t* out_offsets,

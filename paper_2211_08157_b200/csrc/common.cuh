@@ -213,6 +213,9 @@ struct ProfScope {
   ProfScope(const char* n, cudaStream_t s);
   ~ProfScope();
 };
+// Work units (e.g. k-mer start positions) processed by the launches named `name`, reported by
+// god_profile_units for the roofline of bench.py (recorded only while profiling is on).
+void prof_add_units(const char* name, uint64_t units);
 #define GOD_LAUNCH(NAME, KERNEL, GRID, BLOCK, SMEM, ST, ...)      \
   do {                                                           \
     ::god::ProfScope ps_(NAME, ST);                              \

@@ -302,6 +302,7 @@ void run_extract(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const 
   }
   const uint64_t ntiles = (total_pos + EX_T - 1) / EX_T;
   GOD_REQUIRE(ntiles < 0x7FFFFFFFull, "input too large for one extraction launch");
+  prof_add_units(tag, total_pos - n_jobs);  // kb = exclusive scan of nk + 1 (one separator per job)
   const int E = EX_T + 2 * (P.w - 1);
   const size_t smem = (size_t)E * (4 * sizeof(uint64_t) + sizeof(uint32_t) + 1);
   static bool attr_set = false;

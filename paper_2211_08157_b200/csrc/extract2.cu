@@ -621,13 +621,18 @@ __global__ void k_x2_tile_jobs(const uint64_t* __restrict__ kb, uint32_t n_jobs,
 }
 
 // padded position bases (multiple of W) and code-word bases per job
-__global__ void k_x2_sizes(const Job* __restrict__ jobs, uint32_t n, int K, int W, uint64_t* kb, uint64_t* cw) {
+__global__ void k_x2_sizes(const Job* __restrict__ jobs, uint32_t n, int K, int W, uint64_t* kb, uint64_t* cw,
+                           unsigned long long* nk_sum) {
+  uint64_t acc = 0;
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
     const uint64_t nk = jobs[j].nk;
     kb[j] = (nk ? (nk + W - 1) / W : 1) * W;  // no separator: job boundaries are handled in-kernel
     const uint64_t ncode = nk ? nk + K - 1 : 0;
     cw[j] = (ncode + 15) / 16;
+    acc += nk;
   }
+  for (int d = 16; d; d >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, d);
+  if ((threadIdx.x & 31) == 0 && acc) atomicAdd(nk_sum, (unsigned long long)acc);
 }
 
 template <int K, int W, int PS>
@@ -665,16 +670,19 @@ bool run_extract2(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const
   // padded layouts
   uint64_t* kb = scr.alloc<uint64_t>(n_jobs + 1);
   uint64_t* cw = scr.alloc<uint64_t>(n_jobs + 1);
-  uint64_t* tot = scr.alloc<uint64_t>(2);
-  GOD_LAUNCH("k_x2_sizes", k_x2_sizes, grid_for(n_jobs, 256), 256, 0, st, jobs, n_jobs, K, W, kb, cw);
+  uint64_t* tot = scr.alloc<uint64_t>(3);
+  GOD_CUDA(cudaMemsetAsync(tot + 2, 0, sizeof(uint64_t), st));
+  GOD_LAUNCH("k_x2_sizes", k_x2_sizes, grid_for(n_jobs, 256), 256, 0, st, jobs, n_jobs, K, W, kb, cw,
+             reinterpret_cast<unsigned long long*>(tot + 2));
   scan_exclusive_u64(kb, kb, n_jobs, tot, st, scr);
   scan_exclusive_u64(cw, cw, n_jobs, tot + 1, st, scr);
   GOD_CUDA(cudaMemcpyAsync(kb + n_jobs, tot, sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
   GOD_CUDA(cudaMemcpyAsync(cw + n_jobs, tot + 1, sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
-  uint64_t htot[2];
+  uint64_t htot[3];
   GOD_CUDA(cudaMemcpyAsync(htot, tot, sizeof(htot), cudaMemcpyDeviceToHost, st));
   GOD_CUDA(cudaStreamSynchronize(st));
   const uint64_t total_pos = htot[0];
+  prof_add_units(tag, htot[2]);
   const uint64_t total_blocks = total_pos / W;
   const uint64_t ntiles = (total_blocks + X2_OUT_BLOCKS - 1) / X2_OUT_BLOCKS;
   GOD_REQUIRE(ntiles < 0x7FFFFFFFull, "input too large for one extraction launch");
