@@ -6,9 +6,9 @@
 //
 // Layout.  Each job's k-mer starts are padded to a multiple of W positions (the pad slots are
 // window barriers), so a W-block never straddles two jobs; each job's patterned bases are packed
-// 16 per u32 word, MSB-first, starting on a fresh word.  A CTA of 256 threads owns 256 W-blocks
-// (thread t = block t); blocks 0 and 255 are halo (computed, not emitted), so consecutive tiles
-// overlap by two blocks.
+// 16 per u32 word, MSB-first, starting on a fresh word.  A tile of X2_NT = 128 threads owns 128
+// W-blocks (thread t = block t); blocks 0 and 127 are halo (computed, not emitted), so consecutive
+// tiles overlap by two blocks.  CTAs are persistent (occupancy x SMs) and take tiles in order.
 //   A. sparsify: the tile's code words are built once in SMEM straight from the ASCII bytes
 //      (PRMT gathers the included bytes, SIMD 2-bit encode, an IMAD packs 4 codes, a 256-entry
 //      SMEM table of expected letters detects any non-ACGT byte exactly).
