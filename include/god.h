@@ -76,8 +76,8 @@ typedef struct {
     uint64_t tau;              /* keep iff count <= tau */
     uint64_t kept_entries, dropped_entries, kept_distinct, dropped_distinct;
     uint32_t k, w, p, x;       /* parameters the index was built with */
-    uint32_t dir_bits;         /* B: directory = top B bits of the 2k-bit hash */
-    uint32_t reserved;
+    uint32_t dir_bits;         /* mode 0: B, directory = top B bits of the 2k-bit hash; mode 1: floor(log2 slots) */
+    uint32_t dir_mode;         /* 0: top-bit directory; 1: data-sized slot map over the top 12 hash bits */
 } god_index_stats;
 
 /* One seed match ("finds exact matches of minimizers in the reference genome by querying

@@ -147,7 +147,7 @@ class GodIndex:
     def stats(self) -> dict:
         st = _lib.GodIndexStats()
         _lib.check(_lib.load().god_index_get_stats(self._h, ctypes.byref(st)))
-        return {f: int(getattr(st, f)) for f, _ in _lib.GodIndexStats._fields_ if f != "reserved"}
+        return {f: int(getattr(st, f)) for f, _ in _lib.GodIndexStats._fields_}
 
     def dump(self, device: bool = False):
         """Kept entries in (hash, pos) order -> (hash u64, pos u32, strand u8)."""

@@ -29,7 +29,7 @@ STATS_FIELDS = ("n_entries_all", "n_distinct_all", "m", "tau", "kept_entries", "
 class GodIndexStats(ctypes.Structure):
     _fields_ = [(f, ctypes.c_uint64) for f in STATS_FIELDS] + [
         ("k", ctypes.c_uint32), ("w", ctypes.c_uint32), ("p", ctypes.c_uint32), ("x", ctypes.c_uint32),
-        ("dir_bits", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
+        ("dir_bits", ctypes.c_uint32), ("dir_mode", ctypes.c_uint32)]
 
 
 # every symbol include/god.h declares (tests/test_abi.py checks header <-> library agreement)

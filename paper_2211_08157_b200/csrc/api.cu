@@ -400,8 +400,8 @@ GOD_API void god_index_free(god_index* idx) {
   // the arrays come from the stream-ordered pool: wait for all users, then return them in order
   cudaDeviceSynchronize();
   if (idx->dir) cudaFreeAsync(idx->dir, 0);
-  if (idx->ent_key) cudaFreeAsync(idx->ent_key, 0);
-  if (idx->ent_pos) cudaFreeAsync(idx->ent_pos, 0);
+  if (idx->ent) cudaFreeAsync(idx->ent, 0);
+  if (idx->seg) cudaFreeAsync(idx->seg, 0);
   cudaStreamSynchronize(0);
   delete idx;
 }

@@ -687,29 +687,27 @@ __global__ void k_kept(const uint32_t* __restrict__ count, uint64_t nd, CutState
 __global__ void k_write_entries(const uint64_t* __restrict__ hz, const uint32_t* __restrict__ pos, uint64_t n, const uint32_t* __restrict__ flag,
                                 const uint64_t* __restrict__ dix, const uint64_t* __restrict__ dstart,
                                 const uint32_t* __restrict__ count, const uint64_t* __restrict__ kept_off,
-                                const CutState* cs, uint32_t low_bits, uint32_t* ent_key, uint32_t* ent_pos,
-                                uint32_t* kslot) {
+                                const CutState* cs, IndexView iv, uint64_t* ent, uint32_t* kslot) {
   const uint64_t tau = cs->tau;
-  const uint64_t lowmask = (1ull << low_bits) - 1;
+  const uint64_t lowmask = (1ull << iv.low_bits) - 1;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t d = dix[i] + flag[i] - 1;  // run index: exclusive scan of heads counts its own head for non-heads
     if (count[d] > tau) continue;
     const uint64_t e = kept_off[d] + (i - dstart[d]);
     const uint64_t v = hz[i];
     const uint64_t h = v & HASH_BITS_MASK;
-    ent_key[e] = (uint32_t)(((h & lowmask) << 1) | (v >> 63));
-    ent_pos[e] = pos[i];
-    kslot[e] = (uint32_t)(h >> low_bits);
+    ent[e] = ((uint64_t)pos[i] << 32) | ((h & lowmask) << 1) | (v >> 63);
+    kslot[e] = (uint32_t)index_slot(iv, h);
   }
 }
 
 // K6a: dir[slot] = first kept entry of each non-empty slot (dir pre-filled with ~0; dir[2^B] = n_kept)
-__global__ void k_dir_mark(const uint32_t* __restrict__ kslot, uint64_t n_kept, uint32_t dir_bits, uint32_t* dir) {
+__global__ void k_dir_mark(const uint32_t* __restrict__ kslot, uint64_t n_kept, uint64_t n_slots, uint32_t* dir) {
   for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < n_kept; e += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t s = kslot[e];
     if (e == 0 || kslot[e - 1] != s) dir[s] = (uint32_t)e;
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) dir[1ull << dir_bits] = (uint32_t)n_kept;
+  if (blockIdx.x == 0 && threadIdx.x == 0) dir[n_slots] = (uint32_t)n_kept;
 }
 
 // K6b: empty slots take the next non-empty slot's first entry: a suffix-min over dir[0 .. 2^B],
@@ -795,20 +793,34 @@ __global__ void k_count_queries(god::IndexView v, const uint64_t* __restrict__ h
   }
 }
 
+__global__ void k_dir_pairs(const uint32_t* __restrict__ d1, uint64_t n_slots, uint2* dir) {
+  for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < n_slots; s += (uint64_t)gridDim.x * blockDim.x)
+    dir[s] = make_uint2(d1[s], d1[s + 1]);
+}
+
 __global__ void k_dump(god::IndexView v, uint64_t* hash, uint32_t* pos, uint8_t* strand) {
-  const uint64_t nslots = 1ull << v.dir_bits;
   for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < v.n_kept; e += (uint64_t)gridDim.x * blockDim.x) {
     // slot = largest s with dir[s] <= e
-    uint64_t lo = 0, hi = nslots - 1;
+    uint64_t lo = 0, hi = v.n_slots - 1;
     while (lo < hi) {
       uint64_t mid = (lo + hi + 1) >> 1;
-      if (v.dir[mid] <= e) lo = mid;
+      if (v.dir[mid].x <= e) lo = mid;
       else hi = mid - 1;
     }
-    const uint32_t kk = v.ent_key[e];
-    if (hash) hash[e] = (lo << v.low_bits) | (kk >> 1);
-    if (pos) pos[e] = v.ent_pos[e];
-    if (strand) strand[e] = kk & 1u;
+    uint64_t top = lo;
+    if (v.seg) {  // mode 1: the segment whose slot range holds slot lo = the largest t with seg[t].x <= lo
+      uint32_t a = 0, b = (1u << DIR_SEG_BITS) - 1;
+      while (a < b) {
+        const uint32_t mid = (a + b + 1) >> 1;
+        if (v.seg[mid].x <= lo) a = mid;
+        else b = mid - 1;
+      }
+      top = a;
+    }
+    const uint64_t en = v.ent[e];
+    if (hash) hash[e] = (top << v.low_bits) | ((uint32_t)en >> 1);
+    if (pos) pos[e] = (uint32_t)(en >> 32);
+    if (strand) strand[e] = (uint8_t)(en & 1u);
   }
 }
 
@@ -831,6 +843,7 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
   // K2: stable LSD radix sort on the 2k hash bits
   uint64_t* k0 = rec.hz;
   uint32_t* v0 = rec.pos;
+  uint32_t* segc = nullptr;  // records per top-12-bit hash segment (bin sort and directory map)
   if (n > 1) {
     uint64_t* k1 = scr.alloc<uint64_t>(n);
     uint32_t* v1 = scr.alloc<uint32_t>(n);
@@ -859,7 +872,7 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
     if (hbits >= 36 && hbits - SEG_BITS <= 30 && !getenv("GOD_SORT_FULL")) {
       // K2 bin sort (see the comment above k_seg_hist)
       const int L = hbits - SEG_BITS;
-      uint32_t* segc = scr.alloc<uint32_t>(1u << SEG_BITS);
+      segc = scr.alloc<uint32_t>(1u << SEG_BITS);
       uint2* table = scr.alloc<uint2>(1u << SEG_BITS);
       uint32_t* n_bins_d = scr.alloc<uint32_t>(1);
       GOD_CUDA(cudaMemsetAsync(segc, 0, (1u << SEG_BITS) * sizeof(uint32_t), st));
@@ -929,17 +942,38 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
   GOD_CUDA(cudaMemcpyAsync(&n_kept, kept_tot, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
   GOD_CUDA(cudaStreamSynchronize(st));
   GOD_REQUIRE(n_kept < 0xFFFFFFFFull, "index has >= 2^32 kept entries");
-  // directory bits: ~1-2 kept entries per slot (measured best for the probe kernels: a probe is one
-  // directory sector + one key sector); the low hash bits must fit 31 bits next to the strand bit
+  // K6 directory.  mode 1 (2k - 12 in [2, 30]): data-sized monotone slot map over the top-12-bit
+  // segments, ~DIR_TARGET entries per slot (minimizer hashes are skewed toward small values, and so
+  // are the probes; a fixed hash-bit prefix leaves ~20 entries in the dense slots).  mode 0: the top
+  // B hash bits, B = clamp(floor(log2 n_kept), 2k - 31, min(2k, 28)).
   const uint32_t hb = 2 * P.k;
-  const uint32_t lg = floor_log2(n_kept ? n_kept : 1);
-  const char* bdbg = getenv("GOD_DIR_SLACK");
-  const uint32_t slack = bdbg ? (uint32_t)atoi(bdbg) : 0u;
-  uint32_t B = lg > slack ? lg - slack : 0;
-  const uint32_t Bmin = hb > 31 ? hb - 31 : 0;
-  const uint32_t Bmax = hb < 28 ? hb : 28;
-  B = B < Bmin ? Bmin : (B > Bmax ? Bmax : B);
-  const uint32_t low_bits = hb - B;
+  const bool mode1 = hb >= 14 && hb - DIR_SEG_BITS <= 30 && !getenv("GOD_DIR_MODE0");
+  constexpr uint32_t DIR_TARGET = 2;
+  uint32_t B = 0, low_bits = 0;
+  uint64_t n_slots = 0;
+  uint2* seg = nullptr;
+  if (mode1) {
+    if (!segc) {
+      segc = scr.alloc<uint32_t>(1u << SEG_BITS);
+      GOD_CUDA(cudaMemsetAsync(segc, 0, (1u << SEG_BITS) * sizeof(uint32_t), st));
+      if (n) GOD_LAUNCH("k_seg_hist", k_seg_hist, 4u * num_sms(), 512, 0, st, k0, n, (int)(hb - SEG_BITS), segc);
+    }
+    GOD_CUDA(cudaMallocAsync((void**)&seg, (1u << SEG_BITS) * sizeof(uint2), st));
+    uint32_t* ns_d = scr.alloc<uint32_t>(1);
+    GOD_LAUNCH("k_seg_table", k_seg_table, 1, 1024, 0, st, segc, DIR_TARGET, seg, ns_d);
+    n_slots = d2h_scalar(ns_d, st);
+    if (n_slots == 0) n_slots = 1;
+    low_bits = hb - DIR_SEG_BITS;
+    B = floor_log2(n_slots);
+  } else {
+    const uint32_t lg = floor_log2(n_kept ? n_kept : 1);
+    B = lg;
+    const uint32_t Bmin = hb > 31 ? hb - 31 : 0;
+    const uint32_t Bmax = hb < 28 ? hb : 28;
+    B = B < Bmin ? Bmin : (B > Bmax ? Bmax : B);
+    low_bits = hb - B;
+    n_slots = 1ull << B;
+  }
   ix->st.n_entries_all = n;
   ix->st.n_distinct_all = nd;
   ix->st.m = hcs.m;
@@ -949,26 +983,31 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
   ix->st.kept_distinct = hcs.kept_distinct;
   ix->st.dropped_distinct = nd - hcs.kept_distinct;
   ix->st.dir_bits = B;
+  ix->st.dir_mode = mode1 ? 1u : 0u;
   ix->st_alloc = st;
-  GOD_CUDA(cudaMallocAsync((void**)&ix->dir, ((1ull << B) + 1) * sizeof(uint32_t), st));
-  GOD_CUDA(cudaMallocAsync((void**)&ix->ent_key, (n_kept ? n_kept : 1) * sizeof(uint32_t), st));
-  GOD_CUDA(cudaMallocAsync((void**)&ix->ent_pos, (n_kept ? n_kept : 1) * sizeof(uint32_t), st));
+  ix->seg = seg;
+  ix->low_bits = low_bits;
+  ix->n_slots = n_slots;
+  GOD_CUDA(cudaMallocAsync((void**)&ix->dir, n_slots * sizeof(uint2), st));
+  uint32_t* dir1 = scr.alloc<uint32_t>(n_slots + 1);  // first entry per slot (+ n_kept), then pairs
+  GOD_CUDA(cudaMallocAsync((void**)&ix->ent, (n_kept ? n_kept : 1) * sizeof(uint64_t), st));
   uint32_t* kslot = scr.alloc<uint32_t>(n_kept);
   if (n) {
-    GOD_LAUNCH("k_write_entries", k_write_entries, grid_for(n, 256), 256, 0, st, k0, v0, n, flag, dix, dstart, count, kept_off, cs, low_bits, ix->ent_key,
-                                                     ix->ent_pos, kslot);
+    GOD_LAUNCH("k_write_entries", k_write_entries, grid_for(n, 256), 256, 0, st, k0, v0, n, flag, dix, dstart, count,
+               kept_off, cs, ix->view(), ix->ent, kslot);
   }
   {
-    const uint64_t nd1 = (1ull << B) + 1;
-    GOD_CUDA(cudaMemsetAsync(ix->dir, 0xFF, nd1 * sizeof(uint32_t), st));
+    const uint64_t nd1 = n_slots + 1;
+    GOD_CUDA(cudaMemsetAsync(dir1, 0xFF, nd1 * sizeof(uint32_t), st));
     GOD_LAUNCH("k_dir_mark", k_dir_mark, min(grid_for(n_kept ? n_kept : 1, 256), 16u * num_sms()), 256, 0, st, kslot,
-               n_kept, B, ix->dir);
+               n_kept, n_slots, dir1);
     const uint64_t nt = (nd1 + DF_TILE - 1) / DF_TILE;
     uint64_t* dst = scr.alloc<uint64_t>(nt);
     uint32_t* dctr = scr.alloc<uint32_t>(1);
     GOD_CUDA(cudaMemsetAsync(dst, 0, nt * sizeof(uint64_t), st));
     GOD_CUDA(cudaMemsetAsync(dctr, 0, sizeof(uint32_t), st));
-    GOD_LAUNCH("k_dir_suffix_min", k_dir_suffix_min, (unsigned)nt, DF_NT, 0, st, ix->dir, nd1, dst, dctr);
+    GOD_LAUNCH("k_dir_suffix_min", k_dir_suffix_min, (unsigned)nt, DF_NT, 0, st, dir1, nd1, dst, dctr);
+    GOD_LAUNCH("k_dir_pairs", k_dir_pairs, grid_for(n_slots, 256), 256, 0, st, dir1, n_slots, ix->dir);
   }
   GOD_CUDA(cudaStreamSynchronize(st));
   if (const char* dd = getenv("GOD_DEBUG_DIR")) {  // developer aid: dump the intermediates
@@ -982,7 +1021,7 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
     dump("rec_hz", rec.hz, n * 8); dump("sorted_hz", k0, n * 8); dump("sorted_pos", v0, n * 4);
     dump("flag", flag, n * 4); dump("dix", dix, n * 8); dump("dstart", dstart, (nd + 1) * 8);
     dump("count", count, nd * 4); dump("kept_off", kept_off, nd * 8); dump("kslot", kslot, n_kept * 4);
-    dump("ent_key", ix->ent_key, n_kept * 4); dump("dir", ix->dir, ((1ull << B) + 1) * 4);
+    dump("ent", ix->ent, n_kept * 8); dump("dir", ix->dir, n_slots * 8);
   }
 }
 

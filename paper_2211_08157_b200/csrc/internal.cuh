@@ -55,35 +55,74 @@ JobSet make_jobs(const Params& P, const uint64_t* offsets, uint32_t n_seqs, cons
 
 // ------------------------------------------------------------------------------------ index
 // Device view of the seed index (P:286 (3): key = hash, value = sorted start locations).
-// dir[s] (s < 2^B, plus dir[2^B] = n_kept): first kept entry whose hash has top-B bits >= s.
-// ent_key[e] = (low (2k-B) hash bits) << 1 | strand; ent_pos[e] = global start position.
+// ent[e] = pos << 32 | low_hash << 1 | strand, entries in (hash, pos) order.
+// dir[s] = {first, end} kept-entry range of slot s (s < n_slots).
+// Slot of a hash:
+//   mode 0: the top B = dir_bits hash bits (low_bits = 2k - B);
+//   mode 1 (seg != null): data-sized and monotone: segment t = top DIR_SEG_BITS hash bits,
+//           slot = seg[t].x + floor(low(h) * seg[t].y / 2^low_bits), low_bits = 2k - DIR_SEG_BITS,
+//           seg[t].y ~ (entries in segment t) / 2, so slots hold ~2 entries however skewed the
+//           minimizer hashes are (they are window minima: dense at small values).
+constexpr int DIR_SEG_BITS = 12;
 struct IndexView {
-  const uint32_t* dir;
-  const uint32_t* ent_key;
-  const uint32_t* ent_pos;
+  const uint2* dir;
+  const uint64_t* ent;
+  const uint2* seg;
   uint32_t dir_bits;
-  uint32_t low_bits;     // 2k - B
+  uint32_t low_bits;
   uint64_t n_kept;
+  uint64_t n_slots;
 };
 
+// slot of hash h; ~0 if h lies in a segment without slots (mode 1: no reference minimizer there)
+__device__ __forceinline__ uint64_t index_slot(const IndexView& v, uint64_t h) {
+  if (v.seg) {
+    const uint2 t = __ldg(v.seg + (h >> v.low_bits));
+    if (!t.y) return ~0ull;
+    return t.x + (((h & ((1ull << v.low_bits) - 1)) * t.y) >> v.low_bits);
+  }
+  return h >> v.low_bits;
+}
+
 // [begin, end) of the kept entries whose hash == h ("examines the presence of the extracted
-// minimizers (their hash values) in the seed index"): directory slot = top B bits, then a binary
-// search on the low bits inside the slot (entries are in (hash, pos) order).
+// minimizers (their hash values) in the seed index").  One 8-byte directory load gives the slot's
+// range; a slot of <= 4 entries (the common case) is resolved with independent loads (one round
+// trip), a longer one by binary search plus a scan over the matches.
 __device__ __forceinline__ uint2 probe_range(const IndexView& v, uint64_t h) {
-  const uint64_t slot = h >> v.low_bits;
+  const uint64_t slot = index_slot(v, h);
+  if (slot == ~0ull) return make_uint2(0, 0);
   const uint32_t key = (uint32_t)(h & ((1ull << v.low_bits) - 1));
-  const uint32_t lo = __ldg(v.dir + slot), hi = __ldg(v.dir + slot + 1);
-  // lower bound by binary search, then a linear scan over the (usually single) matching entries:
-  // measured faster than a second binary search (most hashes occur once; slots hold ~2 entries)
-  uint32_t a = lo, b = hi;
+  const uint2 r = __ldg(v.dir + slot);
+  const uint32_t lo = r.x, hi = r.y;
+  if (hi - lo <= 4) {
+    uint32_t k4[4];
+#pragma unroll
+    for (int q = 0; q < 4; q++) k4[q] = lo + q < hi ? (uint32_t)__ldg(v.ent + lo + q) >> 1 : 0xFFFFFFFFu;
+    uint32_t below = 0, eq = 0;
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      below += k4[q] < key;
+      eq += k4[q] == key;
+    }
+    return make_uint2(lo + below, lo + below + eq);
+  }
+  // a longer slot is usually one frequent hash: both ends equal the key -> the whole slot
+  const uint32_t kf = (uint32_t)__ldg(v.ent + lo) >> 1, kl = (uint32_t)__ldg(v.ent + hi - 1) >> 1;
+  if (kf == key && kl == key) return make_uint2(lo, hi);
+  if (kf > key || kl < key) return make_uint2(lo, lo);
+  uint32_t a = lo, b = hi;  // lower bound
   while (a < b) {
     const uint32_t mid = (a + b) >> 1;
-    if ((__ldg(v.ent_key + mid) >> 1) < key) a = mid + 1;
+    if (((uint32_t)__ldg(v.ent + mid) >> 1) < key) a = mid + 1;
     else b = mid;
   }
-  uint32_t e = a;
-  while (e < hi && (__ldg(v.ent_key + e) >> 1) == key) ++e;
-  return make_uint2(a, e);
+  uint32_t c = a, d = hi;  // upper bound
+  while (c < d) {
+    const uint32_t mid = (c + d) >> 1;
+    if (((uint32_t)__ldg(v.ent + mid) >> 1) <= key) c = mid + 1;
+    else d = mid;
+  }
+  return make_uint2(a, c);
 }
 
 }  // namespace god
@@ -91,12 +130,14 @@ __device__ __forceinline__ uint2 probe_range(const IndexView& v, uint64_t h) {
 struct god_index {
   god::Params P;
   god_index_stats st;
-  uint32_t* dir = nullptr;
-  uint32_t* ent_key = nullptr;
-  uint32_t* ent_pos = nullptr;
+  uint2* dir = nullptr;
+  uint64_t* ent = nullptr;
+  uint2* seg = nullptr;       // mode 1 slot map (null in mode 0)
+  uint32_t low_bits = 0;
+  uint64_t n_slots = 0;
   cudaStream_t st_alloc = 0;
   god::IndexView view() const {
-    return god::IndexView{dir, ent_key, ent_pos, st.dir_bits, (uint32_t)(2 * P.k) - st.dir_bits, st.kept_entries};
+    return god::IndexView{dir, ent, seg, st.dir_bits, low_bits, st.kept_entries, n_slots};
   }
 };
 

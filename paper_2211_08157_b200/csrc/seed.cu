@@ -9,6 +9,8 @@
 //       fewer than t exact records for some phase (N-dense prefixes) are recomputed uncapped.
 //   S3  extraction over the (read, a_r) jobs -> all minimizers of PQ_a
 //   S4  per record: probe -> anchor count; exclusive scan; probe again -> write anchors
+#include <algorithm>
+#include <cstdlib>
 #include "internal.cuh"
 
 namespace god {
@@ -85,8 +87,10 @@ __global__ void k_make_jobs_ids(Params P, const uint64_t* __restrict__ offsets, 
   }
 }
 
-__global__ void k_anchor_count(IndexView v, const uint64_t* __restrict__ hz, uint64_t n, uint32_t* cnt,
-                               uint32_t* beg) {
+// one probe per thread, one thread per record, large grid: the probe is a chain of two dependent
+// random accesses (directory slot, entries) and is bound by HBM random-access bandwidth; many
+// resident warps hide the latency better than a persistent loop with per-thread ILP (measured).
+__global__ void k_anchor_count(IndexView v, const uint64_t* __restrict__ hz, uint64_t n, uint32_t* cnt, uint32_t* beg) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint2 rg = probe_range(v, hz[i] & ((1ull << 63) - 1));
     cnt[i] = rg.y - rg.x;
@@ -105,10 +109,11 @@ __global__ void k_anchor_write(IndexView v, const uint32_t* __restrict__ pos, co
     uint64_t o = aoff[i];
     for (uint32_t e = b; e < b + c; e++, o++) {
       god_anchor an;
-      an.ref_pos = __ldg(v.ent_pos + e);
+      const uint64_t en = __ldg(v.ent + e);
+      an.ref_pos = (uint32_t)(en >> 32);
       an.read_pos = qpos;
       an.read_id = r;
-      an.strand = (__ldg(v.ent_key + e) & 1u) ^ qz;
+      an.strand = ((uint32_t)en & 1u) ^ qz;
       out[o] = an;
     }
   }
@@ -214,7 +219,8 @@ __global__ void k_read_anchor_offsets(const uint64_t* __restrict__ job_off, cons
 static void probe_all(const IndexView& v, Records& rec, cudaStream_t st, Scratch& scr) {
   rec.cnt = scr.alloc<uint32_t>(rec.n);
   rec.beg = scr.alloc<uint32_t>(rec.n);
-  if (rec.n) GOD_LAUNCH("k_probe", k_anchor_count, grid_for(rec.n, 256), 256, 0, st, v, rec.hz, rec.n, rec.cnt, rec.beg);
+  if (rec.n)
+    GOD_LAUNCH("k_probe", k_anchor_count, grid_for(rec.n, 256), 256, 0, st, v, rec.hz, rec.n, rec.cnt, rec.beg);
 }
 
 uint64_t seed_reads(const god_index* ix, const uint8_t* reads, const uint64_t* offsets, uint32_t n_reads,
