@@ -793,9 +793,17 @@ __global__ void k_count_queries(god::IndexView v, const uint64_t* __restrict__ h
   }
 }
 
-__global__ void k_dir_pairs(const uint32_t* __restrict__ d1, uint64_t n_slots, uint2* dir) {
-  for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < n_slots; s += (uint64_t)gridDim.x * blockDim.x)
-    dir[s] = make_uint2(d1[s], d1[s + 1]);
+__global__ void k_dir_records(const uint32_t* __restrict__ d1, const uint64_t* __restrict__ ent, uint64_t n_slots,
+                              DirRec* dir) {
+  for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < n_slots; s += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t a = d1[s], b = d1[s + 1];
+    uint32_t k[DIR_KEYS];
+#pragma unroll
+    for (int q = 0; q < DIR_KEYS; q++) k[q] = a + q < b ? (uint32_t)ent[a + q] >> 1 : 0xFFFFFFFFu;
+    uint4* o = reinterpret_cast<uint4*>(dir + s);
+    o[0] = make_uint4(a, b, k[0], k[1]);
+    o[1] = make_uint4(k[2], k[3], k[4], k[5]);
+  }
 }
 
 __global__ void k_dump(god::IndexView v, uint64_t* hash, uint32_t* pos, uint8_t* strand) {
@@ -804,7 +812,7 @@ __global__ void k_dump(god::IndexView v, uint64_t* hash, uint32_t* pos, uint8_t*
     uint64_t lo = 0, hi = v.n_slots - 1;
     while (lo < hi) {
       uint64_t mid = (lo + hi + 1) >> 1;
-      if (v.dir[mid].x <= e) lo = mid;
+      if (v.dir[mid].start <= e) lo = mid;
       else hi = mid - 1;
     }
     uint64_t top = lo;
@@ -988,7 +996,7 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
   ix->seg = seg;
   ix->low_bits = low_bits;
   ix->n_slots = n_slots;
-  GOD_CUDA(cudaMallocAsync((void**)&ix->dir, n_slots * sizeof(uint2), st));
+  GOD_CUDA(cudaMallocAsync((void**)&ix->dir, n_slots * sizeof(DirRec), st));
   uint32_t* dir1 = scr.alloc<uint32_t>(n_slots + 1);  // first entry per slot (+ n_kept), then pairs
   GOD_CUDA(cudaMallocAsync((void**)&ix->ent, (n_kept ? n_kept : 1) * sizeof(uint64_t), st));
   uint32_t* kslot = scr.alloc<uint32_t>(n_kept);
@@ -1007,7 +1015,7 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
     GOD_CUDA(cudaMemsetAsync(dst, 0, nt * sizeof(uint64_t), st));
     GOD_CUDA(cudaMemsetAsync(dctr, 0, sizeof(uint32_t), st));
     GOD_LAUNCH("k_dir_suffix_min", k_dir_suffix_min, (unsigned)nt, DF_NT, 0, st, dir1, nd1, dst, dctr);
-    GOD_LAUNCH("k_dir_pairs", k_dir_pairs, grid_for(n_slots, 256), 256, 0, st, dir1, n_slots, ix->dir);
+    GOD_LAUNCH("k_dir_records", k_dir_records, grid_for(n_slots, 256), 256, 0, st, dir1, ix->ent, n_slots, ix->dir);
   }
   GOD_CUDA(cudaStreamSynchronize(st));
   if (const char* dd = getenv("GOD_DEBUG_DIR")) {  // developer aid: dump the intermediates
@@ -1021,7 +1029,7 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
     dump("rec_hz", rec.hz, n * 8); dump("sorted_hz", k0, n * 8); dump("sorted_pos", v0, n * 4);
     dump("flag", flag, n * 4); dump("dix", dix, n * 8); dump("dstart", dstart, (nd + 1) * 8);
     dump("count", count, nd * 4); dump("kept_off", kept_off, nd * 8); dump("kslot", kslot, n_kept * 4);
-    dump("ent", ix->ent, n_kept * 8); dump("dir", ix->dir, n_slots * 8);
+    dump("ent", ix->ent, n_kept * 8); dump("dir", ix->dir, n_slots * sizeof(DirRec));
   }
 }
 

@@ -56,7 +56,9 @@ JobSet make_jobs(const Params& P, const uint64_t* offsets, uint32_t n_seqs, cons
 // ------------------------------------------------------------------------------------ index
 // Device view of the seed index (P:286 (3): key = hash, value = sorted start locations).
 // ent[e] = pos << 32 | low_hash << 1 | strand, entries in (hash, pos) order.
-// dir[s] = {first, end} kept-entry range of slot s (s < n_slots).
+// dir[s] = slot record (32 B, one sector): kept-entry range [start, end) of slot s and the keys
+//          (low hash bits) of its first DIR_KEYS entries, so a probe is one random sector unless
+//          the slot holds more than DIR_KEYS entries.
 // Slot of a hash:
 //   mode 0: the top B = dir_bits hash bits (low_bits = 2k - B);
 //   mode 1 (seg != null): data-sized and monotone: segment t = top DIR_SEG_BITS hash bits,
@@ -64,8 +66,13 @@ JobSet make_jobs(const Params& P, const uint64_t* offsets, uint32_t n_seqs, cons
 //           seg[t].y ~ (entries in segment t) / 2, so slots hold ~2 entries however skewed the
 //           minimizer hashes are (they are window minima: dense at small values).
 constexpr int DIR_SEG_BITS = 12;
+constexpr int DIR_KEYS = 6;
+struct __align__(32) DirRec {
+  uint32_t start, end;
+  uint32_t key[DIR_KEYS];  // 0xFFFFFFFF past the end of the slot
+};
 struct IndexView {
-  const uint2* dir;
+  const DirRec* dir;
   const uint64_t* ent;
   const uint2* seg;
   uint32_t dir_bits;
@@ -85,24 +92,22 @@ __device__ __forceinline__ uint64_t index_slot(const IndexView& v, uint64_t h) {
 }
 
 // [begin, end) of the kept entries whose hash == h ("examines the presence of the extracted
-// minimizers (their hash values) in the seed index").  One 8-byte directory load gives the slot's
-// range; a slot of <= 4 entries (the common case) is resolved with independent loads (one round
-// trip), a longer one by binary search plus a scan over the matches.
+// minimizers (their hash values) in the seed index").  The slot record answers a slot of
+// <= DIR_KEYS entries (almost all) from one 32-B sector; a longer slot is searched in the entries.
 __device__ __forceinline__ uint2 probe_range(const IndexView& v, uint64_t h) {
   const uint64_t slot = index_slot(v, h);
   if (slot == ~0ull) return make_uint2(0, 0);
   const uint32_t key = (uint32_t)(h & ((1ull << v.low_bits) - 1));
-  const uint2 r = __ldg(v.dir + slot);
-  const uint32_t lo = r.x, hi = r.y;
-  if (hi - lo <= 4) {
-    uint32_t k4[4];
-#pragma unroll
-    for (int q = 0; q < 4; q++) k4[q] = lo + q < hi ? (uint32_t)__ldg(v.ent + lo + q) >> 1 : 0xFFFFFFFFu;
+  const uint4 r0 = __ldg(reinterpret_cast<const uint4*>(v.dir + slot));
+  const uint4 r1 = __ldg(reinterpret_cast<const uint4*>(v.dir + slot) + 1);
+  const uint32_t lo = r0.x, hi = r0.y;
+  if (hi - lo <= DIR_KEYS) {  // every key of the slot is in the record
+    const uint32_t k6[DIR_KEYS] = {r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
     uint32_t below = 0, eq = 0;
 #pragma unroll
-    for (int q = 0; q < 4; q++) {
-      below += k4[q] < key;
-      eq += k4[q] == key;
+    for (int q = 0; q < DIR_KEYS; q++) {
+      below += k6[q] < key;
+      eq += k6[q] == key;
     }
     return make_uint2(lo + below, lo + below + eq);
   }
@@ -130,7 +135,7 @@ __device__ __forceinline__ uint2 probe_range(const IndexView& v, uint64_t h) {
 struct god_index {
   god::Params P;
   god_index_stats st;
-  uint2* dir = nullptr;
+  god::DirRec* dir = nullptr;
   uint64_t* ent = nullptr;
   uint2* seg = nullptr;       // mode 1 slot map (null in mode 0)
   uint32_t low_bits = 0;
