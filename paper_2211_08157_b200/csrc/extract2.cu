@@ -58,7 +58,7 @@ struct X2Args {
   uint64_t* total_out;
   uint32_t dbg_flags;      // developer toggles (GOD_X2_DBG): 1 = unordered output, 2 = no tie check
   uint32_t* dbg_counts;    // [0] tiles on the slow path, [1] tiles with a key tie
-  const uint32_t* tile_j;  // [2 * ntiles]: first and last job of each tile
+  const struct X2Desc* desc;  // [ntiles] per-tile descriptors (k_x2_tile_desc)
 };
 
 __device__ __forceinline__ uint32_t find_job_le(const uint64_t* arr, uint32_t lo, uint32_t hi, uint64_t g) {
@@ -103,6 +103,13 @@ __device__ __forceinline__ uint64_t wang_hash_k(uint64_t key) {
   key = (key + (key << 31)) & mask;
   return key;
 }
+
+// per-tile descriptor, precomputed by k_x2_tile_desc so that a CTA never walks a dependent chain
+// of global loads (tile -> jobs -> code-word range) while its other warps wait at a barrier
+struct __align__(16) X2Desc {
+  uint32_t j0, j1, simple, pad;
+  uint64_t cw_lo, cw_hi;
+};
 
 struct X2Tile {  // per-tile scalars, in SMEM
   uint32_t tile, j0, j1, simple, any_n, slow, cnt;
@@ -282,34 +289,29 @@ __global__ void __launch_bounds__(X2_NT, X2_MINB) k_extract2(X2Args a) {
     }
   };
 
+  // tiles are claimed in order from an atomic counter, one tile ahead: thread 0 claims the next
+  // tile and prefetches its descriptor while the CTA works on the current one
+  uint32_t next_t = 0;
+  X2Desc nd{};
+  if (tid == 0) {
+    next_t = atomicAdd(a.tile_ctr, 1u);
+    if (next_t < ntiles) nd = a.desc[next_t];
+  }
   while (true) {
     if (tid == 0) {
-      const uint32_t t = atomicAdd(a.tile_ctr, 1u);
-      T.tile = t;
-      if (t < ntiles) {
-        const int64_t b_first = (int64_t)t * X2_OUT_BLOCKS - 1;
-        const int64_t b_last = (int64_t)t * X2_OUT_BLOCKS + X2_NT - 2;
-        const uint64_t gmax = a.total_blocks * W - 1;
-        const uint64_t gfirst = b_first < 0 ? 0 : (uint64_t)b_first * W;
-        uint64_t glast = (uint64_t)(b_last < 0 ? 0 : b_last) * W;
-        if (glast > gmax) glast = gmax;
-        const uint32_t j0 = a.tile_j[2 * t], j1 = a.tile_j[2 * t + 1];  // precomputed (k_x2_tile_jobs)
-        T.j0 = j0; T.j1 = j1;
-        const uint64_t lo = b_first < 0 ? a.cw[0] : a.cw[j0] + (gfirst - a.kb[j0]) / 16;
-        uint64_t hi = a.cw[j1] + (glast - a.kb[j1] + NB + 15) / 16 + 1;
-        if (hi > a.cw[j1 + 1]) hi = a.cw[j1 + 1];
-        if (hi < lo) hi = lo;
-        if (hi > lo + C::MAXWORDS) hi = lo + C::MAXWORDS;
-        T.cw_lo = lo; T.cw_hi = hi;
-        const Job jb = a.jobs[j0];
-        const uint64_t last_byte = jb.seq_off + jb.phase + a.one0 + (uint64_t)PS * 16 * (hi - a.cw[j0]) + 4 * PS + 8;
-        T.simple = (j0 == j1) && last_byte <= a.seq_bytes;
+      T.tile = next_t < ntiles ? next_t : 0xFFFFFFFFu;
+      if (next_t < ntiles) {
+        T.j0 = nd.j0; T.j1 = nd.j1;
+        T.cw_lo = nd.cw_lo; T.cw_hi = nd.cw_hi;
+        T.simple = nd.simple;
         T.any_n = 0; T.slow = 0;
+        next_t = atomicAdd(a.tile_ctr, 1u);
+        if (next_t < ntiles) nd = a.desc[next_t];
       }
     }
     __syncthreads();
     const uint32_t tile = T.tile;
-    if (tile >= ntiles) break;
+    if (tile == 0xFFFFFFFFu) break;
     uint64_t* HZ = HZ2 + (size_t)buf * POS;
     const uint32_t j0 = T.j0, j1 = T.j1;
     const uint64_t cw_lo = T.cw_lo;
@@ -604,9 +606,11 @@ __global__ void __launch_bounds__(X2_NT, X2_MINB) k_extract2(X2Args a) {
   if (pend_tile >= 0) flush((uint64_t)pend_tile, pend_cnt, buf ^ 1);
 }
 
-// first and last job of every tile (binary searches over the padded bases, one thread per tile)
-__global__ void k_x2_tile_jobs(const uint64_t* __restrict__ kb, uint32_t n_jobs, uint64_t total_blocks, int W,
-                               uint64_t ntiles, uint32_t* tile_j) {
+// per-tile descriptors: first and last job (binary searches over the padded bases), the tile's
+// code-word range, and whether it is a single job whose bytes can be read unchecked
+__global__ void k_x2_tile_desc(const uint64_t* __restrict__ kb, const uint64_t* __restrict__ cw,
+                               const Job* __restrict__ jobs, uint32_t n_jobs, uint64_t total_blocks, int W, int NB,
+                               int maxwords, int PS, uint32_t one0, uint64_t seq_bytes, uint64_t ntiles, X2Desc* desc) {
   for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < ntiles; t += (uint64_t)gridDim.x * blockDim.x) {
     const int64_t b_first = (int64_t)t * X2_OUT_BLOCKS - 1;
     const int64_t b_last = (int64_t)t * X2_OUT_BLOCKS + X2_NT - 2;
@@ -615,8 +619,22 @@ __global__ void k_x2_tile_jobs(const uint64_t* __restrict__ kb, uint32_t n_jobs,
     uint64_t glast = (uint64_t)(b_last < 0 ? 0 : b_last) * W;
     if (glast > gmax) glast = gmax;
     const uint32_t j0 = find_job_le(kb, 0, n_jobs - 1, gfirst);
-    tile_j[2 * t] = j0;
-    tile_j[2 * t + 1] = find_job_le(kb, j0, n_jobs - 1, glast);
+    const uint32_t j1 = find_job_le(kb, j0, n_jobs - 1, glast);
+    const uint64_t lo = b_first < 0 ? cw[0] : cw[j0] + (gfirst - kb[j0]) / 16;
+    uint64_t hi = cw[j1] + (glast - kb[j1] + NB + 15) / 16 + 1;
+    if (hi > cw[j1 + 1]) hi = cw[j1 + 1];
+    if (hi < lo) hi = lo;
+    if (hi > lo + (uint64_t)maxwords) hi = lo + maxwords;
+    const Job jb = jobs[j0];
+    const uint64_t last_byte = jb.seq_off + jb.phase + one0 + (uint64_t)PS * 16 * (hi - cw[j0]) + 4 * PS + 8;
+    X2Desc d;
+    d.j0 = j0;
+    d.j1 = j1;
+    d.simple = (j0 == j1) && last_byte <= seq_bytes;
+    d.pad = 0;
+    d.cw_lo = lo;
+    d.cw_hi = hi;
+    desc[t] = d;
   }
 }
 
@@ -690,11 +708,14 @@ bool run_extract2(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const
   if (cap > total_pos) cap = total_pos;
   if (cap == 0) cap = 1;
   uint64_t* status = scr.alloc<uint64_t>(ntiles + 1);
-  uint32_t* tile_j = scr.alloc<uint32_t>(2 * ntiles + 2);
-  if (ntiles)
-    GOD_LAUNCH("k_x2_tile_jobs", k_x2_tile_jobs, grid_for(ntiles, 256), 256, 0, st, kb, n_jobs, total_blocks, W, ntiles,
-               tile_j);
+  X2Desc* desc = scr.alloc<X2Desc>(ntiles ? ntiles : 1);
   uint32_t* ctr = scr.alloc<uint32_t>(1);
+  if (ntiles) {
+    const int NB = W + K - 1;
+    const int maxwords = (X2_NT * W + X2_NT * (K - 1) + 15) / 16 + X2_NT + 8;  // X2Cfg::MAXWORDS
+    GOD_LAUNCH("k_x2_tile_desc", k_x2_tile_desc, grid_for(ntiles, 256), 256, 0, st, kb, cw, jobs, n_jobs, total_blocks,
+               W, NB, maxwords, PS, P.pat.one[0], seq_bytes, ntiles, desc);
+  }
   uint64_t* dtotal = scr.alloc<uint64_t>(1);
   if (want_job_off) rec.job_off = scr.alloc<uint64_t>(n_jobs + 1);
   const char* dflag = getenv("GOD_X2_DBG");
@@ -718,7 +739,7 @@ bool run_extract2(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const
     GOD_CUDA(cudaMemsetAsync(status, 0, (ntiles + 1) * sizeof(uint64_t), st));
     GOD_CUDA(cudaMemsetAsync(ctr, 0, sizeof(uint32_t), st));
     X2Args a{seq, seq_bytes, jobs, kb, cw, n_jobs, total_blocks, P.pat.one[0], key_shift, status, ctr,
-             rec.hz, rec.pos, rec.job, rec.job_off, cap, dtotal, dbg_flags, dbg_counts, tile_j};
+             rec.hz, rec.pos, rec.job, rec.job_off, cap, dtotal, dbg_flags, dbg_counts, desc};
     if (ntiles) {
       if (K == 21 && W == 11) {
         if (PS == 2) launch_x2<21, 11, 2>(a, ntiles, st, tag);

@@ -1,10 +1,11 @@
 """Per-source-line stall samples / instructions from an ncu report (cuda,sass mixed source page).
-usage: python tools/ncu_lines.py REPORT [N]"""
+usage: python tools/ncu_lines.py REPORT [N] [KERNEL_REGEX]"""
 import csv, subprocess, sys
 from collections import defaultdict
 rep = sys.argv[1]
 N = int(sys.argv[2]) if len(sys.argv) > 2 else 30
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+flt = ["--kernel-name", "regex:" + sys.argv[3], "--launch-count", "1"] if len(sys.argv) > 3 else []
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"] + flt,
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(out.splitlines()))
 hi = next(i for i, r in enumerate(rows) if r and r[0] == "Line No")
@@ -20,7 +21,11 @@ for r in rows[hi + 1:]:
         continue
     if r[0]:
         line = int(r[0]); src[line] = r[1]
-    f = lambda x: float(x) if x not in ("", "-") else 0.0
+    def f(x):
+        try:
+            return float(x)
+        except ValueError:
+            return 0.0
     samp[line] += f(r[iS]); ins[line] += f(r[iX])
 tot = sum(samp.values()) or 1
 print(f"total samples {tot:.0f}  instructions {sum(ins.values()):.0f}")
