@@ -227,9 +227,9 @@ void prof_add_units(const char* name, uint64_t units);
 // Device-wide exclusive scan of n u64 values (in may alias out).  *total (device, may be null)
 // receives the sum.  Single pass, decoupled look-back.
 void scan_exclusive_u64(const uint64_t* in, uint64_t* out, uint64_t n, uint64_t* total, cudaStream_t st,
-                        Scratch& scr);
+                        Scratch& scr, const char* tag = "k_scan");
 void scan_exclusive_u32_to_u64(const uint32_t* in, uint64_t* out, uint64_t n, uint64_t* total, cudaStream_t st,
-                               Scratch& scr);
+                               Scratch& scr, const char* tag = "k_scan");
 
 template <class T>
 inline T d2h_scalar(const T* dptr, cudaStream_t st) {

@@ -273,7 +273,7 @@ JobSet make_jobs(const Params& P, const uint64_t* offsets, uint32_t n_seqs, cons
   if (nj) {
     GOD_LAUNCH("k_make_jobs", k_make_jobs, grid_for(nj, 256), 256, 0, st, P, offsets, n_seqs, phases, p_all, kcap, global_pos, js.jobs, js.kb);
   }
-  scan_exclusive_u64(js.kb, js.kb, nj, tot, st, scr);
+  scan_exclusive_u64(js.kb, js.kb, nj, tot, st, scr, "scan_jobs");
   GOD_CUDA(cudaMemcpyAsync(js.kb + nj, tot, sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
   uint64_t h[2] = {0, 0};
   GOD_CUDA(cudaMemcpyAsync(&h[0], tot, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));

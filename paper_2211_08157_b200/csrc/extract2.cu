@@ -692,8 +692,8 @@ bool run_extract2(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const
   GOD_CUDA(cudaMemsetAsync(tot + 2, 0, sizeof(uint64_t), st));
   GOD_LAUNCH("k_x2_sizes", k_x2_sizes, grid_for(n_jobs, 256), 256, 0, st, jobs, n_jobs, K, W, kb, cw,
              reinterpret_cast<unsigned long long*>(tot + 2));
-  scan_exclusive_u64(kb, kb, n_jobs, tot, st, scr);
-  scan_exclusive_u64(cw, cw, n_jobs, tot + 1, st, scr);
+  scan_exclusive_u64(kb, kb, n_jobs, tot, st, scr, "scan_x2_jobs");
+  scan_exclusive_u64(cw, cw, n_jobs, tot + 1, st, scr, "scan_x2_jobs");
   GOD_CUDA(cudaMemcpyAsync(kb + n_jobs, tot, sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
   GOD_CUDA(cudaMemcpyAsync(cw + n_jobs, tot + 1, sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
   uint64_t htot[3];

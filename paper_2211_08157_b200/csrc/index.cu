@@ -570,32 +570,43 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort_big(uint64_t* __restri
   }
 }
 
-__global__ void k_heads(const uint64_t* __restrict__ hz, uint64_t n, uint32_t* flag) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-    flag[i] = (i == 0 || ((hz[i] ^ hz[i - 1]) & HASH_BITS_MASK)) ? 1u : 0u;
-}
-
-__global__ void k_dstart(const uint32_t* __restrict__ flag, const uint64_t* __restrict__ dix, uint64_t n, uint64_t* dstart,
-                         const uint64_t* nd) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-    if (flag[i]) dstart[dix[i]] = i;
-  if (blockIdx.x == 0 && threadIdx.x == 0) dstart[*nd] = n;
-}
-
 constexpr uint32_t SMALL_BINS = 4096;
 
-// counts per distinct hash + small-count histogram + list of large counts
-__global__ void k_counts(const uint64_t* __restrict__ dstart, uint64_t nd, uint32_t* count, uint32_t* hist_small,
-                         uint32_t* large, uint32_t* n_large) {
+// K3: runs of equal hashes in the sorted records (one run = one distinct hash, P:286 (3)).  The
+// thread holding a run head finds the run end (linear for short runs, exponential + binary search
+// for long ones), writes the run length to every member (rl), and adds it to the count histogram
+// (SMEM bins for counts < SMALL_BINS, a list for the rare larger ones) used by the cutoff.
+__global__ void k_runs(const uint64_t* __restrict__ k, uint64_t n, uint32_t* rl, uint32_t* hist_small, uint32_t* large,
+                       uint32_t* n_large, unsigned long long* n_distinct) {
   __shared__ uint32_t h[SMALL_BINS];
   for (int i = threadIdx.x; i < (int)SMALL_BINS; i += blockDim.x) h[i] = 0;
   __syncthreads();
-  for (uint64_t d = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; d < nd; d += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t c = (uint32_t)(dstart[d + 1] - dstart[d]);
-    count[d] = c;
+  uint32_t local_nd = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t hv = k[i] & HASH_BITS_MASK;
+    if (i > 0 && (k[i - 1] & HASH_BITS_MASK) == hv) continue;
+    uint64_t e = i + 1;
+    while (e < n && e - i < 8 && (k[e] & HASH_BITS_MASK) == hv) ++e;
+    if (e - i == 8 && e < n && (k[e] & HASH_BITS_MASK) == hv) {
+      uint64_t lo = e, step = 8;  // key(lo) == hv
+      while (lo + step < n && (k[lo + step] & HASH_BITS_MASK) == hv) { lo += step; step <<= 1; }
+      uint64_t hi = lo + step < n ? lo + step : n;  // first index with a different key is in (lo, hi]
+      while (hi - lo > 1) {
+        const uint64_t mid = lo + (hi - lo) / 2;
+        if ((k[mid] & HASH_BITS_MASK) == hv) lo = mid;
+        else hi = mid;
+      }
+      e = hi;
+    }
+    const uint64_t L = e - i;
+    const uint32_t c = L < 0xFFFFFFFFull ? (uint32_t)L : 0xFFFFFFFFu;
     if (c < SMALL_BINS) atomicAdd(&h[c], 1u);
     else large[atomicAdd(n_large, 1u)] = c;
+    ++local_nd;
+    for (uint64_t q = i; q < e; q++) rl[q] = c;
   }
+  for (int o = 16; o; o >>= 1) local_nd += __shfl_xor_sync(0xffffffffu, local_nd, o);
+  if ((threadIdx.x & 31) == 0 && local_nd) atomicAdd(n_distinct, (unsigned long long)local_nd);
   __syncthreads();
   for (int i = threadIdx.x; i < (int)SMALL_BINS; i += blockDim.x)
     if (h[i]) atomicAdd(&hist_small[i], h[i]);
@@ -661,47 +672,90 @@ __global__ void __launch_bounds__(1024) k_tau(const uint32_t* hist_small, const 
       tau = s_need;
     }
   }
+  // kept distinct hashes and entries: counts <= tau (histogram bins and the large list)
+  __shared__ unsigned long long s_kd, s_ke;
+  if (threadIdx.x == 0) { s_kd = 0; s_ke = 0; }
+  __syncthreads();
+  unsigned long long kd = 0, ke = 0;
+  for (uint32_t c = threadIdx.x; c < SMALL_BINS && c <= tau; c += blockDim.x) {
+    kd += hist_small[c];
+    ke += (unsigned long long)c * hist_small[c];
+  }
+  for (uint32_t i = threadIdx.x; i < nl; i += blockDim.x)
+    if (large[i] <= tau) { kd += 1; ke += large[i]; }
+  atomicAdd(&s_kd, kd);
+  atomicAdd(&s_ke, ke);
+  __syncthreads();
   if (threadIdx.x == 0) {
     cs->n_entries = n_entries;
     cs->n_distinct = nd;
     cs->m = m;
     cs->tau = tau;
-    cs->kept_entries = 0;
-    cs->kept_distinct = 0;
+    cs->kept_entries = s_ke;
+    cs->kept_distinct = s_kd;
   }
 }
 
-__global__ void k_kept(const uint32_t* __restrict__ count, uint64_t nd, CutState* cs, uint64_t* kept_val) {
+// K5: kept entries in order, one pass: a record is kept iff its run length <= tau (reading O7);
+// tiles of KW_TILE records (warp-striped), ballot compaction, tile offsets by decoupled look-back.
+// Writes the entry (pos << 32 | low hash << 1 | strand) and its directory slot.
+constexpr int KW_NT = 256, KW_IPT = 16, KW_TILE = KW_NT * KW_IPT;
+__global__ void __launch_bounds__(KW_NT) k_keep_write(const uint64_t* __restrict__ k, const uint32_t* __restrict__ pos,
+                                                      const uint32_t* __restrict__ rl, uint64_t n, const CutState* cs,
+                                                      IndexView iv, uint64_t* ent, uint32_t* kslot, uint64_t* status,
+                                                      uint32_t* tile_ctr) {
+  __shared__ uint32_t s_tile;
+  __shared__ uint32_t wtot[KW_NT / 32];
+  __shared__ uint64_t s_excl;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
+  __syncthreads();
+  const uint64_t tile = s_tile;
   const uint64_t tau = cs->tau;
-  uint32_t local = 0;
-  for (uint64_t d = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; d < nd; d += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t c = count[d];
-    const bool keep = c <= tau;
-    kept_val[d] = keep ? c : 0;
-    local += keep;
+  const uint64_t base = tile * KW_TILE + (uint64_t)wid * (32 * KW_IPT);
+  uint32_t masks[KW_IPT];
+  uint32_t wc = 0;
+#pragma unroll
+  for (int j = 0; j < KW_IPT; j++) {
+    const uint64_t i = base + (uint64_t)j * 32 + lane;
+    const bool keep = i < n && rl[i] <= tau;
+    masks[j] = __ballot_sync(0xffffffffu, keep);
+    wc += __popc(masks[j]);
   }
-  for (int o = 16; o; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
-  if ((threadIdx.x & 31) == 0 && local) atomicAdd((unsigned long long*)&cs->kept_distinct, (unsigned long long)local);
-}
-
-__global__ void k_write_entries(const uint64_t* __restrict__ hz, const uint32_t* __restrict__ pos, uint64_t n, const uint32_t* __restrict__ flag,
-                                const uint64_t* __restrict__ dix, const uint64_t* __restrict__ dstart,
-                                const uint32_t* __restrict__ count, const uint64_t* __restrict__ kept_off,
-                                const CutState* cs, IndexView iv, uint64_t* ent, uint32_t* kslot) {
-  const uint64_t tau = cs->tau;
+  if (lane == 0) wtot[wid] = wc;
+  __syncthreads();
+  if (wid == 0) {
+    uint32_t t = lane < KW_NT / 32 ? wtot[lane] : 0u;
+    uint32_t incl = t;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += y;
+    }
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, KW_NT / 32 - 1);
+    const uint64_t ex = lb_exclusive_warp(status, tile, total);
+    if (lane < KW_NT / 32) wtot[lane] = incl - t;  // warp exclusive prefix within the tile
+    if (lane == 0) s_excl = ex;
+  }
+  __syncthreads();
+  uint64_t run = s_excl + wtot[wid];
+  const uint32_t lt = (1u << lane) - 1;
   const uint64_t lowmask = (1ull << iv.low_bits) - 1;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t d = dix[i] + flag[i] - 1;  // run index: exclusive scan of heads counts its own head for non-heads
-    if (count[d] > tau) continue;
-    const uint64_t e = kept_off[d] + (i - dstart[d]);
-    const uint64_t v = hz[i];
-    const uint64_t h = v & HASH_BITS_MASK;
-    ent[e] = ((uint64_t)pos[i] << 32) | ((h & lowmask) << 1) | (v >> 63);
-    kslot[e] = (uint32_t)index_slot(iv, h);
+#pragma unroll
+  for (int j = 0; j < KW_IPT; j++) {
+    const uint32_t m = masks[j];
+    if ((m >> lane) & 1u) {
+      const uint64_t i = base + (uint64_t)j * 32 + lane;
+      const uint64_t v = k[i];
+      const uint64_t h = v & HASH_BITS_MASK;
+      const uint64_t d = run + __popc(m & lt);
+      ent[d] = ((uint64_t)pos[i] << 32) | ((h & lowmask) << 1) | (v >> 63);
+      kslot[d] = (uint32_t)index_slot(iv, h);
+    }
+    run += __popc(m);
   }
 }
 
-// K6a: dir[slot] = first kept entry of each non-empty slot (dir pre-filled with ~0; dir[2^B] = n_kept)
 __global__ void k_dir_mark(const uint32_t* __restrict__ kslot, uint64_t n_kept, uint64_t n_slots, uint32_t* dir) {
   for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < n_kept; e += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t s = kslot[e];
@@ -871,7 +925,7 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
       constexpr int RB = decltype(rb)::value;
       const uint32_t dmask = (1u << bits) - 1;
       GOD_LAUNCH("k_rs_hist", k_rs_hist<RB>, ntiles, RS_NT, 0, st, k0, n, shift, dmask, hist, ntiles);
-      scan_exclusive_u32_to_u64(hist, goff, (uint64_t)(1u << RB) * ntiles, nullptr, st, scr);
+      scan_exclusive_u32_to_u64(hist, goff, (uint64_t)(1u << RB) * ntiles, nullptr, st, scr, "scan_sort_hist");
       GOD_LAUNCH("k_rs_scatter2", k_rs_scatter2<RB>, ntiles, RS2_NT, RS_DYN_SMEM, st, k0, v0, k1, v1, n, shift, dmask,
                  goff, ntiles);
       std::swap(k0, k1);
@@ -912,43 +966,26 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
         lsd_pass(std::integral_constant<int, RS_BITS>(), shift, std::min(RS_BITS, hbits - shift));
     }
   }
-  // K3: distinct hashes
-  uint32_t* flag = scr.alloc<uint32_t>(n);
-  uint64_t* dix = scr.alloc<uint64_t>(n);
-  uint64_t* nd_d = scr.alloc<uint64_t>(1);
-  if (n) {
-    GOD_LAUNCH("k_heads", k_heads, grid_for(n, 256), 256, 0, st, k0, n, flag);
-  }
-  scan_exclusive_u32_to_u64(flag, dix, n, nd_d, st, scr);
-  const uint64_t nd_bound = n;  // distinct <= n
-  uint64_t* dstart = scr.alloc<uint64_t>(nd_bound + 1);
-  GOD_LAUNCH("k_dstart", k_dstart, grid_for(n, 256), 256, 0, st, flag, dix, n, dstart, nd_d);
-  const uint64_t nd = d2h_scalar(nd_d, st);
-  // K4: counts, tau
-  uint32_t* count = scr.alloc<uint32_t>(nd);
+  // K3: runs (distinct hashes) + count histogram; K4: tau and the kept totals
+  uint32_t* rl = scr.alloc<uint32_t>(n ? n : 1);
   uint32_t* hist_small = scr.alloc<uint32_t>(SMALL_BINS);
   const uint64_t large_cap = n / SMALL_BINS + 1;
   uint32_t* large = scr.alloc<uint32_t>(large_cap);
   uint32_t* n_large = scr.alloc<uint32_t>(1);
+  uint64_t* nd_d = scr.alloc<uint64_t>(1);
   CutState* cs = scr.alloc<CutState>(1);
   GOD_CUDA(cudaMemsetAsync(hist_small, 0, SMALL_BINS * sizeof(uint32_t), st));
   GOD_CUDA(cudaMemsetAsync(n_large, 0, sizeof(uint32_t), st));
-  if (nd) {
-    GOD_LAUNCH("k_counts", k_counts, min(grid_for(nd, 512), 4u * num_sms()), 512, 0, st, dstart, nd, count, hist_small, large, n_large);
-  }
+  GOD_CUDA(cudaMemsetAsync(nd_d, 0, sizeof(uint64_t), st));
+  if (n)
+    GOD_LAUNCH("k_runs", k_runs, min(grid_for(n, 512), 8u * num_sms()), 512, 0, st, k0, n, rl, hist_small, large, n_large,
+               reinterpret_cast<unsigned long long*>(nd_d));
   GOD_LAUNCH("k_tau", k_tau, 1, 1024, 0, st, hist_small, large, n_large, nd_d, n, cut.mode, cut.frac_num, cut.frac_den, cut.max_occ, cs);
-  // K5: kept offsets + entries
-  uint64_t* kept_off = scr.alloc<uint64_t>(nd + 1);
-  uint64_t* kept_tot = scr.alloc<uint64_t>(1);
-  if (nd) {
-    GOD_LAUNCH("k_kept", k_kept, min(grid_for(nd, 256), 8u * num_sms()), 256, 0, st, count, nd, cs, kept_off);
-  }
-  scan_exclusive_u64(kept_off, kept_off, nd, kept_tot, st, scr);
   CutState hcs;
   GOD_CUDA(cudaMemcpyAsync(&hcs, cs, sizeof(CutState), cudaMemcpyDeviceToHost, st));
-  uint64_t n_kept = 0;
-  GOD_CUDA(cudaMemcpyAsync(&n_kept, kept_tot, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
   GOD_CUDA(cudaStreamSynchronize(st));
+  const uint64_t nd = hcs.n_distinct;
+  const uint64_t n_kept = hcs.kept_entries;
   GOD_REQUIRE(n_kept < 0xFFFFFFFFull, "index has >= 2^32 kept entries");
   // K6 directory.  mode 1 (2k - 12 in [2, 30]): data-sized monotone slot map over the top-12-bit
   // segments, ~DIR_TARGET entries per slot (minimizer hashes are skewed toward small values, and so
@@ -999,10 +1036,15 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
   GOD_CUDA(cudaMallocAsync((void**)&ix->dir, n_slots * sizeof(DirRec), st));
   uint32_t* dir1 = scr.alloc<uint32_t>(n_slots + 1);  // first entry per slot (+ n_kept), then pairs
   GOD_CUDA(cudaMallocAsync((void**)&ix->ent, (n_kept ? n_kept : 1) * sizeof(uint64_t), st));
-  uint32_t* kslot = scr.alloc<uint32_t>(n_kept);
-  if (n) {
-    GOD_LAUNCH("k_write_entries", k_write_entries, grid_for(n, 256), 256, 0, st, k0, v0, n, flag, dix, dstart, count,
-               kept_off, cs, ix->view(), ix->ent, kslot);
+  uint32_t* kslot = scr.alloc<uint32_t>(n_kept ? n_kept : 1);
+  if (n) {  // K5: kept entries
+    const uint64_t tiles = (n + KW_TILE - 1) / KW_TILE;
+    uint64_t* kst = scr.alloc<uint64_t>(tiles);
+    uint32_t* kctr = scr.alloc<uint32_t>(1);
+    GOD_CUDA(cudaMemsetAsync(kst, 0, tiles * sizeof(uint64_t), st));
+    GOD_CUDA(cudaMemsetAsync(kctr, 0, sizeof(uint32_t), st));
+    GOD_LAUNCH("k_keep_write", k_keep_write, (unsigned)tiles, KW_NT, 0, st, k0, v0, rl, n, cs, ix->view(), ix->ent, kslot,
+               kst, kctr);
   }
   {
     const uint64_t nd1 = n_slots + 1;
@@ -1027,8 +1069,7 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
       if (fp) { fwrite(h.data(), 1, bytes, fp); fclose(fp); }
     };
     dump("rec_hz", rec.hz, n * 8); dump("sorted_hz", k0, n * 8); dump("sorted_pos", v0, n * 4);
-    dump("flag", flag, n * 4); dump("dix", dix, n * 8); dump("dstart", dstart, (nd + 1) * 8);
-    dump("count", count, nd * 4); dump("kept_off", kept_off, nd * 8); dump("kslot", kslot, n_kept * 4);
+    dump("rl", rl, n * 4); dump("kslot", kslot, n_kept * 4);
     dump("ent", ix->ent, n_kept * 8); dump("dir", ix->dir, n_slots * sizeof(DirRec));
   }
 }

@@ -60,7 +60,8 @@ __global__ void __launch_bounds__(SCAN_NT) k_scan(const TIn* in, uint64_t* out, 
 }
 
 template <class TIn>
-void scan_impl(const TIn* in, uint64_t* out, uint64_t n, uint64_t* total, cudaStream_t st, Scratch& scr) {
+void scan_impl(const TIn* in, uint64_t* out, uint64_t n, uint64_t* total, cudaStream_t st, Scratch& scr,
+               const char* tag) {
   if (n == 0) {
     if (total) GOD_CUDA(cudaMemsetAsync(total, 0, sizeof(uint64_t), st));
     return;
@@ -70,17 +71,17 @@ void scan_impl(const TIn* in, uint64_t* out, uint64_t n, uint64_t* total, cudaSt
   uint32_t* ctr = scr.alloc<uint32_t>(1);
   GOD_CUDA(cudaMemsetAsync(status, 0, tiles * sizeof(uint64_t), st));
   GOD_CUDA(cudaMemsetAsync(ctr, 0, sizeof(uint32_t), st));
-  GOD_LAUNCH("k_scan", k_scan<TIn>, (unsigned)tiles, SCAN_NT, 0, st, in, out, n, status, ctr, total);
+  GOD_LAUNCH(tag, k_scan<TIn>, (unsigned)tiles, SCAN_NT, 0, st, in, out, n, status, ctr, total);
 }
 }  // namespace
 
 void scan_exclusive_u64(const uint64_t* in, uint64_t* out, uint64_t n, uint64_t* total, cudaStream_t st,
-                        Scratch& scr) {
-  scan_impl<uint64_t>(in, out, n, total, st, scr);
+                        Scratch& scr, const char* tag) {
+  scan_impl<uint64_t>(in, out, n, total, st, scr, tag);
 }
 void scan_exclusive_u32_to_u64(const uint32_t* in, uint64_t* out, uint64_t n, uint64_t* total, cudaStream_t st,
-                               Scratch& scr) {
-  scan_impl<uint32_t>(in, out, n, total, st, scr);
+                               Scratch& scr, const char* tag) {
+  scan_impl<uint32_t>(in, out, n, total, st, scr, tag);
 }
 
 }  // namespace god

@@ -265,7 +265,7 @@ uint64_t seed_reads(const god_index* ix, const uint8_t* reads, const uint64_t* o
         uint64_t* tot2 = scr.alloc<uint64_t>(1);
         GOD_LAUNCH("k_make_jobs_ids", k_make_jobs_ids, grid_for((uint64_t)nr * p, 256), 256, 0, st, P, offsets, redo,
                    nr, p, jobs2, kb2);
-        scan_exclusive_u64(kb2, kb2, (uint64_t)nr * p, tot2, st, scr);
+        scan_exclusive_u64(kb2, kb2, (uint64_t)nr * p, tot2, st, scr, "scan_seed_jobs");
         GOD_CUDA(cudaMemcpyAsync(kb2 + (uint64_t)nr * p, tot2, sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
         const uint64_t tp2 = d2h_scalar(tot2, st);
         run_extract(P, reads, js1.seq_bytes, jobs2, kb2, nr * p, tp2, false, true, rec2, st, scr, tp2 / 4 + 4096,
@@ -299,7 +299,7 @@ uint64_t seed_reads(const god_index* ix, const uint8_t* reads, const uint64_t* o
       uint64_t* tot3 = scr.alloc<uint64_t>(1);
       GOD_LAUNCH("k_make_jobs_sel", k_make_jobs_sel, grid_for(h3, 256), 256, 0, st, P, offsets, list3, h3, phases,
                  jobs3, kb3, src, srcj);
-      scan_exclusive_u64(kb3, kb3, h3, tot3, st, scr);
+      scan_exclusive_u64(kb3, kb3, h3, tot3, st, scr, "scan_seed_jobs");
       GOD_CUDA(cudaMemcpyAsync(kb3 + h3, tot3, sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
       const uint64_t tp3 = d2h_scalar(tot3, st);
       uint64_t bytes = 0;
@@ -317,7 +317,7 @@ uint64_t seed_reads(const god_index* ix, const uint8_t* reads, const uint64_t* o
   uint64_t* roff = scr.alloc<uint64_t>((uint64_t)n_reads + 1);
   uint64_t* rtot = scr.alloc<uint64_t>(1);
   GOD_LAUNCH("k_seed_counts", k_seed_counts, grid_for(n_reads, 256), 256, 0, st, S, n_reads, src, srcj, roff);
-  scan_exclusive_u64(roff, roff, n_reads, rtot, st, scr);
+  scan_exclusive_u64(roff, roff, n_reads, rtot, st, scr, "scan_read_records");
   GOD_CUDA(cudaMemcpyAsync(roff + n_reads, rtot, sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
   const uint64_t n = d2h_scalar(rtot, st);
   uint64_t* hz = scr.alloc<uint64_t>(n);
@@ -330,7 +330,7 @@ uint64_t seed_reads(const god_index* ix, const uint8_t* reads, const uint64_t* o
   // ---------------- S4: anchors (every read minimizer was probed once, right after its extraction)
   uint64_t* aoff = scr.alloc<uint64_t>(n);
   uint64_t* total = scr.alloc<uint64_t>(1);
-  scan_exclusive_u32_to_u64(cnt, aoff, n, total, st, scr);
+  scan_exclusive_u32_to_u64(cnt, aoff, n, total, st, scr, "scan_anchors");
   GOD_LAUNCH("k_read_anchor_offsets", k_read_anchor_offsets, grid_for((uint64_t)n_reads + 1, 256), 256, 0, st, roff,
              aoff, n, total, n_reads, anchor_offsets);
   const uint64_t tot = d2h_scalar(total, st);
