@@ -69,18 +69,20 @@ __global__ void __launch_bounds__(RS_NT) k_rs_hist(const uint64_t* __restrict__ 
 // lane l is w*256 + 32 j + l, so (warp, j, lane) order is index order.  Ranks come from match_any
 // plus per-warp digit counters (no block barrier per item round).
 template <int RB>
-__global__ void __launch_bounds__(RS2_NT) k_rs_scatter2(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin,
+__global__ void __launch_bounds__(RS2_NT, 2) k_rs_scatter2(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin,
                                                        uint64_t* __restrict__ kout, uint32_t* __restrict__ vout,
                                                        uint64_t n, int shift, uint32_t dmask,
                                                        const uint64_t* __restrict__ goff, uint32_t ntiles) {
   __shared__ uint32_t wcnt[RS2_NT / 32][(1 << RB)];
   __shared__ uint32_t dstart[(1 << RB)];
   __shared__ uint32_t wsum[(1 << RB) / 32];
+  __shared__ uint64_t s_goff[1 << RB];
   extern __shared__ __align__(16) unsigned char rs_dyn[];
   uint64_t* sk = reinterpret_cast<uint64_t*>(rs_dyn);
   uint32_t* sv = reinterpret_cast<uint32_t*>(sk + RS_TILE);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   for (int i = tid; i < (RS2_NT / 32) * (1 << RB); i += RS2_NT) (&wcnt[0][0])[i] = 0;
+  for (int d = tid; d < (1 << RB); d += RS2_NT) s_goff[d] = goff[(uint64_t)d * ntiles + blockIdx.x];  // used at the end
   __syncthreads();
   const uint64_t base = (uint64_t)blockIdx.x * RS_TILE + (uint64_t)wid * (32 * RS2_IPT);
   const uint32_t lt = (1u << lane) - 1;
@@ -88,11 +90,16 @@ __global__ void __launch_bounds__(RS2_NT) k_rs_scatter2(const uint64_t* __restri
   uint32_t val[RS2_IPT];
   uint32_t rk[RS2_IPT];
 #pragma unroll
+  for (int j = 0; j < RS2_IPT; j++) {  // all loads in flight before the ranking
+    const uint64_t i = base + (uint64_t)j * 32 + lane;
+    const bool ok = i < n;
+    key[j] = ok ? __ldcs(kin + i) : 0;
+    val[j] = ok ? __ldcs(vin + i) : 0;
+  }
+#pragma unroll
   for (int j = 0; j < RS2_IPT; j++) {
     const uint64_t i = base + (uint64_t)j * 32 + lane;
     const bool ok = i < n;
-    key[j] = ok ? kin[i] : 0;
-    val[j] = ok ? vin[i] : 0;
     const uint32_t d = ok ? ((uint32_t)((key[j] & HASH_BITS_MASK) >> shift) & dmask) : (1 << RB);
     const uint32_t peers = warp_peers<RB>(d);
     const int leader = __ffs(peers) - 1;
@@ -146,7 +153,7 @@ __global__ void __launch_bounds__(RS2_NT) k_rs_scatter2(const uint64_t* __restri
   for (uint32_t s = tid; s < cnt; s += RS2_NT) {
     const uint64_t kk = sk[s];
     const uint32_t d = (uint32_t)((kk & HASH_BITS_MASK) >> shift) & dmask;
-    const uint64_t dst = goff[(uint64_t)d * ntiles + blockIdx.x] + (s - dstart[d]);
+    const uint64_t dst = s_goff[d] + (s - dstart[d]);
     kout[dst] = kk;
     vout[dst] = sv[s];
   }
@@ -216,15 +223,30 @@ __global__ void __launch_bounds__(1024) k_seg_table(const uint32_t* __restrict__
   if (tid == 1023) *n_bins = before;
 }
 
-__global__ void k_seg_assign(uint64_t* __restrict__ k, uint64_t n, int L, int hbits, const uint2* __restrict__ table) {
+// b(h) into the free key bits above the hash, one RS_TILE tile per CTA; also the tile histogram
+// of the first LSD digit of b (the k_rs_hist of the first pass, fused)
+__global__ void __launch_bounds__(RS_NT) k_seg_assign(uint64_t* __restrict__ k, uint64_t n, int L, int hbits,
+                                                      const uint2* __restrict__ table, uint32_t dmask,
+                                                      uint32_t* hist, uint32_t ntiles) {
+  __shared__ uint32_t hh[1 << BIN_DIGIT];
+  for (int i = threadIdx.x; i < (1 << BIN_DIGIT); i += RS_NT) hh[i] = 0;
+  __syncthreads();
   const uint64_t lmask = (1ull << L) - 1;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t kk = k[i];
-    const uint64_t h = kk & HASH_BITS_MASK;
-    const uint2 t = __ldg(table + (h >> L));
-    const uint64_t b = t.x + (((h & lmask) * t.y) >> L);
-    k[i] = kk | (b << hbits);
+  const uint64_t base = (uint64_t)blockIdx.x * RS_TILE;
+#pragma unroll 4
+  for (int r = 0; r < RS_IPT; r++) {
+    const uint64_t i = base + (uint64_t)r * RS_NT + threadIdx.x;
+    if (i < n) {
+      const uint64_t kk = k[i];
+      const uint64_t h = kk & HASH_BITS_MASK;
+      const uint2 t = __ldg(table + (h >> L));
+      const uint64_t b = t.x + (((h & lmask) * t.y) >> L);
+      k[i] = kk | (b << hbits);
+      atomicAdd(&hh[(uint32_t)b & dmask], 1u);
+    }
   }
+  __syncthreads();
+  for (int d = threadIdx.x; d < (1 << BIN_DIGIT); d += RS_NT) hist[(uint64_t)d * ntiles + blockIdx.x] = hh[d];
 }
 
 __global__ void k_bucket_bounds(const uint64_t* __restrict__ k, uint64_t n, int lo_bits, uint32_t nb, uint64_t* bstart) {
@@ -921,10 +943,10 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
       attr = true;
     }
     const int hbits = 2 * P.k;
-    auto lsd_pass = [&](auto rb, int shift, int bits) {
+    auto lsd_pass = [&](auto rb, int shift, int bits, bool have_hist = false) {
       constexpr int RB = decltype(rb)::value;
       const uint32_t dmask = (1u << bits) - 1;
-      GOD_LAUNCH("k_rs_hist", k_rs_hist<RB>, ntiles, RS_NT, 0, st, k0, n, shift, dmask, hist, ntiles);
+      if (!have_hist) GOD_LAUNCH("k_rs_hist", k_rs_hist<RB>, ntiles, RS_NT, 0, st, k0, n, shift, dmask, hist, ntiles);
       scan_exclusive_u32_to_u64(hist, goff, (uint64_t)(1u << RB) * ntiles, nullptr, st, scr, "scan_sort_hist");
       GOD_LAUNCH("k_rs_scatter2", k_rs_scatter2<RB>, ntiles, RS2_NT, RS_DYN_SMEM, st, k0, v0, k1, v1, n, shift, dmask,
                  goff, ntiles);
@@ -941,8 +963,9 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
       GOD_LAUNCH("k_seg_hist", k_seg_hist, 4u * num_sms(), 512, 0, st, k0, n, L, segc);
       const uint32_t target = (uint32_t)std::max<uint64_t>(BIN_TARGET, n / ((1u << (2 * BIN_DIGIT)) - (1u << SEG_BITS)) + 1);
       GOD_LAUNCH("k_seg_table", k_seg_table, 1, 1024, 0, st, segc, target, table, n_bins_d);
-      GOD_LAUNCH("k_seg_assign", k_seg_assign, grid_for(n, 256), 256, 0, st, k0, n, L, hbits, table);
-      lsd_pass(std::integral_constant<int, BIN_DIGIT>(), hbits, BIN_DIGIT);
+      GOD_LAUNCH("k_seg_assign", k_seg_assign, ntiles, RS_NT, 0, st, k0, n, L, hbits, table, (1u << BIN_DIGIT) - 1, hist,
+                 ntiles);
+      lsd_pass(std::integral_constant<int, BIN_DIGIT>(), hbits, BIN_DIGIT, true);
       lsd_pass(std::integral_constant<int, BIN_DIGIT>(), hbits + BIN_DIGIT, BIN_DIGIT);
       const uint32_t nb = d2h_scalar(n_bins_d, st);
       uint64_t* bstart = scr.alloc<uint64_t>((uint64_t)nb + 1);
