@@ -239,7 +239,6 @@ __global__ void __launch_bounds__(X2_NT, X2_MINB) k_extract2(X2Args a) {
   __shared__ uint64_t skb[X2_NT + 2], scw[X2_NT + 2];
   __shared__ uint32_t sjob[X2_NT];
   __shared__ uint32_t warp_cnt[NWARP];
-  __shared__ uint64_t s_base;
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const uint64_t ntiles = (a.total_blocks + X2_OUT_BLOCKS - 1) / X2_OUT_BLOCKS;
@@ -253,31 +252,26 @@ __global__ void __launch_bounds__(X2_NT, X2_MINB) k_extract2(X2Args a) {
     }
   }
   const uint32_t ks = a.key_shift;
-  int64_t pend_tile = -1;
-  uint32_t pend_cnt = 0;
   int buf = 0;
 
-  // write the staged records of a finished tile (whole CTA); warp 0 resolves its offset first
-  auto flush = [&](uint64_t tile, uint32_t cnt, int b) {
-    if (wid == 0) {
-      uint64_t base;
-      if (a.dbg_flags & 1u) base = lane == 0 ? atomicAdd((unsigned long long*)&a.status[ntiles], (unsigned long long)cnt) : 0;
-      else base = lb_resolve_warp(a.status, tile, cnt);
-      if (lane == 0) {
-        s_base = base;
-        if (tile == ntiles - 1) *a.total_out = base + cnt;
-      }
-    }
-    __syncthreads();
-    const uint64_t base = s_base;
+  // write the staged records of a finished tile: warp 0 alone resolves its output offset (decoupled
+  // look-back) and copies the records out, overlapped with the other warps' sparsify of the next tile
+  auto flush_warp0 = [&](uint64_t tile, uint32_t cnt, int b) {
+    uint64_t base;
+    if (a.dbg_flags & 1u) base = lane == 0 ? atomicAdd((unsigned long long*)&a.status[ntiles], (unsigned long long)cnt) : 0;
+    else base = lb_resolve_warp(a.status, tile, cnt);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (lane == 0 && tile == ntiles - 1) *a.total_out = base + cnt;
     const uint64_t* hzb = HZ2 + (size_t)b * POS;
     const uint32_t* se = SE + (size_t)b * POS;
     const uint32_t* bj = BI + (size_t)b * 4 * X2_NT;
     const uint32_t* bpb = bj + X2_NT;
     const uint32_t* bfirst = bpb + X2_NT;
     const uint32_t* bstart = bfirst + X2_NT;
-    if (a.job_off && bstart[tid]) a.job_off[bj[tid]] = base + bfirst[tid];
-    for (uint32_t r = tid; r < cnt; r += X2_NT) {
+    if (a.job_off)
+      for (int t = lane; t < X2_NT; t += 32)
+        if (bstart[t]) a.job_off[bj[t]] = base + bfirst[t];
+    for (uint32_t r = lane; r < cnt; r += 32) {
       const uint64_t gi = base + r;
       if (gi < a.cap) {
         const int e = se[r] & 0xFFFFu;
@@ -289,24 +283,81 @@ __global__ void __launch_bounds__(X2_NT, X2_MINB) k_extract2(X2Args a) {
     }
   };
 
-  // tiles are claimed in order from an atomic counter, one tile ahead: thread 0 claims the next
-  // tile and prefetches its descriptor while the CTA works on the current one
+  // Warp roles per iteration (tile u): warps 1..3 claim the tile (thread SETUP_TID claims tiles in
+  // order from an atomic counter, one ahead, with the descriptor prefetched), load its job bases
+  // and sparsify it into SMEM (A), synchronising among themselves with named barrier 1; meanwhile
+  // warp 0 finishes tile u-2 (look-back + copy-out from the staging buffer that tile u will reuse).
+  // Then all four warps compute (B-E) and tile u's count is published.
+  constexpr int SETUP_TID = 32;
   uint32_t next_t = 0;
   X2Desc nd{};
-  if (tid == 0) {
+  if (tid == SETUP_TID) {
     next_t = atomicAdd(a.tile_ctr, 1u);
     if (next_t < ntiles) nd = a.desc[next_t];
   }
+  int64_t pend_old = -1, pend_new = -1;
+  uint32_t cnt_old = 0, cnt_new = 0;
   while (true) {
-    if (tid == 0) {
-      T.tile = next_t < ntiles ? next_t : 0xFFFFFFFFu;
-      if (next_t < ntiles) {
-        T.j0 = nd.j0; T.j1 = nd.j1;
-        T.cw_lo = nd.cw_lo; T.cw_hi = nd.cw_hi;
-        T.simple = nd.simple;
-        T.any_n = 0; T.slow = 0;
-        next_t = atomicAdd(a.tile_ctr, 1u);
-        if (next_t < ntiles) nd = a.desc[next_t];
+    if (wid == 0) {
+      if (pend_old >= 0) flush_warp0((uint64_t)pend_old, cnt_old, buf);
+    } else {
+      if (tid == SETUP_TID) {
+        T.tile = next_t < ntiles ? next_t : 0xFFFFFFFFu;
+        if (next_t < ntiles) {
+          T.j0 = nd.j0; T.j1 = nd.j1;
+          T.cw_lo = nd.cw_lo; T.cw_hi = nd.cw_hi;
+          T.simple = nd.simple;
+          T.any_n = 0; T.slow = 0;
+          next_t = atomicAdd(a.tile_ctr, 1u);
+          if (next_t < ntiles) nd = a.desc[next_t];
+        }
+      }
+      asm volatile("bar.sync 1, %0;" ::"r"(X2_NT - 32) : "memory");
+      if (T.tile != 0xFFFFFFFFu) {
+        const uint32_t j0 = T.j0, nj = T.j1 - T.j0 + 1;
+        const uint64_t cw_lo = T.cw_lo;
+        const int nwords = (int)(T.cw_hi - cw_lo);
+        const int t1 = tid - 32, nt1 = X2_NT - 32;
+        // the tile's job bases in SMEM (a tile spans <= NT + 1 jobs: every job owns >= 1 block)
+        for (uint32_t q = t1; q <= nj; q += nt1) {
+          skb[q] = a.kb[j0 + q];
+          scw[q] = a.cw[j0 + q];
+        }
+        asm volatile("bar.sync 1, %0;" ::"r"(X2_NT - 32) : "memory");
+        // ---------------------------------------------------------- A. sparsify into SMEM
+        uint32_t my_n = 0;
+        if (T.simple) {
+          const Job jb = a.jobs[j0];
+          const uint64_t w0 = cw_lo - scw[0];
+          const uint32_t ncode = jb.nk ? jb.nk + K - 1 : 0;
+          const uint64_t A0 = jb.seq_off + jb.phase + a.one0;
+          for (int wi = t1; wi < nwords; wi += nt1) {
+            const uint64_t q0 = (w0 + wi) * 16;
+            uint32_t nm = 0, word = 0;
+            if (q0 < ncode) word = pack16<PS, false>(a.seq, a.seq_bytes, A0 + (uint64_t)PS * q0,
+                                                     (int)min((uint64_t)16, ncode - q0), lut, &nm);
+            codes[wi] = word;
+            nmask[wi] = nm;
+            my_n |= nm;
+          }
+        } else {
+          uint32_t Jw = 0;
+          for (int wi = t1; wi < nwords; wi += nt1) {
+            const uint64_t gw = cw_lo + wi;
+            Jw = find_job_le(scw, Jw, nj - 1, gw);
+            const Job jb = a.jobs[j0 + Jw];
+            const uint64_t ncode = jb.nk ? (uint64_t)jb.nk + K - 1 : 0;
+            const uint64_t q0 = (gw - scw[Jw]) * 16;
+            uint32_t nm = 0, word = 0;
+            if (q0 < ncode)
+              word = pack16<PS, true>(a.seq, a.seq_bytes, jb.seq_off + jb.phase + a.one0 + (uint64_t)PS * q0,
+                                      (int)min((uint64_t)16, ncode - q0), lut, &nm);
+            codes[wi] = word;
+            nmask[wi] = nm;
+            my_n |= nm;
+          }
+        }
+        if (my_n) T.any_n = 1;
       }
     }
     __syncthreads();
@@ -315,14 +366,7 @@ __global__ void __launch_bounds__(X2_NT, X2_MINB) k_extract2(X2Args a) {
     uint64_t* HZ = HZ2 + (size_t)buf * POS;
     const uint32_t j0 = T.j0, j1 = T.j1;
     const uint64_t cw_lo = T.cw_lo;
-    // the tile's job bases in SMEM (a tile spans <= NT + 1 jobs: every job owns >= 1 block)
     const uint32_t nj = j1 - j0 + 1;
-    for (uint32_t q = tid; q <= nj; q += X2_NT) {
-      skb[q] = a.kb[j0 + q];
-      scw[q] = a.cw[j0 + q];
-    }
-    __syncthreads();
-    const int nwords = (int)(T.cw_hi - cw_lo);
 
     // ---- my block: job J, first k-mer index l0
     const int64_t myb = (int64_t)tile * X2_OUT_BLOCKS - 1 + tid;
@@ -335,43 +379,6 @@ __global__ void __launch_bounds__(X2_NT, X2_MINB) k_extract2(X2Args a) {
       nk = a.jobs[J].nk;
     }
     sjob[tid] = blk_in ? J : 0xFFFFFFFFu;  // block -> job (job boundaries are window barriers)
-
-    // ------------------------------------------------------------ A. sparsify into SMEM
-    {
-      uint32_t my_n = 0;
-      if (T.simple) {
-        const Job jb = a.jobs[j0];
-        const uint64_t w0 = cw_lo - a.cw[j0];
-        const uint32_t ncode = jb.nk ? jb.nk + K - 1 : 0;
-        const uint64_t A0 = jb.seq_off + jb.phase + a.one0;
-        for (int wi = tid; wi < nwords; wi += X2_NT) {
-          const uint64_t q0 = (w0 + wi) * 16;
-          uint32_t nm = 0, word = 0;
-          if (q0 < ncode) word = pack16<PS, false>(a.seq, a.seq_bytes, A0 + (uint64_t)PS * q0,
-                                                   (int)min((uint64_t)16, ncode - q0), lut, &nm);
-          codes[wi] = word;
-          nmask[wi] = nm;
-          my_n |= nm;
-        }
-      } else {
-        uint32_t Jw = 0;
-        for (int wi = tid; wi < nwords; wi += X2_NT) {
-          const uint64_t gw = cw_lo + wi;
-          Jw = find_job_le(scw, Jw, nj - 1, gw);
-          const Job jb = a.jobs[j0 + Jw];
-          const uint64_t ncode = jb.nk ? (uint64_t)jb.nk + K - 1 : 0;
-          const uint64_t q0 = (gw - scw[Jw]) * 16;
-          uint32_t nm = 0, word = 0;
-          if (q0 < ncode)
-            word = pack16<PS, true>(a.seq, a.seq_bytes, jb.seq_off + jb.phase + a.one0 + (uint64_t)PS * q0,
-                                    (int)min((uint64_t)16, ncode - q0), lut, &nm);
-          codes[wi] = word;
-          nmask[wi] = nm;
-          my_n |= nm;
-        }
-      }
-      if (__syncthreads_or(my_n != 0) && tid == 0) T.any_n = 1;
-    }
     __syncthreads();
 
     // ------------------------------------------------------------ B. k-mers and hashes
@@ -579,13 +586,21 @@ __global__ void __launch_bounds__(X2_NT, X2_MINB) k_extract2(X2Args a) {
       for (uint32_t r = tid; r < cnt; r += X2_NT) {
         const uint32_t vr = se[r];
         const int er = vr & 0xFFFFu;
-        for (uint32_t q = r + 1; q < cnt; q++) {
-          const uint32_t vq = se[q];
-          if ((int)(vq & 0xFFFFu) - er >= W) break;
-          if ((vq >> 16) == (vr >> 16)) {  // 16 key bits agree: compare the full keys and hashes
-            const uint64_t hr = HZ[er] & ~(1ull << 63), hq = HZ[vq & 0xFFFFu] & ~(1ull << 63);
-            tie |= ((hq >> ks) == (hr >> ks)) & (hq != hr);
+        // later candidates within W positions: three independent SMEM loads per round
+        for (uint32_t q = r + 1; q < cnt; q += 3) {
+          uint32_t vq[3];
+#pragma unroll
+          for (int u = 0; u < 3; u++) vq[u] = q + u < cnt ? se[q + u] : 0xFFFFu;
+          bool more = true;
+#pragma unroll
+          for (int u = 0; u < 3; u++) {
+            if ((int)(vq[u] & 0xFFFFu) - er >= W) { more = false; break; }
+            if ((vq[u] >> 16) == (vr >> 16)) {  // 16 key bits agree: compare the full keys and hashes
+              const uint64_t hr = HZ[er] & ~(1ull << 63), hq = HZ[vq[u] & 0xFFFFu] & ~(1ull << 63);
+              tie |= ((hq >> ks) == (hr >> ks)) & (hq != hr);
+            }
           }
+          if (!more) break;
         }
       }
       if (__syncthreads_or(tie)) {
@@ -597,13 +612,15 @@ __global__ void __launch_bounds__(X2_NT, X2_MINB) k_extract2(X2Args a) {
     }
     // publish this tile's count, then finish the previous tile (its predecessors are done by now)
     if (tid == 0 && !(a.dbg_flags & 1u)) lb_publish(a.status, tile, cnt);
-    if (pend_tile >= 0) flush((uint64_t)pend_tile, pend_cnt, buf ^ 1);
-    pend_tile = tile;
-    pend_cnt = cnt;
+    pend_old = pend_new;
+    cnt_old = cnt_new;
+    pend_new = tile;
+    cnt_new = cnt;
     buf ^= 1;
     __syncthreads();
   }
-  if (pend_tile >= 0) flush((uint64_t)pend_tile, pend_cnt, buf ^ 1);
+  // pend_old was flushed in the last (tile-less) iteration; the newest tile is in buffer buf ^ 1
+  if (pend_new >= 0 && wid == 0) flush_warp0((uint64_t)pend_new, cnt_new, buf ^ 1);
 }
 
 // per-tile descriptors: first and last job (binary searches over the padded bases), the tile's
