@@ -174,8 +174,71 @@ constexpr int BS_NT = 512;
 constexpr int BS_NW = BS_NT / 32;
 constexpr int BS_CAP = 4096;                      // records of a bin held in SMEM (x2 buffers)
 constexpr int BS_IPT = BS_CAP / BS_NT;            // 8
-constexpr int BS_SMEM = 2 * BS_CAP * 8;
+constexpr int BS_SMEM = 2 * BS_CAP * 8 + 4096 * 4;  // + run-count histogram (SMALL_BINS)
 constexpr int SEG_BITS = 12;
+constexpr uint32_t SMALL_BINS = 4096;
+
+// Run statistics (K3) produced by the sort kernels when they can: count histogram (small counts) +
+// list of large counts, number of distinct hashes.  (Per-record run lengths are not stored: the
+// kept-entry pass re-derives each record's run extent from its neighbours, capped at tau + 1.)
+struct RunOut {
+  uint32_t* hist_small;
+  uint32_t* large;
+  uint32_t* n_large;
+  unsigned long long* n_distinct;
+};
+
+// one run [i, i + L) of equal hashes found by a thread: record it (SMEM histogram `h`; runs of
+// length 1, the vast majority, are counted in a register: one SMEM counter would serialise them)
+struct RunAcc {
+  uint32_t nd = 0, ones = 0;
+};
+__device__ __forceinline__ void run_emit(const RunOut& ro, uint32_t* h, uint64_t L, RunAcc& acc) {
+  const uint32_t c = L < 0xFFFFFFFFull ? (uint32_t)L : 0xFFFFFFFFu;
+  if (c == 1) ++acc.ones;
+  else if (c < SMALL_BINS) atomicAdd(&h[c], 1u);
+  else ro.large[atomicAdd(ro.n_large, 1u)] = c;
+  ++acc.nd;
+}
+__device__ __forceinline__ void run_flush(const RunOut& ro, uint32_t* h, RunAcc acc) {
+  for (int o = 16; o; o >>= 1) {
+    acc.nd += __shfl_xor_sync(0xffffffffu, acc.nd, o);
+    acc.ones += __shfl_xor_sync(0xffffffffu, acc.ones, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (acc.nd) atomicAdd(ro.n_distinct, (unsigned long long)acc.nd);
+    if (acc.ones) atomicAdd(&h[1], acc.ones);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < (int)SMALL_BINS; i += blockDim.x)
+    if (h[i]) atomicAdd(&ro.hist_small[i], h[i]);
+}
+// records next to i (excluding i) in one direction with hash hv, capped at lim: galloping then
+// binary search
+__device__ __forceinline__ uint64_t run_side(const uint64_t* __restrict__ k, uint64_t n, uint64_t i, uint64_t hv,
+                                             uint64_t lim, bool fwd, uint64_t hm) {
+  auto same = [&](uint64_t d) -> bool {
+    if (fwd) return i + d < n && (k[i + d] & hm) == hv;
+    return d <= i && (k[i - d] & hm) == hv;
+  };
+  uint64_t good = 0, d = 1;
+  while (d <= lim && same(d)) { good = d; d <<= 1; }
+  uint64_t bad = d <= lim ? d : lim + 1;
+  while (bad - good > 1) {
+    const uint64_t mid = good + (bad - good) / 2;
+    if (same(mid)) good = mid;
+    else bad = mid;
+  }
+  return good;
+}
+
+// length of the run of hash hv containing record i: exact if <= cap, else some value > cap
+__device__ __forceinline__ uint64_t run_len_capped(const uint64_t* __restrict__ k, uint64_t n, uint64_t i, uint64_t hv,
+                                                   uint64_t cap, uint64_t hm) {
+  const uint64_t lim = cap + 1;
+  return 1 + run_side(k, n, i, hv, lim, false, hm) + run_side(k, n, i, hv, lim, true, hm);
+}
+
 constexpr uint32_t BIN_TARGET = 3584;
 constexpr int BIN_DIGIT = 9;                      // LSD digit over b
 constexpr int BIN_INS_MAX = 4;                    // buckets up to this size: insertion sort by one thread
@@ -333,22 +396,30 @@ __device__ __forceinline__ void cta_load_striped(const uint64_t* src, int n, uin
 __global__ void __launch_bounds__(BS_NT, 2) k_bin_sort(uint64_t* __restrict__ k, uint32_t* __restrict__ v,
                                                        const uint64_t* __restrict__ bstart,
                                                        const uint32_t* __restrict__ n_bins, int L, int hbits,
-                                                       uint32_t* big, uint32_t* n_big) {
+                                                       uint32_t* big, uint32_t* n_big, RunOut ro) {
   extern __shared__ __align__(16) unsigned char bs_smem[];
   uint64_t* A = reinterpret_cast<uint64_t*>(bs_smem);
   uint64_t* Bf = A + BS_CAP;
+  uint32_t* rh = reinterpret_cast<uint32_t*>(Bf + BS_CAP);  // [SMALL_BINS] run-count histogram
+  for (int i = threadIdx.x; i < (int)SMALL_BINS; i += BS_NT) rh[i] = 0;
+  __syncthreads();
+  RunAcc racc;
   __shared__ __align__(16) uint32_t cnt[CNT_WORDS];
   __shared__ uint32_t wsum[BS_NW];
   __shared__ uint32_t s_or[BS_NW], s_and[BS_NW];
   __shared__ uint32_t s_big[BS_CAP / (BIN_INS_MAX + 1) + 1];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint64_t lmask = (1ull << L) - 1, hmask = (1ull << hbits) - 1;
+  const uint32_t lmax = (uint32_t)((1ull << (63 - hbits)) - 1);  // run length field above the hash (capped)
   const uint32_t nb = *n_bins;
   for (uint32_t c = blockIdx.x; c < nb; c += gridDim.x) {
     const uint64_t s = bstart[c], e = bstart[c + 1];
     const int n = (int)(e - s);
     if (n <= 1) {
-      if (n == 1 && threadIdx.x == 0) k[s] &= ~(hmask ^ HASH_BITS_MASK);  // strip b
+      if (n == 1 && threadIdx.x == 0) {
+        k[s] = (k[s] & ~(hmask ^ HASH_BITS_MASK)) | (1ull << hbits);  // strip b, run length 1
+        run_emit(ro, rh, 1, racc);
+      }
       continue;
     }
     if (n > BS_CAP) {
@@ -387,7 +458,13 @@ __global__ void __launch_bounds__(BS_NT, 2) k_bin_sort(uint64_t* __restrict__ k,
     const uint64_t segv = wsum[0];
     __syncthreads();
     if (mn == mx) {  // one hash: position order already (the stable passes over b kept it)
-      for (int i = threadIdx.x; i < n; i += BS_NT) k[s + i] &= ~(hmask ^ HASH_BITS_MASK);
+      for (int i = threadIdx.x; i < n; i += BS_NT)
+        k[s + i] = (k[s + i] & ~(hmask ^ HASH_BITS_MASK)) | ((uint64_t)min((uint32_t)n, lmax) << hbits);
+      if (threadIdx.x == 0) {
+        if ((uint32_t)n < SMALL_BINS) atomicAdd(&rh[n], 1u);
+        else ro.large[atomicAdd(ro.n_large, 1u)] = (uint32_t)n;
+        ++racc.nd;
+      }
       __syncthreads();
       continue;
     }
@@ -514,14 +591,64 @@ __global__ void __launch_bounds__(BS_NT, 2) k_bin_sort(uint64_t* __restrict__ k,
       }
       res = dst == A ? Bf : A;
     }
+    // K3 fused: runs never cross a bin (a hash lies in one bin).  Per-element run length from two
+    // block scans over the run-head indices (start = last head <= i, end = first head > i); it is
+    // stored in the key's free bits (capped) for the kept-entry pass, and heads record it in the
+    // count histogram.
+    uint32_t* Lsm = reinterpret_cast<uint32_t*>(res == A ? Bf : A);
+    {
+      // warp w owns items [w*256, w*256+256) as 8 rows of 32 (conflict-free SMEM access)
+      const int wbase = wid * (32 * BS_IPT);
+      uint32_t hm[BS_IPT];
+      int wl = -1, wf = n;  // this warp's last / first head
+#pragma unroll
+      for (int q = 0; q < BS_IPT; q++) {
+        const int idx = wbase + q * 32 + lane;
+        bool h = false;
+        if (idx < n) h = idx == 0 || (uint32_t)(res[idx - 1] >> 33) != (uint32_t)(res[idx] >> 33);
+        hm[q] = __ballot_sync(0xffffffffu, h);
+        if (hm[q]) {
+          wl = wbase + q * 32 + 31 - __clz(hm[q]);
+          if (wf == n) wf = wbase + q * 32 + __ffs(hm[q]) - 1;
+        }
+      }
+      if (lane == 0) { s_or[wid] = (uint32_t)(wl + 1); s_and[wid] = (uint32_t)wf; }
+      __syncthreads();
+      int carry = -1, after = n;
+#pragma unroll
+      for (int q = 0; q < BS_NW; q++) {
+        if (q < wid) carry = max(carry, (int)s_or[q] - 1);
+        if (q > wid) after = min(after, (int)s_and[q]);
+      }
+      const uint32_t le = (lane == 31) ? 0xffffffffu : ((2u << lane) - 1);  // lanes <= lane
+      int st_[BS_IPT];
+#pragma unroll
+      for (int q = 0; q < BS_IPT; q++) {  // start = last head <= idx
+        const uint32_t m = hm[q] & le;
+        st_[q] = m ? wbase + q * 32 + 31 - __clz(m) : carry;
+        if (hm[q]) carry = wbase + q * 32 + 31 - __clz(hm[q]);
+      }
+#pragma unroll
+      for (int q = BS_IPT - 1; q >= 0; q--) {  // next head > idx
+        const uint32_t m = hm[q] & ~le;
+        const int nh = m ? wbase + q * 32 + __ffs(m) - 1 : after;
+        const int idx = wbase + q * 32 + lane;
+        if (idx < n) Lsm[idx] = (uint32_t)(nh - st_[q]);
+        if (hm[q]) after = wbase + q * 32 + __ffs(hm[q]) - 1;
+      }
+    }
+    __syncthreads();
     const uint64_t topv = segv << L;
     for (int i = threadIdx.x; i < n; i += BS_NT) {
       const uint64_t pv = res[i];
-      __stcs(k + s + i, (topv | (pv >> 33)) | ((pv & 1ull) << 63));
+      const uint32_t rlen = Lsm[i];
+      __stcs(k + s + i, (topv | (pv >> 33)) | ((uint64_t)min(rlen, lmax) << hbits) | ((pv & 1ull) << 63));
       __stcs(v + s + i, (uint32_t)(pv >> 1));
+      if (i == 0 || (uint32_t)(res[i - 1] >> 33) != (uint32_t)(pv >> 33)) run_emit(ro, rh, rlen, racc);
     }
     __syncthreads();
   }
+  run_flush(ro, rh, racc);
 }
 
 // oversized bins (repeat-heavy hashes): the same LSD over the low bits, chunk by chunk through
@@ -529,9 +656,13 @@ __global__ void __launch_bounds__(BS_NT, 2) k_bin_sort(uint64_t* __restrict__ k,
 __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort_big(uint64_t* __restrict__ k, uint32_t* __restrict__ v,
                                                               uint64_t* __restrict__ t0, uint64_t* __restrict__ t1,
                                                               const uint64_t* __restrict__ bstart, const uint32_t* big,
-                                                              const uint32_t* n_big, int lo_bits, int hbits) {
+                                                              const uint32_t* n_big, int lo_bits, int hbits, RunOut ro) {
   extern __shared__ __align__(16) unsigned char bs_smem[];
   uint64_t* Bf = reinterpret_cast<uint64_t*>(bs_smem);
+  uint32_t* rh = reinterpret_cast<uint32_t*>(Bf + 2 * BS_CAP);  // [SMALL_BINS] run-count histogram
+  for (int i = threadIdx.x; i < (int)SMALL_BINS; i += BS_NT) rh[i] = 0;
+  __syncthreads();
+  RunAcc racc;
   __shared__ __align__(16) uint32_t cnt[CNT_WORDS];
   __shared__ uint32_t wsum[BS_NW];
   __shared__ uint64_t dbase[RS_BINS];
@@ -589,21 +720,33 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort_big(uint64_t* __restri
       v[s + i] = (uint32_t)(pv >> 1);
     }
     __syncthreads();
+    // K3 fused: every record finds its run's extent in the bin (galloping both ways), stores the
+    // length in the key's free bits (capped) for the kept-entry pass; run heads record it
+    {
+      const uint64_t hm = (1ull << hbits) - 1, lmax = (1ull << (63 - hbits)) - 1;
+      const uint64_t* kb = k + s;
+      for (uint64_t i = threadIdx.x; i < n; i += BS_NT) {
+        const uint64_t hv = kb[i] & hm;
+        const uint64_t back = run_side(kb, n, i, hv, n, false, hm);
+        const uint64_t L = 1 + back + run_side(kb, n, i, hv, n, true, hm);
+        if (back == 0) run_emit(ro, rh, L, racc);
+        k[s + i] = (kb[i] & ~(lmax << hbits)) | ((L < lmax ? L : lmax) << hbits);
+      }
+    }
+    __syncthreads();
   }
+  run_flush(ro, rh, racc);
 }
-
-constexpr uint32_t SMALL_BINS = 4096;
 
 // K3: runs of equal hashes in the sorted records (one run = one distinct hash, P:286 (3)).  The
 // thread holding a run head finds the run end (linear for short runs, exponential + binary search
-// for long ones), writes the run length to every member (rl), and adds it to the count histogram
+// for long ones) and adds its length to the count histogram
 // (SMEM bins for counts < SMALL_BINS, a list for the rare larger ones) used by the cutoff.
-__global__ void k_runs(const uint64_t* __restrict__ k, uint64_t n, uint32_t* rl, uint32_t* hist_small, uint32_t* large,
-                       uint32_t* n_large, unsigned long long* n_distinct) {
+__global__ void k_runs(const uint64_t* __restrict__ k, uint64_t n, RunOut ro) {
   __shared__ uint32_t h[SMALL_BINS];
   for (int i = threadIdx.x; i < (int)SMALL_BINS; i += blockDim.x) h[i] = 0;
   __syncthreads();
-  uint32_t local_nd = 0;
+  RunAcc racc;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t hv = k[i] & HASH_BITS_MASK;
     if (i > 0 && (k[i - 1] & HASH_BITS_MASK) == hv) continue;
@@ -620,18 +763,9 @@ __global__ void k_runs(const uint64_t* __restrict__ k, uint64_t n, uint32_t* rl,
       }
       e = hi;
     }
-    const uint64_t L = e - i;
-    const uint32_t c = L < 0xFFFFFFFFull ? (uint32_t)L : 0xFFFFFFFFu;
-    if (c < SMALL_BINS) atomicAdd(&h[c], 1u);
-    else large[atomicAdd(n_large, 1u)] = c;
-    ++local_nd;
-    for (uint64_t q = i; q < e; q++) rl[q] = c;
+    run_emit(ro, h, e - i, racc);
   }
-  for (int o = 16; o; o >>= 1) local_nd += __shfl_xor_sync(0xffffffffu, local_nd, o);
-  if ((threadIdx.x & 31) == 0 && local_nd) atomicAdd(n_distinct, (unsigned long long)local_nd);
-  __syncthreads();
-  for (int i = threadIdx.x; i < (int)SMALL_BINS; i += blockDim.x)
-    if (h[i]) atomicAdd(&hist_small[i], h[i]);
+  run_flush(ro, h, racc);
 }
 
 struct CutState {
@@ -723,7 +857,7 @@ __global__ void __launch_bounds__(1024) k_tau(const uint32_t* hist_small, const 
 // Writes the entry (pos << 32 | low hash << 1 | strand) and its directory slot.
 constexpr int KW_NT = 256, KW_IPT = 16, KW_TILE = KW_NT * KW_IPT;
 __global__ void __launch_bounds__(KW_NT) k_keep_write(const uint64_t* __restrict__ k, const uint32_t* __restrict__ pos,
-                                                      const uint32_t* __restrict__ rl, uint64_t n, const CutState* cs,
+                                                      uint64_t n, int hbits, const CutState* cs,
                                                       IndexView iv, uint64_t* ent, uint32_t* kslot, uint64_t* status,
                                                       uint32_t* tile_ctr) {
   __shared__ uint32_t s_tile;
@@ -734,13 +868,20 @@ __global__ void __launch_bounds__(KW_NT) k_keep_write(const uint64_t* __restrict
   __syncthreads();
   const uint64_t tile = s_tile;
   const uint64_t tau = cs->tau;
+  const uint64_t hm = (1ull << hbits) - 1, lmax = (1ull << (63 - hbits)) - 1;
   const uint64_t base = tile * KW_TILE + (uint64_t)wid * (32 * KW_IPT);
   uint32_t masks[KW_IPT];
   uint32_t wc = 0;
-#pragma unroll
+#pragma unroll 4
   for (int j = 0; j < KW_IPT; j++) {
     const uint64_t i = base + (uint64_t)j * 32 + lane;
-    const bool keep = i < n && rl[i] <= tau;
+    bool keep = false;
+    if (i < n) {
+      const uint64_t v = k[i];
+      const uint64_t rlf = (v >> hbits) & lmax;  // run length from the bin sort (0: not recorded)
+      if (rlf != 0 && (rlf < lmax || tau < lmax)) keep = rlf <= tau;
+      else keep = run_len_capped(k, n, i, v & hm, tau, hm) <= tau;
+    }
     masks[j] = __ballot_sync(0xffffffffu, keep);
     wc += __popc(masks[j]);
   }
@@ -769,7 +910,7 @@ __global__ void __launch_bounds__(KW_NT) k_keep_write(const uint64_t* __restrict
     if ((m >> lane) & 1u) {
       const uint64_t i = base + (uint64_t)j * 32 + lane;
       const uint64_t v = k[i];
-      const uint64_t h = v & HASH_BITS_MASK;
+      const uint64_t h = v & hm;
       const uint64_t d = run + __popc(m & lt);
       ent[d] = ((uint64_t)pos[i] << 32) | ((h & lowmask) << 1) | (v >> 63);
       kslot[d] = (uint32_t)index_slot(iv, h);
@@ -928,6 +1069,17 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
   uint64_t* k0 = rec.hz;
   uint32_t* v0 = rec.pos;
   uint32_t* segc = nullptr;  // records per top-12-bit hash segment (bin sort and directory map)
+  // K3 outputs (filled by the bin sort when it runs, else by k_runs)
+  RunOut ro;
+  ro.hist_small = scr.alloc<uint32_t>(SMALL_BINS);
+  ro.large = scr.alloc<uint32_t>(n / SMALL_BINS + 1);
+  ro.n_large = scr.alloc<uint32_t>(1);
+  uint64_t* nd_d = scr.alloc<uint64_t>(1);
+  ro.n_distinct = reinterpret_cast<unsigned long long*>(nd_d);
+  GOD_CUDA(cudaMemsetAsync(ro.hist_small, 0, SMALL_BINS * sizeof(uint32_t), st));
+  GOD_CUDA(cudaMemsetAsync(ro.n_large, 0, sizeof(uint32_t), st));
+  GOD_CUDA(cudaMemsetAsync(nd_d, 0, sizeof(uint64_t), st));
+  bool runs_done = false;
   if (n > 1) {
     uint64_t* k1 = scr.alloc<uint64_t>(n);
     uint32_t* v1 = scr.alloc<uint32_t>(n);
@@ -975,34 +1127,28 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
       GOD_LAUNCH("k_bucket_bounds", k_bucket_bounds, grid_for((uint64_t)nb + 1, 256), 256, 0, st, k0, n, hbits, nb,
                  bstart);
       GOD_LAUNCH("k_bin_sort", k_bin_sort, 2u * num_sms(), BS_NT, BS_SMEM, st, k0, v0, bstart, n_bins_d, L, hbits, big,
-                 n_big);
+                 n_big, ro);
+      runs_done = true;
       const uint32_t hb_big = d2h_scalar(n_big, st);
       if (getenv("GOD_DEBUG_BUCKETS"))
         fprintf(stderr, "[bins] n=%llu bins=%u target=%u big=%u lsd=%u\n", (unsigned long long)n, nb, target, hb_big,
                 d2h_scalar(n_big + 1, st));
       if (hb_big)
         GOD_LAUNCH("k_bucket_sort_big", k_bucket_sort_big, std::min(hb_big, (uint32_t)num_sms()), BS_NT, BS_SMEM, st, k0,
-                   v0, /*t0=*/k1, /*t1=*/k0, bstart, big, n_big, L, hbits);
+                   v0, /*t0=*/k1, /*t1=*/k0, bstart, big, n_big, L, hbits, ro);
     } else {
       // K2 full stable LSD over the 2k hash bits (position order kept within equal hashes)
       for (int shift = 0; shift < hbits; shift += RS_BITS)
         lsd_pass(std::integral_constant<int, RS_BITS>(), shift, std::min(RS_BITS, hbits - shift));
     }
   }
-  // K3: runs (distinct hashes) + count histogram; K4: tau and the kept totals
-  uint32_t* rl = scr.alloc<uint32_t>(n ? n : 1);
-  uint32_t* hist_small = scr.alloc<uint32_t>(SMALL_BINS);
-  const uint64_t large_cap = n / SMALL_BINS + 1;
-  uint32_t* large = scr.alloc<uint32_t>(large_cap);
-  uint32_t* n_large = scr.alloc<uint32_t>(1);
-  uint64_t* nd_d = scr.alloc<uint64_t>(1);
+  // K3: runs (distinct hashes) + count histogram (unless the bin sort produced them); K4: tau
+  uint32_t* hist_small = ro.hist_small;
+  uint32_t* large = ro.large;
+  uint32_t* n_large = ro.n_large;
   CutState* cs = scr.alloc<CutState>(1);
-  GOD_CUDA(cudaMemsetAsync(hist_small, 0, SMALL_BINS * sizeof(uint32_t), st));
-  GOD_CUDA(cudaMemsetAsync(n_large, 0, sizeof(uint32_t), st));
-  GOD_CUDA(cudaMemsetAsync(nd_d, 0, sizeof(uint64_t), st));
-  if (n)
-    GOD_LAUNCH("k_runs", k_runs, min(grid_for(n, 512), 8u * num_sms()), 512, 0, st, k0, n, rl, hist_small, large, n_large,
-               reinterpret_cast<unsigned long long*>(nd_d));
+  if (n && !runs_done)
+    GOD_LAUNCH("k_runs", k_runs, min(grid_for(n, 512), 8u * num_sms()), 512, 0, st, k0, n, ro);
   GOD_LAUNCH("k_tau", k_tau, 1, 1024, 0, st, hist_small, large, n_large, nd_d, n, cut.mode, cut.frac_num, cut.frac_den, cut.max_occ, cs);
   CutState hcs;
   GOD_CUDA(cudaMemcpyAsync(&hcs, cs, sizeof(CutState), cudaMemcpyDeviceToHost, st));
@@ -1066,8 +1212,8 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
     uint32_t* kctr = scr.alloc<uint32_t>(1);
     GOD_CUDA(cudaMemsetAsync(kst, 0, tiles * sizeof(uint64_t), st));
     GOD_CUDA(cudaMemsetAsync(kctr, 0, sizeof(uint32_t), st));
-    GOD_LAUNCH("k_keep_write", k_keep_write, (unsigned)tiles, KW_NT, 0, st, k0, v0, rl, n, cs, ix->view(), ix->ent, kslot,
-               kst, kctr);
+    GOD_LAUNCH("k_keep_write", k_keep_write, (unsigned)tiles, KW_NT, 0, st, k0, v0, n, (int)(2 * P.k), cs, ix->view(),
+               ix->ent, kslot, kst, kctr);
   }
   {
     const uint64_t nd1 = n_slots + 1;
@@ -1092,7 +1238,7 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
       if (fp) { fwrite(h.data(), 1, bytes, fp); fclose(fp); }
     };
     dump("rec_hz", rec.hz, n * 8); dump("sorted_hz", k0, n * 8); dump("sorted_pos", v0, n * 4);
-    dump("rl", rl, n * 4); dump("kslot", kslot, n_kept * 4);
+    dump("kslot", kslot, n_kept * 4);
     dump("ent", ix->ent, n_kept * 8); dump("dir", ix->dir, n_slots * sizeof(DirRec));
   }
 }
