@@ -403,10 +403,18 @@ __global__ void __launch_bounds__(X2_NT, X2_MINB) k_extract2(X2Args a) {
     uint32_t key[W];
     uint32_t palmask = 0;
     const uint32_t nvalid = blk_has_kmers ? min((uint32_t)W, nk - l0) : 0u;
+    // the first k-mer of the block is extracted, the others rolled: fwd gains the entering base
+    // as its least significant digit, rev its complement as the most significant (O4)
+    constexpr uint64_t KMASK = (K >= 32) ? ~0ull : ((1ull << (2 * K)) - 1);
+    uint64_t fwd = ext_bits(win, 0, 2 * K);
+    uint64_t rev = ext_bits(rcw, PADB + 2 * (NB - K), 2 * K);
 #pragma unroll
     for (int i = 0; i < W; i++) {
-      const uint64_t fwd = ext_bits(win, 2 * i, 2 * K);
-      const uint64_t rev = ext_bits(rcw, PADB + 2 * (NB - i - K), 2 * K);
+      if (i > 0) {
+        const uint64_t c = ext_bits(win, 2 * (i + K - 1), 2);
+        fwd = ((fwd << 2) | c) & KMASK;
+        rev = (rev >> 2) | ((c ^ 3ull) << (2 * K - 2));
+      }
       const bool z = fwd > rev;
       const uint64_t h = wang_hash_k<K>(z ? rev : fwd);
       HZ[tid * W + i] = h | ((uint64_t)z << 63);
