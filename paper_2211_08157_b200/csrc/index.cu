@@ -241,7 +241,7 @@ __device__ __forceinline__ uint64_t run_len_capped(const uint64_t* __restrict__ 
 
 constexpr uint32_t BIN_TARGET = 3584;
 constexpr int BIN_DIGIT = 9;                      // LSD digit over b
-constexpr int BIN_INS_MAX = 4;                    // buckets up to this size: insertion sort by one thread
+constexpr int BIN_RANK_MAX = 32;                  // buckets up to this size: ranked by counting
 static_assert(RS_BINS * BS_NW == BS_NT * 8, "block scan assumes 8 counters per thread");
 
 __global__ void k_seg_hist(const uint64_t* __restrict__ k, uint64_t n, int L, uint32_t* segc) {
@@ -407,7 +407,7 @@ __global__ void __launch_bounds__(BS_NT, 2) k_bin_sort(uint64_t* __restrict__ k,
   __shared__ __align__(16) uint32_t cnt[CNT_WORDS];
   __shared__ uint32_t wsum[BS_NW];
   __shared__ uint32_t s_or[BS_NW], s_and[BS_NW];
-  __shared__ uint32_t s_big[BS_CAP / (BIN_INS_MAX + 1) + 1];
+  __shared__ uint32_t s_big[BS_CAP / (BIN_RANK_MAX + 1) + 1];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint64_t lmask = (1ull << L) - 1, hmask = (1ull << hbits) - 1;
   const uint32_t lmax = (uint32_t)((1ull << (63 - hbits)) - 1);  // run length field above the hash (capped)
@@ -522,22 +522,20 @@ __global__ void __launch_bounds__(BS_NT, 2) k_bin_sort(uint64_t* __restrict__ k,
       }
       if (threadIdx.x == 0) wsum[0] = 0;
       __syncthreads();
-      // cnt[b] is now the end of bucket b.  Buckets of <= BIN_INS_MAX records: insertion sort by the owning
-      // thread; larger ones: listed for the warps below
-      uint32_t* biglist = s_big;  // buckets of more than BIN_INS_MAX records
-#pragma unroll 1
-      for (int q = 0; q < 8; q++) {
-        const int b2 = threadIdx.x * 8 + q;
+      // cnt[b] is now the end of bucket b.  Every element of a bucket of <= BIN_RANK_MAX records
+      // takes its rank in the bucket by counting smaller values (unique: they contain pos) and moves
+      // to Bf; larger buckets (a frequent hash) are listed for the warps below
+      uint32_t* biglist = s_big;
+      for (int p = threadIdx.x; p < n; p += BS_NT) {
+        const uint64_t xv = A[p];
+        const uint32_t b2 = ((uint32_t)(xv >> 33) - mn) >> shb;
         const int st = b2 ? (int)cnt[b2 - 1] : 0, en = (int)cnt[b2];
-        if (en - st > BIN_INS_MAX) {
-          biglist[atomicAdd(&wsum[0], 1u)] = (uint32_t)b2;
-          continue;
-        }
-        for (int i = st + 1; i < en; i++) {
-          const uint64_t t2 = A[i];
-          int j2 = i - 1;
-          while (j2 >= st && A[j2] > t2) { A[j2 + 1] = A[j2]; --j2; }
-          A[j2 + 1] = t2;
+        if (en - st <= BIN_RANK_MAX) {
+          int rank = 0;
+          for (int q = st; q < en; q++) rank += A[q] < xv;
+          Bf[st + rank] = xv;
+        } else if (p == st) {
+          biglist[atomicAdd(&wsum[0], 1u)] = b2;
         }
       }
       __syncthreads();
@@ -573,10 +571,11 @@ __global__ void __launch_bounds__(BS_NT, 2) k_bin_sort(uint64_t* __restrict__ k,
               __syncwarp();
             }
           }
+          for (int t = lane; t < sz; t += 32) Bf[st + t] = a2[t];
         }
         __syncthreads();
       }
-      res = A;
+      res = Bf;
     } else {
       // (2) a bucket with > 1024 records (a very frequent hash): stable LSD over the low(h) digits below
       //     the highest bit where mn and mx differ (bits above it are constant in the bin)
