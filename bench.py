@@ -423,11 +423,15 @@ def run_e2e(god, torch, cfg, pattern, k, w, n_anchors, steps, dist, world, dev):
         dist.barrier()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
+    walls = []
     for _ in range(steps):
+        t0 = time.perf_counter()
         L.god_index_free(one())
+        walls.append(round((time.perf_counter() - t0) * 1e3, 1))
     e.record()
     torch.cuda.synchronize()
     ms = s.elapsed_time(e)
+    log(f"e2e wall ms per step: {walls}")
     ms = max_over_ranks(ms, dist, dev)
     h2d = cfg.ref.size + cfg.ref_offsets.nbytes + cfg.reads.seq.size + cfg.reads.offsets.nbytes
     d2h = int(need.value) * 16 + (n + 1) * 8 + n
