@@ -107,17 +107,18 @@ __device__ __forceinline__ uint64_t wang_hash_k(uint64_t key) {
 // per-tile descriptor, precomputed by k_x2_tile_desc so that a CTA never walks a dependent chain
 // of global loads (tile -> jobs -> code-word range) while its other warps wait at a barrier
 struct __align__(16) X2Desc {
-  uint32_t j0, j1, simple, pad;
+  uint32_t j0, j1, simple, safe;  // safe: every byte the tile may read is inside the buffer
   uint64_t cw_lo, cw_hi;
 };
 
 struct X2Tile {  // per-tile scalars, in SMEM
-  uint32_t tile, j0, j1, simple, any_n, slow, cnt;
+  uint32_t tile, j0, j1, simple, safe, any_n, slow, cnt;
   uint64_t cw_lo, cw_hi;
 };
 
 template <int K, int W, int PS>
 struct X2Cfg {
+  static_assert(X2_NT * W < 4096, "staged record index must fit 12 bits (block info packing)");
   static constexpr int NB = W + K - 1;                 // bases in a thread's window
   static constexpr int NWIN = (2 * NB + 31) / 32;       // aligned window words
   static constexpr int NLOAD = (30 + 2 * NB + 31) / 32; // words loaded before alignment
@@ -130,8 +131,8 @@ struct X2Cfg {
   static constexpr size_t O_XCHG = O_NMASK + (size_t)MAXWORDS * 4;
   static constexpr size_t O_HZ = (O_XCHG + 2 * (X2_NT / 32) * W * 4 + 15) / 16 * 16;  // [2][POS] hz
   static constexpr size_t O_SE = O_HZ + 2 * (size_t)POS * 8;      // [2][POS] selected: e | key16 << 16
-  static constexpr size_t O_BI = O_SE + 2 * (size_t)POS * 4;      // block info [2][4][NT]
-  static constexpr size_t SMEM = (O_BI + 2 * 4 * X2_NT * 4 + 15) / 16 * 16;
+  static constexpr size_t O_BI = O_SE + 2 * (size_t)POS * 4;      // block info [2][2][NT]
+  static constexpr size_t SMEM = (O_BI + 2 * 2 * X2_NT * 4 + 15) / 16 * 16;
 };
 
 // 16 patterned bases (MSB-first 2-bit codes) from the ASCII bytes at A (a PS-strided gather);
@@ -234,9 +235,15 @@ __global__ void __launch_bounds__(X2_NT, X2_MINB) k_extract2(X2Args a) {
   uint32_t* xsf = xpf + NWARP * W;
   uint64_t* HZ2 = reinterpret_cast<uint64_t*>(x2_smem + C::O_HZ);    // [2][POS]
   uint32_t* SE = reinterpret_cast<uint32_t*>(x2_smem + C::O_SE);     // [2][POS]
-  uint32_t* BI = reinterpret_cast<uint32_t*>(x2_smem + C::O_BI);     // [2][4][NT]: job, pos base, first, start
+  // block info [2][2][NT]: pos base | first staged record (12 bits) + job start flag << 12 + job - j0 << 13
+  uint32_t* BI = reinterpret_cast<uint32_t*>(x2_smem + C::O_BI);
+  __shared__ uint32_t s_bj0[2];  // j0 of the tile staged in each buffer
   __shared__ X2Tile T;
   __shared__ uint64_t skb[X2_NT + 2], scw[X2_NT + 2];
+  __shared__ uint64_t sjb[X2_NT + 2];  // per job of the tile: byte address of its first patterned base
+  __shared__ uint32_t sjn[X2_NT + 2];  // ... its k-mer count n_k
+  __shared__ uint32_t sjp[X2_NT + 2];  // ... its output position base (pos_base + phase + one0)
+  __shared__ uint8_t swj[(X2Cfg<K, W, PS>::MAXWORDS + 3) / 4 * 4];  // code word -> job (relative)
   __shared__ uint32_t sjob[X2_NT];
   __shared__ uint32_t warp_cnt[NWARP];
 
@@ -264,13 +271,14 @@ __global__ void __launch_bounds__(X2_NT, X2_MINB) k_extract2(X2Args a) {
     if (lane == 0 && tile == ntiles - 1) *a.total_out = base + cnt;
     const uint64_t* hzb = HZ2 + (size_t)b * POS;
     const uint32_t* se = SE + (size_t)b * POS;
-    const uint32_t* bj = BI + (size_t)b * 4 * X2_NT;
-    const uint32_t* bpb = bj + X2_NT;
-    const uint32_t* bfirst = bpb + X2_NT;
-    const uint32_t* bstart = bfirst + X2_NT;
+    const uint32_t* bpb = BI + (size_t)b * 2 * X2_NT;
+    const uint32_t* binf = bpb + X2_NT;
+    const uint32_t bj0 = s_bj0[b];
     if (a.job_off)
-      for (int t = lane; t < X2_NT; t += 32)
-        if (bstart[t]) a.job_off[bj[t]] = base + bfirst[t];
+      for (int t = lane; t < X2_NT; t += 32) {
+        const uint32_t f = binf[t];
+        if ((f >> 12) & 1u) a.job_off[bj0 + (f >> 13)] = base + (f & 0xFFFu);
+      }
     for (uint32_t r = lane; r < cnt; r += 32) {
       const uint64_t gi = base + r;
       if (gi < a.cap) {
@@ -278,7 +286,7 @@ __global__ void __launch_bounds__(X2_NT, X2_MINB) k_extract2(X2Args a) {
         const int blk = e / W;
         a.out_hz[gi] = hzb[e];
         a.out_pos[gi] = bpb[blk] + (uint32_t)PS * (uint32_t)(e - blk * W);
-        if (a.out_job) a.out_job[gi] = bj[blk];
+        if (a.out_job) a.out_job[gi] = bj0 + (binf[blk] >> 13);
       }
     }
   };
@@ -307,6 +315,7 @@ __global__ void __launch_bounds__(X2_NT, X2_MINB) k_extract2(X2Args a) {
           T.j0 = nd.j0; T.j1 = nd.j1;
           T.cw_lo = nd.cw_lo; T.cw_hi = nd.cw_hi;
           T.simple = nd.simple;
+          T.safe = nd.safe;
           T.any_n = 0; T.slow = 0;
           next_t = atomicAdd(a.tile_ctr, 1u);
           if (next_t < ntiles) nd = a.desc[next_t];
@@ -322,8 +331,21 @@ __global__ void __launch_bounds__(X2_NT, X2_MINB) k_extract2(X2Args a) {
         for (uint32_t q = t1; q <= nj; q += nt1) {
           skb[q] = a.kb[j0 + q];
           scw[q] = a.cw[j0 + q];
+          if (q < nj) {
+            const Job jq = a.jobs[j0 + q];
+            sjb[q] = jq.seq_off + jq.phase + a.one0;
+            sjn[q] = jq.nk;
+            sjp[q] = (uint32_t)(jq.pos_base + jq.phase + a.one0);
+          }
         }
         asm volatile("bar.sync 1, %0;" ::"r"(X2_NT - 32) : "memory");
+        if (!T.simple) {  // code word -> job, filled job by job
+          for (uint32_t q = t1; q < nj; q += nt1) {
+            const int64_t w0 = (int64_t)scw[q] - (int64_t)cw_lo, w1 = (int64_t)scw[q + 1] - (int64_t)cw_lo;
+            for (int64_t wi = w0 < 0 ? 0 : w0; wi < w1 && wi < nwords; wi++) swj[wi] = (uint8_t)q;
+          }
+          asm volatile("bar.sync 1, %0;" ::"r"(X2_NT - 32) : "memory");
+        }
         // ---------------------------------------------------------- A. sparsify into SMEM
         uint32_t my_n = 0;
         if (T.simple) {
@@ -341,17 +363,19 @@ __global__ void __launch_bounds__(X2_NT, X2_MINB) k_extract2(X2Args a) {
             my_n |= nm;
           }
         } else {
-          uint32_t Jw = 0;
+          const bool safe = T.safe;
           for (int wi = t1; wi < nwords; wi += nt1) {
-            const uint64_t gw = cw_lo + wi;
-            Jw = find_job_le(scw, Jw, nj - 1, gw);
-            const Job jb = a.jobs[j0 + Jw];
-            const uint64_t ncode = jb.nk ? (uint64_t)jb.nk + K - 1 : 0;
-            const uint64_t q0 = (gw - scw[Jw]) * 16;
+            const uint32_t Jw = swj[wi];
+            const uint64_t nkq = sjn[Jw];
+            const uint64_t ncode = nkq ? nkq + K - 1 : 0;
+            const uint64_t q0 = (cw_lo + wi - scw[Jw]) * 16;
             uint32_t nm = 0, word = 0;
-            if (q0 < ncode)
-              word = pack16<PS, true>(a.seq, a.seq_bytes, jb.seq_off + jb.phase + a.one0 + (uint64_t)PS * q0,
-                                      (int)min((uint64_t)16, ncode - q0), lut, &nm);
+            if (q0 < ncode) {
+              const uint64_t A = sjb[Jw] + (uint64_t)PS * q0;
+              const int nb = (int)min((uint64_t)16, ncode - q0);
+              word = safe ? pack16<PS, false>(a.seq, a.seq_bytes, A, nb, lut, &nm)
+                          : pack16<PS, true>(a.seq, a.seq_bytes, A, nb, lut, &nm);
+            }
             codes[wi] = word;
             nmask[wi] = nm;
             my_n |= nm;
@@ -376,7 +400,7 @@ __global__ void __launch_bounds__(X2_NT, X2_MINB) k_extract2(X2Args a) {
       const uint64_t g = (uint64_t)myb * W;
       J = (j0 == j1) ? j0 : j0 + find_job_le(skb, 0, nj - 1, g);
       l0 = (uint32_t)(g - skb[J - j0]);
-      nk = a.jobs[J].nk;
+      nk = sjn[J - j0];
     }
     sjob[tid] = blk_in ? J : 0xFFFFFFFFu;  // block -> job (job boundaries are window barriers)
     __syncthreads();
@@ -554,7 +578,7 @@ __global__ void __launch_bounds__(X2_NT, X2_MINB) k_extract2(X2Args a) {
 
     // ------------------------------------------------------------ E. compaction into staging[buf]
     uint32_t* se = SE + (size_t)buf * POS;
-    uint32_t* bi = BI + (size_t)buf * 4 * X2_NT;
+    uint32_t* bi = BI + (size_t)buf * 2 * X2_NT;
     auto compact = [&]() -> uint32_t {
       const uint32_t cnt = __popc(selmask);
       uint32_t incl = cnt;
@@ -573,10 +597,9 @@ __global__ void __launch_bounds__(X2_NT, X2_MINB) k_extract2(X2Args a) {
         total += c;
       }
       uint32_t idx = before + incl - cnt;
-      bi[tid] = J;
-      bi[X2_NT + tid] = (uint32_t)(a.jobs[J].pos_base + a.jobs[J].phase + a.one0) + (uint32_t)PS * l0;
-      bi[2 * X2_NT + tid] = idx;
-      bi[3 * X2_NT + tid] = (blk_in && tid > 0 && tid < X2_NT - 1 && l0 == 0) ? 1u : 0u;
+      bi[tid] = sjp[J - j0] + (uint32_t)PS * l0;
+      bi[X2_NT + tid] = idx | ((blk_in && tid > 0 && tid < X2_NT - 1 && l0 == 0) ? 1u << 12 : 0u) | ((J - j0) << 13);
+      if (tid == 0) s_bj0[buf] = j0;
       uint32_t m = selmask;
       while (m) {
         const int i = __ffs(m) - 1;
@@ -652,11 +675,14 @@ __global__ void k_x2_tile_desc(const uint64_t* __restrict__ kb, const uint64_t* 
     if (hi > lo + (uint64_t)maxwords) hi = lo + maxwords;
     const Job jb = jobs[j0];
     const uint64_t last_byte = jb.seq_off + jb.phase + one0 + (uint64_t)PS * 16 * (hi - cw[j0]) + 4 * PS + 8;
+    // jobs are in sequence-buffer order: the tile's last bytes are those of job j1
+    const Job jl = jobs[j1];
+    const uint64_t last_l = jl.seq_off + jl.phase + one0 + (uint64_t)PS * 16 * (hi - cw[j1]) + 4 * PS + 8;
     X2Desc d;
     d.j0 = j0;
     d.j1 = j1;
     d.simple = (j0 == j1) && last_byte <= seq_bytes;
-    d.pad = 0;
+    d.safe = last_l <= seq_bytes && last_byte <= seq_bytes;
     d.cw_lo = lo;
     d.cw_hi = hi;
     desc[t] = d;

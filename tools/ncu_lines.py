@@ -1,10 +1,12 @@
 """Per-source-line stall samples / instructions from an ncu report (cuda,sass mixed source page).
-usage: python tools/ncu_lines.py REPORT [N] [KERNEL_REGEX]"""
+usage: python tools/ncu_lines.py REPORT [N] [KERNEL_REGEX] [LAUNCH_SKIP]"""
 import csv, subprocess, sys
 from collections import defaultdict
 rep = sys.argv[1]
 N = int(sys.argv[2]) if len(sys.argv) > 2 else 30
 flt = ["--kernel-name", "regex:" + sys.argv[3], "--launch-count", "1"] if len(sys.argv) > 3 else []
+if len(sys.argv) > 4:
+    flt += ["--launch-skip", sys.argv[4]]
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"] + flt,
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(out.splitlines()))
