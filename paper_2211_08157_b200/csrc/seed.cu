@@ -98,6 +98,64 @@ __global__ void k_anchor_count(IndexView v, const uint64_t* __restrict__ hz, uin
   }
 }
 
+// S4 fast path (every read's PQ_a records are its phase-a job of S1, each <= ~40 records): a group
+// of 8 lanes per read sums its records' probe counts, and after the scan writes its anchors (each
+// lane one record at a time, offsets by a group scan), so no read-ordered copy of the records is made.
+constexpr int RG = 8;
+__global__ void k_read_anchor_counts1(const uint32_t* __restrict__ cnt, const uint64_t* __restrict__ job_off,
+                                      const uint8_t* __restrict__ phases, uint32_t p, uint32_t n_reads, uint64_t* out) {
+  const uint32_t l = threadIdx.x & (RG - 1);
+  for (uint64_t g = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / RG; g < n_reads;
+       g += (uint64_t)gridDim.x * blockDim.x / RG) {
+    const uint32_t r = (uint32_t)g;
+    const uint64_t j = (uint64_t)r * p + phases[r];
+    const uint64_t b = job_off[j], e = job_off[j + 1];
+    uint64_t acc = 0;
+    for (uint64_t q = b + l; q < e; q += RG) acc += cnt[q];
+#pragma unroll
+    for (int d = RG / 2; d; d >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, d, RG);
+    if (l == 0) out[r] = acc;
+  }
+}
+__global__ void k_anchor_write1(IndexView v, const uint64_t* __restrict__ hz, const uint32_t* __restrict__ pos,
+                                const uint32_t* __restrict__ cnt, const uint32_t* __restrict__ beg,
+                                const uint64_t* __restrict__ job_off, const uint8_t* __restrict__ phases, uint32_t p,
+                                uint32_t n_reads, const uint64_t* __restrict__ aoff, god_anchor* out) {
+  const uint32_t l = threadIdx.x & (RG - 1);
+  for (uint64_t g = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / RG; g < n_reads;
+       g += (uint64_t)gridDim.x * blockDim.x / RG) {
+    const uint32_t r = (uint32_t)g;
+    const uint64_t j = (uint64_t)r * p + phases[r];
+    const uint64_t b = job_off[j], e = job_off[j + 1];
+    uint64_t o = aoff[r];
+    for (uint64_t q0 = b; q0 < e; q0 += RG) {  // uniform trip count within the group
+      const uint64_t q = q0 + l;
+      const uint32_t c = q < e ? cnt[q] : 0u;
+      uint32_t incl = c;
+#pragma unroll
+      for (int d = 1; d < RG; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d, RG);
+        if (l >= (uint32_t)d) incl += y;
+      }
+      const uint32_t tot = __shfl_sync(0xffffffffu, incl, RG - 1, RG);
+      if (c) {
+        const uint32_t bg = beg[q], qp = pos[q], qz = (uint32_t)(hz[q] >> 63);
+        uint64_t oo = o + incl - c;
+        for (uint32_t t2 = 0; t2 < c; t2++, oo++) {
+          const uint64_t en = __ldg(v.ent + bg + t2);
+          god_anchor an;
+          an.ref_pos = (uint32_t)(en >> 32);
+          an.read_pos = qp;
+          an.read_id = r;
+          an.strand = ((uint32_t)en & 1u) ^ qz;
+          out[oo] = an;
+        }
+      }
+      o += tot;
+    }
+  }
+}
+
 // one thread per read minimizer: its anchors are the kept entries [beg, beg + cnt)
 __global__ void k_anchor_write(IndexView v, const uint32_t* __restrict__ pos, const uint32_t* __restrict__ rid,
                                const uint64_t* __restrict__ hz, uint64_t n, const uint64_t* __restrict__ aoff,
@@ -242,6 +300,7 @@ uint64_t seed_reads(const god_index* ix, const uint8_t* reads, const uint64_t* o
   GOD_CUDA(cudaMemsetAsync(src, 0, n_reads, st));
   // ---------------- S1/S2: pattern alignment
   bool have_phase_records = false;
+  uint32_t nr = 0;
   Records rec1, rec2, rec3;
   JobSet js1;
   if (mode == GOD_PHASE_SELECT) {
@@ -258,7 +317,7 @@ uint64_t seed_reads(const god_index* ix, const uint8_t* reads, const uint64_t* o
       probe_all(v, rec1, st, scr);
       GOD_LAUNCH("k_phase", k_phase, grid_for(n_reads, 128), 128, 0, st, rec1.cnt, js1.jobs, rec1.job_off, rec1.hz,
                  rec1.pos, nullptr, n_reads, p, t, P.w, kcap, P.pat, P.k, phases, redo, n_redo);
-      const uint32_t nr = d2h_scalar(n_redo, st);
+      nr = d2h_scalar(n_redo, st);
       if (nr) {  // uncapped phase selection for reads whose capped prefix was not enough
         Job* jobs2 = scr.alloc<Job>((uint64_t)nr * p);
         uint64_t* kb2 = scr.alloc<uint64_t>((uint64_t)nr * p + 1);
@@ -309,6 +368,19 @@ uint64_t seed_reads(const god_index* ix, const uint8_t* reads, const uint64_t* o
     }
   }
   if (h3) probe_all(v, rec3, st, scr);
+  if (have_phase_records && nr == 0 && h3 == 0) {
+    // ---------------- S4 fast path: every read's PQ_a records are its phase-a job of S1
+    uint64_t* total = scr.alloc<uint64_t>(1);
+    GOD_LAUNCH("k_read_anchor_counts", k_read_anchor_counts1, grid_for((uint64_t)n_reads * RG, 256), 256, 0, st,
+               rec1.cnt, rec1.job_off, phases, p, n_reads, anchor_offsets);
+    scan_exclusive_u64(anchor_offsets, anchor_offsets, n_reads, total, st, scr, "scan_read_anchors");
+    GOD_CUDA(cudaMemcpyAsync(anchor_offsets + n_reads, total, sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
+    const uint64_t tot = d2h_scalar(total, st);
+    if (tot <= cap)
+      GOD_LAUNCH("k_anchor_write", k_anchor_write1, grid_for((uint64_t)n_reads * RG, 256), 256, 0, st, v, rec1.hz,
+                 rec1.pos, rec1.cnt, rec1.beg, rec1.job_off, phases, p, n_reads, anchor_offsets, anchors);
+    return tot;
+  }
   SeedSources S{};
   S.hz[0] = rec1.hz; S.pos[0] = rec1.pos; S.off[0] = rec1.job_off; S.cnt[0] = rec1.cnt; S.beg[0] = rec1.beg;
   S.hz[1] = rec2.hz; S.pos[1] = rec2.pos; S.off[1] = rec2.job_off; S.cnt[1] = rec2.cnt; S.beg[1] = rec2.beg;
