@@ -182,7 +182,7 @@ def algorithmic_bytes(name: str, ctx: dict):
     n_ref_mz = ctx["n_entries_all"]
     if name == "extract_ref":      # read every reference byte once; write 12 B per minimizer (u64 hash|strand, u32 pos)
         return ctx["ref_bytes"] + 12 * n_ref_mz
-    if name in ("k_rs_scatter2", "k_bin_sort"):  # read + write one 12-B record per pass / per bin sort
+    if name in ("k_rs_scatter", "k_rs_scatter2", "k_bin_sort"):  # read + write one 12-B record per pass / bin sort
         return 24 * n_ref_mz
     if name == "k_rs_hist":
         return 8 * n_ref_mz

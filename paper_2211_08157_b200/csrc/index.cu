@@ -1099,7 +1099,7 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
       const uint32_t dmask = (1u << bits) - 1;
       if (!have_hist) GOD_LAUNCH("k_rs_hist", k_rs_hist<RB>, ntiles, RS_NT, 0, st, k0, n, shift, dmask, hist, ntiles);
       scan_exclusive_u32_to_u64(hist, goff, (uint64_t)(1u << RB) * ntiles, nullptr, st, scr, "scan_sort_hist");
-      GOD_LAUNCH("k_rs_scatter2", k_rs_scatter2<RB>, ntiles, RS2_NT, RS_DYN_SMEM, st, k0, v0, k1, v1, n, shift, dmask,
+      GOD_LAUNCH("k_rs_scatter", k_rs_scatter2<RB>, ntiles, RS2_NT, RS_DYN_SMEM, st, k0, v0, k1, v1, n, shift, dmask,
                  goff, ntiles);
       std::swap(k0, k1);
       std::swap(v0, v1);
