@@ -1,3 +1,4 @@
+#include <algorithm>
 // api.cu — the C ABI (include/god.h): validation, host/device staging, dispatch to the kernels.
 #include <atomic>
 #include <cstring>
@@ -208,6 +209,10 @@ __global__ void k_split_records(const uint64_t* __restrict__ hz, const uint32_t*
     if (strand) strand[i] = (uint8_t)(v >> 63);
   }
 }
+__global__ void k_rebase_u64(uint64_t* a, uint64_t n, uint64_t base, uint64_t add) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    a[i] = a[i] - base + add;
+}
 __global__ void k_check_phases(const uint8_t* ph, uint32_t n, uint32_t p, uint32_t* bad) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     if (ph[i] >= p) atomicAdd(bad, 1u);
@@ -217,6 +222,114 @@ __global__ void k_check_phases(const uint8_t* ph, uint32_t n, uint32_t p, uint32
 }  // namespace god
 
 using namespace god;
+
+// Host-buffer seeding, pipelined over read batches (the runtime analogue of minimap2's -K batching):
+// batch b+1's reads are copied host->device on one stream while batch b is seeded on the caller's
+// stream and batch b-1's anchors, offsets and phases are copied device->host on a third, through a
+// ring of two device buffer sets.  Requires page-locked host buffers to overlap (pageable memory
+// still works, serialised by the driver).  Returns the total number of anchors.
+namespace {
+struct PipeSlot {
+  uint8_t* reads = nullptr;
+  uint64_t reads_cap = 0;
+  uint64_t* off = nullptr;
+  uint64_t off_cap = 0;
+  uint8_t* ph = nullptr;
+  uint64_t* aoff = nullptr;
+  god_anchor* an = nullptr;
+  uint64_t an_cap = 0;
+  cudaEvent_t h2d_done = nullptr, comp_done = nullptr, d2h_done = nullptr;
+  bool d2h_pending = false;
+};
+template <class T>
+void grow(T*& p, uint64_t& cap, uint64_t need, cudaStream_t st) {
+  if (need <= cap) return;
+  if (p) GOD_CUDA(cudaFreeAsync(p, st));
+  cap = need + need / 8 + 1024;
+  GOD_CUDA(cudaMallocAsync((void**)&p, cap * sizeof(T), st));
+}
+}  // namespace
+
+static uint64_t seed_reads_pipelined(const god_index* idx, const uint8_t* reads, const uint64_t* offs, uint32_t n_reads,
+                                     god_phase_mode mode, uint8_t* phases, uint32_t t, god_anchor* anchors,
+                                     uint64_t* anchor_offsets, uint64_t cap, uint32_t n_batches, cudaStream_t st) {
+  static cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  if (!s_h2d) {
+    GOD_CUDA(cudaStreamCreateWithFlags(&s_h2d, cudaStreamNonBlocking));
+    GOD_CUDA(cudaStreamCreateWithFlags(&s_d2h, cudaStreamNonBlocking));
+  }
+  PipeSlot slot[2];
+  for (auto& sl : slot) {
+    GOD_CUDA(cudaEventCreateWithFlags(&sl.h2d_done, cudaEventDisableTiming));
+    GOD_CUDA(cudaEventCreateWithFlags(&sl.comp_done, cudaEventDisableTiming));
+    GOD_CUDA(cudaEventCreateWithFlags(&sl.d2h_done, cudaEventDisableTiming));
+  }
+  uint64_t written = 0;  // anchors before the current batch
+  const uint32_t per = (n_reads + n_batches - 1) / n_batches;
+  for (auto& sl : slot) {
+    GOD_CUDA(cudaMallocAsync((void**)&sl.ph, (uint64_t)per + 1, st));
+    GOD_CUDA(cudaMallocAsync((void**)&sl.aoff, ((uint64_t)per + 1) * sizeof(uint64_t), st));
+  }
+  GOD_CUDA(cudaStreamSynchronize(st));
+  auto r_begin = [&](uint32_t b) { return std::min<uint64_t>((uint64_t)b * per, n_reads); };
+  auto upload = [&](uint32_t b) {
+    PipeSlot& sl = slot[b & 1];
+    const uint64_t r0 = r_begin(b), r1 = r_begin(b + 1), nb = r1 - r0;
+    const uint64_t bytes = offs[r1] - offs[r0];
+    // the slot's buffers are free once its previous batch's results have left the device
+    if (sl.d2h_pending) GOD_CUDA(cudaStreamWaitEvent(s_h2d, sl.d2h_done, 0));
+    if (sl.reads) GOD_CUDA(cudaStreamWaitEvent(s_h2d, sl.comp_done, 0));  // batch b-2 no longer reads them
+    grow(sl.reads, sl.reads_cap, bytes + 16, s_h2d);
+    grow(sl.off, sl.off_cap, nb + 1, s_h2d);
+    if (bytes) GOD_CUDA(cudaMemcpyAsync(sl.reads, reads + offs[r0], bytes, cudaMemcpyHostToDevice, s_h2d));
+    GOD_CUDA(cudaMemcpyAsync(sl.off, offs + r0, (nb + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, s_h2d));
+    if (mode == GOD_PHASE_GIVEN && nb) GOD_CUDA(cudaMemcpyAsync(sl.ph, phases + r0, nb, cudaMemcpyHostToDevice, s_h2d));
+    GOD_CUDA(cudaEventRecord(sl.h2d_done, s_h2d));
+  };
+  upload(0);
+  for (uint32_t b = 0; b < n_batches; b++) {
+    PipeSlot& sl = slot[b & 1];
+    if (b + 1 < n_batches) upload(b + 1);
+    const uint64_t r0 = r_begin(b), r1 = r_begin(b + 1), nb = r1 - r0;
+    GOD_CUDA(cudaStreamWaitEvent(st, sl.h2d_done, 0));
+    GOD_LAUNCH("k_rebase", k_rebase_u64, grid_for(nb + 1, 256), 256, 0, st, sl.off, nb + 1, offs[r0], 0ull);
+    // anchors of this batch: a share of the caller's capacity, grown and redone if too small
+    uint64_t want = cap ? std::min<uint64_t>(cap, cap / n_batches + cap / (4 * n_batches) + 4096) : 4096;
+    uint64_t tot = 0;
+    for (int attempt = 0; attempt < 2; attempt++) {
+      if (sl.d2h_pending) GOD_CUDA(cudaStreamWaitEvent(st, sl.d2h_done, 0));
+      grow(sl.an, sl.an_cap, want, st);
+      tot = god::seed_reads(idx, sl.reads, sl.off, (uint32_t)nb, mode, sl.ph, t, sl.an, sl.aoff, sl.an_cap, st);
+      if (tot <= sl.an_cap) break;
+      want = tot;
+    }
+    // offsets of this batch -> global anchor offsets
+    GOD_LAUNCH("k_rebase", k_rebase_u64, grid_for(nb + 1, 256), 256, 0, st, sl.aoff, nb + 1, 0ull, written);
+    GOD_CUDA(cudaEventRecord(sl.comp_done, st));
+    GOD_CUDA(cudaStreamWaitEvent(s_d2h, sl.comp_done, 0));
+    if (written + tot <= cap && tot)
+      GOD_CUDA(cudaMemcpyAsync(anchors + written, sl.an, tot * sizeof(god_anchor), cudaMemcpyDeviceToHost, s_d2h));
+    GOD_CUDA(cudaMemcpyAsync(anchor_offsets + r0, sl.aoff, (nb + 1) * sizeof(uint64_t), cudaMemcpyDeviceToHost, s_d2h));
+    if (mode == GOD_PHASE_SELECT && nb) GOD_CUDA(cudaMemcpyAsync(phases + r0, sl.ph, nb, cudaMemcpyDeviceToHost, s_d2h));
+    GOD_CUDA(cudaEventRecord(sl.d2h_done, s_d2h));
+    sl.d2h_pending = true;
+    written += tot;
+  }
+  GOD_CUDA(cudaStreamSynchronize(s_d2h));
+  GOD_CUDA(cudaStreamSynchronize(s_h2d));
+  for (auto& sl : slot) {
+    if (sl.reads) cudaFreeAsync(sl.reads, st);
+    if (sl.off) cudaFreeAsync(sl.off, st);
+    if (sl.ph) cudaFreeAsync(sl.ph, st);
+    if (sl.aoff) cudaFreeAsync(sl.aoff, st);
+    if (sl.an) cudaFreeAsync(sl.an, st);
+    cudaEventDestroy(sl.h2d_done);
+    cudaEventDestroy(sl.comp_done);
+    cudaEventDestroy(sl.d2h_done);
+  }
+  GOD_CUDA(cudaStreamSynchronize(st));
+  return written;
+}
 
 extern "C" {
 
@@ -418,6 +531,18 @@ GOD_API god_status god_seed_reads(const god_index* idx, const uint8_t* reads, co
     if (mode == GOD_PHASE_GIVEN && !is_device_ptr(phases))
       for (uint32_t i = 0; i < n_reads; i++) GOD_REQUIRE(phases[i] < idx->P.pat.p, "phase >= p");
     cudaStream_t st = (cudaStream_t)stream;
+    // all-host buffers and a large batch: pipelined transfers (see seed_reads_pipelined)
+    const char* pm = getenv("GOD_PIPE_MIN_READS");  // test hook: smaller batches
+    const uint32_t pipe_min = pm ? (uint32_t)atoi(pm) : (1u << 20);  // reads per batch
+    const uint32_t n_batches = std::min<uint32_t>(8u, n_reads / (pipe_min ? pipe_min : 1u));
+    if (n_batches >= 2 && !is_device_ptr(reads) && !is_device_ptr(read_offsets) && !is_device_ptr(phases) &&
+        !is_device_ptr(anchor_offsets) && (!anchors || !is_device_ptr(anchors))) {
+      const uint64_t tot = seed_reads_pipelined(idx, reads, read_offsets, n_reads, mode, phases, t, anchors,
+                                                anchor_offsets, anchors ? cap : 0, n_batches, st);
+      *needed = tot;
+      if (tot > cap) throw Fail{GOD_ETRUNC};
+      return;
+    }
     Scratch scr(st);
     Stage sg(st, scr);
     const uint64_t L = total_len(read_offsets, n_reads, st);

@@ -264,6 +264,29 @@ def test_seed_host_pointer_path():
     assert np.array_equal(canon(an), canon(oan))
 
 
+@pytest.mark.parametrize("given", [False, True])
+def test_seed_host_pipelined_batches(given, monkeypatch):
+    """All-host buffers above the batch threshold take the pipelined path (read batches copied in,
+    seeded and copied out on three streams); batches shrunk by the test hook so that it runs here,
+    with long reads (the dedicated PQ_a extraction) and edge reads spread over the batches."""
+    monkeypatch.setenv("GOD_PIPE_MIN_READS", "97")
+    rng = np.random.default_rng(23)
+    ref = synth.dup_genome(300_000, 13, dup_frac=0.2, lmin=300, lmax=2000)
+    roffs_ref = np.array([0, ref.size], np.uint64)
+    reads = synth.simulate_reads(ref, 800, 7, mu=5.5, sigma=1.2, lmin=1, lmax=5000, p_sub=0.01, p_ins=0.005,
+                                 p_del=0.005)
+    seqs = [reads.seq[int(reads.offsets[i]):int(reads.offsets[i + 1])] for i in range(reads.n)]
+    seqs[100:100] = [np.zeros(0, np.uint8), np.frombuffer(b"N" * 400, np.uint8), synth.random_acgt(rng, 3000, 0.3)]
+    rs, ro = synth.concat(seqs)
+    ix = god.god_build_index(cu(ref), cu(roffs_ref), "10", 15, 10, cutoff=(1, 500))
+    ox = oracle.Index(ref, roffs_ref, "10", 15, 10, cutoff=(1, 500))
+    ph = rng.integers(0, 2, size=len(ro) - 1).astype(np.uint8) if given else None
+    an, ao, gph = god.god_seed_reads(ix, rs, ro, phases=ph)
+    oan, oao, oph = ox.seed_reads(rs, ro, phases=ph)
+    assert np.array_equal(gph, oph) and np.array_equal(ao, oao)
+    assert np.array_equal(canon(an), canon(oan))
+
+
 # ------------------------------------------------------------------------------------ K1 v2 (specialised)
 X2_COMBOS = [("10", 21, 11), ("01", 21, 11), ("1", 21, 11), ("10", 19, 19), ("1", 19, 19), ("10", 15, 10),
              ("1", 15, 10)]
