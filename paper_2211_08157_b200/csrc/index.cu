@@ -1112,7 +1112,10 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
       uint32_t* n_bins_d = scr.alloc<uint32_t>(1);
       GOD_CUDA(cudaMemsetAsync(segc, 0, (1u << SEG_BITS) * sizeof(uint32_t), st));
       GOD_LAUNCH("k_seg_hist", k_seg_hist, 4u * num_sms(), 512, 0, st, k0, n, L, segc);
-      const uint32_t target = (uint32_t)std::max<uint64_t>(BIN_TARGET, n / ((1u << (2 * BIN_DIGIT)) - (1u << SEG_BITS)) + 1);
+      const char* bt = getenv("GOD_BIN_TARGET");  // test hook: bin size (default BIN_TARGET)
+      const uint64_t base_target = bt ? std::max(1, atoi(bt)) : BIN_TARGET;
+      const uint32_t target =
+          (uint32_t)std::max<uint64_t>(base_target, n / ((1u << (2 * BIN_DIGIT)) - (1u << SEG_BITS)) + 1);
       GOD_LAUNCH("k_seg_table", k_seg_table, 1, 1024, 0, st, segc, target, table, n_bins_d);
       GOD_LAUNCH("k_seg_assign", k_seg_assign, ntiles, RS_NT, 0, st, k0, n, L, hbits, table, (1u << BIN_DIGIT) - 1, hist,
                  ntiles);

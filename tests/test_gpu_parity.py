@@ -186,6 +186,24 @@ def test_index_parity_homopolymer_heavy():
         _index_parity(ref, offs, "1", 7, 5, cutoff=cut)
 
 
+@pytest.mark.parametrize("env", [{}, {"GOD_BIN_TARGET": "6000"}, {"GOD_BIN_TARGET": "40"}, {"GOD_DIR_MODE0": "1"},
+                                 {"GOD_SORT_FULL": "1"}],
+                         ids=["default", "big-bins", "tiny-bins", "dir-mode0", "full-lsd"])
+def test_index_parity_sort_and_directory_variants(env, monkeypatch):
+    """k = 21 on a repeat-rich reference through every sort/directory path: bins above the SMEM
+    capacity (chunked global kernel), one-record bins, the top-bit directory, the full LSD."""
+    for kk, vv in env.items():
+        monkeypatch.setenv(kk, vv)
+    ref = synth.dup_genome(3_000_000, 31, dup_frac=0.35, lmin=200, lmax=4000)
+    rng = np.random.default_rng(31)
+    rep = synth.random_acgt(rng, 900)
+    ref = np.concatenate([ref] + [rep] * 300 + [np.frombuffer(b"ACGTTGCA" * 2000, np.uint8)])
+    offs = np.array([0, 1_000_000, ref.size], np.uint64)
+    ix, ox = _index_parity(ref, offs, "10", 21, 11, cutoff=(1, 2000))
+    reads = synth.simulate_reads(ref, 3000, 41, length=150, p_sub=0.002)
+    _seed_parity(ix, ox, reads.seq, reads.offsets)
+
+
 # ------------------------------------------------------------------------------------ stage 4
 def canon(an):
     """anchors -> array sorted by (read_id, ref_pos, read_pos, strand)"""
