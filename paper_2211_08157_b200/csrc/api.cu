@@ -299,7 +299,8 @@ static uint64_t seed_reads_pipelined(const god_index* idx, const uint8_t* reads,
     for (int attempt = 0; attempt < 2; attempt++) {
       if (sl.d2h_pending) GOD_CUDA(cudaStreamWaitEvent(st, sl.d2h_done, 0));
       grow(sl.an, sl.an_cap, want, st);
-      tot = god::seed_reads(idx, sl.reads, sl.off, (uint32_t)nb, mode, sl.ph, t, sl.an, sl.aoff, sl.an_cap, st);
+      tot = god::seed_reads(idx, sl.reads, sl.off, (uint32_t)nb, mode, sl.ph, t, sl.an, sl.aoff, sl.an_cap, st,
+                            (uint32_t)r0);
       if (tot <= sl.an_cap) break;
       want = tot;
     }

@@ -34,6 +34,11 @@ namespace {
 
 constexpr int X2_NT = 128;
 constexpr int X2_OUT_BLOCKS = X2_NT - 2;
+// Staging capacity (selected records per tile) of the deferred copy-out.  Minimizer density is
+// ~2/(w+1), i.e. ~17% of a tile's positions; a tile with more (all-ties runs: homopolymers, tandem
+// repeats) is written out at once instead, after a synchronous look-back.
+constexpr int X2_CAP = 384;
+constexpr uint32_t X2_FLUSHED = 0xFFFFFFFFu;  // pending-count marker: the tile was written out already
 #ifndef X2_MINB
 #define X2_MINB 6
 #endif
@@ -129,9 +134,10 @@ struct X2Cfg {
   static constexpr size_t O_CODES = O_LUT + 256 * 4;
   static constexpr size_t O_NMASK = O_CODES + (size_t)MAXWORDS * 4;
   static constexpr size_t O_XCHG = O_NMASK + (size_t)MAXWORDS * 4;
-  static constexpr size_t O_HZ = (O_XCHG + 2 * (X2_NT / 32) * W * 4 + 15) / 16 * 16;  // [2][POS] hz
-  static constexpr size_t O_SE = O_HZ + 2 * (size_t)POS * 8;      // [2][POS] selected: e | key16 << 16
-  static constexpr size_t O_BI = O_SE + 2 * (size_t)POS * 4;      // block info [2][2][NT]
+  static constexpr size_t O_HZ = (O_XCHG + 2 * (X2_NT / 32) * W * 4 + 15) / 16 * 16;  // [POS] hz, this tile
+  static constexpr size_t O_SHZ = O_HZ + (size_t)POS * 8;         // [2][X2_CAP] staged hz of the selected
+  static constexpr size_t O_SE = O_SHZ + 2 * (size_t)X2_CAP * 8;  // [2][X2_CAP] staged: e | key16 << 16
+  static constexpr size_t O_BI = O_SE + 2 * (size_t)X2_CAP * 4;   // block info [2][2][NT]
   static constexpr size_t SMEM = (O_BI + 2 * 2 * X2_NT * 4 + 15) / 16 * 16;
 };
 
@@ -233,11 +239,13 @@ __global__ void __launch_bounds__(X2_NT, X2_MINB) k_extract2(X2Args a) {
   uint32_t* nmask = reinterpret_cast<uint32_t*>(x2_smem + C::O_NMASK);
   uint32_t* xpf = reinterpret_cast<uint32_t*>(x2_smem + C::O_XCHG);
   uint32_t* xsf = xpf + NWARP * W;
-  uint64_t* HZ2 = reinterpret_cast<uint64_t*>(x2_smem + C::O_HZ);    // [2][POS]
-  uint32_t* SE = reinterpret_cast<uint32_t*>(x2_smem + C::O_SE);     // [2][POS]
+  uint64_t* HZ = reinterpret_cast<uint64_t*>(x2_smem + C::O_HZ);     // [POS]
+  uint64_t* SHZ = reinterpret_cast<uint64_t*>(x2_smem + C::O_SHZ);   // [2][X2_CAP]
+  uint32_t* SE = reinterpret_cast<uint32_t*>(x2_smem + C::O_SE);     // [2][X2_CAP]
   // block info [2][2][NT]: pos base | first staged record (12 bits) + job start flag << 12 + job - j0 << 13
   uint32_t* BI = reinterpret_cast<uint32_t*>(x2_smem + C::O_BI);
   __shared__ uint32_t s_bj0[2];  // j0 of the tile staged in each buffer
+  __shared__ uint64_t s_ovf_base;
   __shared__ X2Tile T;
   __shared__ uint64_t skb[X2_NT + 2], scw[X2_NT + 2];
   __shared__ uint64_t sjb[X2_NT + 2];  // per job of the tile: byte address of its first patterned base
@@ -269,8 +277,8 @@ __global__ void __launch_bounds__(X2_NT, X2_MINB) k_extract2(X2Args a) {
     else base = lb_resolve_warp(a.status, tile, cnt);
     base = __shfl_sync(0xffffffffu, base, 0);
     if (lane == 0 && tile == ntiles - 1) *a.total_out = base + cnt;
-    const uint64_t* hzb = HZ2 + (size_t)b * POS;
-    const uint32_t* se = SE + (size_t)b * POS;
+    const uint64_t* hzb = SHZ + (size_t)b * X2_CAP;
+    const uint32_t* se = SE + (size_t)b * X2_CAP;
     const uint32_t* bpb = BI + (size_t)b * 2 * X2_NT;
     const uint32_t* binf = bpb + X2_NT;
     const uint32_t bj0 = s_bj0[b];
@@ -284,7 +292,7 @@ __global__ void __launch_bounds__(X2_NT, X2_MINB) k_extract2(X2Args a) {
       if (gi < a.cap) {
         const int e = se[r] & 0xFFFFu;
         const int blk = e / W;
-        a.out_hz[gi] = hzb[e];
+        a.out_hz[gi] = hzb[r];
         a.out_pos[gi] = bpb[blk] + (uint32_t)PS * (uint32_t)(e - blk * W);
         if (a.out_job) a.out_job[gi] = bj0 + (binf[blk] >> 13);
       }
@@ -307,7 +315,7 @@ __global__ void __launch_bounds__(X2_NT, X2_MINB) k_extract2(X2Args a) {
   uint32_t cnt_old = 0, cnt_new = 0;
   while (true) {
     if (wid == 0) {
-      if (pend_old >= 0) flush_warp0((uint64_t)pend_old, cnt_old, buf);
+      if (pend_old >= 0 && cnt_old != X2_FLUSHED) flush_warp0((uint64_t)pend_old, cnt_old, buf);
     } else {
       if (tid == SETUP_TID) {
         T.tile = next_t < ntiles ? next_t : 0xFFFFFFFFu;
@@ -387,7 +395,6 @@ __global__ void __launch_bounds__(X2_NT, X2_MINB) k_extract2(X2Args a) {
     __syncthreads();
     const uint32_t tile = T.tile;
     if (tile == 0xFFFFFFFFu) break;
-    uint64_t* HZ = HZ2 + (size_t)buf * POS;
     const uint32_t j0 = T.j0, j1 = T.j1;
     const uint64_t cw_lo = T.cw_lo;
     const uint32_t nj = j1 - j0 + 1;
@@ -577,8 +584,10 @@ __global__ void __launch_bounds__(X2_NT, X2_MINB) k_extract2(X2Args a) {
     if (tid == 0 || tid == X2_NT - 1 || !blk_in) selmask = 0;
 
     // ------------------------------------------------------------ E. compaction into staging[buf]
-    uint32_t* se = SE + (size_t)buf * POS;
+    uint32_t* se = SE + (size_t)buf * X2_CAP;
+    uint64_t* shz = SHZ + (size_t)buf * X2_CAP;
     uint32_t* bi = BI + (size_t)buf * 2 * X2_NT;
+    uint32_t my_idx0 = 0;
     auto compact = [&]() -> uint32_t {
       const uint32_t cnt = __popc(selmask);
       uint32_t incl = cnt;
@@ -597,6 +606,7 @@ __global__ void __launch_bounds__(X2_NT, X2_MINB) k_extract2(X2Args a) {
         total += c;
       }
       uint32_t idx = before + incl - cnt;
+      my_idx0 = idx;
       bi[tid] = sjp[J - j0] + (uint32_t)PS * l0;
       bi[X2_NT + tid] = idx | ((blk_in && tid > 0 && tid < X2_NT - 1 && l0 == 0) ? 1u << 12 : 0u) | ((J - j0) << 13);
       if (tid == 0) s_bj0[buf] = j0;
@@ -604,7 +614,11 @@ __global__ void __launch_bounds__(X2_NT, X2_MINB) k_extract2(X2Args a) {
       while (m) {
         const int i = __ffs(m) - 1;
         m &= m - 1;
-        se[idx] = (uint32_t)(tid * W + i) | ((uint32_t)(HZ[tid * W + i] >> ks) << 16);
+        if (idx < (uint32_t)X2_CAP) {
+          const uint64_t hv = HZ[tid * W + i];
+          se[idx] = (uint32_t)(tid * W + i) | ((uint32_t)(hv >> ks) << 16);
+          shz[idx] = hv;
+        }
         ++idx;
       }
       __syncthreads();
@@ -612,7 +626,12 @@ __global__ void __launch_bounds__(X2_NT, X2_MINB) k_extract2(X2Args a) {
     };
     uint32_t cnt = compact();
     // exactness of the 31-bit keys: candidates closer than w with equal keys but different hashes
-    if (!T.any_n && !T.slow && ks > 0 && !(a.dbg_flags & 2u)) {
+    if (cnt > (uint32_t)X2_CAP && !T.any_n && !T.slow) {
+      // too many for the staging (and the tie check works on the staged list): exact selection
+      slow_path();
+      if (tid == 0 || tid == X2_NT - 1 || !blk_in) selmask = 0;
+      cnt = compact();
+    } else if (!T.any_n && !T.slow && ks > 0 && !(a.dbg_flags & 2u)) {
       bool tie = false;
       for (uint32_t r = tid; r < cnt; r += X2_NT) {
         const uint32_t vr = se[r];
@@ -641,8 +660,38 @@ __global__ void __launch_bounds__(X2_NT, X2_MINB) k_extract2(X2Args a) {
         cnt = compact();
       }
     }
-    // publish this tile's count, then finish the previous tile (its predecessors are done by now)
+    // publish this tile's count; its records leave two iterations later (warp 0, flush_warp0), or
+    // now if they did not fit the staging
     if (tid == 0 && !(a.dbg_flags & 1u)) lb_publish(a.status, tile, cnt);
+    if (cnt > (uint32_t)X2_CAP) {
+      if (wid == 0) {
+        uint64_t base;
+        if (a.dbg_flags & 1u) base = lane == 0 ? atomicAdd((unsigned long long*)&a.status[ntiles], (unsigned long long)cnt) : 0;
+        else base = lb_resolve_warp(a.status, tile, cnt);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (lane == 0) {
+          s_ovf_base = base;
+          if (tile == ntiles - 1) *a.total_out = base + cnt;
+        }
+      }
+      __syncthreads();
+      const uint64_t base = s_ovf_base;
+      if (a.job_off && blk_in && tid > 0 && tid < X2_NT - 1 && l0 == 0) a.job_off[J] = base + my_idx0;
+      uint32_t m = selmask, idx = my_idx0;
+      const uint32_t pb = sjp[J - j0] + (uint32_t)PS * l0;
+      while (m) {
+        const int i = __ffs(m) - 1;
+        m &= m - 1;
+        const uint64_t gi = base + idx;
+        if (gi < a.cap) {
+          a.out_hz[gi] = HZ[tid * W + i];
+          a.out_pos[gi] = pb + (uint32_t)PS * (uint32_t)i;
+          if (a.out_job) a.out_job[gi] = J;
+        }
+        ++idx;
+      }
+      cnt = X2_FLUSHED;
+    }
     pend_old = pend_new;
     cnt_old = cnt_new;
     pend_new = tile;
@@ -651,7 +700,7 @@ __global__ void __launch_bounds__(X2_NT, X2_MINB) k_extract2(X2Args a) {
     __syncthreads();
   }
   // pend_old was flushed in the last (tile-less) iteration; the newest tile is in buffer buf ^ 1
-  if (pend_new >= 0 && wid == 0) flush_warp0((uint64_t)pend_new, cnt_new, buf ^ 1);
+  if (pend_new >= 0 && cnt_new != X2_FLUSHED && wid == 0) flush_warp0((uint64_t)pend_new, cnt_new, buf ^ 1);
 }
 
 // per-tile descriptors: first and last job (binary searches over the padded bases), the tile's

@@ -151,10 +151,11 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
                  const god_cutoff& cut, god_index* ix, cudaStream_t st);
 void index_count(const god_index* ix, const uint64_t* hashes, uint64_t n, uint32_t* counts, cudaStream_t st);
 void index_dump(const god_index* ix, uint64_t* hash, uint32_t* pos, uint8_t* strand, cudaStream_t st);
-// returns total anchors; writes anchors only if total <= cap
+// returns total anchors; writes anchors only if total <= cap; anchor read ids are rid_base + the
+// read's index in this call (batched callers pass the batch's first read)
 uint64_t seed_reads(const god_index* ix, const uint8_t* reads, const uint64_t* offsets, uint32_t n_reads,
                     god_phase_mode mode, uint8_t* phases, uint32_t t, god_anchor* anchors, uint64_t* anchor_offsets,
-                    uint64_t cap, cudaStream_t st);
+                    uint64_t cap, cudaStream_t st, uint32_t rid_base = 0);
 void sparsify(const Params& P, const uint8_t* seq, const uint64_t* offsets, uint32_t n, const uint8_t* phases,
               uint64_t* packed, uint64_t* nmask, uint64_t* out_offsets, uint64_t* counts, uint64_t cap_words,
               uint64_t* needed_host, cudaStream_t st);

@@ -120,7 +120,8 @@ __global__ void k_read_anchor_counts1(const uint32_t* __restrict__ cnt, const ui
 __global__ void k_anchor_write1(IndexView v, const uint64_t* __restrict__ hz, const uint32_t* __restrict__ pos,
                                 const uint32_t* __restrict__ cnt, const uint32_t* __restrict__ beg,
                                 const uint64_t* __restrict__ job_off, const uint8_t* __restrict__ phases, uint32_t p,
-                                uint32_t n_reads, const uint64_t* __restrict__ aoff, god_anchor* out) {
+                                uint32_t n_reads, const uint64_t* __restrict__ aoff, god_anchor* out,
+                                uint32_t rid_base) {
   const uint32_t l = threadIdx.x & (RG - 1);
   for (uint64_t g = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / RG; g < n_reads;
        g += (uint64_t)gridDim.x * blockDim.x / RG) {
@@ -146,7 +147,7 @@ __global__ void k_anchor_write1(IndexView v, const uint64_t* __restrict__ hz, co
           god_anchor an;
           an.ref_pos = (uint32_t)(en >> 32);
           an.read_pos = qp;
-          an.read_id = r;
+          an.read_id = rid_base + r;
           an.strand = ((uint32_t)en & 1u) ^ qz;
           out[oo] = an;
         }
@@ -159,11 +160,12 @@ __global__ void k_anchor_write1(IndexView v, const uint64_t* __restrict__ hz, co
 // one thread per read minimizer: its anchors are the kept entries [beg, beg + cnt)
 __global__ void k_anchor_write(IndexView v, const uint32_t* __restrict__ pos, const uint32_t* __restrict__ rid,
                                const uint64_t* __restrict__ hz, uint64_t n, const uint64_t* __restrict__ aoff,
-                               const uint32_t* __restrict__ cnt, const uint32_t* __restrict__ beg, god_anchor* out) {
+                               const uint32_t* __restrict__ cnt, const uint32_t* __restrict__ beg, god_anchor* out,
+                               uint32_t rid_base) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t c = cnt[i];
     if (!c) continue;
-    const uint32_t qz = (uint32_t)(hz[i] >> 63), qpos = pos[i], r = rid[i], b = beg[i];
+    const uint32_t qz = (uint32_t)(hz[i] >> 63), qpos = pos[i], r = rid_base + rid[i], b = beg[i];
     uint64_t o = aoff[i];
     for (uint32_t e = b; e < b + c; e++, o++) {
       god_anchor an;
@@ -283,7 +285,7 @@ static void probe_all(const IndexView& v, Records& rec, cudaStream_t st, Scratch
 
 uint64_t seed_reads(const god_index* ix, const uint8_t* reads, const uint64_t* offsets, uint32_t n_reads,
                     god_phase_mode mode, uint8_t* phases, uint32_t t, god_anchor* anchors, uint64_t* anchor_offsets,
-                    uint64_t cap, cudaStream_t st) {
+                    uint64_t cap, cudaStream_t st, uint32_t rid_base) {
   Scratch scr(st);
   const Params& P = ix->P;
   const uint32_t p = P.pat.p;
@@ -378,7 +380,7 @@ uint64_t seed_reads(const god_index* ix, const uint8_t* reads, const uint64_t* o
     const uint64_t tot = d2h_scalar(total, st);
     if (tot <= cap)
       GOD_LAUNCH("k_anchor_write", k_anchor_write1, grid_for((uint64_t)n_reads * RG, 256), 256, 0, st, v, rec1.hz,
-                 rec1.pos, rec1.cnt, rec1.beg, rec1.job_off, phases, p, n_reads, anchor_offsets, anchors);
+                 rec1.pos, rec1.cnt, rec1.beg, rec1.job_off, phases, p, n_reads, anchor_offsets, anchors, rid_base);
     return tot;
   }
   SeedSources S{};
@@ -408,7 +410,7 @@ uint64_t seed_reads(const god_index* ix, const uint8_t* reads, const uint64_t* o
   const uint64_t tot = d2h_scalar(total, st);
   if (tot <= cap && n)
     GOD_LAUNCH("k_anchor_write", k_anchor_write, grid_for(n, 256), 256, 0, st, v, qpos, rid, hz, n, aoff, cnt, beg,
-               anchors);
+               anchors, rid_base);
   return tot;
 }
 
