@@ -39,9 +39,10 @@ constexpr int X2_OUT_BLOCKS = X2_NT - 2;
 // repeats) is written out at once instead, after a synchronous look-back.
 constexpr int X2_CAP = 384;
 constexpr uint32_t X2_FLUSHED = 0xFFFFFFFFu;  // pending-count marker: the tile was written out already
-#ifndef X2_MINB
-#define X2_MINB 6
-#endif
+// resident CTAs per SM the register allocation is sized for (SMEM allows 7): 7 for w <= 11 (72
+// registers, no spills), 6 for w = 19 (more registers per W-block)
+template <int W>
+constexpr int x2_minb() { return W >= 16 ? 6 : 7; }
 
 struct X2Args {
   const uint8_t* seq;
@@ -229,7 +230,7 @@ __device__ inline uint64_t lb_resolve_warp(uint64_t* status, uint64_t tile, uint
 // record count, and only then resolves the PREVIOUS tile's output offset and writes its records,
 // so the look-back never stalls the CTA on a tile that other CTAs are still computing.
 template <int K, int W, int PS>
-__global__ void __launch_bounds__(X2_NT, X2_MINB) k_extract2(X2Args a) {
+__global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract2(X2Args a) {
   using C = X2Cfg<K, W, PS>;
   constexpr int NB = C::NB, NWIN = C::NWIN, NLOAD = C::NLOAD, POS = C::POS;
   constexpr int NWARP = X2_NT / 32;
