@@ -97,16 +97,19 @@ __device__ __forceinline__ uint32_t rev2(uint32_t x) {  // reverse the 16 2-bit 
   return ((y >> 1) & 0x55555555u) | ((y & 0x55555555u) << 1);
 }
 
+// The masked Wang hash (O5).  The shift-add steps are written as the equal multiplications
+// (~x + (x << 21) = x (2^21 - 1) - 1 and x + (x << 31) = x (2^31 + 1) mod 2^64), which the compiler
+// issues on the FMA pipe (IMAD) instead of the integer ALU pipe that the rest of K1 saturates.
 template <int K>
 __device__ __forceinline__ uint64_t wang_hash_k(uint64_t key) {
   constexpr uint64_t mask = (K >= 32) ? ~0ull : ((1ull << (2 * K)) - 1);
-  key = (~key + (key << 21)) & mask;
+  key = (key * ((1ull << 21) - 1) - 1ull) & mask;
   key = key ^ (key >> 24);
   key = (key * 265ull) & mask;
   key = key ^ (key >> 14);
   key = (key * 21ull) & mask;
   key = key ^ (key >> 28);
-  key = (key + (key << 31)) & mask;
+  key = (key * ((1ull << 31) + 1)) & mask;
   return key;
 }
 
