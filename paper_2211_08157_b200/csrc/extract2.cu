@@ -2,7 +2,8 @@
 //
 // Same definitions as extract.cu (P:282/P:286/P:294/P:300/P:370; readings O1-O6 of DESIGN.md §2),
 // specialised at compile time for the hot configurations: k, w and patterns with exactly one '1'
-// (period PS = 1: "1"; PS = 2: "10"/"01").  Everything else runs the generic kernel (extract.cu).
+// (patterns of period p whose x ones come first: "1", "10"/"01", "110", "1110").  Everything else
+// runs the generic kernel (extract.cu).
 //
 // Layout.  Each job's k-mer starts are padded to a multiple of W positions (the pad slots are
 // window barriers), so a W-block never straddles two jobs; each job's patterned bases are packed
@@ -26,6 +27,7 @@
 //   E. ordered compaction: staged in SMEM, tile offset by decoupled look-back, coalesced copy.
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 #include "internal.cuh"
 
 namespace god {
@@ -125,7 +127,7 @@ struct X2Tile {  // per-tile scalars, in SMEM
   uint64_t cw_lo, cw_hi;
 };
 
-template <int K, int W, int PS>
+template <int K, int W, int PP, int PX>
 struct X2Cfg {
   static_assert(X2_NT * W < 4096, "staged record index must fit 12 bits (block info packing)");
   static constexpr int NB = W + K - 1;                 // bases in a thread's window
@@ -145,14 +147,39 @@ struct X2Cfg {
   static constexpr size_t SMEM = (O_BI + 2 * 2 * X2_NT * 4 + 15) / 16 * 16;
 };
 
-// 16 patterned bases (MSB-first 2-bit codes) from the ASCII bytes at A (a PS-strided gather);
+// (pack16 gathers the included bytes with compile-time byte-permutations)
 // *nm gets the N bits (bit 15 - b for base b).  nb = bases that exist (<= 16).
-template <int PS, bool CHECKED>
+// Pattern geometry: period PP with ones at offsets 0..PX-1 (x = 1 patterns may be rotated: their
+// single one's offset is added to the job base).  Included base q of a job lies at byte offset
+// (q / PX) * PP + q % PX.
+__host__ __device__ constexpr int pat_off(int PP, int PX, int q) { return (q / PX) * PP + q % PX; }
+// byte offset, relative to base q0 (q0 % PX == R0), of base q0 + b
+__host__ __device__ constexpr int pat_rel(int PP, int PX, int R0, int b) {
+  return pat_off(PP, PX, R0 + b) - pat_off(PP, PX, R0);
+}
+template <int PP, int PX>
+constexpr int pack_words() {  // u32 words loaded per 16 bases (incl. the alignment shift)
+  int mx = 0;
+  for (int r = 0; r < PX; r++) mx = pat_rel(PP, PX, r, 15) > mx ? pat_rel(PP, PX, r, 15) : mx;
+  return (mx + 3) / 4 + 2;
+}
+// selector of __byte_perm gathering bases 4g..4g+3 from aligned words (a, a+1), a = rel(4g) / 4
+template <int PP, int PX, int R0, int G>
+constexpr uint32_t pack_sel() {
+  const int a4 = (pat_rel(PP, PX, R0, 4 * G) / 4) * 4;
+  uint32_t sel = 0;
+  for (int i = 0; i < 4; i++) sel |= (uint32_t)(pat_rel(PP, PX, R0, 4 * G + i) - a4) << (4 * i);
+  return sel;
+}
+
+// 16 patterned bases (MSB-first 2-bit codes) from the ASCII bytes, base 0 at byte A (its job-relative
+// index has residue R0 mod PX); *nm gets the N bits (bit 15 - b for base b).  nb = bases that exist.
+template <int PP, int PX, int R0, bool CHECKED>
 __device__ __forceinline__ uint32_t pack16(const uint8_t* seq, uint64_t seq_bytes, uint64_t A, int nb,
                                            const uint32_t* lut, uint32_t* nm) {
   const uint64_t Aa = A & ~3ull;
   const uint32_t d8 = (uint32_t)(A - Aa) * 8;
-  constexpr int NL = 4 * PS + 1;
+  constexpr int NL = pack_words<PP, PX>();
   uint32_t w[NL];
   const uint32_t* src = reinterpret_cast<const uint32_t*>(seq + Aa);
 #pragma unroll
@@ -170,16 +197,20 @@ __device__ __forceinline__ uint32_t pack16(const uint8_t* seq, uint64_t seq_byte
   }
   uint32_t t4[4];
   uint32_t bad_any = 0, badw[4];
+  auto gather = [&](auto gc) -> uint32_t {
+    constexpr int G = decltype(gc)::value;
+    constexpr int a = pat_rel(PP, PX, R0, 4 * G) / 4;
+    constexpr uint32_t sel = pack_sel<PP, PX, R0, G>();
+    const uint32_t lo = __funnelshift_r(w[a], w[a + 1], d8);
+    if constexpr (sel == 0x3210u) return lo;  // four consecutive bytes
+    const uint32_t hi = __funnelshift_r(w[a + 1], w[a + 2], d8);
+    return __byte_perm(lo, hi, sel);
+  };
+  const uint32_t xs[4] = {gather(std::integral_constant<int, 0>()), gather(std::integral_constant<int, 1>()),
+                          gather(std::integral_constant<int, 2>()), gather(std::integral_constant<int, 3>())};
 #pragma unroll
   for (int g = 0; g < 4; g++) {
-    uint32_t x;
-    if constexpr (PS == 1) {
-      x = __funnelshift_r(w[g], w[g + 1], d8);
-    } else {
-      const uint32_t lo = __funnelshift_r(w[2 * g], w[2 * g + 1], d8);
-      const uint32_t hi = __funnelshift_r(w[2 * g + 1], w[2 * g + 2], d8);
-      x = __byte_perm(lo, hi, 0x6420);
-    }
+    const uint32_t x = xs[g];
     const uint32_t c = ((x >> 1) ^ (x >> 2)) & 0x03030303u;  // A0 C1 G2 T3 (either case)
     const uint32_t t = c * 0x40100401u;                       // top byte = the 4 codes, MSB-first
     badw[g] = (x & 0xDFDFDFDFu) ^ lut[t >> 24];              // nonzero byte <=> not A/C/G/T
@@ -198,6 +229,30 @@ __device__ __forceinline__ uint32_t pack16(const uint8_t* seq, uint64_t seq_byte
   }
   *nm = n;
   return word;
+}
+
+// code word at job-relative base q0 (a multiple of 16) of the job whose base 0 is byte A0
+template <int PP, int PX, bool CHECKED>
+__device__ __forceinline__ uint32_t pack_word(const uint8_t* seq, uint64_t seq_bytes, uint64_t A0, uint64_t q0, int nb,
+                                              const uint32_t* lut, uint32_t* nm) {
+  const uint32_t r0 = (uint32_t)(q0 % PX);
+  const uint64_t A = A0 + (q0 / PX) * PP + r0;
+  if constexpr (PX == 1) {
+    return pack16<PP, PX, 0, CHECKED>(seq, seq_bytes, A, nb, lut, nm);
+  } else if constexpr (PX == 2) {
+    return r0 ? pack16<PP, PX, 1, CHECKED>(seq, seq_bytes, A, nb, lut, nm)
+              : pack16<PP, PX, 0, CHECKED>(seq, seq_bytes, A, nb, lut, nm);
+  } else {
+    static_assert(PX == 3, "patterns with up to 3 leading ones");
+    return r0 == 0 ? pack16<PP, PX, 0, CHECKED>(seq, seq_bytes, A, nb, lut, nm)
+         : r0 == 1 ? pack16<PP, PX, 1, CHECKED>(seq, seq_bytes, A, nb, lut, nm)
+                   : pack16<PP, PX, 2, CHECKED>(seq, seq_bytes, A, nb, lut, nm);
+  }
+}
+// original-coordinate distance from base q to base q + i, with r = q % PX
+template <int PP, int PX>
+__device__ __forceinline__ uint32_t pat_delta(uint32_t r, uint32_t i) {
+  return ((r + i) / PX) * PP + (r + i) % PX - r;
 }
 
 // deferred decoupled look-back: publish the aggregate as soon as it is known ...
@@ -232,9 +287,9 @@ __device__ inline uint64_t lb_resolve_warp(uint64_t* status, uint64_t tile, uint
 // Persistent CTAs: each grabs tiles in order (atomic counter), computes a tile, publishes its
 // record count, and only then resolves the PREVIOUS tile's output offset and writes its records,
 // so the look-back never stalls the CTA on a tile that other CTAs are still computing.
-template <int K, int W, int PS>
+template <int K, int W, int PP, int PX>
 __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract2(X2Args a) {
-  using C = X2Cfg<K, W, PS>;
+  using C = X2Cfg<K, W, PP, PX>;
   constexpr int NB = C::NB, NWIN = C::NWIN, NLOAD = C::NLOAD, POS = C::POS;
   constexpr int NWARP = X2_NT / 32;
   extern __shared__ __align__(16) unsigned char x2_smem[];
@@ -246,7 +301,8 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract2(X2Args a) {
   uint64_t* HZ = reinterpret_cast<uint64_t*>(x2_smem + C::O_HZ);     // [POS]
   uint64_t* SHZ = reinterpret_cast<uint64_t*>(x2_smem + C::O_SHZ);   // [2][X2_CAP]
   uint32_t* SE = reinterpret_cast<uint32_t*>(x2_smem + C::O_SE);     // [2][X2_CAP]
-  // block info [2][2][NT]: pos base | first staged record (12 bits) + job start flag << 12 + job - j0 << 13
+  // block info [2][2][NT]: pos base | first staged record (12 bits) + job start flag << 12 +
+  // job - j0 << 13 (8 bits) + first k-mer index mod x << 21
   uint32_t* BI = reinterpret_cast<uint32_t*>(x2_smem + C::O_BI);
   __shared__ uint32_t s_bj0[2];  // j0 of the tile staged in each buffer
   __shared__ uint64_t s_ovf_base;
@@ -255,7 +311,7 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract2(X2Args a) {
   __shared__ uint64_t sjb[X2_NT + 2];  // per job of the tile: byte address of its first patterned base
   __shared__ uint32_t sjn[X2_NT + 2];  // ... its k-mer count n_k
   __shared__ uint32_t sjp[X2_NT + 2];  // ... its output position base (pos_base + phase + one0)
-  __shared__ uint8_t swj[(X2Cfg<K, W, PS>::MAXWORDS + 3) / 4 * 4];  // code word -> job (relative)
+  __shared__ uint8_t swj[(X2Cfg<K, W, PP, PX>::MAXWORDS + 3) / 4 * 4];  // code word -> job (relative)
   __shared__ uint32_t sjob[X2_NT];
   __shared__ uint32_t warp_cnt[NWARP];
 
@@ -289,7 +345,7 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract2(X2Args a) {
     if (a.job_off)
       for (int t = lane; t < X2_NT; t += 32) {
         const uint32_t f = binf[t];
-        if ((f >> 12) & 1u) a.job_off[bj0 + (f >> 13)] = base + (f & 0xFFFu);
+        if ((f >> 12) & 1u) a.job_off[bj0 + ((f >> 13) & 0xFFu)] = base + (f & 0xFFFu);
       }
     for (uint32_t r = lane; r < cnt; r += 32) {
       const uint64_t gi = base + r;
@@ -297,8 +353,8 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract2(X2Args a) {
         const int e = se[r] & 0xFFFFu;
         const int blk = e / W;
         a.out_hz[gi] = hzb[r];
-        a.out_pos[gi] = bpb[blk] + (uint32_t)PS * (uint32_t)(e - blk * W);
-        if (a.out_job) a.out_job[gi] = bj0 + (binf[blk] >> 13);
+        a.out_pos[gi] = bpb[blk] + pat_delta<PP, PX>((binf[blk] >> 21) & 3u, (uint32_t)(e - blk * W));
+        if (a.out_job) a.out_job[gi] = bj0 + ((binf[blk] >> 13) & 0xFFu);
       }
     }
   };
@@ -368,8 +424,8 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract2(X2Args a) {
           for (int wi = t1; wi < nwords; wi += nt1) {
             const uint64_t q0 = (w0 + wi) * 16;
             uint32_t nm = 0, word = 0;
-            if (q0 < ncode) word = pack16<PS, false>(a.seq, a.seq_bytes, A0 + (uint64_t)PS * q0,
-                                                     (int)min((uint64_t)16, ncode - q0), lut, &nm);
+            if (q0 < ncode) word = pack_word<PP, PX, false>(a.seq, a.seq_bytes, A0, q0,
+                                                            (int)min((uint64_t)16, ncode - q0), lut, &nm);
             codes[wi] = word;
             nmask[wi] = nm;
             my_n |= nm;
@@ -383,10 +439,9 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract2(X2Args a) {
             const uint64_t q0 = (cw_lo + wi - scw[Jw]) * 16;
             uint32_t nm = 0, word = 0;
             if (q0 < ncode) {
-              const uint64_t A = sjb[Jw] + (uint64_t)PS * q0;
               const int nb = (int)min((uint64_t)16, ncode - q0);
-              word = safe ? pack16<PS, false>(a.seq, a.seq_bytes, A, nb, lut, &nm)
-                          : pack16<PS, true>(a.seq, a.seq_bytes, A, nb, lut, &nm);
+              word = safe ? pack_word<PP, PX, false>(a.seq, a.seq_bytes, sjb[Jw], q0, nb, lut, &nm)
+                          : pack_word<PP, PX, true>(a.seq, a.seq_bytes, sjb[Jw], q0, nb, lut, &nm);
             }
             codes[wi] = word;
             nmask[wi] = nm;
@@ -611,8 +666,9 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract2(X2Args a) {
       }
       uint32_t idx = before + incl - cnt;
       my_idx0 = idx;
-      bi[tid] = sjp[J - j0] + (uint32_t)PS * l0;
-      bi[X2_NT + tid] = idx | ((blk_in && tid > 0 && tid < X2_NT - 1 && l0 == 0) ? 1u << 12 : 0u) | ((J - j0) << 13);
+      bi[tid] = sjp[J - j0] + (uint32_t)pat_off(PP, PX, (int)l0);
+      bi[X2_NT + tid] = idx | ((blk_in && tid > 0 && tid < X2_NT - 1 && l0 == 0) ? 1u << 12 : 0u) | ((J - j0) << 13) |
+                        ((l0 % PX) << 21);
       if (tid == 0) s_bj0[buf] = j0;
       uint32_t m = selmask;
       while (m) {
@@ -682,14 +738,14 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract2(X2Args a) {
       const uint64_t base = s_ovf_base;
       if (a.job_off && blk_in && tid > 0 && tid < X2_NT - 1 && l0 == 0) a.job_off[J] = base + my_idx0;
       uint32_t m = selmask, idx = my_idx0;
-      const uint32_t pb = sjp[J - j0] + (uint32_t)PS * l0;
+      const uint32_t pb = sjp[J - j0] + (uint32_t)pat_off(PP, PX, (int)l0);
       while (m) {
         const int i = __ffs(m) - 1;
         m &= m - 1;
         const uint64_t gi = base + idx;
         if (gi < a.cap) {
           a.out_hz[gi] = HZ[tid * W + i];
-          a.out_pos[gi] = pb + (uint32_t)PS * (uint32_t)i;
+          a.out_pos[gi] = pb + pat_delta<PP, PX>(l0 % PX, (uint32_t)i);
           if (a.out_job) a.out_job[gi] = J;
         }
         ++idx;
@@ -711,7 +767,8 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract2(X2Args a) {
 // code-word range, and whether it is a single job whose bytes can be read unchecked
 __global__ void k_x2_tile_desc(const uint64_t* __restrict__ kb, const uint64_t* __restrict__ cw,
                                const Job* __restrict__ jobs, uint32_t n_jobs, uint64_t total_blocks, int W, int NB,
-                               int maxwords, int PS, uint32_t one0, uint64_t seq_bytes, uint64_t ntiles, X2Desc* desc) {
+                               int maxwords, int PP, int PX, uint32_t one0, uint64_t seq_bytes, uint64_t ntiles,
+                               X2Desc* desc) {
   for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < ntiles; t += (uint64_t)gridDim.x * blockDim.x) {
     const int64_t b_first = (int64_t)t * X2_OUT_BLOCKS - 1;
     const int64_t b_last = (int64_t)t * X2_OUT_BLOCKS + X2_NT - 2;
@@ -727,10 +784,11 @@ __global__ void k_x2_tile_desc(const uint64_t* __restrict__ kb, const uint64_t* 
     if (hi < lo) hi = lo;
     if (hi > lo + (uint64_t)maxwords) hi = lo + maxwords;
     const Job jb = jobs[j0];
-    const uint64_t last_byte = jb.seq_off + jb.phase + one0 + (uint64_t)PS * 16 * (hi - cw[j0]) + 4 * PS + 8;
+    // bytes touched up to word hi: base 16 (hi - cw) at offset <= (q / x + 1) p, plus the load width
+    const uint64_t last_byte = jb.seq_off + jb.phase + one0 + (16 * (hi - cw[j0]) / PX + 1) * PP + 48;
     // jobs are in sequence-buffer order: the tile's last bytes are those of job j1
     const Job jl = jobs[j1];
-    const uint64_t last_l = jl.seq_off + jl.phase + one0 + (uint64_t)PS * 16 * (hi - cw[j1]) + 4 * PS + 8;
+    const uint64_t last_l = jl.seq_off + jl.phase + one0 + (16 * (hi - cw[j1]) / PX + 1) * PP + 48;
     X2Desc d;
     d.j0 = j0;
     d.j1 = j1;
@@ -757,23 +815,23 @@ __global__ void k_x2_sizes(const Job* __restrict__ jobs, uint32_t n, int K, int 
   if ((threadIdx.x & 31) == 0 && acc) atomicAdd(nk_sum, (unsigned long long)acc);
 }
 
-template <int K, int W, int PS>
+template <int K, int W, int PP, int PX>
 size_t x2_smem_bytes() {
-  return X2Cfg<K, W, PS>::SMEM;
+  return X2Cfg<K, W, PP, PX>::SMEM;
 }
 
-template <int K, int W, int PS>
+template <int K, int W, int PP, int PX>
 void launch_x2(const X2Args& a, uint64_t ntiles, cudaStream_t st, const char* tag) {
   static int grid = 0;
-  const size_t smem = x2_smem_bytes<K, W, PS>();
+  const size_t smem = x2_smem_bytes<K, W, PP, PX>();
   if (!grid) {
-    GOD_CUDA(cudaFuncSetAttribute(k_extract2<K, W, PS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    GOD_CUDA(cudaFuncSetAttribute(k_extract2<K, W, PP, PX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
-    GOD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_extract2<K, W, PS>, X2_NT, smem));
+    GOD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_extract2<K, W, PP, PX>, X2_NT, smem));
     grid = (per_sm > 0 ? per_sm : 1) * num_sms();
   }
   const unsigned g = (unsigned)(ntiles < (uint64_t)grid ? ntiles : (uint64_t)grid);
-  GOD_LAUNCH(tag, (k_extract2<K, W, PS>), g, X2_NT, smem, st, a);
+  GOD_LAUNCH(tag, (k_extract2<K, W, PP, PX>), g, X2_NT, smem, st, a);
 }
 
 }  // namespace
@@ -782,8 +840,13 @@ void launch_x2(const X2Args& a, uint64_t ntiles, cudaStream_t st, const char* ta
 bool run_extract2(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const Job* jobs, uint32_t n_jobs,
                   bool want_job, bool want_job_off, Records& rec, cudaStream_t st, Scratch& scr,
                   uint64_t cap_hint, const char* tag) {
-  if (P.pat.x != 1 || (P.pat.p != 1 && P.pat.p != 2)) return false;
-  const int K = P.k, W = P.w, PS = (int)P.pat.p;
+  // patterns: x = 1 with p <= 2 (any rotation), or p = x + 1 <= 4 with the ones first ("110", "1110")
+  const int PP = (int)P.pat.p, PX = (int)P.pat.x;
+  bool pat_ok = (PX == 1 && PP <= 2) || ((PX == 2 || PX == 3) && PP == PX + 1);
+  if (PX >= 2)
+    for (int i = 0; i < PX; i++) pat_ok = pat_ok && P.pat.one[i] == (uint32_t)i;
+  if (!pat_ok) return false;
+  const int K = P.k, W = P.w;
   auto supported = [&](int k, int w) { return K == k && W == w; };
   if (!(supported(21, 11) || supported(19, 19) || supported(15, 10))) return false;
   if (getenv("GOD_DISABLE_X2")) return false;
@@ -818,7 +881,7 @@ bool run_extract2(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const
     const int NB = W + K - 1;
     const int maxwords = (X2_NT * W + X2_NT * (K - 1) + 15) / 16 + X2_NT + 8;  // X2Cfg::MAXWORDS
     GOD_LAUNCH("k_x2_tile_desc", k_x2_tile_desc, grid_for(ntiles, 256), 256, 0, st, kb, cw, jobs, n_jobs, total_blocks,
-               W, NB, maxwords, PS, P.pat.one[0], seq_bytes, ntiles, desc);
+               W, NB, maxwords, PP, PX, P.pat.one[0], seq_bytes, ntiles, desc);
   }
   uint64_t* dtotal = scr.alloc<uint64_t>(1);
   if (want_job_off) rec.job_off = scr.alloc<uint64_t>(n_jobs + 1);
@@ -845,16 +908,16 @@ bool run_extract2(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const
     X2Args a{seq, seq_bytes, jobs, kb, cw, n_jobs, total_blocks, P.pat.one[0], key_shift, status, ctr,
              rec.hz, rec.pos, rec.job, rec.job_off, cap, dtotal, dbg_flags, dbg_counts, desc};
     if (ntiles) {
-      if (K == 21 && W == 11) {
-        if (PS == 2) launch_x2<21, 11, 2>(a, ntiles, st, tag);
-        else launch_x2<21, 11, 1>(a, ntiles, st, tag);
-      } else if (K == 19 && W == 19) {
-        if (PS == 2) launch_x2<19, 19, 2>(a, ntiles, st, tag);
-        else launch_x2<19, 19, 1>(a, ntiles, st, tag);
-      } else {
-        if (PS == 2) launch_x2<15, 10, 2>(a, ntiles, st, tag);
-        else launch_x2<15, 10, 1>(a, ntiles, st, tag);
-      }
+      auto by_pattern = [&](auto kc, auto wc) {
+        constexpr int KK = decltype(kc)::value, WW = decltype(wc)::value;
+        if (PX == 1 && PP == 1) launch_x2<KK, WW, 1, 1>(a, ntiles, st, tag);
+        else if (PX == 1) launch_x2<KK, WW, 2, 1>(a, ntiles, st, tag);
+        else if (PX == 2) launch_x2<KK, WW, 3, 2>(a, ntiles, st, tag);
+        else launch_x2<KK, WW, 4, 3>(a, ntiles, st, tag);
+      };
+      if (K == 21 && W == 11) by_pattern(std::integral_constant<int, 21>(), std::integral_constant<int, 11>());
+      else if (K == 19 && W == 19) by_pattern(std::integral_constant<int, 19>(), std::integral_constant<int, 19>());
+      else by_pattern(std::integral_constant<int, 15>(), std::integral_constant<int, 10>());
     } else {
       GOD_CUDA(cudaMemsetAsync(dtotal, 0, sizeof(uint64_t), st));
     }
