@@ -118,6 +118,8 @@ class ClockSampler:
         self.lines = []
 
     def start(self):
+        if os.environ.get("GOD_BENCH_NO_CLOCKS"):  # diagnostic: run without the sampler
+            return
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={','.join(self.FIELDS)}",
@@ -294,13 +296,20 @@ def main():
     droffs = torch.from_numpy(cfg.reads.offsets).to(dev)
     torch.cuda.synchronize()
 
+    outbuf = {}
+
     def step(cap=None, ev=None):
         if ev:
             ev[0].record()
         ix = god.god_build_index(dref, droff, pattern, k, w, cutoff=cfg.cutoff)
         if ev:
             ev[1].record()
-        an, ao, ph = god.god_seed_reads(ix, dreads, droffs, cap=cap)
+        if cap is not None and "an" not in outbuf:  # steady state: preallocated outputs, no allocation per step
+            outbuf["an"] = torch.empty((cap, 4), dtype=torch.uint32, device=dev)
+            outbuf["ao"] = torch.empty(n_reads + 1, dtype=torch.uint64, device=dev)
+            outbuf["ph"] = torch.empty(max(1, n_reads), dtype=torch.uint8, device=dev)
+        out = (outbuf["an"], outbuf["ao"], outbuf["ph"]) if cap is not None else None
+        an, ao, ph = god.god_seed_reads(ix, dreads, droffs, cap=cap, out=out)
         if ev:
             ev[2].record()
         st = ix.stats()
@@ -342,6 +351,8 @@ def main():
     elapsed_ms = start.elapsed_time(end)
     build_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in evs]))
     seed_ms = float(np.mean([e[1].elapsed_time(e[2]) for e in evs]))
+    log("[bench] per-step build/seed ms: " + " ".join(f"{e[0].elapsed_time(e[1]):.1f}/{e[1].elapsed_time(e[2]):.1f}"
+                                                      for e in evs))
     elapsed_ms = max_over_ranks(elapsed_ms, dist, dev)
     ms_per_step = elapsed_ms / args.steps
     value = aggregate_rate(n_reads, world, ms_per_step)

@@ -197,25 +197,39 @@ def god_build_index(ref, ref_offsets, pattern: str, k: int, w: int, cutoff=(1, 5
 
 
 # ---------------------------------------------------------------------------------------- stage 4
-def god_seed_reads(index: GodIndex, reads, read_offsets, phases=None, t: int = 16, cap: int | None = None):
+def god_seed_reads(index: GodIndex, reads, read_offsets, phases=None, t: int = 16, cap: int | None = None,
+                   out=None):
     """SELECT mode if phases is None (phase per read computed), else GIVEN.
     -> (anchors, anchor_offsets u64[n+1], phases u8[n]).  Device path: anchors is a CUDA u32 tensor
-    of shape (n_anchors, 4) = (ref_pos, read_pos, read_id, strand); host path: structured numpy."""
+    of shape (n_anchors, 4) = (ref_pos, read_pos, read_id, strand); host path: structured numpy.
+    out = (anchors, anchor_offsets, phases) preallocated (device path; anchors (cap, 4) u32) avoids
+    per-call allocations in a serving loop."""
     L = _lib.load()
     dev = _is_cuda(reads)
     reads, read_offsets = _prep(reads, np.uint8), _prep(read_offsets, np.uint64)
     n = int(read_offsets.shape[0]) - 1
     dv = reads.device if dev else None
     mode = _lib.PHASE_SELECT if phases is None else _lib.PHASE_GIVEN
-    ph = _empty(max(1, n), np.uint8, dev, dv) if phases is None else _prep(phases, np.uint8).clone() if dev \
-        else _prep(phases, np.uint8).copy()
-    ao = _empty(n + 1, np.uint64, dev, dv)
+    if out is not None:
+        an_out, ao, ph = out
+        if phases is not None:
+            ph[:n].copy_(_prep(phases, np.uint8))
+        cap = int(an_out.shape[0])
+    else:
+        an_out = None
+        ph = _empty(max(1, n), np.uint8, dev, dv) if phases is None else _prep(phases, np.uint8).clone() if dev \
+            else _prep(phases, np.uint8).copy()
+        ao = _empty(n + 1, np.uint64, dev, dv)
     if cap is None:
         cap = int(reads.shape[0]) // 4 + 1024
     need = ctypes.c_uint64(0)
     st = _stream(dev)
     for _ in range(2):
-        an = torch.empty((max(1, cap), 4), dtype=torch.uint32, device=dv) if dev else np.zeros(max(1, cap), ANCHOR_DTYPE)
+        if an_out is not None and cap <= int(an_out.shape[0]):
+            an = an_out
+        else:
+            an = torch.empty((max(1, cap), 4), dtype=torch.uint32, device=dv) if dev else \
+                np.zeros(max(1, cap), ANCHOR_DTYPE)
         rc = L.god_seed_reads(index.handle, _ptr(reads), _ptr(read_offsets), n, mode, _ptr(ph), int(t), _ptr(an),
                               _ptr(ao), cap, ctypes.byref(need), st)
         if rc == _lib.GOD_ETRUNC:
