@@ -1,18 +1,21 @@
-#include <algorithm>
 // index.cu — stage 3: the seed index (P:286 (3)).
 //
 // "We do not directly insert minimizer information ... Instead, we append the minimizer
 // information to an array and sort the array after collecting information on all minimizers and
-// then add it to the hash table".  B200 version (kernels K2-K6):
-//   K1  fused sparsify+minimizer extraction of the reference (extract.cu) -> records in position order
-//   K2  stable LSD radix sort of (hash | strand<<63, pos) on the 2k hash bits, 8-bit digits:
-//       per pass: tile histograms -> exclusive scan (digit-major) -> stable scatter staged in SMEM
-//       (position order within equal hashes is preserved, so the result is (hash, pos) order)
-//   K3  run heads -> distinct index (scan) -> per-distinct start / count
+// then add it to the hash table".  B200 version:
+//   K1  fused sparsify+minimizer extraction of the reference (extract2.cu / extract.cu) -> records
+//       (hash | strand << 63, pos) in position order
+//   K2  sort to (hash, pos) order.  2k >= 36: data-sized monotone bins over the top 12 hash bits
+//       (k_seg_hist / k_seg_table / k_seg_assign), two stable 9-bit LSD passes over the bin number
+//       (k_rs_hist, scan, k_rs_scatter2), then a per-bin SMEM sort on (low hash, pos) (k_bin_sort;
+//       oversized bins: k_bucket_sort_big).  Otherwise a stable 8-bit LSD over all 2k hash bits.
+//   K3  runs of equal hashes = distinct hashes: fused into the bin sorts (run lengths in the key's
+//       free bits + count histogram); k_runs on the full-LSD path
 //   K4  cutoff tau on device (reading O7): count histogram (small counts) + radix select
 //       over the rare large counts; tau = (m+1)-th largest count, m = floor(n*num/den)
-//   K5  kept-entry offsets (scan), entry write: key = low (2k-B) hash bits << 1 | strand, pos
-//   K6  directory over the top B hash bits (gap fill over the kept entries' slots)
+//   K5  kept entries in one ordered pass (k_keep_write: ballots + decoupled look-back)
+//   K6  directory: data-sized slot map (or top-B-bit prefix) -> 32-B slot records
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>

@@ -7,8 +7,10 @@
 //   S2  one thread per read: c = min(t, min_s |M_s|), score_s = sum over the first c records of
 //       occ(hash) (index probes), a = argmax (smallest s on ties).  Reads whose capped prefix gave
 //       fewer than t exact records for some phase (N-dense prefixes) are recomputed uncapped.
-//   S3  extraction over the (read, a_r) jobs -> all minimizers of PQ_a
-//   S4  per record: probe -> anchor count; exclusive scan; probe again -> write anchors
+//   S3  the minimizers of PQ_a: reused from S1 when the read's phase-a job was complete
+//       (every short read), else extracted again over (read, a_r) jobs and probed
+//   S4  anchors from the probe results: fast path (all reads from S1) = 8-lane groups per read
+//       (counts, scan over reads, write); general path = gather into read order, scan, write
 #include <algorithm>
 #include <cstdlib>
 #include "internal.cuh"
