@@ -20,6 +20,10 @@ _lib = None
 
 MZ_DTYPE = np.dtype([("hash", "<u8"), ("pos", "<u8"), ("strand", "u1")], align=True)
 ANCHOR_DTYPE = np.dtype([("read_id", "<u4"), ("ref_pos", "<u4"), ("read_pos", "<u4"), ("strand", "<u4")])
+HIT_DTYPE = np.dtype([("hash", "<u8"), ("diag", "<i8"), ("strand", "<u4"), ("ref_pos", "<u4"),
+                      ("read_pos", "<u4")], align=True)
+VOTE_DTYPE = np.dtype([("read_id", "<u4"), ("strand", "<u4"), ("diag", "<i8"), ("votes", "<u4"), ("rescued", "<u4"),
+                       ("ref_lo", "<u4"), ("ref_hi", "<u4"), ("read_lo", "<u4"), ("read_hi", "<u4")])
 STATS_FIELDS = ("n_entries_all", "n_distinct_all", "m", "tau", "kept_entries", "dropped_entries",
                 "kept_distinct", "dropped_distinct")
 
@@ -60,6 +64,10 @@ def _load():
     L.or_seed_read.argtypes = [vp, vp, u64, u32, u32, vp, u64]; L.or_seed_read.restype = ctypes.c_int64
     L.or_seed_reads_batch.argtypes = [vp, vp, vp, u32, i32, vp, u32, vp, u64, vp]
     L.or_seed_reads_batch.restype = ctypes.c_int64
+    L.or_vote_hits.argtypes = [vp, u64, u64, u32, u32, u32, vp, u64]; L.or_vote_hits.restype = ctypes.c_int64
+    L.or_vote_read.argtypes = [vp, vp, u64, u32, u32, u32, u32, u32, vp, u64]; L.or_vote_read.restype = ctypes.c_int64
+    L.or_vote_reads_batch.argtypes = [vp, vp, vp, u32, vp, u32, u32, u32, vp, u64, vp]
+    L.or_vote_reads_batch.restype = ctypes.c_int64
     _lib = L
     return L
 
@@ -151,6 +159,19 @@ def minimizers_batch(seq, offsets, pattern: str, k: int, w: int, phases=None, gl
     return out, oo
 
 
+def vote_hits(hits, D: int, V: int = 3, max_pairs: int = 0, read_id: int = 0) -> np.ndarray:
+    """Location voting steps (2)-(4) + rescue on an explicit hit list (HIT_DTYPE, or tuples
+    (hash, diag, strand, ref_pos, read_pos)).  -> VOTE_DTYPE records."""
+    h = np.array(hits, dtype=HIT_DTYPE) if not isinstance(hits, np.ndarray) else hits.astype(HIT_DTYPE)
+    h = np.ascontiguousarray(h)
+    L = _load()
+    n = L.or_vote_hits(_p(h), h.size, D, V, max_pairs, read_id, None, 0)
+    out = np.zeros(n, VOTE_DTYPE)
+    h2 = h.copy()
+    L.or_vote_hits(_p(h2), h2.size, D, V, max_pairs, read_id, _p(out), n)
+    return out
+
+
 class Index:
     """Oracle seed index (O7).  `cutoff` = (num, den) fraction of distinct hashes, or max_occ override."""
 
@@ -214,3 +235,29 @@ class Index:
         ao = np.zeros(n + 1, np.uint64)
         L.or_seed_reads_batch(self._h, _p(reads), _p(offsets), n, mode, _p(ph), t, _p(out), tot, _p(ao))
         return out, ao, ph
+
+    def vote_read(self, read, a: int, D: int = 0, V: int = 3, max_pairs: int = 0, read_id: int = 0) -> np.ndarray:
+        read = _u8(read)
+        L = _load()
+        n = L.or_vote_read(self._h, _p(read), read.size, a, read_id, D, V, max_pairs, None, 0)
+        if n < 0:
+            raise ValueError("invalid voting parameters")
+        out = np.zeros(n, VOTE_DTYPE)
+        L.or_vote_read(self._h, _p(read), read.size, a, read_id, D, V, max_pairs, _p(out), n)
+        return out
+
+    def vote_reads(self, reads, offsets, phases, D: int = 0, V: int = 3, max_pairs: int = 0):
+        """Location voting of every read with its phase.
+        -> (votes VOTE_DTYPE, vote_offsets u64[n+1])"""
+        reads = _u8(reads)
+        offsets = np.ascontiguousarray(offsets, dtype=np.uint64)
+        n = offsets.size - 1
+        ph = np.ascontiguousarray(phases, dtype=np.uint8)
+        L = _load()
+        tot = L.or_vote_reads_batch(self._h, _p(reads), _p(offsets), n, _p(ph), D, V, max_pairs, None, 0, None)
+        if tot < 0:
+            raise ValueError("invalid voting parameters")
+        out = np.zeros(tot, VOTE_DTYPE)
+        vo = np.zeros(n + 1, np.uint64)
+        L.or_vote_reads_batch(self._h, _p(reads), _p(offsets), n, _p(ph), D, V, max_pairs, _p(out), tot, _p(vo))
+        return out, vo

@@ -382,3 +382,148 @@ int64_t or_seed_reads_batch(const or_index* ix, const uint8_t* reads, const uint
     if (anchor_offsets) anchor_offsets[n] = tot;
     return tot > cap && out ? -1 : (int64_t)tot;
 }
+
+/* ------------------------------------------------------------------------------------------ */
+/* Location voting (P:312-324 steps (1)-(4), Fig. 8) and the rescue location.
+ * Readings (V1-V6):
+ *  V1 adjusted location ("subtract the location of each seed extracted from the read sequence
+ *     from that of its corresponding matching seed"): forward hit (strand 0)
+ *     diag = ref_pos - read_pos; reverse hit (strand 1) diag = ref_pos + read_end, read_end = the
+ *     original read coordinate of the read k-mer's LAST included base (O9's reverse invariant:
+ *     colinear reverse hits share ref_pos + read_end = g + L - 1).
+ *  V2 "consider both repeated seeds (e.g., having the same hash value) ... and repeated mapping
+ *     locations only once": hits with equal (hash, strand, diag) are one vote.
+ *  V3 the sweep runs over the hits sorted by (strand, diag); each strand is its own
+ *     coordinate system: Delta0 = first diag, members = following hits of the same strand with
+ *     diag - Delta0 <= D, the first hit beyond D (or of the other strand) is the next Delta0.
+ *  V4 a cluster wins iff votes >= V; winners are sorted by votes (descending; ties by
+ *     strand, then Delta0, ascending) and truncated to max_pairs ("we limit the size of the list
+ *     ... to a user-defined number"; 0 = no limit).
+ *  V5 rescue: if no cluster wins and the read has hits, the output is the single cluster
+ *     with the most votes (same tie order), flagged rescued.
+ *  V6 each cluster reports the ref / read spans [min, max] of its member hits (Fig. 8B's
+ *     subsequence pairs); D = 0 means D = read length (SPEC's short-read default). */
+static int cmp_hit(const void* a, const void* b) {
+    const or_hit* x = (const or_hit*)a; const or_hit* y = (const or_hit*)b;
+    if (x->strand != y->strand) return x->strand < y->strand ? -1 : 1;
+    if (x->diag != y->diag) return x->diag < y->diag ? -1 : 1;
+    if (x->hash != y->hash) return x->hash < y->hash ? -1 : 1;
+    if (x->ref_pos != y->ref_pos) return x->ref_pos < y->ref_pos ? -1 : 1;
+    if (x->read_pos != y->read_pos) return x->read_pos < y->read_pos ? -1 : 1;
+    return 0;
+}
+
+/* V4 order: more votes first, then smaller strand, then smaller Delta0 */
+static int vote_before(const or_vote* x, const or_vote* y) {
+    if (x->votes != y->votes) return x->votes > y->votes;
+    if (x->strand != y->strand) return x->strand < y->strand;
+    return x->diag < y->diag;
+}
+static int cmp_vote(const void* a, const void* b) {
+    const or_vote* x = (const or_vote*)a; const or_vote* y = (const or_vote*)b;
+    return vote_before(x, y) ? -1 : (vote_before(y, x) ? 1 : 0);
+}
+
+int64_t or_vote_hits(or_hit* hits, uint64_t n, uint64_t D, uint32_t V, uint32_t max_pairs, uint32_t read_id,
+                     or_vote* out, uint64_t cap) {
+    if (n == 0) return 0;
+    /* step (2): a single sorted list (the paper merges the per-seed sorted lists; qsort here) */
+    qsort(hits, (size_t)n, sizeof(or_hit), cmp_hit);
+    /* step (3): sweep */
+    or_vote* cl = (or_vote*)malloc(sizeof(or_vote) * (size_t)n);
+    uint64_t ncl = 0, i = 0;
+    while (i < n) {
+        or_vote c;
+        memset(&c, 0, sizeof c);
+        c.read_id = read_id; c.strand = hits[i].strand; c.diag = hits[i].diag;
+        c.ref_lo = c.ref_hi = hits[i].ref_pos; c.read_lo = c.read_hi = hits[i].read_pos;
+        uint64_t j = i;
+        while (j < n && hits[j].strand == c.strand && (uint64_t)(hits[j].diag - c.diag) <= D) {
+            /* V2: one vote per distinct (hash, strand, diag) — duplicates are adjacent after the sort */
+            int dup = j > i && hits[j].diag == hits[j - 1].diag && hits[j].hash == hits[j - 1].hash;
+            if (!dup) c.votes++;
+            if (hits[j].ref_pos < c.ref_lo) c.ref_lo = hits[j].ref_pos;
+            if (hits[j].ref_pos > c.ref_hi) c.ref_hi = hits[j].ref_pos;
+            if (hits[j].read_pos < c.read_lo) c.read_lo = hits[j].read_pos;
+            if (hits[j].read_pos > c.read_hi) c.read_hi = hits[j].read_pos;
+            j++;
+        }
+        cl[ncl++] = c;
+        i = j;                       /* the first location beyond D is the next Delta0 */
+    }
+    /* step (4): winners (votes >= V), sorted by votes, capped; else the rescue location */
+    or_vote* win = (or_vote*)malloc(sizeof(or_vote) * (size_t)ncl);
+    uint64_t nw = 0;
+    for (uint64_t q = 0; q < ncl; q++) if (cl[q].votes >= V) win[nw++] = cl[q];
+    int64_t res;
+    if (nw > 0) {
+        qsort(win, (size_t)nw, sizeof(or_vote), cmp_vote);
+        if (max_pairs && nw > max_pairs) nw = max_pairs;
+        for (uint64_t q = 0; q < nw && q < cap; q++) if (out) out[q] = win[q];
+        res = (int64_t)nw;
+    } else {
+        uint64_t b = 0;
+        for (uint64_t q = 1; q < ncl; q++) if (vote_before(&cl[q], &cl[b])) b = q;
+        cl[b].rescued = 1;
+        if (out && cap) out[0] = cl[b];
+        res = 1;
+    }
+    free(win);
+    free(cl);
+    return res;
+}
+
+/* Step (1) for one read: the minimizers of PQ_a (O6 on Sparsify(read, P, a)) matched against the
+ * index (O9), each match turned into an adjusted location (V1). */
+int64_t or_vote_read(const or_index* ix, const uint8_t* read, uint64_t L, uint32_t a, uint32_t read_id,
+                     uint32_t D, uint32_t V, uint32_t max_pairs, or_vote* out, uint64_t cap) {
+    if (a >= ix->P.p) return -1;
+    int64_t c = or_minimizers(read, L, &ix->P, a, ix->k, ix->w, 0, NULL, 0);
+    if (c <= 0) return c;
+    or_mz* M = (or_mz*)malloc(sizeof(or_mz) * (size_t)c);
+    or_minimizers(read, L, &ix->P, a, ix->k, ix->w, 0, M, (uint64_t)c);
+    int64_t nj = or_sparsify(read, L, &ix->P, a, NULL, NULL);
+    uint64_t* orig = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)(nj ? nj : 1));
+    or_sparsify(read, L, &ix->P, a, NULL, orig);
+    uint64_t nh = 0;
+    for (int64_t i = 0; i < c; i++) { int64_t q = find_key(ix, M[i].hash); if (q >= 0) nh += ix->key_count[q]; }
+    or_hit* H = (or_hit*)malloc(sizeof(or_hit) * (size_t)(nh ? nh : 1));
+    uint64_t h = 0;
+    for (int64_t i = 0; i < c; i++) {
+        int64_t q = find_key(ix, M[i].hash);
+        if (q < 0) continue;
+        /* the read k-mer starting at orig[j] = pos ends at orig[j + k - 1] */
+        int64_t j = 0;
+        while ((uint64_t)orig[j] != M[i].pos) j++;
+        uint64_t read_end = orig[j + ix->k - 1];
+        for (uint64_t e = ix->key_first[q]; e < ix->key_first[q] + ix->key_count[q]; e++) {
+            or_hit* t = &H[h++];
+            t->hash = M[i].hash;
+            t->strand = (uint32_t)(ix->strand[e] ^ M[i].strand);
+            t->ref_pos = (uint32_t)ix->pos[e];
+            t->read_pos = (uint32_t)M[i].pos;
+            t->diag = t->strand == 0 ? (int64_t)ix->pos[e] - (int64_t)M[i].pos
+                                     : (int64_t)ix->pos[e] + (int64_t)read_end;
+        }
+    }
+    int64_t r = or_vote_hits(H, nh, D ? D : L, V, max_pairs, read_id, out, cap);
+    free(M); free(orig); free(H);
+    return r;
+}
+
+int64_t or_vote_reads_batch(const or_index* ix, const uint8_t* reads, const uint64_t* offsets, uint32_t n,
+                            const uint8_t* phases, uint32_t D, uint32_t V, uint32_t max_pairs, or_vote* out,
+                            uint64_t cap, uint64_t* vote_offsets) {
+    uint64_t tot = 0;
+    for (uint32_t r = 0; r < n; r++) {
+        uint32_t a = phases ? phases[r] : 0;
+        if (vote_offsets) vote_offsets[r] = tot;
+        uint64_t room = tot < cap ? cap - tot : 0;
+        int64_t c = or_vote_read(ix, reads + offsets[r], offsets[r + 1] - offsets[r], a, r,
+                                 D, V, max_pairs, out ? out + (tot < cap ? tot : cap) : NULL, room);
+        if (c < 0) return -1;
+        tot += (uint64_t)c;
+    }
+    if (vote_offsets) vote_offsets[n] = tot;
+    return tot > cap && out ? -1 : (int64_t)tot;
+}

@@ -34,6 +34,15 @@ typedef struct { uint64_t hash; uint64_t pos; uint8_t strand; } or_mz;
 
 typedef struct { uint32_t read_id; uint32_t ref_pos; uint32_t read_pos; uint32_t strand; } or_anchor;
 
+/* one adjusted location (P:314 step (1)) and one voted location */
+typedef struct { uint64_t hash; int64_t diag; uint32_t strand; uint32_t ref_pos, read_pos; } or_hit;
+typedef struct {
+    uint32_t read_id, strand;
+    int64_t diag;                 /* Delta0 */
+    uint32_t votes, rescued;
+    uint32_t ref_lo, ref_hi, read_lo, read_hi;   /* member spans */
+} or_vote;
+
 typedef struct {
     uint64_t n_entries_all, n_distinct_all, m, tau;
     uint64_t kept_entries, dropped_entries, kept_distinct, dropped_distinct;
@@ -85,6 +94,21 @@ int64_t or_seed_read(const or_index* ix, const uint8_t* read, uint64_t L, uint32
 int64_t or_seed_reads_batch(const or_index* ix, const uint8_t* reads, const uint64_t* offsets, uint32_t n,
                             int mode, uint8_t* phases, uint32_t t, or_anchor* out, uint64_t cap,
                             uint64_t* anchor_offsets);
+
+/* Location voting (readings V1-V6 in oracle.c / DESIGN.md §2).
+ * or_vote_hits: steps (2)-(4) + rescue on a given hit list (sorted in place).  D = max distance,
+ * V = vote threshold, max_pairs = cap on winners (0 = none).  Returns the number of voted
+ * locations (writes up to cap). */
+int64_t or_vote_hits(or_hit* hits, uint64_t n, uint64_t D, uint32_t V, uint32_t max_pairs, uint32_t read_id,
+                     or_vote* out, uint64_t cap);
+/* Step (1) from the read: minimizers of PQ_a matched against the index, then or_vote_hits with
+ * D (0 = read length). */
+int64_t or_vote_read(const or_index* ix, const uint8_t* read, uint64_t L, uint32_t a, uint32_t read_id,
+                     uint32_t D, uint32_t V, uint32_t max_pairs, or_vote* out, uint64_t cap);
+/* Batch over CSR reads with given phases (NULL = all 0); vote_offsets[n+1]. */
+int64_t or_vote_reads_batch(const or_index* ix, const uint8_t* reads, const uint64_t* offsets, uint32_t n,
+                            const uint8_t* phases, uint32_t D, uint32_t V, uint32_t max_pairs, or_vote* out,
+                            uint64_t cap, uint64_t* vote_offsets);
 
 #ifdef __cplusplus
 }
