@@ -152,6 +152,45 @@ GOD_API god_status god_seed_reads(const god_index* idx, const uint8_t* reads, co
                                   god_anchor* anchors, uint64_t* anchor_offsets, uint64_t cap, uint64_t* needed,
                                   god_stream stream);
 
+/* ---- location voting (section 3.4, Fig. 8; rescue P:398) ----
+ * Consumes the anchors of god_seed_reads (same reads, same phases).  Readings (DESIGN.md §2,
+ * V1-V6):
+ *  (1) adjusted location of each anchor: forward (strand 0) diag = ref_pos - read_pos;
+ *      reverse (strand 1) diag = ref_pos + read_end, read_end = original read coordinate of the
+ *      read k-mer's last included base under the read's phase (colinear reverse anchors share
+ *      it).  Anchors with equal (hash, strand, diag) are one vote ("consider both repeated
+ *      seeds ... and repeated mapping locations only once").
+ *  (2)-(3) one sorted list per read; sweep per strand: Delta0 = the first diag, the
+ *      cluster takes the following anchors with diag - Delta0 <= D, the first beyond D is the next
+ *      Delta0.  D = 0 means D = the read's length.
+ *  (4) winners: votes >= V, sorted by votes descending (ties: strand, then Delta0 ascending),
+ *      at most max_pairs (0 = no limit).  No winner and >= 1 anchor: the single
+ *      best cluster, rescued = 1.  No anchor: no location.
+ * Each location reports the [min, max] ref_pos and read_pos of its member anchors (Fig. 8B's
+ * subsequence pairs).  Output CSR: locations of read r in [out_offsets[r], out_offsets[r+1]);
+ * read_id = r.  cap = location capacity (GOD_ETRUNC + *needed).  GOD_EINVAL if an anchor's
+ * read_pos is not an included position of its read under phases[r] (anchors and phases from
+ * different calls), or a read has >= 2^29 anchors.  Synchronizes. */
+typedef struct {
+    uint32_t D;           /* maximum allowed distance; 0 = read length */
+    uint32_t V;           /* voting threshold */
+    uint32_t max_pairs;   /* cap on winning locations per read; 0 = no limit */
+} god_vote_params;
+
+typedef struct {
+    uint32_t read_id;
+    uint32_t strand;      /* 0 forward, 1 reverse complement */
+    int64_t diag;         /* Delta0 (forward: ref - read; reverse: ref + read_end) */
+    uint32_t votes;
+    uint32_t rescued;     /* 1: the read's rescue location (votes < V) */
+    uint32_t ref_lo, ref_hi, read_lo, read_hi;
+} god_vote;
+
+GOD_API god_status god_vote_reads(const god_index* idx, const uint8_t* reads, const uint64_t* read_offsets,
+                                  uint32_t n_reads, const uint8_t* phases, const god_anchor* anchors,
+                                  const uint64_t* anchor_offsets, const god_vote_params* vp, god_vote* out,
+                                  uint64_t* out_offsets, uint64_t cap, uint64_t* needed, god_stream stream);
+
 /* ---- tracing: per-kernel device time by CUDA events on the launching stream ----
  * Off by default.  When on, every kernel launch is bracketed by two events; god_profile_query
  * synchronizes on the pending events and returns, per kernel name (in first-launch order), the

@@ -23,6 +23,9 @@ except Exception:  # pragma: no cover - torch is in the image
     torch = None
 
 ANCHOR_DTYPE = np.dtype([("ref_pos", "<u4"), ("read_pos", "<u4"), ("read_id", "<u4"), ("strand", "<u4")])
+# god_vote (include/god.h): 40 bytes; the device path returns it as a (n, 10) u32 tensor (diag = words 2-3)
+VOTE_DTYPE = np.dtype([("read_id", "<u4"), ("strand", "<u4"), ("diag", "<i8"), ("votes", "<u4"), ("rescued", "<u4"),
+                       ("ref_lo", "<u4"), ("ref_hi", "<u4"), ("read_lo", "<u4"), ("read_hi", "<u4")])
 
 
 # ---------------------------------------------------------------------------------------- helpers
@@ -241,6 +244,49 @@ def god_seed_reads(index: GodIndex, reads, read_offsets, phases=None, t: int = 1
     raise GodError(_lib.GOD_ETRUNC, "anchor capacity retry failed")
 
 
+# ---------------------------------------------------------------------------------------- voting
+def god_vote_reads(index: GodIndex, reads, read_offsets, phases, anchors, anchor_offsets, D: int = 0, V: int = 3,
+                   max_pairs: int = 0, cap: int | None = None):
+    """Location voting (rescue P:398) on the anchors of god_seed_reads (same reads and
+    phases).  D = 0: the read length.  -> (votes, vote_offsets u64[n+1]).  Device path: votes is a
+    (n_votes, 10) u32 CUDA tensor in god_vote layout (votes_numpy() converts); host path: VOTE_DTYPE."""
+    L = _lib.load()
+    dev = _is_cuda(reads)
+    reads, read_offsets = _prep(reads, np.uint8), _prep(read_offsets, np.uint64)
+    phases, anchor_offsets = _prep(phases, np.uint8), _prep(anchor_offsets, np.uint64)
+    if dev:
+        anchors = anchors.contiguous()
+    else:
+        anchors = np.ascontiguousarray(anchors)
+    n = int(read_offsets.shape[0]) - 1
+    dv = reads.device if dev else None
+    vo = _empty(n + 1, np.uint64, dev, dv)
+    vp = _lib.GodVoteParams(int(D), int(V), int(max_pairs))
+    if cap is None:
+        cap = n * (max_pairs if max_pairs else 4) + 16
+    need = ctypes.c_uint64(0)
+    st = _stream(dev)
+    for _ in range(2):
+        out = torch.empty((max(1, cap), 10), dtype=torch.uint32, device=dv) if dev else \
+            np.zeros(max(1, cap), VOTE_DTYPE)
+        rc = L.god_vote_reads(index.handle, _ptr(reads), _ptr(read_offsets), n, _ptr(phases), _ptr(anchors),
+                              _ptr(anchor_offsets), ctypes.byref(vp), _ptr(out), _ptr(vo), cap, ctypes.byref(need), st)
+        if rc == _lib.GOD_ETRUNC:
+            cap = need.value
+            continue
+        _lib.check(rc)
+        return out[: need.value], vo
+    raise GodError(_lib.GOD_ETRUNC, "vote capacity retry failed")
+
+
+def votes_numpy(votes) -> np.ndarray:
+    """(n, 10) u32 device/host array in god_vote layout -> VOTE_DTYPE numpy records."""
+    if _is_cuda(votes):
+        votes = votes.cpu().numpy()
+    a = np.ascontiguousarray(votes)
+    return a.view(VOTE_DTYPE).reshape(-1) if a.dtype != VOTE_DTYPE else a
+
+
 # ---------------------------------------------------------------------------------------- tracing
 def profile_enable(on: bool = True):
     _lib.load().god_profile_enable(int(on))
@@ -272,5 +318,5 @@ def launch_count() -> int:
     return int(_lib.load().god_launch_count())
 
 
-__all__ = ["god_sparsify", "god_minimizers", "god_build_index", "god_seed_reads", "GodIndex", "GodError",
-           "ANCHOR_DTYPE", "version"]
+__all__ = ["god_sparsify", "god_minimizers", "god_build_index", "god_seed_reads", "god_vote_reads", "votes_numpy",
+           "GodIndex", "GodError", "ANCHOR_DTYPE", "VOTE_DTYPE", "version"]

@@ -22,6 +22,10 @@ class GodCutoff(ctypes.Structure):
                 ("max_occ", ctypes.c_uint32)]
 
 
+class GodVoteParams(ctypes.Structure):
+    _fields_ = [("D", ctypes.c_uint32), ("V", ctypes.c_uint32), ("max_pairs", ctypes.c_uint32)]
+
+
 STATS_FIELDS = ("n_entries_all", "n_distinct_all", "m", "tau", "kept_entries", "dropped_entries",
                 "kept_distinct", "dropped_distinct")
 
@@ -35,6 +39,7 @@ class GodIndexStats(ctypes.Structure):
 # every symbol include/god.h declares (tests/test_abi.py checks header <-> library agreement)
 EXPORTS = ("god_last_error", "god_version", "god_sparsify", "god_minimizers", "god_build_index",
            "god_index_get_stats", "god_index_dump", "god_index_count", "god_index_free", "god_seed_reads",
+           "god_vote_reads",
            "god_profile_enable", "god_profile_reset", "god_profile_query", "god_launch_count",
            "god_profile_units")
 
@@ -62,6 +67,7 @@ def load():
     L.god_index_free.argtypes = [vp]
     L.god_index_free.restype = None
     L.god_seed_reads.argtypes = [vp, vp, vp, u32, i32, vp, u32, vp, vp, u64, P(ctypes.c_uint64), vp]
+    L.god_vote_reads.argtypes = [vp, vp, vp, u32, vp, vp, vp, P(GodVoteParams), vp, vp, u64, P(ctypes.c_uint64), vp]
     L.god_profile_enable.argtypes = [ctypes.c_int]
     L.god_profile_enable.restype = None
     L.god_profile_reset.argtypes = []

@@ -570,4 +570,38 @@ GOD_API god_status god_seed_reads(const god_index* idx, const uint8_t* reads, co
   });
 }
 
+GOD_API god_status god_vote_reads(const god_index* idx, const uint8_t* reads, const uint64_t* read_offsets,
+                                  uint32_t n_reads, const uint8_t* phases, const god_anchor* anchors,
+                                  const uint64_t* anchor_offsets, const god_vote_params* vp, god_vote* out,
+                                  uint64_t* out_offsets, uint64_t cap, uint64_t* needed, god_stream stream) {
+  return guarded([&] {
+    GOD_REQUIRE(idx && read_offsets && anchor_offsets && vp && out_offsets && needed, "NULL argument");
+    GOD_REQUIRE(n_reads == 0 || phases, "NULL phases");
+    GOD_REQUIRE(cap == 0 || out, "NULL output with nonzero capacity");
+    if (!is_device_ptr(phases) && phases)
+      for (uint32_t i = 0; i < n_reads; i++) GOD_REQUIRE(phases[i] < idx->P.pat.p, "phase >= p");
+    cudaStream_t st = (cudaStream_t)stream;
+    Scratch scr(st);
+    Stage sg(st, scr);
+    const uint64_t L = total_len(read_offsets, n_reads, st);
+    const uint64_t NA = total_len(anchor_offsets, n_reads, st);
+    const uint8_t* dreads = sg.in(reads, L);
+    const uint64_t* droff = sg.in(read_offsets, (size_t)n_reads + 1);
+    const uint8_t* dph = sg.in(phases, n_reads);
+    const god_anchor* dan = sg.in(anchors, NA);
+    const uint64_t* daoff = sg.in(anchor_offsets, (size_t)n_reads + 1);
+    GOD_REQUIRE(NA == 0 || dan, "NULL anchors");
+    uint64_t* doo = sg.out(out_offsets, (size_t)n_reads + 1);
+    god_vote* dout = out;
+    const bool host_out = out && !is_device_ptr(out);
+    if (host_out) dout = scr.alloc<god_vote>(cap);
+    const uint64_t tot = god::vote_reads(idx, dreads, droff, n_reads, dph, dan, daoff, *vp, dout, doo, cap, st);
+    *needed = tot;
+    if (host_out && tot <= cap && tot)
+      GOD_CUDA(cudaMemcpyAsync(out, dout, tot * sizeof(god_vote), cudaMemcpyDeviceToHost, st));
+    sg.finish();
+    if (tot > cap) throw Fail{GOD_ETRUNC};
+  });
+}
+
 }  // extern "C"

@@ -156,6 +156,11 @@ void index_dump(const god_index* ix, uint64_t* hash, uint32_t* pos, uint8_t* str
 uint64_t seed_reads(const god_index* ix, const uint8_t* reads, const uint64_t* offsets, uint32_t n_reads,
                     god_phase_mode mode, uint8_t* phases, uint32_t t, god_anchor* anchors, uint64_t* anchor_offsets,
                     uint64_t cap, cudaStream_t st, uint32_t rid_base = 0);
+// location voting on the anchors of seed_reads (vote.cu); returns the number of voted locations and
+// writes them (CSR by read) only if that is <= cap
+uint64_t vote_reads(const god_index* ix, const uint8_t* reads, const uint64_t* roff, uint32_t n_reads,
+                    const uint8_t* phases, const god_anchor* anchors, const uint64_t* aoff, const god_vote_params& vp,
+                    god_vote* out, uint64_t* out_off, uint64_t cap, cudaStream_t st);
 void sparsify(const Params& P, const uint8_t* seq, const uint64_t* offsets, uint32_t n, const uint8_t* phases,
               uint64_t* packed, uint64_t* nmask, uint64_t* out_offsets, uint64_t* counts, uint64_t cap_words,
               uint64_t* needed_host, cudaStream_t st);
