@@ -58,6 +58,10 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-vote", action="store_true")
+    ap.add_argument("--vote-D", type=int, default=0, help="voting distance D (0 = read length)")
+    ap.add_argument("--vote-V", type=int, default=3)
+    ap.add_argument("--vote-max-pairs", type=int, default=0)
     ap.add_argument("--cpu-sample-bp", type=int, default=40_000_000)
     ap.add_argument("--cpu-sample-reads", type=int, default=40_000)
     return ap.parse_args()
@@ -368,6 +372,12 @@ def main():
     kernels = {kname: {"ms_per_step": round(ms / args.steps, 4), "launches_per_step": n // args.steps}
                for kname, (ms, n) in sorted(prof.items(), key=lambda kv: -kv[1][0])}
 
+    # location voting: measured on the last step's anchors, separately
+    # from the step (the §8(a) path ends at the anchors)
+    vote = None
+    if not args.no_vote:
+        vote = run_vote(god, torch, dreads, droffs, dref, droff, cfg, pattern, k, w, args, dist, dev)
+
     # e2e through the C ABI with pinned host buffers
     e2e = None
     if not args.no_e2e:
@@ -394,10 +404,48 @@ def main():
             "n_anchors_per_step": n_anchors,
             "roofline": roof, "kernels": kernels,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
+            "vote": vote,
         }
         print(json.dumps(out), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+def run_vote(god, torch, dreads, droffs, dref, droff, cfg, pattern, k, w, args, dist, dev):
+    """Location voting (god_vote_reads) on the anchors of one seeding pass: W warm-up + K timed calls,
+    CUDA events on the current stream, max over ranks.  HBM view: algorithmic bytes = every anchor
+    read once (16 B) + every voted location written once (40 B) + read offsets/phases."""
+    ix = god.god_build_index(dref, droff, pattern, k, w, cutoff=cfg.cutoff)
+    an, ao, ph = god.god_seed_reads(ix, dreads, droffs)
+    kw = dict(D=args.vote_D, V=args.vote_V, max_pairs=args.vote_max_pairs)
+    for _ in range(max(args.warmup, 1)):
+        v, vo = god.god_vote_reads(ix, dreads, droffs, ph, an, ao, **kw)
+    torch.cuda.synchronize()
+    god.profile_reset()
+    god.profile_enable(True)
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(args.steps):
+        v, vo = god.god_vote_reads(ix, dreads, droffs, ph, an, ao, **kw)
+    e.record()
+    torch.cuda.synchronize()
+    god.profile_enable(False)
+    prof = god.profile_query()
+    ms = max_over_ranks(s.elapsed_time(e) / args.steps, dist, dev)
+    vv = god.votes_numpy(v)
+    n = cfg.reads.n
+    n_an = int(an.shape[0])
+    kern = {kk: round(x[0] / args.steps, 4) for kk, x in sorted(prof.items(), key=lambda kv: -kv[1][0])}
+    peaks = json.load(open(PEAKS)) if os.path.exists(PEAKS) else {"hbm_gbs": 6650.0}
+    alg = 16 * n_an + 40 * int(vv.size) + 8 * 3 * (n + 1) + n
+    ix.free()
+    world = dist.get_world_size() if dist is not None and dist.is_initialized() else 1
+    return {"params": kw, "ms": round(ms, 3), "reads_per_s": round(world * n / (ms / 1e3), 1),
+            "anchors_per_s": round(world * n_an / (ms / 1e3), 1), "n_anchors": n_an, "n_locations": int(vv.size),
+            "rescued": int(vv["rescued"].sum()), "kernels_ms": kern,
+            "hbm_view": {"algorithmic_bytes": alg, "achieved_gbs": round(alg / (ms / 1e3) / 1e9, 1),
+                         "peak_gbs": float(peaks.get("hbm_gbs", 6650.0)),
+                         "frac": round(alg / (ms / 1e3) / 1e9 / float(peaks.get("hbm_gbs", 6650.0)), 4)}}
 
 
 def run_e2e(god, torch, cfg, pattern, k, w, n_anchors, steps, dist, world, dev):

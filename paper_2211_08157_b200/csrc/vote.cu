@@ -1,20 +1,24 @@
 // vote.cu — location voting (section 3.4; Fig. 8) with the rescue location
 // (P:398), on the anchors of god_seed_reads.  Readings V1-V6: DESIGN.md §2 / include/god.h.
 //
-// Per read, the anchors become 64-bit sort keys  strand << 63 | (diag + 2^32) << 29 | i
-// (i = the anchor's index in the read, so keys are unique and carry their payload; diag fits 34
-// bits: forward ref - read in (-2^32, 2^32), reverse ref + read_end in [0, 2^33)).  Sorting the keys
-// is step (2) ("a single sorted list of all adjusted matching locations"); equal (strand, diag)
-// groups are adjacent, so V2's "(hash, strand, diag) once" is a comparison of canonical k-mers
-// (equal canonical k-mer <=> equal hash: H_k is a bijection) inside a group — groups of more than
-// one anchor are rare (tandem repeats), and the canonical k-mer is re-read from the read bytes
-// only there.  The sweep (step (3)) follows the chain of cluster heads: the next Delta0 is the
-// first anchor beyond Delta0 + D.
+// Per read, every anchor becomes a unique 64-bit sort key
+//     strand << 63 | (diag + 2^32) << 29 | fp << ib | i
+// i = the anchor's index in the read (ib = max(5, ceil(log2 n)) bits: the key carries its payload);
+// fp = the top 29 - ib bits of a mix of the canonical k-mer of the anchor's read minimizer (equal
+// canonical k-mer <=> equal hash, H_k being a bijection); diag fits 34 bits (forward ref - read in
+// (-2^32, 2^32), reverse ref + read_end in [0, 2^33)).  Sorting the keys is step (2) ("a single
+// sorted list of all adjusted matching locations").  All anchors of a true location share one
+// (strand, diag), so V2's "(hash, strand, diag) once" must not compare every pair of the group: the
+// fingerprint orders each (strand, diag) group by hash, and only neighbours with equal
+// (strand, diag, fp) compare their exact canonical k-mers.  The canonical k-mer is read from the
+// read's bytes once per read minimizer (anchors of one minimizer share read_pos).  The sweep (step
+// (3)) follows the chain of cluster heads: the next Delta0 is the first anchor beyond Delta0 + D.
 //
-// Reads are bucketed by anchor count: <= 32 anchors -> one warp per read, keys in registers
-// (shuffle bitonic sort, ballots for the sweep); <= VOTE_MID anchors -> one CTA per read, keys in
-// shared memory; larger -> one CTA per read on global scratch.  Results go to per-read slots
-// (min(n, max_pairs) each), then a scan of the per-read counts and a compaction give the CSR output.
+// Reads are bucketed by anchor count n: n <= 32 -> one warp per read, everything in registers
+// (shuffle bitonic sort, ballots); n <= 256 -> one warp per read on a shared-memory slice;
+// n <= 2048 -> one CTA per read in shared memory; larger -> one CTA per read on global scratch.
+// Results go to per-read slots (min(n, max_pairs) each); a scan of the per-read counts and a
+// compaction give the CSR output.
 #include <algorithm>
 
 #include "internal.cuh"
@@ -22,11 +26,11 @@
 namespace god {
 namespace {
 
-constexpr int VOTE_IDX_BITS = 29;
-constexpr uint64_t VOTE_IDX_MASK = (1ull << VOTE_IDX_BITS) - 1;
-constexpr uint64_t DIAG_MASK = (1ull << 34) - 1;   // dk = key >> 29: strand at bit 34, biased diag below
+constexpr uint64_t DIAG_MASK = (1ull << 34) - 1;   // of dk = key >> 29: strand at bit 34, biased diag below
 constexpr int64_t DIAG_BIAS = 1ll << 32;
-constexpr uint32_t VOTE_MID = 2048;   // anchors per read kept in shared memory
+constexpr uint32_t VOTE_IDX_MAX = 1u << 29;        // anchors per read
+constexpr uint32_t VOTE_WSM = 256;                 // warp-per-read shared-memory path
+constexpr uint32_t VOTE_MID = 2048;                // CTA-per-read shared-memory path
 constexpr int VOTE_NT = 256;
 constexpr unsigned FULL = 0xffffffffu;
 
@@ -45,47 +49,79 @@ struct VoteArgs {
   uint32_t* bad;              // anchors inconsistent with the phases
 };
 
-__device__ __forceinline__ bool is_included(const Pattern& P, uint64_t pos, uint32_t a) {
-  return pos >= a && ((P.bits >> ((pos - a) % P.p)) & 1ull);
+// Read coordinates are < 2^32 (god.h limits): 32-bit pattern arithmetic, with the divisions by p
+// and x short-cut for the paper's patterns ('1': p = 1; '10': p = 2, x = 1).
+__device__ __forceinline__ uint32_t div_p(const Pattern& P, uint32_t d, uint32_t& rem) {
+  if (P.p == 1) { rem = 0; return d; }
+  if (P.p == 2) { rem = d & 1u; return d >> 1; }
+  rem = d % P.p;
+  return d / P.p;
+}
+__device__ __forceinline__ uint32_t div_x(const Pattern& P, uint32_t q, uint32_t& rem) {
+  if (P.x == 1) { rem = 0; return q; }
+  rem = q % P.x;
+  return q / P.x;
+}
+__device__ __forceinline__ bool is_included(const Pattern& P, uint32_t pos, uint32_t a) {
+  uint32_t rem;
+  div_p(P, pos - a, rem);
+  return pos >= a && ((P.bits >> rem) & 1ull);
 }
 // patterned index q of an included original position (inverse of orig_of)
-__device__ __forceinline__ uint64_t q_of(const Pattern& P, uint64_t pos, uint32_t a) {
-  const uint64_t d = pos - a;
-  return (d / P.p) * P.x + P.ones_before[d % P.p];
+__device__ __forceinline__ uint32_t q_of(const Pattern& P, uint32_t pos, uint32_t a) {
+  uint32_t rem;
+  const uint32_t blk = div_p(P, pos - a, rem);
+  return blk * P.x + P.ones_before[rem];
 }
-
-// V1: the sort key of one anchor.  Sets *bad if the anchor cannot come from this read and phase.
-__device__ __forceinline__ uint64_t vote_key(const VoteArgs& A, const god_anchor& an, uint32_t a, uint64_t L,
-                                             uint32_t i, bool& bad) {
-  const uint32_t z = an.strand & 1u;
-  if (!is_included(A.pat, an.read_pos, a) || an.read_pos >= L) bad = true;
-  int64_t diag;
-  if (z == 0) {
-    diag = (int64_t)an.ref_pos - (int64_t)an.read_pos;
-  } else {
-    const uint64_t end = orig_of(A.pat, q_of(A.pat, an.read_pos, a) + (uint64_t)A.k - 1, a);
-    if (end >= L) bad = true;
-    diag = (int64_t)an.ref_pos + (int64_t)end;
-  }
-  return ((uint64_t)z << 63) | ((uint64_t)(diag + DIAG_BIAS) << VOTE_IDX_BITS) | i;
+__device__ __forceinline__ uint32_t orig32(const Pattern& P, uint32_t q, uint32_t a) {
+  uint32_t rem;
+  const uint32_t blk = div_x(P, q, rem);
+  return a + blk * P.p + P.one[rem];
 }
 
 // canonical k-mer of the read's patterned k-mer starting at original position pos (phase a)
-__device__ uint64_t canon_at(const uint8_t* rd, uint64_t L, const Pattern& P, uint32_t a, int k, uint32_t pos) {
-  const uint64_t q = q_of(P, pos, a);
+__device__ uint64_t canon_at(const uint8_t* rd, uint32_t L, const Pattern& P, uint32_t a, int k, uint32_t pos) {
+  const uint32_t q = q_of(P, pos, a);
+  uint32_t rr;
+  uint32_t base = a + div_x(P, q, rr) * P.p;
   uint64_t fwd = 0, rev = 0;
   for (int i = 0; i < k; i++) {
-    const uint64_t o = orig_of(P, q + i, a);
-    const uint32_t c = o < L ? (base_code(rd[o]) & 3u) : 0u;
+    const uint32_t o = base + P.one[rr];
+    if (++rr == P.x) { rr = 0; base += P.p; }
+    const uint32_t c = o < L ? (base_code(__ldg(rd + o)) & 3u) : 0u;
     fwd = (fwd << 2) | c;
     rev |= (uint64_t)(3u - c) << (2 * i);
   }
   return fwd < rev ? fwd : rev;
 }
 
+__device__ __forceinline__ uint32_t idx_bits(uint32_t n) {
+  const uint32_t b = n <= 1 ? 0 : 32 - __clz(n - 1);
+  return b < 5 ? 5 : b;
+}
+
+// V1: the sort key of one anchor (fingerprint of its canonical k-mer in the bits below the diag).
+// Sets bad if the anchor cannot come from this read and phase.
+__device__ __forceinline__ uint64_t vote_key(const VoteArgs& A, const god_anchor& an, uint32_t a, uint32_t L,
+                                             uint64_t canon, uint32_t ib, uint32_t i, bool& bad) {
+  const uint32_t z = an.strand & 1u;
+  if (an.read_pos >= L || !is_included(A.pat, an.read_pos, a)) bad = true;
+  int64_t diag;
+  if (z == 0) {
+    diag = (int64_t)an.ref_pos - (int64_t)an.read_pos;
+  } else {
+    const uint32_t end = orig32(A.pat, q_of(A.pat, an.read_pos, a) + (uint32_t)A.k - 1, a);
+    if (end >= L) bad = true;
+    diag = (int64_t)an.ref_pos + (int64_t)end;
+  }
+  const uint32_t fb = 29 - ib;
+  const uint64_t fp = fb ? ((canon * 0x9E3779B97F4A7C15ull) >> (64 - fb)) : 0ull;
+  return ((uint64_t)z << 63) | ((uint64_t)(diag + DIAG_BIAS) << 29) | (fp << ib) | i;
+}
+
 __device__ __forceinline__ int64_t dk_diag(uint64_t dk) { return (int64_t)(dk & DIAG_MASK) - DIAG_BIAS; }
 
-// is anchor (dk) beyond the cluster head (dh): other strand, or diag - Delta0 > D
+// is anchor dk beyond the cluster head dh: other strand, or diag - Delta0 > D (dk >= dh: sorted)
 __device__ __forceinline__ bool beyond(uint64_t dk, uint64_t dh, uint64_t D) {
   return (dk >> 34) != (dh >> 34) || (dk & DIAG_MASK) - (dh & DIAG_MASK) > D;
 }
@@ -93,28 +129,6 @@ __device__ __forceinline__ bool beyond(uint64_t dk, uint64_t dh, uint64_t D) {
 // V4 order of two clusters: more votes first, then strand, then Delta0 (dk orders (strand, diag))
 __device__ __forceinline__ bool better(uint32_t va, uint64_t da, uint32_t vb, uint64_t db) {
   return va > vb || (va == vb && da < db);
-}
-
-// ------------------------------------------------------------------ bucketing + result slots
-__global__ void k_vote_classify(const uint64_t* __restrict__ aoff, uint32_t n_reads, uint32_t mp,
-                                uint64_t* __restrict__ slots, uint32_t* __restrict__ lists,
-                                uint32_t* __restrict__ nlist, uint64_t* __restrict__ big_off,
-                                uint64_t* __restrict__ big_total, uint32_t* __restrict__ bad) {
-  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n_reads; r += gridDim.x * blockDim.x) {
-    const uint64_t n = aoff[r + 1] - aoff[r];
-    slots[r] = n == 0 ? 0 : (mp && n > mp ? mp : n);
-    if (n == 0) continue;
-    if (n > VOTE_IDX_MASK) { atomicAdd(bad + 1, 1u); continue; }
-    if (n <= 32) {
-      lists[atomicAdd(nlist + 0, 1u)] = r;
-    } else if (n <= VOTE_MID) {
-      lists[n_reads + atomicAdd(nlist + 1, 1u)] = r;
-    } else {
-      const uint32_t j = atomicAdd(nlist + 2, 1u);
-      lists[2ull * n_reads + j] = r;
-      big_off[j] = atomicAdd((unsigned long long*)big_total, (unsigned long long)(n + 1));  // n + 1 heads
-    }
-  }
 }
 
 __device__ __forceinline__ void put_result(const VoteArgs& A, uint32_t r, uint32_t rank, uint64_t dh, uint32_t votes,
@@ -132,7 +146,40 @@ __device__ __forceinline__ void put_result(const VoteArgs& A, uint32_t r, uint32
   A.res[A.slot_off[r] + rank] = v;
 }
 
-// ------------------------------------------------------------------ <= 32 anchors: one warp per read
+// ------------------------------------------------------------------ bucketing + result slots
+__global__ void k_vote_classify(const uint64_t* __restrict__ aoff, uint32_t n_reads, uint32_t mp,
+                                uint64_t* __restrict__ slots, uint32_t* __restrict__ lists,
+                                uint32_t* __restrict__ nlist, uint64_t* __restrict__ big_off,
+                                uint64_t* __restrict__ big_total, uint32_t* __restrict__ bad) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t r0 = blockIdx.x * blockDim.x; r0 < n_reads; r0 += stride) {  // warp-uniform trip count
+    const uint32_t r = r0 + threadIdx.x;
+    uint64_t n = 0;
+    if (r < n_reads) {
+      n = aoff[r + 1] - aoff[r];
+      slots[r] = n == 0 ? 0 : (mp && n > mp ? mp : n);
+    }
+    if (n >= VOTE_IDX_MAX) { atomicAdd(bad + 1, 1u); n = 0; }
+    const int c = n == 0 ? -1 : n <= 32 ? 0 : n <= VOTE_WSM ? 1 : n <= VOTE_MID ? 2 : 3;
+#pragma unroll
+    for (int q = 0; q < 4; q++) {  // one atomic per warp and class
+      const uint32_t m = __ballot_sync(FULL, c == q);
+      if (!m) continue;
+      const int leader = __ffs(m) - 1;
+      uint32_t base = 0;
+      if (lane == leader) base = atomicAdd(nlist + q, (uint32_t)__popc(m));
+      base = __shfl_sync(FULL, base, leader);
+      if (c == q) {
+        const uint32_t j = base + __popc(m & ((1u << lane) - 1u));
+        lists[(uint64_t)q * n_reads + j] = r;
+        if (q == 3) big_off[j] = atomicAdd((unsigned long long*)big_total, (unsigned long long)(n + 2));
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ n <= 32: one warp per read, registers
 __global__ void __launch_bounds__(VOTE_NT) k_vote_warp(VoteArgs A, const uint32_t* __restrict__ list, uint32_t nlist) {
   const int lane = threadIdx.x & 31;
   const uint32_t wid = (uint32_t)((blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5);
@@ -140,16 +187,25 @@ __global__ void __launch_bounds__(VOTE_NT) k_vote_warp(VoteArgs A, const uint32_
   const uint32_t r = list[wid];
   const uint64_t a0 = A.aoff[r];
   const uint32_t n = (uint32_t)(A.aoff[r + 1] - a0);
-  const uint64_t rb = A.roff[r], L = A.roff[r + 1] - rb;
+  const uint64_t rb = A.roff[r];
+  const uint32_t L = (uint32_t)(A.roff[r + 1] - rb);
   const uint32_t ph = A.ph[r];
   const uint64_t D = A.D ? A.D : L;
+  const bool valid = lane < (int)n;
+  const uint32_t le = (lane == 31) ? FULL : ((2u << lane) - 1u);
+  god_anchor an = {0, 0, 0, 0};
+  if (valid) an = A.an[a0 + lane];
+  // canonical k-mer once per read minimizer (a run of equal read_pos), then broadcast
+  const uint32_t prev_rp = __shfl_up_sync(FULL, an.read_pos, 1);
+  const bool rhead = valid && (lane == 0 || prev_rp != an.read_pos);
+  uint64_t canon = 0;
+  if (rhead && an.read_pos < L && is_included(A.pat, an.read_pos, ph))
+    canon = canon_at(A.reads + rb, L, A.pat, ph, A.k, an.read_pos);
+  const uint32_t hm = __ballot_sync(FULL, rhead) & le;
+  canon = __shfl_sync(FULL, canon, hm ? 31 - __clz(hm) : 0);
   bool bad = false;
   uint64_t key = ~0ull;
-  god_anchor an = {0, 0, 0, 0};
-  if (lane < (int)n) {
-    an = A.an[a0 + lane];
-    key = vote_key(A, an, ph, L, (uint32_t)lane, bad);
-  }
+  if (valid) key = vote_key(A, an, ph, L, canon, 5, (uint32_t)lane, bad);
   if (__any_sync(FULL, bad)) {
     if (lane == 0) atomicAdd(A.bad, 1u);
     return;
@@ -165,20 +221,19 @@ __global__ void __launch_bounds__(VOTE_NT) k_vote_warp(VoteArgs A, const uint32_
       key = (lower == up) ? (key < o ? key : o) : (key > o ? key : o);
     }
   }
-  const bool valid = lane < (int)n;
   const int src = (int)(key & 31u);
   const uint32_t ref = __shfl_sync(FULL, an.ref_pos, src);
   const uint32_t qp = __shfl_sync(FULL, an.read_pos, src);
-  const uint64_t dk = key >> VOTE_IDX_BITS;
-  // V2: a repeat of (hash, strand, diag) is no new vote
-  const uint64_t dprev = __shfl_up_sync(FULL, dk, 1), dnext = __shfl_down_sync(FULL, dk, 1);
-  const bool grp = valid && ((lane > 0 && dprev == dk) || (lane + 1 < (int)n && dnext == dk));
-  bool dup = false;
-  if (__any_sync(FULL, grp)) {
-    const uint64_t c = grp ? canon_at(A.reads + rb, L, A.pat, ph, A.k, qp) : 0ull;
-    for (int j = 0; j < 31; j++) {
-      const uint64_t cj = __shfl_sync(FULL, c, j), dj = __shfl_sync(FULL, dk, j);
-      dup |= grp && j < lane && dj == dk && cj == c;
+  const uint64_t cn = __shfl_sync(FULL, canon, src);
+  const uint64_t dk = key >> 29;
+  // V2: a repeat of (hash, strand, diag) is no new vote: walk back over equal (strand, diag, fp)
+  bool dup = false, walking = valid;
+  for (int o = 1; __any_sync(FULL, walking); o++) {
+    const uint64_t ko = __shfl_up_sync(FULL, key, o);
+    const uint64_t co = __shfl_up_sync(FULL, cn, o);
+    if (walking) {
+      if (lane < o || (ko >> 5) != (key >> 5)) walking = false;
+      else if (co == cn) { dup = true; walking = false; }
     }
   }
   // step (3): the chain of cluster heads
@@ -189,7 +244,6 @@ __global__ void __launch_bounds__(VOTE_NT) k_vote_warp(VoteArgs A, const uint32_
     const uint32_t b = __ballot_sync(FULL, valid && lane > (int)s && beyond(dk, dh, D));
     s = b ? (uint32_t)(__ffs(b) - 1) : n;
   }
-  const uint32_t le = (lane == 31) ? FULL : ((2u << lane) - 1u);
   const int cid = __popc(starts & le) - 1;
   const uint32_t newmask = __ballot_sync(FULL, valid && !dup);
   // member spans: segmented suffix min/max (clusters are contiguous)
@@ -214,49 +268,113 @@ __global__ void __launch_bounds__(VOTE_NT) k_vote_warp(VoteArgs A, const uint32_
   // step (4) / rescue
   const uint32_t winmask = __ballot_sync(FULL, head && votes >= A.V);
   const bool rescue = winmask == 0;
-  const bool cand = rescue ? head : ((winmask >> lane) & 1u);
   const uint32_t candmask = rescue ? starts : winmask;
+  const bool cand = (candmask >> lane) & 1u;
   uint32_t rank = 0;
-  for (int j = 0; j < 32; j++) {
+  for (uint32_t m = candmask; m; m &= m - 1) {
+    const int j = __ffs(m) - 1;
     const uint32_t vj = __shfl_sync(FULL, votes, j);
     const uint64_t dj = __shfl_sync(FULL, dk, j);
-    rank += ((candmask >> j) & 1u) && j != lane && better(vj, dj, votes, dk);
+    rank += j != lane && better(vj, dj, votes, dk);
   }
   const uint32_t limit = rescue ? 1u : (A.mp ? A.mp : 32u);
   if (cand && rank < limit) put_result(A, r, rank, dk, votes, rescue ? 1u : 0u, rlo, rhi, qlo, qhi);
   if (lane == 0) A.cnt[r] = min((uint32_t)__popc(candmask), limit);
 }
 
-// ------------------------------------------------------------------ > 32 anchors: one CTA per read
-// Arrays (shared memory for <= VOTE_MID anchors, else global scratch): key[n]; flag[n] (1 = new
-// vote); per cluster: head index, votes and spans.
-struct CtaArrays {
+// ------------------------------------------------------------------ n > 32: a group of NT threads per read
+// NT = 32 (one warp, shared-memory slice) or VOTE_NT (one CTA, shared memory or global scratch).
+// Arrays of a read with n anchors: key[n], canon[n], aux[n] (read_pos, then new-vote flags),
+// chead[n + 1] (cluster heads), cv[n] (votes), crank[n] (output rank or ~0); ctr[4] (clusters,
+// winners, bad).
+struct GroupArrays {
   uint64_t* key;
-  uint32_t* flag;
+  uint64_t* canon;
+  uint32_t* aux;
   uint32_t* chead;
-  uint32_t* cvotes;
+  uint32_t* cv;
   uint32_t* crank;
+  uint32_t* ctr;
 };
 
-__device__ void vote_cta(const VoteArgs& A, uint32_t r, const CtaArrays& S) {
-  __shared__ uint32_t s_nclust, s_nwin, s_bad;
-  const int tid = threadIdx.x;
+template <int NT>
+__device__ __forceinline__ void gsync() {
+  if (NT == 32) __syncwarp();
+  else __syncthreads();
+}
+
+// Exclusive scan of two 0/1 flag arrays over [0, n) by a group of NT threads (chunks of NT):
+// fa -> heads (compacted indices of the set flags into `out`, count returned via *total_a),
+// fb -> exclusive prefix written over fb (total via *total_b).
+template <int NT>
+__device__ void group_scan_flags(uint32_t n, const uint32_t* fa, uint32_t* out, uint32_t* fb, uint32_t* ws,
+                                 uint32_t* total_a, uint32_t* total_b, int t) {
+  const int lane = t & 31, warp = t >> 5;
+  constexpr int NW = NT / 32;
+  uint32_t base_a = 0, base_b = 0;
+  for (uint32_t c0 = 0; c0 < n; c0 += NT) {
+    const uint32_t i = c0 + t;
+    const uint32_t a = i < n ? fa[i] : 0u, b = i < n ? fb[i] : 0u;
+    const uint32_t ba = __ballot_sync(FULL, a), bb = __ballot_sync(FULL, b);
+    const uint32_t lt = (1u << lane) - 1u;
+    uint32_t pa = __popc(ba & lt), pb = __popc(bb & lt);
+    uint32_t wa = 0, wb = 0, ta = __popc(ba), tb = __popc(bb);
+    if (NW > 1) {
+      if (lane == 0) { ws[warp] = ta; ws[NW + warp] = tb; }
+      __syncthreads();
+      ta = 0; tb = 0;
+      for (int q = 0; q < NW; q++) {
+        const uint32_t xa = ws[q], xb = ws[NW + q];
+        if (q < warp) { wa += xa; wb += xb; }
+        ta += xa; tb += xb;
+      }
+      __syncthreads();
+    }
+    if (a) out[base_a + wa + pa] = i;
+    if (i < n) fb[i] = base_b + wb + pb;
+    base_a += ta;
+    base_b += tb;
+  }
+  if (t == 0) { *total_a = base_a; *total_b = base_b; }
+}
+
+template <int NT>
+__device__ void vote_group(const VoteArgs& A, uint32_t r, const GroupArrays& S, uint32_t* ws, int t) {
+  const int lane = t & 31, warp = t >> 5;
+  constexpr int NW = NT / 32;
   const uint64_t a0 = A.aoff[r];
   const uint32_t n = (uint32_t)(A.aoff[r + 1] - a0);
-  const uint64_t rb = A.roff[r], L = A.roff[r + 1] - rb;
+  const uint64_t rb = A.roff[r];
+  const uint32_t L = (uint32_t)(A.roff[r + 1] - rb);
   const uint32_t ph = A.ph[r];
   const uint64_t D = A.D ? A.D : L;
-  if (tid == 0) { s_bad = 0; s_nclust = 0; s_nwin = 0; }
-  __syncthreads();
-  bool bad = false;
-  for (uint32_t i = tid; i < n; i += VOTE_NT) {
-    const god_anchor an = A.an[a0 + i];
-    S.key[i] = vote_key(A, an, ph, L, i, bad);
+  const uint32_t ib = idx_bits(n);
+  const uint64_t imask = (1ull << ib) - 1;
+  if (t == 0) { S.ctr[0] = 0; S.ctr[1] = 0; S.ctr[2] = 0; S.ctr[3] = 0; }
+  for (uint32_t i = t; i < n; i += NT) S.aux[i] = __ldg(&A.an[a0 + i].read_pos);
+  gsync<NT>();
+  // canonical k-mer once per read minimizer (heads of runs of equal read_pos)
+  for (uint32_t i = t; i < n; i += NT) {
+    const uint32_t rp = S.aux[i];
+    if ((i == 0 || S.aux[i - 1] != rp) && rp < L && is_included(A.pat, rp, ph))
+      S.canon[i] = canon_at(A.reads + rb, L, A.pat, ph, A.k, rp);
   }
-  if (bad) s_bad = 1;
-  __syncthreads();
-  if (s_bad) {
-    if (tid == 0) atomicAdd(A.bad, 1u);
+  gsync<NT>();
+  // keys; a non-head takes its head's canonical k-mer (heads are not written in this phase)
+  bool bad = false;
+  for (uint32_t i = t; i < n; i += NT) {
+    const god_anchor an = A.an[a0 + i];
+    uint32_t j = i;
+    while (j > 0 && S.aux[j - 1] == an.read_pos) --j;
+    uint64_t c = 0;
+    if (an.read_pos < L && is_included(A.pat, an.read_pos, ph)) c = S.canon[j];
+    if (j != i) S.canon[i] = c;
+    S.key[i] = vote_key(A, an, ph, L, c, ib, i, bad);
+  }
+  if (bad) S.ctr[2] = 1;
+  gsync<NT>();
+  if (S.ctr[2]) {
+    if (t == 0) atomicAdd(A.bad, 1u);
     return;
   }
   // step (2): bitonic sort, all comparators ascending (mirror first step), virtual +inf past n
@@ -264,114 +382,184 @@ __device__ void vote_cta(const VoteArgs& A, uint32_t r, const CtaArrays& S) {
   while (N2 < n) N2 <<= 1;
   for (uint32_t size = 2; size <= N2; size <<= 1) {
     const uint32_t half = size >> 1;
-    for (uint32_t t = tid; t < N2 / 2; t += VOTE_NT) {
-      const uint32_t blk = t / half, off = t % half;
+    for (uint32_t q = t; q < N2 / 2; q += NT) {
+      const uint32_t blk = q / half, off = q % half;
       const uint32_t i = blk * size + off, j = blk * size + size - 1 - off;
       if (j < n) {
         const uint64_t x = S.key[i], y = S.key[j];
         if (y < x) { S.key[i] = y; S.key[j] = x; }
       }
     }
-    __syncthreads();
+    gsync<NT>();
     for (uint32_t stride = half >> 1; stride > 0; stride >>= 1) {
-      for (uint32_t t = tid; t < N2 / 2; t += VOTE_NT) {
-        const uint32_t i = (t / stride) * 2 * stride + (t % stride), j = i + stride;
+      for (uint32_t q = t; q < N2 / 2; q += NT) {
+        const uint32_t i = (q / stride) * 2 * stride + (q % stride), j = i + stride;
         if (j < n) {
           const uint64_t x = S.key[i], y = S.key[j];
           if (y < x) { S.key[i] = y; S.key[j] = x; }
         }
       }
-      __syncthreads();
+      gsync<NT>();
     }
   }
-  // V2: new-vote flags
-  for (uint32_t i = tid; i < n; i += VOTE_NT) {
-    const uint64_t dk = S.key[i] >> VOTE_IDX_BITS;
+  // V2 new-vote flags (aux): walk back over equal (strand, diag, fp); clear the head flags (crank)
+  for (uint32_t i = t; i < n; i += NT) {
+    const uint64_t ki = S.key[i] >> ib;
+    const uint64_t ci = S.canon[S.key[i] & imask];
     uint32_t fresh = 1;
-    if (i > 0 && (S.key[i - 1] >> VOTE_IDX_BITS) == dk) {
-      const uint32_t qi = A.an[a0 + (S.key[i] & VOTE_IDX_MASK)].read_pos;
-      const uint64_t ci = canon_at(A.reads + rb, L, A.pat, ph, A.k, qi);
-      for (uint32_t j = i; j-- > 0 && (S.key[j] >> VOTE_IDX_BITS) == dk;) {
-        const uint32_t qj = A.an[a0 + (S.key[j] & VOTE_IDX_MASK)].read_pos;
-        if (canon_at(A.reads + rb, L, A.pat, ph, A.k, qj) == ci) { fresh = 0; break; }
+    for (uint32_t j = i; j-- > 0 && (S.key[j] >> ib) == ki;)
+      if (S.canon[S.key[j] & imask] == ci) { fresh = 0; break; }
+    S.aux[i] = fresh;
+    S.crank[i] = 0;
+  }
+  gsync<NT>();
+  // step (3): cluster heads.  A gap > D (or a strand change) between sorted neighbours always starts
+  // a cluster; inside a gap-free segment the chain Delta0 -> first anchor beyond Delta0 + D is
+  // walked by the segment's first thread.
+  for (uint32_t i = t; i < n; i += NT) {
+    if (i > 0 && !beyond(S.key[i] >> 29, S.key[i - 1] >> 29, D)) continue;
+    uint32_t s = i;
+    while (true) {
+      S.crank[s] = 1;
+      const uint64_t dh = S.key[s] >> 29;
+      // first e > s beyond Delta0: gallop, then binary search
+      uint32_t e = s + 1;
+      if (e < n && !beyond(S.key[e] >> 29, dh, D)) {
+        uint32_t lo = e, step = 1;  // key[lo] not beyond
+        while (lo + step < n && !beyond(S.key[lo + step] >> 29, dh, D)) { lo += step; step <<= 1; }
+        uint32_t hi = min(lo + step, n);  // beyond at hi, or hi == n
+        while (hi - lo > 1) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (beyond(S.key[mid] >> 29, dh, D)) hi = mid;
+          else lo = mid;
+        }
+        e = hi;
       }
+      if (e >= n || beyond(S.key[e] >> 29, S.key[e - 1] >> 29, D)) break;  // segment ends: its own walker
+      s = e;
     }
-    S.flag[i] = fresh;
   }
-  // step (3): the chain of cluster heads (one thread; binary search for the first anchor beyond D)
-  if (tid == 0) {
-    uint32_t c = 0;
-    for (uint32_t s = 0; s < n;) {
-      S.chead[c++] = s;
-      const uint64_t dh = S.key[s] >> VOTE_IDX_BITS;
-      uint32_t lo = s + 1, hi = n;
-      while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (beyond(S.key[mid] >> VOTE_IDX_BITS, dh, D)) hi = mid;
-        else lo = mid + 1;
+  gsync<NT>();
+  // heads -> chead[0..C), new-vote flags -> exclusive prefix (votes of a cluster = a difference)
+  group_scan_flags<NT>(n, S.crank, S.chead, S.aux, ws, &S.ctr[0], &S.ctr[3], t);
+  gsync<NT>();
+  const uint32_t C = S.ctr[0], nfresh = S.ctr[3];
+  if (t == 0) S.chead[C] = n;
+  gsync<NT>();
+  for (uint32_t c = t; c < C; c += NT) {
+    const uint32_t e = S.chead[c + 1];
+    const uint32_t v = (e < n ? S.aux[e] : nfresh) - S.aux[S.chead[c]];
+    S.cv[c] = v;
+    if (v >= A.V) S.crank[atomicAdd(&S.ctr[1], 1u)] = c;  // winner list (order irrelevant: ranked below)
+  }
+  gsync<NT>();
+  const uint32_t W = S.ctr[1];
+  const bool rescue = W == 0;
+  const uint32_t limit = rescue ? 1u : (A.mp ? min(A.mp, W) : W);
+  if (!rescue) {
+    // step (4): rank the winners; aux[rank] = cluster for rank < limit
+    for (uint32_t w = t; w < W; w += NT) {
+      const uint32_t c = S.crank[w], v = S.cv[c];
+      const uint64_t dc = S.key[S.chead[c]] >> 29;
+      uint32_t rank = 0;
+      for (uint32_t j = 0; j < W && rank < limit; j++) {
+        const uint32_t cj = S.crank[j];
+        rank += cj != c && better(S.cv[cj], S.key[S.chead[cj]] >> 29, v, dc);
       }
-      s = lo;
+      if (rank < limit) S.aux[rank] = c;
     }
-    S.chead[c] = n;
-    s_nclust = c;
-  }
-  __syncthreads();
-  const uint32_t C = s_nclust;
-  uint32_t wins = 0;
-  for (uint32_t c = tid; c < C; c += VOTE_NT) {
-    uint32_t v = 0;
-    for (uint32_t i = S.chead[c]; i < S.chead[c + 1]; i++) v += S.flag[i];
-    S.cvotes[c] = v;
-    wins += v >= A.V;
-  }
-  atomicAdd(&s_nwin, wins);
-  __syncthreads();
-  const bool rescue = s_nwin == 0;
-  const uint32_t limit = rescue ? 1u : (A.mp ? A.mp : 0xffffffffu);
-  for (uint32_t c = tid; c < C; c += VOTE_NT) {
-    const uint32_t v = S.cvotes[c];
-    if (!rescue && v < A.V) continue;
-    const uint64_t dc = S.key[S.chead[c]] >> VOTE_IDX_BITS;
-    uint32_t rank = 0;
-    for (uint32_t j = 0; j < C && rank < limit; j++) {
-      const uint32_t vj = S.cvotes[j];
-      if (j == c || (!rescue && vj < A.V)) continue;
-      rank += better(vj, S.key[S.chead[j]] >> VOTE_IDX_BITS, v, dc);
+  } else {
+    // rescue: the best cluster
+    uint32_t bc = 0xffffffffu, bv = 0;
+    uint64_t bd = ~0ull;
+    for (uint32_t c = t; c < C; c += NT) {
+      const uint32_t v = S.cv[c];
+      const uint64_t d = S.key[S.chead[c]] >> 29;
+      if (bc == 0xffffffffu || better(v, d, bv, bd)) { bc = c; bv = v; bd = d; }
     }
-    if (rank >= limit) continue;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const uint32_t oc = __shfl_xor_sync(FULL, bc, o), ov = __shfl_xor_sync(FULL, bv, o);
+      const uint64_t od = __shfl_xor_sync(FULL, bd, o);
+      if (oc != 0xffffffffu && (bc == 0xffffffffu || better(ov, od, bv, bd))) { bc = oc; bv = ov; bd = od; }
+    }
+    if (NW > 1) {
+      if (lane == 0) ws[warp] = bc;
+      __syncthreads();
+      if (t == 0) {
+        uint32_t best = ws[0];
+        for (int q = 1; q < NW; q++) {
+          const uint32_t c = ws[q];
+          if (c == 0xffffffffu) continue;
+          if (best == 0xffffffffu ||
+              better(S.cv[c], S.key[S.chead[c]] >> 29, S.cv[best], S.key[S.chead[best]] >> 29))
+            best = c;
+        }
+        S.aux[0] = best;
+      }
+    } else if (t == 0) {
+      S.aux[0] = bc;
+    }
+  }
+  gsync<NT>();
+  // spans of the output clusters: one warp per cluster
+  for (uint32_t rank = warp; rank < limit; rank += NW) {
+    const uint32_t c = S.aux[rank];
     uint32_t rlo = 0xffffffffu, rhi = 0, qlo = 0xffffffffu, qhi = 0;
-    for (uint32_t i = S.chead[c]; i < S.chead[c + 1]; i++) {
-      const god_anchor an = A.an[a0 + (S.key[i] & VOTE_IDX_MASK)];
+    for (uint32_t i = S.chead[c] + lane; i < S.chead[c + 1]; i += 32) {
+      const god_anchor an = A.an[a0 + (S.key[i] & imask)];
       rlo = min(rlo, an.ref_pos); rhi = max(rhi, an.ref_pos);
       qlo = min(qlo, an.read_pos); qhi = max(qhi, an.read_pos);
     }
-    put_result(A, r, rank, dc, v, rescue ? 1u : 0u, rlo, rhi, qlo, qhi);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      rlo = min(rlo, __shfl_xor_sync(FULL, rlo, o)); rhi = max(rhi, __shfl_xor_sync(FULL, rhi, o));
+      qlo = min(qlo, __shfl_xor_sync(FULL, qlo, o)); qhi = max(qhi, __shfl_xor_sync(FULL, qhi, o));
+    }
+    if (lane == 0) put_result(A, r, rank, S.key[S.chead[c]] >> 29, S.cv[c], rescue ? 1u : 0u, rlo, rhi, qlo, qhi);
   }
-  if (tid == 0) A.cnt[r] = rescue ? 1u : min(s_nwin, limit);
+  if (t == 0) A.cnt[r] = limit;
 }
 
+__device__ __forceinline__ GroupArrays carve(unsigned char* base, uint32_t cap, uint32_t* ctr) {
+  GroupArrays S;
+  S.key = reinterpret_cast<uint64_t*>(base);
+  S.canon = S.key + cap;
+  S.aux = reinterpret_cast<uint32_t*>(S.canon + cap);
+  S.chead = S.aux + cap;
+  S.cv = S.chead + cap + 1;
+  S.crank = S.cv + cap;
+  S.ctr = ctr;
+  return S;
+}
+__host__ __device__ constexpr size_t group_bytes(uint32_t cap) { return (size_t)cap * 32 + 8; }
+
+// 32 < n <= VOTE_WSM: one warp per read, 8 warps per CTA, a shared-memory slice each
+__global__ void __launch_bounds__(VOTE_NT) k_vote_wsm(VoteArgs A, const uint32_t* __restrict__ list, uint32_t nlist) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ uint32_t ctr[VOTE_NT / 32][4];
+  const int warp = threadIdx.x >> 5;
+  const uint32_t wid = blockIdx.x * (VOTE_NT / 32) + warp;
+  if (wid >= nlist) return;  // warp-uniform
+  const GroupArrays S = carve(smem + warp * group_bytes(VOTE_WSM), VOTE_WSM, ctr[warp]);
+  vote_group<32>(A, list[wid], S, nullptr, threadIdx.x & 31);
+}
+
+// VOTE_WSM < n <= VOTE_MID: one CTA per read in shared memory
 __global__ void __launch_bounds__(VOTE_NT) k_vote_mid(VoteArgs A, const uint32_t* __restrict__ list) {
   extern __shared__ __align__(16) unsigned char smem[];
-  CtaArrays S;
-  S.key = reinterpret_cast<uint64_t*>(smem);
-  S.flag = reinterpret_cast<uint32_t*>(S.key + VOTE_MID);
-  S.chead = S.flag + VOTE_MID;
-  S.cvotes = S.chead + VOTE_MID + 1;
-  S.crank = nullptr;
-  vote_cta(A, list[blockIdx.x], S);
+  __shared__ uint32_t ctr[4], ws[2 * (VOTE_NT / 32)];
+  vote_group<VOTE_NT>(A, list[blockIdx.x], carve(smem, VOTE_MID, ctr), ws, threadIdx.x);
 }
 
+// n > VOTE_MID: one CTA per read on global scratch (32 (n + 2) bytes per read >= group_bytes(n + 1))
 __global__ void __launch_bounds__(VOTE_NT) k_vote_big(VoteArgs A, const uint32_t* __restrict__ list,
-                                                      const uint64_t* __restrict__ big_off, uint64_t* gkey,
-                                                      uint32_t* gflag, uint32_t* ghead, uint32_t* gvotes) {
-  const uint64_t o = big_off[blockIdx.x];
-  CtaArrays S;
-  S.key = gkey + o;
-  S.flag = gflag + o;
-  S.chead = ghead + o;
-  S.cvotes = gvotes + o;
-  S.crank = nullptr;
-  vote_cta(A, list[blockIdx.x], S);
+                                                      const uint64_t* __restrict__ big_off, unsigned char* scratch) {
+  __shared__ uint32_t ctr[4], ws[2 * (VOTE_NT / 32)];
+  const uint32_t r = list[blockIdx.x];
+  const uint32_t n = (uint32_t)(A.aoff[r + 1] - A.aoff[r]);
+  const uint64_t o = big_off[blockIdx.x];  // sum of (n + 2) of the big reads placed before
+  vote_group<VOTE_NT>(A, r, carve(scratch + o * 32, n + 1, ctr), ws, threadIdx.x);
 }
 
 // ------------------------------------------------------------------ compaction into the CSR output
@@ -393,8 +581,8 @@ uint64_t vote_reads(const god_index* ix, const uint8_t* reads, const uint64_t* r
                     god_vote* out, uint64_t* out_off, uint64_t cap, cudaStream_t st) {
   Scratch scr(st);
   uint64_t* slot_off = scr.alloc<uint64_t>((size_t)n_reads + 1);
-  uint32_t* lists = scr.alloc<uint32_t>(3ull * n_reads + 1);
-  uint32_t* ctr = scr.alloc<uint32_t>(8);        // nlist[3], bad[2]
+  uint32_t* lists = scr.alloc<uint32_t>(4ull * n_reads + 1);
+  uint32_t* ctr = scr.alloc<uint32_t>(8);        // nlist[4], bad[2]
   uint64_t* big_total = scr.alloc<uint64_t>(1);
   uint64_t* big_off = scr.alloc<uint64_t>((size_t)n_reads + 1);
   uint32_t* cnt = scr.alloc<uint32_t>((size_t)n_reads + 1);
@@ -405,7 +593,7 @@ uint64_t vote_reads(const god_index* ix, const uint8_t* reads, const uint64_t* r
   const int nsm = num_sms();
   if (n_reads)
     GOD_LAUNCH("k_vote_classify", k_vote_classify, std::min<unsigned>(grid_for(n_reads, 256), nsm * 8u), 256, 0, st,
-               aoff, n_reads, vp.max_pairs, slot_off, lists, ctr, big_off, big_total, ctr + 3);
+               aoff, n_reads, vp.max_pairs, slot_off, lists, ctr, big_off, big_total, ctr + 4);
   scan_exclusive_u64(slot_off, slot_off, (uint64_t)n_reads + 1, nullptr, st, scr, "scan_vote_slots");
   uint32_t h[8];
   GOD_CUDA(cudaMemcpyAsync(h, ctr, sizeof(h), cudaMemcpyDeviceToHost, st));
@@ -413,7 +601,7 @@ uint64_t vote_reads(const god_index* ix, const uint8_t* reads, const uint64_t* r
   GOD_CUDA(cudaMemcpyAsync(&hb[0], slot_off + n_reads, 8, cudaMemcpyDeviceToHost, st));
   GOD_CUDA(cudaMemcpyAsync(&hb[1], big_total, 8, cudaMemcpyDeviceToHost, st));
   GOD_CUDA(cudaStreamSynchronize(st));
-  GOD_REQUIRE(h[4] == 0, "a read has >= 2^29 anchors");
+  GOD_REQUIRE(h[5] == 0, "a read has >= 2^29 anchors");
   god_vote* res = scr.alloc<god_vote>(hb[0] ? hb[0] : 1);
   VoteArgs A;
   A.reads = reads;
@@ -429,30 +617,26 @@ uint64_t vote_reads(const god_index* ix, const uint8_t* reads, const uint64_t* r
   A.slot_off = slot_off;
   A.res = res;
   A.cnt = cnt;
-  A.bad = ctr + 3;
-  if (h[0]) GOD_LAUNCH("k_vote_warp", k_vote_warp, grid_for((uint64_t)h[0] * 32, VOTE_NT), VOTE_NT, 0, st, A, lists, h[0]);
-  if (h[1]) {
-    const size_t sm = VOTE_MID * sizeof(uint64_t) + (3 * VOTE_MID + 1) * sizeof(uint32_t);
-    static bool attr = false;
-    if (!attr) {
-      GOD_CUDA(cudaFuncSetAttribute(k_vote_mid, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-      attr = true;
-    }
-    GOD_LAUNCH("k_vote_mid", k_vote_mid, h[1], VOTE_NT, sm, st, A, lists + n_reads);
+  A.bad = ctr + 4;
+  static bool attr = false;
+  const size_t sm_wsm = (VOTE_NT / 32) * group_bytes(VOTE_WSM), sm_mid = group_bytes(VOTE_MID);
+  if (!attr) {
+    GOD_CUDA(cudaFuncSetAttribute(k_vote_wsm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_wsm));
+    GOD_CUDA(cudaFuncSetAttribute(k_vote_mid, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_mid));
+    attr = true;
   }
-  if (h[2]) {
-    const uint64_t tb = hb[1];
-    uint64_t* gkey = scr.alloc<uint64_t>(tb);
-    uint32_t* gflag = scr.alloc<uint32_t>(tb);
-    uint32_t* ghead = scr.alloc<uint32_t>(tb);
-    uint32_t* gvotes = scr.alloc<uint32_t>(tb);
-    GOD_LAUNCH("k_vote_big", k_vote_big, h[2], VOTE_NT, 0, st, A, lists + 2ull * n_reads, big_off, gkey, gflag,
-               ghead, gvotes);
+  if (h[0]) GOD_LAUNCH("k_vote_warp", k_vote_warp, grid_for((uint64_t)h[0] * 32, VOTE_NT), VOTE_NT, 0, st, A, lists, h[0]);
+  if (h[1])
+    GOD_LAUNCH("k_vote_wsm", k_vote_wsm, grid_for(h[1], VOTE_NT / 32), VOTE_NT, sm_wsm, st, A, lists + n_reads, h[1]);
+  if (h[2]) GOD_LAUNCH("k_vote_mid", k_vote_mid, h[2], VOTE_NT, sm_mid, st, A, lists + 2ull * n_reads);
+  if (h[3]) {
+    unsigned char* gs = scr.alloc<unsigned char>(hb[1] * 32 + 64);
+    GOD_LAUNCH("k_vote_big", k_vote_big, h[3], VOTE_NT, 0, st, A, lists + 3ull * n_reads, big_off, gs);
   }
   scan_exclusive_u32_to_u64(cnt, out_off, (uint64_t)n_reads + 1, nullptr, st, scr, "scan_vote_out");
   uint32_t nbad = 0;
   uint64_t tot = 0;
-  GOD_CUDA(cudaMemcpyAsync(&nbad, ctr + 3, 4, cudaMemcpyDeviceToHost, st));
+  GOD_CUDA(cudaMemcpyAsync(&nbad, ctr + 4, 4, cudaMemcpyDeviceToHost, st));
   GOD_CUDA(cudaMemcpyAsync(&tot, out_off + n_reads, 8, cudaMemcpyDeviceToHost, st));
   GOD_CUDA(cudaStreamSynchronize(st));
   GOD_REQUIRE(nbad == 0, "anchors inconsistent with the reads' phases (read_pos not an included position)");
