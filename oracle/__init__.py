@@ -68,6 +68,9 @@ def _load():
     L.or_vote_read.argtypes = [vp, vp, u64, u32, u32, u32, u32, u32, vp, u64]; L.or_vote_read.restype = ctypes.c_int64
     L.or_vote_reads_batch.argtypes = [vp, vp, vp, u32, vp, u32, u32, u32, vp, u64, vp]
     L.or_vote_reads_batch.restype = ctypes.c_int64
+    L.or_contain.argtypes = [vp, vp, u32, ctypes.c_char_p, i32, i32, u32, u32, ctypes.c_int64, vp, vp, u32, u32, u32,
+                             u32, u32, u64, u32, u32, u32, vp, vp, vp]
+    L.or_contain.restype = i32
     _lib = L
     return L
 
@@ -170,6 +173,23 @@ def vote_hits(hits, D: int, V: int = 3, max_pairs: int = 0, read_id: int = 0) ->
     h2 = h.copy()
     L.or_vote_hits(_p(h2), h2.size, D, V, max_pairs, read_id, _p(out), n)
     return out
+
+
+def contain(refs, ref_offsets, reads, read_offsets, pattern: str, k: int, w: int, cutoff=(1, 5000),
+            max_occ: int = -1, t: int = 16, D: int = 0, V: int = 3, max_pairs: int = 0, batch_bases: int = 0,
+            min_reads: int = 1, cov=(1, 1)):
+    """Containment search (readings C1-C4).  -> (mapped_reads u64[n], mapped_bases u64[n], accepted u8[n])"""
+    refs, reads = _u8(refs), _u8(reads)
+    ro = np.ascontiguousarray(ref_offsets, dtype=np.uint64)
+    qo = np.ascontiguousarray(read_offsets, dtype=np.uint64)
+    n = ro.size - 1
+    mr, mb, acc = np.zeros(n, np.uint64), np.zeros(n, np.uint64), np.zeros(n, np.uint8)
+    rc = _load().or_contain(_p(refs), _p(ro), n, pattern.encode(), k, w, cutoff[0], cutoff[1], max_occ, _p(reads),
+                            _p(qo), qo.size - 1, t, D, V, max_pairs, batch_bases, min_reads, cov[0], cov[1],
+                            _p(mr), _p(mb), _p(acc))
+    if rc:
+        raise ValueError("invalid containment parameters")
+    return mr, mb, acc
 
 
 class Index:

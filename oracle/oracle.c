@@ -527,3 +527,72 @@ int64_t or_vote_reads_batch(const or_index* ix, const uint8_t* reads, const uint
     if (vote_offsets) vote_offsets[n] = tot;
     return tot > cap && out ? -1 : (int64_t)tot;
 }
+
+/* ------------------------------------------------------------------------------------------ */
+/* Containment search at desk scale (SPEC contain module).  Readings
+ * (C1-C4):
+ *  C1 the references are processed in batches of consecutive sequences of at most batch_bases
+ *     bases ("-I", "limit the loaded number of bases at once"; a longer sequence is a batch
+ *     of its own; 0 = one batch); each batch's index is built on the fly, with the cutoff
+ *     computed within the batch.
+ *  C2 every read is phase-selected (O8), seeded (O9) and voted (V1-V6) against each batch's index;
+ *     "mapped read ... the read that receives a mapping location using the location voting step"
+ *     (P:184): a read maps to reference t if one of its voted locations (winning or rescue) has
+ *     its ref_lo inside t.
+ *  C3 per reference: mapped_reads = number of distinct reads mapped to it; mapped_bases = the sum
+ *     of their lengths; genome coverage = mapped_bases / len(t) (read depth; "a genome
+ *     coverage of at least 1").
+ *  C4 accepted iff mapped_reads >= min_reads and mapped_bases * cov_den >= cov_num * len(t)
+ *     (100,000 reads and coverage 1 at RefSeq scale; both are parameters here). */
+int or_contain(const uint8_t* refs, const uint64_t* ref_offsets, uint32_t n_refs, const char* pattern, int k, int w,
+               uint32_t frac_num, uint32_t frac_den, int64_t max_occ, const uint8_t* reads,
+               const uint64_t* read_offsets, uint32_t n_reads, uint32_t t, uint32_t D, uint32_t V,
+               uint32_t max_pairs, uint64_t batch_bases, uint32_t min_reads, uint32_t cov_num, uint32_t cov_den,
+               uint64_t* mapped_reads, uint64_t* mapped_bases, uint8_t* accepted) {
+    for (uint32_t i = 0; i < n_refs; i++) { mapped_reads[i] = 0; mapped_bases[i] = 0; }
+    uint32_t b0 = 0;
+    while (b0 < n_refs) {
+        /* C1: the batch [b0, b1) */
+        uint32_t b1 = b0 + 1;
+        while (b1 < n_refs && batch_bases && ref_offsets[b1 + 1] - ref_offsets[b0] <= batch_bases) b1++;
+        if (!batch_bases) b1 = n_refs;
+        uint32_t nb = b1 - b0;
+        uint64_t* off = (uint64_t*)malloc(sizeof(uint64_t) * (nb + 1));
+        for (uint32_t i = 0; i <= nb; i++) off[i] = ref_offsets[b0 + i] - ref_offsets[b0];
+        or_index* ix = or_build_index(refs + ref_offsets[b0], off, nb, pattern, k, w, frac_num, frac_den, max_occ);
+        if (!ix) { free(off); return -1; }
+        /* C2 */
+        for (uint32_t r = 0; r < n_reads; r++) {
+            const uint8_t* q = reads + read_offsets[r];
+            uint64_t L = read_offsets[r + 1] - read_offsets[r];
+            uint32_t a = (uint32_t)or_select_phase(ix, q, L, t, NULL);
+            int64_t nv = or_vote_read(ix, q, L, a, r, D, V, max_pairs, NULL, 0);
+            if (nv <= 0) continue;
+            or_vote* v = (or_vote*)malloc(sizeof(or_vote) * (size_t)nv);
+            or_vote_read(ix, q, L, a, r, D, V, max_pairs, v, (uint64_t)nv);
+            uint32_t* hit = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)nv);
+            int64_t nh = 0;
+            for (int64_t j = 0; j < nv; j++) {
+                uint32_t ti = 0;                     /* the batch sequence containing ref_lo */
+                while (ti + 1 < nb && off[ti + 1] <= v[j].ref_lo) ti++;
+                int seen = 0;
+                for (int64_t u = 0; u < nh; u++) if (hit[u] == ti) seen = 1;
+                if (!seen) hit[nh++] = ti;
+            }
+            for (int64_t u = 0; u < nh; u++) {    /* C3 */
+                mapped_reads[b0 + hit[u]] += 1;
+                mapped_bases[b0 + hit[u]] += L;
+            }
+            free(v); free(hit);
+        }
+        or_index_free(ix);
+        free(off);
+        b0 = b1;
+    }
+    for (uint32_t i = 0; i < n_refs; i++) {       /* C4 */
+        unsigned __int128 lhs = (unsigned __int128)mapped_bases[i] * cov_den;
+        unsigned __int128 rhs = (unsigned __int128)cov_num * (ref_offsets[i + 1] - ref_offsets[i]);
+        accepted[i] = (uint8_t)(mapped_reads[i] >= min_reads && lhs >= rhs);
+    }
+    return 0;
+}

@@ -110,6 +110,15 @@ int64_t or_vote_reads_batch(const or_index* ix, const uint8_t* reads, const uint
                             const uint8_t* phases, uint32_t D, uint32_t V, uint32_t max_pairs, or_vote* out,
                             uint64_t cap, uint64_t* vote_offsets);
 
+/* Containment search (readings C1-C4 in oracle.c): per reference sequence
+ * the number of mapped reads, their total length, and the accept decision.  Returns 0 (-1 on
+ * invalid parameters). */
+int or_contain(const uint8_t* refs, const uint64_t* ref_offsets, uint32_t n_refs, const char* pattern, int k, int w,
+               uint32_t frac_num, uint32_t frac_den, int64_t max_occ, const uint8_t* reads,
+               const uint64_t* read_offsets, uint32_t n_reads, uint32_t t, uint32_t D, uint32_t V,
+               uint32_t max_pairs, uint64_t batch_bases, uint32_t min_reads, uint32_t cov_num, uint32_t cov_den,
+               uint64_t* mapped_reads, uint64_t* mapped_bases, uint8_t* accepted);
+
 #ifdef __cplusplus
 }
 #endif
