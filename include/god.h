@@ -191,6 +191,30 @@ GOD_API god_status god_vote_reads(const god_index* idx, const uint8_t* reads, co
                                   const uint64_t* anchor_offsets, const god_vote_params* vp, god_vote* out,
                                   uint64_t* out_offsets, uint64_t cap, uint64_t* needed, god_stream stream);
 
+/* ---- containment search, desk scale ----
+ * The reference sequences are processed in batches of consecutive sequences holding at most
+ * batch_bases bases ("-I"; a longer sequence is a batch of its own; 0 = one batch), each
+ * batch's index built on the fly with `cutoff` applied within the batch (C1).  Every read is
+ * phase-selected (SELECT, cap t), seeded and voted (vp) against each batch; "mapped read ... the
+ * read that receives a mapping location using the location voting step": a read maps to
+ * sequence i if one of its voted locations (winning or rescue) has ref_lo inside i (C2).
+ * Outputs per reference sequence (n_refs each): mapped_reads = distinct reads mapped to it,
+ * mapped_bases = the sum of their lengths (coverage = mapped_bases / length, C3), accepted = 1 iff
+ * mapped_reads >= min_reads and mapped_bases * cov_den >= cov_num * length ("at least
+ * 100,000 mapped reads with a genome coverage of at least 1"; C4).  Each batch < 2^32 bases.
+ * Synchronizes. */
+typedef struct {
+    uint64_t batch_bases;   /* I: bases per reference batch (0 = all at once) */
+    uint32_t min_reads;     /* accept: mapped reads >= min_reads */
+    uint32_t cov_num, cov_den;  /* accept: coverage >= cov_num / cov_den (cov_den >= 1) */
+} god_contain_params;
+
+GOD_API god_status god_contain(const god_params* prm, const uint8_t* refs, const uint64_t* ref_offsets,
+                               uint32_t n_refs, const god_cutoff* cutoff, const uint8_t* reads,
+                               const uint64_t* read_offsets, uint32_t n_reads, uint32_t t,
+                               const god_vote_params* vp, const god_contain_params* cp, uint64_t* mapped_reads,
+                               uint64_t* mapped_bases, uint8_t* accepted, god_stream stream);
+
 /* ---- tracing: per-kernel device time by CUDA events on the launching stream ----
  * Off by default.  When on, every kernel launch is bracketed by two events; god_profile_query
  * synchronizes on the pending events and returns, per kernel name (in first-launch order), the

@@ -279,6 +279,31 @@ def god_vote_reads(index: GodIndex, reads, read_offsets, phases, anchors, anchor
     raise GodError(_lib.GOD_ETRUNC, "vote capacity retry failed")
 
 
+def god_contain(refs, ref_offsets, reads, read_offsets, pattern: str, k: int, w: int, cutoff=(1, 5000),
+                max_occ=None, t: int = 16, D: int = 0, V: int = 3, max_pairs: int = 0, batch_bases: int = 0,
+                min_reads: int = 1, cov=(1, 1)):
+    """Desk-scale containment search: per reference sequence the reads that
+    receive a voted location in it, their total length, and the accept decision (mapped reads >=
+    min_reads and coverage >= cov[0] / cov[1]).  -> (mapped_reads u64[n], mapped_bases u64[n],
+    accepted u8[n]) on the device if `reads` is a CUDA tensor, else numpy."""
+    L = _lib.load()
+    dev = _is_cuda(reads)
+    refs, ref_offsets = _prep(refs, np.uint8), _prep(ref_offsets, np.uint64)
+    reads, read_offsets = _prep(reads, np.uint8), _prep(read_offsets, np.uint64)
+    n = int(ref_offsets.shape[0]) - 1
+    dv = reads.device if dev else None
+    mr, mb, acc = _empty(max(1, n), np.uint64, dev, dv), _empty(max(1, n), np.uint64, dev, dv), \
+        _empty(max(1, n), np.uint8, dev, dv)
+    prm = _params(pattern, k, w)
+    cut = _lib.GodCutoff(1, 0, 1, int(max_occ)) if max_occ is not None else _lib.GodCutoff(0, cutoff[0], cutoff[1], 0)
+    vp = _lib.GodVoteParams(int(D), int(V), int(max_pairs))
+    cp = _lib.GodContainParams(int(batch_bases), int(min_reads), int(cov[0]), int(cov[1]))
+    _lib.check(L.god_contain(ctypes.byref(prm), _ptr(refs), _ptr(ref_offsets), n, ctypes.byref(cut), _ptr(reads),
+                             _ptr(read_offsets), int(read_offsets.shape[0]) - 1, int(t), ctypes.byref(vp),
+                             ctypes.byref(cp), _ptr(mr), _ptr(mb), _ptr(acc), _stream(dev)))
+    return mr[:n], mb[:n], acc[:n]
+
+
 def votes_numpy(votes) -> np.ndarray:
     """(n, 10) u32 device/host array in god_vote layout -> VOTE_DTYPE numpy records."""
     if _is_cuda(votes):
@@ -319,4 +344,5 @@ def launch_count() -> int:
 
 
 __all__ = ["god_sparsify", "god_minimizers", "god_build_index", "god_seed_reads", "god_vote_reads", "votes_numpy",
+           "god_contain",
            "GodIndex", "GodError", "ANCHOR_DTYPE", "VOTE_DTYPE", "version"]

@@ -604,4 +604,43 @@ GOD_API god_status god_vote_reads(const god_index* idx, const uint8_t* reads, co
   });
 }
 
+GOD_API god_status god_contain(const god_params* prm, const uint8_t* refs, const uint64_t* ref_offsets,
+                               uint32_t n_refs, const god_cutoff* cutoff, const uint8_t* reads,
+                               const uint64_t* read_offsets, uint32_t n_reads, uint32_t t,
+                               const god_vote_params* vp, const god_contain_params* cp, uint64_t* mapped_reads,
+                               uint64_t* mapped_bases, uint8_t* accepted, god_stream stream) {
+  return guarded([&] {
+    const Params P = make_params(prm);
+    GOD_REQUIRE(refs || n_refs == 0, "NULL refs");
+    GOD_REQUIRE(ref_offsets && read_offsets && cutoff && vp && cp, "NULL argument");
+    GOD_REQUIRE(n_refs == 0 || (mapped_reads && mapped_bases && accepted), "NULL output");
+    GOD_REQUIRE(t >= 1, "t must be >= 1");
+    GOD_REQUIRE(cp->cov_den >= 1, "cov_den must be >= 1");
+    GOD_REQUIRE(cutoff->mode == 1 || cutoff->frac_den >= 1, "cutoff fraction needs frac_den >= 1");
+    cudaStream_t st = (cudaStream_t)stream;
+    Scratch scr(st);
+    Stage sg(st, scr);
+    std::vector<uint64_t> hoff((size_t)n_refs + 1);
+    if (is_device_ptr(ref_offsets))
+      GOD_CUDA(cudaMemcpyAsync(hoff.data(), ref_offsets, hoff.size() * 8, cudaMemcpyDeviceToHost, st));
+    else
+      memcpy(hoff.data(), ref_offsets, hoff.size() * 8);
+    GOD_CUDA(cudaStreamSynchronize(st));
+    for (uint32_t i = 0; i < n_refs; i++) GOD_REQUIRE(hoff[i] <= hoff[i + 1], "ref_offsets must be ascending");
+    const uint64_t LR = hoff[n_refs];
+    const uint64_t LQ = total_len(read_offsets, n_reads, st);
+    const uint8_t* dref = sg.in(refs, LR);
+    const uint64_t* droff = sg.in(ref_offsets, (size_t)n_refs + 1);
+    const uint8_t* dreads = sg.in(reads, LQ);
+    const uint64_t* dqoff = sg.in(read_offsets, (size_t)n_reads + 1);
+    uint64_t* dmr = sg.out(mapped_reads, n_refs);
+    uint64_t* dmb = sg.out(mapped_bases, n_refs);
+    uint8_t* dacc = sg.out(accepted, n_refs);
+    if (n_refs)
+      god::contain(P, dref, droff, hoff.data(), n_refs, *cutoff, dreads, dqoff, n_reads, t, *vp, cp->batch_bases,
+                   cp->min_reads, cp->cov_num, cp->cov_den, dmr, dmb, dacc, st);
+    sg.finish();
+  });
+}
+
 }  // extern "C"

@@ -161,6 +161,11 @@ uint64_t seed_reads(const god_index* ix, const uint8_t* reads, const uint64_t* o
 uint64_t vote_reads(const god_index* ix, const uint8_t* reads, const uint64_t* roff, uint32_t n_reads,
                     const uint8_t* phases, const god_anchor* anchors, const uint64_t* aoff, const god_vote_params& vp,
                     god_vote* out, uint64_t* out_off, uint64_t cap, cudaStream_t st);
+// containment search over reference batches (contain.cu); ref_off on the device and the host
+void contain(const Params& P, const uint8_t* refs, const uint64_t* ref_off, const uint64_t* ref_off_host,
+             uint32_t n_refs, const god_cutoff& cut, const uint8_t* reads, const uint64_t* roff, uint32_t n_reads,
+             uint32_t t, const god_vote_params& vp, uint64_t batch_bases, uint32_t min_reads, uint32_t cov_num,
+             uint32_t cov_den, uint64_t* mreads, uint64_t* mbases, uint8_t* accepted, cudaStream_t st);
 void sparsify(const Params& P, const uint8_t* seq, const uint64_t* offsets, uint32_t n, const uint8_t* phases,
               uint64_t* packed, uint64_t* nmask, uint64_t* out_offsets, uint64_t* counts, uint64_t cap_words,
               uint64_t* needed_host, cudaStream_t st);
