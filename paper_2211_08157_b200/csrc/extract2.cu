@@ -177,19 +177,24 @@ constexpr uint32_t pack_sel() {
 template <int PP, int PX, int R0, bool CHECKED>
 __device__ __forceinline__ uint32_t pack16(const uint8_t* seq, uint64_t seq_bytes, uint64_t A, int nb,
                                            const uint32_t* lut, uint32_t* nm) {
-  const uint64_t Aa = A & ~3ull;
-  const uint32_t d8 = (uint32_t)(A - Aa) * 8;
+  // words aligned in the ADDRESS space (the caller's buffer may start anywhere, e.g. a tensor slice);
+  // the first word may begin up to 3 bytes before byte A (inside the allocation: allocations are
+  // aligned), and the tile descriptor's end margin covers the last one
+  const uintptr_t pA = reinterpret_cast<uintptr_t>(seq + A);
+  const uintptr_t pa = pA & ~(uintptr_t)3;
+  const uint32_t d8 = (uint32_t)(pA - pa) * 8;
   constexpr int NL = pack_words<PP, PX>();
   uint32_t w[NL];
-  const uint32_t* src = reinterpret_cast<const uint32_t*>(seq + Aa);
+  const uint32_t* src = reinterpret_cast<const uint32_t*>(pa);
 #pragma unroll
   for (int i = 0; i < NL; i++) {
     if constexpr (CHECKED) {
-      const uint64_t ad = Aa + 4ull * i;
+      const int64_t ad = (int64_t)(pa - reinterpret_cast<uintptr_t>(seq)) + 4ll * i;  // relative to seq
       uint32_t v = 0;
-      if (ad + 4 <= seq_bytes) v = __ldg(src + i);
+      if (ad >= 0 && (uint64_t)ad + 4 <= seq_bytes) v = __ldg(src + i);
       else
-        for (uint64_t q = ad; q < seq_bytes; q++) v |= (uint32_t)seq[q] << (8 * (q - ad));
+        for (int64_t q = ad < 0 ? 0 : ad; q < ad + 4 && (uint64_t)q < seq_bytes; q++)
+          v |= (uint32_t)seq[q] << (8 * (q - ad));
       w[i] = v;
     } else {
       w[i] = __ldg(src + i);

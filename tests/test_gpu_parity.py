@@ -344,3 +344,28 @@ def test_x2_matches_generic_kernel(monkeypatch):
     b = god.god_minimizers(cu(cfg.ref), cu(cfg.ref_offsets), "10", 21, 11, global_pos=True)
     for x, y in zip(a, b):
         assert torch.equal(x, y)
+
+
+def test_misaligned_device_buffers():
+    """Sequence buffers that start at any byte address (tensor slices): K1 aligns its word loads in
+    the address space, so results equal the aligned case and the oracle."""
+    cfg = synth.make_config("tiny")
+    ox = oracle.Index(cfg.ref, cfg.ref_offsets, "10", 21, 11)
+    n = 300
+    sub, soffs = synth.concat([cfg.reads.seq[int(cfg.reads.offsets[i]):int(cfg.reads.offsets[i + 1])]
+                               for i in range(n)])
+    oan, oao, oph = ox.seed_reads(sub, soffs)
+    for shift in (1, 2, 3, 5):
+        big = torch.zeros(cfg.ref.size + 16, dtype=torch.uint8, device="cuda")
+        big[shift:shift + cfg.ref.size] = cu(cfg.ref)
+        ref_view = big[shift:shift + cfg.ref.size]
+        assert ref_view.data_ptr() % 4 == shift % 4
+        ix = god.god_build_index(ref_view, cu(cfg.ref_offsets), "10", 21, 11)
+        h, p, z = ix.dump()
+        oh, op, oz = ox.dump()
+        assert np.array_equal(h, oh) and np.array_equal(p.astype(np.uint64), op) and np.array_equal(z, oz)
+        rb = torch.zeros(sub.size + 16, dtype=torch.uint8, device="cuda")
+        rb[shift:shift + sub.size] = cu(sub)
+        an, ao, ph = god.god_seed_reads(ix, rb[shift:shift + sub.size], cu(soffs))
+        assert np.array_equal(np_(ph), oph) and np.array_equal(np_(ao), oao)
+        assert np.array_equal(canon(np_(an)), canon(oan))
