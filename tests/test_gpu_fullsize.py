@@ -46,7 +46,26 @@ def _sampled_seed_parity(ix, ox, cfg, n_sample, seed):
     g["read_id"] = remap[g["read_id"]]
     g = np.sort(g, order=["read_id", "ref_pos", "read_pos", "strand"])
     assert np.array_equal(g, np.sort(oan, order=["read_id", "ref_pos", "read_pos", "strand"]))
-    return an, ao, ph
+    return an, ao, ph, ids, sub, soff, oph
+
+
+def _sampled_vote_parity(ix, ox, cfg, seeded, D, V, max_pairs):
+    """Location voting of ALL reads on the GPU (the launch configuration bench.py times), compared
+    on the sampled reads with the oracle's voting of the same reads."""
+    an, ao, ph, ids, sub, soff, oph = seeded
+    reads = cfg.reads
+    v, vo = god.god_vote_reads(ix, cu(reads.seq), cu(reads.offsets), cu(ph), cu(an), cu(ao), D=D, V=V,
+                               max_pairs=max_pairs)
+    gv, vo = god.votes_numpy(v), vo.cpu().numpy()
+    want, wo = ox.vote_reads(sub, soff, oph, D=D, V=V, max_pairs=max_pairs)
+    assert np.array_equal(vo[ids + 1] - vo[ids], np.diff(wo))
+    got = np.concatenate([gv[int(vo[i]):int(vo[i + 1])] for i in ids]) if ids.size else gv[:0]
+    remap = np.zeros(reads.n, np.uint32)
+    remap[ids] = np.arange(ids.size, dtype=np.uint32)
+    got = got.copy()
+    got["read_id"] = remap[got["read_id"]]
+    for f in oracle.VOTE_DTYPE.names:
+        assert np.array_equal(got[f], want[f]), f
 
 
 @pytest.mark.parametrize("name,pattern,n_sample", [("illumina", "10", 3000), ("hifi", "10", 40), ("hifi", "110", 30),
@@ -62,7 +81,10 @@ def test_fullsize_configs_2_to_4(name, pattern, n_sample):
     h, p, z = ix.dump()
     oh, op, oz = ox.dump()
     assert np.array_equal(h, oh) and np.array_equal(p.astype(np.uint64), op) and np.array_equal(z, oz)
-    _sampled_seed_parity(ix, ox, cfg, n_sample, 5)
+    seeded = _sampled_seed_parity(ix, ox, cfg, n_sample, 5)
+    _sampled_vote_parity(ix, ox, cfg, seeded, D=0, V=3, max_pairs=0)
+    if name != "illumina":  # long reads: the Fig. 8B distance (D = 100) and a capped list
+        _sampled_vote_parity(ix, ox, cfg, seeded, D=100, V=3, max_pairs=8)
 
 
 def test_fullsize_human_scale_sampled_and_properties():
@@ -138,3 +160,15 @@ def test_fullsize_human_scale_sampled_and_properties():
             else:
                 qend = int(orig[pos2j[qpos] + k - 1])
                 assert any(int(x[0]) + qend == g0 + 149 and int(x[3]) == 1 for x in hits)
+    # (5) voting: the true location of every exact read is a location with the most votes
+    v, vo = god.god_vote_reads(ix, cu(rs), cu(ro), cu(ph), cu(an), cu(ao), D=0, V=3)
+    gv, vo = god.votes_numpy(v), vo.cpu().numpy()
+    for i, (g0, s) in enumerate(zip(gs, strands)):
+        loc = gv[int(vo[i]):int(vo[i + 1])]
+        if int(ao[i + 1] - ao[i]) == 0:
+            assert loc.size == 0
+            continue
+        want_d = g0 + 149 if s else g0
+        # the cluster whose [Delta0, Delta0 + D] (D = read length) holds the true diagonal
+        hit = loc[(loc["strand"] == s) & (loc["diag"] <= want_d) & (want_d <= loc["diag"] + 150)]
+        assert hit.size == 1 and int(hit["votes"][0]) == int(loc["votes"].max()), (i, loc[:3])
