@@ -80,7 +80,7 @@ __device__ __forceinline__ uint32_t orig32(const Pattern& P, uint32_t q, uint32_
 }
 
 // canonical k-mer of the read's patterned k-mer starting at original position pos (phase a)
-__device__ uint64_t canon_at(const uint8_t* rd, uint32_t L, const Pattern& P, uint32_t a, int k, uint32_t pos) {
+__device__ uint64_t canon_at_generic(const uint8_t* rd, uint32_t L, const Pattern& P, uint32_t a, int k, uint32_t pos) {
   const uint32_t q = q_of(P, pos, a);
   uint32_t rr;
   uint32_t base = a + div_x(P, q, rr) * P.p;
@@ -92,6 +92,47 @@ __device__ uint64_t canon_at(const uint8_t* rd, uint32_t L, const Pattern& P, ui
     fwd = (fwd << 2) | c;
     rev |= (uint64_t)(3u - c) << (2 * i);
   }
+  return fwd < rev ? fwd : rev;
+}
+
+// x = 1 and p <= 2 ('1', '10', '01'): the k bases sit at pos + i p.  Aligned 32-bit loads (each
+// holds >= 1 byte of the k-mer's span, so none can fault), 2-bit codes of 4 bytes at once
+// (A0 C1 G2 T3 either case; a minimizer k-mer has no N), the reverse complement by bit reversal.
+__device__ uint64_t canon_at(const uint8_t* rd, uint32_t L, const Pattern& P, uint32_t a, int k, uint32_t pos) {
+  if (P.x != 1 || P.p > 2 || pos + (uint32_t)(k - 1) * P.p >= L)
+    return canon_at_generic(rd, L, P, a, k, pos);
+  const uintptr_t pb = reinterpret_cast<uintptr_t>(rd + pos), pa = pb & ~(uintptr_t)3;
+  const uint32_t sh = (uint32_t)(pb - pa);
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(pa);
+  uint64_t fwd = 0;
+  int got;  // codes shifted in
+  if (P.p == 1) {
+    const int nw = (int)((sh + (uint32_t)k + 3) >> 2);
+    for (int i = 0; i < nw; i++) {
+      const uint32_t v = __ldg(w + i);
+      const uint32_t c = ((v >> 1) ^ (v >> 2)) & 0x03030303u;
+      fwd = (fwd << 8) | ((c * 0x40100401u) >> 24);  // the 4 codes, first byte most significant
+    }
+    got = 4 * nw;
+    fwd >>= 2 * (got - (int)sh - k);
+  } else {
+    const uint32_t span = sh + 2u * (uint32_t)(k - 1) + 1u;
+    const int nw = (int)((span + 3) >> 2);
+    const uint32_t odd = sh & 1u;  // the k-mer's bytes are the odd (or even) bytes of each word
+    for (int i = 0; i < nw; i++) {
+      const uint32_t v = __ldg(w + i) >> (8 * odd);
+      const uint32_t c = ((v >> 1) ^ (v >> 2)) & 0x00030003u;
+      fwd = (fwd << 4) | ((c << 2) & 0xCu) | (c >> 16);
+    }
+    got = 2 * nw;
+    fwd >>= 2 * (got - (int)(sh >> 1) - k);
+  }
+  const uint64_t m = (1ull << (2 * k)) - 1;
+  fwd &= m;
+  // reverse complement: complement, reverse the order of the 2-bit codes
+  uint64_t x = __brevll(~fwd);
+  x = ((x >> 1) & 0x5555555555555555ull) | ((x & 0x5555555555555555ull) << 1);
+  const uint64_t rev = x >> (64 - 2 * k);
   return fwd < rev ? fwd : rev;
 }
 
@@ -338,6 +379,42 @@ __device__ void group_scan_flags(uint32_t n, const uint32_t* fa, uint32_t* out, 
   if (t == 0) { *total_a = base_a; *total_b = base_b; }
 }
 
+// hidx[i] = the largest h <= i starting a run of equal rp (h == 0 or rp[h-1] != rp[h]), by a
+// chunked max-scan over the group (NT = 32: one warp; else warps combined through ws)
+template <int NT>
+__device__ void group_head_scan(uint32_t n, const uint32_t* rp, uint32_t* hidx, uint32_t* ws, int t) {
+  const int lane = t & 31, warp = t >> 5;
+  constexpr int NW = NT / 32;
+  uint32_t carry = 0;
+  for (uint32_t c0 = 0; c0 < n; c0 += NT) {
+    const uint32_t i = c0 + t;
+    uint32_t v = (i < n && (i == 0 || rp[i - 1] != rp[i])) ? i : 0u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(FULL, v, o);
+      if (lane >= o) v = max(v, u);
+    }
+    uint32_t chunk_max;
+    if (NW > 1) {
+      if (lane == 31) ws[warp] = v;
+      __syncthreads();
+      uint32_t before = 0;
+      chunk_max = 0;
+      for (int q = 0; q < NW; q++) {
+        if (q < warp) before = max(before, ws[q]);
+        chunk_max = max(chunk_max, ws[q]);
+      }
+      __syncthreads();
+      v = max(v, before);
+    } else {
+      chunk_max = __shfl_sync(FULL, v, 31);
+    }
+    v = max(v, carry);
+    if (i < n) hidx[i] = v;
+    carry = max(carry, chunk_max);
+  }
+}
+
 template <int NT>
 __device__ void vote_group(const VoteArgs& A, uint32_t r, const GroupArrays& S, uint32_t* ws, int t) {
   const int lane = t & 31, warp = t >> 5;
@@ -360,12 +437,14 @@ __device__ void vote_group(const VoteArgs& A, uint32_t r, const GroupArrays& S, 
       S.canon[i] = canon_at(A.reads + rb, L, A.pat, ph, A.k, rp);
   }
   gsync<NT>();
+  // head of each run of equal read_pos (one read minimizer): segmented max-scan of head indices
+  group_head_scan<NT>(n, S.aux, S.cv, ws, t);
+  gsync<NT>();
   // keys; a non-head takes its head's canonical k-mer (heads are not written in this phase)
   bool bad = false;
   for (uint32_t i = t; i < n; i += NT) {
     const god_anchor an = A.an[a0 + i];
-    uint32_t j = i;
-    while (j > 0 && S.aux[j - 1] == an.read_pos) --j;
+    const uint32_t j = S.cv[i];
     uint64_t c = 0;
     if (an.read_pos < L && is_included(A.pat, an.read_pos, ph)) c = S.canon[j];
     if (j != i) S.canon[i] = c;
@@ -378,22 +457,25 @@ __device__ void vote_group(const VoteArgs& A, uint32_t r, const GroupArrays& S, 
     return;
   }
   // step (2): bitonic sort, all comparators ascending (mirror first step), virtual +inf past n
-  uint32_t N2 = 1;
-  while (N2 < n) N2 <<= 1;
-  for (uint32_t size = 2; size <= N2; size <<= 1) {
-    const uint32_t half = size >> 1;
+  // (strides are powers of two: index arithmetic by shifts)
+  uint32_t lg = 0;
+  while ((1u << lg) < n) ++lg;
+  const uint32_t N2 = 1u << lg;
+  for (uint32_t ls = 1; ls <= lg; ++ls) {  // size = 2^ls
+    const uint32_t lh = ls - 1, half = 1u << lh;
     for (uint32_t q = t; q < N2 / 2; q += NT) {
-      const uint32_t blk = q / half, off = q % half;
-      const uint32_t i = blk * size + off, j = blk * size + size - 1 - off;
+      const uint32_t base = (q >> lh) << ls, off = q & (half - 1);
+      const uint32_t i = base + off, j = base + (2u * half) - 1 - off;
       if (j < n) {
         const uint64_t x = S.key[i], y = S.key[j];
         if (y < x) { S.key[i] = y; S.key[j] = x; }
       }
     }
     gsync<NT>();
-    for (uint32_t stride = half >> 1; stride > 0; stride >>= 1) {
+    for (int lstr = (int)lh - 1; lstr >= 0; --lstr) {
+      const uint32_t stride = 1u << lstr;
       for (uint32_t q = t; q < N2 / 2; q += NT) {
-        const uint32_t i = (q / stride) * 2 * stride + (q % stride), j = i + stride;
+        const uint32_t i = ((q >> lstr) << (lstr + 1)) | (q & (stride - 1)), j = i + stride;
         if (j < n) {
           const uint64_t x = S.key[i], y = S.key[j];
           if (y < x) { S.key[i] = y; S.key[j] = x; }
