@@ -14,8 +14,8 @@
 // read's bytes once per read minimizer (anchors of one minimizer share read_pos).  The sweep (step
 // (3)) follows the chain of cluster heads: the next Delta0 is the first anchor beyond Delta0 + D.
 //
-// Reads are bucketed by anchor count n: n <= 32 -> one warp per read, everything in registers
-// (shuffle bitonic sort, ballots); n <= 256 -> one warp per read on a shared-memory slice;
+// Reads are bucketed by anchor count n: n <= 16 / n <= 32 -> 16 / 32 lanes per read, everything in
+// registers (shuffle bitonic sort, ballots); n <= VOTE_WSM -> one warp per read on a shared-memory slice;
 // n <= 2048 -> one CTA per read in shared memory; larger -> one CTA per read on global scratch.
 // Results go to per-read slots (min(n, max_pairs) each); a scan of the per-read counts and a
 // compaction give the CSR output.
@@ -29,7 +29,7 @@ namespace {
 constexpr uint64_t DIAG_MASK = (1ull << 34) - 1;   // of dk = key >> 29: strand at bit 34, biased diag below
 constexpr int64_t DIAG_BIAS = 1ll << 32;
 constexpr uint32_t VOTE_IDX_MAX = 1u << 29;        // anchors per read
-constexpr uint32_t VOTE_WSM = 256;                 // warp-per-read shared-memory path
+constexpr uint32_t VOTE_WSM = 128;                 // warp-per-read shared-memory path
 constexpr uint32_t VOTE_MID = 2048;                // CTA-per-read shared-memory path
 constexpr int VOTE_NT = 256;
 constexpr unsigned FULL = 0xffffffffu;
@@ -202,9 +202,9 @@ __global__ void k_vote_classify(const uint64_t* __restrict__ aoff, uint32_t n_re
       slots[r] = n == 0 ? 0 : (mp && n > mp ? mp : n);
     }
     if (n >= VOTE_IDX_MAX) { atomicAdd(bad + 1, 1u); n = 0; }
-    const int c = n == 0 ? -1 : n <= 32 ? 0 : n <= VOTE_WSM ? 1 : n <= VOTE_MID ? 2 : 3;
+    const int c = n == 0 ? -1 : n <= 16 ? 0 : n <= 32 ? 1 : n <= VOTE_WSM ? 2 : n <= VOTE_MID ? 3 : 4;
 #pragma unroll
-    for (int q = 0; q < 4; q++) {  // one atomic per warp and class
+    for (int q = 0; q < 5; q++) {  // one atomic per warp and class
       const uint32_t m = __ballot_sync(FULL, c == q);
       if (!m) continue;
       const int leader = __ffs(m) - 1;
@@ -214,113 +214,123 @@ __global__ void k_vote_classify(const uint64_t* __restrict__ aoff, uint32_t n_re
       if (c == q) {
         const uint32_t j = base + __popc(m & ((1u << lane) - 1u));
         lists[(uint64_t)q * n_reads + j] = r;
-        if (q == 3) big_off[j] = atomicAdd((unsigned long long*)big_total, (unsigned long long)(n + 2));
+        if (q == 4) big_off[j] = atomicAdd((unsigned long long*)big_total, (unsigned long long)(n + 2));
       }
     }
   }
 }
 
-// ------------------------------------------------------------------ n <= 32: one warp per read, registers
+// ------------------------------------------------------------------ n <= SEG: SEG lanes per read, registers
+// SEG = 16 (two reads per warp) or 32.  Every loop that shuffles runs a warp-uniform trip count.
+template <int SEG>
 __global__ void __launch_bounds__(VOTE_NT) k_vote_warp(VoteArgs A, const uint32_t* __restrict__ list, uint32_t nlist) {
-  const int lane = threadIdx.x & 31;
-  const uint32_t wid = (uint32_t)((blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5);
-  if (wid >= nlist) return;  // warp-uniform
-  const uint32_t r = list[wid];
-  const uint64_t a0 = A.aoff[r];
-  const uint32_t n = (uint32_t)(A.aoff[r + 1] - a0);
-  const uint64_t rb = A.roff[r];
-  const uint32_t L = (uint32_t)(A.roff[r + 1] - rb);
-  const uint32_t ph = A.ph[r];
+  constexpr uint32_t SB = SEG == 32 ? FULL : ((1u << SEG) - 1u);
+  const int lane = threadIdx.x & 31, sl = lane & (SEG - 1), sbase = lane & ~(SEG - 1);
+  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / SEG;
+  if (__all_sync(FULL, gw >= nlist)) return;  // warp-uniform
+  const bool active = gw < nlist;
+  const uint32_t r = active ? list[gw] : 0u;
+  const uint64_t a0 = active ? A.aoff[r] : 0;
+  const uint32_t n = active ? (uint32_t)(A.aoff[r + 1] - a0) : 0u;
+  const uint64_t rb = active ? A.roff[r] : 0;
+  const uint32_t L = active ? (uint32_t)(A.roff[r + 1] - rb) : 0u;
+  const uint32_t ph = active ? A.ph[r] : 0u;
   const uint64_t D = A.D ? A.D : L;
-  const bool valid = lane < (int)n;
-  const uint32_t le = (lane == 31) ? FULL : ((2u << lane) - 1u);
+  const bool valid = sl < (int)n;
+  const uint32_t le = (sl == 31) ? FULL : ((2u << sl) - 1u);
+  auto ballot = [&](bool p) { return (__ballot_sync(FULL, p) >> sbase) & SB; };
   god_anchor an = {0, 0, 0, 0};
-  if (valid) an = A.an[a0 + lane];
+  if (valid) an = A.an[a0 + sl];
   // canonical k-mer once per read minimizer (a run of equal read_pos), then broadcast
-  const uint32_t prev_rp = __shfl_up_sync(FULL, an.read_pos, 1);
-  const bool rhead = valid && (lane == 0 || prev_rp != an.read_pos);
+  const uint32_t prev_rp = __shfl_up_sync(FULL, an.read_pos, 1, SEG);
+  const bool rhead = valid && (sl == 0 || prev_rp != an.read_pos);
   uint64_t canon = 0;
   if (rhead && an.read_pos < L && is_included(A.pat, an.read_pos, ph))
     canon = canon_at(A.reads + rb, L, A.pat, ph, A.k, an.read_pos);
-  const uint32_t hm = __ballot_sync(FULL, rhead) & le;
-  canon = __shfl_sync(FULL, canon, hm ? 31 - __clz(hm) : 0);
+  const uint32_t hm = ballot(rhead) & le;
+  canon = __shfl_sync(FULL, canon, hm ? 31 - __clz(hm) : 0, SEG);
   bool bad = false;
   uint64_t key = ~0ull;
-  if (valid) key = vote_key(A, an, ph, L, canon, 5, (uint32_t)lane, bad);
-  if (__any_sync(FULL, bad)) {
-    if (lane == 0) atomicAdd(A.bad, 1u);
-    return;
-  }
-  // step (2): bitonic sort of the 32 keys across the warp (pads ~0 sink to the end)
+  if (valid) key = vote_key(A, an, ph, L, canon, 5, (uint32_t)sl, bad);
+  const bool seg_bad = ballot(bad) != 0;
+  if (seg_bad && sl == 0) atomicAdd(A.bad, 1u);
+  // step (2): bitonic sort of the SEG keys (pads ~0 sink to the end)
 #pragma unroll
-  for (int size = 2; size <= 32; size <<= 1) {
+  for (int size = 2; size <= SEG; size <<= 1) {
 #pragma unroll
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
       const uint64_t o = __shfl_xor_sync(FULL, key, stride);
-      const bool up = (lane & size) == 0;
-      const bool lower = (lane & stride) == 0;
+      const bool up = (sl & size) == 0 || size == SEG;
+      const bool lower = (sl & stride) == 0;
       key = (lower == up) ? (key < o ? key : o) : (key > o ? key : o);
     }
   }
   const int src = (int)(key & 31u);
-  const uint32_t ref = __shfl_sync(FULL, an.ref_pos, src);
-  const uint32_t qp = __shfl_sync(FULL, an.read_pos, src);
-  const uint64_t cn = __shfl_sync(FULL, canon, src);
+  const uint32_t ref = __shfl_sync(FULL, an.ref_pos, src, SEG);
+  const uint32_t qp = __shfl_sync(FULL, an.read_pos, src, SEG);
+  const uint64_t cn = __shfl_sync(FULL, canon, src, SEG);
   const uint64_t dk = key >> 29;
   // V2: a repeat of (hash, strand, diag) is no new vote: walk back over equal (strand, diag, fp)
   bool dup = false, walking = valid;
   for (int o = 1; __any_sync(FULL, walking); o++) {
-    const uint64_t ko = __shfl_up_sync(FULL, key, o);
-    const uint64_t co = __shfl_up_sync(FULL, cn, o);
+    const uint64_t ko = __shfl_up_sync(FULL, key, o, SEG);
+    const uint64_t co = __shfl_up_sync(FULL, cn, o, SEG);
     if (walking) {
-      if (lane < o || (ko >> 5) != (key >> 5)) walking = false;
+      if (sl < o || (ko >> 5) != (key >> 5)) walking = false;
       else if (co == cn) { dup = true; walking = false; }
     }
   }
   // step (3): the chain of cluster heads
-  uint32_t starts = 0;
-  for (uint32_t s = 0; s < n;) {
-    starts |= 1u << s;
-    const uint64_t dh = __shfl_sync(FULL, dk, (int)s);
-    const uint32_t b = __ballot_sync(FULL, valid && lane > (int)s && beyond(dk, dh, D));
-    s = b ? (uint32_t)(__ffs(b) - 1) : n;
+  uint32_t starts = 0, s = 0;
+  while (__any_sync(FULL, s < n)) {
+    const bool live = s < n;
+    const uint64_t dh = __shfl_sync(FULL, dk, live ? (int)s : 0, SEG);
+    const uint32_t b = ballot(valid && sl > (int)s && beyond(dk, dh, D));
+    if (live) {
+      starts |= 1u << s;
+      s = b ? (uint32_t)(__ffs(b) - 1) : n;
+    }
   }
   const int cid = __popc(starts & le) - 1;
-  const uint32_t newmask = __ballot_sync(FULL, valid && !dup);
+  const uint32_t newmask = ballot(valid && !dup);
   // member spans: segmented suffix min/max (clusters are contiguous)
   uint32_t rlo = ref, rhi = ref, qlo = qp, qhi = qp;
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t a1 = __shfl_down_sync(FULL, rlo, o), a2 = __shfl_down_sync(FULL, rhi, o);
-    const uint32_t a3 = __shfl_down_sync(FULL, qlo, o), a4 = __shfl_down_sync(FULL, qhi, o);
-    const int oc = __shfl_down_sync(FULL, cid, o);
-    if (lane + o < (int)n && oc == cid) {
+  for (int o = 1; o < SEG; o <<= 1) {
+    const uint32_t a1 = __shfl_down_sync(FULL, rlo, o, SEG), a2 = __shfl_down_sync(FULL, rhi, o, SEG);
+    const uint32_t a3 = __shfl_down_sync(FULL, qlo, o, SEG), a4 = __shfl_down_sync(FULL, qhi, o, SEG);
+    const int oc = __shfl_down_sync(FULL, cid, o, SEG);
+    if (sl + o < (int)n && oc == cid) {
       rlo = min(rlo, a1); rhi = max(rhi, a2); qlo = min(qlo, a3); qhi = max(qhi, a4);
     }
   }
-  const bool head = valid && ((starts >> lane) & 1u);
+  const bool head = valid && ((starts >> sl) & 1u);
   uint32_t votes = 0;
   if (head) {
     const uint32_t after = starts & ~le;
     const uint32_t e = after ? (uint32_t)(__ffs(after) - 1) : n;
-    const uint32_t range = (e >= 32 ? FULL : ((1u << e) - 1u)) & ~((1u << lane) - 1u);
+    const uint32_t range = (e >= 32 ? FULL : ((1u << e) - 1u)) & ~((1u << sl) - 1u);
     votes = __popc(newmask & range);
   }
   // step (4) / rescue
-  const uint32_t winmask = __ballot_sync(FULL, head && votes >= A.V);
+  const uint32_t winmask = ballot(head && votes >= A.V);
   const bool rescue = winmask == 0;
   const uint32_t candmask = rescue ? starts : winmask;
-  const bool cand = (candmask >> lane) & 1u;
+  const bool cand = (candmask >> sl) & 1u;
   uint32_t rank = 0;
-  for (uint32_t m = candmask; m; m &= m - 1) {
-    const int j = __ffs(m) - 1;
-    const uint32_t vj = __shfl_sync(FULL, votes, j);
-    const uint64_t dj = __shfl_sync(FULL, dk, j);
-    rank += j != lane && better(vj, dj, votes, dk);
+  for (uint32_t m = candmask; __any_sync(FULL, m != 0);) {
+    const int j = m ? __ffs(m) - 1 : 0;
+    const uint32_t vj = __shfl_sync(FULL, votes, j, SEG);
+    const uint64_t dj = __shfl_sync(FULL, dk, j, SEG);
+    if (m) {
+      rank += j != sl && better(vj, dj, votes, dk);
+      m &= m - 1;
+    }
   }
   const uint32_t limit = rescue ? 1u : (A.mp ? A.mp : 32u);
+  if (!active || seg_bad) return;
   if (cand && rank < limit) put_result(A, r, rank, dk, votes, rescue ? 1u : 0u, rlo, rhi, qlo, qhi);
-  if (lane == 0) A.cnt[r] = min((uint32_t)__popc(candmask), limit);
+  if (sl == 0) A.cnt[r] = n ? min((uint32_t)__popc(candmask), limit) : 0u;
 }
 
 // ------------------------------------------------------------------ n > 32: a group of NT threads per read
@@ -663,8 +673,8 @@ uint64_t vote_reads(const god_index* ix, const uint8_t* reads, const uint64_t* r
                     god_vote* out, uint64_t* out_off, uint64_t cap, cudaStream_t st) {
   Scratch scr(st);
   uint64_t* slot_off = scr.alloc<uint64_t>((size_t)n_reads + 1);
-  uint32_t* lists = scr.alloc<uint32_t>(4ull * n_reads + 1);
-  uint32_t* ctr = scr.alloc<uint32_t>(8);        // nlist[4], bad[2]
+  uint32_t* lists = scr.alloc<uint32_t>(5ull * n_reads + 1);
+  uint32_t* ctr = scr.alloc<uint32_t>(8);        // nlist[5], bad[2]
   uint64_t* big_total = scr.alloc<uint64_t>(1);
   uint64_t* big_off = scr.alloc<uint64_t>((size_t)n_reads + 1);
   uint32_t* cnt = scr.alloc<uint32_t>((size_t)n_reads + 1);
@@ -675,7 +685,7 @@ uint64_t vote_reads(const god_index* ix, const uint8_t* reads, const uint64_t* r
   const int nsm = num_sms();
   if (n_reads)
     GOD_LAUNCH("k_vote_classify", k_vote_classify, std::min<unsigned>(grid_for(n_reads, 256), nsm * 8u), 256, 0, st,
-               aoff, n_reads, vp.max_pairs, slot_off, lists, ctr, big_off, big_total, ctr + 4);
+               aoff, n_reads, vp.max_pairs, slot_off, lists, ctr, big_off, big_total, ctr + 5);
   scan_exclusive_u64(slot_off, slot_off, (uint64_t)n_reads + 1, nullptr, st, scr, "scan_vote_slots");
   uint32_t h[8];
   GOD_CUDA(cudaMemcpyAsync(h, ctr, sizeof(h), cudaMemcpyDeviceToHost, st));
@@ -683,7 +693,7 @@ uint64_t vote_reads(const god_index* ix, const uint8_t* reads, const uint64_t* r
   GOD_CUDA(cudaMemcpyAsync(&hb[0], slot_off + n_reads, 8, cudaMemcpyDeviceToHost, st));
   GOD_CUDA(cudaMemcpyAsync(&hb[1], big_total, 8, cudaMemcpyDeviceToHost, st));
   GOD_CUDA(cudaStreamSynchronize(st));
-  GOD_REQUIRE(h[5] == 0, "a read has >= 2^29 anchors");
+  GOD_REQUIRE(h[6] == 0, "a read has >= 2^29 anchors");
   god_vote* res = scr.alloc<god_vote>(hb[0] ? hb[0] : 1);
   VoteArgs A;
   A.reads = reads;
@@ -699,7 +709,7 @@ uint64_t vote_reads(const god_index* ix, const uint8_t* reads, const uint64_t* r
   A.slot_off = slot_off;
   A.res = res;
   A.cnt = cnt;
-  A.bad = ctr + 4;
+  A.bad = ctr + 5;
   static bool attr = false;
   const size_t sm_wsm = (VOTE_NT / 32) * group_bytes(VOTE_WSM), sm_mid = group_bytes(VOTE_MID);
   if (!attr) {
@@ -707,18 +717,23 @@ uint64_t vote_reads(const god_index* ix, const uint8_t* reads, const uint64_t* r
     GOD_CUDA(cudaFuncSetAttribute(k_vote_mid, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_mid));
     attr = true;
   }
-  if (h[0]) GOD_LAUNCH("k_vote_warp", k_vote_warp, grid_for((uint64_t)h[0] * 32, VOTE_NT), VOTE_NT, 0, st, A, lists, h[0]);
+  if (h[0])
+    GOD_LAUNCH("k_vote_warp16", k_vote_warp<16>, grid_for((uint64_t)h[0] * 16, VOTE_NT), VOTE_NT, 0, st, A, lists, h[0]);
   if (h[1])
-    GOD_LAUNCH("k_vote_wsm", k_vote_wsm, grid_for(h[1], VOTE_NT / 32), VOTE_NT, sm_wsm, st, A, lists + n_reads, h[1]);
-  if (h[2]) GOD_LAUNCH("k_vote_mid", k_vote_mid, h[2], VOTE_NT, sm_mid, st, A, lists + 2ull * n_reads);
-  if (h[3]) {
+    GOD_LAUNCH("k_vote_warp", k_vote_warp<32>, grid_for((uint64_t)h[1] * 32, VOTE_NT), VOTE_NT, 0, st, A,
+               lists + n_reads, h[1]);
+  if (h[2])
+    GOD_LAUNCH("k_vote_wsm", k_vote_wsm, grid_for(h[2], VOTE_NT / 32), VOTE_NT, sm_wsm, st, A, lists + 2ull * n_reads,
+               h[2]);
+  if (h[3]) GOD_LAUNCH("k_vote_mid", k_vote_mid, h[3], VOTE_NT, sm_mid, st, A, lists + 3ull * n_reads);
+  if (h[4]) {
     unsigned char* gs = scr.alloc<unsigned char>(hb[1] * 32 + 64);
-    GOD_LAUNCH("k_vote_big", k_vote_big, h[3], VOTE_NT, 0, st, A, lists + 3ull * n_reads, big_off, gs);
+    GOD_LAUNCH("k_vote_big", k_vote_big, h[4], VOTE_NT, 0, st, A, lists + 4ull * n_reads, big_off, gs);
   }
   scan_exclusive_u32_to_u64(cnt, out_off, (uint64_t)n_reads + 1, nullptr, st, scr, "scan_vote_out");
   uint32_t nbad = 0;
   uint64_t tot = 0;
-  GOD_CUDA(cudaMemcpyAsync(&nbad, ctr + 4, 4, cudaMemcpyDeviceToHost, st));
+  GOD_CUDA(cudaMemcpyAsync(&nbad, ctr + 5, 4, cudaMemcpyDeviceToHost, st));
   GOD_CUDA(cudaMemcpyAsync(&tot, out_off + n_reads, 8, cudaMemcpyDeviceToHost, st));
   GOD_CUDA(cudaStreamSynchronize(st));
   GOD_REQUIRE(nbad == 0, "anchors inconsistent with the reads' phases (read_pos not an included position)");
