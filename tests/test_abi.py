@@ -83,3 +83,22 @@ def test_einval_null_and_python_error(lib):
     with pytest.raises(GodError):
         god_minimizers(np.frombuffer(b"ACGT", np.uint8), np.array([0, 4], np.uint64), "10", 3, 2,
                        phases=np.array([2], np.uint8))
+
+
+def test_einval_voting_and_containment(lib):
+    """god_vote_reads / god_contain validate their arguments on the host before any CUDA call."""
+    from paper_2211_08157_b200 import _lib, god_contain, GodError
+    need = ctypes.c_uint64(0)
+    vp = _lib.GodVoteParams(0, 3, 0)
+    assert lib.god_vote_reads(None, None, None, 0, None, None, None, ctypes.byref(vp), None, None, 0,
+                              ctypes.byref(need), None) == 1
+    assert b"EINVAL" in lib.god_last_error()
+    refs = np.frombuffer(b"ACGT" * 64, np.uint8)
+    ro = np.array([0, refs.size], np.uint64)
+    for kw in ({"cov": (1, 0)}, {"t": 0}):
+        with pytest.raises(GodError) as ei:
+            god_contain(refs, ro, refs, ro, "10", 15, 10, **kw)
+        assert ei.value.status == _lib.GOD_EINVAL
+    with pytest.raises(GodError) as ei:
+        god_contain(refs, ro, refs, ro, "102", 15, 10)
+    assert ei.value.status == _lib.GOD_EINVAL

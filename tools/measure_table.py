@@ -8,8 +8,8 @@ ROWS = [("Tiny '10'", "tiny"), ("Illumina '10'", "illumina"), ("HiFi '10'", "hif
         ("Human '1'", "human-1")]
 PEAK = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
 print("| Config / pattern | Index build Gbp/s | Stage 1+2 GB/s (% of 6.53 TB/s; of 8 TB/s) | Stage 3 ms (sort, count, "
-      "cutoff, table) | Reads/s | Anchors/s | Step ms | Oracle (1 core) reads/s (sample) | Bit-exact |")
-print("|---|---|---|---|---|---|---|---|---|")
+      "cutoff, table) | Reads/s | Anchors/s | Step ms | Voting ms (reads/s) | Oracle (1 core) reads/s (sample) | Bit-exact |")
+print("|---|---|---|---|---|---|---|---|---|---|")
 for label, wl in ROWS:
     steps = "3" if wl.startswith("human") else "5"
     cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--workload", wl, "--steps", steps, "--warmup", "3",
@@ -31,4 +31,5 @@ for label, wl in ROWS:
         "yes on sampled outputs + properties (tests/test_gpu_fullsize.py)"
     print(f"| {label} | {d['index_build_gbps']:.1f} | {gbs:.0f} ({100 * gbs / PEAK:.1f}%; {100 * gbs / 8000:.1f}%) | "
           f"{st3:.1f} | {d['seed_reads_per_s'] / 1e6:.1f} M | {d['anchors_per_s'] / 1e9:.2f} G | {d['ms_per_step']:.2f} | "
+          f"{(d.get('vote') or {}).get('ms', float('nan')):.2f} ({(d.get('vote') or {}).get('reads_per_s', float('nan')) / 1e6:.1f} M) | "
           f"{cpu.get('value', float('nan')):.0f} | {exact} |", flush=True)
