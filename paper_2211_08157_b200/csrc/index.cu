@@ -13,8 +13,10 @@
 //       free bits + count histogram); k_runs on the full-LSD path
 //   K4  cutoff tau on device (reading O7): count histogram (small counts) + radix select
 //       over the rare large counts; tau = (m+1)-th largest count, m = floor(n*num/den)
-//   K5  kept entries in one ordered pass (k_keep_write: ballots + decoupled look-back)
-//   K6  directory: data-sized slot map (or top-B-bit prefix) -> 32-B slot records
+//   K5  kept entries in one ordered pass (k_keep_write: ballots + decoupled look-back), which also
+//       marks the first entry of every non-empty directory slot (K6a)
+//   K6  directory: data-sized slot map (or top-B-bit prefix); one right-to-left suffix-min pass
+//       fills the empty slots and writes the 32-B slot records (k_dir_suffix_min, K6b + K6c)
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -817,7 +819,7 @@ __global__ void __launch_bounds__(1024) k_tau(const uint32_t* hist_small, const 
 constexpr int KW_NT = 256, KW_IPT = 16, KW_TILE = KW_NT * KW_IPT;
 __global__ void __launch_bounds__(KW_NT) k_keep_write(const uint64_t* __restrict__ k, const uint32_t* __restrict__ pos,
                                                       uint64_t n, int hbits, const CutState* cs,
-                                                      IndexView iv, uint64_t* ent, uint32_t* kslot, uint64_t* status,
+                                                      IndexView iv, uint64_t* ent, uint32_t* dir1, uint64_t* status,
                                                       uint32_t* tile_ctr) {
   __shared__ uint32_t s_tile;
   __shared__ uint32_t wtot[KW_NT / 32];
@@ -866,30 +868,38 @@ __global__ void __launch_bounds__(KW_NT) k_keep_write(const uint64_t* __restrict
 #pragma unroll
   for (int j = 0; j < KW_IPT; j++) {
     const uint32_t m = masks[j];
-    if ((m >> lane) & 1u) {
+    const bool mine = (m >> lane) & 1u;
+    uint32_t slot = 0;
+    uint64_t d = 0;
+    if (mine) {
       const uint64_t i = base + (uint64_t)j * 32 + lane;
       const uint64_t v = k[i];
       const uint64_t h = v & hm;
-      const uint64_t d = run + __popc(m & lt);
+      d = run + __popc(m & lt);
       ent[d] = ((uint64_t)pos[i] << 32) | ((h & lowmask) << 1) | (v >> 63);
-      kslot[d] = (uint32_t)index_slot(iv, h);
+      slot = (uint32_t)index_slot(iv, h);
+    }
+    // K6a fused: the first entry of each slot (entries are in slot order).  The previous kept entry
+    // of this round decides; the first kept lane of a round cannot see its predecessor and takes an
+    // atomic minimum (a plain store only ever writes the true first entry, so the two commute).
+    const uint32_t before = m & lt;
+    const int prev = before ? 31 - __clz(before) : lane;
+    const uint32_t pslot = __shfl_sync(0xffffffffu, slot, prev);
+    if (mine) {
+      if (!before) atomicMin(dir1 + slot, (uint32_t)d);
+      else if (pslot != slot) dir1[slot] = (uint32_t)d;
     }
     run += __popc(m);
   }
 }
 
-__global__ void k_dir_mark(const uint32_t* __restrict__ kslot, uint64_t n_kept, uint64_t n_slots, uint32_t* dir) {
-  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < n_kept; e += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t s = kslot[e];
-    if (e == 0 || kslot[e - 1] != s) dir[s] = (uint32_t)e;
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) dir[n_slots] = (uint32_t)n_kept;
-}
 
 // K6b: empty slots take the next non-empty slot's first entry: a suffix-min over dir[0 .. 2^B],
 // single pass, tiles processed right to left with a decoupled look-back on the running minimum.
 constexpr int DF_NT = 256, DF_IPT = 16, DF_TILE = DF_NT * DF_IPT;
-__global__ void __launch_bounds__(DF_NT) k_dir_suffix_min(uint32_t* dir, uint64_t n, uint64_t* status, uint32_t* ctr) {
+__global__ void __launch_bounds__(DF_NT) k_dir_suffix_min(const uint32_t* dir, uint64_t n, uint64_t* status, uint32_t* ctr,
+                                                          const uint64_t* __restrict__ ent, uint64_t n_slots,
+                                                          DirRec* __restrict__ rec) {
   __shared__ uint32_t s_tile;
   __shared__ uint32_t warp_min[DF_NT / 32];
   __shared__ uint32_t s_carry;
@@ -954,10 +964,29 @@ __global__ void __launch_bounds__(DF_NT) k_dir_suffix_min(uint32_t* dir, uint64_
     else if (lane < 31 && wid + 1 < DF_NT / 32) after = min(after, warp_min[wid + 1]);
   }
   after = min(after, s_carry);
+  // K6c fused: slot s holds the kept entries [d(s), d(s + 1)); the tile's final d values go to SMEM
+  // (d(tile end) = the carry from the right), then consecutive threads write consecutive 32-B slot
+  // records (coalesced) with the low-bit keys of each slot's first entries
+  __shared__ uint32_t sd[DF_TILE + 1];
 #pragma unroll
-  for (int i = 0; i < DF_IPT; i++)
-    if (base + i < n) dir[base + i] = min(v[i], after);
+  for (int i = 0; i < DF_IPT; i++) sd[threadIdx.x * DF_IPT + i] = min(v[i], after);
+  if (threadIdx.x == 0) sd[DF_TILE] = s_carry;
+  __syncthreads();
+  const uint64_t t0 = t * DF_TILE;
+  for (uint32_t q = threadIdx.x; q < (uint32_t)DF_TILE; q += DF_NT) {
+    const uint64_t sl = t0 + q;
+    if (sl >= n_slots) break;
+    const uint32_t a = sd[q], b = sd[q + 1];
+    uint32_t kk[DIR_KEYS];
+#pragma unroll
+    for (int e = 0; e < DIR_KEYS; e++) kk[e] = a + e < b ? (uint32_t)ent[a + e] >> 1 : 0xFFFFFFFFu;
+    uint4* o = reinterpret_cast<uint4*>(rec + sl);
+    o[0] = make_uint4(a, b, kk[0], kk[1]);
+    o[1] = make_uint4(kk[2], kk[3], kk[4], kk[5]);
+  }
 }
+
+__global__ void k_put_u32(uint32_t* p, uint32_t v) { *p = v; }
 
 }  // namespace
 
@@ -969,18 +998,6 @@ __global__ void k_count_queries(god::IndexView v, const uint64_t* __restrict__ h
   }
 }
 
-__global__ void k_dir_records(const uint32_t* __restrict__ d1, const uint64_t* __restrict__ ent, uint64_t n_slots,
-                              DirRec* dir) {
-  for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < n_slots; s += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t a = d1[s], b = d1[s + 1];
-    uint32_t k[DIR_KEYS];
-#pragma unroll
-    for (int q = 0; q < DIR_KEYS; q++) k[q] = a + q < b ? (uint32_t)ent[a + q] >> 1 : 0xFFFFFFFFu;
-    uint4* o = reinterpret_cast<uint4*>(dir + s);
-    o[0] = make_uint4(a, b, k[0], k[1]);
-    o[1] = make_uint4(k[2], k[3], k[4], k[5]);
-  }
-}
 
 __global__ void k_dump(god::IndexView v, uint64_t* hash, uint32_t* pos, uint8_t* strand) {
   for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < v.n_kept; e += (uint64_t)gridDim.x * blockDim.x) {
@@ -1167,28 +1184,26 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
   GOD_CUDA(cudaMallocAsync((void**)&ix->dir, n_slots * sizeof(DirRec), st));
   uint32_t* dir1 = scr.alloc<uint32_t>(n_slots + 1);  // first entry per slot (+ n_kept), then pairs
   GOD_CUDA(cudaMallocAsync((void**)&ix->ent, (n_kept ? n_kept : 1) * sizeof(uint64_t), st));
-  uint32_t* kslot = scr.alloc<uint32_t>(n_kept ? n_kept : 1);
-  if (n) {  // K5: kept entries
+  const uint64_t nd1 = n_slots + 1;
+  GOD_CUDA(cudaMemsetAsync(dir1, 0xFF, nd1 * sizeof(uint32_t), st));
+  if (n) {  // K5: kept entries (+ K6a: the first entry of every non-empty slot)
     const uint64_t tiles = (n + KW_TILE - 1) / KW_TILE;
     uint64_t* kst = scr.alloc<uint64_t>(tiles);
     uint32_t* kctr = scr.alloc<uint32_t>(1);
     GOD_CUDA(cudaMemsetAsync(kst, 0, tiles * sizeof(uint64_t), st));
     GOD_CUDA(cudaMemsetAsync(kctr, 0, sizeof(uint32_t), st));
     GOD_LAUNCH("k_keep_write", k_keep_write, (unsigned)tiles, KW_NT, 0, st, k0, v0, n, (int)(2 * P.k), cs, ix->view(),
-               ix->ent, kslot, kst, kctr);
+               ix->ent, dir1, kst, kctr);
   }
-  {
-    const uint64_t nd1 = n_slots + 1;
-    GOD_CUDA(cudaMemsetAsync(dir1, 0xFF, nd1 * sizeof(uint32_t), st));
-    GOD_LAUNCH("k_dir_mark", k_dir_mark, min(grid_for(n_kept ? n_kept : 1, 256), 16u * num_sms()), 256, 0, st, kslot,
-               n_kept, n_slots, dir1);
+  GOD_LAUNCH("k_put_u32", k_put_u32, 1, 1, 0, st, dir1 + n_slots, (uint32_t)n_kept);
+  {  // K6b + K6c: suffix minimum over the slots, then the 32-B slot records, one pass
     const uint64_t nt = (nd1 + DF_TILE - 1) / DF_TILE;
     uint64_t* dst = scr.alloc<uint64_t>(nt);
     uint32_t* dctr = scr.alloc<uint32_t>(1);
     GOD_CUDA(cudaMemsetAsync(dst, 0, nt * sizeof(uint64_t), st));
     GOD_CUDA(cudaMemsetAsync(dctr, 0, sizeof(uint32_t), st));
-    GOD_LAUNCH("k_dir_suffix_min", k_dir_suffix_min, (unsigned)nt, DF_NT, 0, st, dir1, nd1, dst, dctr);
-    GOD_LAUNCH("k_dir_records", k_dir_records, grid_for(n_slots, 256), 256, 0, st, dir1, ix->ent, n_slots, ix->dir);
+    GOD_LAUNCH("k_dir_suffix_min", k_dir_suffix_min, (unsigned)nt, DF_NT, 0, st, dir1, nd1, dst, dctr, ix->ent,
+               n_slots, ix->dir);
   }
   GOD_CUDA(cudaStreamSynchronize(st));
   if (const char* dd = getenv("GOD_DEBUG_DIR")) {  // developer aid: dump the intermediates
@@ -1200,7 +1215,7 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
       if (fp) { fwrite(h.data(), 1, bytes, fp); fclose(fp); }
     };
     dump("rec_hz", rec.hz, n * 8); dump("sorted_hz", k0, n * 8); dump("sorted_pos", v0, n * 4);
-    dump("kslot", kslot, n_kept * 4);
+    dump("dir1", dir1, (n_slots + 1) * 4);
     dump("ent", ix->ent, n_kept * 8); dump("dir", ix->dir, n_slots * sizeof(DirRec));
   }
 }

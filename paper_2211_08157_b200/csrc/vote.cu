@@ -15,8 +15,9 @@
 // (3)) follows the chain of cluster heads: the next Delta0 is the first anchor beyond Delta0 + D.
 //
 // Reads are bucketed by anchor count n: n <= 16 / n <= 32 -> 16 / 32 lanes per read, everything in
-// registers (shuffle bitonic sort, ballots); n <= VOTE_WSM -> one warp per read on a shared-memory slice;
-// n <= 2048 -> one CTA per read in shared memory; larger -> one CTA per read on global scratch.
+// registers (shuffle bitonic sort, ballots); n <= 128 / n <= 512 -> one warp per read on a 3 / 12 KB
+// shared-memory slice; n <= 2048 -> one CTA per read in shared memory; larger -> one CTA per read
+// on global scratch.
 // Results go to per-read slots (min(n, max_pairs) each); a scan of the per-read counts and a
 // compaction give the CSR output.
 #include <algorithm>
@@ -29,7 +30,8 @@ namespace {
 constexpr uint64_t DIAG_MASK = (1ull << 34) - 1;   // of dk = key >> 29: strand at bit 34, biased diag below
 constexpr int64_t DIAG_BIAS = 1ll << 32;
 constexpr uint32_t VOTE_IDX_MAX = 1u << 29;        // anchors per read
-constexpr uint32_t VOTE_WSM = 128;                 // warp-per-read shared-memory path
+constexpr uint32_t VOTE_WSM = 128;                 // warp-per-read shared-memory path (8 warps per CTA)
+constexpr uint32_t VOTE_WSM2 = 512;                // ... larger slices (4 warps per CTA)
 constexpr uint32_t VOTE_MID = 2048;                // CTA-per-read shared-memory path
 constexpr int VOTE_NT = 256;
 constexpr unsigned FULL = 0xffffffffu;
@@ -202,9 +204,9 @@ __global__ void k_vote_classify(const uint64_t* __restrict__ aoff, uint32_t n_re
       slots[r] = n == 0 ? 0 : (mp && n > mp ? mp : n);
     }
     if (n >= VOTE_IDX_MAX) { atomicAdd(bad + 1, 1u); n = 0; }
-    const int c = n == 0 ? -1 : n <= 16 ? 0 : n <= 32 ? 1 : n <= VOTE_WSM ? 2 : n <= VOTE_MID ? 3 : 4;
+    const int c = n == 0 ? -1 : n <= 16 ? 0 : n <= 32 ? 1 : n <= VOTE_WSM ? 2 : n <= VOTE_WSM2 ? 3 : n <= VOTE_MID ? 4 : 5;
 #pragma unroll
-    for (int q = 0; q < 5; q++) {  // one atomic per warp and class
+    for (int q = 0; q < 6; q++) {  // one atomic per warp and class
       const uint32_t m = __ballot_sync(FULL, c == q);
       if (!m) continue;
       const int leader = __ffs(m) - 1;
@@ -214,7 +216,7 @@ __global__ void k_vote_classify(const uint64_t* __restrict__ aoff, uint32_t n_re
       if (c == q) {
         const uint32_t j = base + __popc(m & ((1u << lane) - 1u));
         lists[(uint64_t)q * n_reads + j] = r;
-        if (q == 4) big_off[j] = atomicAdd((unsigned long long*)big_total, (unsigned long long)(n + 2));
+        if (q == 5) big_off[j] = atomicAdd((unsigned long long*)big_total, (unsigned long long)(n + 2));
       }
     }
   }
@@ -335,9 +337,10 @@ __global__ void __launch_bounds__(VOTE_NT) k_vote_warp(VoteArgs A, const uint32_
 
 // ------------------------------------------------------------------ n > 32: a group of NT threads per read
 // NT = 32 (one warp, shared-memory slice) or VOTE_NT (one CTA, shared memory or global scratch).
-// Arrays of a read with n anchors: key[n], canon[n], aux[n] (read_pos, then new-vote flags),
-// chead[n + 1] (cluster heads), cv[n] (votes), crank[n] (output rank or ~0); ctr[4] (clusters,
-// winners, bad).
+// Arrays of a read with n anchors: key[n], canon[n] (until the new-vote flags are set; its bytes
+// then hold chead[n + 1] (cluster heads) and cv[n] (votes)), aux[n] (read_pos, then new-vote flags,
+// then their prefix), crank[n] (run heads, then cluster-head flags, then the winner list); ctr[4]
+// (clusters, winners, bad, new votes).
 struct GroupArrays {
   uint64_t* key;
   uint64_t* canon;
@@ -448,13 +451,13 @@ __device__ void vote_group(const VoteArgs& A, uint32_t r, const GroupArrays& S, 
   }
   gsync<NT>();
   // head of each run of equal read_pos (one read minimizer): segmented max-scan of head indices
-  group_head_scan<NT>(n, S.aux, S.cv, ws, t);
+  group_head_scan<NT>(n, S.aux, S.crank, ws, t);
   gsync<NT>();
   // keys; a non-head takes its head's canonical k-mer (heads are not written in this phase)
   bool bad = false;
   for (uint32_t i = t; i < n; i += NT) {
     const god_anchor an = A.an[a0 + i];
-    const uint32_t j = S.cv[i];
+    const uint32_t j = S.crank[i];
     uint64_t c = 0;
     if (an.read_pos < L && is_included(A.pat, an.read_pos, ph)) c = S.canon[j];
     if (j != i) S.canon[i] = c;
@@ -613,27 +616,30 @@ __device__ void vote_group(const VoteArgs& A, uint32_t r, const GroupArrays& S, 
   if (t == 0) A.cnt[r] = limit;
 }
 
+// Layout (24 B per anchor): key | canon, whose bytes chead / cv reuse once the new-vote flags are
+// set (canon is not read after that) | aux | crank.
 __device__ __forceinline__ GroupArrays carve(unsigned char* base, uint32_t cap, uint32_t* ctr) {
   GroupArrays S;
   S.key = reinterpret_cast<uint64_t*>(base);
   S.canon = S.key + cap;
-  S.aux = reinterpret_cast<uint32_t*>(S.canon + cap);
-  S.chead = S.aux + cap;
-  S.cv = S.chead + cap + 1;
-  S.crank = S.cv + cap;
+  S.chead = reinterpret_cast<uint32_t*>(S.canon);      // cap + 1 entries
+  S.cv = S.chead + cap + 1;                             // cap entries (ends 4 B past canon[cap-1])
+  S.aux = reinterpret_cast<uint32_t*>(S.key + 2 * (size_t)cap + 1);
+  S.crank = S.aux + cap;
   S.ctr = ctr;
   return S;
 }
-__host__ __device__ constexpr size_t group_bytes(uint32_t cap) { return (size_t)cap * 32 + 8; }
+__host__ __device__ constexpr size_t group_bytes(uint32_t cap) { return (size_t)cap * 24 + 16; }
 
-// 32 < n <= VOTE_WSM: one warp per read, 8 warps per CTA, a shared-memory slice each
-__global__ void __launch_bounds__(VOTE_NT) k_vote_wsm(VoteArgs A, const uint32_t* __restrict__ list, uint32_t nlist) {
+// 32 < n <= CAP: one warp per read, WPB warps per CTA, a shared-memory slice each
+template <uint32_t CAP, int WPB>
+__global__ void __launch_bounds__(WPB * 32) k_vote_wsm(VoteArgs A, const uint32_t* __restrict__ list, uint32_t nlist) {
   extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ uint32_t ctr[VOTE_NT / 32][4];
+  __shared__ uint32_t ctr[WPB][4];
   const int warp = threadIdx.x >> 5;
-  const uint32_t wid = blockIdx.x * (VOTE_NT / 32) + warp;
+  const uint32_t wid = blockIdx.x * WPB + warp;
   if (wid >= nlist) return;  // warp-uniform
-  const GroupArrays S = carve(smem + warp * group_bytes(VOTE_WSM), VOTE_WSM, ctr[warp]);
+  const GroupArrays S = carve(smem + warp * group_bytes(CAP), CAP, ctr[warp]);
   vote_group<32>(A, list[wid], S, nullptr, threadIdx.x & 31);
 }
 
@@ -673,8 +679,8 @@ uint64_t vote_reads(const god_index* ix, const uint8_t* reads, const uint64_t* r
                     god_vote* out, uint64_t* out_off, uint64_t cap, cudaStream_t st) {
   Scratch scr(st);
   uint64_t* slot_off = scr.alloc<uint64_t>((size_t)n_reads + 1);
-  uint32_t* lists = scr.alloc<uint32_t>(5ull * n_reads + 1);
-  uint32_t* ctr = scr.alloc<uint32_t>(8);        // nlist[5], bad[2]
+  uint32_t* lists = scr.alloc<uint32_t>(6ull * n_reads + 1);
+  uint32_t* ctr = scr.alloc<uint32_t>(8);        // nlist[6], bad[2]
   uint64_t* big_total = scr.alloc<uint64_t>(1);
   uint64_t* big_off = scr.alloc<uint64_t>((size_t)n_reads + 1);
   uint32_t* cnt = scr.alloc<uint32_t>((size_t)n_reads + 1);
@@ -685,7 +691,7 @@ uint64_t vote_reads(const god_index* ix, const uint8_t* reads, const uint64_t* r
   const int nsm = num_sms();
   if (n_reads)
     GOD_LAUNCH("k_vote_classify", k_vote_classify, std::min<unsigned>(grid_for(n_reads, 256), nsm * 8u), 256, 0, st,
-               aoff, n_reads, vp.max_pairs, slot_off, lists, ctr, big_off, big_total, ctr + 5);
+               aoff, n_reads, vp.max_pairs, slot_off, lists, ctr, big_off, big_total, ctr + 6);
   scan_exclusive_u64(slot_off, slot_off, (uint64_t)n_reads + 1, nullptr, st, scr, "scan_vote_slots");
   uint32_t h[8];
   GOD_CUDA(cudaMemcpyAsync(h, ctr, sizeof(h), cudaMemcpyDeviceToHost, st));
@@ -693,7 +699,7 @@ uint64_t vote_reads(const god_index* ix, const uint8_t* reads, const uint64_t* r
   GOD_CUDA(cudaMemcpyAsync(&hb[0], slot_off + n_reads, 8, cudaMemcpyDeviceToHost, st));
   GOD_CUDA(cudaMemcpyAsync(&hb[1], big_total, 8, cudaMemcpyDeviceToHost, st));
   GOD_CUDA(cudaStreamSynchronize(st));
-  GOD_REQUIRE(h[6] == 0, "a read has >= 2^29 anchors");
+  GOD_REQUIRE(h[7] == 0, "a read has >= 2^29 anchors");
   god_vote* res = scr.alloc<god_vote>(hb[0] ? hb[0] : 1);
   VoteArgs A;
   A.reads = reads;
@@ -709,11 +715,15 @@ uint64_t vote_reads(const god_index* ix, const uint8_t* reads, const uint64_t* r
   A.slot_off = slot_off;
   A.res = res;
   A.cnt = cnt;
-  A.bad = ctr + 5;
+  A.bad = ctr + 6;
   static bool attr = false;
-  const size_t sm_wsm = (VOTE_NT / 32) * group_bytes(VOTE_WSM), sm_mid = group_bytes(VOTE_MID);
+  constexpr int WPB1 = 8, WPB2 = 4;
+  const size_t sm_wsm = WPB1 * group_bytes(VOTE_WSM), sm_wsm2 = WPB2 * group_bytes(VOTE_WSM2),
+               sm_mid = group_bytes(VOTE_MID);
   if (!attr) {
-    GOD_CUDA(cudaFuncSetAttribute(k_vote_wsm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_wsm));
+    GOD_CUDA(cudaFuncSetAttribute(k_vote_wsm<VOTE_WSM, WPB1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_wsm));
+    GOD_CUDA(cudaFuncSetAttribute(k_vote_wsm<VOTE_WSM2, WPB2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)sm_wsm2));
     GOD_CUDA(cudaFuncSetAttribute(k_vote_mid, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_mid));
     attr = true;
   }
@@ -723,17 +733,20 @@ uint64_t vote_reads(const god_index* ix, const uint8_t* reads, const uint64_t* r
     GOD_LAUNCH("k_vote_warp", k_vote_warp<32>, grid_for((uint64_t)h[1] * 32, VOTE_NT), VOTE_NT, 0, st, A,
                lists + n_reads, h[1]);
   if (h[2])
-    GOD_LAUNCH("k_vote_wsm", k_vote_wsm, grid_for(h[2], VOTE_NT / 32), VOTE_NT, sm_wsm, st, A, lists + 2ull * n_reads,
-               h[2]);
-  if (h[3]) GOD_LAUNCH("k_vote_mid", k_vote_mid, h[3], VOTE_NT, sm_mid, st, A, lists + 3ull * n_reads);
-  if (h[4]) {
+    GOD_LAUNCH("k_vote_wsm", (k_vote_wsm<VOTE_WSM, WPB1>), grid_for(h[2], WPB1), WPB1 * 32, sm_wsm, st, A,
+               lists + 2ull * n_reads, h[2]);
+  if (h[3])
+    GOD_LAUNCH("k_vote_wsm2", (k_vote_wsm<VOTE_WSM2, WPB2>), grid_for(h[3], WPB2), WPB2 * 32, sm_wsm2, st, A,
+               lists + 3ull * n_reads, h[3]);
+  if (h[4]) GOD_LAUNCH("k_vote_mid", k_vote_mid, h[4], VOTE_NT, sm_mid, st, A, lists + 4ull * n_reads);
+  if (h[5]) {
     unsigned char* gs = scr.alloc<unsigned char>(hb[1] * 32 + 64);
-    GOD_LAUNCH("k_vote_big", k_vote_big, h[4], VOTE_NT, 0, st, A, lists + 4ull * n_reads, big_off, gs);
+    GOD_LAUNCH("k_vote_big", k_vote_big, h[5], VOTE_NT, 0, st, A, lists + 5ull * n_reads, big_off, gs);
   }
   scan_exclusive_u32_to_u64(cnt, out_off, (uint64_t)n_reads + 1, nullptr, st, scr, "scan_vote_out");
   uint32_t nbad = 0;
   uint64_t tot = 0;
-  GOD_CUDA(cudaMemcpyAsync(&nbad, ctr + 5, 4, cudaMemcpyDeviceToHost, st));
+  GOD_CUDA(cudaMemcpyAsync(&nbad, ctr + 6, 4, cudaMemcpyDeviceToHost, st));
   GOD_CUDA(cudaMemcpyAsync(&tot, out_off + n_reads, 8, cudaMemcpyDeviceToHost, st));
   GOD_CUDA(cudaStreamSynchronize(st));
   GOD_REQUIRE(nbad == 0, "anchors inconsistent with the reads' phases (read_pos not an included position)");
