@@ -68,6 +68,11 @@ def _load():
     L.or_vote_read.argtypes = [vp, vp, u64, u32, u32, u32, u32, u32, vp, u64]; L.or_vote_read.restype = ctypes.c_int64
     L.or_vote_reads_batch.argtypes = [vp, vp, vp, u32, vp, u32, u32, u32, vp, u64, vp]
     L.or_vote_reads_batch.restype = ctypes.c_int64
+    L.or_harness_seeds.argtypes = [vp, u64, i32, i32, i32, ctypes.c_char_p, u32, vp, u64]
+    L.or_harness_seeds.restype = ctypes.c_int64
+    L.or_levenshtein.argtypes = [vp, u64, vp, u64]; L.or_levenshtein.restype = ctypes.c_int64
+    L.or_harness_pair.argtypes = [vp, vp, u64, i32, i32, ctypes.c_char_p, vp, vp, vp]
+    L.or_harness_pair.restype = ctypes.c_int64
     L.or_contain.argtypes = [vp, vp, u32, ctypes.c_char_p, i32, i32, u32, u32, ctypes.c_int64, vp, vp, u32, u32, u32,
                              u32, u32, u64, u32, u32, u32, vp, vp, vp]
     L.or_contain.restype = i32
@@ -190,6 +195,66 @@ def contain(refs, ref_offsets, reads, read_offsets, pattern: str, k: int, w: int
     if rc:
         raise ValueError("invalid containment parameters")
     return mr, mb, acc
+
+
+ALGOS = ("all", "minimizers", "spaced", "god")
+
+
+def harness_seeds(seq, algo: int, k: int, w: int, pattern: str, s: int = 0) -> np.ndarray:
+    """Seed hashes of one sequence (algo 0 all, 1 minimizers, 2 spaced, 3 Genome-on-Diet phase s)."""
+    seq = _u8(seq)
+    L = _load()
+    n = L.or_harness_seeds(_p(seq), seq.size, algo, k, w, pattern.encode(), s, None, 0)
+    if n < 0:
+        raise ValueError("invalid harness parameters")
+    out = np.zeros(n, np.uint64)
+    L.or_harness_seeds(_p(seq), seq.size, algo, k, w, pattern.encode(), s, _p(out), n)
+    return out
+
+
+def levenshtein(a, b) -> int:
+    a, b = _u8(a), _u8(b)
+    return int(_load().or_levenshtein(_p(a), a.size, _p(b), b.size))
+
+
+def harness_pairs(orig, mut, offsets, k: int, w: int, pattern: str):
+    """Seed-comparison harness over CSR pairs (orig[i], mut[i] share offsets).
+    -> (edit u64[n], matches u64[n, 4], totals u64[n, 4], god_phase u32[n]); algos in ALGOS order."""
+    orig, mut = _u8(orig), _u8(mut)
+    off = np.ascontiguousarray(offsets, dtype=np.uint64)
+    n = off.size - 1
+    ed = np.zeros(n, np.uint64)
+    m = np.zeros((n, 4), np.uint64)
+    t = np.zeros((n, 4), np.uint64)
+    ph = np.zeros(n, np.uint32)
+    L = _load()
+    for i in range(n):
+        a, b = int(off[i]), int(off[i + 1])
+        mi, ti, pi = np.zeros(4, np.uint64), np.zeros(4, np.uint64), np.zeros(1, np.uint32)
+        d = L.or_harness_pair(_p(orig[a:b]) if b > a else ctypes.c_void_p(0), _p(mut[a:b]) if b > a else ctypes.c_void_p(0),
+                              b - a, k, w, pattern.encode(), _p(mi), _p(ti), _p(pi))
+        if d < 0:
+            raise ValueError("invalid harness parameters")
+        ed[i], m[i], t[i], ph[i] = d, mi, ti, pi[0]
+    return ed, m, t, ph
+
+
+def accepted_pairs(ed, m, t, E: int) -> np.ndarray:
+    """the rate threshold of an edit-distance threshold E is the minimum seed matching rate of
+    the pairs with edit distance <= E; a pair is accepted iff its rate >= that threshold.  Pairs
+    without seeds (total 0) have no rate and are never accepted.  -> accepted count per algorithm."""
+    out = np.zeros(m.shape[1], np.int64)
+    for a in range(m.shape[1]):
+        rated = [i for i in range(len(ed)) if t[i, a] > 0]
+        cand = [i for i in rated if ed[i] <= E]
+        if not cand:
+            continue
+        j = cand[0]
+        for i in cand[1:]:  # minimum rate m/t, exact (cross-multiplication)
+            if int(m[i, a]) * int(t[j, a]) < int(m[j, a]) * int(t[i, a]):
+                j = i
+        out[a] = sum(1 for i in rated if int(m[i, a]) * int(t[j, a]) >= int(m[j, a]) * int(t[i, a]))
+    return out
 
 
 class Index:

@@ -596,3 +596,137 @@ int or_contain(const uint8_t* refs, const uint64_t* ref_offsets, uint32_t n_refs
     }
     return 0;
 }
+
+/* ------------------------------------------------------------------------------------------ */
+/* Seed-comparison harness (section 2.1.1-2.1.2).  Readings (DESIGN.md §2,
+ * S1-S5):
+ *  S2 a seed is the hash H of a canonical (multi-)k-mer; four extractors over a sequence:
+ *     algo 0 "All Seeds": every k-mer start without N: H_k(canon);
+ *     algo 1 "Minimizers": O6 with pattern '1', phase 0;
+ *     algo 2 "Spaced": per window start i, the bases i + j for the ones of the mask
+ *            M[j] = P[j mod p], j < k (span k, weight x_k = ones of M: "spaced seeds", the
+ *            literature patterns are given with span = seed length); canonical over the included
+ *            bases, hash H_{x_k};
+ *     algo 3 "Genome-on-Diet": O6 on Sparsify(seq, P, s) (the original with s = 0).
+ *  S3 rate = matches / total: total = seeds (occurrences) of the mutated sequence, matches = those
+ *     whose hash is among the original's seeds ("ratio of the number of matching seeds ... to
+ *     the total number of extracted seeds").  Genome-on-Diet scores the mutated sequence in every
+ *     phase s < p against the original's phase 0 and keeps the best rate (smallest s on ties).
+ *  S4 edit distance = Levenshtein, unit costs ("outputs the Levenshtein distance").  */
+int64_t or_harness_seeds(const uint8_t* seq, uint64_t L, int algo, int k, int w, const char* pattern, uint32_t s,
+                         uint64_t* out, uint64_t cap) {
+    or_pattern P;
+    if (or_parse_pattern(pattern, &P)) return -1;
+    if (k < 1 || k > 28 || w < 1) return -1;
+    int64_t n = 0;
+    if (algo == 0) {
+        for (uint64_t i = 0; i + (uint64_t)k <= L; i++) {
+            uint64_t fwd = 0, rev = 0; int ok = 1;
+            for (int j = 0; j < k; j++) {
+                int c = or_code(seq[i + j]);
+                if (c == OR_N) { ok = 0; break; }
+                fwd = fwd * 4 + (uint64_t)c;
+            }
+            if (!ok) continue;
+            for (int j = 0; j < k; j++) rev = rev * 4 + (uint64_t)(3 - or_code(seq[i + k - 1 - j]));
+            uint64_t h = or_hash(fwd < rev ? fwd : rev, k);
+            if (out && (uint64_t)n < cap) out[n] = h;
+            n++;
+        }
+    } else if (algo == 1 || algo == 3) {
+        or_pattern Q;
+        if (algo == 1) or_parse_pattern("1", &Q); else Q = P;
+        if (s >= Q.p) return -1;
+        int64_t c = or_minimizers(seq, L, &Q, s, k, w, 0, NULL, 0);
+        or_mz* M = (or_mz*)malloc(sizeof(or_mz) * (size_t)(c ? c : 1));
+        or_minimizers(seq, L, &Q, s, k, w, 0, M, (uint64_t)c);
+        for (int64_t i = 0; i < c; i++) { if (out && (uint64_t)n < cap) out[n] = M[i].hash; n++; }
+        free(M);
+    } else if (algo == 2) {
+        int x = 0;
+        for (int j = 0; j < k; j++) x += P.bit[j % P.p];
+        if (x == 0 || x > 28) return x == 0 ? 0 : -1;
+        for (uint64_t i = 0; i + (uint64_t)k <= L; i++) {
+            uint8_t inc[28]; int ni = 0, ok = 1;
+            for (int j = 0; j < k; j++) {
+                if (!P.bit[j % P.p]) continue;
+                int c = or_code(seq[i + j]);
+                if (c == OR_N) { ok = 0; break; }
+                inc[ni++] = (uint8_t)c;
+            }
+            if (!ok) continue;
+            uint64_t fwd = 0, rev = 0;
+            for (int j = 0; j < x; j++) fwd = fwd * 4 + inc[j];
+            for (int j = 0; j < x; j++) rev = rev * 4 + (uint64_t)(3 - inc[x - 1 - j]);
+            uint64_t h = or_hash(fwd < rev ? fwd : rev, x);
+            if (out && (uint64_t)n < cap) out[n] = h;
+            n++;
+        }
+    } else {
+        return -1;
+    }
+    return n;
+}
+
+/* S3: matches of b's seeds among a's (set membership by linear scan of a's sorted seeds) */
+static void rate_of(const uint64_t* sa, int64_t na, const uint64_t* sb, int64_t nb, uint64_t* m, uint64_t* t) {
+    uint64_t mm = 0;
+    for (int64_t i = 0; i < nb; i++) {
+        int found = 0;
+        for (int64_t j = 0; j < na && !found; j++) found = sa[j] == sb[i];
+        mm += (uint64_t)found;
+    }
+    *m = mm; *t = (uint64_t)nb;
+}
+
+/* S4: textbook dynamic programming, unit costs */
+int64_t or_levenshtein(const uint8_t* a, uint64_t la, const uint8_t* b, uint64_t lb) {
+    uint64_t* prev = (uint64_t*)malloc(sizeof(uint64_t) * (lb + 1));
+    uint64_t* cur = (uint64_t*)malloc(sizeof(uint64_t) * (lb + 1));
+    for (uint64_t j = 0; j <= lb; j++) prev[j] = j;
+    for (uint64_t i = 1; i <= la; i++) {
+        cur[0] = i;
+        for (uint64_t j = 1; j <= lb; j++) {
+            uint64_t del = prev[j] + 1, ins = cur[j - 1] + 1, sub = prev[j - 1] + (a[i - 1] != b[j - 1]);
+            uint64_t v = del < ins ? del : ins;
+            cur[j] = v < sub ? v : sub;
+        }
+        uint64_t* t = prev; prev = cur; cur = t;
+    }
+    int64_t d = (int64_t)prev[lb];
+    free(prev); free(cur);
+    return d;
+}
+
+/* One pair: edit distance and (matches, total) for the four extractors (out_m[4], out_t[4]); the
+ * Genome-on-Diet phase kept is written to *god_phase.  Returns the edit distance (-1 on error). */
+int64_t or_harness_pair(const uint8_t* a, const uint8_t* b, uint64_t L, int k, int w, const char* pattern,
+                        uint64_t* out_m, uint64_t* out_t, uint32_t* god_phase) {
+    or_pattern P;
+    if (or_parse_pattern(pattern, &P)) return -1;
+    uint64_t* sa = (uint64_t*)malloc(sizeof(uint64_t) * (L + 1));
+    uint64_t* sb = (uint64_t*)malloc(sizeof(uint64_t) * (L + 1));
+    for (int algo = 0; algo < 4; algo++) {
+        int64_t na = or_harness_seeds(a, L, algo, k, w, pattern, 0, sa, L + 1);
+        if (na < 0) { free(sa); free(sb); return -1; }
+        if (algo < 3) {
+            int64_t nb = or_harness_seeds(b, L, algo, k, w, pattern, 0, sb, L + 1);
+            rate_of(sa, na, sb, nb, &out_m[algo], &out_t[algo]);
+        } else {
+            /* the best rate m/t over the phases; a phase without seeds has no rate; ties -> smaller s */
+            uint64_t bm = 0, bt = 0; uint32_t bs = 0;
+            for (uint32_t s = 0; s < P.p; s++) {
+                int64_t nb = or_harness_seeds(b, L, 3, k, w, pattern, s, sb, L + 1);
+                uint64_t m, t;
+                rate_of(sa, na, sb, nb, &m, &t);
+                if (t > 0 && (bt == 0 || (unsigned __int128)m * bt > (unsigned __int128)bm * t)) {
+                    bm = m; bt = t; bs = s;
+                }
+            }
+            out_m[3] = bm; out_t[3] = bt;
+            if (god_phase) *god_phase = bs;
+        }
+    }
+    free(sa); free(sb);
+    return or_levenshtein(a, L, b, L);
+}

@@ -119,6 +119,14 @@ int or_contain(const uint8_t* refs, const uint64_t* ref_offsets, uint32_t n_refs
                uint32_t max_pairs, uint64_t batch_bases, uint32_t min_reads, uint32_t cov_num, uint32_t cov_den,
                uint64_t* mapped_reads, uint64_t* mapped_bases, uint8_t* accepted);
 
+/* Seed-comparison harness (readings S1-S4 in oracle.c).  algo 0 all k-mers, 1 minimizers,
+ * 2 spaced seeds, 3 Genome-on-Diet (phase s).  Seeds = hashes, in extraction order. */
+int64_t or_harness_seeds(const uint8_t* seq, uint64_t L, int algo, int k, int w, const char* pattern, uint32_t s,
+                         uint64_t* out, uint64_t cap);
+int64_t or_levenshtein(const uint8_t* a, uint64_t la, const uint8_t* b, uint64_t lb);
+int64_t or_harness_pair(const uint8_t* a, const uint8_t* b, uint64_t L, int k, int w, const char* pattern,
+                        uint64_t* out_m, uint64_t* out_t, uint32_t* god_phase);
+
 #ifdef __cplusplus
 }
 #endif

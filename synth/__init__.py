@@ -227,3 +227,21 @@ def concat(seqs) -> tuple:
     np.cumsum(lens, out=offs[1:])
     cat = np.concatenate([np.asarray(s, dtype=np.uint8) for s in seqs]) if len(seqs) else np.zeros(0, np.uint8)
     return np.ascontiguousarray(cat), offs
+
+
+def mutation_pairs(n: int, length: int, max_subs: int, seed: int):
+    """Seed-comparison inputs: n random ACGT sequences of `length` bases and, for each, a copy
+    with a uniform number in [0, max_subs] of substitutions at distinct uniform positions, each to
+    one of the three other bases.  -> (orig u8, mutated u8, offsets u64[n+1], n_subs u32[n])"""
+    rng = np.random.default_rng(seed)
+    orig = np.frombuffer(b"ACGT", np.uint8)[rng.integers(0, 4, size=n * length)].copy()
+    mut = orig.copy()
+    subs = rng.integers(0, max_subs + 1, size=n).astype(np.uint32)
+    lut = {ord("A"): 0, ord("C"): 1, ord("G"): 2, ord("T"): 3}
+    for i in range(n):
+        pos = rng.choice(length, size=int(subs[i]), replace=False)
+        for q in pos:
+            c = lut[int(mut[i * length + q])]
+            mut[i * length + q] = b"ACGT"[(c + int(rng.integers(1, 4))) % 4]
+    offsets = (np.arange(n + 1, dtype=np.uint64) * length).astype(np.uint64)
+    return orig, mut, offsets, subs
