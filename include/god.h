@@ -215,6 +215,32 @@ GOD_API god_status god_contain(const god_params* prm, const uint8_t* refs, const
                                const god_vote_params* vp, const god_contain_params* cp, uint64_t* mapped_reads,
                                uint64_t* mapped_bases, uint8_t* accepted, god_stream stream);
 
+/* ---- seed-comparison harness (section 2.1.1-2.1.2, Fig. 4) ----
+ * For pair i, sequences orig[offsets[i] .. offsets[i+1]) and mut[same range] (equal lengths,
+ * <= 4096 bases), with prm's pattern P, k and w:
+ *  matches[4i + a], totals[4i + a]: the seed matching rate matches/totals of extractor a (P:87:
+ *    "the ratio of the number of matching seeds ... to the total number of extracted seeds"):
+ *    totals = seed occurrences of the mutated sequence, matches = those whose hash is among the
+ *    original's seeds.  a = 0 "All Seeds": every N-free k-mer, H_k(canonical); 1 "Minimizers":
+ *    (w,k)-minimizers (pattern '1'); 2 "Spaced": per window start the bases at offsets j < k with
+ *    P[j mod p] = 1, H over the included bases (canonical); 3 "Genome-on-Diet": minimizers of the
+ *    patterned sequence, the original in phase 0, the mutated one in the phase s < p with the best
+ *    rate (god_phase[i]; a phase without seeds has no rate; ties -> smaller s).
+ *  edit[i]: Levenshtein distance of the pair, unit costs, bytes compared exactly.
+ * Readings S1-S5: DESIGN.md §2.  GOD_EINVAL: a pair longer than 4096 bases, or a spaced mask of
+ * weight > 28.  Synchronizes. */
+GOD_API god_status god_seed_harness(const god_params* prm, const uint8_t* orig, const uint8_t* mut,
+                                    const uint64_t* offsets, uint32_t n_pairs, uint64_t* edit, uint64_t* matches,
+                                    uint64_t* totals, uint32_t* god_phase, god_stream stream);
+
+/* Accepted pairs (reading S5) for n_thresholds edit-distance thresholds E[e]: the rate
+ * threshold is the minimum rate matches/totals over the pairs with edit <= E[e]; accepted[4e + a] =
+ * pairs of extractor a whose rate >= that threshold (pairs with totals 0 have no rate; no rated pair
+ * within E -> 0).  Inputs as written by god_seed_harness.  Synchronizes. */
+GOD_API god_status god_harness_accepted(const uint64_t* edit, const uint64_t* matches, const uint64_t* totals,
+                                        uint32_t n_pairs, const uint64_t* thresholds, uint32_t n_thresholds,
+                                        uint64_t* accepted, god_stream stream);
+
 /* ---- tracing: per-kernel device time by CUDA events on the launching stream ----
  * Off by default.  When on, every kernel launch is bracketed by two events; god_profile_query
  * synchronizes on the pending events and returns, per kernel name (in first-launch order), the

@@ -304,6 +304,40 @@ def god_contain(refs, ref_offsets, reads, read_offsets, pattern: str, k: int, w:
     return mr[:n], mb[:n], acc[:n]
 
 
+def god_seed_harness(orig, mut, offsets, pattern: str, k: int, w: int):
+    """Seed-comparison harness: per pair the edit distance and, for the four extractors
+    (all k-mers, minimizers, spaced seeds, Genome-on-Diet), the seed matching rate as
+    (matches, totals).  -> (edit u64[n], matches u64[n, 4], totals u64[n, 4], god_phase u32[n])"""
+    L = _lib.load()
+    dev = _is_cuda(orig)
+    orig, mut, offsets = _prep(orig, np.uint8), _prep(mut, np.uint8), _prep(offsets, np.uint64)
+    n = int(offsets.shape[0]) - 1
+    dv = orig.device if dev else None
+    ed = _empty(max(1, n), np.uint64, dev, dv)
+    mm = _empty(max(1, 4 * n), np.uint64, dev, dv)
+    tt = _empty(max(1, 4 * n), np.uint64, dev, dv)
+    ph = _empty(max(1, n), np.uint32, dev, dv)
+    prm = _params(pattern, k, w)
+    _lib.check(L.god_seed_harness(ctypes.byref(prm), _ptr(orig), _ptr(mut), _ptr(offsets), n, _ptr(ed), _ptr(mm),
+                                  _ptr(tt), _ptr(ph), _stream(dev)))
+    return ed[:n], mm[:4 * n].reshape(n, 4), tt[:4 * n].reshape(n, 4), ph[:n]
+
+
+def god_harness_accepted(edit, matches, totals, thresholds):
+    """Accepted sequence pairs per edit-distance threshold and extractor.
+    -> u64[len(thresholds), 4]"""
+    L = _lib.load()
+    dev = _is_cuda(edit)
+    edit, thresholds = _prep(edit, np.uint64), _prep(thresholds, np.uint64)
+    matches = matches.contiguous() if dev else np.ascontiguousarray(matches, dtype=np.uint64)
+    totals = totals.contiguous() if dev else np.ascontiguousarray(totals, dtype=np.uint64)
+    n, ne = int(edit.shape[0]), int(thresholds.shape[0])
+    out = _empty(max(1, 4 * ne), np.uint64, dev, edit.device if dev else None)
+    _lib.check(L.god_harness_accepted(_ptr(edit), _ptr(matches), _ptr(totals), n, _ptr(thresholds), ne, _ptr(out),
+                                      _stream(dev)))
+    return out[:4 * ne].reshape(ne, 4)
+
+
 def votes_numpy(votes) -> np.ndarray:
     """(n, 10) u32 device/host array in god_vote layout -> VOTE_DTYPE numpy records."""
     if _is_cuda(votes):
@@ -344,5 +378,6 @@ def launch_count() -> int:
 
 
 __all__ = ["god_sparsify", "god_minimizers", "god_build_index", "god_seed_reads", "god_vote_reads", "votes_numpy",
-           "god_contain",
+           "god_contain", "god_seed_harness",
+           "god_harness_accepted",
            "GodIndex", "GodError", "ANCHOR_DTYPE", "VOTE_DTYPE", "version"]

@@ -44,7 +44,8 @@ class GodIndexStats(ctypes.Structure):
 # every symbol include/god.h declares (tests/test_abi.py checks header <-> library agreement)
 EXPORTS = ("god_last_error", "god_version", "god_sparsify", "god_minimizers", "god_build_index",
            "god_index_get_stats", "god_index_dump", "god_index_count", "god_index_free", "god_seed_reads",
-           "god_vote_reads", "god_contain",
+           "god_vote_reads", "god_contain", "god_seed_harness",
+           "god_harness_accepted",
            "god_profile_enable", "god_profile_reset", "god_profile_query", "god_launch_count",
            "god_profile_units")
 
@@ -75,6 +76,8 @@ def load():
     L.god_vote_reads.argtypes = [vp, vp, vp, u32, vp, vp, vp, P(GodVoteParams), vp, vp, u64, P(ctypes.c_uint64), vp]
     L.god_contain.argtypes = [P(GodParams), vp, vp, u32, P(GodCutoff), vp, vp, u32, u32, P(GodVoteParams),
                               P(GodContainParams), vp, vp, vp, vp]
+    L.god_seed_harness.argtypes = [P(GodParams), vp, vp, vp, u32, vp, vp, vp, vp, vp]
+    L.god_harness_accepted.argtypes = [vp, vp, vp, u32, vp, u32, vp, vp]
     L.god_profile_enable.argtypes = [ctypes.c_int]
     L.god_profile_enable.restype = None
     L.god_profile_reset.argtypes = []

@@ -643,4 +643,57 @@ GOD_API god_status god_contain(const god_params* prm, const uint8_t* refs, const
   });
 }
 
+GOD_API god_status god_seed_harness(const god_params* prm, const uint8_t* orig, const uint8_t* mut,
+                                    const uint64_t* offsets, uint32_t n_pairs, uint64_t* edit, uint64_t* matches,
+                                    uint64_t* totals, uint32_t* god_phase, god_stream stream) {
+  return guarded([&] {
+    const Params P = make_params(prm);
+    GOD_REQUIRE(offsets && (n_pairs == 0 || (orig && mut && edit && matches && totals && god_phase)), "NULL argument");
+    uint32_t x = 0;
+    for (int j = 0; j < P.k; j++) x += (uint32_t)((P.pat.bits >> (j % P.pat.p)) & 1ull);
+    GOD_REQUIRE(x <= 28, "spaced mask weight must be <= 28");
+    cudaStream_t st = (cudaStream_t)stream;
+    std::vector<uint64_t> hoff((size_t)n_pairs + 1);
+    if (is_device_ptr(offsets))
+      GOD_CUDA(cudaMemcpyAsync(hoff.data(), offsets, hoff.size() * 8, cudaMemcpyDeviceToHost, st));
+    else
+      memcpy(hoff.data(), offsets, hoff.size() * 8);
+    GOD_CUDA(cudaStreamSynchronize(st));
+    for (uint32_t i = 0; i < n_pairs; i++)
+      GOD_REQUIRE(hoff[i] <= hoff[i + 1] && hoff[i + 1] - hoff[i] <= god::harness_max_len(),
+                  "pairs must be <= 4096 bases (and offsets ascending)");
+    Scratch scr(st);
+    Stage sg(st, scr);
+    const uint64_t L = hoff[n_pairs];
+    const uint8_t* da = sg.in(orig, L);
+    const uint8_t* db = sg.in(mut, L);
+    const uint64_t* doff = sg.in(offsets, (size_t)n_pairs + 1);
+    uint64_t* de = sg.out(edit, n_pairs);
+    uint64_t* dm = sg.out(matches, 4ull * n_pairs);
+    uint64_t* dt = sg.out(totals, 4ull * n_pairs);
+    uint32_t* dp = sg.out(god_phase, n_pairs);
+    god::seed_harness(P, da, db, doff, n_pairs, de, dm, dt, dp, st);
+    sg.finish();
+  });
+}
+
+GOD_API god_status god_harness_accepted(const uint64_t* edit, const uint64_t* matches, const uint64_t* totals,
+                                        uint32_t n_pairs, const uint64_t* thresholds, uint32_t n_thresholds,
+                                        uint64_t* accepted, god_stream stream) {
+  return guarded([&] {
+    GOD_REQUIRE(n_thresholds == 0 || (thresholds && accepted), "NULL argument");
+    GOD_REQUIRE(n_pairs == 0 || (edit && matches && totals), "NULL argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    Scratch scr(st);
+    Stage sg(st, scr);
+    const uint64_t* de = sg.in(edit, n_pairs);
+    const uint64_t* dm = sg.in(matches, 4ull * n_pairs);
+    const uint64_t* dt = sg.in(totals, 4ull * n_pairs);
+    const uint64_t* dE = sg.in(thresholds, n_thresholds);
+    uint64_t* da = sg.out(accepted, 4ull * n_thresholds);
+    god::harness_accepted(de, dm, dt, n_pairs, dE, n_thresholds, da, st);
+    sg.finish();
+  });
+}
+
 }  // extern "C"

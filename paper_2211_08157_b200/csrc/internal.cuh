@@ -166,6 +166,12 @@ void contain(const Params& P, const uint8_t* refs, const uint64_t* ref_off, cons
              uint32_t n_refs, const god_cutoff& cut, const uint8_t* reads, const uint64_t* roff, uint32_t n_reads,
              uint32_t t, const god_vote_params& vp, uint64_t batch_bases, uint32_t min_reads, uint32_t cov_num,
              uint32_t cov_den, uint64_t* mreads, uint64_t* mbases, uint8_t* accepted, cudaStream_t st);
+// seed-comparison harness (harness.cu); pairs of <= harness_max_len() bases
+void seed_harness(const Params& P, const uint8_t* a, const uint8_t* b, const uint64_t* off, uint32_t n,
+                  uint64_t* ed, uint64_t* matches, uint64_t* totals, uint32_t* god_phase, cudaStream_t st);
+uint32_t harness_max_len();
+void harness_accepted(const uint64_t* ed, const uint64_t* mm, const uint64_t* tt, uint32_t n, const uint64_t* E,
+                      uint32_t nE, uint64_t* acc, cudaStream_t st);
 void sparsify(const Params& P, const uint8_t* seq, const uint64_t* offsets, uint32_t n, const uint8_t* phases,
               uint64_t* packed, uint64_t* nmask, uint64_t* out_offsets, uint64_t* counts, uint64_t cap_words,
               uint64_t* needed_host, cudaStream_t st);
