@@ -201,14 +201,15 @@ def god_build_index(ref, ref_offsets, pattern: str, k: int, w: int, cutoff=(1, 5
 
 # ---------------------------------------------------------------------------------------- stage 4
 def god_seed_reads(index: GodIndex, reads, read_offsets, phases=None, t: int = 16, cap: int | None = None,
-                   out=None):
+                   out=None, host_out: bool = False):
     """SELECT mode if phases is None (phase per read computed), else GIVEN.
     -> (anchors, anchor_offsets u64[n+1], phases u8[n]).  Device path: anchors is a CUDA u32 tensor
     of shape (n_anchors, 4) = (ref_pos, read_pos, read_id, strand); host path: structured numpy.
     out = (anchors, anchor_offsets, phases) preallocated (device path; anchors (cap, 4) u32) avoids
-    per-call allocations in a serving loop."""
+    per-call allocations in a serving loop.  host_out=True with CUDA reads returns host (numpy) outputs:
+    the library then streams the results of read batches back while later batches are seeded."""
     L = _lib.load()
-    dev = _is_cuda(reads)
+    dev = _is_cuda(reads) and not host_out
     reads, read_offsets = _prep(reads, np.uint8), _prep(read_offsets, np.uint64)
     n = int(read_offsets.shape[0]) - 1
     dv = reads.device if dev else None

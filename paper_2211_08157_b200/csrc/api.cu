@@ -252,7 +252,8 @@ void grow(T*& p, uint64_t& cap, uint64_t need, cudaStream_t st) {
 
 static uint64_t seed_reads_pipelined(const god_index* idx, const uint8_t* reads, const uint64_t* offs, uint32_t n_reads,
                                      god_phase_mode mode, uint8_t* phases, uint32_t t, god_anchor* anchors,
-                                     uint64_t* anchor_offsets, uint64_t cap, uint32_t n_batches, cudaStream_t st) {
+                                     uint64_t* anchor_offsets, uint64_t cap, uint32_t n_batches, cudaStream_t st,
+                                     bool reads_on_device) {
   static cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
   if (!s_h2d) {
     GOD_CUDA(cudaStreamCreateWithFlags(&s_h2d, cudaStreamNonBlocking));
@@ -272,17 +273,31 @@ static uint64_t seed_reads_pipelined(const god_index* idx, const uint8_t* reads,
   }
   GOD_CUDA(cudaStreamSynchronize(st));
   auto r_begin = [&](uint32_t b) { return std::min<uint64_t>((uint64_t)b * per, n_reads); };
+  // byte offset of each batch's first read (device-resident offsets: one small copy per batch start)
+  std::vector<uint64_t> boff(n_batches + 1);
+  for (uint32_t b = 0; b <= n_batches; b++) {
+    if (reads_on_device) d2h_small(&boff[b], offs + r_begin(b), 8, st);
+    else boff[b] = offs[r_begin(b)];
+  }
+  GOD_CUDA(cudaStreamSynchronize(st));
+  std::vector<const uint8_t*> breads(n_batches);
   auto upload = [&](uint32_t b) {
     PipeSlot& sl = slot[b & 1];
     const uint64_t r0 = r_begin(b), r1 = r_begin(b + 1), nb = r1 - r0;
-    const uint64_t bytes = offs[r1] - offs[r0];
+    const uint64_t bytes = boff[b + 1] - boff[b];
     // the slot's buffers are free once its previous batch's results have left the device
     if (sl.d2h_pending) GOD_CUDA(cudaStreamWaitEvent(s_h2d, sl.d2h_done, 0));
-    if (sl.reads) GOD_CUDA(cudaStreamWaitEvent(s_h2d, sl.comp_done, 0));  // batch b-2 no longer reads them
-    grow(sl.reads, sl.reads_cap, bytes + 16, s_h2d);
+    if (sl.off) GOD_CUDA(cudaStreamWaitEvent(s_h2d, sl.comp_done, 0));  // batch b-2 no longer reads them
     grow(sl.off, sl.off_cap, nb + 1, s_h2d);
-    if (bytes) GOD_CUDA(cudaMemcpyAsync(sl.reads, reads + offs[r0], bytes, cudaMemcpyHostToDevice, s_h2d));
-    GOD_CUDA(cudaMemcpyAsync(sl.off, offs + r0, (nb + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, s_h2d));
+    if (reads_on_device) {  // the reads stay where they are; only the batch's offsets are copied
+      breads[b] = reads + boff[b];
+      GOD_CUDA(cudaMemcpyAsync(sl.off, offs + r0, (nb + 1) * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s_h2d));
+    } else {
+      grow(sl.reads, sl.reads_cap, bytes + 16, s_h2d);
+      breads[b] = sl.reads;
+      if (bytes) GOD_CUDA(cudaMemcpyAsync(sl.reads, reads + boff[b], bytes, cudaMemcpyHostToDevice, s_h2d));
+      GOD_CUDA(cudaMemcpyAsync(sl.off, offs + r0, (nb + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, s_h2d));
+    }
     if (mode == GOD_PHASE_GIVEN && nb) GOD_CUDA(cudaMemcpyAsync(sl.ph, phases + r0, nb, cudaMemcpyHostToDevice, s_h2d));
     GOD_CUDA(cudaEventRecord(sl.h2d_done, s_h2d));
   };
@@ -292,14 +307,14 @@ static uint64_t seed_reads_pipelined(const god_index* idx, const uint8_t* reads,
     if (b + 1 < n_batches) upload(b + 1);
     const uint64_t r0 = r_begin(b), r1 = r_begin(b + 1), nb = r1 - r0;
     GOD_CUDA(cudaStreamWaitEvent(st, sl.h2d_done, 0));
-    GOD_LAUNCH("k_rebase", k_rebase_u64, grid_for(nb + 1, 256), 256, 0, st, sl.off, nb + 1, offs[r0], 0ull);
+    GOD_LAUNCH("k_rebase", k_rebase_u64, grid_for(nb + 1, 256), 256, 0, st, sl.off, nb + 1, boff[b], 0ull);
     // anchors of this batch: a share of the caller's capacity, grown and redone if too small
     uint64_t want = cap ? std::min<uint64_t>(cap, cap / n_batches + cap / (4 * n_batches) + 4096) : 4096;
     uint64_t tot = 0;
     for (int attempt = 0; attempt < 2; attempt++) {
       if (sl.d2h_pending) GOD_CUDA(cudaStreamWaitEvent(st, sl.d2h_done, 0));
       grow(sl.an, sl.an_cap, want, st);
-      tot = god::seed_reads(idx, sl.reads, sl.off, (uint32_t)nb, mode, sl.ph, t, sl.an, sl.aoff, sl.an_cap, st,
+      tot = god::seed_reads(idx, breads[b], sl.off, (uint32_t)nb, mode, sl.ph, t, sl.an, sl.aoff, sl.an_cap, st,
                             (uint32_t)r0);
       if (tot <= sl.an_cap) break;
       want = tot;
@@ -536,10 +551,13 @@ GOD_API god_status god_seed_reads(const god_index* idx, const uint8_t* reads, co
     const char* pm = getenv("GOD_PIPE_MIN_READS");  // test hook: smaller batches
     const uint32_t pipe_min = pm ? (uint32_t)atoi(pm) : (1u << 20);  // reads per batch
     const uint32_t n_batches = std::min<uint32_t>(8u, n_reads / (pipe_min ? pipe_min : 1u));
-    if (n_batches >= 2 && !is_device_ptr(reads) && !is_device_ptr(read_offsets) && !is_device_ptr(phases) &&
-        !is_device_ptr(anchor_offsets) && (!anchors || !is_device_ptr(anchors))) {
+    // reads and their offsets both on the host, or both on the device (then only the results are
+    // streamed back); phases, anchor offsets and anchors on the host
+    const bool rdev = is_device_ptr(reads), odev = is_device_ptr(read_offsets);
+    if (n_batches >= 2 && rdev == odev && !is_device_ptr(phases) && !is_device_ptr(anchor_offsets) &&
+        (!anchors || !is_device_ptr(anchors))) {
       const uint64_t tot = seed_reads_pipelined(idx, reads, read_offsets, n_reads, mode, phases, t, anchors,
-                                                anchor_offsets, anchors ? cap : 0, n_batches, st);
+                                                anchor_offsets, anchors ? cap : 0, n_batches, st, rdev);
       *needed = tot;
       if (tot > cap) throw Fail{GOD_ETRUNC};
       return;

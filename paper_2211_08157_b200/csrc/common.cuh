@@ -231,11 +231,14 @@ void scan_exclusive_u64(const uint64_t* in, uint64_t* out, uint64_t n, uint64_t*
 void scan_exclusive_u32_to_u64(const uint32_t* in, uint64_t* out, uint64_t n, uint64_t* total, cudaStream_t st,
                                Scratch& scr, const char* tag = "k_scan");
 
+// Small device->host reads (counts, totals; <= 4096 bytes) through host-mapped pinned memory written
+// by a kernel on `st`, then a synchronize of `st`.  No copy engine is involved, so the read never
+// queues behind large device->host copies of other streams (the pipelined seeding's result copies).
+void d2h_small(void* host, const void* dev, size_t bytes, cudaStream_t st);
 template <class T>
 inline T d2h_scalar(const T* dptr, cudaStream_t st) {
   T v;
-  GOD_CUDA(cudaMemcpyAsync(&v, dptr, sizeof(T), cudaMemcpyDeviceToHost, st));
-  GOD_CUDA(cudaStreamSynchronize(st));
+  d2h_small(&v, dptr, sizeof(T), st);
   return v;
 }
 

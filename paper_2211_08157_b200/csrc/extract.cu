@@ -276,8 +276,8 @@ JobSet make_jobs(const Params& P, const uint64_t* offsets, uint32_t n_seqs, cons
   scan_exclusive_u64(js.kb, js.kb, nj, tot, st, scr, "scan_jobs");
   GOD_CUDA(cudaMemcpyAsync(js.kb + nj, tot, sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
   uint64_t h[2] = {0, 0};
-  GOD_CUDA(cudaMemcpyAsync(&h[0], tot, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
-  GOD_CUDA(cudaMemcpyAsync(&h[1], offsets + n_seqs, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+  d2h_small(&h[0], tot, sizeof(uint64_t), st);
+  d2h_small(&h[1], offsets + n_seqs, sizeof(uint64_t), st);
   GOD_CUDA(cudaStreamSynchronize(st));
   js.total_pos = h[0];
   js.seq_bytes = h[1];

@@ -869,7 +869,7 @@ bool run_extract2(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const
   GOD_CUDA(cudaMemcpyAsync(kb + n_jobs, tot, sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
   GOD_CUDA(cudaMemcpyAsync(cw + n_jobs, tot + 1, sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
   uint64_t htot[3];
-  GOD_CUDA(cudaMemcpyAsync(htot, tot, sizeof(htot), cudaMemcpyDeviceToHost, st));
+  d2h_small(htot, tot, sizeof(htot), st);
   GOD_CUDA(cudaStreamSynchronize(st));
   const uint64_t total_pos = htot[0];
   prof_add_units(tag, htot[2]);

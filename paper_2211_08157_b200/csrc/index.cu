@@ -1130,7 +1130,7 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
     GOD_LAUNCH("k_runs", k_runs, min(grid_for(n, 512), 8u * num_sms()), 512, 0, st, k0, n, ro);
   GOD_LAUNCH("k_tau", k_tau, 1, 1024, 0, st, hist_small, large, n_large, nd_d, n, cut.mode, cut.frac_num, cut.frac_den, cut.max_occ, cs);
   CutState hcs;
-  GOD_CUDA(cudaMemcpyAsync(&hcs, cs, sizeof(CutState), cudaMemcpyDeviceToHost, st));
+  d2h_small(&hcs, cs, sizeof(CutState), st);
   GOD_CUDA(cudaStreamSynchronize(st));
   const uint64_t nd = hcs.n_distinct;
   const uint64_t n_kept = hcs.kept_entries;

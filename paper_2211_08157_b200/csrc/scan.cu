@@ -1,4 +1,6 @@
 // scan.cu — device-wide exclusive prefix sums (single pass, decoupled look-back) and small utilities.
+#include <cstring>
+
 #include "common.cuh"
 
 namespace god {
@@ -82,6 +84,22 @@ void scan_exclusive_u64(const uint64_t* in, uint64_t* out, uint64_t n, uint64_t*
 void scan_exclusive_u32_to_u64(const uint32_t* in, uint64_t* out, uint64_t n, uint64_t* total, cudaStream_t st,
                                Scratch& scr, const char* tag) {
   scan_impl<uint32_t>(in, out, n, total, st, scr, tag);
+}
+
+namespace {
+__global__ void k_d2h_small(const uint8_t* __restrict__ src, uint8_t* dst, uint32_t n) {
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+}
+}  // namespace
+
+void d2h_small(void* host, const void* dev, size_t bytes, cudaStream_t st) {
+  thread_local uint8_t* mapped = nullptr;  // host-mapped pinned page of this host thread
+  if (!mapped) GOD_CUDA(cudaHostAlloc((void**)&mapped, 4096, cudaHostAllocMapped | cudaHostAllocPortable));
+  GOD_REQUIRE(bytes <= 4096, "d2h_small: at most 4096 bytes");
+  if (bytes) GOD_LAUNCH("k_d2h_small", k_d2h_small, 1, 128, 0, st, static_cast<const uint8_t*>(dev), mapped,
+                        (uint32_t)bytes);
+  GOD_CUDA(cudaStreamSynchronize(st));
+  memcpy(host, mapped, bytes);
 }
 
 }  // namespace god

@@ -366,7 +366,7 @@ uint64_t seed_reads(const god_index* ix, const uint8_t* reads, const uint64_t* o
       GOD_CUDA(cudaMemcpyAsync(kb3 + h3, tot3, sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
       const uint64_t tp3 = d2h_scalar(tot3, st);
       uint64_t bytes = 0;
-      GOD_CUDA(cudaMemcpyAsync(&bytes, offsets + n_reads, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+      d2h_small(&bytes, offsets + n_reads, sizeof(uint64_t), st);
       GOD_CUDA(cudaStreamSynchronize(st));
       run_extract(P, reads, bytes, jobs3, kb3, h3, tp3, false, true, rec3, st, scr, tp3 / 4 + 4096, "extract_seed");
     }

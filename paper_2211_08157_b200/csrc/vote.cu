@@ -694,10 +694,10 @@ uint64_t vote_reads(const god_index* ix, const uint8_t* reads, const uint64_t* r
                aoff, n_reads, vp.max_pairs, slot_off, lists, ctr, big_off, big_total, ctr + 6);
   scan_exclusive_u64(slot_off, slot_off, (uint64_t)n_reads + 1, nullptr, st, scr, "scan_vote_slots");
   uint32_t h[8];
-  GOD_CUDA(cudaMemcpyAsync(h, ctr, sizeof(h), cudaMemcpyDeviceToHost, st));
+  d2h_small(h, ctr, sizeof(h), st);
   uint64_t hb[2];
-  GOD_CUDA(cudaMemcpyAsync(&hb[0], slot_off + n_reads, 8, cudaMemcpyDeviceToHost, st));
-  GOD_CUDA(cudaMemcpyAsync(&hb[1], big_total, 8, cudaMemcpyDeviceToHost, st));
+  d2h_small(&hb[0], slot_off + n_reads, 8, st);
+  d2h_small(&hb[1], big_total, 8, st);
   GOD_CUDA(cudaStreamSynchronize(st));
   GOD_REQUIRE(h[7] == 0, "a read has >= 2^29 anchors");
   god_vote* res = scr.alloc<god_vote>(hb[0] ? hb[0] : 1);
@@ -746,8 +746,8 @@ uint64_t vote_reads(const god_index* ix, const uint8_t* reads, const uint64_t* r
   scan_exclusive_u32_to_u64(cnt, out_off, (uint64_t)n_reads + 1, nullptr, st, scr, "scan_vote_out");
   uint32_t nbad = 0;
   uint64_t tot = 0;
-  GOD_CUDA(cudaMemcpyAsync(&nbad, ctr + 6, 4, cudaMemcpyDeviceToHost, st));
-  GOD_CUDA(cudaMemcpyAsync(&tot, out_off + n_reads, 8, cudaMemcpyDeviceToHost, st));
+  d2h_small(&nbad, ctr + 6, 4, st);
+  d2h_small(&tot, out_off + n_reads, 8, st);
   GOD_CUDA(cudaStreamSynchronize(st));
   GOD_REQUIRE(nbad == 0, "anchors inconsistent with the reads' phases (read_pos not an included position)");
   if (tot <= cap && tot && n_reads)

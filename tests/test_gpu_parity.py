@@ -282,8 +282,8 @@ def test_seed_host_pointer_path():
     assert np.array_equal(canon(an), canon(oan))
 
 
-@pytest.mark.parametrize("given", [False, True])
-def test_seed_host_pipelined_batches(given, monkeypatch):
+@pytest.mark.parametrize("given,reads_dev", [(False, False), (True, False), (False, True), (True, True)])
+def test_seed_host_pipelined_batches(given, reads_dev, monkeypatch):
     """All-host buffers above the batch threshold take the pipelined path (read batches copied in,
     seeded and copied out on three streams); batches shrunk by the test hook so that it runs here,
     with long reads (the dedicated PQ_a extraction) and edge reads spread over the batches."""
@@ -299,7 +299,10 @@ def test_seed_host_pipelined_batches(given, monkeypatch):
     ix = god.god_build_index(cu(ref), cu(roffs_ref), "10", 15, 10, cutoff=(1, 500))
     ox = oracle.Index(ref, roffs_ref, "10", 15, 10, cutoff=(1, 500))
     ph = rng.integers(0, 2, size=len(ro) - 1).astype(np.uint8) if given else None
-    an, ao, gph = god.god_seed_reads(ix, rs, ro, phases=ph)
+    if reads_dev:  # reads on the device, results streamed back to host buffers batch by batch
+        an, ao, gph = god.god_seed_reads(ix, cu(rs), cu(ro), phases=ph, host_out=True)
+    else:
+        an, ao, gph = god.god_seed_reads(ix, rs, ro, phases=ph)
     oan, oao, oph = ox.seed_reads(rs, ro, phases=ph)
     assert np.array_equal(gph, oph) and np.array_equal(ao, oao)
     assert np.array_equal(canon(an), canon(oan))
