@@ -634,17 +634,27 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort_big(uint64_t* __restri
     const uint32_t b = big[q];
     const uint64_t s = bstart[b], e = bstart[b + 1], n = e - s;
     const uint64_t top = ((k[s] & ((1ull << hbits) - 1)) >> lo_bits) << lo_bits;  // the bin's segment
+    __shared__ unsigned long long s_diff;
+    if (threadIdx.x == 0) s_diff = 0;
+    __syncthreads();
+    const uint64_t k0 = k[s] & lowmask;
+    uint64_t diff = 0;  // low-hash bits that vary across the bin (a bin of one frequent hash: none)
     for (uint64_t i = threadIdx.x; i < n; i += BS_NT) {
       const uint64_t kk = k[s + i];
+      diff |= (kk & lowmask) ^ k0;
       t0[s + i] = ((kk & lowmask) << 33) | ((uint64_t)v[s + i] << 1) | (kk >> 63);
     }
+    for (int o = 16; o; o >>= 1) diff |= __shfl_xor_sync(0xffffffffu, diff, o);
+    if ((threadIdx.x & 31) == 0 && diff) atomicOr(&s_diff, (unsigned long long)diff);
     __syncthreads();
+    const uint64_t vary = s_diff;
     uint64_t* src = t0 + s;
     uint64_t* dst = t1 + s;
     for (int sh = 0; sh < lo_bits; sh += RS_BITS) {
       const int bits = min(RS_BITS, lo_bits - sh);
       const uint32_t dmask = (1u << bits) - 1;
       const int shift = 33 + sh;
+      if (((vary >> sh) & dmask) == 0) continue;  // a constant digit: the stable pass is the identity
       for (int i = threadIdx.x; i < RS_BINS; i += BS_NT) hist[i] = 0;
       __syncthreads();
       for (uint64_t i = threadIdx.x; i < n; i += BS_NT) atomicAdd(&hist[(uint32_t)(src[i] >> shift) & dmask], 1u);
