@@ -853,7 +853,8 @@ bool run_extract2(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const
   if (!pat_ok) return false;
   const int K = P.k, W = P.w;
   auto supported = [&](int k, int w) { return K == k && W == w; };
-  if (!(supported(21, 11) || supported(19, 19) || supported(15, 10))) return false;
+  // the BASELINE configs (21,11), (19,19), (15,10) and the paper's containment search (19,16)
+  if (!(supported(21, 11) || supported(19, 19) || supported(15, 10) || supported(19, 16))) return false;
   if (getenv("GOD_DISABLE_X2")) return false;
   rec.n = 0;
   if (n_jobs == 0) return false;
@@ -922,6 +923,7 @@ bool run_extract2(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const
       };
       if (K == 21 && W == 11) by_pattern(std::integral_constant<int, 21>(), std::integral_constant<int, 11>());
       else if (K == 19 && W == 19) by_pattern(std::integral_constant<int, 19>(), std::integral_constant<int, 19>());
+      else if (K == 19 && W == 16) by_pattern(std::integral_constant<int, 19>(), std::integral_constant<int, 16>());
       else by_pattern(std::integral_constant<int, 15>(), std::integral_constant<int, 10>());
     } else {
       GOD_CUDA(cudaMemsetAsync(dtotal, 0, sizeof(uint64_t), st));
