@@ -1,6 +1,6 @@
 """GPU parity of location voting (-m gpu): god_vote_reads (CUDA, through the C ABI) against the
 oracle's or_vote_reads_batch (Fig. 8, rescue P:398; readings V1-V6), bit-exact on every
-field and in output order.  Covers every kernel path (<= 16 / 32 / 64 anchors per read: registers;
+field and in output order.  Covers every kernel path (<= 16 / 32 anchors per read: registers;
 <= 128 / 512: a warp on a shared-memory slice; <= 2048: a CTA in shared memory; larger: a CTA on
 global scratch), repeated seeds on one diagonal (V2), both strands, D / V / max_pairs variants,
 reads without anchors, the host-pointer path and the inconsistent-phase error."""
@@ -85,8 +85,8 @@ def test_vote_parity_repeats_long_reads(pattern, k, w):
     ox = oracle.Index(ref, roffs_ref, pattern, k, w, max_occ=400)
     got, vo, (an, ao, _) = _vote_parity(ix, ox, rs, ro)
     per_read = np.diff(ao.cpu().numpy())
-    # every kernel path: <= 16, <= 32, <= 64 (registers), <= 128, <= 512 (warp + SMEM), <= 2048 (CTA), more
-    for lo, hi in [(0, 16), (16, 32), (32, 64), (64, 128), (128, 512), (512, 2048), (2048, 1 << 40)]:
+    # every kernel path: <= 16, <= 32 (registers), <= 128, <= 512 (warp + SMEM), <= 2048 (CTA), more
+    for lo, hi in [(0, 16), (16, 32), (32, 128), (128, 512), (512, 2048), (2048, 1 << 40)]:
         assert ((per_read > lo) & (per_read <= hi)).any(), (lo, hi)
     for D, V, mp in [(50, 2, 4), (500, 1, 0), (0, 10, 1)]:
         _vote_parity(ix, ox, rs, ro, D=D, V=V, max_pairs=mp)
