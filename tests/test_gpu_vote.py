@@ -86,8 +86,9 @@ def test_vote_parity_repeats_long_reads(pattern, k, w):
     got, vo, (an, ao, _) = _vote_parity(ix, ox, rs, ro)
     per_read = np.diff(ao.cpu().numpy())
     # every kernel path: <= 16, <= 32 (registers), <= 128, <= 512 (warp + SMEM), <= 2048 (CTA), more
-    for lo, hi in [(0, 16), (16, 32), (32, 128), (128, 512), (512, 2048), (2048, 1 << 40)]:
-        assert ((per_read > lo) & (per_read <= hi)).any(), (lo, hi)
+    if pattern != "1":  # ('1', 11, 5) gives almost every read > 32 anchors
+        for lo, hi in [(0, 16), (16, 32), (32, 128), (128, 512), (512, 2048), (2048, 1 << 40)]:
+            assert ((per_read > lo) & (per_read <= hi)).any(), (lo, hi)
     for D, V, mp in [(50, 2, 4), (500, 1, 0), (0, 10, 1)]:
         _vote_parity(ix, ox, rs, ro, D=D, V=V, max_pairs=mp)
 
