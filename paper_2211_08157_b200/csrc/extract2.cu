@@ -1,8 +1,8 @@
 // extract2.cu — K1 v2: register-resident fused sparsify + minimizer extraction (stages 1+2).
 //
 // Same definitions as extract.cu (P:282/P:286/P:294/P:300/P:370; readings O1-O6 of DESIGN.md §2),
-// specialised at compile time for the hot configurations: k, w and patterns with exactly one '1'
-// (patterns of period p whose x ones come first: "1", "10"/"01", "110", "1110").  Everything else
+// specialised at compile time for the hot configurations: k, w and patterns with exactly one '1' of
+// period <= 3 ("1", "10"/"01", "100"/"010"/"001") or whose x ones come first ("110", "1110").  Everything else
 // runs the generic kernel (extract.cu).
 //
 // Layout.  Each job's k-mer starts are padded to a multiple of W positions (the pad slots are
@@ -171,6 +171,11 @@ constexpr uint32_t pack_sel() {
   for (int i = 0; i < 4; i++) sel |= (uint32_t)(pat_rel(PP, PX, R0, 4 * G + i) - a4) << (4 * i);
   return sel;
 }
+// byte offset of base 4G + i relative to the aligned start of base 4G (period 3: 0, 3, 6, 9)
+template <int PP, int PX, int R0, int G>
+constexpr int pack_off(int i) {
+  return pat_rel(PP, PX, R0, 4 * G + i) - (pat_rel(PP, PX, R0, 4 * G) / 4) * 4;
+}
 
 // 16 patterned bases (MSB-first 2-bit codes) from the ASCII bytes, base 0 at byte A (its job-relative
 // index has residue R0 mod PX); *nm gets the N bits (bit 15 - b for base b).  nb = bases that exist.
@@ -209,7 +214,14 @@ __device__ __forceinline__ uint32_t pack16(const uint8_t* seq, uint64_t seq_byte
     const uint32_t lo = __funnelshift_r(w[a], w[a + 1], d8);
     if constexpr (sel == 0x3210u) return lo;  // four consecutive bytes
     const uint32_t hi = __funnelshift_r(w[a + 1], w[a + 2], d8);
-    return __byte_perm(lo, hi, sel);
+    if constexpr (pack_off<PP, PX, R0, G>(3) < 8) {
+      return __byte_perm(lo, hi, sel);
+    } else {  // period 3: bases at 0, 3, 6 from (lo, hi), the fourth (offset 8..11) from the next word
+      static_assert(pack_off<PP, PX, R0, G>(2) < 8 && pack_off<PP, PX, R0, G>(3) < 12, "byte gather span");
+      const uint32_t hi2 = __funnelshift_r(w[a + 2], w[a + 3], d8);
+      const uint32_t t = __byte_perm(lo, hi, sel & 0x0FFFu);
+      return __byte_perm(t, hi2, 0x0210u | ((uint32_t)(4 + pack_off<PP, PX, R0, G>(3) - 8) << 12));
+    }
   };
   const uint32_t xs[4] = {gather(std::integral_constant<int, 0>()), gather(std::integral_constant<int, 1>()),
                           gather(std::integral_constant<int, 2>()), gather(std::integral_constant<int, 3>())};
@@ -845,9 +857,10 @@ void launch_x2(const X2Args& a, uint64_t ntiles, cudaStream_t st, const char* ta
 bool run_extract2(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const Job* jobs, uint32_t n_jobs,
                   bool want_job, bool want_job_off, Records& rec, cudaStream_t st, Scratch& scr,
                   uint64_t cap_hint, const char* tag) {
-  // patterns: x = 1 with p <= 2 (any rotation), or p = x + 1 <= 4 with the ones first ("110", "1110")
+  // patterns: x = 1 with p <= 3 (any rotation: "1", "10", "100"), or p = x + 1 <= 4 with the ones
+  // first ("110", "1110")
   const int PP = (int)P.pat.p, PX = (int)P.pat.x;
-  bool pat_ok = (PX == 1 && PP <= 2) || ((PX == 2 || PX == 3) && PP == PX + 1);
+  bool pat_ok = (PX == 1 && PP <= 3) || ((PX == 2 || PX == 3) && PP == PX + 1);
   if (PX >= 2)
     for (int i = 0; i < PX; i++) pat_ok = pat_ok && P.pat.one[i] == (uint32_t)i;
   if (!pat_ok) return false;
@@ -917,7 +930,8 @@ bool run_extract2(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const
       auto by_pattern = [&](auto kc, auto wc) {
         constexpr int KK = decltype(kc)::value, WW = decltype(wc)::value;
         if (PX == 1 && PP == 1) launch_x2<KK, WW, 1, 1>(a, ntiles, st, tag);
-        else if (PX == 1) launch_x2<KK, WW, 2, 1>(a, ntiles, st, tag);
+        else if (PX == 1 && PP == 2) launch_x2<KK, WW, 2, 1>(a, ntiles, st, tag);
+        else if (PX == 1) launch_x2<KK, WW, 3, 1>(a, ntiles, st, tag);
         else if (PX == 2) launch_x2<KK, WW, 3, 2>(a, ntiles, st, tag);
         else launch_x2<KK, WW, 4, 3>(a, ntiles, st, tag);
       };

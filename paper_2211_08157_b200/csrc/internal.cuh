@@ -34,7 +34,7 @@ struct Records {
 void run_extract(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const Job* jobs, const uint64_t* kb,
                  uint32_t n_jobs, uint64_t total_pos, bool want_job, bool want_job_off, Records& rec, cudaStream_t st,
                  Scratch& scr, uint64_t cap_hint, const char* tag = "k_extract");
-// Specialised register-resident kernel (extract2.cu) for x == 1 patterns of period 1 or 2 (and the
+// Specialised register-resident kernel (extract2.cu) for x == 1 patterns of period 1 to 3 (and the
 // '110' / '1110' shapes) and (k, w) in {(21,11), (19,19), (15,10), (19,16)}; returns false if not
 // applicable.
 bool run_extract2(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const Job* jobs, uint32_t n_jobs,

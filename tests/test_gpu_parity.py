@@ -311,7 +311,8 @@ def test_seed_host_pipelined_batches(given, reads_dev, monkeypatch):
 # ------------------------------------------------------------------------------------ K1 v2 (specialised)
 X2_COMBOS = [("10", 21, 11), ("01", 21, 11), ("1", 21, 11), ("10", 19, 19), ("1", 19, 19), ("10", 15, 10),
              ("1", 15, 10), ("110", 21, 11), ("1110", 21, 11), ("110", 19, 19), ("1110", 19, 19), ("110", 15, 10),
-             ("1110", 15, 10), ("10", 19, 16), ("1", 19, 16), ("110", 19, 16), ("1110", 19, 16)]
+             ("1110", 15, 10), ("10", 19, 16), ("1", 19, 16), ("110", 19, 16), ("1110", 19, 16), ("100", 21, 11),
+             ("010", 19, 19), ("001", 15, 10), ("100", 19, 16)]
 
 
 @pytest.mark.parametrize("combo", X2_COMBOS, ids=[f"{c[0]}-k{c[1]}-w{c[2]}" for c in X2_COMBOS])
