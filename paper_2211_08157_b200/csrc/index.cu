@@ -77,7 +77,8 @@ template <int RB>
 __global__ void __launch_bounds__(RS2_NT, 2) k_rs_scatter2(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin,
                                                        uint64_t* __restrict__ kout, uint32_t* __restrict__ vout,
                                                        uint64_t n, int shift, uint32_t dmask,
-                                                       const uint64_t* __restrict__ goff, uint32_t ntiles) {
+                                                       const uint64_t* __restrict__ goff, uint32_t ntiles,
+                                                       const uint2* __restrict__ table, int L) {
   __shared__ uint32_t wcnt[RS2_NT / 32][(1 << RB)];
   __shared__ uint32_t dstart[(1 << RB)];
   __shared__ uint32_t wsum[(1 << RB) / 32];
@@ -100,6 +101,16 @@ __global__ void __launch_bounds__(RS2_NT, 2) k_rs_scatter2(const uint64_t* __res
     const bool ok = i < n;
     key[j] = ok ? __ldcs(kin + i) : 0;
     val[j] = ok ? __ldcs(vin + i) : 0;
+  }
+  if (table) {  // first bin-sort pass: the key gets its data-sized bin (k_seg_assign's rule) here
+    const uint64_t lmask = (1ull << L) - 1;
+#pragma unroll
+    for (int j = 0; j < RS2_IPT; j++) {
+      const uint64_t h = key[j] & HASH_BITS_MASK;
+      const uint2 t = __ldg(table + (h >> L));
+      const uint64_t b = t.x + (((h & lmask) * t.y) >> L);
+      key[j] |= b << shift;
+    }
   }
 #pragma unroll
   for (int j = 0; j < RS2_IPT; j++) {
@@ -295,7 +306,7 @@ __global__ void __launch_bounds__(1024) k_seg_table(const uint32_t* __restrict__
 // of the first LSD digit of b (the k_rs_hist of the first pass, fused)
 __global__ void __launch_bounds__(RS_NT) k_seg_assign(uint64_t* __restrict__ k, uint64_t n, int L, int hbits,
                                                       const uint2* __restrict__ table, uint32_t dmask,
-                                                      uint32_t* hist, uint32_t ntiles) {
+                                                      uint32_t* hist, uint32_t ntiles, int write_keys) {
   __shared__ uint32_t hh[1 << BIN_DIGIT];
   for (int i = threadIdx.x; i < (1 << BIN_DIGIT); i += RS_NT) hh[i] = 0;
   __syncthreads();
@@ -309,7 +320,7 @@ __global__ void __launch_bounds__(RS_NT) k_seg_assign(uint64_t* __restrict__ k, 
       const uint64_t h = kk & HASH_BITS_MASK;
       const uint2 t = __ldg(table + (h >> L));
       const uint64_t b = t.x + (((h & lmask) * t.y) >> L);
-      k[i] = kk | (b << hbits);
+      if (write_keys) k[i] = kk | (b << hbits);
       atomicAdd(&hh[(uint32_t)b & dmask], 1u);
     }
   }
@@ -1081,13 +1092,14 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
       attr = true;
     }
     const int hbits = 2 * P.k;
-    auto lsd_pass = [&](auto rb, int shift, int bits, bool have_hist = false) {
+    auto lsd_pass = [&](auto rb, int shift, int bits, bool have_hist = false, const uint2* table = nullptr,
+                        int L = 0) {
       constexpr int RB = decltype(rb)::value;
       const uint32_t dmask = (1u << bits) - 1;
       if (!have_hist) GOD_LAUNCH("k_rs_hist", k_rs_hist<RB>, ntiles, RS_NT, 0, st, k0, n, shift, dmask, hist, ntiles);
       scan_exclusive_u32_to_u64(hist, goff, (uint64_t)(1u << RB) * ntiles, nullptr, st, scr, "scan_sort_hist");
       GOD_LAUNCH("k_rs_scatter", k_rs_scatter2<RB>, ntiles, RS2_NT, RS_DYN_SMEM, st, k0, v0, k1, v1, n, shift, dmask,
-                 goff, ntiles);
+                 goff, ntiles, table, L);
       std::swap(k0, k1);
       std::swap(v0, v1);
     };
@@ -1104,9 +1116,10 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
       const uint32_t target =
           (uint32_t)std::max<uint64_t>(base_target, n / ((1u << (2 * BIN_DIGIT)) - (1u << SEG_BITS)) + 1);
       GOD_LAUNCH("k_seg_table", k_seg_table, 1, 1024, 0, st, segc, target, table, n_bins_d);
+      // the first pass's tile histograms of the bins; the first scatter assigns the bins itself
       GOD_LAUNCH("k_seg_assign", k_seg_assign, ntiles, RS_NT, 0, st, k0, n, L, hbits, table, (1u << BIN_DIGIT) - 1, hist,
-                 ntiles);
-      lsd_pass(std::integral_constant<int, BIN_DIGIT>(), hbits, BIN_DIGIT, true);
+                 ntiles, 0);
+      lsd_pass(std::integral_constant<int, BIN_DIGIT>(), hbits, BIN_DIGIT, true, table, L);
       lsd_pass(std::integral_constant<int, BIN_DIGIT>(), hbits + BIN_DIGIT, BIN_DIGIT);
       const uint32_t nb = d2h_scalar(n_bins_d, st);
       uint64_t* bstart = scr.alloc<uint64_t>((uint64_t)nb + 1);
