@@ -18,7 +18,8 @@
 // registers (shuffle bitonic sort, ballots); n <= 128 / n <= 512 -> one warp per read on a 3 / 12 KB
 // shared-memory slice; n <= 2048 -> one CTA per read in shared memory; larger -> one CTA per read
 // on global scratch.
-// Results go to per-read slots (min(n, max_pairs) each); a scan of the per-read counts and a
+// Results go to per-read slots (max(1, min(n / V, max_pairs)) each: winners are disjoint clusters of
+// >= V votes); a scan of the per-read counts and a
 // compaction give the CSR output.
 #include <algorithm>
 
@@ -190,35 +191,52 @@ __device__ __forceinline__ void put_result(const VoteArgs& A, uint32_t r, uint32
 }
 
 // ------------------------------------------------------------------ bucketing + result slots
-__global__ void k_vote_classify(const uint64_t* __restrict__ aoff, uint32_t n_reads, uint32_t mp,
-                                uint64_t* __restrict__ slots, uint32_t* __restrict__ lists,
-                                uint32_t* __restrict__ nlist, uint64_t* __restrict__ big_off,
-                                uint64_t* __restrict__ big_total, uint32_t* __restrict__ bad) {
-  const int lane = threadIdx.x & 31;
+constexpr int VC_NT = 1024;   // classify: one list reservation per class and block of 1024 reads
+constexpr int VC_CLASSES = 6;
+__global__ void __launch_bounds__(VC_NT) k_vote_classify(const uint64_t* __restrict__ aoff, uint32_t n_reads,
+                                                         uint32_t mp, uint32_t V, uint64_t* __restrict__ slots,
+                                                         uint32_t* __restrict__ lists, uint32_t* __restrict__ nlist,
+                                                         uint64_t* __restrict__ big_off,
+                                                         uint64_t* __restrict__ big_total, uint32_t* __restrict__ bad) {
+  constexpr int NW = VC_NT / 32;
+  __shared__ uint32_t s_cnt[VC_CLASSES][NW];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t stride = gridDim.x * blockDim.x;
-  for (uint32_t r0 = blockIdx.x * blockDim.x; r0 < n_reads; r0 += stride) {  // warp-uniform trip count
+  for (uint32_t r0 = blockIdx.x * blockDim.x; r0 < n_reads; r0 += stride) {  // block-uniform trip count
     const uint32_t r = r0 + threadIdx.x;
     uint64_t n = 0;
     if (r < n_reads) {
       n = aoff[r + 1] - aoff[r];
-      slots[r] = n == 0 ? 0 : (mp && n > mp ? mp : n);
+      // result slots: winners are disjoint clusters of >= V votes (each vote an anchor), so at most
+      // n / V of them (max_pairs caps it further); a rescue location needs one
+      uint64_t sl = n / (V ? V : 1u);
+      if (mp && sl > mp) sl = mp;
+      slots[r] = n == 0 ? 0 : (sl ? sl : 1);
     }
     if (n >= VOTE_IDX_MAX) { atomicAdd(bad + 1, 1u); n = 0; }
     const int c = n == 0 ? -1 : n <= 16 ? 0 : n <= 32 ? 1 : n <= VOTE_WSM ? 2 : n <= VOTE_WSM2 ? 3 : n <= VOTE_MID ? 4 : 5;
+    uint32_t mine = 0;  // ballot of this lane's class
 #pragma unroll
-    for (int q = 0; q < 6; q++) {  // one atomic per warp and class
+    for (int q = 0; q < VC_CLASSES; q++) {
       const uint32_t m = __ballot_sync(FULL, c == q);
-      if (!m) continue;
-      const int leader = __ffs(m) - 1;
-      uint32_t base = 0;
-      if (lane == leader) base = atomicAdd(nlist + q, (uint32_t)__popc(m));
-      base = __shfl_sync(FULL, base, leader);
-      if (c == q) {
-        const uint32_t j = base + __popc(m & ((1u << lane) - 1u));
-        lists[(uint64_t)q * n_reads + j] = r;
-        if (q == 5) big_off[j] = atomicAdd((unsigned long long*)big_total, (unsigned long long)(n + 2));
-      }
+      if (c == q) mine = m;
+      if (lane == 0) s_cnt[q][warp] = __popc(m);
     }
+    __syncthreads();
+    if (threadIdx.x < VC_CLASSES) {  // one reservation per class: exclusive prefix over the warps
+      const int q = threadIdx.x;
+      uint32_t tot = 0;
+      for (int w = 0; w < NW; w++) { const uint32_t x = s_cnt[q][w]; s_cnt[q][w] = tot; tot += x; }
+      const uint32_t base = tot ? atomicAdd(nlist + q, tot) : 0u;
+      for (int w = 0; w < NW; w++) s_cnt[q][w] += base;
+    }
+    __syncthreads();
+    if (c >= 0) {
+      const uint32_t j = s_cnt[c][warp] + __popc(mine & ((1u << lane) - 1u));
+      lists[(uint64_t)c * n_reads + j] = r;
+      if (c == 5) big_off[j] = atomicAdd((unsigned long long*)big_total, (unsigned long long)(n + 2));
+    }
+    __syncthreads();
   }
 }
 
@@ -690,8 +708,8 @@ uint64_t vote_reads(const god_index* ix, const uint8_t* reads, const uint64_t* r
   GOD_CUDA(cudaMemsetAsync(slot_off, 0, ((size_t)n_reads + 1) * sizeof(uint64_t), st));
   const int nsm = num_sms();
   if (n_reads)
-    GOD_LAUNCH("k_vote_classify", k_vote_classify, std::min<unsigned>(grid_for(n_reads, 256), nsm * 8u), 256, 0, st,
-               aoff, n_reads, vp.max_pairs, slot_off, lists, ctr, big_off, big_total, ctr + 6);
+    GOD_LAUNCH("k_vote_classify", k_vote_classify, std::min<unsigned>(grid_for(n_reads, VC_NT), nsm * 2u), VC_NT, 0, st,
+               aoff, n_reads, vp.max_pairs, vp.V, slot_off, lists, ctr, big_off, big_total, ctr + 6);
   scan_exclusive_u64(slot_off, slot_off, (uint64_t)n_reads + 1, nullptr, st, scr, "scan_vote_slots");
   uint32_t h[8];
   d2h_small(h, ctr, sizeof(h), st);
