@@ -302,6 +302,8 @@ static uint64_t seed_reads_pipelined(const god_index* idx, const uint8_t* reads,
     GOD_CUDA(cudaEventRecord(sl.h2d_done, s_h2d));
   };
   upload(0);
+  set_copies_in_flight(true);
+  struct Reset { ~Reset() { set_copies_in_flight(false); } } reset_flag;
   for (uint32_t b = 0; b < n_batches; b++) {
     PipeSlot& sl = slot[b & 1];
     if (b + 1 < n_batches) upload(b + 1);

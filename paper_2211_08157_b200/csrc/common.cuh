@@ -231,10 +231,13 @@ void scan_exclusive_u64(const uint64_t* in, uint64_t* out, uint64_t n, uint64_t*
 void scan_exclusive_u32_to_u64(const uint32_t* in, uint64_t* out, uint64_t n, uint64_t* total, cudaStream_t st,
                                Scratch& scr, const char* tag = "k_scan");
 
-// Small device->host reads (counts, totals; <= 4096 bytes) through host-mapped pinned memory written
-// by a kernel on `st`, then a synchronize of `st`.  No copy engine is involved, so the read never
-// queues behind large device->host copies of other streams (the pipelined seeding's result copies).
+// Small device->host reads (counts, totals; <= 4096 bytes) into a pinned page, then a synchronize of
+// `st`.  While large device->host copies of other streams are in flight (the pipelined seeding's
+// result copies) the page is written through its host mapping by a one-thread kernel instead, so the
+// read does not queue behind them on the copy engine.
 void d2h_small(void* host, const void* dev, size_t bytes, cudaStream_t st);
+// set while this host thread streams large device->host copies on other streams (pipelined seeding)
+void set_copies_in_flight(bool on);
 template <class T>
 inline T d2h_scalar(const T* dptr, cudaStream_t st) {
   T v;

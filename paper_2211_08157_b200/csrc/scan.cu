@@ -92,12 +92,19 @@ __global__ void k_d2h_small(const uint8_t* __restrict__ src, uint8_t* dst, uint3
 }
 }  // namespace
 
+thread_local bool t_copies_in_flight = false;
+void set_copies_in_flight(bool on) { t_copies_in_flight = on; }
+
 void d2h_small(void* host, const void* dev, size_t bytes, cudaStream_t st) {
   thread_local uint8_t* mapped = nullptr;  // host-mapped pinned page of this host thread
   if (!mapped) GOD_CUDA(cudaHostAlloc((void**)&mapped, 4096, cudaHostAllocMapped | cudaHostAllocPortable));
   GOD_REQUIRE(bytes <= 4096, "d2h_small: at most 4096 bytes");
-  if (bytes) GOD_LAUNCH("k_d2h_small", k_d2h_small, 1, 128, 0, st, static_cast<const uint8_t*>(dev), mapped,
-                        (uint32_t)bytes);
+  if (bytes) {
+    if (t_copies_in_flight)  // large copies of another stream occupy the copy engine: write through mapping
+      GOD_LAUNCH("k_d2h_small", k_d2h_small, 1, 128, 0, st, static_cast<const uint8_t*>(dev), mapped, (uint32_t)bytes);
+    else  // an idle copy engine: a pinned copy has the lower latency
+      GOD_CUDA(cudaMemcpyAsync(mapped, dev, bytes, cudaMemcpyDeviceToHost, st));
+  }
   GOD_CUDA(cudaStreamSynchronize(st));
   memcpy(host, mapped, bytes);
 }
