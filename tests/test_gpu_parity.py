@@ -373,3 +373,23 @@ def test_misaligned_device_buffers():
         an, ao, ph = god.god_seed_reads(ix, rb[shift:shift + sub.size], cu(soffs))
         assert np.array_equal(np_(ph), oph) and np.array_equal(np_(ao), oao)
         assert np.array_equal(canon(np_(an)), canon(oan))
+
+
+def test_rebuild_and_reseed_are_byte_identical():
+    """re-indexing is byte-identical; seeding and voting are deterministic too (anchor order,
+    phases, voted locations), on a repeat-rich reference whose sort paths include big bins."""
+    rng = np.random.default_rng(31)
+    rep = synth.random_acgt(rng, 3000)
+    ref = np.concatenate([synth.dup_genome(500_000, 17, dup_frac=0.3, lmin=300, lmax=3000)] + [rep] * 200)
+    offs = np.array([0, ref.size], np.uint64)
+    reads = synth.simulate_reads(ref, 3000, 19, length=150, p_sub=0.002)
+    outs = []
+    for _ in range(2):
+        ix = god.god_build_index(cu(ref), cu(offs), "10", 21, 11, cutoff=(1, 1000))
+        h, p, z = ix.dump()
+        an, ao, ph = god.god_seed_reads(ix, cu(reads.seq), cu(reads.offsets))
+        v, vo = god.god_vote_reads(ix, cu(reads.seq), cu(reads.offsets), ph, an, ao, V=2)
+        outs.append([np.asarray(x) for x in (h, p, z)] + [np_(x) for x in (an, ao, ph, v, vo)])
+        ix.free()
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)

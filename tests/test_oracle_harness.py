@@ -128,3 +128,15 @@ def test_accepted_pairs_no_false_negatives_and_trend():
         r = mm[:, a] / np.maximum(tt[:, a], 1)
         lo, hi = r[ed <= np.percentile(ed, 25)].mean(), r[ed >= np.percentile(ed, 75)].mean()
         assert lo > hi
+
+
+def test_mutation_pairs_generator():
+    """S1 inputs: the mutated copy differs from the original at exactly n_subs positions, every
+    difference a substitution to another base; same seed, same pairs."""
+    o, m, off, subs = synth.mutation_pairs(50, 400, 120, 3)
+    assert off[-1] == 50 * 400 and set(np.unique(o).tolist()) <= set(b"ACGT")
+    for i in range(50):
+        a, c = o[int(off[i]):int(off[i + 1])], m[int(off[i]):int(off[i + 1])]
+        assert int((a != c).sum()) == int(subs[i]) <= 120
+    o2, m2, _, s2 = synth.mutation_pairs(50, 400, 120, 3)
+    assert np.array_equal(o, o2) and np.array_equal(m, m2) and np.array_equal(subs, s2)
