@@ -441,7 +441,7 @@ GOD_API god_status god_minimizers(const god_params* prm, const uint8_t* seq, con
     JobSet js = make_jobs(P, doff, n_seqs, dph, 0, 0, global_pos != 0, st, scr);
     Records rec;
     run_extract(P, dseq, js.seq_bytes, js.jobs, js.kb, js.n, js.total_pos, false, true, rec, st, scr,
-                js.total_pos / (uint64_t)(P.w + 1) * 2 + js.total_pos / 8 + 4096, "extract_mz");
+                js.total_pos / (uint64_t)(P.w + 1) * 2 + js.total_pos / 8 + 4096, "extract_mz", js.x2p());
     *needed = rec.n;
     uint64_t* doo = sg.out(out_offsets, (size_t)n_seqs + 1);
     GOD_CUDA(cudaMemcpyAsync(doo, rec.job_off, ((size_t)n_seqs + 1) * sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));

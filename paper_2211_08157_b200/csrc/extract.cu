@@ -240,9 +240,14 @@ __global__ void __launch_bounds__(EX_NT) k_extract(ExArgs a) {
 }
 
 // ---------------------------------------------------------------------------------- job building
+// kb[j]: the generic layout's nk + 1 (one separator per job), or with x2 the specialised kernel's
+// padded count (nk rounded up to a multiple of w, >= w) and cw[j] its 16-base code words; nk_sum
+// accumulates the k-mer starts (x2 only)
 __global__ void k_make_jobs(Params P, const uint64_t* offsets, uint32_t n_seqs, const uint8_t* phases, uint32_t p_all,
-                            uint32_t kcap, int global_pos, Job* jobs, uint64_t* nkp1) {
+                            uint32_t kcap, int global_pos, Job* jobs, uint64_t* nkp1, int x2, uint64_t* cw,
+                            unsigned long long* nk_sum) {
   const uint64_t nj = p_all ? (uint64_t)n_seqs * p_all : n_seqs;
+  uint64_t acc = 0;
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < nj; j += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t sidx = p_all ? j / p_all : j;
     const uint32_t s = p_all ? (uint32_t)(j % p_all) : (phases ? phases[sidx] : 0u);
@@ -256,7 +261,18 @@ __global__ void k_make_jobs(Params P, const uint64_t* offsets, uint32_t n_seqs, 
     if (kcap && nk > kcap) nk = kcap;
     jb.nk = (uint32_t)nk;
     jobs[j] = jb;
-    nkp1[j] = nk + 1;
+    if (x2) {
+      const uint64_t W = (uint64_t)P.w;
+      nkp1[j] = (nk ? (nk + W - 1) / W : 1) * W;
+      cw[j] = nk ? (nk + P.k - 1 + 15) / 16 : 0;
+      acc += nk;
+    } else {
+      nkp1[j] = nk + 1;
+    }
+  }
+  if (x2) {
+    for (int d = 16; d; d >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, d);
+    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(nk_sum, (unsigned long long)acc);
   }
 }
 }  // namespace
@@ -268,17 +284,39 @@ JobSet make_jobs(const Params& P, const uint64_t* offsets, uint32_t n_seqs, cons
   GOD_REQUIRE(nj < 0x7FFFFFFFull, "too many (sequence, phase) jobs");
   js.n = (uint32_t)nj;
   js.jobs = scr.alloc<Job>(nj);
+  if (nj && x2_supported(P)) {  // the specialised kernel's layout in the same pass (no generic layout)
+    uint64_t* kb = scr.alloc<uint64_t>(nj + 1);
+    uint64_t* cw = scr.alloc<uint64_t>(nj + 1);
+    uint64_t* tot = scr.alloc<uint64_t>(3);
+    GOD_CUDA(cudaMemsetAsync(tot + 2, 0, sizeof(uint64_t), st));
+    GOD_LAUNCH("k_make_jobs", k_make_jobs, grid_for(nj, 256), 256, 0, st, P, offsets, n_seqs, phases, p_all, kcap,
+               global_pos, js.jobs, kb, 1, cw, reinterpret_cast<unsigned long long*>(tot + 2));
+    scan_exclusive_u64(kb, kb, nj, tot, st, scr, "scan_jobs");
+    scan_exclusive_u64(cw, cw, nj, tot + 1, st, scr, "scan_jobs");
+    GOD_CUDA(cudaMemcpyAsync(kb + nj, tot, sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
+    GOD_CUDA(cudaMemcpyAsync(cw + nj, tot + 1, sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
+    uint64_t h[4] = {0, 0, 0, 0};
+    d2h_small(h, tot, 3 * sizeof(uint64_t), st);
+    d2h_small(&h[3], offsets + n_seqs, sizeof(uint64_t), st);
+    js.x2.kb = kb;
+    js.x2.cw = cw;
+    js.x2.total_pos = h[0];
+    js.x2.nk_sum = h[2];
+    js.total_pos = h[2] + nj;  // the generic layout's size (cap estimates)
+    js.seq_bytes = h[3];
+    return js;
+  }
   js.kb = scr.alloc<uint64_t>(nj + 1);
   uint64_t* tot = scr.alloc<uint64_t>(1);
   if (nj) {
-    GOD_LAUNCH("k_make_jobs", k_make_jobs, grid_for(nj, 256), 256, 0, st, P, offsets, n_seqs, phases, p_all, kcap, global_pos, js.jobs, js.kb);
+    GOD_LAUNCH("k_make_jobs", k_make_jobs, grid_for(nj, 256), 256, 0, st, P, offsets, n_seqs, phases, p_all, kcap,
+               global_pos, js.jobs, js.kb, 0, nullptr, nullptr);
   }
   scan_exclusive_u64(js.kb, js.kb, nj, tot, st, scr, "scan_jobs");
   GOD_CUDA(cudaMemcpyAsync(js.kb + nj, tot, sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
   uint64_t h[2] = {0, 0};
   d2h_small(&h[0], tot, sizeof(uint64_t), st);
   d2h_small(&h[1], offsets + n_seqs, sizeof(uint64_t), st);
-  GOD_CUDA(cudaStreamSynchronize(st));
   js.total_pos = h[0];
   js.seq_bytes = h[1];
   return js;
@@ -286,9 +324,9 @@ JobSet make_jobs(const Params& P, const uint64_t* offsets, uint32_t n_seqs, cons
 
 void run_extract(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const Job* jobs, const uint64_t* kb,
                  uint32_t n_jobs, uint64_t total_pos, bool want_job, bool want_job_off, Records& rec, cudaStream_t st,
-                 Scratch& scr, uint64_t cap_hint, const char* tag) {
+                 Scratch& scr, uint64_t cap_hint, const char* tag, const X2Layout* x2) {
   rec.n = 0;
-  if (run_extract2(P, seq, seq_bytes, jobs, n_jobs, want_job, want_job_off, rec, st, scr, cap_hint, tag)) return;
+  if (run_extract2(P, seq, seq_bytes, jobs, n_jobs, want_job, want_job_off, rec, st, scr, cap_hint, tag, x2)) return;
   if (n_jobs == 0 || total_pos == 0) {
     rec.cap = 1;
     rec.hz = scr.alloc<uint64_t>(1);

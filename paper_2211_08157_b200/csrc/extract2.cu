@@ -853,10 +853,7 @@ void launch_x2(const X2Args& a, uint64_t ntiles, cudaStream_t st, const char* ta
 
 }  // namespace
 
-// Returns false if no specialised kernel exists for these parameters (caller uses the generic one).
-bool run_extract2(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const Job* jobs, uint32_t n_jobs,
-                  bool want_job, bool want_job_off, Records& rec, cudaStream_t st, Scratch& scr,
-                  uint64_t cap_hint, const char* tag) {
+bool x2_supported(const Params& P) {
   // patterns: x = 1 with p <= 3 (any rotation: "1", "10", "100"), or p = x + 1 <= 4 with the ones
   // first ("110", "1110")
   const int PP = (int)P.pat.p, PX = (int)P.pat.x;
@@ -868,25 +865,46 @@ bool run_extract2(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const
   auto supported = [&](int k, int w) { return K == k && W == w; };
   // the BASELINE configs (21,11), (19,19), (15,10) and the paper's containment search (19,16)
   if (!(supported(21, 11) || supported(19, 19) || supported(15, 10) || supported(19, 16))) return false;
-  if (getenv("GOD_DISABLE_X2")) return false;
+  return !getenv("GOD_DISABLE_X2");
+}
+
+// Returns false if no specialised kernel exists for these parameters (caller uses the generic one).
+bool run_extract2(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const Job* jobs, uint32_t n_jobs,
+                  bool want_job, bool want_job_off, Records& rec, cudaStream_t st, Scratch& scr,
+                  uint64_t cap_hint, const char* tag, const X2Layout* x2) {
+  if (!x2_supported(P)) return false;
+  const int PP = (int)P.pat.p, PX = (int)P.pat.x;
+  const int K = P.k, W = P.w;
   rec.n = 0;
   if (n_jobs == 0) return false;
-  // padded layouts
-  uint64_t* kb = scr.alloc<uint64_t>(n_jobs + 1);
-  uint64_t* cw = scr.alloc<uint64_t>(n_jobs + 1);
-  uint64_t* tot = scr.alloc<uint64_t>(3);
-  GOD_CUDA(cudaMemsetAsync(tot + 2, 0, sizeof(uint64_t), st));
-  GOD_LAUNCH("k_x2_sizes", k_x2_sizes, grid_for(n_jobs, 256), 256, 0, st, jobs, n_jobs, K, W, kb, cw,
-             reinterpret_cast<unsigned long long*>(tot + 2));
-  scan_exclusive_u64(kb, kb, n_jobs, tot, st, scr, "scan_x2_jobs");
-  scan_exclusive_u64(cw, cw, n_jobs, tot + 1, st, scr, "scan_x2_jobs");
-  GOD_CUDA(cudaMemcpyAsync(kb + n_jobs, tot, sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
-  GOD_CUDA(cudaMemcpyAsync(cw + n_jobs, tot + 1, sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
-  uint64_t htot[3];
-  d2h_small(htot, tot, sizeof(htot), st);
-  GOD_CUDA(cudaStreamSynchronize(st));
-  const uint64_t total_pos = htot[0];
-  prof_add_units(tag, htot[2]);
+  // padded layouts (built by make_jobs in the same pass as the jobs, else here)
+  const uint64_t* kb;
+  const uint64_t* cw;
+  uint64_t total_pos, nk_sum;
+  if (x2) {
+    kb = x2->kb;
+    cw = x2->cw;
+    total_pos = x2->total_pos;
+    nk_sum = x2->nk_sum;
+  } else {
+    uint64_t* kbw = scr.alloc<uint64_t>(n_jobs + 1);
+    uint64_t* cww = scr.alloc<uint64_t>(n_jobs + 1);
+    uint64_t* tot = scr.alloc<uint64_t>(3);
+    GOD_CUDA(cudaMemsetAsync(tot + 2, 0, sizeof(uint64_t), st));
+    GOD_LAUNCH("k_x2_sizes", k_x2_sizes, grid_for(n_jobs, 256), 256, 0, st, jobs, n_jobs, K, W, kbw, cww,
+               reinterpret_cast<unsigned long long*>(tot + 2));
+    scan_exclusive_u64(kbw, kbw, n_jobs, tot, st, scr, "scan_x2_jobs");
+    scan_exclusive_u64(cww, cww, n_jobs, tot + 1, st, scr, "scan_x2_jobs");
+    GOD_CUDA(cudaMemcpyAsync(kbw + n_jobs, tot, sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
+    GOD_CUDA(cudaMemcpyAsync(cww + n_jobs, tot + 1, sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
+    uint64_t htot[3];
+    d2h_small(htot, tot, sizeof(htot), st);
+    kb = kbw;
+    cw = cww;
+    total_pos = htot[0];
+    nk_sum = htot[2];
+  }
+  prof_add_units(tag, nk_sum);
   const uint64_t total_blocks = total_pos / W;
   const uint64_t ntiles = (total_blocks + X2_OUT_BLOCKS - 1) / X2_OUT_BLOCKS;
   GOD_REQUIRE(ntiles < 0x7FFFFFFFull, "input too large for one extraction launch");

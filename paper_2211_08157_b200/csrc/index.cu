@@ -1060,7 +1060,7 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
   JobSet js = make_jobs(P, ref_offsets, n_refs, nullptr, 0, 0, true, st, scr);
   Records rec;
   const uint64_t est = js.total_pos / (uint64_t)(P.w + 1) * 2 + js.total_pos / 8 + 4096;
-  run_extract(P, ref, js.seq_bytes, js.jobs, js.kb, js.n, js.total_pos, false, false, rec, st, scr, est, "extract_ref");
+  run_extract(P, ref, js.seq_bytes, js.jobs, js.kb, js.n, js.total_pos, false, false, rec, st, scr, est, "extract_ref", js.x2p());
   const uint64_t n = rec.n;
   // K2: stable LSD radix sort on the 2k hash bits
   uint64_t* k0 = rec.hz;

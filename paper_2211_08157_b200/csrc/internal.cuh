@@ -28,28 +28,41 @@ struct Records {
   uint32_t* beg = nullptr;
 };
 
+// Layout of the jobs for the specialised kernel (extract2.cu), when make_jobs built it: kb = exclusive
+// scan of the k-mer counts padded to multiples of w, cw = exclusive scan of the 16-base code words
+// (both with the total at [n]); nk_sum = the k-mer starts.
+struct X2Layout {
+  const uint64_t* kb = nullptr;
+  const uint64_t* cw = nullptr;
+  uint64_t total_pos = 0, nk_sum = 0;
+};
+// true iff run_extract2 has a specialised kernel for these parameters
+bool x2_supported(const Params& P);
+
 // Run the fused sparsify + minimizer kernel over device jobs (kb = exclusive scan of nk + 1,
-// total_pos = kb[n_jobs]).  Allocates rec arrays from `scr` (capacity grown on demand), fills
-// rec.n (synchronizes once to read the count).
+// total_pos = kb[n_jobs]; both unused when x2 carries the specialised layout).  Allocates rec arrays
+// from `scr` (capacity grown on demand), fills rec.n (synchronizes once to read the count).
 void run_extract(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const Job* jobs, const uint64_t* kb,
                  uint32_t n_jobs, uint64_t total_pos, bool want_job, bool want_job_off, Records& rec, cudaStream_t st,
-                 Scratch& scr, uint64_t cap_hint, const char* tag = "k_extract");
+                 Scratch& scr, uint64_t cap_hint, const char* tag = "k_extract", const X2Layout* x2 = nullptr);
 // Specialised register-resident kernel (extract2.cu) for x == 1 patterns of period 1 to 3 (and the
 // '110' / '1110' shapes) and (k, w) in {(21,11), (19,19), (15,10), (19,16)}; returns false if not
 // applicable.
 bool run_extract2(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const Job* jobs, uint32_t n_jobs,
                   bool want_job, bool want_job_off, Records& rec, cudaStream_t st, Scratch& scr,
-                  uint64_t cap_hint, const char* tag);
+                  uint64_t cap_hint, const char* tag, const X2Layout* x2 = nullptr);
 
 // Build jobs for n sequences: phase from `phases` (nullable -> 0) or, if p_all != 0, one job per
 // (sequence, s) for s < p_all (job index = seq * p_all + s).  nk capped at kcap (0 = no cap).
 // Returns device jobs, kb (exclusive scan of nk+1) and total positions.
 struct JobSet {
   Job* jobs = nullptr;
-  uint64_t* kb = nullptr;
+  uint64_t* kb = nullptr;   // generic layout (null when x2 is set: the specialised kernel runs)
   uint32_t n = 0;
   uint64_t total_pos = 0;
   uint64_t seq_bytes = 0;   // offsets[n_seqs]: bytes of the sequence buffer
+  X2Layout x2;              // specialised layout, built in the same pass when x2_supported(P)
+  const X2Layout* x2p() const { return x2.kb ? &x2 : nullptr; }
 };
 JobSet make_jobs(const Params& P, const uint64_t* offsets, uint32_t n_seqs, const uint8_t* phases, uint32_t p_all,
                  uint32_t kcap, bool global_pos, cudaStream_t st, Scratch& scr);

@@ -314,7 +314,7 @@ uint64_t seed_reads(const god_index* ix, const uint8_t* reads, const uint64_t* o
       const uint32_t kcap = (t + 1) * (uint32_t)P.w + (uint32_t)P.w;
       js1 = make_jobs(P, offsets, n_reads, nullptr, p, kcap, false, st, scr);
       run_extract(P, reads, js1.seq_bytes, js1.jobs, js1.kb, js1.n, js1.total_pos, false, true, rec1, st, scr,
-                  js1.total_pos / (uint64_t)(P.w + 1) * 2 + js1.total_pos / 8 + 4096, "extract_phase");
+                  js1.total_pos / (uint64_t)(P.w + 1) * 2 + js1.total_pos / 8 + 4096, "extract_phase", js1.x2p());
       uint32_t* redo = scr.alloc<uint32_t>(n_reads);
       uint32_t* n_redo = scr.alloc<uint32_t>(1);
       GOD_CUDA(cudaMemsetAsync(n_redo, 0, sizeof(uint32_t), st));
@@ -354,7 +354,7 @@ uint64_t seed_reads(const god_index* ix, const uint8_t* reads, const uint64_t* o
     if (h3 == n_reads) {  // every read: phase-a jobs in read order
       JobSet js3 = make_jobs(P, offsets, n_reads, phases, 0, 0, false, st, scr);
       run_extract(P, reads, js3.seq_bytes, js3.jobs, js3.kb, js3.n, js3.total_pos, false, true, rec3, st, scr,
-                  js3.total_pos / (uint64_t)(P.w + 1) * 2 + js3.total_pos / 8 + 4096, "extract_seed");
+                  js3.total_pos / (uint64_t)(P.w + 1) * 2 + js3.total_pos / 8 + 4096, "extract_seed", js3.x2p());
       GOD_LAUNCH("k_iota_src3", k_iota_src3, grid_for(n_reads, 256), 256, 0, st, n_reads, src, srcj);
     } else {
       Job* jobs3 = scr.alloc<Job>(h3);
