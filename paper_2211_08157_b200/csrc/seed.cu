@@ -30,7 +30,7 @@ namespace {
 __global__ void k_phase(const uint32_t* __restrict__ occ, const Job* __restrict__ jobs, const uint64_t* __restrict__ job_off,
                         const uint64_t* __restrict__ hz, const uint32_t* __restrict__ pos, const uint32_t* __restrict__ ids,
                         uint32_t n_reads, uint32_t p, uint32_t t, uint32_t w, uint32_t kcap, Pattern pat, int k,
-                        uint8_t* phases, uint32_t* redo, uint32_t* n_redo) {
+                        uint8_t* phases, uint32_t* redo, uint32_t* n_redo, uint64_t* acount) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_reads; i += gridDim.x * blockDim.x) {
     const uint32_t r = ids ? ids[i] : i;
     uint64_t nmin = ~0ull;
@@ -68,6 +68,12 @@ __global__ void k_phase(const uint32_t* __restrict__ occ, const Job* __restrict_
       if (s == 0 || sc > best) { best = sc; a = s; }
     }
     phases[r] = (uint8_t)a;
+    if (acount) {  // anchors of the read if PQ_a's records are this phase job's (the S4 fast path)
+      const uint64_t j = (uint64_t)i * p + a;
+      uint64_t na = 0;
+      for (uint64_t q = job_off[j]; q < job_off[j + 1]; q++) na += occ[q];
+      acount[r] = na;
+    }
   }
 }
 
@@ -304,6 +310,7 @@ uint64_t seed_reads(const god_index* ix, const uint8_t* reads, const uint64_t* o
   GOD_CUDA(cudaMemsetAsync(src, 0, n_reads, st));
   // ---------------- S1/S2: pattern alignment
   bool have_phase_records = false;
+  bool counted = false;  // k_phase wrote each read's phase-a anchor count into anchor_offsets
   uint32_t nr = 0;
   Records rec1, rec2, rec3;
   JobSet js1;
@@ -320,7 +327,8 @@ uint64_t seed_reads(const god_index* ix, const uint8_t* reads, const uint64_t* o
       GOD_CUDA(cudaMemsetAsync(n_redo, 0, sizeof(uint32_t), st));
       probe_all(v, rec1, st, scr);
       GOD_LAUNCH("k_phase", k_phase, grid_for(n_reads, 128), 128, 0, st, rec1.cnt, js1.jobs, rec1.job_off, rec1.hz,
-                 rec1.pos, nullptr, n_reads, p, t, P.w, kcap, P.pat, P.k, phases, redo, n_redo);
+                 rec1.pos, nullptr, n_reads, p, t, P.w, kcap, P.pat, P.k, phases, redo, n_redo, anchor_offsets);
+      counted = true;
       nr = d2h_scalar(n_redo, st);
       if (nr) {  // uncapped phase selection for reads whose capped prefix was not enough
         Job* jobs2 = scr.alloc<Job>((uint64_t)nr * p);
@@ -337,7 +345,7 @@ uint64_t seed_reads(const god_index* ix, const uint8_t* reads, const uint64_t* o
         GOD_CUDA(cudaMemsetAsync(n_redo2, 0, sizeof(uint32_t), st));
         probe_all(v, rec2, st, scr);
         GOD_LAUNCH("k_phase", k_phase, grid_for(nr, 128), 128, 0, st, rec2.cnt, jobs2, rec2.job_off, rec2.hz, rec2.pos,
-                   redo, nr, p, t, P.w, 0, P.pat, P.k, phases, redo, n_redo2);
+                   redo, nr, p, t, P.w, 0, P.pat, P.k, phases, redo, n_redo2, nullptr);
         GOD_LAUNCH("k_redo_src", k_redo_src, grid_for(nr, 256), 256, 0, st, nr, p, redo, phases, src, srcj);
       }
       have_phase_records = true;
@@ -375,8 +383,9 @@ uint64_t seed_reads(const god_index* ix, const uint8_t* reads, const uint64_t* o
   if (have_phase_records && nr == 0 && h3 == 0) {
     // ---------------- S4 fast path: every read's PQ_a records are its phase-a job of S1
     uint64_t* total = scr.alloc<uint64_t>(1);
-    GOD_LAUNCH("k_read_anchor_counts", k_read_anchor_counts1, grid_for((uint64_t)n_reads * RG, 256), 256, 0, st,
-               rec1.cnt, rec1.job_off, phases, p, n_reads, anchor_offsets);
+    if (!counted)
+      GOD_LAUNCH("k_read_anchor_counts", k_read_anchor_counts1, grid_for((uint64_t)n_reads * RG, 256), 256, 0, st,
+                 rec1.cnt, rec1.job_off, phases, p, n_reads, anchor_offsets);
     scan_exclusive_u64(anchor_offsets, anchor_offsets, n_reads, total, st, scr, "scan_read_anchors");
     GOD_CUDA(cudaMemcpyAsync(anchor_offsets + n_reads, total, sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
     const uint64_t tot = d2h_scalar(total, st);
