@@ -456,7 +456,9 @@ def run_e2e(god, torch, cfg, pattern, k, w, n_anchors, steps, dist, world, dev):
     hroffs = torch.from_numpy(cfg.reads.offsets).pin_memory()
     n = cfg.reads.n
     n_anchors = int(n_anchors * 1.02) + 1024  # slack; the path is deterministic
-    an_host = torch.empty(n_anchors * 4 + 4, dtype=torch.uint32).pin_memory()
+    # god_anchor_compact (8 B: ref_pos, read_pos | strand << 31; the read id is implied by the anchor
+    # offsets): the same result as god_seed_reads' 16-B anchors at half the D2H bytes
+    an_host = torch.empty(n_anchors * 2 + 2, dtype=torch.uint32).pin_memory()
     ao_host = torch.empty(n + 1, dtype=torch.uint64).pin_memory()
     ph_host = torch.empty(max(1, n), dtype=torch.uint8).pin_memory()
     import ctypes
@@ -491,7 +493,7 @@ def run_e2e(god, torch, cfg, pattern, k, w, n_anchors, steps, dist, world, dev):
         _lib.check(L.god_build_index(ctypes.byref(prm), vp(dref.data_ptr()), vp(droff.data_ptr()), 1,
                                      ctypes.byref(cut), ctypes.byref(h), stream))
         main.wait_stream(side)
-        _lib.check(L.god_seed_reads(h, vp(dreads.data_ptr()), vp(droffs.data_ptr()), n, _lib.PHASE_SELECT,
+        _lib.check(L.god_seed_reads_compact(h, vp(dreads.data_ptr()), vp(droffs.data_ptr()), n, _lib.PHASE_SELECT,
                                     vp(ph_host.data_ptr()), 16, vp(an_host.data_ptr()), vp(ao_host.data_ptr()),
                                     n_anchors, ctypes.byref(need), stream))
         return h
@@ -513,9 +515,10 @@ def run_e2e(god, torch, cfg, pattern, k, w, n_anchors, steps, dist, world, dev):
     log(f"e2e wall ms per step: {walls}")
     ms = max_over_ranks(ms, dist, dev)
     h2d = cfg.ref.size + cfg.ref_offsets.nbytes + cfg.reads.seq.size + cfg.reads.offsets.nbytes
-    d2h = int(need.value) * 16 + (n + 1) * 8 + n
+    d2h = int(need.value) * 8 + (n + 1) * 8 + n
     return {"value": round(world * n / (ms / steps / 1e3), 1), "unit": "reads/s", "h2d_bytes_per_step": int(h2d),
-            "d2h_bytes_per_step": int(d2h), "steps": steps, "ms_per_step": round(ms / steps, 3)}
+            "d2h_bytes_per_step": int(d2h), "steps": steps, "ms_per_step": round(ms / steps, 3),
+            "outputs": "phases u8[n], anchor_offsets u64[n+1], god_anchor_compact[n_anchors] (8 B)"}
 
 
 def run_reference(args, world, rank):

@@ -152,6 +152,20 @@ GOD_API god_status god_seed_reads(const god_index* idx, const uint8_t* reads, co
                                   god_anchor* anchors, uint64_t* anchor_offsets, uint64_t cap, uint64_t* needed,
                                   god_stream stream);
 
+/* The same seeding with 8-byte anchors for transfers: the read id is implied by anchor_offsets
+ * (anchors of read r occupy [anchor_offsets[r], anchor_offsets[r+1])), and the strand is bit 31 of
+ * read_pos_strand (read positions must be < 2^31, else GOD_EINVAL after the call's device work).
+ * Same order, conventions and errors as god_seed_reads. */
+typedef struct {
+    uint32_t ref_pos;
+    uint32_t read_pos_strand;   /* read_pos | strand << 31 */
+} god_anchor_compact;
+
+GOD_API god_status god_seed_reads_compact(const god_index* idx, const uint8_t* reads, const uint64_t* read_offsets,
+                                          uint32_t n_reads, god_phase_mode mode, uint8_t* phases, uint32_t t,
+                                          god_anchor_compact* anchors, uint64_t* anchor_offsets, uint64_t cap,
+                                          uint64_t* needed, god_stream stream);
+
 /* ---- location voting (section 3.4, Fig. 8; rescue P:398) ----
  * Consumes the anchors of god_seed_reads (same reads, same phases).  Readings (DESIGN.md §2,
  * V1-V6):

@@ -23,6 +23,8 @@ except Exception:  # pragma: no cover - torch is in the image
     torch = None
 
 ANCHOR_DTYPE = np.dtype([("ref_pos", "<u4"), ("read_pos", "<u4"), ("read_id", "<u4"), ("strand", "<u4")])
+# god_anchor_compact: 8 bytes, read id implied by the anchor offsets, strand in bit 31
+ANCHOR_COMPACT_DTYPE = np.dtype([("ref_pos", "<u4"), ("read_pos_strand", "<u4")])
 # god_vote (include/god.h): 40 bytes; the device path returns it as a (n, 10) u32 tensor (diag = words 2-3)
 VOTE_DTYPE = np.dtype([("read_id", "<u4"), ("strand", "<u4"), ("diag", "<i8"), ("votes", "<u4"), ("rescued", "<u4"),
                        ("ref_lo", "<u4"), ("ref_hi", "<u4"), ("read_lo", "<u4"), ("read_hi", "<u4")])
@@ -201,13 +203,15 @@ def god_build_index(ref, ref_offsets, pattern: str, k: int, w: int, cutoff=(1, 5
 
 # ---------------------------------------------------------------------------------------- stage 4
 def god_seed_reads(index: GodIndex, reads, read_offsets, phases=None, t: int = 16, cap: int | None = None,
-                   out=None, host_out: bool = False):
+                   out=None, host_out: bool = False, compact: bool = False):
     """SELECT mode if phases is None (phase per read computed), else GIVEN.
     -> (anchors, anchor_offsets u64[n+1], phases u8[n]).  Device path: anchors is a CUDA u32 tensor
     of shape (n_anchors, 4) = (ref_pos, read_pos, read_id, strand); host path: structured numpy.
     out = (anchors, anchor_offsets, phases) preallocated (device path; anchors (cap, 4) u32) avoids
     per-call allocations in a serving loop.  host_out=True with CUDA reads returns host (numpy) outputs:
-    the library then streams the results of read batches back while later batches are seeded."""
+    the library then streams the results of read batches back while later batches are seeded.
+    compact=True: 8-byte god_anchor_compact anchors ((n, 2) u32 tensor / ANCHOR_COMPACT_DTYPE;
+    expand_compact() restores the full form)."""
     L = _lib.load()
     dev = _is_cuda(reads) and not host_out
     reads, read_offsets = _prep(reads, np.uint8), _prep(read_offsets, np.uint64)
@@ -232,9 +236,10 @@ def god_seed_reads(index: GodIndex, reads, read_offsets, phases=None, t: int = 1
         if an_out is not None and cap <= int(an_out.shape[0]):
             an = an_out
         else:
-            an = torch.empty((max(1, cap), 4), dtype=torch.uint32, device=dv) if dev else \
-                np.zeros(max(1, cap), ANCHOR_DTYPE)
-        rc = L.god_seed_reads(index.handle, _ptr(reads), _ptr(read_offsets), n, mode, _ptr(ph), int(t), _ptr(an),
+            an = torch.empty((max(1, cap), 2 if compact else 4), dtype=torch.uint32, device=dv) if dev else \
+                np.zeros(max(1, cap), ANCHOR_COMPACT_DTYPE if compact else ANCHOR_DTYPE)
+        fn = L.god_seed_reads_compact if compact else L.god_seed_reads
+        rc = fn(index.handle, _ptr(reads), _ptr(read_offsets), n, mode, _ptr(ph), int(t), _ptr(an),
                               _ptr(ao), cap, ctypes.byref(need), st)
         if rc == _lib.GOD_ETRUNC:
             cap = need.value
@@ -243,6 +248,23 @@ def god_seed_reads(index: GodIndex, reads, read_offsets, phases=None, t: int = 1
         _lib.check(rc)
         return an[: need.value], ao, ph[:n]
     raise GodError(_lib.GOD_ETRUNC, "anchor capacity retry failed")
+
+
+def expand_compact(anchors, anchor_offsets) -> np.ndarray:
+    """god_anchor_compact (host or device) -> ANCHOR_DTYPE on the host (argument marshalling for
+    callers and tests: the read id is the anchor's segment in anchor_offsets)."""
+    if torch is not None and isinstance(anchors, torch.Tensor):
+        a = anchors.cpu().numpy().view(ANCHOR_COMPACT_DTYPE).reshape(-1)
+    else:
+        a = np.asarray(anchors).view(ANCHOR_COMPACT_DTYPE).reshape(-1)
+    ao = anchor_offsets.cpu().numpy() if torch is not None and isinstance(anchor_offsets, torch.Tensor) \
+        else np.asarray(anchor_offsets)
+    out = np.zeros(a.size, ANCHOR_DTYPE)
+    out["ref_pos"] = a["ref_pos"]
+    out["read_pos"] = a["read_pos_strand"] & 0x7FFFFFFF
+    out["strand"] = a["read_pos_strand"] >> 31
+    out["read_id"] = np.repeat(np.arange(ao.size - 1, dtype=np.uint32), np.diff(ao.astype(np.int64)))
+    return out
 
 
 # ---------------------------------------------------------------------------------------- voting
@@ -381,4 +403,4 @@ def launch_count() -> int:
 __all__ = ["god_sparsify", "god_minimizers", "god_build_index", "god_seed_reads", "god_vote_reads", "votes_numpy",
            "god_contain", "god_seed_harness",
            "god_harness_accepted",
-           "GodIndex", "GodError", "ANCHOR_DTYPE", "VOTE_DTYPE", "version"]
+           "expand_compact", "GodIndex", "GodError", "ANCHOR_DTYPE", "ANCHOR_COMPACT_DTYPE", "VOTE_DTYPE", "version"]

@@ -213,6 +213,16 @@ __global__ void k_rebase_u64(uint64_t* a, uint64_t n, uint64_t base, uint64_t ad
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
     a[i] = a[i] - base + add;
 }
+// god_anchor -> god_anchor_compact (the read id is implied by the anchor offsets); a read position
+// >= 2^31 cannot carry the strand bit
+__global__ void k_compact_anchors(const god_anchor* __restrict__ in, uint64_t n, god_anchor_compact* __restrict__ out,
+                                  uint32_t* bad) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const god_anchor a = in[i];
+    if (a.read_pos >> 31) atomicAdd(bad, 1u);
+    out[i] = god_anchor_compact{a.ref_pos, a.read_pos | (a.strand << 31)};
+  }
+}
 __global__ void k_check_phases(const uint8_t* ph, uint32_t n, uint32_t p, uint32_t* bad) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     if (ph[i] >= p) atomicAdd(bad, 1u);
@@ -238,6 +248,8 @@ struct PipeSlot {
   uint64_t* aoff = nullptr;
   god_anchor* an = nullptr;
   uint64_t an_cap = 0;
+  god_anchor_compact* anc = nullptr;
+  uint64_t anc_cap = 0;
   cudaEvent_t h2d_done = nullptr, comp_done = nullptr, d2h_done = nullptr;
   bool d2h_pending = false;
 };
@@ -251,9 +263,9 @@ void grow(T*& p, uint64_t& cap, uint64_t need, cudaStream_t st) {
 }  // namespace
 
 static uint64_t seed_reads_pipelined(const god_index* idx, const uint8_t* reads, const uint64_t* offs, uint32_t n_reads,
-                                     god_phase_mode mode, uint8_t* phases, uint32_t t, god_anchor* anchors,
+                                     god_phase_mode mode, uint8_t* phases, uint32_t t, void* anchors,
                                      uint64_t* anchor_offsets, uint64_t cap, uint32_t n_batches, cudaStream_t st,
-                                     bool reads_on_device) {
+                                     bool reads_on_device, bool compact, uint32_t* bad_compact) {
   static cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
   if (!s_h2d) {
     GOD_CUDA(cudaStreamCreateWithFlags(&s_h2d, cudaStreamNonBlocking));
@@ -323,10 +335,20 @@ static uint64_t seed_reads_pipelined(const god_index* idx, const uint8_t* reads,
     }
     // offsets of this batch -> global anchor offsets
     GOD_LAUNCH("k_rebase", k_rebase_u64, grid_for(nb + 1, 256), 256, 0, st, sl.aoff, nb + 1, 0ull, written);
+    const void* src = sl.an;
+    size_t asz = sizeof(god_anchor);
+    if (compact && tot && tot <= sl.an_cap) {  // 8-B anchors leave the device: half the copy
+      grow(sl.anc, sl.anc_cap, tot, st);
+      GOD_LAUNCH("k_compact_anchors", k_compact_anchors, grid_for(tot, 256), 256, 0, st, sl.an, tot, sl.anc,
+                 bad_compact);
+      src = sl.anc;
+      asz = sizeof(god_anchor_compact);
+    }
     GOD_CUDA(cudaEventRecord(sl.comp_done, st));
     GOD_CUDA(cudaStreamWaitEvent(s_d2h, sl.comp_done, 0));
     if (written + tot <= cap && tot)
-      GOD_CUDA(cudaMemcpyAsync(anchors + written, sl.an, tot * sizeof(god_anchor), cudaMemcpyDeviceToHost, s_d2h));
+      GOD_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(anchors) + written * asz, src, tot * asz, cudaMemcpyDeviceToHost,
+                               s_d2h));
     GOD_CUDA(cudaMemcpyAsync(anchor_offsets + r0, sl.aoff, (nb + 1) * sizeof(uint64_t), cudaMemcpyDeviceToHost, s_d2h));
     if (mode == GOD_PHASE_SELECT && nb) GOD_CUDA(cudaMemcpyAsync(phases + r0, sl.ph, nb, cudaMemcpyDeviceToHost, s_d2h));
     GOD_CUDA(cudaEventRecord(sl.d2h_done, s_d2h));
@@ -341,6 +363,7 @@ static uint64_t seed_reads_pipelined(const god_index* idx, const uint8_t* reads,
     if (sl.ph) cudaFreeAsync(sl.ph, st);
     if (sl.aoff) cudaFreeAsync(sl.aoff, st);
     if (sl.an) cudaFreeAsync(sl.an, st);
+    if (sl.anc) cudaFreeAsync(sl.anc, st);
     cudaEventDestroy(sl.h2d_done);
     cudaEventDestroy(sl.comp_done);
     cudaEventDestroy(sl.d2h_done);
@@ -537,56 +560,87 @@ GOD_API void god_index_free(god_index* idx) {
   delete idx;
 }
 
+static void seed_entry(const god_index* idx, const uint8_t* reads, const uint64_t* read_offsets, uint32_t n_reads,
+                       god_phase_mode mode, uint8_t* phases, uint32_t t, void* anchors, bool compact,
+                       uint64_t* anchor_offsets, uint64_t cap, uint64_t* needed, god_stream stream) {
+  GOD_REQUIRE(idx && read_offsets && phases && anchor_offsets && needed, "NULL argument");
+  GOD_REQUIRE(mode == GOD_PHASE_SELECT || mode == GOD_PHASE_GIVEN, "mode must be SELECT or GIVEN");
+  GOD_REQUIRE(t >= 1, "t must be >= 1");
+  GOD_REQUIRE(cap == 0 || anchors, "NULL anchors with nonzero capacity");
+  if (mode == GOD_PHASE_GIVEN && !is_device_ptr(phases))
+    for (uint32_t i = 0; i < n_reads; i++) GOD_REQUIRE(phases[i] < idx->P.pat.p, "phase >= p");
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t asz = compact ? sizeof(god_anchor_compact) : sizeof(god_anchor);
+  // all-host buffers and a large batch: pipelined transfers (see seed_reads_pipelined)
+  const char* pm = getenv("GOD_PIPE_MIN_READS");  // test hook: smaller batches
+  const uint32_t pipe_min = pm ? (uint32_t)atoi(pm) : (1u << 20);  // reads per batch
+  const uint32_t n_batches = std::min<uint32_t>(8u, n_reads / (pipe_min ? pipe_min : 1u));
+  // reads and their offsets both on the host, or both on the device (then only the results are
+  // streamed back); phases, anchor offsets and anchors on the host
+  const bool rdev = is_device_ptr(reads), odev = is_device_ptr(read_offsets);
+  if (n_batches >= 2 && rdev == odev && !is_device_ptr(phases) && !is_device_ptr(anchor_offsets) &&
+      (!anchors || !is_device_ptr(anchors))) {
+    Scratch scr(st);
+    uint32_t* bad = scr.alloc<uint32_t>(1);
+    GOD_CUDA(cudaMemsetAsync(bad, 0, 4, st));
+    const uint64_t tot = seed_reads_pipelined(idx, reads, read_offsets, n_reads, mode, phases, t, anchors,
+                                              anchor_offsets, anchors ? cap : 0, n_batches, st, rdev, compact, bad);
+    *needed = tot;
+    if (compact) GOD_REQUIRE(d2h_scalar(bad, st) == 0, "compact anchors need read positions < 2^31");
+    if (tot > cap) throw Fail{GOD_ETRUNC};
+    return;
+  }
+  Scratch scr(st);
+  Stage sg(st, scr);
+  const uint64_t L = total_len(read_offsets, n_reads, st);
+  const uint8_t* dreads = sg.in(reads, L);
+  const uint64_t* doff = sg.in(read_offsets, (size_t)n_reads + 1);
+  uint8_t* dph = mode == GOD_PHASE_GIVEN ? sg.inout(phases, n_reads) : sg.out(phases, n_reads);
+  if (mode == GOD_PHASE_GIVEN && is_device_ptr(phases) && n_reads) {
+    uint32_t* bad = scr.alloc<uint32_t>(1);
+    GOD_CUDA(cudaMemsetAsync(bad, 0, 4, st));
+    GOD_LAUNCH("k_check_phases", k_check_phases, grid_for(n_reads, 256), 256, 0, st, dph, n_reads, idx->P.pat.p, bad);
+    GOD_REQUIRE(d2h_scalar(bad, st) == 0, "phase >= p");
+  }
+  uint64_t* dao = sg.out(anchor_offsets, (size_t)n_reads + 1);
+  // anchors: a device god_anchor buffer (the caller's, or staging for host / compact outputs)
+  const bool host_anchors = anchors && !is_device_ptr(anchors);
+  god_anchor* dan = (!compact && !host_anchors) ? static_cast<god_anchor*>(anchors)
+                                                : (cap ? scr.alloc<god_anchor>(cap) : nullptr);
+  const uint64_t tot = god::seed_reads(idx, dreads, doff, n_reads, mode, dph, t, dan, dao, cap, st);
+  *needed = tot;
+  if (tot <= cap && tot) {
+    const void* src = dan;
+    if (compact) {
+      god_anchor_compact* dc = host_anchors ? scr.alloc<god_anchor_compact>(tot)
+                                            : static_cast<god_anchor_compact*>(anchors);
+      uint32_t* bad = scr.alloc<uint32_t>(1);
+      GOD_CUDA(cudaMemsetAsync(bad, 0, 4, st));
+      GOD_LAUNCH("k_compact_anchors", k_compact_anchors, grid_for(tot, 256), 256, 0, st, dan, tot, dc, bad);
+      GOD_REQUIRE(d2h_scalar(bad, st) == 0, "compact anchors need read positions < 2^31");
+      src = dc;
+    }
+    if (host_anchors) GOD_CUDA(cudaMemcpyAsync(anchors, src, tot * asz, cudaMemcpyDeviceToHost, st));
+  }
+  sg.finish();
+  if (tot > cap) throw Fail{GOD_ETRUNC};
+}
+
 GOD_API god_status god_seed_reads(const god_index* idx, const uint8_t* reads, const uint64_t* read_offsets,
                                   uint32_t n_reads, god_phase_mode mode, uint8_t* phases, uint32_t t,
                                   god_anchor* anchors, uint64_t* anchor_offsets, uint64_t cap, uint64_t* needed,
                                   god_stream stream) {
   return guarded([&] {
-    GOD_REQUIRE(idx && read_offsets && phases && anchor_offsets && needed, "NULL argument");
-    GOD_REQUIRE(mode == GOD_PHASE_SELECT || mode == GOD_PHASE_GIVEN, "mode must be SELECT or GIVEN");
-    GOD_REQUIRE(t >= 1, "t must be >= 1");
-    GOD_REQUIRE(cap == 0 || anchors, "NULL anchors with nonzero capacity");
-    if (mode == GOD_PHASE_GIVEN && !is_device_ptr(phases))
-      for (uint32_t i = 0; i < n_reads; i++) GOD_REQUIRE(phases[i] < idx->P.pat.p, "phase >= p");
-    cudaStream_t st = (cudaStream_t)stream;
-    // all-host buffers and a large batch: pipelined transfers (see seed_reads_pipelined)
-    const char* pm = getenv("GOD_PIPE_MIN_READS");  // test hook: smaller batches
-    const uint32_t pipe_min = pm ? (uint32_t)atoi(pm) : (1u << 20);  // reads per batch
-    const uint32_t n_batches = std::min<uint32_t>(8u, n_reads / (pipe_min ? pipe_min : 1u));
-    // reads and their offsets both on the host, or both on the device (then only the results are
-    // streamed back); phases, anchor offsets and anchors on the host
-    const bool rdev = is_device_ptr(reads), odev = is_device_ptr(read_offsets);
-    if (n_batches >= 2 && rdev == odev && !is_device_ptr(phases) && !is_device_ptr(anchor_offsets) &&
-        (!anchors || !is_device_ptr(anchors))) {
-      const uint64_t tot = seed_reads_pipelined(idx, reads, read_offsets, n_reads, mode, phases, t, anchors,
-                                                anchor_offsets, anchors ? cap : 0, n_batches, st, rdev);
-      *needed = tot;
-      if (tot > cap) throw Fail{GOD_ETRUNC};
-      return;
-    }
-    Scratch scr(st);
-    Stage sg(st, scr);
-    const uint64_t L = total_len(read_offsets, n_reads, st);
-    const uint8_t* dreads = sg.in(reads, L);
-    const uint64_t* doff = sg.in(read_offsets, (size_t)n_reads + 1);
-    uint8_t* dph = mode == GOD_PHASE_GIVEN ? sg.inout(phases, n_reads) : sg.out(phases, n_reads);
-    if (mode == GOD_PHASE_GIVEN && is_device_ptr(phases) && n_reads) {
-      uint32_t* bad = scr.alloc<uint32_t>(1);
-      GOD_CUDA(cudaMemsetAsync(bad, 0, 4, st));
-      GOD_LAUNCH("k_check_phases", k_check_phases, grid_for(n_reads, 256), 256, 0, st, dph, n_reads, idx->P.pat.p, bad);
-      GOD_REQUIRE(d2h_scalar(bad, st) == 0, "phase >= p");
-    }
-    uint64_t* dao = sg.out(anchor_offsets, (size_t)n_reads + 1);
-    // anchors: if host, stage at full capacity only when it fits
-    god_anchor* dan = anchors;
-    const bool host_anchors = anchors && !is_device_ptr(anchors);
-    if (host_anchors) dan = scr.alloc<god_anchor>(cap);
-    const uint64_t tot = god::seed_reads(idx, dreads, doff, n_reads, mode, dph, t, dan, dao, cap, st);
-    *needed = tot;
-    if (host_anchors && tot <= cap && tot)
-      GOD_CUDA(cudaMemcpyAsync(anchors, dan, tot * sizeof(god_anchor), cudaMemcpyDeviceToHost, st));
-    sg.finish();
-    if (tot > cap) throw Fail{GOD_ETRUNC};
+    seed_entry(idx, reads, read_offsets, n_reads, mode, phases, t, anchors, false, anchor_offsets, cap, needed, stream);
+  });
+}
+
+GOD_API god_status god_seed_reads_compact(const god_index* idx, const uint8_t* reads, const uint64_t* read_offsets,
+                                          uint32_t n_reads, god_phase_mode mode, uint8_t* phases, uint32_t t,
+                                          god_anchor_compact* anchors, uint64_t* anchor_offsets, uint64_t cap,
+                                          uint64_t* needed, god_stream stream) {
+  return guarded([&] {
+    seed_entry(idx, reads, read_offsets, n_reads, mode, phases, t, anchors, true, anchor_offsets, cap, needed, stream);
   });
 }
 

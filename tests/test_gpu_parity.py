@@ -308,6 +308,39 @@ def test_seed_host_pipelined_batches(given, reads_dev, monkeypatch):
     assert np.array_equal(canon(an), canon(oan))
 
 
+@pytest.mark.parametrize("where", ["device", "host", "host_pipelined", "reads_dev_pipelined"])
+def test_seed_compact_anchors(where, monkeypatch):
+    """god_seed_reads_compact: the 8-byte anchors expand (read id from the offsets, strand from bit
+    31) to exactly god_seed_reads' anchors, in the same order, on every buffer path; a too-small
+    capacity reports the needed count and the retry matches too."""
+    if where.endswith("pipelined"):
+        monkeypatch.setenv("GOD_PIPE_MIN_READS", "97")
+    rng = np.random.default_rng(41)
+    ref = synth.dup_genome(300_000, 19, dup_frac=0.2, lmin=300, lmax=2000)
+    roffs_ref = np.array([0, ref.size], np.uint64)
+    reads = synth.simulate_reads(ref, 700, 3, mu=5.5, sigma=1.2, lmin=1, lmax=5000, p_sub=0.01, p_ins=0.005,
+                                 p_del=0.005)
+    seqs = [reads.seq[int(reads.offsets[i]):int(reads.offsets[i + 1])] for i in range(reads.n)]
+    seqs[50:50] = [np.zeros(0, np.uint8), np.frombuffer(b"N" * 300, np.uint8), synth.random_acgt(rng, 2000, 0.3)]
+    rs, ro = synth.concat(seqs)
+    ix = god.god_build_index(cu(ref), cu(roffs_ref), "10", 15, 10, cutoff=(1, 500))
+    ox = oracle.Index(ref, roffs_ref, "10", 15, 10, cutoff=(1, 500))
+    args = {"device": (cu(rs), cu(ro), {}), "host": (rs, ro, {}), "host_pipelined": (rs, ro, {}),
+            "reads_dev_pipelined": (cu(rs), cu(ro), {"host_out": True})}[where]
+    full = god.god_seed_reads(ix, args[0], args[1], **args[2])
+    for cap in (None, 7):
+        cmp_ = god.god_seed_reads(ix, args[0], args[1], compact=True, cap=cap, **args[2])
+        ao = cmp_[1].cpu().numpy() if isinstance(cmp_[1], torch.Tensor) else cmp_[1]
+        fao = full[1].cpu().numpy() if isinstance(full[1], torch.Tensor) else full[1]
+        assert np.array_equal(ao, fao)
+        exp = god.expand_compact(cmp_[0], cmp_[1])
+        fa = full[0].cpu().numpy().view(god.ANCHOR_DTYPE).reshape(-1) if isinstance(full[0], torch.Tensor) \
+            else full[0]
+        assert np.array_equal(exp, fa)
+    oan, oao, _ = ox.seed_reads(rs, ro)
+    assert np.array_equal(canon(exp), canon(oan))
+
+
 # ------------------------------------------------------------------------------------ K1 v2 (specialised)
 X2_COMBOS = [("10", 21, 11), ("01", 21, 11), ("1", 21, 11), ("10", 19, 19), ("1", 19, 19), ("10", 15, 10),
              ("1", 15, 10), ("110", 21, 11), ("1110", 21, 11), ("110", 19, 19), ("1110", 19, 19), ("110", 15, 10),
