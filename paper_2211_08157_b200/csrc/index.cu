@@ -999,8 +999,33 @@ __global__ void __launch_bounds__(DF_NT) k_dir_suffix_min(const uint32_t* dir, u
     if (sl >= n_slots) break;
     const uint32_t a = sd[q], b = sd[q + 1];
     uint32_t kk[DIR_KEYS];
+    if (b - a <= DIR_KEYS) {
 #pragma unroll
-    for (int e = 0; e < DIR_KEYS; e++) kk[e] = a + e < b ? (uint32_t)ent[a + e] >> 1 : 0xFFFFFFFFu;
+      for (int e = 0; e < DIR_KEYS; e++) kk[e] = a + e < b ? (uint32_t)ent[a + e] >> 1 : 0xFFFFFFFFu;
+    } else {
+      // a long slot (frequent hashes: probed in proportion to their counts) holding <= DIR_RUNS
+      // distinct keys: (key, run end) pairs, so its probes also read the record only; more keys:
+      // key[0] = ~0 and the probe searches the entries
+#pragma unroll
+      for (int e = 0; e < DIR_KEYS; e++) kk[e] = (e & 1) ? b : 0xFFFFFFFFu;
+      uint32_t s0 = a;
+      int r = 0;
+      for (; r < DIR_RUNS && s0 < b; r++) {
+        const uint32_t ks = (uint32_t)ent[s0] >> 1;
+        uint32_t lo = s0 + 1, st = 1;  // gallop, then bisect, to the first entry with another key
+        while (lo + st <= b && ((uint32_t)ent[lo + st - 1] >> 1) == ks) { lo += st; st <<= 1; }
+        uint32_t hi = min(lo + st - 1, b);
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (((uint32_t)ent[mid] >> 1) == ks) lo = mid + 1;
+          else hi = mid;
+        }
+        kk[2 * r] = ks;
+        kk[2 * r + 1] = lo;
+        s0 = lo;
+      }
+      if (s0 < b) kk[0] = 0xFFFFFFFFu;
+    }
     uint4* o = reinterpret_cast<uint4*>(rec + sl);
     o[0] = make_uint4(a, b, kk[0], kk[1]);
     o[1] = make_uint4(kk[2], kk[3], kk[4], kk[5]);

@@ -81,9 +81,13 @@ JobSet make_jobs(const Params& P, const uint64_t* offsets, uint32_t n_seqs, cons
 //           minimizer hashes are (they are window minima: dense at small values).
 constexpr int DIR_SEG_BITS = 12;
 constexpr int DIR_KEYS = 6;
+constexpr int DIR_RUNS = DIR_KEYS / 2;
 struct __align__(32) DirRec {
   uint32_t start, end;
-  uint32_t key[DIR_KEYS];  // 0xFFFFFFFF past the end of the slot
+  // end - start <= DIR_KEYS: the keys of the slot's entries, 0xFFFFFFFF past the end.
+  // longer: (key, end of its run) x DIR_RUNS for a slot of <= DIR_RUNS distinct keys (unused pairs
+  // (0xFFFFFFFF, end)); key[0] = 0xFFFFFFFF for more (keys are < 2^31, so ~0 is never one)
+  uint32_t key[DIR_KEYS];
 };
 struct IndexView {
   const DirRec* dir;
@@ -107,7 +111,8 @@ __device__ __forceinline__ uint64_t index_slot(const IndexView& v, uint64_t h) {
 
 // [begin, end) of the kept entries whose hash == h ("examines the presence of the extracted
 // minimizers (their hash values) in the seed index").  The slot record answers a slot of
-// <= DIR_KEYS entries (almost all) from one 32-B sector; a longer slot is searched in the entries.
+// <= DIR_KEYS entries (almost all) or <= DIR_RUNS distinct keys from one 32-B sector; a longer
+// slot is searched in the entries.
 __device__ __forceinline__ uint2 probe_range(const IndexView& v, uint64_t h) {
   const uint64_t slot = index_slot(v, h);
   if (slot == ~0ull) return make_uint2(0, 0);
@@ -125,7 +130,14 @@ __device__ __forceinline__ uint2 probe_range(const IndexView& v, uint64_t h) {
     }
     return make_uint2(lo + below, lo + below + eq);
   }
-  // a longer slot is usually one frequent hash: both ends equal the key -> the whole slot
+  if (r0.z != 0xFFFFFFFFu) {  // <= DIR_RUNS distinct keys: (key, run end) pairs
+    if (key == r0.z) return make_uint2(lo, r0.w);
+    if (key == r1.x) return make_uint2(r0.w, r1.y);
+    if (key == r1.z) return make_uint2(r1.y, r1.w);
+    const uint32_t at = key < r0.z ? lo : key < r1.x ? r0.w : key < r1.z ? r1.y : r1.w;
+    return make_uint2(at, at);
+  }
+  // more keys: both ends equal the key -> the whole slot, else search the entries
   const uint32_t kf = (uint32_t)__ldg(v.ent + lo) >> 1, kl = (uint32_t)__ldg(v.ent + hi - 1) >> 1;
   if (kf == key && kl == key) return make_uint2(lo, hi);
   if (kf > key || kl < key) return make_uint2(lo, lo);

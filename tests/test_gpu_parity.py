@@ -186,6 +186,34 @@ def test_index_parity_homopolymer_heavy():
         _index_parity(ref, offs, "1", 7, 5, cutoff=cut)
 
 
+@pytest.mark.parametrize("mode0", [False, True])
+@pytest.mark.parametrize("k,w", [(21, 11), (15, 10), (9, 5)])
+def test_index_probe_every_hash(k, w, mode0, monkeypatch):
+    """Every kept hash and both its neighbours probed (god_index_count) against the oracle's kept
+    entries: slots of <= 6 entries, long slots of 1-3 distinct keys (answered from the slot
+    record) and of more keys (searched), absent keys between and around the runs."""
+    if mode0:
+        monkeypatch.setenv("GOD_DIR_MODE0", "1")
+    rng = np.random.default_rng(53 + k)
+    base = synth.dup_genome(600_000, 5 + k, dup_frac=0.3, lmin=100, lmax=3000)
+    reps = [synth.random_acgt(rng, int(rng.integers(30, 400))) for _ in range(40)]
+    parts = [base]
+    for i, r in enumerate(reps):  # copy numbers 2..80: hashes of every count up to the cutoff
+        parts += [r] * (2 + 2 * i)
+    ref, offs = synth.concat([np.concatenate(parts)])
+    ix = god.god_build_index(cu(ref), cu(offs), "10", k, w, max_occ=70)
+    ox = oracle.Index(ref, offs, "10", k, w, max_occ=70)
+    oh, _, _ = ox.dump()
+    dist = np.unique(oh)
+    top = np.uint64((1 << (2 * k)) - 1)
+    q = np.unique(np.concatenate([dist, dist + np.uint64(1), dist - np.uint64(1)]))
+    q = q[q <= top]
+    got = np_(ix.count(cu(q)))
+    want = (np.searchsorted(oh, q, side="right") - np.searchsorted(oh, q, side="left")).astype(np.uint32)
+    assert np.array_equal(got, want), np.flatnonzero(got != want)[:10]
+    assert (want > 6).sum() > 100  # frequent hashes present: long slots
+
+
 @pytest.mark.parametrize("env", [{}, {"GOD_BIN_TARGET": "6000"}, {"GOD_BIN_TARGET": "40"}, {"GOD_DIR_MODE0": "1"},
                                  {"GOD_SORT_FULL": "1"}],
                          ids=["default", "big-bins", "tiny-bins", "dir-mode0", "full-lsd"])
