@@ -1189,7 +1189,8 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
   // B hash bits, B = clamp(floor(log2 n_kept), 2k - 31, min(2k, 28)).
   const uint32_t hb = 2 * P.k;
   const bool mode1 = hb >= 14 && hb - DIR_SEG_BITS <= 30 && !getenv("GOD_DIR_MODE0");
-  constexpr uint32_t DIR_TARGET = 2;
+  const char* dt = getenv("GOD_DIR_TARGET");  // test hook: entries per slot
+  const uint32_t DIR_TARGET = dt ? (uint32_t)std::max(1, atoi(dt)) : 2u;
   uint32_t B = 0, low_bits = 0;
   uint64_t n_slots = 0;
   uint2* seg = nullptr;
