@@ -54,6 +54,13 @@ __device__ __forceinline__ uint32_t warp_peers(uint32_t d) {
   return peers;
 }
 
+// bulk L2 prefetch of [p, p + bytes) (16-B aligned, whole 16-B units)
+__device__ __forceinline__ void l2_prefetch_range(const void* p, uint64_t bytes) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p) & ~(uintptr_t)15;
+  const uintptr_t e = (reinterpret_cast<uintptr_t>(p) + bytes + 15) & ~(uintptr_t)15;
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((uint32_t)(e - a)) : "memory");
+}
+
 template <int RB>
 __global__ void __launch_bounds__(RS_NT) k_rs_hist(const uint64_t* __restrict__ keys, uint64_t n, int shift,
                                                    uint32_t dmask, uint32_t* hist, uint32_t ntiles) {
@@ -78,7 +85,7 @@ __global__ void __launch_bounds__(RS2_NT, 2) k_rs_scatter2(const uint64_t* __res
                                                        uint64_t* __restrict__ kout, uint32_t* __restrict__ vout,
                                                        uint64_t n, int shift, uint32_t dmask,
                                                        const uint64_t* __restrict__ goff, uint32_t ntiles,
-                                                       const uint2* __restrict__ table, int L) {
+                                                       const uint2* __restrict__ table, int L, uint32_t ahead) {
   __shared__ uint32_t wcnt[RS2_NT / 32][(1 << RB)];
   __shared__ uint32_t dstart[(1 << RB)];
   __shared__ uint32_t wsum[(1 << RB) / 32];
@@ -87,6 +94,14 @@ __global__ void __launch_bounds__(RS2_NT, 2) k_rs_scatter2(const uint64_t* __res
   uint64_t* sk = reinterpret_cast<uint64_t*>(rs_dyn);
   uint32_t* sv = reinterpret_cast<uint32_t*>(sk + RS_TILE);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid == 0) {  // the tile a CTA launched after the resident wave will take, into L2
+    const uint64_t t2 = (uint64_t)blockIdx.x + ahead;  // ahead = resident CTAs (2 per SM)
+    if (t2 * RS_TILE < n) {
+      const uint64_t c2 = min((uint64_t)RS_TILE, n - t2 * RS_TILE);
+      l2_prefetch_range(kin + t2 * RS_TILE, c2 * sizeof(uint64_t));
+      l2_prefetch_range(vin + t2 * RS_TILE, c2 * sizeof(uint32_t));
+    }
+  }
   for (int i = tid; i < (RS2_NT / 32) * (1 << RB); i += RS2_NT) (&wcnt[0][0])[i] = 0;
   for (int d = tid; d < (1 << RB); d += RS2_NT) s_goff[d] = goff[(uint64_t)d * ntiles + blockIdx.x];  // used at the end
   __syncthreads();
@@ -430,6 +445,13 @@ __global__ void __launch_bounds__(BS_NT, 2) k_bin_sort(uint64_t* __restrict__ k,
   for (uint32_t c = blockIdx.x; c < nb; c += gridDim.x) {
     const uint64_t s = bstart[c], e = bstart[c + 1];
     const int n = (int)(e - s);
+    if (threadIdx.x == 0 && c + gridDim.x < nb) {  // the CTA's next bin into L2 while this one is sorted
+      const uint64_t s2 = bstart[c + gridDim.x], e2 = bstart[c + gridDim.x + 1];
+      if (e2 - s2 > 1 && e2 - s2 <= (uint64_t)BS_CAP) {
+        l2_prefetch_range(k + s2, (e2 - s2) * sizeof(uint64_t));
+        l2_prefetch_range(v + s2, (e2 - s2) * sizeof(uint32_t));
+      }
+    }
     if (n <= 1) {
       if (n == 1 && threadIdx.x == 0) {
         k[s] = (k[s] & ~(hmask ^ HASH_BITS_MASK)) | (1ull << hbits);  // strip b, run length 1
@@ -1071,6 +1093,14 @@ __global__ void k_dump(god::IndexView v, uint64_t* hash, uint32_t* pos, uint8_t*
   }
 }
 
+// CTAs of a kernel resident on the whole GPU (the wave after which a tile-per-CTA grid continues)
+template <typename F>
+uint32_t resident_ctas(F kernel, int nt, size_t smem) {
+  int per_sm = 0;
+  GOD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, nt, smem));
+  return (uint32_t)std::max(1, per_sm) * (uint32_t)num_sms();
+}
+
 inline uint32_t floor_log2(uint64_t v) { return v ? 63u - (uint32_t)__builtin_clzll(v) : 0u; }
 }  // namespace
 
@@ -1124,7 +1154,7 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
       if (!have_hist) GOD_LAUNCH("k_rs_hist", k_rs_hist<RB>, ntiles, RS_NT, 0, st, k0, n, shift, dmask, hist, ntiles);
       scan_exclusive_u32_to_u64(hist, goff, (uint64_t)(1u << RB) * ntiles, nullptr, st, scr, "scan_sort_hist");
       GOD_LAUNCH("k_rs_scatter", k_rs_scatter2<RB>, ntiles, RS2_NT, RS_DYN_SMEM, st, k0, v0, k1, v1, n, shift, dmask,
-                 goff, ntiles, table, L);
+                 goff, ntiles, table, L, resident_ctas(k_rs_scatter2<RB>, RS2_NT, RS_DYN_SMEM));
       std::swap(k0, k1);
       std::swap(v0, v1);
     };
