@@ -125,6 +125,7 @@ __global__ void k_read_anchor_counts1(const uint32_t* __restrict__ cnt, const ui
     if (l == 0) out[r] = acc;
   }
 }
+template <bool A16>  // A16: out is 16-B aligned -> one 128-bit store per anchor
 __global__ void k_anchor_write1(IndexView v, const uint64_t* __restrict__ hz, const uint32_t* __restrict__ pos,
                                 const uint32_t* __restrict__ cnt, const uint32_t* __restrict__ beg,
                                 const uint64_t* __restrict__ job_off, const uint8_t* __restrict__ phases, uint32_t p,
@@ -152,12 +153,17 @@ __global__ void k_anchor_write1(IndexView v, const uint64_t* __restrict__ hz, co
         uint64_t oo = o + incl - c;
         for (uint32_t t2 = 0; t2 < c; t2++, oo++) {
           const uint64_t en = __ldg(v.ent + bg + t2);
-          god_anchor an;
-          an.ref_pos = (uint32_t)(en >> 32);
-          an.read_pos = qp;
-          an.read_id = rid_base + r;
-          an.strand = ((uint32_t)en & 1u) ^ qz;
-          out[oo] = an;
+          if (A16) {
+            reinterpret_cast<uint4*>(out)[oo] =
+                make_uint4((uint32_t)(en >> 32), qp, rid_base + r, ((uint32_t)en & 1u) ^ qz);
+          } else {
+            god_anchor an;
+            an.ref_pos = (uint32_t)(en >> 32);
+            an.read_pos = qp;
+            an.read_id = rid_base + r;
+            an.strand = ((uint32_t)en & 1u) ^ qz;
+            out[oo] = an;
+          }
         }
       }
       o += tot;
@@ -390,8 +396,16 @@ uint64_t seed_reads(const god_index* ix, const uint8_t* reads, const uint64_t* o
     GOD_CUDA(cudaMemcpyAsync(anchor_offsets + n_reads, total, sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
     const uint64_t tot = d2h_scalar(total, st);
     if (tot <= cap)
-      GOD_LAUNCH("k_anchor_write", k_anchor_write1, grid_for((uint64_t)n_reads * RG, 256), 256, 0, st, v, rec1.hz,
-                 rec1.pos, rec1.cnt, rec1.beg, rec1.job_off, phases, p, n_reads, anchor_offsets, anchors, rid_base);
+    {
+      if ((reinterpret_cast<uintptr_t>(anchors) & 15u) == 0)
+        GOD_LAUNCH("k_anchor_write", k_anchor_write1<true>, grid_for((uint64_t)n_reads * RG, 256), 256, 0, st, v,
+                   rec1.hz, rec1.pos, rec1.cnt, rec1.beg, rec1.job_off, phases, p, n_reads, anchor_offsets, anchors,
+                   rid_base);
+      else
+        GOD_LAUNCH("k_anchor_write", k_anchor_write1<false>, grid_for((uint64_t)n_reads * RG, 256), 256, 0, st, v,
+                   rec1.hz, rec1.pos, rec1.cnt, rec1.beg, rec1.job_off, phases, p, n_reads, anchor_offsets, anchors,
+                   rid_base);
+    }
     return tot;
   }
   SeedSources S{};
