@@ -50,7 +50,16 @@ struct VoteArgs {
   god_vote* res;              // result slots
   uint32_t* cnt;              // results per read
   uint32_t* bad;              // anchors inconsistent with the phases
+  bool an16;                  // an is 16-B aligned: one 128-bit load per anchor
 };
+
+__device__ __forceinline__ god_anchor load_anchor(const VoteArgs& A, uint64_t i) {
+  if (A.an16) {
+    const uint4 u = __ldg(reinterpret_cast<const uint4*>(A.an) + i);
+    return god_anchor{u.x, u.y, u.z, u.w};
+  }
+  return A.an[i];
+}
 
 // Read coordinates are < 2^32 (god.h limits): 32-bit pattern arithmetic, with the divisions by p
 // and x short-cut for the paper's patterns ('1': p = 1; '10': p = 2, x = 1).
@@ -260,7 +269,7 @@ __global__ void __launch_bounds__(VOTE_NT) k_vote_warp(VoteArgs A, const uint32_
   const uint32_t le = (sl == 31) ? FULL : ((2u << sl) - 1u);
   auto ballot = [&](bool p) { return (__ballot_sync(FULL, p) >> sbase) & SB; };
   god_anchor an = {0, 0, 0, 0};
-  if (valid) an = A.an[a0 + sl];
+  if (valid) an = load_anchor(A, a0 + sl);
   // canonical k-mer once per read minimizer (a run of equal read_pos), then broadcast
   const uint32_t prev_rp = __shfl_up_sync(FULL, an.read_pos, 1, SEG);
   const bool rhead = valid && (sl == 0 || prev_rp != an.read_pos);
@@ -474,7 +483,7 @@ __device__ void vote_group(const VoteArgs& A, uint32_t r, const GroupArrays& S, 
   // keys; a non-head takes its head's canonical k-mer (heads are not written in this phase)
   bool bad = false;
   for (uint32_t i = t; i < n; i += NT) {
-    const god_anchor an = A.an[a0 + i];
+    const god_anchor an = load_anchor(A, a0 + i);
     const uint32_t j = S.crank[i];
     uint64_t c = 0;
     if (an.read_pos < L && is_included(A.pat, an.read_pos, ph)) c = S.canon[j];
@@ -620,7 +629,7 @@ __device__ void vote_group(const VoteArgs& A, uint32_t r, const GroupArrays& S, 
     const uint32_t c = S.aux[rank];
     uint32_t rlo = 0xffffffffu, rhi = 0, qlo = 0xffffffffu, qhi = 0;
     for (uint32_t i = S.chead[c] + lane; i < S.chead[c + 1]; i += 32) {
-      const god_anchor an = A.an[a0 + (S.key[i] & imask)];
+      const god_anchor an = load_anchor(A, a0 + (S.key[i] & imask));
       rlo = min(rlo, an.ref_pos); rhi = max(rhi, an.ref_pos);
       qlo = min(qlo, an.read_pos); qhi = max(qhi, an.read_pos);
     }
@@ -724,6 +733,7 @@ uint64_t vote_reads(const god_index* ix, const uint8_t* reads, const uint64_t* r
   A.roff = roff;
   A.ph = phases;
   A.an = anchors;
+  A.an16 = (reinterpret_cast<uintptr_t>(anchors) & 15u) == 0;
   A.aoff = aoff;
   A.pat = ix->P.pat;
   A.k = ix->P.k;
