@@ -666,6 +666,12 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort_big(uint64_t* __restri
   for (uint32_t q = blockIdx.x; q < nbig; q += gridDim.x) {
     const uint32_t b = big[q];
     const uint64_t s = bstart[b], e = bstart[b + 1], n = e - s;
+    if (threadIdx.x == 0 && q + gridDim.x < nbig) {  // the CTA's next bin into L2 (its first 16 K records)
+      const uint32_t b2 = big[q + gridDim.x];
+      const uint64_t s2 = bstart[b2], n2 = min(bstart[b2 + 1] - s2, (uint64_t)16384);
+      l2_prefetch_range(k + s2, n2 * sizeof(uint64_t));
+      l2_prefetch_range(v + s2, n2 * sizeof(uint32_t));
+    }
     const uint64_t top = ((k[s] & ((1ull << hbits) - 1)) >> lo_bits) << lo_bits;  // the bin's segment
     __shared__ unsigned long long s_diff;
     if (threadIdx.x == 0) s_diff = 0;
