@@ -182,7 +182,9 @@ GOD_API god_status god_seed_reads_compact(const god_index* idx, const uint8_t* r
  *      best cluster, rescued = 1.  No anchor: no location.
  * Each location reports the [min, max] ref_pos and read_pos of its member anchors (Fig. 8B's
  * subsequence pairs).  Output CSR: locations of read r in [out_offsets[r], out_offsets[r+1]);
- * read_id = r.  cap = location capacity (GOD_ETRUNC + *needed).  GOD_EINVAL if an anchor's
+ * read_id = r.  anchors: 16-B god_anchor records (the full form of god_seed_reads; the 8-B
+ * god_anchor_compact form is NOT accepted), at least anchor_offsets[n_reads] of them; any
+ * alignment.  cap = location capacity (GOD_ETRUNC + *needed).  GOD_EINVAL if an anchor's
  * read_pos is not an included position of its read under phases[r] (anchors and phases from
  * different calls), or a read has >= 2^29 anchors.  Synchronizes. */
 typedef struct {

@@ -268,6 +268,27 @@ def expand_compact(anchors, anchor_offsets) -> np.ndarray:
 
 
 # ---------------------------------------------------------------------------------------- voting
+def _check_anchor_records(anchors, anchor_offsets, n: int):
+    """god_vote_reads reads 16-B god_anchor records (include/god.h): reject the 8-B compact form
+    (expand_compact() converts it) and a buffer shorter than anchor_offsets[n]."""
+    if torch is not None and isinstance(anchors, torch.Tensor):
+        rec = anchors.element_size() * (int(anchors.shape[-1]) if anchors.dim() == 2 else 1)
+        nrec = int(anchors.shape[0]) if anchors.dim() >= 1 else 0
+    else:
+        a = np.asarray(anchors)
+        rec = a.dtype.itemsize * (int(a.shape[-1]) if a.ndim == 2 else 1)
+        nrec = int(a.shape[0]) if a.ndim >= 1 else 0
+        if a.ndim == 1 and a.dtype.itemsize != 16:
+            rec, nrec = 16, a.size * a.dtype.itemsize // 16
+    if rec != 16:
+        raise GodError(_lib.GOD_EINVAL, f"anchors must be 16-B god_anchor records (got {rec}-B rows; "
+                                        "compact anchors need expand_compact())")
+    ao = anchor_offsets
+    need = int(ao[n].item()) if torch is not None and isinstance(ao, torch.Tensor) else int(np.asarray(ao)[n])
+    if nrec < need:
+        raise GodError(_lib.GOD_EINVAL, f"anchors hold {nrec} records, anchor_offsets[{n}] = {need}")
+
+
 def god_vote_reads(index: GodIndex, reads, read_offsets, phases, anchors, anchor_offsets, D: int = 0, V: int = 3,
                    max_pairs: int = 0, cap: int | None = None):
     """Location voting (rescue P:398) on the anchors of god_seed_reads (same reads and
@@ -282,6 +303,7 @@ def god_vote_reads(index: GodIndex, reads, read_offsets, phases, anchors, anchor
     else:
         anchors = np.ascontiguousarray(anchors)
     n = int(read_offsets.shape[0]) - 1
+    _check_anchor_records(anchors, anchor_offsets, n)
     dv = reads.device if dev else None
     vo = _empty(n + 1, np.uint64, dev, dv)
     vp = _lib.GodVoteParams(int(D), int(V), int(max_pairs))
