@@ -25,6 +25,7 @@
 //   D. exact slow path for the whole tile (64-bit hashes in SMEM, direct window rule incl. partial
 //      windows) when the tile has an N, a run shorter than w, or such a key tie.
 //   E. ordered compaction: staged in SMEM, tile offset by decoupled look-back, coalesced copy.
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <type_traits>
@@ -36,15 +37,13 @@ namespace {
 
 constexpr int X2_NT = 128;
 constexpr int X2_OUT_BLOCKS = X2_NT - 2;
-// Staging capacity (selected records per tile) of the deferred copy-out.  Minimizer density is
-// ~2/(w+1), i.e. ~17% of a tile's positions; a tile with more (all-ties runs: homopolymers, tandem
-// repeats) is written out at once instead, after a synchronous look-back.
-constexpr int X2_CAP = 384;
-constexpr uint32_t X2_FLUSHED = 0xFFFFFFFFu;  // pending-count marker: the tile was written out already
+// unordered output staging (selected records per tile); density is ~2/(w+1), i.e. ~17% of a tile's
+// positions: a tile with more (all-ties runs) writes its records directly
+constexpr int X2_CAP = 512;
 // resident CTAs per SM the register allocation is sized for (SMEM allows 7): 7 for w <= 11 (72
 // registers, no spills), 6 for w = 19 (more registers per W-block)
 template <int W>
-constexpr int x2_minb() { return W >= 16 ? 6 : 7; }
+constexpr int x2_minb() { return W >= 16 ? 5 : 7; }
 
 struct X2Args {
   const uint8_t* seq;
@@ -64,7 +63,7 @@ struct X2Args {
   uint64_t* job_off;
   uint64_t cap;
   uint64_t* total_out;
-  uint32_t dbg_flags;      // developer toggles (GOD_X2_DBG): 1 = unordered output, 2 = no tie check
+  uint32_t dbg_flags;      // developer toggles (GOD_X2_DBG): 2 = no tie check
   uint32_t* dbg_counts;    // [0] tiles on the slow path, [1] tiles with a key tie
   const struct X2Desc* desc;  // [ntiles] per-tile descriptors (k_x2_tile_desc)
 };
@@ -84,35 +83,9 @@ __device__ __forceinline__ uint32_t word_at(const uint32_t (&w)[NW], int i) {
   return i < NW ? w[i] : 0u;
 }
 
-// bits [S, S+LEN) of the MSB-first bit string held in w[], right-aligned (LEN <= 56).  Called
-// from fully unrolled loops, so S is a compile-time constant after inlining (no local memory).
-template <int NW>
-__device__ __forceinline__ uint64_t ext_bits(const uint32_t (&w)[NW], const int S, const int LEN) {
-  const int w0 = S >> 5, off = S & 31;
-  const uint64_t hi64 = ((uint64_t)word_at(w, w0) << 32) | word_at(w, w0 + 1);
-  const uint64_t v = off ? (hi64 << off) | (word_at(w, w0 + 2) >> (32 - off)) : hi64;
-  return v >> (64 - LEN);
-}
-
 __device__ __forceinline__ uint32_t rev2(uint32_t x) {  // reverse the 16 2-bit fields of x
   const uint32_t y = __brev(x);
   return ((y >> 1) & 0x55555555u) | ((y & 0x55555555u) << 1);
-}
-
-// The masked Wang hash (O5).  The shift-add steps are written as the equal multiplications
-// (~x + (x << 21) = x (2^21 - 1) - 1 and x + (x << 31) = x (2^31 + 1) mod 2^64), which the compiler
-// issues on the FMA pipe (IMAD) instead of the integer ALU pipe that the rest of K1 saturates.
-template <int K>
-__device__ __forceinline__ uint64_t wang_hash_k(uint64_t key) {
-  constexpr uint64_t mask = (K >= 32) ? ~0ull : ((1ull << (2 * K)) - 1);
-  key = (key * ((1ull << 21) - 1) - 1ull) & mask;
-  key = key ^ (key >> 24);
-  key = (key * 265ull) & mask;
-  key = key ^ (key >> 14);
-  key = (key * 21ull) & mask;
-  key = key ^ (key >> 28);
-  key = (key * ((1ull << 31) + 1)) & mask;
-  return key;
 }
 
 // per-tile descriptor, precomputed by k_x2_tile_desc so that a CTA never walks a dependent chain
@@ -123,7 +96,7 @@ struct __align__(16) X2Desc {
 };
 
 struct X2Tile {  // per-tile scalars, in SMEM
-  uint32_t tile, j0, j1, simple, safe, any_n, slow, cnt;
+  uint32_t tile, j0, j1, simple, safe, slow;
   uint64_t cw_lo, cw_hi;
 };
 
@@ -140,11 +113,10 @@ struct X2Cfg {
   static constexpr size_t O_CODES = O_LUT + 256 * 4;
   static constexpr size_t O_NMASK = O_CODES + (size_t)MAXWORDS * 4;
   static constexpr size_t O_XCHG = O_NMASK + (size_t)MAXWORDS * 4;
-  static constexpr size_t O_HZ = (O_XCHG + 2 * (X2_NT / 32) * W * 4 + 15) / 16 * 16;  // [POS] hz, this tile
-  static constexpr size_t O_SHZ = O_HZ + (size_t)POS * 8;         // [2][X2_CAP] staged hz of the selected
-  static constexpr size_t O_SE = O_SHZ + 2 * (size_t)X2_CAP * 8;  // [2][X2_CAP] staged: e | key16 << 16
-  static constexpr size_t O_BI = O_SE + 2 * (size_t)X2_CAP * 4;   // block info [2][2][NT]
-  static constexpr size_t SMEM = (O_BI + 2 * 2 * X2_NT * 4 + 15) / 16 * 16;
+  static constexpr size_t O_STG = (O_XCHG + 2 * (X2_NT / 32) * W * 4 + 15) / 16 * 16;  // [X2_CAP] hz + pos
+  static constexpr size_t O_HZ = O_STG + (size_t)X2_CAP * 12;                                 // [NHZ][POS] hz
+  // ordered output keeps the previous tile's hashes until its look-back resolves (2 buffers)
+  static constexpr size_t smem(bool ordered) { return (O_HZ + (ordered ? 2 : 1) * (size_t)POS * 8 + 15) / 16 * 16; }
 };
 
 // (pack16 gathers the included bytes with compile-time byte-permutations)
@@ -285,6 +257,7 @@ __device__ inline uint64_t lb_resolve_warp(uint64_t* status, uint64_t tile, uint
   while (true) {
     uint64_t s = j >= 0 ? lb_load(&status[j]) : (LB_INC | 0ull);
     while (__any_sync(0xffffffffu, (s & ~LB_VAL) == 0)) {
+      __nanosleep(32);  // back off: a spinning warp takes issue slots from the CTAs doing the work
       if ((s & ~LB_VAL) == 0) s = lb_load(&status[j]);
     }
     const uint32_t inc = __ballot_sync(0xffffffffu, (s & ~LB_VAL) == LB_INC);
@@ -301,11 +274,83 @@ __device__ inline uint64_t lb_resolve_warp(uint64_t* status, uint64_t tile, uint
 }
 
 // ---------------------------------------------------------------------------------------------
-// Persistent CTAs: each grabs tiles in order (atomic counter), computes a tile, publishes its
-// record count, and only then resolves the PREVIOUS tile's output offset and writes its records,
-// so the look-back never stalls the CTA on a tile that other CTAs are still computing.
-template <int K, int W, int PP, int PX>
-__global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract2(X2Args a) {
+// Lean two-word arithmetic for B.  A k-mer / hash value of 2K bits is held as hi:lo with the top
+// HB = 2K - 32 bits in hi (K = 21: 10 bits, K = 19: 6 bits) or, for 2K <= 32, in lo alone.  A
+// multiplication by a 32-bit constant is one IMAD.WIDE.U32 plus one IMAD (the wide product's high
+// word is the carry into hi); an xor-shift by s >= HB is one mask of hi, one funnel shift and one
+// LOP3 (hi ^ hi >> s == hi).  Every step is reduced mod 2^2K as in O5.
+template <int K>
+struct KW {
+  static constexpr int HB = 2 * K > 32 ? 2 * K - 32 : 0;
+  static constexpr uint32_t HM = HB ? (1u << HB) - 1 : 0u;
+  static constexpr uint32_t LM = 2 * K >= 32 ? 0xFFFFFFFFu : (1u << (2 * K)) - 1;
+  static_assert(HB <= 14, "xor-shift steps assume hi has at most 14 bits");
+};
+
+template <int K>
+__device__ __forceinline__ void wang_hash_2w(uint32_t& hi, uint32_t& lo) {
+  if constexpr (KW<K>::HB > 0) {
+    constexpr uint32_t HM = KW<K>::HM;
+    auto mul = [&](uint32_t c) {
+      const uint64_t p = (uint64_t)lo * c;
+      hi = hi * c + (uint32_t)(p >> 32);
+      lo = (uint32_t)p;
+    };
+    {  // x1 = (2^21 - 1) x - 1: the -1 rides in the wide multiply's 64-bit addend
+      const uint64_t p = (uint64_t)lo * ((1u << 21) - 1) + ~0ull;
+      hi = hi * ((1u << 21) - 1) + (uint32_t)(p >> 32);
+      lo = (uint32_t)p;
+    }
+    hi &= HM; lo ^= __funnelshift_r(lo, hi, 24);   // x2 = x1 ^ x1 >> 24
+    mul(265u);                                      // x3
+    hi &= HM; lo ^= __funnelshift_r(lo, hi, 14);   // x4
+    mul(21u);                                       // x5
+    hi &= HM; lo ^= __funnelshift_r(lo, hi, 28);   // x6
+    mul(0x80000001u);                               // H = (2^31 + 1) x6
+    hi &= HM;
+  } else {
+    constexpr uint32_t LM = KW<K>::LM;
+    uint32_t x = lo;
+    x = (x * ((1u << 21) - 1) - 1u) & LM;
+    x ^= x >> 24;
+    x = (x * 265u) & LM;
+    x ^= x >> 14;
+    x = (x * 21u) & LM;
+    x ^= x >> 28;
+    x = (x * 0x80000001u) & LM;
+    lo = x;
+    hi = 0;
+  }
+}
+
+// 32 bits of the MSB-first bit string w[] starting at bit S (compile-time after unrolling)
+template <int NW>
+__device__ __forceinline__ uint32_t ext32(const uint32_t (&w)[NW], const int S) {
+  const int i = S >> 5, o = S & 31;
+  return o ? __funnelshift_l(word_at(w, i + 1), word_at(w, i), o) : word_at(w, i);
+}
+// the 2K-bit k-mer at bit S of w[] as hi:lo
+template <int K, int NW>
+__device__ __forceinline__ void kmer_2w(const uint32_t (&w)[NW], const int S, uint32_t& hi, uint32_t& lo) {
+  constexpr int HB = KW<K>::HB;
+  if constexpr (HB > 0) {
+    lo = ext32(w, S + HB);
+    hi = ext32(w, S) >> (32 - HB);
+  } else {
+    lo = ext32(w, S) >> (32 - 2 * K);
+    hi = 0;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Persistent CTAs take tiles in order (one ahead, descriptor prefetched).  Per tile: A (all warps)
+// sparsify into SMEM; B/C per thread-block of W positions; the exact slow path when the tile needs
+// it; E: every thread writes its own selected records straight to the output at the tile's base,
+// which comes from a decoupled look-back over tiles (ORDERED: position order, as god_minimizers
+// and the phase path need) or from one atomicAdd (the index path, whose sort orders by (hash, pos)).
+template <int K, int W, int PP, int PX, bool ORDERED>
+__global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract3(X2Args a) {
+  static_assert((K & 1) == 1, "odd k only: no palindromic k-mers (O4); even k runs the generic kernel");
   using C = X2Cfg<K, W, PP, PX>;
   constexpr int NB = C::NB, NWIN = C::NWIN, NLOAD = C::NLOAD, POS = C::POS;
   constexpr int NWARP = X2_NT / 32;
@@ -315,14 +360,11 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract2(X2Args a) {
   uint32_t* nmask = reinterpret_cast<uint32_t*>(x2_smem + C::O_NMASK);
   uint32_t* xpf = reinterpret_cast<uint32_t*>(x2_smem + C::O_XCHG);
   uint32_t* xsf = xpf + NWARP * W;
-  uint64_t* HZ = reinterpret_cast<uint64_t*>(x2_smem + C::O_HZ);     // [POS]
-  uint64_t* SHZ = reinterpret_cast<uint64_t*>(x2_smem + C::O_SHZ);   // [2][X2_CAP]
-  uint32_t* SE = reinterpret_cast<uint32_t*>(x2_smem + C::O_SE);     // [2][X2_CAP]
-  // block info [2][2][NT]: pos base | first staged record (12 bits) + job start flag << 12 +
-  // job - j0 << 13 (8 bits) + first k-mer index mod x << 21
-  uint32_t* BI = reinterpret_cast<uint32_t*>(x2_smem + C::O_BI);
-  __shared__ uint32_t s_bj0[2];  // j0 of the tile staged in each buffer
-  __shared__ uint64_t s_ovf_base;
+  uint64_t* const HZ0 = reinterpret_cast<uint64_t*>(x2_smem + C::O_HZ);  // [NHZ][POS] hash | strand << 63
+  uint64_t* HZ = HZ0;
+  // unordered output: the tile's selected records staged in position order before one coalesced copy
+  uint64_t* SHZ = reinterpret_cast<uint64_t*>(x2_smem + C::O_STG);              // [X2_CAP]
+  uint32_t* SPOS = reinterpret_cast<uint32_t*>(x2_smem + C::O_STG + X2_CAP * 8);  // [X2_CAP]
   __shared__ X2Tile T;
   __shared__ uint64_t skb[X2_NT + 2], scw[X2_NT + 2];
   __shared__ uint64_t sjb[X2_NT + 2];  // per job of the tile: byte address of its first patterned base
@@ -331,9 +373,13 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract2(X2Args a) {
   __shared__ uint8_t swj[(X2Cfg<K, W, PP, PX>::MAXWORDS + 3) / 4 * 4];  // code word -> job (relative)
   __shared__ uint32_t sjob[X2_NT];
   __shared__ uint32_t warp_cnt[NWARP];
+  __shared__ uint32_t xlast[NWARP];    // per warp: lane 31's last selected (offset << 27 | key >> 5) ...
+  __shared__ uint32_t xlastk[NWARP];   // ... and its key
+  __shared__ uint64_t s_base;
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const uint64_t ntiles = (a.total_blocks + X2_OUT_BLOCKS - 1) / X2_OUT_BLOCKS;
+  const uint32_t ks = a.key_shift;  // <= 31
   {  // expected-letter table: for 4 MSB-first codes pk, bytes "ACGT"[c_i], base 0 in byte 0
     const uint32_t L4 = 0x54474341u;
     for (int pk = tid; pk < 256; pk += X2_NT) {
@@ -343,137 +389,124 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract2(X2Args a) {
       lut[pk] = e;
     }
   }
-  const uint32_t ks = a.key_shift;
-  int buf = 0;
-
-  // write the staged records of a finished tile: warp 0 alone resolves its output offset (decoupled
-  // look-back) and copies the records out, overlapped with the other warps' sparsify of the next tile
-  auto flush_warp0 = [&](uint64_t tile, uint32_t cnt, int b) {
-    uint64_t base;
-    if (a.dbg_flags & 1u) base = lane == 0 ? atomicAdd((unsigned long long*)&a.status[ntiles], (unsigned long long)cnt) : 0;
-    else base = lb_resolve_warp(a.status, tile, cnt);
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if (lane == 0 && tile == ntiles - 1) *a.total_out = base + cnt;
-    const uint64_t* hzb = SHZ + (size_t)b * X2_CAP;
-    const uint32_t* se = SE + (size_t)b * X2_CAP;
-    const uint32_t* bpb = BI + (size_t)b * 2 * X2_NT;
-    const uint32_t* binf = bpb + X2_NT;
-    const uint32_t bj0 = s_bj0[b];
-    if (a.job_off)
-      for (int t = lane; t < X2_NT; t += 32) {
-        const uint32_t f = binf[t];
-        if ((f >> 12) & 1u) a.job_off[bj0 + ((f >> 13) & 0xFFu)] = base + (f & 0xFFFu);
-      }
-    for (uint32_t r = lane; r < cnt; r += 32) {
-      const uint64_t gi = base + r;
-      if (gi < a.cap) {
-        const int e = se[r] & 0xFFFFu;
-        const int blk = e / W;
-        a.out_hz[gi] = hzb[r];
-        a.out_pos[gi] = bpb[blk] + pat_delta<PP, PX>((binf[blk] >> 21) & 3u, (uint32_t)(e - blk * W));
-        if (a.out_job) a.out_job[gi] = bj0 + ((binf[blk] >> 13) & 0xFFu);
-      }
-    }
-  };
-
-  // Warp roles per iteration (tile u): warps 1..3 claim the tile (thread SETUP_TID claims tiles in
-  // order from an atomic counter, one ahead, with the descriptor prefetched), load its job bases
-  // and sparsify it into SMEM (A), synchronising among themselves with named barrier 1; meanwhile
-  // warp 0 finishes tile u-2 (look-back + copy-out from the staging buffer that tile u will reuse).
-  // Then all four warps compute (B-E) and tile u's count is published.
-  constexpr int SETUP_TID = 32;
+  // tiles are claimed one ahead (descriptor prefetched) when the output is unordered; ORDERED claims
+  // each tile when it starts, so tiles are computed in claim order and a tile's predecessors have
+  // published their counts by the time its deferred look-back runs
   uint32_t next_t = 0;
   X2Desc nd{};
-  if (tid == SETUP_TID) {
+  if (!ORDERED && tid == 0) {
     next_t = atomicAdd(a.tile_ctr, 1u);
     if (next_t < ntiles) nd = a.desc[next_t];
   }
-  int64_t pend_old = -1, pend_new = -1;
-  uint32_t cnt_old = 0, cnt_new = 0;
+  // ORDERED: the previous tile's records, written one iteration late so that its look-back finds the
+  // predecessors' counts published instead of spinning on tiles that other CTAs are still computing
+  int64_t p_tile = -1;
+  uint32_t p_total = 0, p_sel = 0, p_rank = 0, p_pb = 0, p_r0 = 0, p_J = 0;
+  bool p_start = false;
+  const uint64_t* p_hz = HZ0;
+  auto resolve_pending = [&]() {  // warp 0
+    const uint64_t b = lb_resolve_warp(a.status, (uint64_t)p_tile, p_total);
+    if (lane == 0) {
+      s_base = b;
+      if ((uint64_t)p_tile == ntiles - 1) *a.total_out = b + p_total;
+    }
+  };
+  auto write_pending = [&]() {  // all threads, after a barrier that follows resolve_pending
+    uint64_t gi = s_base + p_rank;
+    if (a.job_off && p_start) a.job_off[p_J] = gi;
+    uint32_t m = p_sel;
+    while (m) {
+      const int i = __ffs(m) - 1;
+      m &= m - 1;
+      if (gi < a.cap) {
+        a.out_hz[gi] = p_hz[tid * W + i];
+        a.out_pos[gi] = p_pb + pat_delta<PP, PX>(p_r0, (uint32_t)i);
+        if (a.out_job) a.out_job[gi] = p_J;
+      }
+      ++gi;
+    }
+  };
   while (true) {
-    if (wid == 0) {
-      if (pend_old >= 0 && cnt_old != X2_FLUSHED) flush_warp0((uint64_t)pend_old, cnt_old, buf);
-    } else {
-      if (tid == SETUP_TID) {
-        T.tile = next_t < ntiles ? next_t : 0xFFFFFFFFu;
-        if (next_t < ntiles) {
-          T.j0 = nd.j0; T.j1 = nd.j1;
-          T.cw_lo = nd.cw_lo; T.cw_hi = nd.cw_hi;
-          T.simple = nd.simple;
-          T.safe = nd.safe;
-          T.any_n = 0; T.slow = 0;
+    if (tid == 0) {
+      if (ORDERED) {
+        next_t = atomicAdd(a.tile_ctr, 1u);
+        if (next_t < ntiles) nd = a.desc[next_t];
+      }
+      T.tile = next_t < ntiles ? next_t : 0xFFFFFFFFu;
+      if (next_t < ntiles) {
+        T.j0 = nd.j0; T.j1 = nd.j1;
+        T.cw_lo = nd.cw_lo; T.cw_hi = nd.cw_hi;
+        T.simple = nd.simple;
+        T.safe = nd.safe;
+        T.slow = 0;
+        if (!ORDERED) {
           next_t = atomicAdd(a.tile_ctr, 1u);
           if (next_t < ntiles) nd = a.desc[next_t];
         }
-      }
-      asm volatile("bar.sync 1, %0;" ::"r"(X2_NT - 32) : "memory");
-      if (T.tile != 0xFFFFFFFFu) {
-        const uint32_t j0 = T.j0, nj = T.j1 - T.j0 + 1;
-        const uint64_t cw_lo = T.cw_lo;
-        const int nwords = (int)(T.cw_hi - cw_lo);
-        const int t1 = tid - 32, nt1 = X2_NT - 32;
-        // the tile's job bases in SMEM (a tile spans <= NT + 1 jobs: every job owns >= 1 block)
-        for (uint32_t q = t1; q <= nj; q += nt1) {
-          skb[q] = a.kb[j0 + q];
-          scw[q] = a.cw[j0 + q];
-          if (q < nj) {
-            const Job jq = a.jobs[j0 + q];
-            sjb[q] = jq.seq_off + jq.phase + a.one0;
-            sjn[q] = jq.nk;
-            sjp[q] = (uint32_t)(jq.pos_base + jq.phase + a.one0);
-          }
-        }
-        asm volatile("bar.sync 1, %0;" ::"r"(X2_NT - 32) : "memory");
-        if (!T.simple) {  // code word -> job, filled job by job
-          for (uint32_t q = t1; q < nj; q += nt1) {
-            const int64_t w0 = (int64_t)scw[q] - (int64_t)cw_lo, w1 = (int64_t)scw[q + 1] - (int64_t)cw_lo;
-            for (int64_t wi = w0 < 0 ? 0 : w0; wi < w1 && wi < nwords; wi++) swj[wi] = (uint8_t)q;
-          }
-          asm volatile("bar.sync 1, %0;" ::"r"(X2_NT - 32) : "memory");
-        }
-        // ---------------------------------------------------------- A. sparsify into SMEM
-        uint32_t my_n = 0;
-        if (T.simple) {
-          const Job jb = a.jobs[j0];
-          const uint64_t w0 = cw_lo - scw[0];
-          const uint32_t ncode = jb.nk ? jb.nk + K - 1 : 0;
-          const uint64_t A0 = jb.seq_off + jb.phase + a.one0;
-          for (int wi = t1; wi < nwords; wi += nt1) {
-            const uint64_t q0 = (w0 + wi) * 16;
-            uint32_t nm = 0, word = 0;
-            if (q0 < ncode) word = pack_word<PP, PX, false>(a.seq, a.seq_bytes, A0, q0,
-                                                            (int)min((uint64_t)16, ncode - q0), lut, &nm);
-            codes[wi] = word;
-            nmask[wi] = nm;
-            my_n |= nm;
-          }
-        } else {
-          const bool safe = T.safe;
-          for (int wi = t1; wi < nwords; wi += nt1) {
-            const uint32_t Jw = swj[wi];
-            const uint64_t nkq = sjn[Jw];
-            const uint64_t ncode = nkq ? nkq + K - 1 : 0;
-            const uint64_t q0 = (cw_lo + wi - scw[Jw]) * 16;
-            uint32_t nm = 0, word = 0;
-            if (q0 < ncode) {
-              const int nb = (int)min((uint64_t)16, ncode - q0);
-              word = safe ? pack_word<PP, PX, false>(a.seq, a.seq_bytes, sjb[Jw], q0, nb, lut, &nm)
-                          : pack_word<PP, PX, true>(a.seq, a.seq_bytes, sjb[Jw], q0, nb, lut, &nm);
-            }
-            codes[wi] = word;
-            nmask[wi] = nm;
-            my_n |= nm;
-          }
-        }
-        if (my_n) T.any_n = 1;
       }
     }
     __syncthreads();
     const uint32_t tile = T.tile;
     if (tile == 0xFFFFFFFFu) break;
+
     const uint32_t j0 = T.j0, j1 = T.j1;
-    const uint64_t cw_lo = T.cw_lo;
     const uint32_t nj = j1 - j0 + 1;
+    const uint64_t cw_lo = T.cw_lo;
+    const int nwords = (int)(T.cw_hi - cw_lo);
+    // the tile's job bases in SMEM (a tile spans <= NT + 1 jobs: every job owns >= 1 block)
+    for (uint32_t q = tid; q <= nj; q += X2_NT) {
+      skb[q] = a.kb[j0 + q];
+      scw[q] = a.cw[j0 + q];
+      if (q < nj) {
+        const Job jq = a.jobs[j0 + q];
+        sjb[q] = jq.seq_off + jq.phase + a.one0;
+        sjn[q] = jq.nk;
+        sjp[q] = (uint32_t)(jq.pos_base + jq.phase + a.one0);
+      }
+    }
+    __syncthreads();
+    const bool simple = T.simple;
+    if (!simple) {  // code word -> job, filled job by job
+      for (uint32_t q = tid; q < nj; q += X2_NT) {
+        const int64_t w0 = (int64_t)scw[q] - (int64_t)cw_lo, w1 = (int64_t)scw[q + 1] - (int64_t)cw_lo;
+        for (int64_t wi = w0 < 0 ? 0 : w0; wi < w1 && wi < nwords; wi++) swj[wi] = (uint8_t)q;
+      }
+      __syncthreads();
+    }
+    // ------------------------------------------------------------------ A. sparsify into SMEM
+    uint32_t my_n = 0;
+    if (simple) {
+      const uint64_t w0 = cw_lo - scw[0];
+      const uint32_t ncode = sjn[0] ? sjn[0] + K - 1 : 0;
+      const uint64_t A0 = sjb[0];
+      for (int wi = tid; wi < nwords; wi += X2_NT) {
+        const uint64_t q0 = (w0 + wi) * 16;
+        uint32_t nm = 0, word = 0;
+        if (q0 < ncode) word = pack_word<PP, PX, false>(a.seq, a.seq_bytes, A0, q0,
+                                                        (int)min((uint64_t)16, ncode - q0), lut, &nm);
+        codes[wi] = word;
+        nmask[wi] = nm;
+        my_n |= nm;
+      }
+    } else {
+      const bool safe = T.safe;
+      for (int wi = tid; wi < nwords; wi += X2_NT) {
+        const uint32_t Jw = swj[wi];
+        const uint64_t nkq = sjn[Jw];
+        const uint64_t ncode = nkq ? nkq + K - 1 : 0;
+        const uint64_t q0 = (cw_lo + wi - scw[Jw]) * 16;
+        uint32_t nm = 0, word = 0;
+        if (q0 < ncode) {
+          const int nb = (int)min((uint64_t)16, ncode - q0);
+          word = safe ? pack_word<PP, PX, false>(a.seq, a.seq_bytes, sjb[Jw], q0, nb, lut, &nm)
+                      : pack_word<PP, PX, true>(a.seq, a.seq_bytes, sjb[Jw], q0, nb, lut, &nm);
+        }
+        codes[wi] = word;
+        nmask[wi] = nm;
+        my_n |= nm;
+      }
+    }
+    const bool any_n = __syncthreads_or(my_n != 0);
 
     // ---- my block: job J, first k-mer index l0
     const int64_t myb = (int64_t)tile * X2_OUT_BLOCKS - 1 + tid;
@@ -486,9 +519,8 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract2(X2Args a) {
       nk = sjn[J - j0];
     }
     sjob[tid] = blk_in ? J : 0xFFFFFFFFu;  // block -> job (job boundaries are window barriers)
-    __syncthreads();
 
-    // ------------------------------------------------------------ B. k-mers and hashes
+    // ------------------------------------------------------------------ B. k-mers and hashes
     const bool blk_has_kmers = blk_in && l0 < nk;
     uint32_t win[NWIN];
     {
@@ -508,33 +540,29 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract2(X2Args a) {
     for (int i = 0; i < NWIN; i++) rcw[i] = ~rev2(win[NWIN - 1 - i]);
     constexpr int PADB = 32 * NWIN - 2 * NB;
     uint32_t key[W];
-    uint32_t palmask = 0;
     const uint32_t nvalid = blk_has_kmers ? min((uint32_t)W, nk - l0) : 0u;
-    // the first k-mer of the block is extracted, the others rolled: fwd gains the entering base
-    // as its least significant digit, rev its complement as the most significant (O4)
-    constexpr uint64_t KMASK = (K >= 32) ? ~0ull : ((1ull << (2 * K)) - 1);
-    uint64_t fwd = ext_bits(win, 0, 2 * K);
-    uint64_t rev = ext_bits(rcw, PADB + 2 * (NB - K), 2 * K);
 #pragma unroll
     for (int i = 0; i < W; i++) {
-      if (i > 0) {
-        const uint64_t c = ext_bits(win, 2 * (i + K - 1), 2);
-        fwd = ((fwd << 2) | c) & KMASK;
-        rev = (rev >> 2) | ((c ^ 3ull) << (2 * K - 2));
-      }
-      const bool z = fwd > rev;
-      const uint64_t h = wang_hash_k<K>(z ? rev : fwd);
-      HZ[tid * W + i] = h | ((uint64_t)z << 63);
-      uint32_t kk = (uint32_t)(h >> ks) + 1u;
-      if constexpr ((K & 1) == 0) {
-        if (fwd == rev) { kk = 0xFFFFFFFFu; palmask |= 1u << i; }
-      }
-      key[i] = (uint32_t)i < nvalid ? kk : 0u;
+      uint32_t fh, fl, rh, rl;
+      kmer_2w<K>(win, 2 * i, fh, fl);
+      kmer_2w<K>(rcw, PADB + 2 * (NB - K - i), rh, rl);
+      const bool z = (((uint64_t)fh << 32) | fl) > (((uint64_t)rh << 32) | rl);  // canonical (O4)
+      uint32_t hi = z ? rh : fh, lo = z ? rl : fl;
+      wang_hash_2w<K>(hi, lo);
+      HZ[tid * W + i] = ((uint64_t)(hi | (z ? 0x80000000u : 0u)) << 32) | lo;
+      const uint32_t kk = __funnelshift_r(lo, hi, ks) + 1u;  // top 31 hash bits + 1 (0 = barrier)
+      key[i] = kk;
     }
+    if (nvalid < (uint32_t)W) {  // the last block of a job (or past the data): barrier keys
+#pragma unroll
+      for (int i = 0; i < W; i++)
+        if ((uint32_t)i >= nvalid) key[i] = 0u;
+    }
+    __syncthreads();  // sjob, and the code words are no longer needed by anyone but the slow path
 
-    // ------------------------------------------------------------ C. selection on keys
+    // ------------------------------------------------------------------ C. selection on keys
     uint32_t selmask = 0;
-    if (!T.any_n) {
+    if (!any_n) {
       bool need_slow = false;
       uint32_t PF[W], SF[W];
       PF[0] = key[0];
@@ -564,10 +592,10 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract2(X2Args a) {
       WM[0] = SF[0];
 #pragma unroll
       for (int i = 1; i < W; i++) WM[i] = min(SF[i], nPF[i - 1]);
-      uint32_t PX[W], SX[W];
-      PX[0] = WM[0];
+      uint32_t PXM[W], SX[W];
+      PXM[0] = WM[0];
 #pragma unroll
-      for (int i = 1; i < W; i++) PX[i] = max(PX[i - 1], WM[i]);
+      for (int i = 1; i < W; i++) PXM[i] = max(PXM[i - 1], WM[i]);
       SX[W - 1] = WM[W - 1];
 #pragma unroll
       for (int i = W - 2; i >= 0; i--) SX[i] = max(SX[i + 1], WM[i]);
@@ -575,34 +603,55 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract2(X2Args a) {
 #pragma unroll
         for (int i = 0; i < W; i++) xsf[wid * W + i] = SX[i];
       }
-      __syncthreads();
       uint32_t pSX[W];
 #pragma unroll
       for (int i = 0; i < W; i++) pSX[i] = __shfl_up_sync(0xffffffffu, SX[i], 1);
+      // tie check, part 1: within the block, each selected position against the previous one
+      bool tie = false;
+      uint32_t prevk = 0;
+      __syncthreads();
       if (lane == 0) {
 #pragma unroll
         for (int i = 0; i < W; i++) pSX[i] = (wid > 0) ? xsf[(wid - 1) * W + i] : 0u;
       }
 #pragma unroll
       for (int o = 0; o < W; o++) {
-        const uint32_t mm = (o == W - 1) ? PX[W - 1] : max(pSX[o + 1], PX[o]);
+        const uint32_t mm = (o == W - 1) ? PXM[W - 1] : max(pSX[o + 1], PXM[o]);
         const uint32_t k = key[o];
-        bool s = (k == mm) && k != 0u;
-        if constexpr ((K & 1) == 0) s = s && k != 0xFFFFFFFFu;
+        const bool s = (k == mm) && k != 0u;
         need_slow |= (k != 0u) & (mm == 0u);  // a run shorter than w: partial-window rule
-        if (s) selmask |= 1u << o;
+        tie |= s & (k == prevk);
+        if (s) {
+          selmask |= 1u << o;
+          prevk = k;
+        }
+      }
+      // tie check, part 2: the first selected position against the previous block's last one when they
+      // are closer than w (offset in this block < offset in the previous block)
+      const uint32_t lasto = selmask ? 31u - __clz(selmask) : 0xFFu;
+      uint32_t plo = __shfl_up_sync(0xffffffffu, lasto, 1), plk = __shfl_up_sync(0xffffffffu, prevk, 1);
+      if (lane == 31) { xlast[wid] = lasto; xlastk[wid] = prevk; }
+      __syncthreads();
+      if (lane == 0) { plo = wid > 0 ? xlast[wid - 1] : 0xFFu; plk = wid > 0 ? xlastk[wid - 1] : 0u; }
+      if (tid > 0 && plo != 0xFFu && selmask) {
+        const uint32_t firsto = __ffs(selmask) - 1;
+        const uint32_t firstk = (uint32_t)((HZ[tid * W + firsto] & ~(1ull << 63)) >> ks) + 1u;
+        if (firsto < plo && firstk == plk) tie = true;
       }
       if (tid == 0 || tid == X2_NT - 1) need_slow = false;  // halo blocks are not emitted
-      if (__syncthreads_or(need_slow) && tid == 0) T.slow = 1;
+      if (a.dbg_flags & 2u) tie = false;
+      const int flags = __syncthreads_or((need_slow ? 1 : 0) | (tie ? 2 : 0));
+      if (tid == 0 && flags) T.slow = (uint32_t)flags;
+      __syncthreads();
     }
-    __syncthreads();
 
-    // ------------------------------------------------------------ D. exact slow path (whole tile)
-    auto slow_path = [&]() {
+    // ------------------------------------------------------------------ D. exact slow path (whole tile)
+    if (any_n || T.slow) {
+      if (tid == 0 && a.dbg_counts) atomicAdd(&a.dbg_counts[(T.slow & 2u) && !any_n ? 1 : 0], 1u);
       uint32_t zmask = 0;
 #pragma unroll
       for (int i = 0; i < W; i++) zmask |= (uint32_t)(HZ[tid * W + i] >> 63) << i;
-      uint64_t* H64 = HZ;  // hash+1, 0 barrier, ~0 palindrome
+      uint64_t* H64 = HZ;  // hash+1, 0 barrier
 #pragma unroll
       for (int i = 0; i < W; i++) {
         uint64_t hv = 0;
@@ -615,7 +664,7 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract2(X2Args a) {
             const int wi2 = wb + (int)((o + bb) / 16);
             if (wi2 < C::MAXWORDS && ((nmask[wi2] >> (15 - ((o + bb) % 16))) & 1u)) anyn = true;
           }
-          if (!anyn) hv = ((palmask >> i) & 1u) ? ~0ull : (HZ[tid * W + i] & ~(1ull << 63)) + 1;
+          if (!anyn) hv = (HZ[tid * W + i] & ~(1ull << 63)) + 1;
         }
         H64[tid * W + i] = hv;
       }
@@ -625,22 +674,20 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract2(X2Args a) {
         for (int i = 0; i < W; i++) {
           const int j = tid * W + i;
           const uint64_t hj = H64[j];
-          if (hj == 0 || hj == ~0ull) continue;
+          if (hj == 0) continue;
           int lo = j, hi = j;
           while (lo > j - (W - 1) && H64[lo - 1] != 0 && sjob[(lo - 1) / W] == J) --lo;
           while (hi < j + (W - 1) && H64[hi + 1] != 0 && sjob[(hi + 1) / W] == J) ++hi;
           bool s = false;
           if (hi - lo + 1 < W) {
             uint64_t mn = ~0ull;
-            for (int q = lo; q <= hi; q++)
-              if (H64[q] != ~0ull) mn = min(mn, H64[q]);
+            for (int q = lo; q <= hi; q++) mn = min(mn, H64[q]);
             s = (hj == mn);
           } else {
             const int a0 = max(lo, j - (W - 1)), a1 = min(j, hi - (W - 1));
             for (int st = a0; st <= a1 && !s; st++) {
               uint64_t mn = ~0ull;
-              for (int q = st; q < st + W; q++)
-                if (H64[q] != ~0ull) mn = min(mn, H64[q]);
+              for (int q = st; q < st + W; q++) mn = min(mn, H64[q]);
               s = (hj == mn);
             }
           }
@@ -652,132 +699,99 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract2(X2Args a) {
       for (int i = 0; i < W; i++)  // back to hash | strand (only selected entries matter)
         HZ[tid * W + i] = (H64[tid * W + i] - 1) | ((uint64_t)((zmask >> i) & 1u) << 63);
       selmask = m;
-    };
-    if (T.any_n || T.slow) {
-      if (tid == 0 && a.dbg_counts) atomicAdd(&a.dbg_counts[0], 1u);
-      slow_path();
     }
     if (tid == 0 || tid == X2_NT - 1 || !blk_in) selmask = 0;
 
-    // ------------------------------------------------------------ E. compaction into staging[buf]
-    uint32_t* se = SE + (size_t)buf * X2_CAP;
-    uint64_t* shz = SHZ + (size_t)buf * X2_CAP;
-    uint32_t* bi = BI + (size_t)buf * 2 * X2_NT;
-    uint32_t my_idx0 = 0;
-    auto compact = [&]() -> uint32_t {
-      const uint32_t cnt = __popc(selmask);
-      uint32_t incl = cnt;
+    // ------------------------------------------------------------------ E. output
+    const uint32_t cnt = __popc(selmask);
+    uint32_t incl = cnt;
 #pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
-        if (lane >= d) incl += y;
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += y;
+    }
+    if (lane == 31) warp_cnt[wid] = incl;
+    __syncthreads();
+    uint32_t before = 0, total = 0;
+#pragma unroll
+    for (int q = 0; q < NWARP; q++) {
+      const uint32_t c = warp_cnt[q];
+      before += q < wid ? c : 0u;
+      total += c;
+    }
+    if constexpr (ORDERED) {
+      // publish this tile's count, then write the PREVIOUS tile's records: its predecessors had a whole
+      // tile's time to publish theirs, so the look-back rarely waits
+      if (tid == 0) lb_publish(a.status, tile, total);
+      if (p_tile >= 0) {
+        if (wid == 0) resolve_pending();
+        __syncthreads();
+        write_pending();
       }
-      if (lane == 31) warp_cnt[wid] = incl;
+      p_tile = tile;
+      p_total = total;
+      p_sel = selmask;
+      p_rank = before + incl - cnt;
+      p_pb = sjp[J - j0] + (uint32_t)pat_off(PP, PX, (int)l0);
+      p_r0 = l0 % PX;
+      p_J = J;
+      p_start = blk_in && tid > 0 && tid < X2_NT - 1 && l0 == 0;
+      p_hz = HZ;
+      HZ = (HZ == HZ0) ? HZ0 + POS : HZ0;
+      continue;
+    }
+    if (tid == 0) s_base = atomicAdd(reinterpret_cast<unsigned long long*>(a.total_out), (unsigned long long)total);
+    uint32_t rank = before + incl - cnt;
+    if (total <= (uint32_t)X2_CAP && !a.out_job) {
+      // stage the tile's records in SMEM (predicated, no divergent loop), then one coalesced copy
+      const uint32_t pb = sjp[J - j0] + (uint32_t)pat_off(PP, PX, (int)l0);
+      const uint32_t r0 = l0 % PX;
+#pragma unroll
+      for (int o = 0; o < W; o++) {
+        if ((selmask >> o) & 1u) {
+          SHZ[rank] = HZ[tid * W + o];
+          SPOS[rank] = pb + pat_delta<PP, PX>(r0, (uint32_t)o);
+          ++rank;
+        }
+      }
       __syncthreads();
-      uint32_t before = 0, total = 0;
-#pragma unroll
-      for (int q = 0; q < NWARP; q++) {
-        const uint32_t c = warp_cnt[q];
-        before += q < wid ? c : 0u;
-        total += c;
+      const uint64_t base = s_base;
+      if (a.job_off && blk_in && tid > 0 && tid < X2_NT - 1 && l0 == 0) a.job_off[J] = base + before + incl - cnt;
+      for (uint32_t r = tid; r < total; r += X2_NT) {
+        const uint64_t gi = base + r;
+        if (gi < a.cap) {
+          a.out_hz[gi] = SHZ[r];
+          a.out_pos[gi] = SPOS[r];
+        }
       }
-      uint32_t idx = before + incl - cnt;
-      my_idx0 = idx;
-      bi[tid] = sjp[J - j0] + (uint32_t)pat_off(PP, PX, (int)l0);
-      bi[X2_NT + tid] = idx | ((blk_in && tid > 0 && tid < X2_NT - 1 && l0 == 0) ? 1u << 12 : 0u) | ((J - j0) << 13) |
-                        ((l0 % PX) << 21);
-      if (tid == 0) s_bj0[buf] = j0;
+      continue;
+    }
+    __syncthreads();
+    uint64_t gi = s_base + rank;
+    if (a.job_off && blk_in && tid > 0 && tid < X2_NT - 1 && l0 == 0) a.job_off[J] = gi;
+    if (selmask) {
+      const uint32_t pb = sjp[J - j0] + (uint32_t)pat_off(PP, PX, (int)l0);
+      const uint32_t r0 = l0 % PX;
       uint32_t m = selmask;
       while (m) {
         const int i = __ffs(m) - 1;
         m &= m - 1;
-        if (idx < (uint32_t)X2_CAP) {
-          const uint64_t hv = HZ[tid * W + i];
-          se[idx] = (uint32_t)(tid * W + i) | ((uint32_t)(hv >> ks) << 16);
-          shz[idx] = hv;
-        }
-        ++idx;
-      }
-      __syncthreads();
-      return total;
-    };
-    uint32_t cnt = compact();
-    // exactness of the 31-bit keys: candidates closer than w with equal keys but different hashes
-    if (cnt > (uint32_t)X2_CAP && !T.any_n && !T.slow) {
-      // too many for the staging (and the tie check works on the staged list): exact selection
-      slow_path();
-      if (tid == 0 || tid == X2_NT - 1 || !blk_in) selmask = 0;
-      cnt = compact();
-    } else if (!T.any_n && !T.slow && ks > 0 && !(a.dbg_flags & 2u)) {
-      bool tie = false;
-      for (uint32_t r = tid; r < cnt; r += X2_NT) {
-        const uint32_t vr = se[r];
-        const int er = vr & 0xFFFFu;
-        // later candidates within W positions: three independent SMEM loads per round
-        for (uint32_t q = r + 1; q < cnt; q += 3) {
-          uint32_t vq[3];
-#pragma unroll
-          for (int u = 0; u < 3; u++) vq[u] = q + u < cnt ? se[q + u] : 0xFFFFu;
-          bool more = true;
-#pragma unroll
-          for (int u = 0; u < 3; u++) {
-            if ((int)(vq[u] & 0xFFFFu) - er >= W) { more = false; break; }
-            if ((vq[u] >> 16) == (vr >> 16)) {  // 16 key bits agree: compare the full keys and hashes
-              const uint64_t hr = HZ[er] & ~(1ull << 63), hq = HZ[vq[u] & 0xFFFFu] & ~(1ull << 63);
-              tie |= ((hq >> ks) == (hr >> ks)) & (hq != hr);
-            }
-          }
-          if (!more) break;
-        }
-      }
-      if (__syncthreads_or(tie)) {
-        if (tid == 0 && a.dbg_counts) atomicAdd(&a.dbg_counts[1], 1u);
-        slow_path();
-        if (tid == 0 || tid == X2_NT - 1 || !blk_in) selmask = 0;
-        cnt = compact();
-      }
-    }
-    // publish this tile's count; its records leave two iterations later (warp 0, flush_warp0), or
-    // now if they did not fit the staging
-    if (tid == 0 && !(a.dbg_flags & 1u)) lb_publish(a.status, tile, cnt);
-    if (cnt > (uint32_t)X2_CAP) {
-      if (wid == 0) {
-        uint64_t base;
-        if (a.dbg_flags & 1u) base = lane == 0 ? atomicAdd((unsigned long long*)&a.status[ntiles], (unsigned long long)cnt) : 0;
-        else base = lb_resolve_warp(a.status, tile, cnt);
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (lane == 0) {
-          s_ovf_base = base;
-          if (tile == ntiles - 1) *a.total_out = base + cnt;
-        }
-      }
-      __syncthreads();
-      const uint64_t base = s_ovf_base;
-      if (a.job_off && blk_in && tid > 0 && tid < X2_NT - 1 && l0 == 0) a.job_off[J] = base + my_idx0;
-      uint32_t m = selmask, idx = my_idx0;
-      const uint32_t pb = sjp[J - j0] + (uint32_t)pat_off(PP, PX, (int)l0);
-      while (m) {
-        const int i = __ffs(m) - 1;
-        m &= m - 1;
-        const uint64_t gi = base + idx;
         if (gi < a.cap) {
           a.out_hz[gi] = HZ[tid * W + i];
-          a.out_pos[gi] = pb + pat_delta<PP, PX>(l0 % PX, (uint32_t)i);
+          a.out_pos[gi] = pb + pat_delta<PP, PX>(r0, (uint32_t)i);
           if (a.out_job) a.out_job[gi] = J;
         }
-        ++idx;
+        ++gi;
       }
-      cnt = X2_FLUSHED;
     }
-    pend_old = pend_new;
-    cnt_old = cnt_new;
-    pend_new = tile;
-    cnt_new = cnt;
-    buf ^= 1;
-    __syncthreads();
   }
-  // pend_old was flushed in the last (tile-less) iteration; the newest tile is in buffer buf ^ 1
-  if (pend_new >= 0 && cnt_new != X2_FLUSHED && wid == 0) flush_warp0((uint64_t)pend_new, cnt_new, buf ^ 1);
+  if constexpr (ORDERED) {
+    if (p_tile >= 0) {
+      if (wid == 0) resolve_pending();
+      __syncthreads();
+      write_pending();
+    }
+  }
 }
 
 // per-tile descriptors: first and last job (binary searches over the padded bases), the tile's
@@ -832,23 +846,27 @@ __global__ void k_x2_sizes(const Job* __restrict__ jobs, uint32_t n, int K, int 
   if ((threadIdx.x & 31) == 0 && acc) atomicAdd(nk_sum, (unsigned long long)acc);
 }
 
-template <int K, int W, int PP, int PX>
+template <int K, int W, int PP, int PX, bool ORDERED>
 size_t x2_smem_bytes() {
-  return X2Cfg<K, W, PP, PX>::SMEM;
+  return X2Cfg<K, W, PP, PX>::smem(ORDERED);
 }
 
-template <int K, int W, int PP, int PX>
-void launch_x2(const X2Args& a, uint64_t ntiles, cudaStream_t st, const char* tag) {
-  static int grid = 0;
-  const size_t smem = x2_smem_bytes<K, W, PP, PX>();
-  if (!grid) {
-    GOD_CUDA(cudaFuncSetAttribute(k_extract2<K, W, PP, PX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+template <int K, int W, int PP, int PX, bool ORDERED>
+void launch_x3(const X2Args& a, uint64_t ntiles, cudaStream_t st, const char* tag) {
+  static int grid[64] = {0};  // per device
+  int dev = 0;
+  GOD_CUDA(cudaGetDevice(&dev));
+  const size_t smem = x2_smem_bytes<K, W, PP, PX, ORDERED>();
+  if (!grid[dev & 63]) {
+    GOD_CUDA(cudaFuncSetAttribute(k_extract3<K, W, PP, PX, ORDERED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
     int per_sm = 0;
-    GOD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_extract2<K, W, PP, PX>, X2_NT, smem));
-    grid = (per_sm > 0 ? per_sm : 1) * num_sms();
+    GOD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_extract3<K, W, PP, PX, ORDERED>, X2_NT, smem));
+    grid[dev & 63] = (per_sm > 0 ? per_sm : 1) * num_sms();
   }
-  const unsigned g = (unsigned)(ntiles < (uint64_t)grid ? ntiles : (uint64_t)grid);
-  GOD_LAUNCH(tag, (k_extract2<K, W, PP, PX>), g, X2_NT, smem, st, a);
+  const int g0 = grid[dev & 63];
+  const unsigned g = (unsigned)(ntiles < (uint64_t)g0 ? ntiles : (uint64_t)g0);
+  GOD_LAUNCH(tag, (k_extract3<K, W, PP, PX, ORDERED>), g, X2_NT, smem, st, a);
 }
 
 }  // namespace
@@ -871,7 +889,10 @@ bool x2_supported(const Params& P) {
 // Returns false if no specialised kernel exists for these parameters (caller uses the generic one).
 bool run_extract2(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const Job* jobs, uint32_t n_jobs,
                   bool want_job, bool want_job_off, Records& rec, cudaStream_t st, Scratch& scr,
-                  uint64_t cap_hint, const char* tag, const X2Layout* x2) {
+                  uint64_t cap_hint, const char* tag, const X2Layout* x2, bool any_order) {
+  // record order: position order unless the caller sorts by (hash, pos) itself and needs no job offsets
+  const bool ordered = getenv("GOD_X2_ANY_ORDER_TIMING") ? false  // developer timing hook: unordered, wrong order
+                       : (!any_order || want_job || want_job_off || 2 * P.k < 36 || getenv("GOD_X2_ORDERED"));
   if (!x2_supported(P)) return false;
   const int PP = (int)P.pat.p, PX = (int)P.pat.x;
   const int K = P.k, W = P.w;
@@ -933,7 +954,7 @@ bool run_extract2(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const
   uint32_t key_shift = 2 * K > 31 ? 2 * K - 31 : 0;
   if (dbg) {
     const int kbits = atoi(dbg);
-    if (kbits > 0 && kbits < 2 * K) key_shift = 2 * K - kbits;
+    if (kbits > 0 && kbits < 2 * K) key_shift = std::min(2 * K - kbits, 31);  // keys of >= 2k - 31 bits
   }
   for (int attempt = 0; attempt < 2; attempt++) {
     rec.cap = cap;
@@ -942,16 +963,27 @@ bool run_extract2(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const
     rec.job = want_job ? scr.alloc<uint32_t>(cap) : nullptr;
     GOD_CUDA(cudaMemsetAsync(status, 0, (ntiles + 1) * sizeof(uint64_t), st));
     GOD_CUDA(cudaMemsetAsync(ctr, 0, sizeof(uint32_t), st));
+    GOD_CUDA(cudaMemsetAsync(dtotal, 0, sizeof(uint64_t), st));  // the unordered kernel's output counter
     X2Args a{seq, seq_bytes, jobs, kb, cw, n_jobs, total_blocks, P.pat.one[0], key_shift, status, ctr,
              rec.hz, rec.pos, rec.job, rec.job_off, cap, dtotal, dbg_flags, dbg_counts, desc};
     if (ntiles) {
       auto by_pattern = [&](auto kc, auto wc) {
         constexpr int KK = decltype(kc)::value, WW = decltype(wc)::value;
-        if (PX == 1 && PP == 1) launch_x2<KK, WW, 1, 1>(a, ntiles, st, tag);
-        else if (PX == 1 && PP == 2) launch_x2<KK, WW, 2, 1>(a, ntiles, st, tag);
-        else if (PX == 1) launch_x2<KK, WW, 3, 1>(a, ntiles, st, tag);
-        else if (PX == 2) launch_x2<KK, WW, 3, 2>(a, ntiles, st, tag);
-        else launch_x2<KK, WW, 4, 3>(a, ntiles, st, tag);
+        auto go = [&](auto oc) {
+          constexpr bool O = decltype(oc)::value;
+          if (PX == 1 && PP == 1) launch_x3<KK, WW, 1, 1, O>(a, ntiles, st, tag);
+          else if (PX == 1 && PP == 2) launch_x3<KK, WW, 2, 1, O>(a, ntiles, st, tag);
+          else if (PX == 1) launch_x3<KK, WW, 3, 1, O>(a, ntiles, st, tag);
+          else if (PX == 2) launch_x3<KK, WW, 3, 2, O>(a, ntiles, st, tag);
+          else launch_x3<KK, WW, 4, 3, O>(a, ntiles, st, tag);
+        };
+        // unordered instances only where a caller may ask for them (the index path, 2k >= 36)
+        if constexpr (2 * KK >= 36) {
+          if (!ordered) go(std::false_type());
+          else go(std::true_type());
+        } else {
+          go(std::true_type());
+        }
       };
       if (K == 21 && W == 11) by_pattern(std::integral_constant<int, 21>(), std::integral_constant<int, 11>());
       else if (K == 19 && W == 19) by_pattern(std::integral_constant<int, 19>(), std::integral_constant<int, 19>());

@@ -438,6 +438,7 @@ __global__ void __launch_bounds__(BS_NT, 2) k_bin_sort(uint64_t* __restrict__ k,
   __shared__ __align__(16) uint32_t cnt[CNT_WORDS];
   __shared__ uint32_t wsum[BS_NW];
   __shared__ uint32_t s_or[BS_NW], s_and[BS_NW];
+  __shared__ uint64_t s_vo[BS_NW], s_va[BS_NW];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint64_t lmask = (1ull << L) - 1, hmask = (1ull << hbits) - 1;
   const uint32_t lmax = (uint32_t)((1ull << (63 - hbits)) - 1);  // run length field above the hash (capped)
@@ -494,9 +495,56 @@ __global__ void __launch_bounds__(BS_NT, 2) k_bin_sort(uint64_t* __restrict__ k,
     for (int q = 0; q < BS_NW; q++) { mn = min(mn, s_or[q]); mx = max(mx, s_and[q]); }
     const uint64_t segv = wsum[0];
     __syncthreads();
-    if (mn == mx) {  // one hash: position order already (the stable passes over b kept it)
-      for (int i = threadIdx.x; i < n; i += BS_NT)
-        k[s + i] = (k[s + i] & ~(hmask ^ HASH_BITS_MASK)) | ((uint64_t)min((uint32_t)n, lmax) << hbits);
+    // K1 emits records in tile order (any order within a bin): one-hash bins and buckets of very
+    // frequent hashes are put in (hash, pos) order by an LSD over the packed bits that vary
+    auto lsd_varying = [&](int top_bit) -> const uint64_t* {
+      uint64_t o = 0, a = ~0ull;
+#pragma unroll
+      for (int j = 0; j < BS_IPT; j++) {
+        const int i = wid * (32 * BS_IPT) + j * 32 + lane;
+        if (i < n) { o |= x[j]; a &= x[j]; }
+      }
+#pragma unroll
+      for (int d = 16; d; d >>= 1) {
+        o |= __shfl_xor_sync(0xffffffffu, o, d);
+        a &= __shfl_xor_sync(0xffffffffu, a, d);
+      }
+      if (lane == 0) { s_vo[wid] = o; s_va[wid] = a; }
+      __syncthreads();
+      uint64_t vo = 0, va = ~0ull;
+#pragma unroll
+      for (int q = 0; q < BS_NW; q++) { vo |= s_vo[q]; va &= s_va[q]; }
+      const uint64_t vary = vo & ~va;
+      __syncthreads();
+      uint64_t* dst = A;
+      bool first = true;
+      for (int sh = 1; sh < top_bit; sh += RS_BITS) {
+        const int bits = min(RS_BITS, top_bit - sh);
+        const uint32_t dm = (1u << bits) - 1;
+        if (((vary >> sh) & dm) == 0) continue;  // a constant digit: the pass is the identity
+        if (!first) cta_load_striped(dst == A ? Bf : A, n, x);
+        cta_rank_scatter(x, n, sh, dm, dst, cnt, wsum);
+        dst = dst == A ? Bf : A;
+        first = false;
+      }
+      if (first) {  // nothing varies (cannot happen: positions differ within a bin): the loaded order
+#pragma unroll
+        for (int j = 0; j < BS_IPT; j++) {
+          const int i = wid * (32 * BS_IPT) + j * 32 + lane;
+          if (i < n) A[i] = x[j];
+        }
+        __syncthreads();
+        return A;
+      }
+      return dst == A ? Bf : A;
+    };
+    if (mn == mx) {  // one hash: sort by position
+      const uint64_t* res = lsd_varying(33);
+      for (int i = threadIdx.x; i < n; i += BS_NT) {
+        const uint64_t pv = res[i];
+        __stcs(k + s + i, ((segv << L) | (pv >> 33)) | ((uint64_t)min((uint32_t)n, lmax) << hbits) | ((pv & 1ull) << 63));
+        __stcs(v + s + i, (uint32_t)(pv >> 1));
+      }
       if (threadIdx.x == 0) {
         if ((uint32_t)n < SMALL_BINS) atomicAdd(&rh[n], 1u);
         else ro.large[atomicAdd(ro.n_large, 1u)] = (uint32_t)n;
@@ -576,14 +624,7 @@ __global__ void __launch_bounds__(BS_NT, 2) k_bin_sort(uint64_t* __restrict__ k,
       //     the highest bit where mn and mx differ (bits above it are constant in the bin)
       if (threadIdx.x == 0) atomicAdd(n_big + 1, 1u);  // statistics: bins sorted this way
       const int hib = 32 - __clz(mn ^ mx);
-      uint64_t* dst = A;
-      for (int sh = 0; sh < hib; sh += RS_BITS) {
-        const int bits = min(RS_BITS, hib - sh);
-        if (sh) cta_load_striped(dst == A ? Bf : A, n, x);
-        cta_rank_scatter(x, n, 33 + sh, (1u << bits) - 1, dst, cnt, wsum);
-        dst = dst == A ? Bf : A;
-      }
-      res = dst == A ? Bf : A;
+      res = lsd_varying(33 + hib);
     }
     // K3 fused: runs never cross a bin (a hash lies in one bin).  Per-element run length from two
     // block scans over the run-head indices (start = last head <= i, end = first head > i); it is
@@ -676,12 +717,13 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort_big(uint64_t* __restri
     __shared__ unsigned long long s_diff;
     if (threadIdx.x == 0) s_diff = 0;
     __syncthreads();
-    const uint64_t k0 = k[s] & lowmask;
-    uint64_t diff = 0;  // low-hash bits that vary across the bin (a bin of one frequent hash: none)
+    const uint64_t x0 = ((k[s] & lowmask) << 33) | ((uint64_t)v[s] << 1) | (k[s] >> 63);
+    uint64_t diff = 0;  // packed bits that vary across the bin (records arrive in any order)
     for (uint64_t i = threadIdx.x; i < n; i += BS_NT) {
       const uint64_t kk = k[s + i];
-      diff |= (kk & lowmask) ^ k0;
-      t0[s + i] = ((kk & lowmask) << 33) | ((uint64_t)v[s + i] << 1) | (kk >> 63);
+      const uint64_t xv = ((kk & lowmask) << 33) | ((uint64_t)v[s + i] << 1) | (kk >> 63);
+      diff |= xv ^ x0;
+      t0[s + i] = xv;
     }
     for (int o = 16; o; o >>= 1) diff |= __shfl_xor_sync(0xffffffffu, diff, o);
     if ((threadIdx.x & 31) == 0 && diff) atomicOr(&s_diff, (unsigned long long)diff);
@@ -689,10 +731,10 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort_big(uint64_t* __restri
     const uint64_t vary = s_diff;
     uint64_t* src = t0 + s;
     uint64_t* dst = t1 + s;
-    for (int sh = 0; sh < lo_bits; sh += RS_BITS) {
-      const int bits = min(RS_BITS, lo_bits - sh);
+    for (int sh = 1; sh < 33 + lo_bits; sh += RS_BITS) {  // (pos, then low hash) digits, LSD
+      const int bits = min(RS_BITS, 33 + lo_bits - sh);
       const uint32_t dmask = (1u << bits) - 1;
-      const int shift = 33 + sh;
+      const int shift = sh;
       if (((vary >> sh) & dmask) == 0) continue;  // a constant digit: the stable pass is the identity
       for (int i = threadIdx.x; i < RS_BINS; i += BS_NT) hist[i] = 0;
       __syncthreads();
@@ -1121,7 +1163,10 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
   JobSet js = make_jobs(P, ref_offsets, n_refs, nullptr, 0, 0, true, st, scr);
   Records rec;
   const uint64_t est = js.total_pos / (uint64_t)(P.w + 1) * 2 + js.total_pos / 8 + 4096;
-  run_extract(P, ref, js.seq_bytes, js.jobs, js.kb, js.n, js.total_pos, false, false, rec, st, scr, est, "extract_ref", js.x2p());
+  const bool bin_sort = 2 * P.k >= 36 && 2 * P.k - SEG_BITS <= 30 && !getenv("GOD_SORT_FULL");
+  // the bin sort orders every bin by the packed (hash, pos) key, so K1 may emit records in tile order
+  run_extract(P, ref, js.seq_bytes, js.jobs, js.kb, js.n, js.total_pos, false, false, rec, st, scr, est, "extract_ref",
+              js.x2p(), bin_sort);
   const uint64_t n = rec.n;
   // K2: stable LSD radix sort on the 2k hash bits
   uint64_t* k0 = rec.hz;
@@ -1164,7 +1209,7 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
       std::swap(k0, k1);
       std::swap(v0, v1);
     };
-    if (hbits >= 36 && hbits - SEG_BITS <= 30 && !getenv("GOD_SORT_FULL")) {
+    if (bin_sort) {
       // K2 bin sort (see the comment above k_seg_hist)
       const int L = hbits - SEG_BITS;
       segc = scr.alloc<uint32_t>(1u << SEG_BITS);

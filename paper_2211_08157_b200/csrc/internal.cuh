@@ -44,13 +44,16 @@ bool x2_supported(const Params& P);
 // from `scr` (capacity grown on demand), fills rec.n (synchronizes once to read the count).
 void run_extract(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const Job* jobs, const uint64_t* kb,
                  uint32_t n_jobs, uint64_t total_pos, bool want_job, bool want_job_off, Records& rec, cudaStream_t st,
-                 Scratch& scr, uint64_t cap_hint, const char* tag = "k_extract", const X2Layout* x2 = nullptr);
+                 Scratch& scr, uint64_t cap_hint, const char* tag = "k_extract", const X2Layout* x2 = nullptr,
+                 bool any_order = false);
 // Specialised register-resident kernel (extract2.cu) for x == 1 patterns of period 1 to 3 (and the
 // '110' / '1110' shapes) and (k, w) in {(21,11), (19,19), (15,10), (19,16)}; returns false if not
 // applicable.
+// any_order: the caller sorts the records by (hash, pos) itself (tile order, one atomic per tile,
+// instead of position order through a decoupled look-back)
 bool run_extract2(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const Job* jobs, uint32_t n_jobs,
                   bool want_job, bool want_job_off, Records& rec, cudaStream_t st, Scratch& scr,
-                  uint64_t cap_hint, const char* tag, const X2Layout* x2 = nullptr);
+                  uint64_t cap_hint, const char* tag, const X2Layout* x2 = nullptr, bool any_order = false);
 
 // Build jobs for n sequences: phase from `phases` (nullable -> 0) or, if p_all != 0, one job per
 // (sequence, s) for s < p_all (job index = seq * p_all + s).  nk capped at kcap (0 = no cap).
