@@ -247,7 +247,7 @@ __global__ void k_make_jobs(Params P, const uint64_t* offsets, uint32_t n_seqs, 
                             uint32_t kcap, int global_pos, Job* jobs, uint64_t* nkp1, int x2, uint64_t* cw,
                             unsigned long long* nk_sum) {
   const uint64_t nj = p_all ? (uint64_t)n_seqs * p_all : n_seqs;
-  uint64_t acc = 0;
+  uint64_t acc = 0, mxb = 0;
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < nj; j += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t sidx = p_all ? j / p_all : j;
     const uint32_t s = p_all ? (uint32_t)(j % p_all) : (phases ? phases[sidx] : 0u);
@@ -266,13 +266,24 @@ __global__ void k_make_jobs(Params P, const uint64_t* offsets, uint32_t n_seqs, 
       nkp1[j] = (nk ? (nk + W - 1) / W : 1) * W;
       cw[j] = nk ? (nk + P.k - 1 + 15) / 16 : 0;
       acc += nk;
+      mxb = max(mxb, nk ? (nk + W - 1) / W : 1);
     } else {
       nkp1[j] = nk + 1;
     }
   }
   if (x2) {
-    for (int d = 16; d; d >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, d);
+    for (int d = 16; d; d >>= 1) {
+      acc += __shfl_xor_sync(0xffffffffu, acc, d);
+      mxb = max(mxb, __shfl_xor_sync(0xffffffffu, mxb, d));
+    }
     if ((threadIdx.x & 31) == 0 && acc) atomicAdd(nk_sum, (unsigned long long)acc);
+    // blocks of the longest job: one atomic per CTA (a per-warp atomicMax on one word serialised)
+    __shared__ unsigned long long s_mx;
+    if (threadIdx.x == 0) s_mx = 0;
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0 && mxb) atomicMax(&s_mx, (unsigned long long)mxb);
+    __syncthreads();
+    if (threadIdx.x == 0 && s_mx) atomicMax(nk_sum + 1, s_mx);
   }
 }
 }  // namespace
@@ -287,23 +298,24 @@ JobSet make_jobs(const Params& P, const uint64_t* offsets, uint32_t n_seqs, cons
   if (nj && x2_supported(P)) {  // the specialised kernel's layout in the same pass (no generic layout)
     uint64_t* kb = scr.alloc<uint64_t>(nj + 1);
     uint64_t* cw = scr.alloc<uint64_t>(nj + 1);
-    uint64_t* tot = scr.alloc<uint64_t>(3);
-    GOD_CUDA(cudaMemsetAsync(tot + 2, 0, sizeof(uint64_t), st));
+    uint64_t* tot = scr.alloc<uint64_t>(4);
+    GOD_CUDA(cudaMemsetAsync(tot + 2, 0, 2 * sizeof(uint64_t), st));
     GOD_LAUNCH("k_make_jobs", k_make_jobs, grid_for(nj, 256), 256, 0, st, P, offsets, n_seqs, phases, p_all, kcap,
                global_pos, js.jobs, kb, 1, cw, reinterpret_cast<unsigned long long*>(tot + 2));
     scan_exclusive_u64(kb, kb, nj, tot, st, scr, "scan_jobs");
     scan_exclusive_u64(cw, cw, nj, tot + 1, st, scr, "scan_jobs");
     GOD_CUDA(cudaMemcpyAsync(kb + nj, tot, sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
     GOD_CUDA(cudaMemcpyAsync(cw + nj, tot + 1, sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
-    uint64_t h[4] = {0, 0, 0, 0};
-    d2h_small(h, tot, 3 * sizeof(uint64_t), st);
-    d2h_small(&h[3], offsets + n_seqs, sizeof(uint64_t), st);
+    uint64_t h[5] = {0, 0, 0, 0, 0};
+    d2h_small(h, tot, 4 * sizeof(uint64_t), st);
+    d2h_small(&h[4], offsets + n_seqs, sizeof(uint64_t), st);
     js.x2.kb = kb;
     js.x2.cw = cw;
     js.x2.total_pos = h[0];
     js.x2.nk_sum = h[2];
+    js.x2.max_job_blocks = h[3];
     js.total_pos = h[2] + nj;  // the generic layout's size (cap estimates)
-    js.seq_bytes = h[3];
+    js.seq_bytes = h[4];
     return js;
   }
   js.kb = scr.alloc<uint64_t>(nj + 1);
@@ -324,9 +336,9 @@ JobSet make_jobs(const Params& P, const uint64_t* offsets, uint32_t n_seqs, cons
 
 void run_extract(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const Job* jobs, const uint64_t* kb,
                  uint32_t n_jobs, uint64_t total_pos, bool want_job, bool want_job_off, Records& rec, cudaStream_t st,
-                 Scratch& scr, uint64_t cap_hint, const char* tag, const X2Layout* x2, bool any_order) {
+                 Scratch& scr, uint64_t cap_hint, const char* tag, const X2Layout* x2, RecOrder order) {
   rec.n = 0;
-  if (run_extract2(P, seq, seq_bytes, jobs, n_jobs, want_job, want_job_off, rec, st, scr, cap_hint, tag, x2, any_order))
+  if (run_extract2(P, seq, seq_bytes, jobs, n_jobs, want_job, want_job_off, rec, st, scr, cap_hint, tag, x2, order))
     return;
   if (n_jobs == 0 || total_pos == 0) {
     rec.cap = 1;
@@ -335,6 +347,7 @@ void run_extract(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const 
     if (want_job) rec.job = scr.alloc<uint32_t>(1);
     if (want_job_off) {
       rec.job_off = scr.alloc<uint64_t>(n_jobs + 1);
+      rec.job_end = rec.job_off + 1;
       GOD_CUDA(cudaMemsetAsync(rec.job_off, 0, (n_jobs + 1) * sizeof(uint64_t), st));
     }
     return;
@@ -354,7 +367,10 @@ void run_extract(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const 
   uint64_t* status = scr.alloc<uint64_t>(ntiles);
   uint32_t* ctr = scr.alloc<uint32_t>(1);
   uint64_t* dtotal = scr.alloc<uint64_t>(1);
-  if (want_job_off) rec.job_off = scr.alloc<uint64_t>(n_jobs + 1);
+  if (want_job_off) {
+    rec.job_off = scr.alloc<uint64_t>(n_jobs + 1);
+    rec.job_end = rec.job_off + 1;  // position order: a job ends where the next begins
+  }
   for (int attempt = 0; attempt < 2; attempt++) {
     rec.cap = cap;
     rec.hz = scr.alloc<uint64_t>(cap);

@@ -61,11 +61,14 @@ struct X2Args {
   uint32_t* out_pos;
   uint32_t* out_job;
   uint64_t* job_off;
+  uint64_t* job_end;    // aligned tiles: one past each job's last record (else null: job_off[j + 1])
   uint64_t cap;
   uint64_t* total_out;
   uint32_t dbg_flags;      // developer toggles (GOD_X2_DBG): 2 = no tie check
   uint32_t* dbg_counts;    // [0] tiles on the slow path, [1] tiles with a key tie
   const struct X2Desc* desc;  // [ntiles] per-tile descriptors (k_x2_tile_desc)
+  uint32_t aligned;     // tiles are whole jobs (k_x2_tile_desc_aligned): no halo blocks
+  uint64_t ntiles;
 };
 
 __device__ __forceinline__ uint32_t find_job_le(const uint64_t* arr, uint32_t lo, uint32_t hi, uint64_t g) {
@@ -93,11 +96,13 @@ __device__ __forceinline__ uint32_t rev2(uint32_t x) {  // reverse the 16 2-bit 
 struct __align__(16) X2Desc {
   uint32_t j0, j1, simple, safe;  // safe: every byte the tile may read is inside the buffer
   uint64_t cw_lo, cw_hi;
+  uint64_t b0;                    // aligned tiles: first block (thread 0's), and the block count
+  uint32_t nb, pad;
 };
 
 struct X2Tile {  // per-tile scalars, in SMEM
-  uint32_t tile, j0, j1, simple, safe, slow;
-  uint64_t cw_lo, cw_hi;
+  uint32_t tile, j0, j1, simple, safe, slow, nb;
+  uint64_t cw_lo, cw_hi, b0;
 };
 
 template <int K, int W, int PP, int PX>
@@ -378,7 +383,7 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract3(X2Args a) {
   __shared__ uint64_t s_base;
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const uint64_t ntiles = (a.total_blocks + X2_OUT_BLOCKS - 1) / X2_OUT_BLOCKS;
+  const uint64_t ntiles = a.ntiles;
   const uint32_t ks = a.key_shift;  // <= 31
   {  // expected-letter table: for 4 MSB-first codes pk, bytes "ACGT"[c_i], base 0 in byte 0
     const uint32_t L4 = 0x54474341u;
@@ -439,6 +444,8 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract3(X2Args a) {
         T.simple = nd.simple;
         T.safe = nd.safe;
         T.slow = 0;
+        T.b0 = nd.b0;
+        T.nb = nd.nb;
         if (!ORDERED) {
           next_t = atomicAdd(a.tile_ctr, 1u);
           if (next_t < ntiles) nd = a.desc[next_t];
@@ -509,8 +516,13 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract3(X2Args a) {
     const bool any_n = __syncthreads_or(my_n != 0);
 
     // ---- my block: job J, first k-mer index l0
-    const int64_t myb = (int64_t)tile * X2_OUT_BLOCKS - 1 + tid;
-    const bool blk_in = myb >= 0 && (uint64_t)myb < a.total_blocks;
+    // aligned tiles: blocks b0 .. b0 + nb - 1 (whole jobs, job boundaries are window barriers, no halo);
+    // else blocks tile * 126 - 1 .. tile * 126 + 126, the first and last computed as halo only
+    const bool aligned = a.aligned != 0;
+    const int64_t myb = aligned ? (int64_t)(T.b0 + tid) : (int64_t)tile * X2_OUT_BLOCKS - 1 + tid;
+    const bool blk_in = aligned ? (uint32_t)tid < T.nb : (myb >= 0 && (uint64_t)myb < a.total_blocks);
+    const bool emit_blk = blk_in && (aligned || (tid > 0 && tid < X2_NT - 1));
+    const int tile_nb = (int)T.nb;  // (T is rewritten for the next tile while this one writes out)
     uint32_t J = j0, l0 = 0, nk = 0;
     if (blk_in) {
       const uint64_t g = (uint64_t)myb * W;
@@ -638,7 +650,7 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract3(X2Args a) {
         const uint32_t firstk = (uint32_t)((HZ[tid * W + firsto] & ~(1ull << 63)) >> ks) + 1u;
         if (firsto < plo && firstk == plk) tie = true;
       }
-      if (tid == 0 || tid == X2_NT - 1) need_slow = false;  // halo blocks are not emitted
+      if (!aligned && (tid == 0 || tid == X2_NT - 1)) need_slow = false;  // halo blocks are not emitted
       if (a.dbg_flags & 2u) tie = false;
       const int flags = __syncthreads_or((need_slow ? 1 : 0) | (tie ? 2 : 0));
       if (tid == 0 && flags) T.slow = (uint32_t)flags;
@@ -670,14 +682,14 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract3(X2Args a) {
       }
       __syncthreads();
       uint32_t m = 0;
-      if (tid > 0 && tid < X2_NT - 1) {
+      if (emit_blk) {
         for (int i = 0; i < W; i++) {
           const int j = tid * W + i;
           const uint64_t hj = H64[j];
           if (hj == 0) continue;
           int lo = j, hi = j;
-          while (lo > j - (W - 1) && H64[lo - 1] != 0 && sjob[(lo - 1) / W] == J) --lo;
-          while (hi < j + (W - 1) && H64[hi + 1] != 0 && sjob[(hi + 1) / W] == J) ++hi;
+          while (lo > 0 && lo > j - (W - 1) && H64[lo - 1] != 0 && sjob[(lo - 1) / W] == J) --lo;
+          while (hi + 1 < POS && hi < j + (W - 1) && H64[hi + 1] != 0 && sjob[(hi + 1) / W] == J) ++hi;
           bool s = false;
           if (hi - lo + 1 < W) {
             uint64_t mn = ~0ull;
@@ -700,7 +712,7 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract3(X2Args a) {
         HZ[tid * W + i] = (H64[tid * W + i] - 1) | ((uint64_t)((zmask >> i) & 1u) << 63);
       selmask = m;
     }
-    if (tid == 0 || tid == X2_NT - 1 || !blk_in) selmask = 0;
+    if (!emit_blk) selmask = 0;
 
     // ------------------------------------------------------------------ E. output
     const uint32_t cnt = __popc(selmask);
@@ -735,7 +747,7 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract3(X2Args a) {
       p_pb = sjp[J - j0] + (uint32_t)pat_off(PP, PX, (int)l0);
       p_r0 = l0 % PX;
       p_J = J;
-      p_start = blk_in && tid > 0 && tid < X2_NT - 1 && l0 == 0;
+      p_start = emit_blk && l0 == 0;
       p_hz = HZ;
       HZ = (HZ == HZ0) ? HZ0 + POS : HZ0;
       continue;
@@ -756,7 +768,9 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract3(X2Args a) {
       }
       __syncthreads();
       const uint64_t base = s_base;
-      if (a.job_off && blk_in && tid > 0 && tid < X2_NT - 1 && l0 == 0) a.job_off[J] = base + before + incl - cnt;
+      if (a.job_off && emit_blk && l0 == 0) a.job_off[J] = base + before + incl - cnt;
+      // aligned tiles: the last block of each job records the job's end (jobs lie in one tile)
+      if (a.job_end && emit_blk && (tid + 1 >= tile_nb || sjob[tid + 1] != J)) a.job_end[J] = base + before + incl;
       for (uint32_t r = tid; r < total; r += X2_NT) {
         const uint64_t gi = base + r;
         if (gi < a.cap) {
@@ -768,7 +782,8 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract3(X2Args a) {
     }
     __syncthreads();
     uint64_t gi = s_base + rank;
-    if (a.job_off && blk_in && tid > 0 && tid < X2_NT - 1 && l0 == 0) a.job_off[J] = gi;
+    if (a.job_off && emit_blk && l0 == 0) a.job_off[J] = gi;
+    if (a.job_end && emit_blk && (tid + 1 >= tile_nb || sjob[tid + 1] != J)) a.job_end[J] = gi + cnt;
     if (selmask) {
       const uint32_t pb = sjp[J - j0] + (uint32_t)pat_off(PP, PX, (int)l0);
       const uint32_t r0 = l0 % PX;
@@ -831,19 +846,62 @@ __global__ void k_x2_tile_desc(const uint64_t* __restrict__ kb, const uint64_t* 
   }
 }
 
+// job-aligned tiles (every job <= 129 - S blocks): tile t starts at the first job whose first block
+// is >= t * S and ends where tile t + 1 starts, so it holds whole jobs and at most 128 blocks
+__global__ void k_x2_tile_desc_aligned(const uint64_t* __restrict__ kb, const uint64_t* __restrict__ cw,
+                                       const Job* __restrict__ jobs, uint32_t n_jobs, int W, uint32_t S, int PP,
+                                       int PX, uint32_t one0, uint64_t seq_bytes, uint64_t ntiles, X2Desc* desc) {
+  auto first_job_at = [&](uint64_t g) -> uint32_t {  // smallest j with kb[j] >= g (n_jobs if none)
+    uint32_t lo = 0, hi = n_jobs;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (kb[mid] < g) lo = mid + 1;
+      else hi = mid;
+    }
+    return lo;
+  };
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < ntiles; t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t j0 = first_job_at(t * S * (uint64_t)W);
+    const uint32_t je = first_job_at((t + 1) * S * (uint64_t)W);  // first job of the next tile
+    X2Desc d;
+    d.j0 = j0 < n_jobs ? j0 : n_jobs - 1;
+    d.j1 = je > j0 ? je - 1 : d.j0;
+    d.b0 = kb[j0 < n_jobs ? j0 : n_jobs] / W;
+    d.nb = je > j0 ? (uint32_t)((kb[je] - kb[j0]) / W) : 0u;
+    d.pad = 0;
+    d.cw_lo = cw[d.j0];
+    d.cw_hi = je > j0 ? cw[je] : cw[d.j0];
+    const Job jl = jobs[d.j1];
+    const uint64_t last_l = jl.seq_off + jl.phase + one0 + (16 * (d.cw_hi - cw[d.j1]) / PX + 1) * PP + 48;
+    d.simple = (d.j0 == d.j1) && last_l <= seq_bytes;
+    d.safe = last_l <= seq_bytes;
+    desc[t] = d;
+  }
+}
+
 // padded position bases (multiple of W) and code-word bases per job
 __global__ void k_x2_sizes(const Job* __restrict__ jobs, uint32_t n, int K, int W, uint64_t* kb, uint64_t* cw,
                            unsigned long long* nk_sum) {
-  uint64_t acc = 0;
+  uint64_t acc = 0, mxb = 0;
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
     const uint64_t nk = jobs[j].nk;
     kb[j] = (nk ? (nk + W - 1) / W : 1) * W;  // no separator: job boundaries are handled in-kernel
     const uint64_t ncode = nk ? nk + K - 1 : 0;
     cw[j] = (ncode + 15) / 16;
     acc += nk;
+    mxb = max(mxb, kb[j] / W);
   }
-  for (int d = 16; d; d >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, d);
+  for (int d = 16; d; d >>= 1) {
+    acc += __shfl_xor_sync(0xffffffffu, acc, d);
+    mxb = max(mxb, __shfl_xor_sync(0xffffffffu, mxb, d));
+  }
   if ((threadIdx.x & 31) == 0 && acc) atomicAdd(nk_sum, (unsigned long long)acc);
+  __shared__ unsigned long long s_mx;  // blocks of the longest job: one atomic per CTA
+  if (threadIdx.x == 0) s_mx = 0;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0 && mxb) atomicMax(&s_mx, (unsigned long long)mxb);
+  __syncthreads();
+  if (threadIdx.x == 0 && s_mx) atomicMax(nk_sum + 1, s_mx);
 }
 
 template <int K, int W, int PP, int PX, bool ORDERED>
@@ -889,10 +947,7 @@ bool x2_supported(const Params& P) {
 // Returns false if no specialised kernel exists for these parameters (caller uses the generic one).
 bool run_extract2(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const Job* jobs, uint32_t n_jobs,
                   bool want_job, bool want_job_off, Records& rec, cudaStream_t st, Scratch& scr,
-                  uint64_t cap_hint, const char* tag, const X2Layout* x2, bool any_order) {
-  // record order: position order unless the caller sorts by (hash, pos) itself and needs no job offsets
-  const bool ordered = getenv("GOD_X2_ANY_ORDER_TIMING") ? false  // developer timing hook: unordered, wrong order
-                       : (!any_order || want_job || want_job_off || 2 * P.k < 36 || getenv("GOD_X2_ORDERED"));
+                  uint64_t cap_hint, const char* tag, const X2Layout* x2, RecOrder order) {
   if (!x2_supported(P)) return false;
   const int PP = (int)P.pat.p, PX = (int)P.pat.x;
   const int K = P.k, W = P.w;
@@ -901,33 +956,42 @@ bool run_extract2(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const
   // padded layouts (built by make_jobs in the same pass as the jobs, else here)
   const uint64_t* kb;
   const uint64_t* cw;
-  uint64_t total_pos, nk_sum;
+  uint64_t total_pos, nk_sum, max_jb;
   if (x2) {
     kb = x2->kb;
     cw = x2->cw;
     total_pos = x2->total_pos;
     nk_sum = x2->nk_sum;
+    max_jb = x2->max_job_blocks;
   } else {
     uint64_t* kbw = scr.alloc<uint64_t>(n_jobs + 1);
     uint64_t* cww = scr.alloc<uint64_t>(n_jobs + 1);
-    uint64_t* tot = scr.alloc<uint64_t>(3);
-    GOD_CUDA(cudaMemsetAsync(tot + 2, 0, sizeof(uint64_t), st));
+    uint64_t* tot = scr.alloc<uint64_t>(4);
+    GOD_CUDA(cudaMemsetAsync(tot + 2, 0, 2 * sizeof(uint64_t), st));
     GOD_LAUNCH("k_x2_sizes", k_x2_sizes, grid_for(n_jobs, 256), 256, 0, st, jobs, n_jobs, K, W, kbw, cww,
                reinterpret_cast<unsigned long long*>(tot + 2));
     scan_exclusive_u64(kbw, kbw, n_jobs, tot, st, scr, "scan_x2_jobs");
     scan_exclusive_u64(cww, cww, n_jobs, tot + 1, st, scr, "scan_x2_jobs");
     GOD_CUDA(cudaMemcpyAsync(kbw + n_jobs, tot, sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
     GOD_CUDA(cudaMemcpyAsync(cww + n_jobs, tot + 1, sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
-    uint64_t htot[3];
+    uint64_t htot[4];
     d2h_small(htot, tot, sizeof(htot), st);
     kb = kbw;
     cw = cww;
     total_pos = htot[0];
     nk_sum = htot[2];
+    max_jb = htot[3];
   }
   prof_add_units(tag, nk_sum);
   const uint64_t total_blocks = total_pos / W;
-  const uint64_t ntiles = (total_blocks + X2_OUT_BLOCKS - 1) / X2_OUT_BLOCKS;
+  // Output order (RecOrder): ORDER_NONE -> tiles at atomically claimed offsets; ORDER_JOB with short jobs
+  // -> job-aligned tiles at atomically claimed offsets (each job contiguous, in position order); else
+  // position order through the decoupled look-back.  Unordered instances exist for 2k >= 36.
+  const bool can_unordered = 2 * K >= 36 && !want_job && !getenv("GOD_X2_ORDERED");
+  const bool aligned = can_unordered && order == ORDER_JOB && max_jb <= 32 && !getenv("GOD_X2_NO_ALIGN");
+  const bool ordered = !(can_unordered && (order == ORDER_NONE || aligned));
+  const uint32_t S_al = (uint32_t)(X2_NT + 1 - max_jb);  // tile stride (blocks) of the aligned layout
+  const uint64_t ntiles = aligned ? (total_blocks + S_al - 1) / S_al : (total_blocks + X2_OUT_BLOCKS - 1) / X2_OUT_BLOCKS;
   GOD_REQUIRE(ntiles < 0x7FFFFFFFull, "input too large for one extraction launch");
   uint64_t cap = cap_hint ? cap_hint : total_pos;
   if (cap > total_pos) cap = total_pos;
@@ -938,11 +1002,19 @@ bool run_extract2(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const
   if (ntiles) {
     const int NB = W + K - 1;
     const int maxwords = (X2_NT * W + X2_NT * (K - 1) + 15) / 16 + X2_NT + 8;  // X2Cfg::MAXWORDS
-    GOD_LAUNCH("k_x2_tile_desc", k_x2_tile_desc, grid_for(ntiles, 256), 256, 0, st, kb, cw, jobs, n_jobs, total_blocks,
-               W, NB, maxwords, PP, PX, P.pat.one[0], seq_bytes, ntiles, desc);
+    if (aligned)
+      GOD_LAUNCH("k_x2_tile_desc", k_x2_tile_desc_aligned, grid_for(ntiles, 256), 256, 0, st, kb, cw, jobs, n_jobs, W,
+                 S_al, PP, PX, P.pat.one[0], seq_bytes, ntiles, desc);
+    else
+      GOD_LAUNCH("k_x2_tile_desc", k_x2_tile_desc, grid_for(ntiles, 256), 256, 0, st, kb, cw, jobs, n_jobs, total_blocks,
+                 W, NB, maxwords, PP, PX, P.pat.one[0], seq_bytes, ntiles, desc);
   }
   uint64_t* dtotal = scr.alloc<uint64_t>(1);
-  if (want_job_off) rec.job_off = scr.alloc<uint64_t>(n_jobs + 1);
+  if (want_job_off) {
+    rec.job_off = scr.alloc<uint64_t>(n_jobs + 1);
+    // a job's end is the next job's start unless jobs are placed tile by tile (aligned)
+    rec.job_end = aligned ? scr.alloc<uint64_t>(n_jobs) : rec.job_off + 1;
+  }
   const char* dflag = getenv("GOD_X2_DBG");
   const uint32_t dbg_flags = dflag ? (uint32_t)atoi(dflag) : 0u;
   uint32_t* dbg_counts = nullptr;
@@ -965,7 +1037,8 @@ bool run_extract2(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const
     GOD_CUDA(cudaMemsetAsync(ctr, 0, sizeof(uint32_t), st));
     GOD_CUDA(cudaMemsetAsync(dtotal, 0, sizeof(uint64_t), st));  // the unordered kernel's output counter
     X2Args a{seq, seq_bytes, jobs, kb, cw, n_jobs, total_blocks, P.pat.one[0], key_shift, status, ctr,
-             rec.hz, rec.pos, rec.job, rec.job_off, cap, dtotal, dbg_flags, dbg_counts, desc};
+             rec.hz, rec.pos, rec.job, rec.job_off, aligned ? rec.job_end : nullptr, cap, dtotal, dbg_flags,
+             dbg_counts, desc, aligned ? 1u : 0u, ntiles};
     if (ntiles) {
       auto by_pattern = [&](auto kc, auto wc) {
         constexpr int KK = decltype(kc)::value, WW = decltype(wc)::value;

@@ -21,7 +21,8 @@ struct Records {
   uint64_t* hz = nullptr;
   uint32_t* pos = nullptr;
   uint32_t* job = nullptr;      // optional: job index per record
-  uint64_t* job_off = nullptr;  // optional: [n_jobs + 1] record offset per job
+  uint64_t* job_off = nullptr;  // optional: [n_jobs + 1] first record of each job
+  uint64_t* job_end = nullptr;  // with job_off: [n_jobs] one past each job's last record
   uint64_t n = 0;               // records written (host)
   uint64_t cap = 0;
   uint32_t* cnt = nullptr;      // optional probe results (seeding)
@@ -35,7 +36,13 @@ struct X2Layout {
   const uint64_t* kb = nullptr;
   const uint64_t* cw = nullptr;
   uint64_t total_pos = 0, nk_sum = 0;
+  uint64_t max_job_blocks = 0;  // padded w-blocks of the longest job
 };
+// What record order a caller of the extraction needs:
+//   ORDER_GLOBAL  position order across all jobs (god_minimizers' CSR output)
+//   ORDER_JOB     each job's records contiguous and in position order, jobs anywhere (job_off/job_end)
+//   ORDER_NONE    any order (the index build sorts by (hash, pos))
+enum RecOrder { ORDER_GLOBAL = 0, ORDER_JOB = 1, ORDER_NONE = 2 };
 // true iff run_extract2 has a specialised kernel for these parameters
 bool x2_supported(const Params& P);
 
@@ -45,15 +52,15 @@ bool x2_supported(const Params& P);
 void run_extract(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const Job* jobs, const uint64_t* kb,
                  uint32_t n_jobs, uint64_t total_pos, bool want_job, bool want_job_off, Records& rec, cudaStream_t st,
                  Scratch& scr, uint64_t cap_hint, const char* tag = "k_extract", const X2Layout* x2 = nullptr,
-                 bool any_order = false);
+                 RecOrder order = ORDER_GLOBAL);
 // Specialised register-resident kernel (extract2.cu) for x == 1 patterns of period 1 to 3 (and the
 // '110' / '1110' shapes) and (k, w) in {(21,11), (19,19), (15,10), (19,16)}; returns false if not
 // applicable.
-// any_order: the caller sorts the records by (hash, pos) itself (tile order, one atomic per tile,
-// instead of position order through a decoupled look-back)
+// order: see RecOrder (weaker orders let K1 write each tile at an atomically claimed offset instead
+// of through a decoupled look-back)
 bool run_extract2(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const Job* jobs, uint32_t n_jobs,
                   bool want_job, bool want_job_off, Records& rec, cudaStream_t st, Scratch& scr,
-                  uint64_t cap_hint, const char* tag, const X2Layout* x2 = nullptr, bool any_order = false);
+                  uint64_t cap_hint, const char* tag, const X2Layout* x2 = nullptr, RecOrder order = ORDER_GLOBAL);
 
 // Build jobs for n sequences: phase from `phases` (nullable -> 0) or, if p_all != 0, one job per
 // (sequence, s) for s < p_all (job index = seq * p_all + s).  nk capped at kcap (0 = no cap).

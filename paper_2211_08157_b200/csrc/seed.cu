@@ -12,6 +12,7 @@
 //   S4  anchors from the probe results: fast path (all reads from S1) = 8-lane groups per read
 //       (counts, scan over reads, write); general path = gather into read order, scan, write
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include "internal.cuh"
 
@@ -20,7 +21,8 @@ namespace god {
 struct SeedSources {
   const uint64_t* hz[3];
   const uint32_t* pos[3];
-  const uint64_t* off[3];
+  const uint64_t* off[3];   // first record of each job ...
+  const uint64_t* end[3];   // ... and one past its last (job-aligned extraction places jobs tile by tile)
   const uint32_t* cnt[3];   // probe result per record: number of kept entries with its hash
   const uint32_t* beg[3];   // ... and the first of them
 };
@@ -28,6 +30,7 @@ struct SeedSources {
 namespace {
 
 __global__ void k_phase(const uint32_t* __restrict__ occ, const Job* __restrict__ jobs, const uint64_t* __restrict__ job_off,
+                        const uint64_t* __restrict__ job_end,
                         const uint64_t* __restrict__ hz, const uint32_t* __restrict__ pos, const uint32_t* __restrict__ ids,
                         uint32_t n_reads, uint32_t p, uint32_t t, uint32_t w, uint32_t kcap, Pattern pat, int k,
                         uint8_t* phases, uint32_t* redo, uint32_t* n_redo, uint64_t* acount) {
@@ -38,7 +41,7 @@ __global__ void k_phase(const uint32_t* __restrict__ occ, const Job* __restrict_
     for (uint32_t s = 0; s < p; s++) {
       const uint64_t j = (uint64_t)i * p + s;
       const Job jb = jobs[j];
-      uint64_t c = job_off[j + 1] - job_off[j];
+      uint64_t c = job_end[j] - job_off[j];
       if (kcap) {
         const uint64_t ninc = included_count(pat, jb.len, s);
         const uint64_t nk_full = ninc >= (uint64_t)k ? ninc - k + 1 : 0;
@@ -46,7 +49,7 @@ __global__ void k_phase(const uint32_t* __restrict__ occ, const Job* __restrict_
           uint64_t safe = 0;
           if (jb.nk >= w) {
             const uint64_t lim = orig_of(pat, jb.nk - w, s);
-            for (uint64_t q = job_off[j]; q < job_off[j + 1] && pos[q] <= lim; q++) ++safe;
+            for (uint64_t q = job_off[j]; q < job_end[j] && pos[q] <= lim; q++) ++safe;
           }
           if (safe < t) fallback = true;
           c = safe;
@@ -71,7 +74,7 @@ __global__ void k_phase(const uint32_t* __restrict__ occ, const Job* __restrict_
     if (acount) {  // anchors of the read if PQ_a's records are this phase job's (the S4 fast path)
       const uint64_t j = (uint64_t)i * p + a;
       uint64_t na = 0;
-      for (uint64_t q = job_off[j]; q < job_off[j + 1]; q++) na += occ[q];
+      for (uint64_t q = job_off[j]; q < job_end[j]; q++) na += occ[q];
       acount[r] = na;
     }
   }
@@ -95,6 +98,13 @@ __global__ void k_make_jobs_ids(Params P, const uint64_t* __restrict__ offsets, 
   }
 }
 
+// developer check (GOD_DEBUG_JOBS): every job's record range lies inside the records
+__global__ void k_check_jobs(const uint64_t* job_off, const uint64_t* job_end, uint64_t nj, uint64_t n,
+                             unsigned long long* bad) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < nj; j += (uint64_t)gridDim.x * blockDim.x)
+    if (job_off[j] > job_end[j] || job_end[j] > n) atomicMin(bad, (unsigned long long)j);
+}
+
 // one probe per thread, one thread per record, large grid: the probe is a chain of two dependent
 // random accesses (directory slot, entries) and is bound by HBM random-access bandwidth; many
 // resident warps hide the latency better than a persistent loop with per-thread ILP (measured).
@@ -111,13 +121,14 @@ __global__ void k_anchor_count(IndexView v, const uint64_t* __restrict__ hz, uin
 // lane one record at a time, offsets by a group scan), so no read-ordered copy of the records is made.
 constexpr int RG = 8;
 __global__ void k_read_anchor_counts1(const uint32_t* __restrict__ cnt, const uint64_t* __restrict__ job_off,
+                                      const uint64_t* __restrict__ job_end,
                                       const uint8_t* __restrict__ phases, uint32_t p, uint32_t n_reads, uint64_t* out) {
   const uint32_t l = threadIdx.x & (RG - 1);
   for (uint64_t g = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / RG; g < n_reads;
        g += (uint64_t)gridDim.x * blockDim.x / RG) {
     const uint32_t r = (uint32_t)g;
     const uint64_t j = (uint64_t)r * p + phases[r];
-    const uint64_t b = job_off[j], e = job_off[j + 1];
+    const uint64_t b = job_off[j], e = job_end[j];
     uint64_t acc = 0;
     for (uint64_t q = b + l; q < e; q += RG) acc += cnt[q];
 #pragma unroll
@@ -128,7 +139,8 @@ __global__ void k_read_anchor_counts1(const uint32_t* __restrict__ cnt, const ui
 template <bool A16>  // A16: out is 16-B aligned -> one 128-bit store per anchor
 __global__ void k_anchor_write1(IndexView v, const uint64_t* __restrict__ hz, const uint32_t* __restrict__ pos,
                                 const uint32_t* __restrict__ cnt, const uint32_t* __restrict__ beg,
-                                const uint64_t* __restrict__ job_off, const uint8_t* __restrict__ phases, uint32_t p,
+                                const uint64_t* __restrict__ job_off, const uint64_t* __restrict__ job_end,
+                                const uint8_t* __restrict__ phases, uint32_t p,
                                 uint32_t n_reads, const uint64_t* __restrict__ aoff, god_anchor* out,
                                 uint32_t rid_base) {
   const uint32_t l = threadIdx.x & (RG - 1);
@@ -136,7 +148,7 @@ __global__ void k_anchor_write1(IndexView v, const uint64_t* __restrict__ hz, co
        g += (uint64_t)gridDim.x * blockDim.x / RG) {
     const uint32_t r = (uint32_t)g;
     const uint64_t j = (uint64_t)r * p + phases[r];
-    const uint64_t b = job_off[j], e = job_off[j + 1];
+    const uint64_t b = job_off[j], e = job_end[j];
     uint64_t o = aoff[r];
     for (uint64_t q0 = b; q0 < e; q0 += RG) {  // uniform trip count within the group
       const uint64_t q = q0 + l;
@@ -256,7 +268,7 @@ __global__ void k_seed_counts(SeedSources S, uint32_t n_reads, const uint8_t* __
   for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n_reads; r += gridDim.x * blockDim.x) {
     const int s = src[r] - 1;
     const uint32_t j = srcj[r];
-    cntr[r] = s >= 0 ? S.off[s][j + 1] - S.off[s][j] : 0;
+    cntr[r] = s >= 0 ? S.end[s][j] - S.off[s][j] : 0;
   }
 }
 
@@ -327,12 +339,29 @@ uint64_t seed_reads(const god_index* ix, const uint8_t* reads, const uint64_t* o
       const uint32_t kcap = (t + 1) * (uint32_t)P.w + (uint32_t)P.w;
       js1 = make_jobs(P, offsets, n_reads, nullptr, p, kcap, false, st, scr);
       run_extract(P, reads, js1.seq_bytes, js1.jobs, js1.kb, js1.n, js1.total_pos, false, true, rec1, st, scr,
-                  js1.total_pos / (uint64_t)(P.w + 1) * 2 + js1.total_pos / 8 + 4096, "extract_phase", js1.x2p());
+                  js1.total_pos / (uint64_t)(P.w + 1) * 2 + js1.total_pos / 8 + 4096, "extract_phase", js1.x2p(), ORDER_JOB);
+      if (getenv("GOD_DEBUG_JOBS")) {
+        unsigned long long* bad = scr.alloc<unsigned long long>(1);
+        GOD_CUDA(cudaMemsetAsync(bad, 0xFF, 8, st));
+        GOD_LAUNCH("k_check_jobs", k_check_jobs, grid_for(js1.n, 256), 256, 0, st, rec1.job_off, rec1.job_end, js1.n,
+                   rec1.n, bad);
+        unsigned long long hb = 0;
+        uint64_t h2[2] = {0, 0};
+        GOD_CUDA(cudaMemcpy(&hb, bad, 8, cudaMemcpyDeviceToHost));
+        if (hb != ~0ull) {
+          GOD_CUDA(cudaMemcpy(&h2[0], rec1.job_off + hb, 8, cudaMemcpyDeviceToHost));
+          GOD_CUDA(cudaMemcpy(&h2[1], rec1.job_end + hb, 8, cudaMemcpyDeviceToHost));
+        }
+        fprintf(stderr, "[jobs] n_jobs=%u n=%llu max_jb=%llu first_bad=%lld off=%llu end=%llu\n", js1.n,
+                (unsigned long long)rec1.n, (unsigned long long)js1.x2.max_job_blocks,
+                hb == ~0ull ? -1ll : (long long)hb, (unsigned long long)h2[0], (unsigned long long)h2[1]);
+      }
       uint32_t* redo = scr.alloc<uint32_t>(n_reads);
       uint32_t* n_redo = scr.alloc<uint32_t>(1);
       GOD_CUDA(cudaMemsetAsync(n_redo, 0, sizeof(uint32_t), st));
       probe_all(v, rec1, st, scr);
-      GOD_LAUNCH("k_phase", k_phase, grid_for(n_reads, 128), 128, 0, st, rec1.cnt, js1.jobs, rec1.job_off, rec1.hz,
+      GOD_LAUNCH("k_phase", k_phase, grid_for(n_reads, 128), 128, 0, st, rec1.cnt, js1.jobs, rec1.job_off, rec1.job_end,
+                 rec1.hz,
                  rec1.pos, nullptr, n_reads, p, t, P.w, kcap, P.pat, P.k, phases, redo, n_redo, anchor_offsets);
       counted = true;
       nr = d2h_scalar(n_redo, st);
@@ -346,11 +375,12 @@ uint64_t seed_reads(const god_index* ix, const uint8_t* reads, const uint64_t* o
         GOD_CUDA(cudaMemcpyAsync(kb2 + (uint64_t)nr * p, tot2, sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
         const uint64_t tp2 = d2h_scalar(tot2, st);
         run_extract(P, reads, js1.seq_bytes, jobs2, kb2, nr * p, tp2, false, true, rec2, st, scr, tp2 / 4 + 4096,
-                    "extract_phase_redo");
+                    "extract_phase_redo", nullptr, ORDER_JOB);
         uint32_t* n_redo2 = scr.alloc<uint32_t>(1);
         GOD_CUDA(cudaMemsetAsync(n_redo2, 0, sizeof(uint32_t), st));
         probe_all(v, rec2, st, scr);
-        GOD_LAUNCH("k_phase", k_phase, grid_for(nr, 128), 128, 0, st, rec2.cnt, jobs2, rec2.job_off, rec2.hz, rec2.pos,
+        GOD_LAUNCH("k_phase", k_phase, grid_for(nr, 128), 128, 0, st, rec2.cnt, jobs2, rec2.job_off, rec2.job_end,
+                   rec2.hz, rec2.pos,
                    redo, nr, p, t, P.w, 0, P.pat, P.k, phases, redo, n_redo2, nullptr);
         GOD_LAUNCH("k_redo_src", k_redo_src, grid_for(nr, 256), 256, 0, st, nr, p, redo, phases, src, srcj);
       }
@@ -368,7 +398,7 @@ uint64_t seed_reads(const god_index* ix, const uint8_t* reads, const uint64_t* o
     if (h3 == n_reads) {  // every read: phase-a jobs in read order
       JobSet js3 = make_jobs(P, offsets, n_reads, phases, 0, 0, false, st, scr);
       run_extract(P, reads, js3.seq_bytes, js3.jobs, js3.kb, js3.n, js3.total_pos, false, true, rec3, st, scr,
-                  js3.total_pos / (uint64_t)(P.w + 1) * 2 + js3.total_pos / 8 + 4096, "extract_seed", js3.x2p());
+                  js3.total_pos / (uint64_t)(P.w + 1) * 2 + js3.total_pos / 8 + 4096, "extract_seed", js3.x2p(), ORDER_JOB);
       GOD_LAUNCH("k_iota_src3", k_iota_src3, grid_for(n_reads, 256), 256, 0, st, n_reads, src, srcj);
     } else {
       Job* jobs3 = scr.alloc<Job>(h3);
@@ -382,7 +412,7 @@ uint64_t seed_reads(const god_index* ix, const uint8_t* reads, const uint64_t* o
       uint64_t bytes = 0;
       d2h_small(&bytes, offsets + n_reads, sizeof(uint64_t), st);
       GOD_CUDA(cudaStreamSynchronize(st));
-      run_extract(P, reads, bytes, jobs3, kb3, h3, tp3, false, true, rec3, st, scr, tp3 / 4 + 4096, "extract_seed");
+      run_extract(P, reads, bytes, jobs3, kb3, h3, tp3, false, true, rec3, st, scr, tp3 / 4 + 4096, "extract_seed", nullptr, ORDER_JOB);
     }
   }
   if (h3) probe_all(v, rec3, st, scr);
@@ -391,7 +421,7 @@ uint64_t seed_reads(const god_index* ix, const uint8_t* reads, const uint64_t* o
     uint64_t* total = scr.alloc<uint64_t>(1);
     if (!counted)
       GOD_LAUNCH("k_read_anchor_counts", k_read_anchor_counts1, grid_for((uint64_t)n_reads * RG, 256), 256, 0, st,
-                 rec1.cnt, rec1.job_off, phases, p, n_reads, anchor_offsets);
+                 rec1.cnt, rec1.job_off, rec1.job_end, phases, p, n_reads, anchor_offsets);
     scan_exclusive_u64(anchor_offsets, anchor_offsets, n_reads, total, st, scr, "scan_read_anchors");
     GOD_CUDA(cudaMemcpyAsync(anchor_offsets + n_reads, total, sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
     const uint64_t tot = d2h_scalar(total, st);
@@ -399,11 +429,11 @@ uint64_t seed_reads(const god_index* ix, const uint8_t* reads, const uint64_t* o
     {
       if ((reinterpret_cast<uintptr_t>(anchors) & 15u) == 0)
         GOD_LAUNCH("k_anchor_write", k_anchor_write1<true>, grid_for((uint64_t)n_reads * RG, 256), 256, 0, st, v,
-                   rec1.hz, rec1.pos, rec1.cnt, rec1.beg, rec1.job_off, phases, p, n_reads, anchor_offsets, anchors,
+                   rec1.hz, rec1.pos, rec1.cnt, rec1.beg, rec1.job_off, rec1.job_end, phases, p, n_reads, anchor_offsets, anchors,
                    rid_base);
       else
         GOD_LAUNCH("k_anchor_write", k_anchor_write1<false>, grid_for((uint64_t)n_reads * RG, 256), 256, 0, st, v,
-                   rec1.hz, rec1.pos, rec1.cnt, rec1.beg, rec1.job_off, phases, p, n_reads, anchor_offsets, anchors,
+                   rec1.hz, rec1.pos, rec1.cnt, rec1.beg, rec1.job_off, rec1.job_end, phases, p, n_reads, anchor_offsets, anchors,
                    rid_base);
     }
     return tot;
@@ -412,6 +442,7 @@ uint64_t seed_reads(const god_index* ix, const uint8_t* reads, const uint64_t* o
   S.hz[0] = rec1.hz; S.pos[0] = rec1.pos; S.off[0] = rec1.job_off; S.cnt[0] = rec1.cnt; S.beg[0] = rec1.beg;
   S.hz[1] = rec2.hz; S.pos[1] = rec2.pos; S.off[1] = rec2.job_off; S.cnt[1] = rec2.cnt; S.beg[1] = rec2.beg;
   S.hz[2] = rec3.hz; S.pos[2] = rec3.pos; S.off[2] = rec3.job_off; S.cnt[2] = rec3.cnt; S.beg[2] = rec3.beg;
+  S.end[0] = rec1.job_end; S.end[1] = rec2.job_end; S.end[2] = rec3.job_end;
   // per-read record counts -> offsets -> one contiguous record array in read order
   uint64_t* roff = scr.alloc<uint64_t>((uint64_t)n_reads + 1);
   uint64_t* rtot = scr.alloc<uint64_t>(1);
