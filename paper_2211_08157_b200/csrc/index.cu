@@ -206,6 +206,8 @@ constexpr int BS_NW = BS_NT / 32;
 constexpr int BS_CAP = 4096;                      // records of a bin held in SMEM (x2 buffers)
 constexpr int BS_IPT = BS_CAP / BS_NT;            // 8
 constexpr int BS_SMEM = 2 * BS_CAP * 8 + 4096 * 4;  // + run-count histogram (SMALL_BINS)
+constexpr uint32_t S_MAX = 2048;                  // directory slots per bin (k_bin_build: first[S + 1] in SMEM)
+constexpr int BB_SMEM = BS_SMEM + (S_MAX + 1) * 4;
 constexpr int SEG_BITS = 12;
 constexpr uint32_t SMALL_BINS = 4096;
 
@@ -315,6 +317,12 @@ __global__ void __launch_bounds__(1024) k_seg_table(const uint32_t* __restrict__
     before += nb[q];
   }
   if (tid == 1023) *n_bins = before;
+}
+
+// directory slot map aligned with the bins: S slots per bin (k_bin_build writes its bin's slots)
+__global__ void k_seg_slots(const uint2* __restrict__ table, uint32_t S, uint2* seg) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < (1u << SEG_BITS)) seg[t] = make_uint2(table[t].x * S, table[t].y * S);
 }
 
 // b(h) into the free key bits above the hash, one RS_TILE tile per CTA; also the tile histogram
@@ -686,12 +694,338 @@ __global__ void __launch_bounds__(BS_NT, 2) k_bin_sort(uint64_t* __restrict__ k,
   run_flush(ro, rh, racc);
 }
 
+// in-place suffix minimum of f[0 .. m) by the whole CTA (BS_NT threads; ws: BS_NW words)
+__device__ __forceinline__ void suffix_min_block(uint32_t* f, uint32_t m, uint32_t* ws) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint32_t C = (m + BS_NT - 1) / BS_NT;
+  const uint32_t b0 = threadIdx.x * C, b1 = min(b0 + C, m);
+  uint32_t mn = 0xFFFFFFFFu;
+  for (uint32_t q = b1; q > b0; q--) { mn = min(mn, f[q - 1]); f[q - 1] = mn; }
+  uint32_t x = mn;  // inclusive suffix min over the lanes >= lane
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t y = __shfl_down_sync(0xffffffffu, x, d);
+    if (lane + d < 32) x = min(x, y);
+  }
+  if (lane == 0) ws[wid] = x;
+  const uint32_t nxt = __shfl_down_sync(0xffffffffu, x, 1);
+  __syncthreads();
+  uint32_t after = lane < 31 ? nxt : 0xFFFFFFFFu;
+#pragma unroll
+  for (int q = 0; q < BS_NW; q++)
+    if (q > wid) after = min(after, ws[q]);
+  for (uint32_t q = b0; q < b1; q++) f[q] = min(f[q], after);
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(BS_NT, 2) k_bin_build(const uint64_t* __restrict__ k, const uint32_t* __restrict__ v,
+                                                        const uint64_t* __restrict__ bstart,
+                                                        const uint32_t* __restrict__ n_bins, int L, int hbits,
+                                                        uint32_t* big, uint32_t* n_big, RunOut ro,
+                                                        const uint2* __restrict__ table,
+                                                        const uint32_t* __restrict__ binseg, uint32_t S,
+                                                        uint64_t* __restrict__ ent, DirRec* __restrict__ dir) {
+  extern __shared__ __align__(16) unsigned char bs_smem[];
+  uint64_t* A = reinterpret_cast<uint64_t*>(bs_smem);
+  uint64_t* Bf = A + BS_CAP;
+  uint32_t* rh = reinterpret_cast<uint32_t*>(Bf + BS_CAP);  // [SMALL_BINS] run-count histogram
+  uint32_t* first = rh + SMALL_BINS;                          // [S + 1] first record of each slot of the bin
+  for (int i = threadIdx.x; i < (int)SMALL_BINS; i += BS_NT) rh[i] = 0;
+  __syncthreads();
+  RunAcc racc;
+  __shared__ __align__(16) uint32_t cnt[CNT_WORDS];
+  __shared__ uint32_t wsum[BS_NW];
+  __shared__ uint32_t s_or[BS_NW], s_and[BS_NW];
+  __shared__ uint64_t s_vo[BS_NW], s_va[BS_NW];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint64_t lmask = (1ull << L) - 1, hmask = (1ull << hbits) - 1;
+  const uint32_t nb = *n_bins;
+  for (uint32_t c = blockIdx.x; c < nb; c += gridDim.x) {
+    const uint64_t s = bstart[c], e = bstart[c + 1];
+    const int n = (int)(e - s);
+    if (threadIdx.x == 0 && c + gridDim.x < nb) {  // the CTA's next bin into L2 while this one is sorted
+      const uint64_t s2 = bstart[c + gridDim.x], e2 = bstart[c + gridDim.x + 1];
+      if (e2 - s2 > 1 && e2 - s2 <= (uint64_t)BS_CAP) {
+        l2_prefetch_range(k + s2, (e2 - s2) * sizeof(uint64_t));
+        l2_prefetch_range(v + s2, (e2 - s2) * sizeof(uint32_t));
+      }
+    }
+    if (n == 0) {  // an empty bin: its S slots are empty
+      for (uint32_t q = threadIdx.x; q < S; q += BS_NT) {
+        uint4* o = reinterpret_cast<uint4*>(dir + (uint64_t)c * S + q);
+        o[0] = make_uint4((uint32_t)s, (uint32_t)s, 0xFFFFFFFFu, 0xFFFFFFFFu);
+        o[1] = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+      }
+      continue;
+    }
+    if (n > BS_CAP) {
+      if (threadIdx.x == 0) big[atomicAdd(n_big, 1u)] = c;
+      continue;
+    }
+    uint64_t x[BS_IPT];
+    uint32_t lmin = 0xFFFFFFFFu, lmax = 0;
+    uint64_t seg = 0;
+#pragma unroll
+    for (int j = 0; j < BS_IPT; j++) {  // all loads of the bin in flight at once
+      const int i = wid * (32 * BS_IPT) + j * 32 + lane;
+      uint64_t kk = 0;
+      uint32_t pp = 0;
+      if (i < n) {
+        kk = __ldcs(k + s + i);
+        pp = __ldcs(v + s + i);
+        const uint32_t lo = (uint32_t)(kk & lmask);
+        lmin = min(lmin, lo);
+        lmax = max(lmax, lo);
+        seg = (kk & hmask) >> L;
+      }
+      x[j] = ((kk & lmask) << 33) | ((uint64_t)pp << 1) | (kk >> 63);
+    }
+#pragma unroll
+    for (int d = 16; d; d >>= 1) {
+      lmin = min(lmin, __shfl_xor_sync(0xffffffffu, lmin, d));
+      lmax = max(lmax, __shfl_xor_sync(0xffffffffu, lmax, d));
+    }
+    if (lane == 0) { s_or[wid] = lmin; s_and[wid] = lmax; }
+    if (wid == 0 && lane == 0) wsum[0] = (uint32_t)seg;  // every record of a bin has the same segment
+    __syncthreads();
+    uint32_t mn = 0xFFFFFFFFu, mx = 0;
+#pragma unroll
+    for (int q = 0; q < BS_NW; q++) { mn = min(mn, s_or[q]); mx = max(mx, s_and[q]); }
+    const uint64_t segv = wsum[0];
+    __syncthreads();
+    // K1 emits records in tile order (any order within a bin): one-hash bins and buckets of very
+    // frequent hashes are put in (hash, pos) order by an LSD over the packed bits that vary
+    auto lsd_varying = [&](int top_bit) -> const uint64_t* {
+      uint64_t o = 0, a = ~0ull;
+#pragma unroll
+      for (int j = 0; j < BS_IPT; j++) {
+        const int i = wid * (32 * BS_IPT) + j * 32 + lane;
+        if (i < n) { o |= x[j]; a &= x[j]; }
+      }
+#pragma unroll
+      for (int d = 16; d; d >>= 1) {
+        o |= __shfl_xor_sync(0xffffffffu, o, d);
+        a &= __shfl_xor_sync(0xffffffffu, a, d);
+      }
+      if (lane == 0) { s_vo[wid] = o; s_va[wid] = a; }
+      __syncthreads();
+      uint64_t vo = 0, va = ~0ull;
+#pragma unroll
+      for (int q = 0; q < BS_NW; q++) { vo |= s_vo[q]; va &= s_va[q]; }
+      const uint64_t vary = vo & ~va;
+      __syncthreads();
+      uint64_t* dst = A;
+      bool first = true;
+      for (int sh = 1; sh < top_bit; sh += RS_BITS) {
+        const int bits = min(RS_BITS, top_bit - sh);
+        const uint32_t dm = (1u << bits) - 1;
+        if (((vary >> sh) & dm) == 0) continue;  // a constant digit: the pass is the identity
+        if (!first) cta_load_striped(dst == A ? Bf : A, n, x);
+        cta_rank_scatter(x, n, sh, dm, dst, cnt, wsum);
+        dst = dst == A ? Bf : A;
+        first = false;
+      }
+      if (first) {  // nothing varies (cannot happen: positions differ within a bin): the loaded order
+#pragma unroll
+        for (int j = 0; j < BS_IPT; j++) {
+          const int i = wid * (32 * BS_IPT) + j * 32 + lane;
+          if (i < n) A[i] = x[j];
+        }
+        __syncthreads();
+        return A;
+      }
+      return dst == A ? Bf : A;
+    };
+    const bool one = mn == mx;  // one hash: sort by position
+    const uint64_t* res = one ? lsd_varying(33) : nullptr;
+    if (!one) {
+    // (1) MSD placement by the top 12 bits of low(h) - mn (4096 buckets, ~1 record each), then an
+    //     insertion sort of each bucket on the full packed value (unique: it contains pos)
+    const int rbits = 32 - __clz(mx - mn);
+    const int shb = rbits > 12 ? rbits - 12 : 0;
+    {
+      uint4* c4 = reinterpret_cast<uint4*>(cnt);
+      c4[2 * threadIdx.x] = make_uint4(0, 0, 0, 0);
+      c4[2 * threadIdx.x + 1] = make_uint4(0, 0, 0, 0);
+    }
+    __syncthreads();
+    uint32_t bk[BS_IPT];
+#pragma unroll
+    for (int j = 0; j < BS_IPT; j++) {
+      const int i = wid * (32 * BS_IPT) + j * 32 + lane;
+      bk[j] = ((uint32_t)(x[j] >> 33) - mn) >> shb;
+      if (i < n) atomicAdd(&cnt[bk[j]], 1u);
+    }
+    __syncthreads();
+    uint32_t cmax;
+    {
+      uint4* c4 = reinterpret_cast<uint4*>(cnt);
+      const uint4 p0 = c4[2 * threadIdx.x], p1 = c4[2 * threadIdx.x + 1];
+      uint32_t y[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+      uint32_t tsum = 0, tmax = 0;
+#pragma unroll
+      for (int q = 0; q < 8; q++) { const uint32_t c2 = y[q]; y[q] = tsum; tsum += c2; tmax = max(tmax, c2); }
+      uint32_t incl = tsum;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t t2 = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += t2;
+      }
+#pragma unroll
+      for (int d = 16; d; d >>= 1) tmax = max(tmax, __shfl_xor_sync(0xffffffffu, tmax, d));
+      if (lane == 31) wsum[wid] = incl;
+      if (lane == 0) s_or[wid] = tmax;
+      __syncthreads();
+      uint32_t before = incl - tsum;
+      cmax = 0;
+#pragma unroll
+      for (int q = 0; q < BS_NW; q++) { before += q < wid ? wsum[q] : 0u; cmax = max(cmax, s_or[q]); }
+      c4[2 * threadIdx.x] = make_uint4(y[0] + before, y[1] + before, y[2] + before, y[3] + before);
+      c4[2 * threadIdx.x + 1] = make_uint4(y[4] + before, y[5] + before, y[6] + before, y[7] + before);
+    }
+    __syncthreads();
+    if (cmax <= (uint32_t)BIN_RANK_MAX) {
+#pragma unroll
+      for (int j = 0; j < BS_IPT; j++) {
+        const int i = wid * (32 * BS_IPT) + j * 32 + lane;
+        if (i < n) A[atomicAdd(&cnt[bk[j]], 1u)] = x[j];
+      }
+      __syncthreads();
+      // cnt[b] is now the end of bucket b.  Every element takes its rank in its bucket by counting
+      // the smaller values (unique: they contain pos) and moves to Bf — measured faster than
+      // per-bucket bitonic or insertion sorts at every bucket size up to the 1024 cap
+      for (int p = threadIdx.x; p < n; p += BS_NT) {
+        const uint64_t xv = A[p];
+        const uint32_t b2 = ((uint32_t)(xv >> 33) - mn) >> shb;
+        const int st = b2 ? (int)cnt[b2 - 1] : 0, en = (int)cnt[b2];
+        int rank = 0;
+        for (int q = st; q < en; q++) rank += A[q] < xv;
+        Bf[st + rank] = xv;
+      }
+      __syncthreads();
+      res = Bf;
+    } else {
+      // (2) a bucket with > 1024 records (a very frequent hash): stable LSD over the low(h) digits below
+      //     the highest bit where mn and mx differ (bits above it are constant in the bin)
+      if (threadIdx.x == 0) atomicAdd(n_big + 1, 1u);  // statistics: bins sorted this way
+      const int hib = 32 - __clz(mn ^ mx);
+      res = lsd_varying(33 + hib);
+    }
+    }  // !one
+    // K3 fused: runs never cross a bin (a hash lies in one bin).  Per-element run length from two
+    // block scans over the run-head indices (start = last head <= i, end = first head > i); it is
+    // stored in the key's free bits (capped) for the kept-entry pass, and heads record it in the
+    // count histogram.
+    uint32_t* Lsm = reinterpret_cast<uint32_t*>(res == A ? Bf : A);
+    if (!one) {
+      // warp w owns items [w*256, w*256+256) as 8 rows of 32 (conflict-free SMEM access)
+      const int wbase = wid * (32 * BS_IPT);
+      uint32_t hm[BS_IPT];
+      int wl = -1, wf = n;  // this warp's last / first head
+#pragma unroll
+      for (int q = 0; q < BS_IPT; q++) {
+        const int idx = wbase + q * 32 + lane;
+        bool h = false;
+        if (idx < n) h = idx == 0 || (uint32_t)(res[idx - 1] >> 33) != (uint32_t)(res[idx] >> 33);
+        hm[q] = __ballot_sync(0xffffffffu, h);
+        if (hm[q]) {
+          wl = wbase + q * 32 + 31 - __clz(hm[q]);
+          if (wf == n) wf = wbase + q * 32 + __ffs(hm[q]) - 1;
+        }
+      }
+      if (lane == 0) { s_or[wid] = (uint32_t)(wl + 1); s_and[wid] = (uint32_t)wf; }
+      __syncthreads();
+      int carry = -1, after = n;
+#pragma unroll
+      for (int q = 0; q < BS_NW; q++) {
+        if (q < wid) carry = max(carry, (int)s_or[q] - 1);
+        if (q > wid) after = min(after, (int)s_and[q]);
+      }
+      const uint32_t le = (lane == 31) ? 0xffffffffu : ((2u << lane) - 1);  // lanes <= lane
+      int st_[BS_IPT];
+#pragma unroll
+      for (int q = 0; q < BS_IPT; q++) {  // start = last head <= idx
+        const uint32_t m = hm[q] & le;
+        st_[q] = m ? wbase + q * 32 + 31 - __clz(m) : carry;
+        if (hm[q]) carry = wbase + q * 32 + 31 - __clz(hm[q]);
+      }
+#pragma unroll
+      for (int q = BS_IPT - 1; q >= 0; q--) {  // next head > idx
+        const uint32_t m = hm[q] & ~le;
+        const int nh = m ? wbase + q * 32 + __ffs(m) - 1 : after;
+        const int idx = wbase + q * 32 + lane;
+        if (idx < n) Lsm[idx] = (uint32_t)(nh - st_[q]);
+        if (hm[q]) after = wbase + q * 32 + __ffs(hm[q]) - 1;
+      }
+    }
+    __syncthreads();
+    // K5 + K6 fused: entries in final position (all of them: a hash with count > tau is dropped at
+    // probe time, reading O7), then the bin's S directory slots (bins are unions of whole slots)
+    const uint2 tb = table[segv];                  // (first bin, bins) of the bin's segment
+    const uint64_t slots_t = (uint64_t)tb.y * S;   // slots of the segment
+    const uint64_t qbase = (uint64_t)(c - tb.x) * S;
+    for (uint32_t q = threadIdx.x; q <= S; q += BS_NT) first[q] = (uint32_t)n;
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += BS_NT) {
+      const uint64_t pv = res[i];
+      __stcs(ent + s + i, ((pv >> 1) << 32) | ((pv >> 33) << 1) | (pv & 1ull));
+      const uint32_t lo = (uint32_t)(pv >> 33);
+      const bool head = i == 0 || (uint32_t)(res[i - 1] >> 33) != lo;
+      if (one) {
+        if (i == 0) run_emit(ro, rh, (uint64_t)n, racc);
+      } else if (head) {
+        run_emit(ro, rh, Lsm[i], racc);
+      }
+      if (head) {  // a slot starts at a run head: its first record
+        const uint32_t q = (uint32_t)((((uint64_t)lo * slots_t) >> L) - qbase);
+        const uint32_t qp = i ? (uint32_t)((((res[i - 1] >> 33) * slots_t) >> L) - qbase) : 0xFFFFFFFFu;
+        if (q != qp) first[q] = (uint32_t)i;
+      }
+    }
+    __syncthreads();
+    suffix_min_block(first, S + 1, wsum);
+    for (uint32_t q = threadIdx.x; q < S; q += BS_NT) {
+      const uint32_t a0 = first[q], b0 = first[q + 1];
+      uint32_t kk[DIR_KEYS];
+      if (b0 - a0 <= DIR_KEYS) {
+#pragma unroll
+        for (int e2 = 0; e2 < DIR_KEYS; e2++) kk[e2] = a0 + e2 < b0 ? (uint32_t)(res[a0 + e2] >> 33) : 0xFFFFFFFFu;
+      } else {  // <= DIR_RUNS distinct keys: (key, run end) pairs; more: key[0] = ~0 (the probe searches)
+#pragma unroll
+        for (int e2 = 0; e2 < DIR_KEYS; e2++) kk[e2] = (e2 & 1) ? (uint32_t)(s + b0) : 0xFFFFFFFFu;
+        uint32_t s0 = a0;
+        for (int r = 0; r < DIR_RUNS && s0 < b0; r++) {
+          const uint32_t ks = (uint32_t)(res[s0] >> 33);
+          uint32_t lo2 = s0 + 1, st = 1;  // gallop, then bisect, to the first record with another key
+          while (lo2 + st <= b0 && (uint32_t)(res[lo2 + st - 1] >> 33) == ks) { lo2 += st; st <<= 1; }
+          uint32_t hi2 = min(lo2 + st - 1, b0);
+          while (lo2 < hi2) {
+            const uint32_t mid = (lo2 + hi2) >> 1;
+            if ((uint32_t)(res[mid] >> 33) == ks) lo2 = mid + 1;
+            else hi2 = mid;
+          }
+          kk[2 * r] = ks;
+          kk[2 * r + 1] = (uint32_t)(s + lo2);
+          s0 = lo2;
+        }
+        if (s0 < b0) kk[0] = 0xFFFFFFFFu;
+      }
+      uint4* o = reinterpret_cast<uint4*>(dir + (uint64_t)c * S + q);
+      o[0] = make_uint4((uint32_t)(s + a0), (uint32_t)(s + b0), kk[0], kk[1]);
+      o[1] = make_uint4(kk[2], kk[3], kk[4], kk[5]);
+    }
+    __syncthreads();
+  }
+  run_flush(ro, rh, racc);
+}
+
 // oversized bins (repeat-heavy hashes): the same LSD over the low bits, chunk by chunk through
 // global memory (stable across chunks: chunks are taken in order, each digit's run appended)
 __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort_big(uint64_t* __restrict__ k, uint32_t* __restrict__ v,
                                                               uint64_t* __restrict__ t0, uint64_t* __restrict__ t1,
                                                               const uint64_t* __restrict__ bstart, const uint32_t* big,
-                                                              const uint32_t* n_big, int lo_bits, int hbits, RunOut ro) {
+                                                              const uint32_t* n_big, int lo_bits, int hbits, RunOut ro,
+                                                              uint64_t* __restrict__ ent) {
   extern __shared__ __align__(16) unsigned char bs_smem[];
   uint64_t* Bf = reinterpret_cast<uint64_t*>(bs_smem);
   uint32_t* rh = reinterpret_cast<uint32_t*>(Bf + 2 * BS_CAP);  // [SMALL_BINS] run-count histogram
@@ -770,6 +1104,7 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort_big(uint64_t* __restri
       const uint64_t pv = src[i];
       k[s + i] = (top | (pv >> 33)) | ((pv & 1ull) << 63);
       v[s + i] = (uint32_t)(pv >> 1);
+      if (ent) ent[s + i] = ((pv >> 1) << 32) | ((pv >> 33) << 1) | (pv & 1ull);
     }
     __syncthreads();
     // K3 fused: every record finds its run's extent in the bin (galloping both ways), stores the
@@ -788,6 +1123,63 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort_big(uint64_t* __restri
     __syncthreads();
   }
   run_flush(ro, rh, racc);
+}
+
+// K6 for the oversized bins (sorted by k_bucket_sort_big into k and ent): each slot's first record by
+// binary search (slot numbers are non-decreasing in the sorted records), then the slot records
+__global__ void __launch_bounds__(BS_NT) k_big_dir(const uint64_t* __restrict__ k, const uint64_t* __restrict__ bstart,
+                                                   const uint32_t* big, const uint32_t* n_big, int L, int hbits,
+                                                   const uint2* __restrict__ table, uint32_t S,
+                                                   DirRec* __restrict__ dir) {
+  const uint64_t lmask = (1ull << L) - 1, hmask = (1ull << hbits) - 1;
+  const uint32_t nbig = *n_big;
+  for (uint32_t qb = blockIdx.x; qb < nbig; qb += gridDim.x) {
+    const uint32_t c = big[qb];
+    const uint64_t s = bstart[c], n = bstart[c + 1] - s;
+    const uint2 tb = table[(k[s] & hmask) >> L];
+    const uint64_t slots_t = (uint64_t)tb.y * S, qbase = (uint64_t)(c - tb.x) * S;
+    auto key = [&](uint64_t i) -> uint32_t { return (uint32_t)(k[s + i] & lmask); };
+    auto slot = [&](uint64_t i) -> uint64_t { return (((uint64_t)key(i) * slots_t) >> L) - qbase; };
+    auto first_at = [&](uint64_t q) -> uint64_t {  // first record with slot >= q
+      uint64_t lo = 0, hi = n;
+      while (lo < hi) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (slot(mid) < q) lo = mid + 1;
+        else hi = mid;
+      }
+      return lo;
+    };
+    for (uint32_t q = threadIdx.x; q < S; q += BS_NT) {
+      const uint64_t a0 = first_at(q), b0 = first_at(q + 1);
+      uint32_t kk[DIR_KEYS];
+      if (b0 - a0 <= DIR_KEYS) {
+#pragma unroll
+        for (int e2 = 0; e2 < DIR_KEYS; e2++) kk[e2] = a0 + e2 < b0 ? key(a0 + e2) : 0xFFFFFFFFu;
+      } else {
+#pragma unroll
+        for (int e2 = 0; e2 < DIR_KEYS; e2++) kk[e2] = (e2 & 1) ? (uint32_t)(s + b0) : 0xFFFFFFFFu;
+        uint64_t s0 = a0;
+        for (int r = 0; r < DIR_RUNS && s0 < b0; r++) {
+          const uint32_t ks = key(s0);
+          uint64_t lo2 = s0 + 1, st = 1;
+          while (lo2 + st <= b0 && key(lo2 + st - 1) == ks) { lo2 += st; st <<= 1; }
+          uint64_t hi2 = min(lo2 + st - 1, b0);
+          while (lo2 < hi2) {
+            const uint64_t mid = (lo2 + hi2) >> 1;
+            if (key(mid) == ks) lo2 = mid + 1;
+            else hi2 = mid;
+          }
+          kk[2 * r] = ks;
+          kk[2 * r + 1] = (uint32_t)(s + lo2);
+          s0 = lo2;
+        }
+        if (s0 < b0) kk[0] = 0xFFFFFFFFu;
+      }
+      uint4* o = reinterpret_cast<uint4*>(dir + (uint64_t)c * S + q);
+      o[0] = make_uint4((uint32_t)(s + a0), (uint32_t)(s + b0), kk[0], kk[1]);
+      o[1] = make_uint4(kk[2], kk[3], kk[4], kk[5]);
+    }
+  }
 }
 
 // K3: runs of equal hashes in the sorted records (one run = one distinct hash, P:286 (3)).  The
@@ -1115,29 +1507,52 @@ __global__ void k_count_queries(god::IndexView v, const uint64_t* __restrict__ h
 }
 
 
+// the full hash of entry e: its slot (largest s with dir[s].start <= e) gives the top bits
+__device__ __forceinline__ uint64_t entry_hash(const god::IndexView& v, uint64_t e) {
+  uint64_t lo = 0, hi = v.n_slots - 1;
+  while (lo < hi) {
+    uint64_t mid = (lo + hi + 1) >> 1;
+    if (v.dir[mid].start <= e) lo = mid;
+    else hi = mid - 1;
+  }
+  uint64_t top = lo;
+  if (v.seg) {  // mode 1: the segment whose slot range holds slot lo = the largest t with seg[t].x <= lo
+    uint32_t a = 0, b = (1u << DIR_SEG_BITS) - 1;
+    while (a < b) {
+      const uint32_t mid = (a + b + 1) >> 1;
+      if (v.seg[mid].x <= lo) a = mid;
+      else b = mid - 1;
+    }
+    top = a;
+  }
+  return (top << v.low_bits) | ((uint32_t)v.ent[e] >> 1);
+}
+
 __global__ void k_dump(god::IndexView v, uint64_t* hash, uint32_t* pos, uint8_t* strand) {
   for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < v.n_kept; e += (uint64_t)gridDim.x * blockDim.x) {
-    // slot = largest s with dir[s] <= e
-    uint64_t lo = 0, hi = v.n_slots - 1;
-    while (lo < hi) {
-      uint64_t mid = (lo + hi + 1) >> 1;
-      if (v.dir[mid].start <= e) lo = mid;
-      else hi = mid - 1;
-    }
-    uint64_t top = lo;
-    if (v.seg) {  // mode 1: the segment whose slot range holds slot lo = the largest t with seg[t].x <= lo
-      uint32_t a = 0, b = (1u << DIR_SEG_BITS) - 1;
-      while (a < b) {
-        const uint32_t mid = (a + b + 1) >> 1;
-        if (v.seg[mid].x <= lo) a = mid;
-        else b = mid - 1;
-      }
-      top = a;
-    }
     const uint64_t en = v.ent[e];
-    if (hash) hash[e] = (top << v.low_bits) | ((uint32_t)en >> 1);
+    if (hash) hash[e] = entry_hash(v, e);
     if (pos) pos[e] = (uint32_t)(en >> 32);
     if (strand) strand[e] = (uint8_t)(en & 1u);
+  }
+}
+
+// bin-built index (all entries held, cutoff at probe time): keep flag per entry, then the kept ones
+__global__ void k_dump_flag(god::IndexView v, uint32_t* keep) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < v.n_ent; e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint2 r = probe_range_all(v, entry_hash(v, e));
+    keep[e] = (r.y - r.x) <= v.tau ? 1u : 0u;
+  }
+}
+__global__ void k_dump_sel(god::IndexView v, const uint32_t* keep, const uint64_t* at, uint64_t* hash, uint32_t* pos,
+                           uint8_t* strand) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < v.n_ent; e += (uint64_t)gridDim.x * blockDim.x) {
+    if (!keep[e]) continue;
+    const uint64_t o = at[e];
+    const uint64_t en = v.ent[e];
+    if (hash) hash[o] = entry_hash(v, e);
+    if (pos) pos[o] = (uint32_t)(en >> 32);
+    if (strand) strand[o] = (uint8_t)(en & 1u);
   }
 }
 
@@ -1183,6 +1598,19 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
   GOD_CUDA(cudaMemsetAsync(ro.n_large, 0, sizeof(uint32_t), st));
   GOD_CUDA(cudaMemsetAsync(nd_d, 0, sizeof(uint64_t), st));
   bool runs_done = false;
+  // K6 directory.  mode 1 (2k - 12 in [2, 30]): data-sized monotone slot map over the top-12-bit
+  // segments, ~DIR_TARGET entries per slot (minimizer hashes are skewed toward small values, and so
+  // are the probes; a fixed hash-bit prefix leaves ~20 entries in the dense slots).  mode 0: the top
+  // B hash bits, B = clamp(floor(log2 n_kept), 2k - 31, min(2k, 28)).
+  const uint32_t hb = 2 * P.k;
+  const bool mode1 = hb >= 14 && hb - DIR_SEG_BITS <= 30 && !getenv("GOD_DIR_MODE0");
+  const char* dt = getenv("GOD_DIR_TARGET");  // test hook: entries per slot
+  const uint32_t DIR_TARGET = dt ? (uint32_t)std::max(1, atoi(dt)) : 2u;
+  uint32_t B = 0, low_bits = 0;
+  uint64_t n_slots = 0;
+  uint2* seg = nullptr;
+  bool built = false;  // the bin sort wrote the entries and the directory (bin_sort && mode1)
+  uint32_t S_dir = 0;
   if (n > 1) {
     uint64_t* k1 = scr.alloc<uint64_t>(n);
     uint32_t* v1 = scr.alloc<uint32_t>(n);
@@ -1194,6 +1622,7 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
       GOD_CUDA(cudaFuncSetAttribute(k_rs_scatter2<RS_BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize, RS_DYN_SMEM));
       GOD_CUDA(cudaFuncSetAttribute(k_rs_scatter2<BIN_DIGIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, RS_DYN_SMEM));
       GOD_CUDA(cudaFuncSetAttribute(k_bin_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, BS_SMEM));
+      GOD_CUDA(cudaFuncSetAttribute(k_bin_build, cudaFuncAttributeMaxDynamicSharedMemorySize, BB_SMEM));
       GOD_CUDA(cudaFuncSetAttribute(k_bucket_sort_big, cudaFuncAttributeMaxDynamicSharedMemorySize, BS_SMEM));
       attr = true;
     }
@@ -1234,16 +1663,35 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
       GOD_CUDA(cudaMemsetAsync(n_big, 0, 2 * sizeof(uint32_t), st));
       GOD_LAUNCH("k_bucket_bounds", k_bucket_bounds, grid_for((uint64_t)nb + 1, 256), 256, 0, st, k0, n, hbits, nb,
                  bstart);
-      GOD_LAUNCH("k_bin_sort", k_bin_sort, 2u * num_sms(), BS_NT, BS_SMEM, st, k0, v0, bstart, n_bins_d, L, hbits, big,
-                 n_big, ro);
+      if (mode1) {
+        // K5 + K6 fused into the bin sort: the directory slots are cut from the same segment table, S per
+        // bin (slots_t = S * bins_t), so every bin owns whole slots; entries go to their final place
+        built = true;
+        S_dir = std::max(1u, std::min(S_MAX, target / DIR_TARGET));
+        n_slots = (uint64_t)S_dir * nb;
+        GOD_REQUIRE(n < 0xFFFFFFFFull, "index has >= 2^32 entries");
+        GOD_CUDA(cudaMallocAsync((void**)&seg, (1u << SEG_BITS) * sizeof(uint2), st));
+        GOD_LAUNCH("k_seg_slots", k_seg_slots, (1u << SEG_BITS) / 256, 256, 0, st, table, S_dir, seg);
+        GOD_CUDA(cudaMallocAsync((void**)&ix->dir, std::max<uint64_t>(n_slots, 1) * sizeof(DirRec), st));
+        GOD_CUDA(cudaMallocAsync((void**)&ix->ent, n * sizeof(uint64_t), st));
+        GOD_LAUNCH("k_bin_build", k_bin_build, 2u * num_sms(), BS_NT, BB_SMEM, st, k0, v0, bstart, n_bins_d, L, hbits,
+                   big, n_big, ro, table, nullptr, S_dir, ix->ent, ix->dir);
+      } else {
+        GOD_LAUNCH("k_bin_sort", k_bin_sort, 2u * num_sms(), BS_NT, BS_SMEM, st, k0, v0, bstart, n_bins_d, L, hbits, big,
+                   n_big, ro);
+      }
       runs_done = true;
       const uint32_t hb_big = d2h_scalar(n_big, st);
       if (getenv("GOD_DEBUG_BUCKETS"))
-        fprintf(stderr, "[bins] n=%llu bins=%u target=%u big=%u lsd=%u\n", (unsigned long long)n, nb, target, hb_big,
-                d2h_scalar(n_big + 1, st));
-      if (hb_big)
+        fprintf(stderr, "[bins] n=%llu bins=%u target=%u big=%u lsd=%u S=%u\n", (unsigned long long)n, nb, target, hb_big,
+                d2h_scalar(n_big + 1, st), S_dir);
+      if (hb_big) {
         GOD_LAUNCH("k_bucket_sort_big", k_bucket_sort_big, std::min(hb_big, (uint32_t)num_sms()), BS_NT, BS_SMEM, st, k0,
-                   v0, /*t0=*/k1, /*t1=*/k0, bstart, big, n_big, L, hbits, ro);
+                   v0, /*t0=*/k1, /*t1=*/k0, bstart, big, n_big, L, hbits, ro, built ? ix->ent : nullptr);
+        if (built)
+          GOD_LAUNCH("k_big_dir", k_big_dir, std::min(hb_big, 4u * (uint32_t)num_sms()), BS_NT, 0, st, k0, bstart, big,
+                     n_big, L, hbits, table, S_dir, ix->dir);
+      }
     } else {
       // K2 full stable LSD over the 2k hash bits (position order kept within equal hashes)
       for (int shift = 0; shift < hbits; shift += RS_BITS)
@@ -1264,18 +1712,10 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
   const uint64_t nd = hcs.n_distinct;
   const uint64_t n_kept = hcs.kept_entries;
   GOD_REQUIRE(n_kept < 0xFFFFFFFFull, "index has >= 2^32 kept entries");
-  // K6 directory.  mode 1 (2k - 12 in [2, 30]): data-sized monotone slot map over the top-12-bit
-  // segments, ~DIR_TARGET entries per slot (minimizer hashes are skewed toward small values, and so
-  // are the probes; a fixed hash-bit prefix leaves ~20 entries in the dense slots).  mode 0: the top
-  // B hash bits, B = clamp(floor(log2 n_kept), 2k - 31, min(2k, 28)).
-  const uint32_t hb = 2 * P.k;
-  const bool mode1 = hb >= 14 && hb - DIR_SEG_BITS <= 30 && !getenv("GOD_DIR_MODE0");
-  const char* dt = getenv("GOD_DIR_TARGET");  // test hook: entries per slot
-  const uint32_t DIR_TARGET = dt ? (uint32_t)std::max(1, atoi(dt)) : 2u;
-  uint32_t B = 0, low_bits = 0;
-  uint64_t n_slots = 0;
-  uint2* seg = nullptr;
-  if (mode1) {
+  if (built) {
+    low_bits = hb - DIR_SEG_BITS;
+    B = floor_log2(n_slots);
+  } else if (mode1) {
     if (!segc) {
       segc = scr.alloc<uint32_t>(1u << SEG_BITS);
       GOD_CUDA(cudaMemsetAsync(segc, 0, (1u << SEG_BITS) * sizeof(uint32_t), st));
@@ -1311,6 +1751,14 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
   ix->seg = seg;
   ix->low_bits = low_bits;
   ix->n_slots = n_slots;
+  if (built) {  // every entry is in ent; hashes above tau are dropped at probe time
+    ix->n_ent = n;
+    ix->tau_probe = (uint32_t)std::min<uint64_t>(hcs.tau, 0xFFFFFFFEull);
+    GOD_CUDA(cudaStreamSynchronize(st));
+    return;
+  }
+  ix->n_ent = n_kept;
+  ix->tau_probe = 0xFFFFFFFFu;
   GOD_CUDA(cudaMallocAsync((void**)&ix->dir, n_slots * sizeof(DirRec), st));
   uint32_t* dir1 = scr.alloc<uint32_t>(n_slots + 1);  // first entry per slot (+ n_kept), then pairs
   GOD_CUDA(cudaMallocAsync((void**)&ix->ent, (n_kept ? n_kept : 1) * sizeof(uint64_t), st));
@@ -1357,7 +1805,19 @@ void index_count(const god_index* ix, const uint64_t* hashes, uint64_t n, uint32
 
 void index_dump(const god_index* ix, uint64_t* hash, uint32_t* pos, uint8_t* strand, cudaStream_t st) {
   if (!ix->st.kept_entries) return;
-  GOD_LAUNCH("k_dump", k_dump, grid_for(ix->st.kept_entries, 256), 256, 0, st, ix->view(), hash, pos, strand);
+  if (ix->tau_probe == 0xFFFFFFFFu) {  // ent holds exactly the kept entries
+    GOD_LAUNCH("k_dump", k_dump, grid_for(ix->st.kept_entries, 256), 256, 0, st, ix->view(), hash, pos, strand);
+    return;
+  }
+  Scratch scr(st);
+  const uint64_t n = ix->n_ent;
+  uint32_t* keep = scr.alloc<uint32_t>(n);
+  uint64_t* at = scr.alloc<uint64_t>(n);
+  uint64_t* tot = scr.alloc<uint64_t>(1);
+  GOD_LAUNCH("k_dump_flag", k_dump_flag, grid_for(n, 256), 256, 0, st, ix->view(), keep);
+  scan_exclusive_u32_to_u64(keep, at, n, tot, st, scr, "scan_dump");
+  GOD_LAUNCH("k_dump_sel", k_dump_sel, grid_for(n, 256), 256, 0, st, ix->view(), keep, at, hash, pos, strand);
+  GOD_CUDA(cudaStreamSynchronize(st));
 }
 
 }  // namespace god

@@ -107,6 +107,8 @@ struct IndexView {
   uint32_t low_bits;
   uint64_t n_kept;
   uint64_t n_slots;
+  uint64_t n_ent;   // entries held: all of them (tau != ~0, the bin-built index) or only the kept ones
+  uint32_t tau;     // occurrence cutoff applied at probe time: a hash with more entries is absent (O7)
 };
 
 // slot of hash h; ~0 if h lies in a segment without slots (mode 1: no reference minimizer there)
@@ -123,7 +125,7 @@ __device__ __forceinline__ uint64_t index_slot(const IndexView& v, uint64_t h) {
 // minimizers (their hash values) in the seed index").  The slot record answers a slot of
 // <= DIR_KEYS entries (almost all) or <= DIR_RUNS distinct keys from one 32-B sector; a longer
 // slot is searched in the entries.
-__device__ __forceinline__ uint2 probe_range(const IndexView& v, uint64_t h) {
+__device__ __forceinline__ uint2 probe_range_all(const IndexView& v, uint64_t h) {
   const uint64_t slot = index_slot(v, h);
   if (slot == ~0ull) return make_uint2(0, 0);
   const uint32_t key = (uint32_t)(h & ((1ull << v.low_bits) - 1));
@@ -165,6 +167,11 @@ __device__ __forceinline__ uint2 probe_range(const IndexView& v, uint64_t h) {
   }
   return make_uint2(a, c);
 }
+// the kept entries with hash h: a hash with more than tau entries is dropped (reading O7)
+__device__ __forceinline__ uint2 probe_range(const IndexView& v, uint64_t h) {
+  const uint2 r = probe_range_all(v, h);
+  return r.y - r.x > v.tau ? make_uint2(r.x, r.x) : r;
+}
 
 }  // namespace god
 
@@ -176,9 +183,11 @@ struct god_index {
   uint2* seg = nullptr;       // mode 1 slot map (null in mode 0)
   uint32_t low_bits = 0;
   uint64_t n_slots = 0;
+  uint64_t n_ent = 0;              // entries in ent (all of them when tau_probe != ~0)
+  uint32_t tau_probe = 0xFFFFFFFFu;  // cutoff applied at probe time (~0: ent holds the kept entries only)
   cudaStream_t st_alloc = 0;
   god::IndexView view() const {
-    return god::IndexView{dir, ent, seg, st.dir_bits, low_bits, st.kept_entries, n_slots};
+    return god::IndexView{dir, ent, seg, st.dir_bits, low_bits, st.kept_entries, n_slots, n_ent, tau_probe};
   }
 };
 
