@@ -272,7 +272,7 @@ __device__ __forceinline__ uint64_t run_len_capped(const uint64_t* __restrict__ 
   return 1 + run_side(k, n, i, hv, lim, false, hm) + run_side(k, n, i, hv, lim, true, hm);
 }
 
-constexpr uint32_t BIN_TARGET = 3584;
+constexpr uint32_t BIN_TARGET = 3072;  // measured: 2048 13.9 ms, 2560 13.7, 3072 13.6, 3584 14.5 (stage 3, human)
 constexpr int BIN_DIGIT = 9;                      // LSD digit over b
 constexpr int BIN_RANK_MAX = 1024;                // buckets up to this size: ranked by counting, else LSD
 static_assert(RS_BINS * BS_NW == BS_NT * 8, "block scan assumes 8 counters per thread");
