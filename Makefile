@@ -11,12 +11,22 @@ PKG      := paper_2211_08157_b200
 CU_SRCS  := $(wildcard $(PKG)/csrc/*.cu)
 CU_HDRS  := $(wildcard $(PKG)/csrc/*.cuh) include/god.h
 CU_OBJS  := $(patsubst $(PKG)/csrc/%.cu,build/%.o,$(CU_SRCS))
+CK_OBJS  := $(patsubst $(PKG)/csrc/%.cu,build/checked/%.o,$(CU_SRCS))
 
-all: $(PKG)/lib/libgod.so oracle/liboracle.so synth/libsynth.so
+all: $(PKG)/lib/libgod.so $(PKG)/lib/libgod_checked.so oracle/liboracle.so synth/libsynth.so
 
 build/%.o: $(PKG)/csrc/%.cu $(CU_HDRS)
 	@mkdir -p build
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; exit 1)
+
+# the memory-safety build (GOD_CHECKED=1 loads it): device-side bounds checks on computed indices
+build/checked/%.o: $(PKG)/csrc/%.cu $(CU_HDRS)
+	@mkdir -p build/checked
+	$(NVCC) $(NVFLAGS) -DGOD_CHECKED -c $< -o $@ 2> build/checked/$*.ptxas.log || (cat build/checked/$*.ptxas.log; exit 1)
+
+$(PKG)/lib/libgod_checked.so: $(CK_OBJS)
+	@mkdir -p $(PKG)/lib
+	$(NVCC) $(ARCH) -shared -Xcompiler -fPIC $(CK_OBJS) -o $@ -lcudart
 
 $(PKG)/lib/libgod.so: $(CU_OBJS)
 	@mkdir -p $(PKG)/lib
@@ -29,6 +39,6 @@ synth/libsynth.so: synth/synth.c
 	gcc -O2 -std=c11 -shared -fPIC -fopenmp -Wall -o $@ synth/synth.c -lm
 
 clean:
-	rm -rf build $(PKG)/lib/libgod.so oracle/liboracle.so synth/libsynth.so
+	rm -rf build $(PKG)/lib/libgod.so $(PKG)/lib/libgod_checked.so oracle/liboracle.so synth/libsynth.so
 
 .PHONY: all clean

@@ -167,20 +167,11 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------------ roofline
-# Algorithmic integer operations per k-mer start position of the fused extraction:
-# the oracle's arithmetic (oracle.c or_minimizers / or_hash) mapped onto a 32-bit ALU, one op per
-# 32-bit instruction: base code 1, forward k-mer update 6, reverse-complement update 7, canonical
-# compare + select 4, strand/palindrome test 1, masked Wang hash 23 x 2 = 46, window minimum
-# (van Herk: prefix min, suffix min, combine on 64-bit keys) 12 -> 77.
-ALU_OPS_PER_POS = 77
 EXTRACT_KERNELS = ("extract_ref", "extract_phase", "extract_seed")
-
-
-def alu_peak_tops(peaks: dict) -> float:
-    """Integer-op issue peak: 148 SMs x 4 SMSPs x 32 lanes (one warp instruction per SMSP per clock;
-    alu pipe 16 lanes/clk + fma pipe (IMAD) 16 lanes/clk per SMSP) x the max SM clock."""
-    mhz = float(peaks.get("sm_max_mhz", 1965.0))
-    return 148 * 4 * 32 * mhz * 1e6 / 1e12
+# stage 1+2 (K1 on the reference) and the job set-up around it; everything else in the build is stage 3
+STAGE12_BUILD = ("extract_ref", "k_make_jobs", "scan_jobs", "k_x2_tile_desc")
+NOMINAL_HBM_GBS = 8000.0   # the north star's "~8 TB/s" (report against both)
+G0_RANDOM_GATHER = {"64MB": 226.5e9, "512MB": 49.2e9, "4GB": 37.9e9}  # profiles/g0_microbench_r01.jsonl, sectors/s
 
 
 def algorithmic_bytes(name: str, ctx: dict):
@@ -189,7 +180,7 @@ def algorithmic_bytes(name: str, ctx: dict):
     n_ref_mz = ctx["n_entries_all"]
     if name == "extract_ref":      # read every reference byte once; write 12 B per minimizer (u64 hash|strand, u32 pos)
         return ctx["ref_bytes"] + 12 * n_ref_mz
-    if name in ("k_rs_scatter", "k_rs_scatter2", "k_bin_sort"):  # read + write one 12-B record per pass / bin sort
+    if name in ("k_rs_scatter", "k_rs_scatter2"):  # read + write one 12-B record per pass
         return 24 * n_ref_mz
     if name == "k_rs_hist":
         return 8 * n_ref_mz
@@ -201,78 +192,163 @@ def algorithmic_bytes(name: str, ctx: dict):
 
 
 def load_traffic():
-    """ncu-measured DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum from one
-    `ncu --set full` capture) of the kernels profiled this round, written by tools/ncu_traffic.py."""
-    p = os.path.join(ROOT, "profiles", "ncu_traffic_r01.json")
-    if not os.path.exists(p):
-        return {}
-    try:
-        return json.load(open(p))
-    except Exception:
-        return {}
+    """ncu-measured per-launch DRAM bytes, L2 sectors and instructions of one step (`ncu --set full`
+    capture of tools/perf_step.py, summarised by tools/ncu_step_traffic.py); round 2 first."""
+    for name in ("ncu_traffic_r02.json", "ncu_traffic_r01.json"):
+        p = os.path.join(ROOT, "profiles", name)
+        if os.path.exists(p):
+            try:
+                d = json.load(open(p))
+                for v in d.values():
+                    v.setdefault("file", "profiles/" + name)
+                return d
+            except Exception:
+                pass
+    return {}
 
 
-def pick_roofline(prof: dict, ctx: dict, peaks: dict, units: dict):
-    """Roofline of the dominant kernel (largest share of device time in the timed region)."""
+def pick_roofline(prof: dict, ctx: dict, peaks: dict, units: dict, steps: int):
+    """Headline roofline = the dominant kernel's HBM view (algorithmic bytes / measured launch time
+    against the measured copy peak), plus roofline.stages: stage 1+2 (K1 on the reference), stage 3
+    (index sort/cutoff/table: survey floor bytes / stage time, ncu bytes and passes) and stage 4
+    (seeding: probes and 32-B sectors per second against G0's random-gather rates)."""
     items = sorted(prof.items(), key=lambda kv: -kv[1][0])
     total_ms = sum(v[0] for v in prof.values())
-    peak_gbs = float(peaks.get("hbm_gbs", 6650.0))
+    peak_gbs = float(peaks.get("hbm_gbs", 6451.8))
     traffic = load_traffic()
+    head = None
     for name, (ms, n) in items:
-        avg_s = ms / n / 1e3
         b = algorithmic_bytes(name, ctx)
-        tr = traffic.get(name, {})
-        common = {"kernel": name, "share_of_step": round(ms / total_ms, 4), "avg_launch_ms": round(avg_s * 1e3, 4),
-                  "traffic": tr.get("dram_bytes_per_launch"), "traffic_source": tr.get("source")}
-        if name in EXTRACT_KERNELS and units.get(name):
-            pos = units[name] / n
-            ops = ALU_OPS_PER_POS * pos
-            ach = ops / avg_s / 1e12
-            pk = alu_peak_tops(peaks)
-            out = {"bound": "alu", "achieved": round(ach, 3), "peak": round(pk, 2), "unit": "Tops/s",
-                   "frac": round(ach / pk, 4), **common, "positions_per_launch": int(pos),
-                   "algorithmic_ops_per_position": ALU_OPS_PER_POS,
-                   "peak_source": "DESIGN.md §5: 148 SM x 128 int32 lanes/clk x sm_max_mhz (G0 measured 31.35 Tops/s)"}
-            if b is not None:
-                out["hbm_view"] = {"achieved_gbs": round(b / avg_s / 1e9, 1), "peak_gbs": peak_gbs,
-                                   "frac": round(b / avg_s / 1e9 / peak_gbs, 4), "algorithmic_bytes_per_launch": int(b)}
-            return out
         if b is None:
             continue
+        avg_s = ms / n / 1e3
+        tr = traffic.get(name, {})
         ach = b / avg_s / 1e9
-        return {"bound": "hbm", "achieved": round(ach, 1), "peak": peak_gbs, "unit": "GB/s",
-                "frac": round(ach / peak_gbs, 4), **common, "algorithmic_bytes_per_launch": int(b),
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, measured)"}
-    return None
+        head = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak_gbs, "unit": "GB/s", "frac": round(ach / peak_gbs, 4),
+                "traffic": tr.get("dram_bytes_per_launch"), "kernel": name, "share_of_step": round(ms / total_ms, 4),
+                "avg_launch_ms": round(avg_s * 1e3, 4), "algorithmic_bytes_per_launch": int(b),
+                "frac_of_8tbs": round(ach / NOMINAL_HBM_GBS, 4),
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, measured; burst)",
+                "traffic_source": tr.get("file")}
+        if name in EXTRACT_KERNELS and units.get(name):
+            pos = units[name] / n
+            head["positions_per_launch"] = int(pos)
+            if tr.get("inst_executed"):  # measured instruction issue (the kernel is issue-bound, DESIGN.md §5)
+                slots = 32.0 * tr["inst_executed"] / pos
+                issue_floor_ms = tr["inst_executed"] / (148 * 4 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6) * 1e3
+                head["issue_view"] = {"warp_inst_per_launch": tr["inst_executed"],
+                                      "thread_slots_per_position": round(slots, 1),
+                                      "issue_bound_ms_at_100pct": round(issue_floor_ms, 3),
+                                      "frac_of_issue_peak": round(issue_floor_ms / (avg_s * 1e3), 4),
+                                      "source": tr.get("file")}
+        break
+    stages = {}
+    ms_of = lambda t: prof.get(t, (0.0, 1))[0] / steps  # noqa: E731
+    n = ctx["n_entries_all"]
+    if "extract_ref" in prof:
+        b = ctx["ref_bytes"] + 12 * n
+        t = ms_of("extract_ref")
+        stages["stage12_sparsify_extract"] = {
+            "kernel": "extract_ref", "ms": round(t, 4), "algorithmic_bytes": int(b),
+            "achieved_gbs": round(b / t / 1e6, 1), "frac": round(b / t / 1e6 / peak_gbs, 4),
+            "frac_of_8tbs": round(b / t / 1e6 / NOMINAL_HBM_GBS, 4),
+            "ncu_dram_bytes": traffic.get("extract_ref", {}).get("dram_bytes_per_launch")}
+    s3 = {k: v for k, v in prof.items() if k in ctx["build_kernels"] and k not in STAGE12_BUILD}
+    if s3:
+        t = sum(v[0] for v in s3.values()) / steps
+        floor = 12 * n + 8 * ctx["kept_entries"] + 16 * ctx["kept_distinct"] + 4 * (1 << ctx["dir_bits"])
+        nb = sum(traffic[k]["dram_bytes_per_launch"] * (v[1] // steps) for k, v in s3.items() if k in traffic)
+        stages["stage3_index"] = {
+            "ms": round(t, 4), "floor_bytes": int(floor),
+            "floor_def": "SURVEY §8(d): 12 B read per record + 8 B per kept entry + 16 B per kept distinct key + 4 B x 2^dir_bits",
+            "achieved_gbs": round(floor / t / 1e6, 1), "frac": round(floor / t / 1e6 / peak_gbs, 4),
+            "ncu_dram_bytes": int(nb) if nb else None,
+            "ncu_bytes_over_floor": round(nb / floor, 2) if nb else None,
+            "record_passes": round(nb / (24.0 * n), 2) if nb else None,
+            "kernels_ms": {k: round(v[0] / steps, 4) for k, v in sorted(s3.items(), key=lambda kv: -kv[1][0])}}
+    if "k_probe" in prof and units.get("k_probe"):
+        t = ms_of("k_probe")
+        probes = units["k_probe"] / steps
+        tr = traffic.get("k_probe", {})
+        sec = tr.get("l2_read_sectors")
+        st4 = {"kernel": "k_probe", "ms": round(t, 4), "probes": int(probes), "probes_per_s": round(probes / t * 1e3, 1),
+               "g0_random_gather_sectors_per_s": G0_RANDOM_GATHER}
+        if sec:
+            sps = sec / (tr.get("ncu_ms_per_launch") or t) * 1e3
+            st4.update({"l2_read_sectors_per_probe": round(sec / probes, 2), "sectors_per_s_in_bench": round(sec / t * 1e3, 1),
+                        "frac_of_g0_4gb_gather": round(sec / t * 1e3 / G0_RANDOM_GATHER["4GB"], 3),
+                        "dram_bytes_per_probe": round(tr["dram_bytes_per_launch"] / probes, 1),
+                        "l2_hit_rate_pct": tr.get("l2_hit_rate_pct"), "source": tr.get("file")})
+        if "k_anchor_write" in prof:
+            ta = ms_of("k_anchor_write")
+            st4["anchor_write"] = {"ms": round(ta, 4), "anchors_per_s": round(ctx["n_anchors"] / ta * 1e3, 1),
+                                   "ncu_dram_bytes": traffic.get("k_anchor_write", {}).get("dram_bytes_per_launch"),
+                                   "algorithmic_bytes": 16 * ctx["n_anchors"]}
+        stages["stage4_seeding"] = st4
+    if head is not None:
+        head["stages"] = stages
+    return head
 
 
 # ------------------------------------------------------------------------------------------ CPU oracle
+def host_info() -> dict:
+    model = ""
+    try:
+        for line in subprocess.run(["lscpu"], capture_output=True, text=True).stdout.splitlines():
+            if line.startswith("Model name:"):
+                model = line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
+
+
 def oracle_sample(cfg, pattern, k, w, sample_bp: int, sample_reads: int):
-    """Time the CPU oracle on a bounded sample: index over a reference prefix of sample_bp bases and
-    seeding of sample_reads reads simulated from that prefix (same error model).  Returns
-    (seconds for the full workload extrapolated linearly, description)."""
+    """Time the CPU oracle (single thread, as it stands) stage by stage on a bounded sample: a
+    reference prefix of sample_bp bases (stage 1 sparsify, stage 2 minimizers, stage 1-3 index) and
+    sample_reads reads simulated from it (stage 4: SELECT-mode phase selection + seeding, and
+    GIVEN-mode seeding alone, so phase selection = the difference).  Each stage is extrapolated
+    linearly to the full workload (reference bases, reads).  Returns (seconds for the whole step
+    extrapolated, description, seconds spent, per-stage dict)."""
     import oracle
     import synth
     L = min(sample_bp, cfg.ref.size)
     pref = np.ascontiguousarray(cfg.ref[:L])
     off = np.array([0, L], np.uint64)
+    fr = cfg.ref.size / L
+    t0 = time.perf_counter()
+    oracle.sparsify(pref, pattern, 0)
+    t_sp = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    oracle.minimizers_batch(pref, off, pattern, k, w, global_pos=True)
+    t_mz = time.perf_counter() - t0
     t0 = time.perf_counter()
     ix = oracle.Index(pref, off, pattern, k, w)
     t_idx = time.perf_counter() - t0
     rd = cfg.reads
     nr = min(sample_reads, rd.n)
+    fq = rd.n / max(1, nr)
     lens = np.diff(rd.offsets.astype(np.int64))
     mean_len = float(lens.mean()) if lens.size else 150.0
     sim = synth.simulate_reads(pref, nr, 9001, length=int(round(mean_len)), start_margin=int(mean_len * 1.3) + 64,
                                p_sub=0.001, p_ins=0.00005, p_del=0.00005)
     t0 = time.perf_counter()
-    ix.seed_reads(sim.seq, sim.offsets)
+    _, _, ph = ix.seed_reads(sim.seq, sim.offsets)
     t_seed = time.perf_counter() - t0
-    full = t_idx * (cfg.ref.size / L) + t_seed * (rd.n / max(1, nr))
-    desc = (f"oracle index over a {L/1e6:.0f} Mbp prefix of the reference ({t_idx:.1f}s) + SELECT-mode seeding of "
-            f"{nr} reads simulated from that prefix ({t_seed:.1f}s), each scaled linearly to the full workload "
-            f"({cfg.ref.size/1e9:.2f} Gbp, {rd.n} reads)")
-    return full, desc, t_idx + t_seed
+    t0 = time.perf_counter()
+    ix.seed_reads(sim.seq, sim.offsets, phases=ph)
+    t_given = time.perf_counter() - t0
+    full = t_idx * fr + t_seed * fq
+    stages = {  # seconds for the full workload, extrapolated linearly from the sample
+        "stage1_sparsify_ref_s": round(t_sp * fr, 2),
+        "stage2_minimizers_ref_s": round(t_mz * fr, 2),
+        "stage3_index_build_s": round(t_idx * fr, 2),   # includes its own stage 1+2 pass (oracle.c or_build_index)
+        "stage4a_phase_select_s": round(max(0.0, t_seed - t_given) * fq, 2),
+        "stage4b_seeding_s": round(t_given * fq, 2),
+        "extrapolated": True, "sample_ref_bp": int(L), "sample_reads": int(nr), **host_info(), "cores_used": 1}
+    desc = (f"oracle stage by stage on a {L/1e6:.0f} Mbp reference prefix (sparsify {t_sp:.1f}s, minimizers {t_mz:.1f}s, "
+            f"index {t_idx:.1f}s) and {nr} reads simulated from it (SELECT seeding {t_seed:.1f}s, GIVEN seeding "
+            f"{t_given:.1f}s), each extrapolated linearly to the full workload ({cfg.ref.size/1e9:.2f} Gbp, {rd.n} reads)")
+    return full, desc, t_sp + t_mz + t_idx + t_seed + t_given, stages
 
 
 # ------------------------------------------------------------------------------------------ main
@@ -352,7 +428,7 @@ def main():
     god.profile_enable(False)
     launches = god.launch_count() - launches0
     prof = god.profile_query()
-    units = {kname: god.profile_units(kname) for kname in EXTRACT_KERNELS}
+    units = {kname: god.profile_units(kname) for kname in EXTRACT_KERNELS + ("k_probe",)}
     elapsed_ms = start.elapsed_time(end)
     build_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in evs]))
     seed_ms = float(np.mean([e[1].elapsed_time(e[2]) for e in evs]))
@@ -362,14 +438,24 @@ def main():
     ms_per_step = elapsed_ms / args.steps
     value = aggregate_rate(n_reads, world, ms_per_step)
 
+    # which kernels belong to the index build (stage 1+2 + stage 3), from one untimed profiled build
+    god.profile_reset()
+    god.profile_enable(True)
+    ixb = god.god_build_index(dref, droff, pattern, k, w, cutoff=cfg.cutoff)
+    torch.cuda.synchronize()
+    ixb.free()
+    build_kernels = set(god.profile_query().keys())
+    god.profile_enable(False)
     # records counts for the byte model (one extra untimed pass)
     hz, _, _, _ = god.god_minimizers(dreads, droffs, pattern, k, w, phases=None)  # phase-0 read minimizers (approx.)
     n_read_mz = int(hz.shape[0])
     del hz
     peaks = json.load(open(PEAKS)) if os.path.exists(PEAKS) else {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}
     ctx = {"ref_bytes": int(cfg.ref.size), "read_bytes": int(cfg.reads.seq.size), "n_entries_all": st["n_entries_all"],
-           "n_read_mz": n_read_mz, "n_phase_mz": n_read_mz * 2}
-    roof = pick_roofline(prof, ctx, peaks, units)
+           "n_read_mz": n_read_mz, "n_phase_mz": n_read_mz * 2, "kept_entries": st["kept_entries"],
+           "kept_distinct": st["kept_distinct"], "dir_bits": st["dir_bits"], "n_anchors": n_anchors,
+           "build_kernels": build_kernels}
+    roof = pick_roofline(prof, ctx, peaks, units, args.steps)
     kernels = {kname: {"ms_per_step": round(ms / args.steps, 4), "launches_per_step": n // args.steps}
                for kname, (ms, n) in sorted(prof.items(), key=lambda kv: -kv[1][0])}
 
@@ -386,10 +472,19 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        full_s, desc, spent = oracle_sample(cfg, pattern, k, w, int(args.cpu_sample_bp * args.scale) or 1_000_000,
-                                            max(1000, int(args.cpu_sample_reads * args.scale)))
+        full_s, desc, spent, ostages = oracle_sample(cfg, pattern, k, w,
+                                                     int(args.cpu_sample_bp * args.scale) or 1_000_000,
+                                                     max(1000, int(args.cpu_sample_reads * args.scale)))
+        gpu_s = {"stage12_extract_ref_s": prof.get("extract_ref", (0.0, 1))[0] / args.steps / 1e3,
+                 "stage3_index_build_s": build_ms / 1e3, "stage4_phase_select_and_seed_s": seed_ms / 1e3}
         cpu = {"value": round(n_reads / full_s, 2), "unit": "reads/s", "cores": 1, "kind": "oracle",
-               "sample": desc, "cpu_seconds_spent": round(spent, 1)}
+               "sample": desc, "cpu_seconds_spent": round(spent, 1), "stages": ostages,
+               "speedup_gpu_over_oracle": {
+                   "stage1+2 (minimizers of the reference)": round(ostages["stage2_minimizers_ref_s"] / gpu_s["stage12_extract_ref_s"], 1)
+                   if gpu_s["stage12_extract_ref_s"] else None,
+                   "index build (stages 1-3)": round(ostages["stage3_index_build_s"] / gpu_s["stage3_index_build_s"], 1),
+                   "phase selection + seeding (stage 4)": round((ostages["stage4a_phase_select_s"] + ostages["stage4b_seeding_s"])
+                                                                / gpu_s["stage4_phase_select_and_seed_s"], 1)}}
 
     if rank == 0:
         out = {
@@ -531,8 +626,9 @@ def run_reference(args, world, rank):
     spent = 0.0
     sbp = max(1_000_000, int(4_000_000 * args.scale))
     srd = max(500, int(4_000 * args.scale))
+    ostages = None
     for i in range(args.warmup + args.steps):
-        full_s, desc, sp = oracle_sample(cfg, pattern, k, w, sbp, srd)
+        full_s, desc, sp, ostages = oracle_sample(cfg, pattern, k, w, sbp, srd)
         if i >= args.warmup:
             times.append(full_s)
             spent += sp
@@ -542,7 +638,8 @@ def run_reference(args, world, rank):
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(full * 1e3, 1), "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
            "config": workload_config(args, cfg, pattern, k, w, world),
-           "cpu_baseline": {"value": round(v, 2), "unit": "reads/s", "cores": 1, "kind": "oracle", "sample": desc},
+           "cpu_baseline": {"value": round(v, 2), "unit": "reads/s", "cores": 1, "kind": "oracle", "sample": desc,
+                            "stages": ostages},
            "e2e": {"value": round(v, 2), "unit": "reads/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 

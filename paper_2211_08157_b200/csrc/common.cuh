@@ -1,5 +1,6 @@
 // common.cuh — shared device/host helpers of libgod (the product path; never includes oracle/).
 #pragma once
+#include <cstdio>
 #include <cuda_runtime.h>
 #include <cuda/atomic>
 #include <stdint.h>
@@ -201,6 +202,26 @@ inline unsigned grid_for(uint64_t n, unsigned block) {
 }
 
 int num_sms();
+
+// ------------------------------------------------------------------------------------ checked build
+// GOD_DCHECK(cond, what): with -DGOD_CHECKED (libgod_checked.so, loaded when GOD_CHECKED=1) a computed
+// global index or address that leaves its buffer prints the site and traps (the launch then fails with
+// an illegal-instruction error that the C ABI reports as GOD_ECUDA); compiled out otherwise.  This is
+// the memory-safety layer that stands in for compute-sanitizer, which the GPU pool refuses.
+#ifdef GOD_CHECKED
+#define GOD_DCHECK(cond, what)                                                                             \
+  do {                                                                                                     \
+    if (!(cond)) {                                                                                         \
+      printf("GOD_CHECKED: %s violated at %s:%d (block %u, thread %u)\n", what, __FILE__, __LINE__,         \
+             blockIdx.x, threadIdx.x);                                                                     \
+      __trap();                                                                                            \
+    }                                                                                                      \
+  } while (0)
+#else
+#define GOD_DCHECK(cond, what) \
+  do {                         \
+  } while (0)
+#endif
 
 // ------------------------------------------------------------------------------------ tracing
 // Every kernel launch goes through GOD_LAUNCH: it counts launches (god_launch_count) and, when

@@ -179,6 +179,9 @@ __device__ __forceinline__ uint32_t pack16(const uint8_t* seq, uint64_t seq_byte
           v |= (uint32_t)seq[q] << (8 * (q - ad));
       w[i] = v;
     } else {
+      GOD_DCHECK((int64_t)(pa - reinterpret_cast<uintptr_t>(seq)) + 4ll * i >= -3 &&
+                     (int64_t)(pa - reinterpret_cast<uintptr_t>(seq)) + 4ll * i < (int64_t)seq_bytes,
+                 "K1 unchecked sequence load inside the buffer");
       w[i] = __ldg(src + i);
     }
   }
@@ -461,6 +464,7 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract3(X2Args a) {
     const uint64_t cw_lo = T.cw_lo;
     const int nwords = (int)(T.cw_hi - cw_lo);
     // the tile's job bases in SMEM (a tile spans <= NT + 1 jobs: every job owns >= 1 block)
+    GOD_DCHECK(j1 < a.n_jobs && nj <= X2_NT + 1 && nwords >= 0 && nwords <= C::MAXWORDS, "K1 tile descriptor");
     for (uint32_t q = tid; q <= nj; q += X2_NT) {
       skb[q] = a.kb[j0 + q];
       scw[q] = a.cw[j0 + q];
@@ -761,6 +765,7 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract3(X2Args a) {
 #pragma unroll
       for (int o = 0; o < W; o++) {
         if ((selmask >> o) & 1u) {
+          GOD_DCHECK(rank < (uint32_t)X2_CAP, "K1 staging index");
           SHZ[rank] = HZ[tid * W + o];
           SPOS[rank] = pb + pat_delta<PP, PX>(r0, (uint32_t)o);
           ++rank;
@@ -768,6 +773,7 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract3(X2Args a) {
       }
       __syncthreads();
       const uint64_t base = s_base;
+      GOD_DCHECK(!emit_blk || J < a.n_jobs, "K1 job index");
       if (a.job_off && emit_blk && l0 == 0) a.job_off[J] = base + before + incl - cnt;
       // aligned tiles: the last block of each job records the job's end (jobs lie in one tile)
       if (a.job_end && emit_blk && (tid + 1 >= tile_nb || sjob[tid + 1] != J)) a.job_end[J] = base + before + incl;

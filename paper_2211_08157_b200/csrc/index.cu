@@ -185,6 +185,7 @@ __global__ void __launch_bounds__(RS2_NT, 2) k_rs_scatter2(const uint64_t* __res
     const uint64_t kk = sk[s];
     const uint32_t d = (uint32_t)((kk & HASH_BITS_MASK) >> shift) & dmask;
     const uint64_t dst = s_goff[d] + (s - dstart[d]);
+    GOD_DCHECK(dst < n, "LSD scatter destination");
     kout[dst] = kk;
     vout[dst] = sv[s];
   }
@@ -275,13 +276,17 @@ __device__ __forceinline__ uint64_t run_len_capped(const uint64_t* __restrict__ 
 constexpr uint32_t BIN_TARGET = 3072;  // measured: 2048 13.9 ms, 2560 13.7, 3072 13.6, 3584 14.5 (stage 3, human)
 constexpr int BIN_DIGIT = 9;                      // LSD digit over b
 constexpr int BIN_RANK_MAX = 1024;                // buckets up to this size: ranked by counting, else LSD
+constexpr uint32_t RANK_SQ_PER_REC = 48;          // k_bin_build: LSD once sum(bucket^2) / n exceeds this
 static_assert(RS_BINS * BS_NW == BS_NT * 8, "block scan assumes 8 counters per thread");
 
-__global__ void k_seg_hist(const uint64_t* __restrict__ k, uint64_t n, int L, uint32_t* segc) {
+// records per top-SEG_BITS segment, counting every `stride`-th record (the bin widths only balance the
+// bins: every segment gets >= 1 bin, so a sampled count never lets a bin span two segments)
+__global__ void k_seg_hist(const uint64_t* __restrict__ k, uint64_t n, int L, uint32_t* segc, uint32_t stride) {
   __shared__ uint32_t h[1 << SEG_BITS];
   for (int i = threadIdx.x; i < (1 << SEG_BITS); i += blockDim.x) h[i] = 0;
   __syncthreads();
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+  for (uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) * stride; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x * stride)
     atomicAdd(&h[(uint32_t)((k[i] & HASH_BITS_MASK) >> L)], 1u);
   __syncthreads();
   for (int i = threadIdx.x; i < (1 << SEG_BITS); i += blockDim.x)
@@ -290,7 +295,7 @@ __global__ void k_seg_hist(const uint64_t* __restrict__ k, uint64_t n, int L, ui
 
 // one CTA of 1024 threads: bins_t, base_t (exclusive scan) and the total bin count
 __global__ void __launch_bounds__(1024) k_seg_table(const uint32_t* __restrict__ segc, uint32_t target, uint2* table,
-                                                    uint32_t* n_bins) {
+                                                    uint32_t* n_bins, uint32_t scale = 1, uint32_t min_bins = 0) {
   constexpr int PER = (1 << SEG_BITS) / 1024;
   __shared__ uint32_t wsum[32];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -298,7 +303,7 @@ __global__ void __launch_bounds__(1024) k_seg_table(const uint32_t* __restrict__
 #pragma unroll
   for (int q = 0; q < PER; q++) {
     const uint32_t c = segc[tid * PER + q];
-    nb[q] = (c + target - 1) / target;
+    nb[q] = max(min_bins, (uint32_t)(((uint64_t)c * scale + target - 1) / target));
     tsum += nb[q];
   }
   uint32_t incl = tsum;
@@ -863,8 +868,15 @@ __global__ void __launch_bounds__(BS_NT, 2) k_bin_build(const uint64_t* __restri
       const uint4 p0 = c4[2 * threadIdx.x], p1 = c4[2 * threadIdx.x + 1];
       uint32_t y[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
       uint32_t tsum = 0, tmax = 0;
+      uint64_t tsq = 0;  // sum of squared bucket sizes: the cost of ranking by counting
 #pragma unroll
-      for (int q = 0; q < 8; q++) { const uint32_t c2 = y[q]; y[q] = tsum; tsum += c2; tmax = max(tmax, c2); }
+      for (int q = 0; q < 8; q++) {
+        const uint32_t c2 = y[q];
+        y[q] = tsum;
+        tsum += c2;
+        tmax = max(tmax, c2);
+        tsq += (uint64_t)c2 * c2;
+      }
       uint32_t incl = tsum;
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
@@ -872,14 +884,26 @@ __global__ void __launch_bounds__(BS_NT, 2) k_bin_build(const uint64_t* __restri
         if (lane >= d) incl += t2;
       }
 #pragma unroll
-      for (int d = 16; d; d >>= 1) tmax = max(tmax, __shfl_xor_sync(0xffffffffu, tmax, d));
+      for (int d = 16; d; d >>= 1) {
+        tmax = max(tmax, __shfl_xor_sync(0xffffffffu, tmax, d));
+        tsq += __shfl_xor_sync(0xffffffffu, tsq, d);
+      }
+      if (lane == 0) s_vo[wid] = tsq;
       if (lane == 31) wsum[wid] = incl;
       if (lane == 0) s_or[wid] = tmax;
       __syncthreads();
       uint32_t before = incl - tsum;
       cmax = 0;
+      uint64_t sq = 0;
 #pragma unroll
-      for (int q = 0; q < BS_NW; q++) { before += q < wid ? wsum[q] : 0u; cmax = max(cmax, s_or[q]); }
+      for (int q = 0; q < BS_NW; q++) {
+        before += q < wid ? wsum[q] : 0u;
+        cmax = max(cmax, s_or[q]);
+        sq += s_vo[q];
+      }
+      // ranking by counting costs sum(c^2) compares (runs of a repeated hash share a bucket); past
+      // ~RANK_SQ_PER_REC per record the LSD over the varying bits is cheaper
+      if (sq > (uint64_t)RANK_SQ_PER_REC * (uint64_t)n) cmax = BIN_RANK_MAX + 1;
       c4[2 * threadIdx.x] = make_uint4(y[0] + before, y[1] + before, y[2] + before, y[3] + before);
       c4[2 * threadIdx.x + 1] = make_uint4(y[4] + before, y[5] + before, y[6] + before, y[7] + before);
     }
@@ -966,6 +990,7 @@ __global__ void __launch_bounds__(BS_NT, 2) k_bin_build(const uint64_t* __restri
     const uint64_t qbase = (uint64_t)(c - tb.x) * S;
     for (uint32_t q = threadIdx.x; q <= S; q += BS_NT) first[q] = (uint32_t)n;
     __syncthreads();
+    GOD_DCHECK(e <= bstart[nb] && (uint64_t)c * S + S <= (uint64_t)nb * S, "bin build: bin range");
     for (int i = threadIdx.x; i < n; i += BS_NT) {
       const uint64_t pv = res[i];
       __stcs(ent + s + i, ((pv >> 1) << 32) | ((pv >> 33) << 1) | (pv & 1ull));
@@ -978,6 +1003,7 @@ __global__ void __launch_bounds__(BS_NT, 2) k_bin_build(const uint64_t* __restri
       }
       if (head) {  // a slot starts at a run head: its first record
         const uint32_t q = (uint32_t)((((uint64_t)lo * slots_t) >> L) - qbase);
+        GOD_DCHECK(q < S, "bin build: slot of a record inside its bin");
         const uint32_t qp = i ? (uint32_t)((((res[i - 1] >> 33) * slots_t) >> L) - qbase) : 0xFFFFFFFFu;
         if (q != qp) first[q] = (uint32_t)i;
       }
@@ -1645,12 +1671,13 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
       uint2* table = scr.alloc<uint2>(1u << SEG_BITS);
       uint32_t* n_bins_d = scr.alloc<uint32_t>(1);
       GOD_CUDA(cudaMemsetAsync(segc, 0, (1u << SEG_BITS) * sizeof(uint32_t), st));
-      GOD_LAUNCH("k_seg_hist", k_seg_hist, 4u * num_sms(), 512, 0, st, k0, n, L, segc);
+      const uint32_t seg_stride = n >= (1ull << 24) ? 16u : 1u;  // sampled widths on large inputs
+      GOD_LAUNCH("k_seg_hist", k_seg_hist, 4u * num_sms(), 512, 0, st, k0, n, L, segc, seg_stride);
       const char* bt = getenv("GOD_BIN_TARGET");  // test hook: bin size (default BIN_TARGET)
       const uint64_t base_target = bt ? std::max(1, atoi(bt)) : BIN_TARGET;
       const uint32_t target =
           (uint32_t)std::max<uint64_t>(base_target, n / ((1u << (2 * BIN_DIGIT)) - (1u << SEG_BITS)) + 1);
-      GOD_LAUNCH("k_seg_table", k_seg_table, 1, 1024, 0, st, segc, target, table, n_bins_d);
+      GOD_LAUNCH("k_seg_table", k_seg_table, 1, 1024, 0, st, segc, target, table, n_bins_d, seg_stride, 1u);
       // the first pass's tile histograms of the bins; the first scatter assigns the bins itself
       GOD_LAUNCH("k_seg_assign", k_seg_assign, ntiles, RS_NT, 0, st, k0, n, L, hbits, table, (1u << BIN_DIGIT) - 1, hist,
                  ntiles, 0);
@@ -1719,7 +1746,7 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
     if (!segc) {
       segc = scr.alloc<uint32_t>(1u << SEG_BITS);
       GOD_CUDA(cudaMemsetAsync(segc, 0, (1u << SEG_BITS) * sizeof(uint32_t), st));
-      if (n) GOD_LAUNCH("k_seg_hist", k_seg_hist, 4u * num_sms(), 512, 0, st, k0, n, (int)(hb - SEG_BITS), segc);
+      if (n) GOD_LAUNCH("k_seg_hist", k_seg_hist, 4u * num_sms(), 512, 0, st, k0, n, (int)(hb - SEG_BITS), segc, 1u);
     }
     GOD_CUDA(cudaMallocAsync((void**)&seg, (1u << SEG_BITS) * sizeof(uint2), st));
     uint32_t* ns_d = scr.alloc<uint32_t>(1);

@@ -128,10 +128,12 @@ __device__ __forceinline__ uint64_t index_slot(const IndexView& v, uint64_t h) {
 __device__ __forceinline__ uint2 probe_range_all(const IndexView& v, uint64_t h) {
   const uint64_t slot = index_slot(v, h);
   if (slot == ~0ull) return make_uint2(0, 0);
+  GOD_DCHECK(slot < v.n_slots, "probe: directory slot");
   const uint32_t key = (uint32_t)(h & ((1ull << v.low_bits) - 1));
   const uint4 r0 = __ldg(reinterpret_cast<const uint4*>(v.dir + slot));
   const uint4 r1 = __ldg(reinterpret_cast<const uint4*>(v.dir + slot) + 1);
   const uint32_t lo = r0.x, hi = r0.y;
+  GOD_DCHECK(lo <= hi && hi <= v.n_ent, "probe: slot entry range inside the entries");
   if (hi - lo <= DIR_KEYS) {  // every key of the slot is in the record
     const uint32_t k6[DIR_KEYS] = {r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
     uint32_t below = 0, eq = 0;

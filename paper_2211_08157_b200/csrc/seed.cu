@@ -149,6 +149,7 @@ __global__ void k_anchor_write1(IndexView v, const uint64_t* __restrict__ hz, co
     const uint32_t r = (uint32_t)g;
     const uint64_t j = (uint64_t)r * p + phases[r];
     const uint64_t b = job_off[j], e = job_end[j];
+    GOD_DCHECK(b <= e, "anchor writer: job record range");
     uint64_t o = aoff[r];
     for (uint64_t q0 = b; q0 < e; q0 += RG) {  // uniform trip count within the group
       const uint64_t q = q0 + l;
@@ -163,6 +164,7 @@ __global__ void k_anchor_write1(IndexView v, const uint64_t* __restrict__ hz, co
       if (c) {
         const uint32_t bg = beg[q], qp = pos[q], qz = (uint32_t)(hz[q] >> 63);
         uint64_t oo = o + incl - c;
+        GOD_DCHECK((uint64_t)bg + c <= v.n_ent && oo + c <= aoff[n_reads], "anchor writer: entry and anchor ranges");
         for (uint32_t t2 = 0; t2 < c; t2++, oo++) {
           const uint64_t en = __ldg(v.ent + bg + t2);
           if (A16) {
@@ -305,8 +307,10 @@ __global__ void k_read_anchor_offsets(const uint64_t* __restrict__ job_off, cons
 static void probe_all(const IndexView& v, Records& rec, cudaStream_t st, Scratch& scr) {
   rec.cnt = scr.alloc<uint32_t>(rec.n);
   rec.beg = scr.alloc<uint32_t>(rec.n);
-  if (rec.n)
+  if (rec.n) {
+    prof_add_units("k_probe", rec.n);  // probes (records looked up) for the stage-4 roofline
     GOD_LAUNCH("k_probe", k_anchor_count, grid_for(rec.n, 256), 256, 0, st, v, rec.hz, rec.n, rec.cnt, rec.beg);
+  }
 }
 
 uint64_t seed_reads(const god_index* ix, const uint8_t* reads, const uint64_t* offsets, uint32_t n_reads,
