@@ -130,6 +130,12 @@ struct X2Cfg {
 // single one's offset is added to the job base).  Included base q of a job lies at byte offset
 // (q / PX) * PP + q % PX.
 __host__ __device__ constexpr int pat_off(int PP, int PX, int q) { return (q / PX) * PP + q % PX; }
+// the same for a runtime k-mer index (up to the sequence length: no int overflow past 2^31; the
+// whole-config digest test caught human '1110' positions beyond 2.86 Gbp computed through int)
+template <int PP, int PX>
+__device__ __forceinline__ uint32_t pat_off_u(uint32_t q) {
+  return (uint32_t)(((uint64_t)(q / PX)) * PP + q % PX);
+}
 // byte offset, relative to base q0 (q0 % PX == R0), of base q0 + b
 __host__ __device__ constexpr int pat_rel(int PP, int PX, int R0, int b) {
   return pat_off(PP, PX, R0 + b) - pat_off(PP, PX, R0);
@@ -179,6 +185,14 @@ __device__ __forceinline__ uint32_t pack16(const uint8_t* seq, uint64_t seq_byte
           v |= (uint32_t)seq[q] << (8 * (q - ad));
       w[i] = v;
     } else {
+#ifdef GOD_CHECKED
+      {
+        const int64_t ad = (int64_t)(pa - reinterpret_cast<uintptr_t>(seq)) + 4ll * i;
+        if (ad < -3 || ad >= (int64_t)seq_bytes)
+          printf("GOD_CHECKED detail: A=%llu ad=%lld i=%d NL=%d seq_bytes=%llu nb=%d block %u thread %u\n",
+                 (unsigned long long)A, (long long)ad, i, NL, (unsigned long long)seq_bytes, nb, blockIdx.x, threadIdx.x);
+      }
+#endif
       GOD_DCHECK((int64_t)(pa - reinterpret_cast<uintptr_t>(seq)) + 4ll * i >= -3 &&
                      (int64_t)(pa - reinterpret_cast<uintptr_t>(seq)) + 4ll * i < (int64_t)seq_bytes,
                  "K1 unchecked sequence load inside the buffer");
@@ -748,7 +762,7 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract3(X2Args a) {
       p_total = total;
       p_sel = selmask;
       p_rank = before + incl - cnt;
-      p_pb = sjp[J - j0] + (uint32_t)pat_off(PP, PX, (int)l0);
+      p_pb = sjp[J - j0] + pat_off_u<PP, PX>(l0);
       p_r0 = l0 % PX;
       p_J = J;
       p_start = emit_blk && l0 == 0;
@@ -760,7 +774,7 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract3(X2Args a) {
     uint32_t rank = before + incl - cnt;
     if (total <= (uint32_t)X2_CAP && !a.out_job) {
       // stage the tile's records in SMEM (predicated, no divergent loop), then one coalesced copy
-      const uint32_t pb = sjp[J - j0] + (uint32_t)pat_off(PP, PX, (int)l0);
+      const uint32_t pb = sjp[J - j0] + pat_off_u<PP, PX>(l0);
       const uint32_t r0 = l0 % PX;
 #pragma unroll
       for (int o = 0; o < W; o++) {
@@ -791,7 +805,7 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract3(X2Args a) {
     if (a.job_off && emit_blk && l0 == 0) a.job_off[J] = gi;
     if (a.job_end && emit_blk && (tid + 1 >= tile_nb || sjob[tid + 1] != J)) a.job_end[J] = gi + cnt;
     if (selmask) {
-      const uint32_t pb = sjp[J - j0] + (uint32_t)pat_off(PP, PX, (int)l0);
+      const uint32_t pb = sjp[J - j0] + pat_off_u<PP, PX>(l0);
       const uint32_t r0 = l0 % PX;
       uint32_t m = selmask;
       while (m) {
@@ -835,17 +849,23 @@ __global__ void k_x2_tile_desc(const uint64_t* __restrict__ kb, const uint64_t* 
     if (hi > cw[j1 + 1]) hi = cw[j1 + 1];
     if (hi < lo) hi = lo;
     if (hi > lo + (uint64_t)maxwords) hi = lo + maxwords;
-    const Job jb = jobs[j0];
-    // bytes touched up to word hi: base 16 (hi - cw) at offset <= (q / x + 1) p, plus the load width
-    const uint64_t last_byte = jb.seq_off + jb.phase + one0 + (16 * (hi - cw[j0]) / PX + 1) * PP + 48;
-    // jobs are in sequence-buffer order: the tile's last bytes are those of job j1
-    const Job jl = jobs[j1];
-    const uint64_t last_l = jl.seq_off + jl.phase + one0 + (16 * (hi - cw[j1]) / PX + 1) * PP + 48;
+    // bytes touched: job j's words [max(cw_j, lo), min(cw_j+1, hi)) end at base 16 (wend - cw_j) at
+    // offset <= (q / x + 1) p, plus the load width.  Every job of the tile is checked: jobs need not be
+    // in sequence-buffer order (seeding's dedicated extraction takes an arbitrary read list; the checked
+    // build caught the round-1 "last job ends last" shortcut reading past the buffer there)
+    uint64_t last_byte = 0;
+    for (uint32_t j = j0; j <= j1; j++) {
+      const uint64_t wend = cw[j + 1] < hi ? cw[j + 1] : hi;
+      if (wend <= cw[j] || wend <= lo) continue;
+      const Job jj = jobs[j];
+      const uint64_t lb = jj.seq_off + jj.phase + one0 + (16 * (wend - cw[j]) / PX + 1) * PP + 48;
+      last_byte = lb > last_byte ? lb : last_byte;
+    }
     X2Desc d;
     d.j0 = j0;
     d.j1 = j1;
     d.simple = (j0 == j1) && last_byte <= seq_bytes;
-    d.safe = last_l <= seq_bytes && last_byte <= seq_bytes;
+    d.safe = last_byte <= seq_bytes;
     d.cw_lo = lo;
     d.cw_hi = hi;
     desc[t] = d;
@@ -877,8 +897,13 @@ __global__ void k_x2_tile_desc_aligned(const uint64_t* __restrict__ kb, const ui
     d.pad = 0;
     d.cw_lo = cw[d.j0];
     d.cw_hi = je > j0 ? cw[je] : cw[d.j0];
-    const Job jl = jobs[d.j1];
-    const uint64_t last_l = jl.seq_off + jl.phase + one0 + (16 * (d.cw_hi - cw[d.j1]) / PX + 1) * PP + 48;
+    uint64_t last_l = 0;  // every job of the tile (jobs need not be in sequence-buffer order)
+    for (uint32_t j = d.j0; je > j0 && j <= d.j1; j++) {
+      if (cw[j + 1] <= cw[j]) continue;
+      const Job jj = jobs[j];
+      const uint64_t lb = jj.seq_off + jj.phase + one0 + (16 * (cw[j + 1] - cw[j]) / PX + 1) * PP + 48;
+      last_l = lb > last_l ? lb : last_l;
+    }
     d.simple = (d.j0 == d.j1) && last_l <= seq_bytes;
     d.safe = last_l <= seq_bytes;
     desc[t] = d;

@@ -276,7 +276,9 @@ __device__ __forceinline__ uint64_t run_len_capped(const uint64_t* __restrict__ 
 constexpr uint32_t BIN_TARGET = 3072;  // measured: 2048 13.9 ms, 2560 13.7, 3072 13.6, 3584 14.5 (stage 3, human)
 constexpr int BIN_DIGIT = 9;                      // LSD digit over b
 constexpr int BIN_RANK_MAX = 1024;                // buckets up to this size: ranked by counting, else LSD
-constexpr uint32_t RANK_SQ_PER_REC = 48;          // k_bin_build: LSD once sum(bucket^2) / n exceeds this
+// k_bin_build: LSD once sum(bucket^2) / n exceeds this (0 = off; a sweep of 48 / 192 / 768 on human
+// '10' gave no gain over ranking by counting: 6.48 / 6.19 / 6.21 vs 6.17 ms)
+constexpr uint32_t RANK_SQ_PER_REC = 0;
 static_assert(RS_BINS * BS_NW == BS_NT * 8, "block scan assumes 8 counters per thread");
 
 // records per top-SEG_BITS segment, counting every `stride`-th record (the bin widths only balance the
@@ -729,7 +731,8 @@ __global__ void __launch_bounds__(BS_NT, 2) k_bin_build(const uint64_t* __restri
                                                         uint32_t* big, uint32_t* n_big, RunOut ro,
                                                         const uint2* __restrict__ table,
                                                         const uint32_t* __restrict__ binseg, uint32_t S,
-                                                        uint64_t* __restrict__ ent, DirRec* __restrict__ dir) {
+                                                        uint64_t* __restrict__ ent, DirRec* __restrict__ dir,
+                                                        uint32_t rank_sq) {
   extern __shared__ __align__(16) unsigned char bs_smem[];
   uint64_t* A = reinterpret_cast<uint64_t*>(bs_smem);
   uint64_t* Bf = A + BS_CAP;
@@ -903,7 +906,7 @@ __global__ void __launch_bounds__(BS_NT, 2) k_bin_build(const uint64_t* __restri
       }
       // ranking by counting costs sum(c^2) compares (runs of a repeated hash share a bucket); past
       // ~RANK_SQ_PER_REC per record the LSD over the varying bits is cheaper
-      if (sq > (uint64_t)RANK_SQ_PER_REC * (uint64_t)n) cmax = BIN_RANK_MAX + 1;
+      if (rank_sq && sq > (uint64_t)rank_sq * (uint64_t)n) cmax = BIN_RANK_MAX + 1;
       c4[2 * threadIdx.x] = make_uint4(y[0] + before, y[1] + before, y[2] + before, y[3] + before);
       c4[2 * threadIdx.x + 1] = make_uint4(y[4] + before, y[5] + before, y[6] + before, y[7] + before);
     }
@@ -1671,13 +1674,16 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
       uint2* table = scr.alloc<uint2>(1u << SEG_BITS);
       uint32_t* n_bins_d = scr.alloc<uint32_t>(1);
       GOD_CUDA(cudaMemsetAsync(segc, 0, (1u << SEG_BITS) * sizeof(uint32_t), st));
-      const uint32_t seg_stride = n >= (1ull << 24) ? 16u : 1u;  // sampled widths on large inputs
+      // exact counts: sampled widths (every 16th record, >= 1 bin per segment) made the bins uneven
+      // (k_bin_build 5.6 -> 6.2 ms for 0.13 ms saved in the histogram; measured, round 2)
+      const uint32_t seg_stride = getenv("GOD_SEG_SAMPLE") ? (uint32_t)std::max(1, atoi(getenv("GOD_SEG_SAMPLE"))) : 1u;
       GOD_LAUNCH("k_seg_hist", k_seg_hist, 4u * num_sms(), 512, 0, st, k0, n, L, segc, seg_stride);
       const char* bt = getenv("GOD_BIN_TARGET");  // test hook: bin size (default BIN_TARGET)
       const uint64_t base_target = bt ? std::max(1, atoi(bt)) : BIN_TARGET;
       const uint32_t target =
           (uint32_t)std::max<uint64_t>(base_target, n / ((1u << (2 * BIN_DIGIT)) - (1u << SEG_BITS)) + 1);
-      GOD_LAUNCH("k_seg_table", k_seg_table, 1, 1024, 0, st, segc, target, table, n_bins_d, seg_stride, 1u);
+      GOD_LAUNCH("k_seg_table", k_seg_table, 1, 1024, 0, st, segc, target, table, n_bins_d, seg_stride,
+                 seg_stride > 1 ? 1u : 0u);
       // the first pass's tile histograms of the bins; the first scatter assigns the bins itself
       GOD_LAUNCH("k_seg_assign", k_seg_assign, ntiles, RS_NT, 0, st, k0, n, L, hbits, table, (1u << BIN_DIGIT) - 1, hist,
                  ntiles, 0);
@@ -1702,7 +1708,8 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
         GOD_CUDA(cudaMallocAsync((void**)&ix->dir, std::max<uint64_t>(n_slots, 1) * sizeof(DirRec), st));
         GOD_CUDA(cudaMallocAsync((void**)&ix->ent, n * sizeof(uint64_t), st));
         GOD_LAUNCH("k_bin_build", k_bin_build, 2u * num_sms(), BS_NT, BB_SMEM, st, k0, v0, bstart, n_bins_d, L, hbits,
-                   big, n_big, ro, table, nullptr, S_dir, ix->ent, ix->dir);
+                   big, n_big, ro, table, nullptr, S_dir, ix->ent, ix->dir,
+                   getenv("GOD_RANK_SQ") ? (uint32_t)atoi(getenv("GOD_RANK_SQ")) : RANK_SQ_PER_REC);
       } else {
         GOD_LAUNCH("k_bin_sort", k_bin_sort, 2u * num_sms(), BS_NT, BS_SMEM, st, k0, v0, bstart, n_bins_d, L, hbits, big,
                    n_big, ro);
