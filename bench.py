@@ -273,11 +273,13 @@ def pick_roofline(prof: dict, ctx: dict, peaks: dict, units: dict, steps: int):
         sec = tr.get("l2_read_sectors")
         st4 = {"kernel": "k_probe", "ms": round(t, 4), "probes": int(probes), "probes_per_s": round(probes / t * 1e3, 1),
                "g0_random_gather_sectors_per_s": G0_RANDOM_GATHER}
+        # each probe is one dependent random 32-B directory read (plus streaming record I/O): its
+        # ceiling is G0's random 32-B gather rate over a buffer of the directory's size (4.2 GB here)
+        st4["frac_of_g0_4gb_gather"] = round(probes / t * 1e3 / G0_RANDOM_GATHER["4GB"], 3)
         if sec:
-            sps = sec / (tr.get("ncu_ms_per_launch") or t) * 1e3
-            st4.update({"l2_read_sectors_per_probe": round(sec / probes, 2), "sectors_per_s_in_bench": round(sec / t * 1e3, 1),
-                        "frac_of_g0_4gb_gather": round(sec / t * 1e3 / G0_RANDOM_GATHER["4GB"], 3),
+            st4.update({"l2_read_sectors_per_probe": round(sec / probes, 2),
                         "dram_bytes_per_probe": round(tr["dram_bytes_per_launch"] / probes, 1),
+                        "algorithmic_bytes_per_probe": 32 + 8 + 8,  # directory sector + record in + (count, first) out
                         "l2_hit_rate_pct": tr.get("l2_hit_rate_pct"), "source": tr.get("file")})
         if "k_anchor_write" in prof:
             ta = ms_of("k_anchor_write")

@@ -276,9 +276,6 @@ __device__ __forceinline__ uint64_t run_len_capped(const uint64_t* __restrict__ 
 constexpr uint32_t BIN_TARGET = 3072;  // measured: 2048 13.9 ms, 2560 13.7, 3072 13.6, 3584 14.5 (stage 3, human)
 constexpr int BIN_DIGIT = 9;                      // LSD digit over b
 constexpr int BIN_RANK_MAX = 1024;                // buckets up to this size: ranked by counting, else LSD
-// k_bin_build: LSD once sum(bucket^2) / n exceeds this (0 = off; a sweep of 48 / 192 / 768 on human
-// '10' gave no gain over ranking by counting: 6.48 / 6.19 / 6.21 vs 6.17 ms)
-constexpr uint32_t RANK_SQ_PER_REC = 0;
 static_assert(RS_BINS * BS_NW == BS_NT * 8, "block scan assumes 8 counters per thread");
 
 // records per top-SEG_BITS segment, counting every `stride`-th record (the bin widths only balance the
@@ -731,8 +728,7 @@ __global__ void __launch_bounds__(BS_NT, 2) k_bin_build(const uint64_t* __restri
                                                         uint32_t* big, uint32_t* n_big, RunOut ro,
                                                         const uint2* __restrict__ table,
                                                         const uint32_t* __restrict__ binseg, uint32_t S,
-                                                        uint64_t* __restrict__ ent, DirRec* __restrict__ dir,
-                                                        uint32_t rank_sq) {
+                                                        uint64_t* __restrict__ ent, DirRec* __restrict__ dir) {
   extern __shared__ __align__(16) unsigned char bs_smem[];
   uint64_t* A = reinterpret_cast<uint64_t*>(bs_smem);
   uint64_t* Bf = A + BS_CAP;
@@ -871,15 +867,8 @@ __global__ void __launch_bounds__(BS_NT, 2) k_bin_build(const uint64_t* __restri
       const uint4 p0 = c4[2 * threadIdx.x], p1 = c4[2 * threadIdx.x + 1];
       uint32_t y[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
       uint32_t tsum = 0, tmax = 0;
-      uint64_t tsq = 0;  // sum of squared bucket sizes: the cost of ranking by counting
 #pragma unroll
-      for (int q = 0; q < 8; q++) {
-        const uint32_t c2 = y[q];
-        y[q] = tsum;
-        tsum += c2;
-        tmax = max(tmax, c2);
-        tsq += (uint64_t)c2 * c2;
-      }
+      for (int q = 0; q < 8; q++) { const uint32_t c2 = y[q]; y[q] = tsum; tsum += c2; tmax = max(tmax, c2); }
       uint32_t incl = tsum;
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
@@ -887,26 +876,14 @@ __global__ void __launch_bounds__(BS_NT, 2) k_bin_build(const uint64_t* __restri
         if (lane >= d) incl += t2;
       }
 #pragma unroll
-      for (int d = 16; d; d >>= 1) {
-        tmax = max(tmax, __shfl_xor_sync(0xffffffffu, tmax, d));
-        tsq += __shfl_xor_sync(0xffffffffu, tsq, d);
-      }
-      if (lane == 0) s_vo[wid] = tsq;
+      for (int d = 16; d; d >>= 1) tmax = max(tmax, __shfl_xor_sync(0xffffffffu, tmax, d));
       if (lane == 31) wsum[wid] = incl;
       if (lane == 0) s_or[wid] = tmax;
       __syncthreads();
       uint32_t before = incl - tsum;
       cmax = 0;
-      uint64_t sq = 0;
 #pragma unroll
-      for (int q = 0; q < BS_NW; q++) {
-        before += q < wid ? wsum[q] : 0u;
-        cmax = max(cmax, s_or[q]);
-        sq += s_vo[q];
-      }
-      // ranking by counting costs sum(c^2) compares (runs of a repeated hash share a bucket); past
-      // ~RANK_SQ_PER_REC per record the LSD over the varying bits is cheaper
-      if (rank_sq && sq > (uint64_t)rank_sq * (uint64_t)n) cmax = BIN_RANK_MAX + 1;
+      for (int q = 0; q < BS_NW; q++) { before += q < wid ? wsum[q] : 0u; cmax = max(cmax, s_or[q]); }
       c4[2 * threadIdx.x] = make_uint4(y[0] + before, y[1] + before, y[2] + before, y[3] + before);
       c4[2 * threadIdx.x + 1] = make_uint4(y[4] + before, y[5] + before, y[6] + before, y[7] + before);
     }
@@ -1708,8 +1685,7 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
         GOD_CUDA(cudaMallocAsync((void**)&ix->dir, std::max<uint64_t>(n_slots, 1) * sizeof(DirRec), st));
         GOD_CUDA(cudaMallocAsync((void**)&ix->ent, n * sizeof(uint64_t), st));
         GOD_LAUNCH("k_bin_build", k_bin_build, 2u * num_sms(), BS_NT, BB_SMEM, st, k0, v0, bstart, n_bins_d, L, hbits,
-                   big, n_big, ro, table, nullptr, S_dir, ix->ent, ix->dir,
-                   getenv("GOD_RANK_SQ") ? (uint32_t)atoi(getenv("GOD_RANK_SQ")) : RANK_SQ_PER_REC);
+                   big, n_big, ro, table, nullptr, S_dir, ix->ent, ix->dir);
       } else {
         GOD_LAUNCH("k_bin_sort", k_bin_sort, 2u * num_sms(), BS_NT, BS_SMEM, st, k0, v0, bstart, n_bins_d, L, hbits, big,
                    n_big, ro);
