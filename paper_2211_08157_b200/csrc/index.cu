@@ -902,8 +902,13 @@ __global__ void __launch_bounds__(BS_NT, 2) k_bin_build(const uint64_t* __restri
         const uint64_t xv = A[p];
         const uint32_t b2 = ((uint32_t)(xv >> 33) - mn) >> shb;
         const int st = b2 ? (int)cnt[b2 - 1] : 0, en = (int)cnt[b2];
-        int rank = 0;
-        for (int q = st; q < en; q++) rank += A[q] < xv;
+        int rank = 0, q = st;
+        if (q & 1) rank += A[q++] < xv;  // then two keys per 128-bit SMEM load
+        for (; q + 1 < en; q += 2) {
+          const ulonglong2 two = *reinterpret_cast<const ulonglong2*>(A + q);
+          rank += (two.x < xv) + (two.y < xv);
+        }
+        if (q < en) rank += A[q] < xv;
         Bf[st + rank] = xv;
       }
       __syncthreads();
@@ -916,53 +921,16 @@ __global__ void __launch_bounds__(BS_NT, 2) k_bin_build(const uint64_t* __restri
       res = lsd_varying(33 + hib);
     }
     }  // !one
-    // K3 fused: runs never cross a bin (a hash lies in one bin).  Per-element run length from two
-    // block scans over the run-head indices (start = last head <= i, end = first head > i); it is
-    // stored in the key's free bits (capped) for the kept-entry pass, and heads record it in the
-    // count histogram.
-    uint32_t* Lsm = reinterpret_cast<uint32_t*>(res == A ? Bf : A);
+    // K3 fused: runs never cross a bin (a hash lies in one bin).  Run heads mark NH[i] = i, a block
+    // suffix minimum gives every i the next head >= i, and a head's run length is NH[i + 1] - i.
+    uint32_t* NH = reinterpret_cast<uint32_t*>(res == A ? Bf : A);  // [n + 1] (the non-result buffer)
     if (!one) {
-      // warp w owns items [w*256, w*256+256) as 8 rows of 32 (conflict-free SMEM access)
-      const int wbase = wid * (32 * BS_IPT);
-      uint32_t hm[BS_IPT];
-      int wl = -1, wf = n;  // this warp's last / first head
-#pragma unroll
-      for (int q = 0; q < BS_IPT; q++) {
-        const int idx = wbase + q * 32 + lane;
-        bool h = false;
-        if (idx < n) h = idx == 0 || (uint32_t)(res[idx - 1] >> 33) != (uint32_t)(res[idx] >> 33);
-        hm[q] = __ballot_sync(0xffffffffu, h);
-        if (hm[q]) {
-          wl = wbase + q * 32 + 31 - __clz(hm[q]);
-          if (wf == n) wf = wbase + q * 32 + __ffs(hm[q]) - 1;
-        }
-      }
-      if (lane == 0) { s_or[wid] = (uint32_t)(wl + 1); s_and[wid] = (uint32_t)wf; }
+      for (int i = threadIdx.x; i < n; i += BS_NT)
+        NH[i] = (i == 0 || (uint32_t)(res[i - 1] >> 33) != (uint32_t)(res[i] >> 33)) ? (uint32_t)i : (uint32_t)n;
+      if (threadIdx.x == 0) NH[n] = (uint32_t)n;
       __syncthreads();
-      int carry = -1, after = n;
-#pragma unroll
-      for (int q = 0; q < BS_NW; q++) {
-        if (q < wid) carry = max(carry, (int)s_or[q] - 1);
-        if (q > wid) after = min(after, (int)s_and[q]);
-      }
-      const uint32_t le = (lane == 31) ? 0xffffffffu : ((2u << lane) - 1);  // lanes <= lane
-      int st_[BS_IPT];
-#pragma unroll
-      for (int q = 0; q < BS_IPT; q++) {  // start = last head <= idx
-        const uint32_t m = hm[q] & le;
-        st_[q] = m ? wbase + q * 32 + 31 - __clz(m) : carry;
-        if (hm[q]) carry = wbase + q * 32 + 31 - __clz(hm[q]);
-      }
-#pragma unroll
-      for (int q = BS_IPT - 1; q >= 0; q--) {  // next head > idx
-        const uint32_t m = hm[q] & ~le;
-        const int nh = m ? wbase + q * 32 + __ffs(m) - 1 : after;
-        const int idx = wbase + q * 32 + lane;
-        if (idx < n) Lsm[idx] = (uint32_t)(nh - st_[q]);
-        if (hm[q]) after = wbase + q * 32 + __ffs(hm[q]) - 1;
-      }
+      suffix_min_block(NH, (uint32_t)n + 1, wsum);
     }
-    __syncthreads();
     // K5 + K6 fused: entries in final position (all of them: a hash with count > tau is dropped at
     // probe time, reading O7), then the bin's S directory slots (bins are unions of whole slots)
     const uint2 tb = table[segv];                  // (first bin, bins) of the bin's segment
@@ -979,7 +947,7 @@ __global__ void __launch_bounds__(BS_NT, 2) k_bin_build(const uint64_t* __restri
       if (one) {
         if (i == 0) run_emit(ro, rh, (uint64_t)n, racc);
       } else if (head) {
-        run_emit(ro, rh, Lsm[i], racc);
+        run_emit(ro, rh, NH[i + 1] - (uint32_t)i, racc);
       }
       if (head) {  // a slot starts at a run head: its first record
         const uint32_t q = (uint32_t)((((uint64_t)lo * slots_t) >> L) - qbase);
