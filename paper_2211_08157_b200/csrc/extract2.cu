@@ -119,7 +119,7 @@ struct X2Cfg {
   static constexpr size_t O_NMASK = O_CODES + (size_t)MAXWORDS * 4;
   static constexpr size_t O_XCHG = O_NMASK + (size_t)MAXWORDS * 4;
   static constexpr size_t O_STG = (O_XCHG + 2 * (X2_NT / 32) * W * 4 + 15) / 16 * 16;  // [X2_CAP] hz + pos
-  static constexpr size_t O_HZ = O_STG + (size_t)X2_CAP * 12;                                 // [NHZ][POS] hz
+  static constexpr size_t O_HZ = O_STG + (size_t)X2_CAP * 2;                                  // [NHZ][POS] hz
   // ordered output keeps the previous tile's hashes until its look-back resolves (2 buffers)
   static constexpr size_t smem(bool ordered) { return (O_HZ + (ordered ? 2 : 1) * (size_t)POS * 8 + 15) / 16 * 16; }
 };
@@ -384,9 +384,10 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract3(X2Args a) {
   uint32_t* xsf = xpf + NWARP * W;
   uint64_t* const HZ0 = reinterpret_cast<uint64_t*>(x2_smem + C::O_HZ);  // [NHZ][POS] hash | strand << 63
   uint64_t* HZ = HZ0;
-  // unordered output: the tile's selected records staged in position order before one coalesced copy
-  uint64_t* SHZ = reinterpret_cast<uint64_t*>(x2_smem + C::O_STG);              // [X2_CAP]
-  uint32_t* SPOS = reinterpret_cast<uint32_t*>(x2_smem + C::O_STG + X2_CAP * 8);  // [X2_CAP]
+  // unordered output: the tile's selected positions (tile-local index) staged in position order
+  uint16_t* SIDX = reinterpret_cast<uint16_t*>(x2_smem + C::O_STG);  // [X2_CAP]
+  __shared__ uint32_t SBASE[X2_NT];  // per block: output position of its first k-mer start
+  __shared__ uint8_t SR0[X2_NT];     // per block: its first k-mer index mod x
   __shared__ X2Tile T;
   __shared__ uint64_t skb[X2_NT + 2], scw[X2_NT + 2];
   __shared__ uint64_t sjb[X2_NT + 2];  // per job of the tile: byte address of its first patterned base
@@ -651,10 +652,8 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract3(X2Args a) {
         const bool s = (k == mm) && k != 0u;
         need_slow |= (k != 0u) & (mm == 0u);  // a run shorter than w: partial-window rule
         tie |= s & (k == prevk);
-        if (s) {
-          selmask |= 1u << o;
-          prevk = k;
-        }
+        selmask |= (uint32_t)s << o;
+        prevk = s ? k : prevk;
       }
       // tie check, part 2: the first selected position against the previous block's last one when they
       // are closer than w (offset in this block < offset in the previous block)
@@ -773,17 +772,17 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract3(X2Args a) {
     if (tid == 0) s_base = atomicAdd(reinterpret_cast<unsigned long long*>(a.total_out), (unsigned long long)total);
     uint32_t rank = before + incl - cnt;
     if (total <= (uint32_t)X2_CAP && !a.out_job) {
-      // stage the tile's records in SMEM (predicated, no divergent loop), then one coalesced copy
-      const uint32_t pb = sjp[J - j0] + pat_off_u<PP, PX>(l0);
-      const uint32_t r0 = l0 % PX;
-#pragma unroll
-      for (int o = 0; o < W; o++) {
-        if ((selmask >> o) & 1u) {
-          GOD_DCHECK(rank < (uint32_t)X2_CAP, "K1 staging index");
-          SHZ[rank] = HZ[tid * W + o];
-          SPOS[rank] = pb + pat_delta<PP, PX>(r0, (uint32_t)o);
-          ++rank;
-        }
+      // stage the tile-local indices of the selected positions (u16, position order), then one
+      // coalesced copy that reads each record's hash from HZ and computes its position from its
+      // block's base (a predicated staging of full records cost ~13 slots per position, measured)
+      SBASE[tid] = sjp[J - j0] + pat_off_u<PP, PX>(l0);
+      if (PX > 1) SR0[tid] = (uint8_t)(l0 % PX);
+      uint32_t m = selmask;
+      while (m) {
+        const int i = __ffs(m) - 1;
+        m &= m - 1;
+        GOD_DCHECK(rank < (uint32_t)X2_CAP, "K1 staging index");
+        SIDX[rank++] = (uint16_t)(tid * W + i);
       }
       __syncthreads();
       const uint64_t base = s_base;
@@ -794,8 +793,9 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract3(X2Args a) {
       for (uint32_t r = tid; r < total; r += X2_NT) {
         const uint64_t gi = base + r;
         if (gi < a.cap) {
-          a.out_hz[gi] = SHZ[r];
-          a.out_pos[gi] = SPOS[r];
+          const uint32_t e = SIDX[r], blk = e / W, o = e - blk * W;
+          a.out_hz[gi] = HZ[e];
+          a.out_pos[gi] = SBASE[blk] + pat_delta<PP, PX>(PX > 1 ? SR0[blk] : 0u, o);
         }
       }
       continue;
