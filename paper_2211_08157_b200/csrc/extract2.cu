@@ -69,6 +69,7 @@ struct X2Args {
   const struct X2Desc* desc;  // [ntiles] per-tile descriptors (k_x2_tile_desc)
   uint32_t aligned;     // tiles are whole jobs (k_x2_tile_desc_aligned): no halo blocks
   uint64_t ntiles;
+  uint32_t no_stage;    // developer toggle (GOD_X2_NO_STAGE): direct global loads in the sparsify stage
 };
 
 __device__ __forceinline__ uint32_t find_job_le(const uint64_t* arr, uint32_t lo, uint32_t hi, uint64_t g) {
@@ -97,12 +98,41 @@ struct __align__(16) X2Desc {
   uint32_t j0, j1, simple, safe;  // safe: every byte the tile may read is inside the buffer
   uint64_t cw_lo, cw_hi;
   uint64_t b0;                    // aligned tiles: first block (thread 0's), and the block count
-  uint32_t nb, pad;
+  uint32_t nb, raw_len;           // raw_len: bytes a bulk copy stages for the tile (0: direct loads)
+  uint64_t raw_lo;                // ... from this 16-B aligned global address
+  uint64_t pad;
 };
+// bytes of the SMEM buffer the next tile's ASCII bytes are staged into (unordered K1)
+constexpr uint32_t X2_RAW_CAP = 6144;
+// the byte span [lo, hi) one job's code words [ws, we) load from (pack16: words aligned in the address
+// space, pack_words of them from each word's first byte)
+__device__ __forceinline__ void job_byte_span(uint64_t base, uint64_t ws, uint64_t we, int PP, int PX, int NL,
+                                              uint64_t& lo, uint64_t& hi) {
+  const uint64_t q0 = 16 * ws, q1 = 16 * (we - 1);
+  lo = base + (q0 / PX) * PP + q0 % PX;
+  hi = ((base + (q1 / PX) * PP + q1 % PX) & ~3ull) + 4ull * NL;
+}
+__device__ __forceinline__ int pack_words_rt(int PP, int PX) {
+  int mx = 0;
+  for (int r = 0; r < PX; r++) {
+    const int q = r + 15;
+    const int v = ((q / PX) * PP + q % PX) - ((r / PX) * PP + r % PX);
+    mx = v > mx ? v : mx;
+  }
+  return (mx + 3) / 4 + 2;
+}
+// the tile's staged span if it fits X2_RAW_CAP and lies inside [seq, seq + seq_bytes) after 16-B alignment
+__device__ __forceinline__ void raw_span(const uint8_t* seq, uint64_t seq_bytes, uint64_t lo, uint64_t hi,
+                                         uint64_t& raw_lo, uint32_t& raw_len) {
+  const uint64_t s0 = reinterpret_cast<uintptr_t>(seq);
+  const uint64_t a = (s0 + lo) & ~15ull, b = (s0 + hi + 15) & ~15ull;
+  raw_lo = a;
+  raw_len = (a >= s0 && b <= s0 + seq_bytes && b - a <= X2_RAW_CAP && hi > lo) ? (uint32_t)(b - a) : 0u;
+}
 
 struct X2Tile {  // per-tile scalars, in SMEM
-  uint32_t tile, j0, j1, simple, safe, slow, nb;
-  uint64_t cw_lo, cw_hi, b0;
+  uint32_t tile, j0, j1, simple, safe, slow, nb, raw_len;
+  uint64_t cw_lo, cw_hi, b0, raw_lo;
 };
 
 template <int K, int W, int PP, int PX>
@@ -117,11 +147,16 @@ struct X2Cfg {
   static constexpr size_t O_LUT = 0;
   static constexpr size_t O_CODES = O_LUT + 256 * 4;
   static constexpr size_t O_NMASK = O_CODES + (size_t)MAXWORDS * 4;
-  static constexpr size_t O_XCHG = O_NMASK + (size_t)MAXWORDS * 4;
-  static constexpr size_t O_STG = (O_XCHG + 2 * (X2_NT / 32) * W * 4 + 15) / 16 * 16;  // [X2_CAP] hz + pos
+  static constexpr int WP = (W + 3) / 4 * 4;  // exchange row (16-B vectors)
+  static constexpr size_t O_XCHG = (O_NMASK + (size_t)MAXWORDS * 4 + 15) / 16 * 16;
+  static constexpr size_t O_STG = (O_XCHG + 2 * (X2_NT / 32) * WP * 4 + 15) / 16 * 16;  // [X2_CAP] indices
   static constexpr size_t O_HZ = O_STG + (size_t)X2_CAP * 2;                                  // [NHZ][POS] hz
   // ordered output keeps the previous tile's hashes until its look-back resolves (2 buffers)
-  static constexpr size_t smem(bool ordered) { return (O_HZ + (ordered ? 2 : 1) * (size_t)POS * 8 + 15) / 16 * 16; }
+  // unordered: one HZ buffer + the raw-byte staging buffer of the next tile; ordered: two HZ buffers
+  static constexpr size_t O_RAW = O_HZ + (size_t)POS * 8;
+  static constexpr size_t smem(bool ordered) {
+    return ((ordered ? O_HZ + 2 * (size_t)POS * 8 : O_RAW + X2_RAW_CAP) + 15) / 16 * 16;
+  }
 };
 
 // (pack16 gathers the included bytes with compile-time byte-permutations)
@@ -162,9 +197,12 @@ constexpr int pack_off(int i) {
 
 // 16 patterned bases (MSB-first 2-bit codes) from the ASCII bytes, base 0 at byte A (its job-relative
 // index has residue R0 mod PX); *nm gets the N bits (bit 15 - b for base b).  nb = bases that exist.
-template <int PP, int PX, int R0, bool CHECKED>
+// SMEM: the tile's bytes were staged by a bulk copy into sm (its first byte is the global address
+// sm_base, 16-B aligned); the same aligned words are read from there
+template <int PP, int PX, int R0, bool CHECKED, bool SMEM = false>
 __device__ __forceinline__ uint32_t pack16(const uint8_t* seq, uint64_t seq_bytes, uint64_t A, int nb,
-                                           const uint32_t* lut, uint32_t* nm) {
+                                           const uint32_t* lut, uint32_t* nm, const uint32_t* sm = nullptr,
+                                           uintptr_t sm_base = 0) {
   // words aligned in the ADDRESS space (the caller's buffer may start anywhere, e.g. a tensor slice);
   // the first word may begin up to 3 bytes before byte A (inside the allocation: allocations are
   // aligned), and the tile descriptor's end margin covers the last one
@@ -176,7 +214,9 @@ __device__ __forceinline__ uint32_t pack16(const uint8_t* seq, uint64_t seq_byte
   const uint32_t* src = reinterpret_cast<const uint32_t*>(pa);
 #pragma unroll
   for (int i = 0; i < NL; i++) {
-    if constexpr (CHECKED) {
+    if constexpr (SMEM) {
+      w[i] = sm[(pa - sm_base) / 4 + i];
+    } else if constexpr (CHECKED) {
       const int64_t ad = (int64_t)(pa - reinterpret_cast<uintptr_t>(seq)) + 4ll * i;  // relative to seq
       uint32_t v = 0;
       if (ad >= 0 && (uint64_t)ad + 4 <= seq_bytes) v = __ldg(src + i);
@@ -243,21 +283,22 @@ __device__ __forceinline__ uint32_t pack16(const uint8_t* seq, uint64_t seq_byte
 }
 
 // code word at job-relative base q0 (a multiple of 16) of the job whose base 0 is byte A0
-template <int PP, int PX, bool CHECKED>
+template <int PP, int PX, bool CHECKED, bool SMEM = false>
 __device__ __forceinline__ uint32_t pack_word(const uint8_t* seq, uint64_t seq_bytes, uint64_t A0, uint64_t q0, int nb,
-                                              const uint32_t* lut, uint32_t* nm) {
+                                              const uint32_t* lut, uint32_t* nm, const uint32_t* sm = nullptr,
+                                              uintptr_t sm_base = 0) {
   const uint32_t r0 = (uint32_t)(q0 % PX);
   const uint64_t A = A0 + (q0 / PX) * PP + r0;
   if constexpr (PX == 1) {
-    return pack16<PP, PX, 0, CHECKED>(seq, seq_bytes, A, nb, lut, nm);
+    return pack16<PP, PX, 0, CHECKED, SMEM>(seq, seq_bytes, A, nb, lut, nm, sm, sm_base);
   } else if constexpr (PX == 2) {
-    return r0 ? pack16<PP, PX, 1, CHECKED>(seq, seq_bytes, A, nb, lut, nm)
-              : pack16<PP, PX, 0, CHECKED>(seq, seq_bytes, A, nb, lut, nm);
+    return r0 ? pack16<PP, PX, 1, CHECKED, SMEM>(seq, seq_bytes, A, nb, lut, nm, sm, sm_base)
+              : pack16<PP, PX, 0, CHECKED, SMEM>(seq, seq_bytes, A, nb, lut, nm, sm, sm_base);
   } else {
     static_assert(PX == 3, "patterns with up to 3 leading ones");
-    return r0 == 0 ? pack16<PP, PX, 0, CHECKED>(seq, seq_bytes, A, nb, lut, nm)
-         : r0 == 1 ? pack16<PP, PX, 1, CHECKED>(seq, seq_bytes, A, nb, lut, nm)
-                   : pack16<PP, PX, 2, CHECKED>(seq, seq_bytes, A, nb, lut, nm);
+    return r0 == 0 ? pack16<PP, PX, 0, CHECKED, SMEM>(seq, seq_bytes, A, nb, lut, nm, sm, sm_base)
+         : r0 == 1 ? pack16<PP, PX, 1, CHECKED, SMEM>(seq, seq_bytes, A, nb, lut, nm, sm, sm_base)
+                   : pack16<PP, PX, 2, CHECKED, SMEM>(seq, seq_bytes, A, nb, lut, nm, sm, sm_base);
   }
 }
 // original-coordinate distance from base q to base q + i, with r = q % PX
@@ -381,8 +422,52 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract3(X2Args a) {
   uint32_t* codes = reinterpret_cast<uint32_t*>(x2_smem + C::O_CODES);
   uint32_t* nmask = reinterpret_cast<uint32_t*>(x2_smem + C::O_NMASK);
   uint32_t* xpf = reinterpret_cast<uint32_t*>(x2_smem + C::O_XCHG);
-  uint32_t* xsf = xpf + NWARP * W;
+  uint32_t* xsf = xpf + NWARP * C::WP;
+  // a warp's boundary values go through SMEM as 16-B vectors (W scalar stores/loads per value set cost
+  // ~6 slots per position, measured)
+  auto put_row = [&](uint32_t* row, const uint32_t (&v)[W]) {
+#pragma unroll
+    for (int j = 0; j < C::WP / 4; j++)
+      reinterpret_cast<uint4*>(row)[j] = make_uint4(v[4 * j], 4 * j + 1 < W ? v[4 * j + 1] : 0u,
+                                                    4 * j + 2 < W ? v[4 * j + 2] : 0u, 4 * j + 3 < W ? v[4 * j + 3] : 0u);
+  };
+  auto get_row = [&](const uint32_t* row, uint32_t (&v)[W]) {
+#pragma unroll
+    for (int j = 0; j < C::WP / 4; j++) {
+      const uint4 q = reinterpret_cast<const uint4*>(row)[j];
+      v[4 * j] = q.x;
+      if (4 * j + 1 < W) v[4 * j + 1] = q.y;
+      if (4 * j + 2 < W) v[4 * j + 2] = q.z;
+      if (4 * j + 3 < W) v[4 * j + 3] = q.w;
+    }
+  };
   uint64_t* const HZ0 = reinterpret_cast<uint64_t*>(x2_smem + C::O_HZ);  // [NHZ][POS] hash | strand << 63
+  // Unordered: thread 0 stages the NEXT tile's ASCII bytes into raw[] by one bulk copy (cp.async.bulk,
+  // completion on an mbarrier) while this tile computes, so the sparsify stage reads SMEM, not global
+  // memory, on its critical path.
+  const uint32_t* raw = reinterpret_cast<const uint32_t*>(x2_smem + C::O_RAW);
+  __shared__ __align__(8) uint64_t s_mbar;
+  const uint32_t mbar = (uint32_t)__cvta_generic_to_shared(&s_mbar);
+  uint32_t raw_phase = 0;
+  auto raw_issue = [&](const X2Desc& d) {  // thread 0
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the previous tile's generic reads of raw[]
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(d.raw_len) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(raw)),
+                 "l"(d.raw_lo), "r"(d.raw_len), "r"(mbar)
+                 : "memory");
+  };
+  auto raw_wait = [&]() {  // every thread
+    uint32_t done = 0;
+    do {
+      asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                   : "=r"(done)
+                   : "r"(mbar), "r"(raw_phase)
+                   : "memory");
+    } while (!done);
+    raw_phase ^= 1u;
+  };
+
   uint64_t* HZ = HZ0;
   // unordered output: the tile's selected positions (tile-local index) staged in position order
   uint16_t* SIDX = reinterpret_cast<uint16_t*>(x2_smem + C::O_STG);  // [X2_CAP]
@@ -402,6 +487,10 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract3(X2Args a) {
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const uint64_t ntiles = a.ntiles;
+  if (!ORDERED && tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   const uint32_t ks = a.key_shift;  // <= 31
   {  // expected-letter table: for 4 MSB-first codes pk, bytes "ACGT"[c_i], base 0 in byte 0
     const uint32_t L4 = 0x54474341u;
@@ -419,7 +508,10 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract3(X2Args a) {
   X2Desc nd{};
   if (!ORDERED && tid == 0) {
     next_t = atomicAdd(a.tile_ctr, 1u);
-    if (next_t < ntiles) nd = a.desc[next_t];
+    if (next_t < ntiles) {
+      nd = a.desc[next_t];
+      if (nd.raw_len && !a.no_stage) raw_issue(nd);
+    }
   }
   // ORDERED: the previous tile's records, written one iteration late so that its look-back finds the
   // predecessors' counts published instead of spinning on tiles that other CTAs are still computing
@@ -464,6 +556,8 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract3(X2Args a) {
         T.slow = 0;
         T.b0 = nd.b0;
         T.nb = nd.nb;
+        T.raw_len = (!ORDERED && !a.no_stage) ? nd.raw_len : 0u;
+        T.raw_lo = nd.raw_lo;
         if (!ORDERED) {
           next_t = atomicAdd(a.tile_ctr, 1u);
           if (next_t < ntiles) nd = a.desc[next_t];
@@ -501,7 +595,24 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract3(X2Args a) {
     }
     // ------------------------------------------------------------------ A. sparsify into SMEM
     uint32_t my_n = 0;
-    if (simple) {
+    const bool staged = T.raw_len != 0;
+    const uintptr_t raw_lo = (uintptr_t)T.raw_lo;
+    if (staged) raw_wait();
+    if (staged) {
+      for (int wi = tid; wi < nwords; wi += X2_NT) {
+        const uint32_t Jw = simple ? 0u : swj[wi];
+        const uint64_t nkq = sjn[Jw];
+        const uint64_t ncode = nkq ? nkq + K - 1 : 0;
+        const uint64_t q0 = (cw_lo + wi - scw[Jw]) * 16;
+        uint32_t nm = 0, word = 0;
+        if (q0 < ncode)
+          word = pack_word<PP, PX, false, true>(a.seq, a.seq_bytes, sjb[Jw], q0, (int)min((uint64_t)16, ncode - q0),
+                                                lut, &nm, raw, raw_lo);
+        codes[wi] = word;
+        nmask[wi] = nm;
+        my_n |= nm;
+      }
+    } else if (simple) {
       const uint64_t w0 = cw_lo - scw[0];
       const uint32_t ncode = sjn[0] ? sjn[0] + K - 1 : 0;
       const uint64_t A0 = sjb[0];
@@ -533,6 +644,8 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract3(X2Args a) {
       }
     }
     const bool any_n = __syncthreads_or(my_n != 0);
+    // raw[] is free again: stage the next tile (claimed one ahead) while this one computes
+    if (!ORDERED && tid == 0 && next_t < ntiles && nd.raw_len && !a.no_stage) raw_issue(nd);
 
     // ---- my block: job J, first k-mer index l0
     // aligned tiles: blocks b0 .. b0 + nb - 1 (whole jobs, job boundaries are window barriers, no halo);
@@ -603,16 +716,19 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract3(X2Args a) {
 #pragma unroll
       for (int i = W - 2; i >= 0; i--) SF[i] = min(SF[i + 1], key[i]);
       if (lane == 0) {
-#pragma unroll
-        for (int i = 0; i < W; i++) xpf[wid * W + i] = PF[i];
+        put_row(xpf + wid * C::WP, PF);
       }
       __syncthreads();
       uint32_t nPF[W];
 #pragma unroll
       for (int i = 0; i < W; i++) nPF[i] = __shfl_down_sync(0xffffffffu, PF[i], 1);
       if (lane == 31) {
+        if (wid < NWARP - 1) {
+          get_row(xpf + (wid + 1) * C::WP, nPF);
+        } else {
 #pragma unroll
-        for (int i = 0; i < W; i++) nPF[i] = (wid < NWARP - 1) ? xpf[(wid + 1) * W + i] : 0u;
+          for (int q = 0; q < W; q++) nPF[q] = 0u;
+        }
       }
       // the next block starting another job: no window crosses into it (a job boundary is a barrier)
       if (tid + 1 < X2_NT && sjob[tid + 1] != J) {
@@ -631,8 +747,7 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract3(X2Args a) {
 #pragma unroll
       for (int i = W - 2; i >= 0; i--) SX[i] = max(SX[i + 1], WM[i]);
       if (lane == 31) {
-#pragma unroll
-        for (int i = 0; i < W; i++) xsf[wid * W + i] = SX[i];
+        put_row(xsf + wid * C::WP, SX);
       }
       uint32_t pSX[W];
 #pragma unroll
@@ -642,8 +757,12 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract3(X2Args a) {
       uint32_t prevk = 0;
       __syncthreads();
       if (lane == 0) {
+        if (wid > 0) {
+          get_row(xsf + (wid - 1) * C::WP, pSX);
+        } else {
 #pragma unroll
-        for (int i = 0; i < W; i++) pSX[i] = (wid > 0) ? xsf[(wid - 1) * W + i] : 0u;
+          for (int q = 0; q < W; q++) pSX[q] = 0u;
+        }
       }
 #pragma unroll
       for (int o = 0; o < W; o++) {
@@ -834,7 +953,8 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract3(X2Args a) {
 __global__ void k_x2_tile_desc(const uint64_t* __restrict__ kb, const uint64_t* __restrict__ cw,
                                const Job* __restrict__ jobs, uint32_t n_jobs, uint64_t total_blocks, int W, int NB,
                                int maxwords, int PP, int PX, uint32_t one0, uint64_t seq_bytes, uint64_t ntiles,
-                               X2Desc* desc) {
+                               X2Desc* desc, const uint8_t* seq) {
+  const int NL = pack_words_rt(PP, PX);
   for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < ntiles; t += (uint64_t)gridDim.x * blockDim.x) {
     const int64_t b_first = (int64_t)t * X2_OUT_BLOCKS - 1;
     const int64_t b_last = (int64_t)t * X2_OUT_BLOCKS + X2_NT - 2;
@@ -853,19 +973,28 @@ __global__ void k_x2_tile_desc(const uint64_t* __restrict__ kb, const uint64_t* 
     // offset <= (q / x + 1) p, plus the load width.  Every job of the tile is checked: jobs need not be
     // in sequence-buffer order (seeding's dedicated extraction takes an arbitrary read list; the checked
     // build caught the round-1 "last job ends last" shortcut reading past the buffer there)
-    uint64_t last_byte = 0;
+    uint64_t last_byte = 0, sp_lo = ~0ull, sp_hi = 0;
     for (uint32_t j = j0; j <= j1; j++) {
       const uint64_t wend = cw[j + 1] < hi ? cw[j + 1] : hi;
       if (wend <= cw[j] || wend <= lo) continue;
       const Job jj = jobs[j];
       const uint64_t lb = jj.seq_off + jj.phase + one0 + (16 * (wend - cw[j]) / PX + 1) * PP + 48;
       last_byte = lb > last_byte ? lb : last_byte;
+      const uint64_t wst = cw[j] > lo ? cw[j] : lo;
+      uint64_t a, b;
+      job_byte_span(jj.seq_off + jj.phase + one0, wst - cw[j], wend - cw[j], PP, PX, NL, a, b);
+      sp_lo = a < sp_lo ? a : sp_lo;
+      sp_hi = b > sp_hi ? b : sp_hi;
     }
     X2Desc d;
     d.j0 = j0;
     d.j1 = j1;
     d.simple = (j0 == j1) && last_byte <= seq_bytes;
     d.safe = last_byte <= seq_bytes;
+    d.b0 = 0;
+    d.nb = 0;
+    d.pad = 0;
+    raw_span(seq, seq_bytes, sp_lo, sp_hi, d.raw_lo, d.raw_len);
     d.cw_lo = lo;
     d.cw_hi = hi;
     desc[t] = d;
@@ -876,7 +1005,9 @@ __global__ void k_x2_tile_desc(const uint64_t* __restrict__ kb, const uint64_t* 
 // is >= t * S and ends where tile t + 1 starts, so it holds whole jobs and at most 128 blocks
 __global__ void k_x2_tile_desc_aligned(const uint64_t* __restrict__ kb, const uint64_t* __restrict__ cw,
                                        const Job* __restrict__ jobs, uint32_t n_jobs, int W, uint32_t S, int PP,
-                                       int PX, uint32_t one0, uint64_t seq_bytes, uint64_t ntiles, X2Desc* desc) {
+                                       int PX, uint32_t one0, uint64_t seq_bytes, uint64_t ntiles, X2Desc* desc,
+                                       const uint8_t* seq) {
+  const int NL = pack_words_rt(PP, PX);
   auto first_job_at = [&](uint64_t g) -> uint32_t {  // smallest j with kb[j] >= g (n_jobs if none)
     uint32_t lo = 0, hi = n_jobs;
     while (lo < hi) {
@@ -897,13 +1028,18 @@ __global__ void k_x2_tile_desc_aligned(const uint64_t* __restrict__ kb, const ui
     d.pad = 0;
     d.cw_lo = cw[d.j0];
     d.cw_hi = je > j0 ? cw[je] : cw[d.j0];
-    uint64_t last_l = 0;  // every job of the tile (jobs need not be in sequence-buffer order)
+    uint64_t last_l = 0, sp_lo = ~0ull, sp_hi = 0;  // every job (jobs need not be in buffer order)
     for (uint32_t j = d.j0; je > j0 && j <= d.j1; j++) {
       if (cw[j + 1] <= cw[j]) continue;
       const Job jj = jobs[j];
       const uint64_t lb = jj.seq_off + jj.phase + one0 + (16 * (cw[j + 1] - cw[j]) / PX + 1) * PP + 48;
       last_l = lb > last_l ? lb : last_l;
+      uint64_t a, b;
+      job_byte_span(jj.seq_off + jj.phase + one0, 0, cw[j + 1] - cw[j], PP, PX, NL, a, b);
+      sp_lo = a < sp_lo ? a : sp_lo;
+      sp_hi = b > sp_hi ? b : sp_hi;
     }
+    raw_span(seq, seq_bytes, sp_lo, sp_hi, d.raw_lo, d.raw_len);
     d.simple = (d.j0 == d.j1) && last_l <= seq_bytes;
     d.safe = last_l <= seq_bytes;
     desc[t] = d;
@@ -1035,10 +1171,10 @@ bool run_extract2(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const
     const int maxwords = (X2_NT * W + X2_NT * (K - 1) + 15) / 16 + X2_NT + 8;  // X2Cfg::MAXWORDS
     if (aligned)
       GOD_LAUNCH("k_x2_tile_desc", k_x2_tile_desc_aligned, grid_for(ntiles, 256), 256, 0, st, kb, cw, jobs, n_jobs, W,
-                 S_al, PP, PX, P.pat.one[0], seq_bytes, ntiles, desc);
+                 S_al, PP, PX, P.pat.one[0], seq_bytes, ntiles, desc, seq);
     else
       GOD_LAUNCH("k_x2_tile_desc", k_x2_tile_desc, grid_for(ntiles, 256), 256, 0, st, kb, cw, jobs, n_jobs, total_blocks,
-                 W, NB, maxwords, PP, PX, P.pat.one[0], seq_bytes, ntiles, desc);
+                 W, NB, maxwords, PP, PX, P.pat.one[0], seq_bytes, ntiles, desc, seq);
   }
   uint64_t* dtotal = scr.alloc<uint64_t>(1);
   if (want_job_off) {
@@ -1069,7 +1205,7 @@ bool run_extract2(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const
     GOD_CUDA(cudaMemsetAsync(dtotal, 0, sizeof(uint64_t), st));  // the unordered kernel's output counter
     X2Args a{seq, seq_bytes, jobs, kb, cw, n_jobs, total_blocks, P.pat.one[0], key_shift, status, ctr,
              rec.hz, rec.pos, rec.job, rec.job_off, aligned ? rec.job_end : nullptr, cap, dtotal, dbg_flags,
-             dbg_counts, desc, aligned ? 1u : 0u, ntiles};
+             dbg_counts, desc, aligned ? 1u : 0u, ntiles, getenv("GOD_X2_NO_STAGE") ? 1u : 0u};
     if (ntiles) {
       auto by_pattern = [&](auto kc, auto wc) {
         constexpr int KK = decltype(kc)::value, WW = decltype(wc)::value;
