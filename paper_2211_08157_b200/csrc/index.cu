@@ -79,8 +79,10 @@ __global__ void __launch_bounds__(RS_NT) k_rs_hist(const uint64_t* __restrict__ 
 
 // Stable scatter, warp-striped ranking: warp w owns items [w*256, w*256+256) of the tile, item j of
 // lane l is w*256 + 32 j + l, so (warp, j, lane) order is index order.  Ranks come from match_any
-// plus per-warp digit counters (no block barrier per item round).
-template <int RB>
+// plus per-warp digit counters (no block barrier per item round).  STABLE = false (the first LSD
+// pass over records that arrive in any order anyway: K1's tile-order output): one SMEM atomic per
+// item on the warp's digit counter gives its rank (the ballot peer masks were ~36% of the pass).
+template <int RB, bool STABLE = true>
 __global__ void __launch_bounds__(RS2_NT, 2) k_rs_scatter2(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin,
                                                        uint64_t* __restrict__ kout, uint32_t* __restrict__ vout,
                                                        uint64_t n, int shift, uint32_t dmask,
@@ -132,6 +134,10 @@ __global__ void __launch_bounds__(RS2_NT, 2) k_rs_scatter2(const uint64_t* __res
     const uint64_t i = base + (uint64_t)j * 32 + lane;
     const bool ok = i < n;
     const uint32_t d = ok ? ((uint32_t)((key[j] & HASH_BITS_MASK) >> shift) & dmask) : (1 << RB);
+    if constexpr (!STABLE) {
+      rk[j] = ok ? atomicAdd(&wcnt[wid][d], 1u) : 0u;
+      continue;
+    }
     const uint32_t peers = warp_peers<RB>(d);
     const int leader = __ffs(peers) - 1;
     uint32_t old = 0;
@@ -1595,6 +1601,8 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
     if (!attr) {
       GOD_CUDA(cudaFuncSetAttribute(k_rs_scatter2<RS_BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize, RS_DYN_SMEM));
       GOD_CUDA(cudaFuncSetAttribute(k_rs_scatter2<BIN_DIGIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, RS_DYN_SMEM));
+      GOD_CUDA(cudaFuncSetAttribute(k_rs_scatter2<BIN_DIGIT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    RS_DYN_SMEM));
       GOD_CUDA(cudaFuncSetAttribute(k_bin_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, BS_SMEM));
       GOD_CUDA(cudaFuncSetAttribute(k_bin_build, cudaFuncAttributeMaxDynamicSharedMemorySize, BB_SMEM));
       GOD_CUDA(cudaFuncSetAttribute(k_bucket_sort_big, cudaFuncAttributeMaxDynamicSharedMemorySize, BS_SMEM));
@@ -1602,13 +1610,17 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
     }
     const int hbits = 2 * P.k;
     auto lsd_pass = [&](auto rb, int shift, int bits, bool have_hist = false, const uint2* table = nullptr,
-                        int L = 0) {
+                        int L = 0, bool stable = true) {
       constexpr int RB = decltype(rb)::value;
       const uint32_t dmask = (1u << bits) - 1;
       if (!have_hist) GOD_LAUNCH("k_rs_hist", k_rs_hist<RB>, ntiles, RS_NT, 0, st, k0, n, shift, dmask, hist, ntiles);
       scan_exclusive_u32_to_u64(hist, goff, (uint64_t)(1u << RB) * ntiles, nullptr, st, scr, "scan_sort_hist");
-      GOD_LAUNCH("k_rs_scatter", k_rs_scatter2<RB>, ntiles, RS2_NT, RS_DYN_SMEM, st, k0, v0, k1, v1, n, shift, dmask,
-                 goff, ntiles, table, L, resident_ctas(k_rs_scatter2<RB>, RS2_NT, RS_DYN_SMEM));
+      if (stable)
+        GOD_LAUNCH("k_rs_scatter", (k_rs_scatter2<RB, true>), ntiles, RS2_NT, RS_DYN_SMEM, st, k0, v0, k1, v1, n, shift,
+                   dmask, goff, ntiles, table, L, resident_ctas(k_rs_scatter2<RB, true>, RS2_NT, RS_DYN_SMEM));
+      else
+        GOD_LAUNCH("k_rs_scatter", (k_rs_scatter2<RB, false>), ntiles, RS2_NT, RS_DYN_SMEM, st, k0, v0, k1, v1, n, shift,
+                   dmask, goff, ntiles, table, L, resident_ctas(k_rs_scatter2<RB, false>, RS2_NT, RS_DYN_SMEM));
       std::swap(k0, k1);
       std::swap(v0, v1);
     };
@@ -1632,7 +1644,8 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
       // the first pass's tile histograms of the bins; the first scatter assigns the bins itself
       GOD_LAUNCH("k_seg_assign", k_seg_assign, ntiles, RS_NT, 0, st, k0, n, L, hbits, table, (1u << BIN_DIGIT) - 1, hist,
                  ntiles, 0);
-      lsd_pass(std::integral_constant<int, BIN_DIGIT>(), hbits, BIN_DIGIT, true, table, L);
+      // the first pass need not be stable: the records arrive from K1 in tile order
+      lsd_pass(std::integral_constant<int, BIN_DIGIT>(), hbits, BIN_DIGIT, true, table, L, getenv("GOD_RS_STABLE1") != nullptr);
       lsd_pass(std::integral_constant<int, BIN_DIGIT>(), hbits + BIN_DIGIT, BIN_DIGIT);
       const uint32_t nb = d2h_scalar(n_bins_d, st);
       uint64_t* bstart = scr.alloc<uint64_t>((uint64_t)nb + 1);
