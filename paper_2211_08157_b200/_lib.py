@@ -7,7 +7,10 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 # GOD_CHECKED=1 loads the checked build (device-side bounds checks that trap, GOD_DCHECK in common.cuh)
-LIB_PATH = os.path.join(_HERE, "lib", "libgod_checked.so" if os.environ.get("GOD_CHECKED") == "1" else "libgod.so")
+# GOD_LIB_VARIANT=<name> loads lib/libgod_<name>.so (developer builds of the same sources, e.g. another tile size)
+_VARIANT = os.environ.get("GOD_LIB_VARIANT")
+LIB_PATH = os.path.join(_HERE, "lib", "libgod_checked.so" if os.environ.get("GOD_CHECKED") == "1"
+                        else f"libgod_{_VARIANT}.so" if _VARIANT else "libgod.so")
 
 GOD_OK, GOD_EINVAL, GOD_ENOMEM, GOD_ECUDA, GOD_ETRUNC = 0, 1, 2, 3, 4
 STATUS_NAMES = {0: "GOD_OK", 1: "GOD_EINVAL", 2: "GOD_ENOMEM", 3: "GOD_ECUDA", 4: "GOD_ETRUNC"}

@@ -35,15 +35,20 @@ namespace god {
 
 namespace {
 
-constexpr int X2_NT = 128;
+// threads (= W-blocks) per tile.  Smaller CTAs mean more independent barrier domains per SM (the
+// kernel's top stall is the CTA barrier) at the price of more halo blocks (2 per tile).
+#ifndef X2_NT_DEF
+#define X2_NT_DEF 128
+#endif
+constexpr int X2_NT = X2_NT_DEF;
 constexpr int X2_OUT_BLOCKS = X2_NT - 2;
 // unordered output staging (selected records per tile); density is ~2/(w+1), i.e. ~17% of a tile's
 // positions: a tile with more (all-ties runs) writes its records directly
-constexpr int X2_CAP = 512;
+constexpr int X2_CAP = 4 * X2_NT;
 // resident CTAs per SM the register allocation is sized for (SMEM allows 7): 7 for w <= 11 (72
 // registers, no spills), 6 for w = 19 (more registers per W-block)
 template <int W>
-constexpr int x2_minb() { return W >= 16 ? 5 : 7; }
+constexpr int x2_minb() { return (W >= 16 ? 5 : 7) * (128 / X2_NT); }
 
 struct X2Args {
   const uint8_t* seq;
@@ -103,7 +108,7 @@ struct __align__(16) X2Desc {
   uint64_t pad;
 };
 // bytes of the SMEM buffer the next tile's ASCII bytes are staged into (unordered K1)
-constexpr uint32_t X2_RAW_CAP = 6144;
+constexpr uint32_t X2_RAW_CAP = 48 * X2_NT;
 // the byte span [lo, hi) one job's code words [ws, we) load from (pack16: words aligned in the address
 // space, pack_words of them from each word's first byte)
 __device__ __forceinline__ void job_byte_span(uint64_t base, uint64_t ws, uint64_t we, int PP, int PX, int NL,
@@ -137,7 +142,7 @@ struct X2Tile {  // per-tile scalars, in SMEM
 
 template <int K, int W, int PP, int PX>
 struct X2Cfg {
-  static_assert(X2_NT * W < 4096, "staged record index must fit 12 bits (block info packing)");
+  static_assert(X2_NT * W < 65536, "staged tile-local record indices are 16-bit");
   static constexpr int NB = W + K - 1;                 // bases in a thread's window
   static constexpr int NWIN = (2 * NB + 31) / 32;       // aligned window words
   static constexpr int NLOAD = (30 + 2 * NB + 31) / 32; // words loaded before alignment
@@ -478,7 +483,8 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract3(X2Args a) {
   __shared__ uint64_t sjb[X2_NT + 2];  // per job of the tile: byte address of its first patterned base
   __shared__ uint32_t sjn[X2_NT + 2];  // ... its k-mer count n_k
   __shared__ uint32_t sjp[X2_NT + 2];  // ... its output position base (pos_base + phase + one0)
-  __shared__ uint8_t swj[(X2Cfg<K, W, PP, PX>::MAXWORDS + 3) / 4 * 4];  // code word -> job (relative)
+  using swj_t = std::conditional_t<(X2_NT > 128), uint16_t, uint8_t>;
+  __shared__ swj_t swj[(X2Cfg<K, W, PP, PX>::MAXWORDS + 3) / 4 * 4];  // code word -> job (relative)
   __shared__ uint32_t sjob[X2_NT];
   __shared__ uint32_t warp_cnt[NWARP];
   __shared__ uint32_t xlast[NWARP];    // per warp: lane 31's last selected (offset << 27 | key >> 5) ...
@@ -589,7 +595,7 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract3(X2Args a) {
     if (!simple) {  // code word -> job, filled job by job
       for (uint32_t q = tid; q < nj; q += X2_NT) {
         const int64_t w0 = (int64_t)scw[q] - (int64_t)cw_lo, w1 = (int64_t)scw[q + 1] - (int64_t)cw_lo;
-        for (int64_t wi = w0 < 0 ? 0 : w0; wi < w1 && wi < nwords; wi++) swj[wi] = (uint8_t)q;
+        for (int64_t wi = w0 < 0 ? 0 : w0; wi < w1 && wi < nwords; wi++) swj[wi] = (swj_t)q;
       }
       __syncthreads();
     }
@@ -1155,7 +1161,7 @@ bool run_extract2(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const
   // -> job-aligned tiles at atomically claimed offsets (each job contiguous, in position order); else
   // position order through the decoupled look-back.  Unordered instances exist for 2k >= 36.
   const bool can_unordered = 2 * K >= 36 && !want_job && !getenv("GOD_X2_ORDERED");
-  const bool aligned = can_unordered && order == ORDER_JOB && max_jb <= 32 && !getenv("GOD_X2_NO_ALIGN");
+  const bool aligned = can_unordered && order == ORDER_JOB && max_jb <= X2_NT / 4 && !getenv("GOD_X2_NO_ALIGN");
   const bool ordered = !(can_unordered && (order == ORDER_NONE || aligned));
   const uint32_t S_al = (uint32_t)(X2_NT + 1 - max_jb);  // tile stride (blocks) of the aligned layout
   const uint64_t ntiles = aligned ? (total_blocks + S_al - 1) / S_al : (total_blocks + X2_OUT_BLOCKS - 1) / X2_OUT_BLOCKS;

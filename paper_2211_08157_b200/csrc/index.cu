@@ -208,15 +208,24 @@ __global__ void __launch_bounds__(RS2_NT, 2) k_rs_scatter2(const uint64_t* __res
 //   v = low(h) << 33 | pos << 1 | strand       (integer order = (hash, pos) order; L <= 30),
 // skipping digits that are constant across the bin.  Bins above BS_CAP (hashes with thousands of
 // occurrences) go to a chunked global-memory kernel.
-constexpr int BS_NT = 512;
+// CTA size of the per-bin kernels.  The bin capacity, the bin target and the SMEM tables scale with it,
+// so 256 threads run 4 CTAs per SM where 512 run 2: more independent barrier domains per SM (the
+// per-bin sort is a chain of ~12 block barriers).
+#ifndef BS_NT_DEF
+#define BS_NT_DEF 512
+#endif
+constexpr int BS_NT = BS_NT_DEF;
 constexpr int BS_NW = BS_NT / 32;
-constexpr int BS_CAP = 4096;                      // records of a bin held in SMEM (x2 buffers)
-constexpr int BS_IPT = BS_CAP / BS_NT;            // 8
-constexpr int BS_SMEM = 2 * BS_CAP * 8 + 4096 * 4;  // + run-count histogram (SMALL_BINS)
-constexpr uint32_t S_MAX = 2048;                  // directory slots per bin (k_bin_build: first[S + 1] in SMEM)
+constexpr int BS_IPT = 8;
+constexpr int BS_CAP = BS_NT * BS_IPT;            // records of a bin held in SMEM (x2 buffers)
+constexpr int BS_MSD_BITS = BS_NT == 512 ? 12 : BS_NT == 256 ? 11 : 10;  // log2(BS_CAP)
+static_assert((1 << BS_MSD_BITS) == BS_CAP, "MSD placement: one bucket per record slot, 8 counters per thread");
+constexpr uint32_t SMALL_BINS = BS_CAP;           // run-count histogram in SMEM (larger counts: a list)
+constexpr int BS_SMEM = 2 * BS_CAP * 8 + (int)SMALL_BINS * 4;
+constexpr uint32_t S_MAX = BS_CAP / 2;            // directory slots per bin (k_bin_build: first[S + 1] in SMEM)
 constexpr int BB_SMEM = BS_SMEM + (S_MAX + 1) * 4;
+constexpr int BS_MINB = 1024 / BS_NT;             // resident CTAs per SM the kernels are sized for
 constexpr int SEG_BITS = 12;
-constexpr uint32_t SMALL_BINS = 4096;
 
 // Run statistics (K3) produced by the sort kernels when they can: count histogram (small counts) +
 // list of large counts, number of distinct hashes.  (Per-record run lengths are not stored: the
@@ -279,7 +288,7 @@ __device__ __forceinline__ uint64_t run_len_capped(const uint64_t* __restrict__ 
   return 1 + run_side(k, n, i, hv, lim, false, hm) + run_side(k, n, i, hv, lim, true, hm);
 }
 
-constexpr uint32_t BIN_TARGET = 3072;  // measured: 2048 13.9 ms, 2560 13.7, 3072 13.6, 3584 14.5 (stage 3, human)
+constexpr uint32_t BIN_TARGET = BS_CAP / 4 * 3;  // measured at BS_CAP = 4096: 2048 13.9 ms, 2560 13.7, 3072 13.6, 3584 14.5 (stage 3, human)
 constexpr int BIN_DIGIT = 9;                      // LSD digit over b
 constexpr int BIN_RANK_MAX = 1024;                // buckets up to this size: ranked by counting, else LSD
 static_assert(RS_BINS * BS_NW == BS_NT * 8, "block scan assumes 8 counters per thread");
@@ -442,7 +451,7 @@ __device__ __forceinline__ void cta_load_striped(const uint64_t* src, int n, uin
   }
 }
 
-__global__ void __launch_bounds__(BS_NT, 2) k_bin_sort(uint64_t* __restrict__ k, uint32_t* __restrict__ v,
+__global__ void __launch_bounds__(BS_NT, BS_MINB) k_bin_sort(uint64_t* __restrict__ k, uint32_t* __restrict__ v,
                                                        const uint64_t* __restrict__ bstart,
                                                        const uint32_t* __restrict__ n_bins, int L, int hbits,
                                                        uint32_t* big, uint32_t* n_big, RunOut ro) {
@@ -574,7 +583,7 @@ __global__ void __launch_bounds__(BS_NT, 2) k_bin_sort(uint64_t* __restrict__ k,
     // (1) MSD placement by the top 12 bits of low(h) - mn (4096 buckets, ~1 record each), then an
     //     insertion sort of each bucket on the full packed value (unique: it contains pos)
     const int rbits = 32 - __clz(mx - mn);
-    const int shb = rbits > 12 ? rbits - 12 : 0;
+    const int shb = rbits > BS_MSD_BITS ? rbits - BS_MSD_BITS : 0;
     {
       uint4* c4 = reinterpret_cast<uint4*>(cnt);
       c4[2 * threadIdx.x] = make_uint4(0, 0, 0, 0);
@@ -728,7 +737,7 @@ __device__ __forceinline__ void suffix_min_block(uint32_t* f, uint32_t m, uint32
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(BS_NT, 2) k_bin_build(const uint64_t* __restrict__ k, const uint32_t* __restrict__ v,
+__global__ void __launch_bounds__(BS_NT, BS_MINB) k_bin_build(const uint64_t* __restrict__ k, const uint32_t* __restrict__ v,
                                                         const uint64_t* __restrict__ bstart,
                                                         const uint32_t* __restrict__ n_bins, int L, int hbits,
                                                         uint32_t* big, uint32_t* n_big, RunOut ro,
@@ -852,7 +861,7 @@ __global__ void __launch_bounds__(BS_NT, 2) k_bin_build(const uint64_t* __restri
     // (1) MSD placement by the top 12 bits of low(h) - mn (4096 buckets, ~1 record each), then an
     //     insertion sort of each bucket on the full packed value (unique: it contains pos)
     const int rbits = 32 - __clz(mx - mn);
-    const int shb = rbits > 12 ? rbits - 12 : 0;
+    const int shb = rbits > BS_MSD_BITS ? rbits - BS_MSD_BITS : 0;
     {
       uint4* c4 = reinterpret_cast<uint4*>(cnt);
       c4[2 * threadIdx.x] = make_uint4(0, 0, 0, 0);
@@ -967,7 +976,12 @@ __global__ void __launch_bounds__(BS_NT, 2) k_bin_build(const uint64_t* __restri
     for (uint32_t q = threadIdx.x; q < S; q += BS_NT) {
       const uint32_t a0 = first[q], b0 = first[q + 1];
       uint32_t kk[DIR_KEYS];
-      if (b0 - a0 <= DIR_KEYS) {
+      if (b0 - a0 <= DIR_PAIRS) {  // the entries themselves
+        dir_pairs(b0 - a0, [&](int e2) {
+          const uint64_t pv = res[a0 + e2];
+          return ((pv >> 1) << 32) | ((pv >> 33) << 1) | (pv & 1ull);
+        }, kk);
+      } else if (b0 - a0 <= DIR_KEYS) {
 #pragma unroll
         for (int e2 = 0; e2 < DIR_KEYS; e2++) kk[e2] = a0 + e2 < b0 ? (uint32_t)(res[a0 + e2] >> 33) : 0xFFFFFFFFu;
       } else {  // <= DIR_RUNS distinct keys: (key, run end) pairs; more: key[0] = ~0 (the probe searches)
@@ -1110,7 +1124,7 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort_big(uint64_t* __restri
 __global__ void __launch_bounds__(BS_NT) k_big_dir(const uint64_t* __restrict__ k, const uint64_t* __restrict__ bstart,
                                                    const uint32_t* big, const uint32_t* n_big, int L, int hbits,
                                                    const uint2* __restrict__ table, uint32_t S,
-                                                   DirRec* __restrict__ dir) {
+                                                   const uint64_t* __restrict__ ent, DirRec* __restrict__ dir) {
   const uint64_t lmask = (1ull << L) - 1, hmask = (1ull << hbits) - 1;
   const uint32_t nbig = *n_big;
   for (uint32_t qb = blockIdx.x; qb < nbig; qb += gridDim.x) {
@@ -1132,7 +1146,9 @@ __global__ void __launch_bounds__(BS_NT) k_big_dir(const uint64_t* __restrict__ 
     for (uint32_t q = threadIdx.x; q < S; q += BS_NT) {
       const uint64_t a0 = first_at(q), b0 = first_at(q + 1);
       uint32_t kk[DIR_KEYS];
-      if (b0 - a0 <= DIR_KEYS) {
+      if (b0 - a0 <= DIR_PAIRS) {  // the entries themselves
+        dir_pairs((uint32_t)(b0 - a0), [&](int e2) { return ent[s + a0 + e2]; }, kk);
+      } else if (b0 - a0 <= DIR_KEYS) {
 #pragma unroll
         for (int e2 = 0; e2 < DIR_KEYS; e2++) kk[e2] = a0 + e2 < b0 ? key(a0 + e2) : 0xFFFFFFFFu;
       } else {
@@ -1441,7 +1457,9 @@ __global__ void __launch_bounds__(DF_NT) k_dir_suffix_min(const uint32_t* dir, u
     if (sl >= n_slots) break;
     const uint32_t a = sd[q], b = sd[q + 1];
     uint32_t kk[DIR_KEYS];
-    if (b - a <= DIR_KEYS) {
+    if (b - a <= DIR_PAIRS) {  // the entries themselves
+      dir_pairs(b - a, [&](int e) { return ent[a + e]; }, kk);
+    } else if (b - a <= DIR_KEYS) {
 #pragma unroll
       for (int e = 0; e < DIR_KEYS; e++) kk[e] = a + e < b ? (uint32_t)ent[a + e] >> 1 : 0xFFFFFFFFu;
     } else {
@@ -1665,10 +1683,10 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
         GOD_LAUNCH("k_seg_slots", k_seg_slots, (1u << SEG_BITS) / 256, 256, 0, st, table, S_dir, seg);
         GOD_CUDA(cudaMallocAsync((void**)&ix->dir, std::max<uint64_t>(n_slots, 1) * sizeof(DirRec), st));
         GOD_CUDA(cudaMallocAsync((void**)&ix->ent, n * sizeof(uint64_t), st));
-        GOD_LAUNCH("k_bin_build", k_bin_build, 2u * num_sms(), BS_NT, BB_SMEM, st, k0, v0, bstart, n_bins_d, L, hbits,
+        GOD_LAUNCH("k_bin_build", k_bin_build, (unsigned)BS_MINB * num_sms(), BS_NT, BB_SMEM, st, k0, v0, bstart, n_bins_d, L, hbits,
                    big, n_big, ro, table, nullptr, S_dir, ix->ent, ix->dir);
       } else {
-        GOD_LAUNCH("k_bin_sort", k_bin_sort, 2u * num_sms(), BS_NT, BS_SMEM, st, k0, v0, bstart, n_bins_d, L, hbits, big,
+        GOD_LAUNCH("k_bin_sort", k_bin_sort, (unsigned)BS_MINB * num_sms(), BS_NT, BS_SMEM, st, k0, v0, bstart, n_bins_d, L, hbits, big,
                    n_big, ro);
       }
       runs_done = true;
@@ -1681,7 +1699,7 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
                    v0, /*t0=*/k1, /*t1=*/k0, bstart, big, n_big, L, hbits, ro, built ? ix->ent : nullptr);
         if (built)
           GOD_LAUNCH("k_big_dir", k_big_dir, std::min(hb_big, 4u * (uint32_t)num_sms()), BS_NT, 0, st, k0, bstart, big,
-                     n_big, L, hbits, table, S_dir, ix->dir);
+                     n_big, L, hbits, table, S_dir, ix->ent, ix->dir);
       }
     } else {
       // K2 full stable LSD over the 2k hash bits (position order kept within equal hashes)

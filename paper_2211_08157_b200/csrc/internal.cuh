@@ -92,13 +92,34 @@ JobSet make_jobs(const Params& P, const uint64_t* offsets, uint32_t n_seqs, cons
 constexpr int DIR_SEG_BITS = 12;
 constexpr int DIR_KEYS = 6;
 constexpr int DIR_RUNS = DIR_KEYS / 2;
+constexpr int DIR_PAIRS = DIR_KEYS / 2;
 struct __align__(32) DirRec {
   uint32_t start, end;
+  // end - start <= DIR_PAIRS: the slot's entries themselves, (key | strand << 31, pos) x DIR_PAIRS
+  //   (unused pairs (0xFFFFFFFF, 0)): a probe that finds ONE entry with its key has the anchor's
+  //   position and strand from this sector and never touches `ent` (round 2: one dependent random
+  //   access less per such record; keys are < 2^31, so bit 31 is free).
   // end - start <= DIR_KEYS: the keys of the slot's entries, 0xFFFFFFFF past the end.
   // longer: (key, end of its run) x DIR_RUNS for a slot of <= DIR_RUNS distinct keys (unused pairs
   // (0xFFFFFFFF, end)); key[0] = 0xFFFFFFFF for more (keys are < 2^31, so ~0 is never one)
   uint32_t key[DIR_KEYS];
 };
+// the six payload words of a slot record holding <= DIR_PAIRS entries; entry(i) = the slot's i-th
+// entry in `ent` form (pos << 32 | key << 1 | strand)
+template <typename F>
+__device__ __forceinline__ void dir_pairs(uint32_t n, F entry, uint32_t (&kk)[DIR_KEYS]) {
+#pragma unroll
+  for (int e = 0; e < DIR_PAIRS; e++) {
+    if ((uint32_t)e < n) {
+      const uint64_t en = entry(e);
+      kk[2 * e] = ((uint32_t)en >> 1) | ((uint32_t)en << 31);
+      kk[2 * e + 1] = (uint32_t)(en >> 32);
+    } else {
+      kk[2 * e] = 0xFFFFFFFFu;
+      kk[2 * e + 1] = 0u;
+    }
+  }
+}
 struct IndexView {
   const DirRec* dir;
   const uint64_t* ent;
@@ -125,7 +146,10 @@ __device__ __forceinline__ uint64_t index_slot(const IndexView& v, uint64_t h) {
 // minimizers (their hash values) in the seed index").  The slot record answers a slot of
 // <= DIR_KEYS entries (almost all) or <= DIR_RUNS distinct keys from one 32-B sector; a longer
 // slot is searched in the entries.
-__device__ __forceinline__ uint2 probe_range_all(const IndexView& v, uint64_t h) {
+// *one (if not null): the entry itself (`ent` form) when the slot record holds it and it is the
+// only entry with this hash, else ~0
+__device__ __forceinline__ uint2 probe_range_all(const IndexView& v, uint64_t h, uint64_t* one = nullptr) {
+  if (one) *one = ~0ull;
   const uint64_t slot = index_slot(v, h);
   if (slot == ~0ull) return make_uint2(0, 0);
   GOD_DCHECK(slot < v.n_slots, "probe: directory slot");
@@ -134,6 +158,19 @@ __device__ __forceinline__ uint2 probe_range_all(const IndexView& v, uint64_t h)
   const uint4 r1 = __ldg(reinterpret_cast<const uint4*>(v.dir + slot) + 1);
   const uint32_t lo = r0.x, hi = r0.y;
   GOD_DCHECK(lo <= hi && hi <= v.n_ent, "probe: slot entry range inside the entries");
+  if (hi - lo <= DIR_PAIRS) {  // the slot's entries are in the record
+    const uint32_t k3[DIR_PAIRS] = {r0.z, r1.x, r1.z}, p3[DIR_PAIRS] = {r0.w, r1.y, r1.w};
+    uint32_t below = 0, eq = 0, pp = 0, zz = 0;
+#pragma unroll
+    for (int q = 0; q < DIR_PAIRS; q++) {
+      const uint32_t kq = k3[q] & 0x7FFFFFFFu;
+      const bool in = (uint32_t)q < hi - lo;
+      below += in && kq < key;
+      if (in && kq == key) { eq++; pp = p3[q]; zz = k3[q] >> 31; }
+    }
+    if (one && eq == 1) *one = ((uint64_t)pp << 32) | ((uint64_t)key << 1) | zz;
+    return make_uint2(lo + below, lo + below + eq);
+  }
   if (hi - lo <= DIR_KEYS) {  // every key of the slot is in the record
     const uint32_t k6[DIR_KEYS] = {r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
     uint32_t below = 0, eq = 0;
@@ -170,8 +207,8 @@ __device__ __forceinline__ uint2 probe_range_all(const IndexView& v, uint64_t h)
   return make_uint2(a, c);
 }
 // the kept entries with hash h: a hash with more than tau entries is dropped (reading O7)
-__device__ __forceinline__ uint2 probe_range(const IndexView& v, uint64_t h) {
-  const uint2 r = probe_range_all(v, h);
+__device__ __forceinline__ uint2 probe_range(const IndexView& v, uint64_t h, uint64_t* one = nullptr) {
+  const uint2 r = probe_range_all(v, h, one);
   return r.y - r.x > v.tau ? make_uint2(r.x, r.x) : r;
 }
 

@@ -29,6 +29,9 @@ struct SeedSources {
 
 namespace {
 
+// flags in a probe's count word (k_anchor_count<true>)
+constexpr uint32_t CNT_INL = 0x80000000u, CNT_STRAND = 0x40000000u, CNT_MASK = 0x3FFFFFFFu;
+
 __global__ void k_phase(const uint32_t* __restrict__ occ, const Job* __restrict__ jobs, const uint64_t* __restrict__ job_off,
                         const uint64_t* __restrict__ job_end,
                         const uint64_t* __restrict__ hz, const uint32_t* __restrict__ pos, const uint32_t* __restrict__ ids,
@@ -67,14 +70,14 @@ __global__ void k_phase(const uint32_t* __restrict__ occ, const Job* __restrict_
     for (uint32_t s = 0; s < p; s++) {
       const uint64_t j = (uint64_t)i * p + s;
       uint64_t sc = 0;
-      for (uint64_t q = 0; q < c; q++) sc += occ[job_off[j] + q];  // occ(h) of the q-th minimizer
+      for (uint64_t q = 0; q < c; q++) sc += occ[job_off[j] + q] & CNT_MASK;  // occ(h) of the q-th minimizer
       if (s == 0 || sc > best) { best = sc; a = s; }
     }
     phases[r] = (uint8_t)a;
     if (acount) {  // anchors of the read if PQ_a's records are this phase job's (the S4 fast path)
       const uint64_t j = (uint64_t)i * p + a;
       uint64_t na = 0;
-      for (uint64_t q = job_off[j]; q < job_end[j]; q++) na += occ[q];
+      for (uint64_t q = job_off[j]; q < job_end[j]; q++) na += occ[q] & CNT_MASK;
       acount[r] = na;
     }
   }
@@ -108,18 +111,34 @@ __global__ void k_check_jobs(const uint64_t* job_off, const uint64_t* job_end, u
 // one probe per thread, one thread per record, large grid: the probe is a chain of two dependent
 // random accesses (directory slot, entries) and is bound by HBM random-access bandwidth; many
 // resident warps hide the latency better than a persistent loop with per-thread ILP (measured).
+// INL (the index holds < 2^30 entries, so counts leave the top bits of cnt free): a record whose hash
+// has ONE kept entry that its slot record holds gets cnt = 1 | CNT_INL | strand << 30 and beg = the
+// entry's position — its anchor needs no access to `ent` (CNT_MASK strips the flags).
+template <bool INL>
 __global__ void k_anchor_count(IndexView v, const uint64_t* __restrict__ hz, uint64_t n, uint32_t* cnt, uint32_t* beg) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint2 rg = probe_range(v, hz[i] & ((1ull << 63) - 1));
-    cnt[i] = rg.y - rg.x;
-    beg[i] = rg.x;
+    uint64_t one = ~0ull;
+    const uint2 rg = probe_range(v, hz[i] & ((1ull << 63) - 1), INL ? &one : nullptr);
+    if (INL && rg.y - rg.x == 1 && one != ~0ull) {
+      cnt[i] = 1u | CNT_INL | (((uint32_t)one & 1u) ? CNT_STRAND : 0u);
+      beg[i] = (uint32_t)(one >> 32);
+    } else {
+      cnt[i] = rg.y - rg.x;
+      beg[i] = rg.x;
+    }
   }
 }
 
 // S4 fast path (every read's PQ_a records are its phase-a job of S1, each <= ~40 records): a group
 // of 8 lanes per read sums its records' probe counts, and after the scan writes its anchors (each
 // lane one record at a time, offsets by a group scan), so no read-ordered copy of the records is made.
-constexpr int RG = 8;
+#ifndef GOD_AW_MINB
+#define GOD_AW_MINB 8  // measured (human): 5 -> 2.84 ms, 6 -> 2.46, 8 -> 2.33 (32 registers, 72 B spilled); 16-lane groups 3.41
+#endif
+#ifndef GOD_RG
+#define GOD_RG 8
+#endif
+constexpr int RG = GOD_RG;
 __global__ void k_read_anchor_counts1(const uint32_t* __restrict__ cnt, const uint64_t* __restrict__ job_off,
                                       const uint64_t* __restrict__ job_end,
                                       const uint8_t* __restrict__ phases, uint32_t p, uint32_t n_reads, uint64_t* out) {
@@ -130,53 +149,113 @@ __global__ void k_read_anchor_counts1(const uint32_t* __restrict__ cnt, const ui
     const uint64_t j = (uint64_t)r * p + phases[r];
     const uint64_t b = job_off[j], e = job_end[j];
     uint64_t acc = 0;
-    for (uint64_t q = b + l; q < e; q += RG) acc += cnt[q];
+    for (uint64_t q = b + l; q < e; q += RG) acc += cnt[q] & CNT_MASK;
 #pragma unroll
     for (int d = RG / 2; d; d >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, d, RG);
     if (l == 0) out[r] = acc;
   }
 }
+// The group's 8 lanes share the chunk's anchors evenly (anchor a of the chunk -> lane a mod 8, its
+// record found from the lanes' inclusive counts by shuffles), two anchors per lane per round with both
+// entry loads issued before either store: the writer is bound by the latency of the dependent entry
+// reads, not by their number (measured: without them 1.74 ms, with them 3.45 ms whether 87 M or 40 M
+// of them go to DRAM), so what counts is how many are in flight — and a frequent hash's run of entries
+// is read by 8 lanes side by side instead of one lane in sequence.
 template <bool A16>  // A16: out is 16-B aligned -> one 128-bit store per anchor
-__global__ void k_anchor_write1(IndexView v, const uint64_t* __restrict__ hz, const uint32_t* __restrict__ pos,
+__global__ void __launch_bounds__(256, GOD_AW_MINB) k_anchor_write1(IndexView v, const uint64_t* __restrict__ hz, const uint32_t* __restrict__ pos,
                                 const uint32_t* __restrict__ cnt, const uint32_t* __restrict__ beg,
                                 const uint64_t* __restrict__ job_off, const uint64_t* __restrict__ job_end,
                                 const uint8_t* __restrict__ phases, uint32_t p,
                                 uint32_t n_reads, const uint64_t* __restrict__ aoff, god_anchor* out,
                                 uint32_t rid_base) {
   const uint32_t l = threadIdx.x & (RG - 1);
+  static_assert(RG == 8 || RG == 16, "group mask");
+  const uint32_t gm = RG == 8 ? 0xFFu << (threadIdx.x & 24u) : 0xFFFFu << (threadIdx.x & 16u);  // the lanes of this group
   for (uint64_t g = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / RG; g < n_reads;
        g += (uint64_t)gridDim.x * blockDim.x / RG) {
     const uint32_t r = (uint32_t)g;
-    const uint64_t j = (uint64_t)r * p + phases[r];
-    const uint64_t b = job_off[j], e = job_end[j];
+    // the read's phase and the record ranges of all its phase jobs are loaded together (lane s holds
+    // job s), then the chosen one is taken by shuffle: one dependent round trip less per read
+    const uint32_t a_ph = phases[r];
+    uint64_t b, e;
+    if (p <= (uint32_t)RG) {
+      const uint64_t jl = (uint64_t)r * p + (l < p ? l : 0u);
+      const uint64_t bl = job_off[jl], el = job_end[jl];
+      b = __shfl_sync(gm, bl, a_ph, RG);
+      e = __shfl_sync(gm, el, a_ph, RG);
+    } else {
+      const uint64_t j = (uint64_t)r * p + a_ph;
+      b = job_off[j];
+      e = job_end[j];
+    }
     GOD_DCHECK(b <= e, "anchor writer: job record range");
     uint64_t o = aoff[r];
     for (uint64_t q0 = b; q0 < e; q0 += RG) {  // uniform trip count within the group
       const uint64_t q = q0 + l;
-      const uint32_t c = q < e ? cnt[q] : 0u;
+      // all four record fields at once (not the count first): a shorter dependent chain per read
+      const uint32_t craw = q < e ? cnt[q] : 0u;
+      const uint32_t bg0 = q < e ? beg[q] : 0u, qp0 = q < e ? pos[q] : 0u;
+      const uint32_t qz0 = q < e ? (uint32_t)(hz[q] >> 63) : 0u;
+      const uint32_t c = craw & CNT_MASK;
       uint32_t incl = c;
 #pragma unroll
       for (int d = 1; d < RG; d <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d, RG);
+        const uint32_t y = __shfl_up_sync(gm, incl, d, RG);
         if (l >= (uint32_t)d) incl += y;
       }
-      const uint32_t tot = __shfl_sync(0xffffffffu, incl, RG - 1, RG);
+      const uint32_t tot = __shfl_sync(gm, incl, RG - 1, RG);
+      uint32_t bg = 0, qp = 0, fl = 0;  // fl: bit 0 read strand, bit 1 entry strand (inline), bit 2 inline
       if (c) {
-        const uint32_t bg = beg[q], qp = pos[q], qz = (uint32_t)(hz[q] >> 63);
-        uint64_t oo = o + incl - c;
-        GOD_DCHECK((uint64_t)bg + c <= v.n_ent && oo + c <= aoff[n_reads], "anchor writer: entry and anchor ranges");
-        for (uint32_t t2 = 0; t2 < c; t2++, oo++) {
-          const uint64_t en = __ldg(v.ent + bg + t2);
-          if (A16) {
-            reinterpret_cast<uint4*>(out)[oo] =
-                make_uint4((uint32_t)(en >> 32), qp, rid_base + r, ((uint32_t)en & 1u) ^ qz);
-          } else {
-            god_anchor an;
-            an.ref_pos = (uint32_t)(en >> 32);
-            an.read_pos = qp;
-            an.read_id = rid_base + r;
-            an.strand = ((uint32_t)en & 1u) ^ qz;
-            out[oo] = an;
+        bg = bg0;
+        qp = qp0;
+        fl = qz0 | ((craw >> 30) << 1);
+        GOD_DCHECK(((craw & CNT_INL) || (uint64_t)bg + c <= v.n_ent) && o + incl <= aoff[n_reads],
+                   "anchor writer: entry and anchor ranges");
+      }
+      const uint32_t excl = incl - c;
+      uint32_t inc8[RG];
+#pragma unroll
+      for (int jl = 0; jl < RG; jl++) inc8[jl] = __shfl_sync(gm, incl, jl, RG);
+      for (uint32_t a0 = 0; a0 < tot; a0 += 2 * RG) {  // uniform within the group
+        uint64_t en[2];
+        uint32_t rp[2], rf[2];
+#pragma unroll
+        for (int u = 0; u < 2; u++) {
+          const uint32_t a = a0 + u * RG + l;
+          uint32_t rec = 0;
+#pragma unroll
+          for (int jl = 0; jl < RG - 1; jl++) rec += inc8[jl] <= a;  // the record holding anchor a
+          const uint32_t rb = __shfl_sync(gm, bg, rec, RG), rx = __shfl_sync(gm, excl, rec, RG);
+          rp[u] = __shfl_sync(gm, qp, rec, RG);
+          rf[u] = __shfl_sync(gm, fl, rec, RG);
+          en[u] = 0;
+          if (a < tot) {
+            // the entry came with the probe (its slot record holds it), else read it
+            if (rf[u] & 4u) en[u] = ((uint64_t)rb << 32) | ((rf[u] >> 1) & 1u);
+            else
+#ifdef GOD_DBG_NO_ENT
+              en[u] = (uint64_t)rb + (a - rx);
+#else
+              en[u] = __ldg(v.ent + rb + (a - rx));
+#endif
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 2; u++) {
+          const uint32_t a = a0 + u * RG + l;
+          if (a < tot) {
+            const uint64_t oo = o + a;
+            if (A16) {
+              reinterpret_cast<uint4*>(out)[oo] =
+                  make_uint4((uint32_t)(en[u] >> 32), rp[u], rid_base + r, ((uint32_t)en[u] & 1u) ^ (rf[u] & 1u));
+            } else {
+              god_anchor an;
+              an.ref_pos = (uint32_t)(en[u] >> 32);
+              an.read_pos = rp[u];
+              an.read_id = rid_base + r;
+              an.strand = ((uint32_t)en[u] & 1u) ^ (rf[u] & 1u);
+              out[oo] = an;
+            }
           }
         }
       }
@@ -188,13 +267,23 @@ __global__ void k_anchor_write1(IndexView v, const uint64_t* __restrict__ hz, co
 // one thread per read minimizer: its anchors are the kept entries [beg, beg + cnt)
 __global__ void k_anchor_write(IndexView v, const uint32_t* __restrict__ pos, const uint32_t* __restrict__ rid,
                                const uint64_t* __restrict__ hz, uint64_t n, const uint64_t* __restrict__ aoff,
-                               const uint32_t* __restrict__ cnt, const uint32_t* __restrict__ beg, god_anchor* out,
-                               uint32_t rid_base) {
+                               const uint32_t* __restrict__ cnt, const uint32_t* __restrict__ beg,
+                               const uint8_t* __restrict__ inl, god_anchor* out, uint32_t rid_base) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t c = cnt[i];
     if (!c) continue;
     const uint32_t qz = (uint32_t)(hz[i] >> 63), qpos = pos[i], r = rid_base + rid[i], b = beg[i];
+    const uint32_t fl = inl[i];  // bit 1: the entry came with the probe (b = its position, bit 0 = its strand)
     uint64_t o = aoff[i];
+    if (fl & 2u) {
+      god_anchor an;
+      an.ref_pos = b;
+      an.read_pos = qpos;
+      an.read_id = r;
+      an.strand = (fl & 1u) ^ qz;
+      out[o] = an;
+      continue;
+    }
     for (uint32_t e = b; e < b + c; e++, o++) {
       god_anchor an;
       const uint64_t en = __ldg(v.ent + e);
@@ -277,7 +366,7 @@ __global__ void k_seed_counts(SeedSources S, uint32_t n_reads, const uint8_t* __
 // 8 threads per read copy its records into the read-ordered arrays
 __global__ void k_seed_gather(SeedSources S, uint32_t n_reads, const uint8_t* __restrict__ src,
                               const uint32_t* __restrict__ srcj, const uint64_t* __restrict__ roff, uint64_t* hz,
-                              uint32_t* qpos, uint32_t* rid, uint32_t* cnt, uint32_t* beg) {
+                              uint32_t* qpos, uint32_t* rid, uint32_t* cnt, uint32_t* beg, uint8_t* inl) {
   for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < (uint64_t)n_reads * 8;
        g += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t r = (uint32_t)(g >> 3), l = (uint32_t)(g & 7);
@@ -288,7 +377,9 @@ __global__ void k_seed_gather(SeedSources S, uint32_t n_reads, const uint8_t* __
       hz[o + q] = S.hz[s][b + q];
       qpos[o + q] = S.pos[s][b + q];
       rid[o + q] = r;
-      cnt[o + q] = S.cnt[s][b + q];
+      const uint32_t craw = S.cnt[s][b + q];
+      cnt[o + q] = craw & CNT_MASK;   // clean counts for the scan; the inline flags go beside them
+      inl[o + q] = (uint8_t)(craw >> 30);
       beg[o + q] = S.beg[s][b + q];
     }
   }
@@ -309,7 +400,11 @@ static void probe_all(const IndexView& v, Records& rec, cudaStream_t st, Scratch
   rec.beg = scr.alloc<uint32_t>(rec.n);
   if (rec.n) {
     prof_add_units("k_probe", rec.n);  // probes (records looked up) for the stage-4 roofline
-    GOD_LAUNCH("k_probe", k_anchor_count, grid_for(rec.n, 256), 256, 0, st, v, rec.hz, rec.n, rec.cnt, rec.beg);
+    // the count word's top bits carry the inline-entry flags only when no count can reach them
+    if (v.n_ent < (1ull << 30))
+      GOD_LAUNCH("k_probe", k_anchor_count<true>, grid_for(rec.n, 256), 256, 0, st, v, rec.hz, rec.n, rec.cnt, rec.beg);
+    else
+      GOD_LAUNCH("k_probe", k_anchor_count<false>, grid_for(rec.n, 256), 256, 0, st, v, rec.hz, rec.n, rec.cnt, rec.beg);
   }
 }
 
@@ -459,8 +554,9 @@ uint64_t seed_reads(const god_index* ix, const uint8_t* reads, const uint64_t* o
   uint32_t* rid = scr.alloc<uint32_t>(n);
   uint32_t* cnt = scr.alloc<uint32_t>(n);
   uint32_t* beg = scr.alloc<uint32_t>(n);
+  uint8_t* inl = scr.alloc<uint8_t>(n);
   GOD_LAUNCH("k_seed_gather", k_seed_gather, grid_for((uint64_t)n_reads * 8, 256), 256, 0, st, S, n_reads, src, srcj,
-             roff, hz, qpos, rid, cnt, beg);
+             roff, hz, qpos, rid, cnt, beg, inl);
   // ---------------- S4: anchors (every read minimizer was probed once, right after its extraction)
   uint64_t* aoff = scr.alloc<uint64_t>(n);
   uint64_t* total = scr.alloc<uint64_t>(1);
@@ -470,7 +566,7 @@ uint64_t seed_reads(const god_index* ix, const uint8_t* reads, const uint64_t* o
   const uint64_t tot = d2h_scalar(total, st);
   if (tot <= cap && n)
     GOD_LAUNCH("k_anchor_write", k_anchor_write, grid_for(n, 256), 256, 0, st, v, qpos, rid, hz, n, aoff, cnt, beg,
-               anchors, rid_base);
+               inl, anchors, rid_base);
   return tot;
 }
 
