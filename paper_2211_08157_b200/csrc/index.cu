@@ -212,7 +212,7 @@ __global__ void __launch_bounds__(RS2_NT, 2) k_rs_scatter2(const uint64_t* __res
 // so 256 threads run 4 CTAs per SM where 512 run 2: more independent barrier domains per SM (the
 // per-bin sort is a chain of ~12 block barriers).
 #ifndef BS_NT_DEF
-#define BS_NT_DEF 512
+#define BS_NT_DEF 256
 #endif
 constexpr int BS_NT = BS_NT_DEF;
 constexpr int BS_NW = BS_NT / 32;
@@ -225,6 +225,7 @@ constexpr int BS_SMEM = 2 * BS_CAP * 8 + (int)SMALL_BINS * 4;
 constexpr uint32_t S_MAX = BS_CAP / 2;            // directory slots per bin (k_bin_build: first[S + 1] in SMEM)
 constexpr int BB_SMEM = BS_SMEM + (S_MAX + 1) * 4;
 constexpr int BS_MINB = 1024 / BS_NT;             // resident CTAs per SM the kernels are sized for
+constexpr int BS_BIG_MINB = BS_NT >= 512 ? 1 : 2;  // ... of k_bucket_sort_big (138 registers unconstrained)
 constexpr int SEG_BITS = 12;
 
 // Run statistics (K3) produced by the sort kernels when they can: count histogram (small counts) +
@@ -293,21 +294,25 @@ constexpr int BIN_DIGIT = 9;                      // LSD digit over b
 constexpr int BIN_RANK_MAX = 1024;                // buckets up to this size: ranked by counting, else LSD
 static_assert(RS_BINS * BS_NW == BS_NT * 8, "block scan assumes 8 counters per thread");
 
-// records per top-SEG_BITS segment, counting every `stride`-th record (the bin widths only balance the
-// bins: every segment gets >= 1 bin, so a sampled count never lets a bin span two segments)
+// records per top-SEG_BITS segment over a sample: one block of 32 consecutive records (256 B, one
+// coalesced warp load) out of every `stride` blocks.  K1 emits records in tile (position) order, so a
+// block's hashes are independent of its index and the sample is uniform.  The counts only size the
+// bins (every segment gets >= 1 bin, so a sampled count never lets a bin span two segments).
 __global__ void k_seg_hist(const uint64_t* __restrict__ k, uint64_t n, int L, uint32_t* segc, uint32_t stride) {
   __shared__ uint32_t h[1 << SEG_BITS];
   for (int i = threadIdx.x; i < (1 << SEG_BITS); i += blockDim.x) h[i] = 0;
   __syncthreads();
-  for (uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) * stride; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x * stride)
-    atomicAdd(&h[(uint32_t)((k[i] & HASH_BITS_MASK) >> L)], 1u);
+  const uint64_t nwarps = (uint64_t)gridDim.x * blockDim.x / 32;
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint64_t b = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / 32; b * 32 * stride < n; b += nwarps) {
+    const uint64_t i = b * 32 * stride + lane;
+    if (i < n) atomicAdd(&h[(uint32_t)((k[i] & HASH_BITS_MASK) >> L)], 1u);
+  }
   __syncthreads();
   for (int i = threadIdx.x; i < (1 << SEG_BITS); i += blockDim.x)
     if (h[i]) atomicAdd(&segc[i], h[i]);
 }
 
-// one CTA of 1024 threads: bins_t, base_t (exclusive scan) and the total bin count
 __global__ void __launch_bounds__(1024) k_seg_table(const uint32_t* __restrict__ segc, uint32_t target, uint2* table,
                                                     uint32_t* n_bins, uint32_t scale = 1, uint32_t min_bins = 0) {
   constexpr int PER = (1 << SEG_BITS) / 1024;
@@ -412,7 +417,9 @@ __device__ __forceinline__ void cta_rank_scatter(const uint64_t (&v)[BS_IPT], in
   }
   __syncthreads();
   // block-wide exclusive scan of the 4096 counters in (digit, warp) order, 8 per thread
-  uint32_t* row = cnt + (tid >> 1) * CNT_LD + (tid & 1) * 8;
+  constexpr int TPD = BS_NW / 8;  // threads per digit row (8 warp counters each)
+  static_assert(BS_NW % 8 == 0 && RS_BINS * TPD == BS_NT, "one thread per 8 counters");
+  uint32_t* row = cnt + (tid / TPD) * CNT_LD + (tid % TPD) * 8;
   uint32_t x[8];
   uint32_t tsum = 0;
 #pragma unroll
@@ -743,7 +750,8 @@ __global__ void __launch_bounds__(BS_NT, BS_MINB) k_bin_build(const uint64_t* __
                                                         uint32_t* big, uint32_t* n_big, RunOut ro,
                                                         const uint2* __restrict__ table,
                                                         const uint32_t* __restrict__ binseg, uint32_t S,
-                                                        uint64_t* __restrict__ ent, DirRec* __restrict__ dir) {
+                                                        uint64_t* __restrict__ ent, DirRec* __restrict__ dir,
+                                                        uint32_t* bin_ctr) {
   extern __shared__ __align__(16) unsigned char bs_smem[];
   uint64_t* A = reinterpret_cast<uint64_t*>(bs_smem);
   uint64_t* Bf = A + BS_CAP;
@@ -759,14 +767,26 @@ __global__ void __launch_bounds__(BS_NT, BS_MINB) k_bin_build(const uint64_t* __
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint64_t lmask = (1ull << L) - 1, hmask = (1ull << hbits) - 1;
   const uint32_t nb = *n_bins;
-  for (uint32_t c = blockIdx.x; c < nb; c += gridDim.x) {
+  // Bins are claimed from a counter, one ahead (the first one is the CTA's index): a bin's cost varies
+  // several-fold (a mid bin ~2.5 average bins), and a static round-robin left the CTAs with the most
+  // of those running alone at the end (measured: 2056 mid bins cost 0.76 ms that way).
+  __shared__ uint32_t s_next[2];
+  uint32_t c = blockIdx.x, nxt = 0, it = 0;
+  if (threadIdx.x == 0) nxt = atomicAdd(bin_ctr, 1u) + gridDim.x;
+  while (c < nb) {
+    uint32_t nn = 0;
+    do {
     const uint64_t s = bstart[c], e = bstart[c + 1];
     const int n = (int)(e - s);
-    if (threadIdx.x == 0 && c + gridDim.x < nb) {  // the CTA's next bin into L2 while this one is sorted
-      const uint64_t s2 = bstart[c + gridDim.x], e2 = bstart[c + gridDim.x + 1];
-      if (e2 - s2 > 1 && e2 - s2 <= (uint64_t)BS_CAP) {
-        l2_prefetch_range(k + s2, (e2 - s2) * sizeof(uint64_t));
-        l2_prefetch_range(v + s2, (e2 - s2) * sizeof(uint32_t));
+    if (threadIdx.x == 0) {
+      s_next[it & 1u] = nxt;
+      nn = atomicAdd(bin_ctr, 1u) + gridDim.x;  // the bin after the next (its latency hides under this bin)
+      if (nxt < nb) {  // the CTA's next bin into L2 while this one is sorted
+        const uint64_t s2 = bstart[nxt], e2 = bstart[nxt + 1];
+        if (e2 - s2 > 1 && e2 - s2 <= (uint64_t)(2 * BS_CAP)) {
+          l2_prefetch_range(k + s2, (e2 - s2) * sizeof(uint64_t));
+          l2_prefetch_range(v + s2, (e2 - s2) * sizeof(uint32_t));
+        }
       }
     }
     if (n == 0) {  // an empty bin: its S slots are empty
@@ -775,12 +795,47 @@ __global__ void __launch_bounds__(BS_NT, BS_MINB) k_bin_build(const uint64_t* __
         o[0] = make_uint4((uint32_t)s, (uint32_t)s, 0xFFFFFFFFu, 0xFFFFFFFFu);
         o[1] = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
       }
-      continue;
+      break;
     }
-    if (n > BS_CAP) {
+    if (n > 2 * BS_CAP) {
       if (threadIdx.x == 0) big[atomicAdd(n_big, 1u)] = c;
-      continue;
+      break;
     }
+    const uint64_t* res = nullptr;
+    bool one = false;
+    uint64_t segv = 0;
+    const bool mid = n > BS_CAP;
+    if (mid) {
+      // BS_CAP < n <= 2 BS_CAP (a frequent hash on top of a full bin): the two buffers together hold the
+      // bin; an in-place bitonic sort of the packed values (unique, so no stability is needed), padded
+      // with ~0 to 2 BS_CAP.  (Through k_bucket_sort_big's chunked global-memory LSD such a bin cost
+      // ~150 us; measured, round 2.)
+      if (threadIdx.x == 0) atomicAdd(n_big + 2, 1u);  // statistics: bins sorted this way
+      constexpr int N2 = 2 * BS_CAP;
+      for (int i = threadIdx.x; i < N2; i += BS_NT) {
+        uint64_t xv = ~0ull;
+        if (i < n) {
+          const uint64_t kk = __ldcs(k + s + i);
+          const uint32_t pp = __ldcs(v + s + i);
+          xv = ((kk & lmask) << 33) | ((uint64_t)pp << 1) | (kk >> 63);
+        }
+        A[i] = xv;
+      }
+      segv = (k[s] & hmask) >> L;
+      __syncthreads();
+      for (int kk2 = 2; kk2 <= N2; kk2 <<= 1) {
+        for (int j = kk2 >> 1; j > 0; j >>= 1) {
+          for (int t = threadIdx.x; t < N2 / 2; t += BS_NT) {
+            const int lo = 2 * t - (t & (j - 1)), hi = lo + j;
+            const uint64_t a = A[lo], b = A[hi];
+            const bool up = (lo & kk2) == 0;
+            if ((a > b) == up) { A[lo] = b; A[hi] = a; }
+          }
+          __syncthreads();
+        }
+      }
+      res = A;
+    } else {
     uint64_t x[BS_IPT];
     uint32_t lmin = 0xFFFFFFFFu, lmax = 0;
     uint64_t seg = 0;
@@ -810,7 +865,7 @@ __global__ void __launch_bounds__(BS_NT, BS_MINB) k_bin_build(const uint64_t* __
     uint32_t mn = 0xFFFFFFFFu, mx = 0;
 #pragma unroll
     for (int q = 0; q < BS_NW; q++) { mn = min(mn, s_or[q]); mx = max(mx, s_and[q]); }
-    const uint64_t segv = wsum[0];
+    segv = wsum[0];
     __syncthreads();
     // K1 emits records in tile order (any order within a bin): one-hash bins and buckets of very
     // frequent hashes are put in (hash, pos) order by an LSD over the packed bits that vary
@@ -855,8 +910,8 @@ __global__ void __launch_bounds__(BS_NT, BS_MINB) k_bin_build(const uint64_t* __
       }
       return dst == A ? Bf : A;
     };
-    const bool one = mn == mx;  // one hash: sort by position
-    const uint64_t* res = one ? lsd_varying(33) : nullptr;
+    one = mn == mx;  // one hash: sort by position
+    res = one ? lsd_varying(33) : nullptr;
     if (!one) {
     // (1) MSD placement by the top 12 bits of low(h) - mn (4096 buckets, ~1 record each), then an
     //     insertion sort of each bucket on the full packed value (unique: it contains pos)
@@ -936,10 +991,12 @@ __global__ void __launch_bounds__(BS_NT, BS_MINB) k_bin_build(const uint64_t* __
       res = lsd_varying(33 + hib);
     }
     }  // !one
+    }  // !mid
     // K3 fused: runs never cross a bin (a hash lies in one bin).  Run heads mark NH[i] = i, a block
     // suffix minimum gives every i the next head >= i, and a head's run length is NH[i + 1] - i.
+    // (A mid bin fills both buffers: its run heads gallop to their run's end instead.)
     uint32_t* NH = reinterpret_cast<uint32_t*>(res == A ? Bf : A);  // [n + 1] (the non-result buffer)
-    if (!one) {
+    if (!one && !mid) {
       for (int i = threadIdx.x; i < n; i += BS_NT)
         NH[i] = (i == 0 || (uint32_t)(res[i - 1] >> 33) != (uint32_t)(res[i] >> 33)) ? (uint32_t)i : (uint32_t)n;
       if (threadIdx.x == 0) NH[n] = (uint32_t)n;
@@ -961,6 +1018,16 @@ __global__ void __launch_bounds__(BS_NT, BS_MINB) k_bin_build(const uint64_t* __
       const bool head = i == 0 || (uint32_t)(res[i - 1] >> 33) != lo;
       if (one) {
         if (i == 0) run_emit(ro, rh, (uint64_t)n, racc);
+      } else if (head && mid) {
+        int lo2 = i + 1, st = 1;  // gallop, then bisect, to the first record with another key
+        while (lo2 + st <= n && (uint32_t)(res[lo2 + st - 1] >> 33) == lo) { lo2 += st; st <<= 1; }
+        int hi2 = min(lo2 + st - 1, n);
+        while (lo2 < hi2) {
+          const int m2 = (lo2 + hi2) >> 1;
+          if ((uint32_t)(res[m2] >> 33) == lo) lo2 = m2 + 1;
+          else hi2 = m2;
+        }
+        run_emit(ro, rh, (uint64_t)(lo2 - i), racc);
       } else if (head) {
         run_emit(ro, rh, NH[i + 1] - (uint32_t)i, racc);
       }
@@ -1008,14 +1075,18 @@ __global__ void __launch_bounds__(BS_NT, BS_MINB) k_bin_build(const uint64_t* __
       o[0] = make_uint4((uint32_t)(s + a0), (uint32_t)(s + b0), kk[0], kk[1]);
       o[1] = make_uint4(kk[2], kk[3], kk[4], kk[5]);
     }
+    } while (0);
     __syncthreads();
+    c = s_next[it & 1u];
+    nxt = nn;
+    ++it;
   }
   run_flush(ro, rh, racc);
 }
 
 // oversized bins (repeat-heavy hashes): the same LSD over the low bits, chunk by chunk through
 // global memory (stable across chunks: chunks are taken in order, each digit's run appended)
-__global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort_big(uint64_t* __restrict__ k, uint32_t* __restrict__ v,
+__global__ void __launch_bounds__(BS_NT, BS_BIG_MINB) k_bucket_sort_big(uint64_t* __restrict__ k, uint32_t* __restrict__ v,
                                                               uint64_t* __restrict__ t0, uint64_t* __restrict__ t1,
                                                               const uint64_t* __restrict__ bstart, const uint32_t* big,
                                                               const uint32_t* n_big, int lo_bits, int hbits, RunOut ro,
@@ -1649,14 +1720,17 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
       uint2* table = scr.alloc<uint2>(1u << SEG_BITS);
       uint32_t* n_bins_d = scr.alloc<uint32_t>(1);
       GOD_CUDA(cudaMemsetAsync(segc, 0, (1u << SEG_BITS) * sizeof(uint32_t), st));
-      // exact counts: sampled widths (every 16th record, >= 1 bin per segment) made the bins uneven
-      // (k_bin_build 5.6 -> 6.2 ms for 0.13 ms saved in the histogram; measured, round 2)
-      const uint32_t seg_stride = getenv("GOD_SEG_SAMPLE") ? (uint32_t)std::max(1, atoi(getenv("GOD_SEG_SAMPLE"))) : 1u;
+      // large inputs: a 1/16 sample in whole 256-B blocks (k_seg_hist 0.44 -> 0.03 ms on human; the bins come
+      // out within ~2% of the target, which the dynamically claimed k_bin_build absorbs.  Round 2's
+      // first try, every 16th RECORD, still read every DRAM line and cost k_bin_build 0.6 ms under the
+      // static bin assignment of the time)
+      const uint32_t seg_stride = getenv("GOD_SEG_SAMPLE") ? (uint32_t)std::max(1, atoi(getenv("GOD_SEG_SAMPLE")))
+                                                           : (n >= (1ull << 24) ? 16u : 1u);
       GOD_LAUNCH("k_seg_hist", k_seg_hist, 4u * num_sms(), 512, 0, st, k0, n, L, segc, seg_stride);
       const char* bt = getenv("GOD_BIN_TARGET");  // test hook: bin size (default BIN_TARGET)
       const uint64_t base_target = bt ? std::max(1, atoi(bt)) : BIN_TARGET;
       const uint32_t target =
-          (uint32_t)std::max<uint64_t>(base_target, n / ((1u << (2 * BIN_DIGIT)) - (1u << SEG_BITS)) + 1);
+          (uint32_t)std::max<uint64_t>(base_target, (n + n / 16) / ((1u << (2 * BIN_DIGIT)) - (1u << SEG_BITS)) + 1);
       GOD_LAUNCH("k_seg_table", k_seg_table, 1, 1024, 0, st, segc, target, table, n_bins_d, seg_stride,
                  seg_stride > 1 ? 1u : 0u);
       // the first pass's tile histograms of the bins; the first scatter assigns the bins itself
@@ -1668,8 +1742,8 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
       const uint32_t nb = d2h_scalar(n_bins_d, st);
       uint64_t* bstart = scr.alloc<uint64_t>((uint64_t)nb + 1);
       uint32_t* big = scr.alloc<uint32_t>(nb ? nb : 1);
-      uint32_t* n_big = scr.alloc<uint32_t>(2);
-      GOD_CUDA(cudaMemsetAsync(n_big, 0, 2 * sizeof(uint32_t), st));
+      uint32_t* n_big = scr.alloc<uint32_t>(4);  // [1], [2]: statistics (bins sorted by the LSD / bitonic paths); [3]: bin claims
+      GOD_CUDA(cudaMemsetAsync(n_big, 0, 4 * sizeof(uint32_t), st));
       GOD_LAUNCH("k_bucket_bounds", k_bucket_bounds, grid_for((uint64_t)nb + 1, 256), 256, 0, st, k0, n, hbits, nb,
                  bstart);
       if (mode1) {
@@ -1684,7 +1758,7 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
         GOD_CUDA(cudaMallocAsync((void**)&ix->dir, std::max<uint64_t>(n_slots, 1) * sizeof(DirRec), st));
         GOD_CUDA(cudaMallocAsync((void**)&ix->ent, n * sizeof(uint64_t), st));
         GOD_LAUNCH("k_bin_build", k_bin_build, (unsigned)BS_MINB * num_sms(), BS_NT, BB_SMEM, st, k0, v0, bstart, n_bins_d, L, hbits,
-                   big, n_big, ro, table, nullptr, S_dir, ix->ent, ix->dir);
+                   big, n_big, ro, table, nullptr, S_dir, ix->ent, ix->dir, n_big + 3);
       } else {
         GOD_LAUNCH("k_bin_sort", k_bin_sort, (unsigned)BS_MINB * num_sms(), BS_NT, BS_SMEM, st, k0, v0, bstart, n_bins_d, L, hbits, big,
                    n_big, ro);
@@ -1692,10 +1766,10 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
       runs_done = true;
       const uint32_t hb_big = d2h_scalar(n_big, st);
       if (getenv("GOD_DEBUG_BUCKETS"))
-        fprintf(stderr, "[bins] n=%llu bins=%u target=%u big=%u lsd=%u S=%u\n", (unsigned long long)n, nb, target, hb_big,
-                d2h_scalar(n_big + 1, st), S_dir);
+        fprintf(stderr, "[bins] n=%llu bins=%u target=%u big=%u lsd=%u mid=%u S=%u\n", (unsigned long long)n, nb, target,
+                hb_big, d2h_scalar(n_big + 1, st), d2h_scalar(n_big + 2, st), S_dir);
       if (hb_big) {
-        GOD_LAUNCH("k_bucket_sort_big", k_bucket_sort_big, std::min(hb_big, (uint32_t)num_sms()), BS_NT, BS_SMEM, st, k0,
+        GOD_LAUNCH("k_bucket_sort_big", k_bucket_sort_big, std::min(hb_big, (uint32_t)(BS_BIG_MINB * num_sms())), BS_NT, BS_SMEM, st, k0,
                    v0, /*t0=*/k1, /*t1=*/k0, bstart, big, n_big, L, hbits, ro, built ? ix->ent : nullptr);
         if (built)
           GOD_LAUNCH("k_big_dir", k_big_dir, std::min(hb_big, 4u * (uint32_t)num_sms()), BS_NT, 0, st, k0, bstart, big,
