@@ -13,13 +13,15 @@ namespace god {
 static thread_local std::string g_err;
 void set_error(const std::string& msg) { g_err = msg; }
 
-int num_sms() {
-  static int n = 0;
+int num_sms() {  // of the current device
+  static int sms[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int& n = sms[dev & 63];
   if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    n = v > 0 ? v : 148;
   }
   return n;
 }
@@ -266,11 +268,15 @@ static uint64_t seed_reads_pipelined(const god_index* idx, const uint8_t* reads,
                                      god_phase_mode mode, uint8_t* phases, uint32_t t, void* anchors,
                                      uint64_t* anchor_offsets, uint64_t cap, uint32_t n_batches, cudaStream_t st,
                                      bool reads_on_device, bool compact, uint32_t* bad_compact) {
-  static cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
-  if (!s_h2d) {
-    GOD_CUDA(cudaStreamCreateWithFlags(&s_h2d, cudaStreamNonBlocking));
-    GOD_CUDA(cudaStreamCreateWithFlags(&s_d2h, cudaStreamNonBlocking));
-  }
+  static cudaStream_t h2d_of[64] = {nullptr}, d2h_of[64] = {nullptr};  // copy streams of each device
+  static DeviceOnce once;
+  int dev_ord = 0;
+  GOD_CUDA(cudaGetDevice(&dev_ord));
+  once.run([&] {
+    GOD_CUDA(cudaStreamCreateWithFlags(&h2d_of[dev_ord & 63], cudaStreamNonBlocking));
+    GOD_CUDA(cudaStreamCreateWithFlags(&d2h_of[dev_ord & 63], cudaStreamNonBlocking));
+  });
+  const cudaStream_t s_h2d = h2d_of[dev_ord & 63], s_d2h = d2h_of[dev_ord & 63];
   PipeSlot slot[2];
   for (auto& sl : slot) {
     GOD_CUDA(cudaEventCreateWithFlags(&sl.h2d_done, cudaEventDisableTiming));

@@ -5,6 +5,7 @@
 #include <cuda/atomic>
 #include <stdint.h>
 #include <string>
+#include <mutex>
 #include <vector>
 #include "god.h"
 
@@ -157,6 +158,23 @@ __device__ inline uint64_t lb_exclusive_warp(uint64_t* status, uint64_t tile, ui
   return excl;
 }
 
+// One-time setup per device (kernel attributes, streams and pool settings belong to a device): f runs
+// once for each device a call site is reached on, under a lock, before anyone passes.
+struct DeviceOnce {
+  std::mutex mu;
+  uint64_t done = 0;  // bit per device ordinal (mod 64)
+  template <class F>
+  void run(F f) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = 1ull << (dev & 63);
+    std::lock_guard<std::mutex> g(mu);
+    if (done & bit) return;
+    f();
+    done |= bit;
+  }
+};
+
 // ------------------------------------------------------------------------------------ memory
 // Stream-ordered scratch allocation (cudaMallocAsync pool), freed in reverse at scope exit.
 struct Scratch {
@@ -166,16 +184,16 @@ struct Scratch {
   // Keep freed pool memory mapped (release threshold = max): without this every synchronize
   // trims the pool and the next multi-GB cudaMallocAsync re-maps physical memory.
   static void keep_pool() {
-    static bool done = false;
-    if (done) return;
-    done = true;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t thr = ~0ull;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
+    static DeviceOnce once;
+    once.run([] {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      }
+    });
   }
   template <class T>
   T* alloc(size_t count) {

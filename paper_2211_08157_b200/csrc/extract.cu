@@ -357,11 +357,8 @@ void run_extract(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const 
   prof_add_units(tag, total_pos - n_jobs);  // kb = exclusive scan of nk + 1 (one separator per job)
   const int E = EX_T + 2 * (P.w - 1);
   const size_t smem = (size_t)E * (4 * sizeof(uint64_t) + sizeof(uint32_t) + 1);
-  static bool attr_set = false;
-  if (!attr_set) {
-    GOD_CUDA(cudaFuncSetAttribute(k_extract, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr_set = true;
-  }
+  static DeviceOnce attr_once;
+  attr_once.run([] { GOD_CUDA(cudaFuncSetAttribute(k_extract, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)); });
   uint64_t cap = cap_hint ? cap_hint : total_pos;
   if (cap > total_pos) cap = total_pos;
   uint64_t* status = scr.alloc<uint64_t>(ntiles);

@@ -1085,16 +1085,17 @@ size_t x2_smem_bytes() {
 template <int K, int W, int PP, int PX, bool ORDERED>
 void launch_x3(const X2Args& a, uint64_t ntiles, cudaStream_t st, const char* tag) {
   static int grid[64] = {0};  // per device
+  static DeviceOnce once;
   int dev = 0;
   GOD_CUDA(cudaGetDevice(&dev));
   const size_t smem = x2_smem_bytes<K, W, PP, PX, ORDERED>();
-  if (!grid[dev & 63]) {
+  once.run([&] {
     GOD_CUDA(cudaFuncSetAttribute(k_extract3<K, W, PP, PX, ORDERED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)smem));
     int per_sm = 0;
     GOD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_extract3<K, W, PP, PX, ORDERED>, X2_NT, smem));
     grid[dev & 63] = (per_sm > 0 ? per_sm : 1) * num_sms();
-  }
+  });
   const int g0 = grid[dev & 63];
   const unsigned g = (unsigned)(ntiles < (uint64_t)g0 ? ntiles : (uint64_t)g0);
   GOD_LAUNCH(tag, (k_extract3<K, W, PP, PX, ORDERED>), g, X2_NT, smem, st, a);

@@ -337,11 +337,8 @@ void seed_harness(const Params& P, const uint8_t* a, const uint8_t* b, const uin
   A.totals = totals;
   A.god_phase = god_phase;
   const size_t sm = 3 * HN_MAXL * sizeof(uint64_t);
-  static bool attr = false;
-  if (!attr) {
-    GOD_CUDA(cudaFuncSetAttribute(k_harness_seeds, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    attr = true;
-  }
+  static DeviceOnce attr_once;
+  attr_once.run([&] { GOD_CUDA(cudaFuncSetAttribute(k_harness_seeds, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); });
   GOD_LAUNCH("k_harness_seeds", k_harness_seeds, n, HN_NT, sm, st, A);
   GOD_LAUNCH("k_levenshtein", k_levenshtein, grid_for(n, 64), 64, 0, st, a, b, off, n, ed);
 }

@@ -38,6 +38,15 @@ constexpr int RS_BINS = 1 << RS_BITS;
 constexpr uint64_t HASH_BITS_MASK = (1ull << 63) - 1;
 constexpr int RS_DYN_SMEM = RS_TILE * (sizeof(uint64_t) + sizeof(uint32_t));
 constexpr int RS2_NT = 512, RS2_IPT = RS_TILE / RS2_NT;  // scatter: 16 warps, 8 items per thread
+// tiles per histogram column of the bin-sort passes: one CTA can scatter RS_GROUP consecutive tiles,
+// carrying its digit offsets from tile to tile, so that the tile histograms and their scan are
+// RS_GROUP times smaller.  Measured (human, both passes): the scan falls 0.49 -> 0.27 / 0.15 / 0.09 ms
+// at 2 / 4 / 8 but the scatter itself slows 4.61 -> 5.03 / 6.07 / 6.41 ms (a digit's 128-B output
+// line is then completed by one CTA over several tiles instead of by neighbouring CTAs at once), so 1.
+#ifndef RS_GROUP_DEF
+#define RS_GROUP_DEF 1
+#endif
+constexpr int RS_GROUP = RS_GROUP_DEF;
 
 // Lanes of the warp holding the same digit as this lane (digit < 2^NBITS; invalid lanes carry
 // d = 2^NBITS and only match each other): one ballot per digit bit.  Measured much cheaper than
@@ -61,15 +70,15 @@ __device__ __forceinline__ void l2_prefetch_range(const void* p, uint64_t bytes)
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((uint32_t)(e - a)) : "memory");
 }
 
-template <int RB>
+template <int RB, int G = 1>
 __global__ void __launch_bounds__(RS_NT) k_rs_hist(const uint64_t* __restrict__ keys, uint64_t n, int shift,
                                                    uint32_t dmask, uint32_t* hist, uint32_t ntiles) {
   __shared__ uint32_t h[(1 << RB)];
   for (int i = threadIdx.x; i < (1 << RB); i += RS_NT) h[i] = 0;
   __syncthreads();
-  const uint64_t base = (uint64_t)blockIdx.x * RS_TILE;
+  const uint64_t base = (uint64_t)blockIdx.x * RS_TILE * G;
 #pragma unroll 4
-  for (int r = 0; r < RS_IPT; r++) {
+  for (int r = 0; r < RS_IPT * G; r++) {
     uint64_t i = base + (uint64_t)r * RS_NT + threadIdx.x;
     if (i < n) atomicAdd(&h[(uint32_t)((keys[i] & HASH_BITS_MASK) >> shift) & dmask], 1u);
   }
@@ -82,22 +91,27 @@ __global__ void __launch_bounds__(RS_NT) k_rs_hist(const uint64_t* __restrict__ 
 // plus per-warp digit counters (no block barrier per item round).  STABLE = false (the first LSD
 // pass over records that arrive in any order anyway: K1's tile-order output): one SMEM atomic per
 // item on the warp's digit counter gives its rank (the ballot peer masks were ~36% of the pass).
-template <int RB, bool STABLE = true>
+template <int RB, bool STABLE = true, int G = 1>
 __global__ void __launch_bounds__(RS2_NT, 2) k_rs_scatter2(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin,
                                                        uint64_t* __restrict__ kout, uint32_t* __restrict__ vout,
                                                        uint64_t n, int shift, uint32_t dmask,
                                                        const uint64_t* __restrict__ goff, uint32_t ntiles,
                                                        const uint2* __restrict__ table, int L, uint32_t ahead) {
   __shared__ uint32_t wcnt[RS2_NT / 32][(1 << RB)];
-  __shared__ uint32_t dstart[(1 << RB)];
+  __shared__ uint32_t dstart[(1 << RB) + 1];
   __shared__ uint32_t wsum[(1 << RB) / 32];
   __shared__ uint64_t s_goff[1 << RB];
   extern __shared__ __align__(16) unsigned char rs_dyn[];
   uint64_t* sk = reinterpret_cast<uint64_t*>(rs_dyn);
   uint32_t* sv = reinterpret_cast<uint32_t*>(sk + RS_TILE);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  if (tid == 0) {  // the tile a CTA launched after the resident wave will take, into L2
-    const uint64_t t2 = (uint64_t)blockIdx.x + ahead;  // ahead = resident CTAs (2 per SM)
+  // ntiles = histogram columns = CTAs; CTA c scatters tiles c G .. c G + G - 1 in order
+  for (int d = tid; d < (1 << RB); d += RS2_NT) s_goff[d] = goff[(uint64_t)d * ntiles + blockIdx.x];
+  for (int sub = 0; sub < G; sub++) {
+  const uint64_t tile = (uint64_t)blockIdx.x * G + sub;
+  if (tile * RS_TILE >= n) break;
+  if (tid == 0) {  // into L2: this CTA's next tile, or (last tile) the first tile of the CTA launched after the resident wave
+    const uint64_t t2 = sub + 1 < G ? tile + 1 : ((uint64_t)blockIdx.x + ahead) * G;  // ahead = resident CTAs (2 per SM)
     if (t2 * RS_TILE < n) {
       const uint64_t c2 = min((uint64_t)RS_TILE, n - t2 * RS_TILE);
       l2_prefetch_range(kin + t2 * RS_TILE, c2 * sizeof(uint64_t));
@@ -105,9 +119,8 @@ __global__ void __launch_bounds__(RS2_NT, 2) k_rs_scatter2(const uint64_t* __res
     }
   }
   for (int i = tid; i < (RS2_NT / 32) * (1 << RB); i += RS2_NT) (&wcnt[0][0])[i] = 0;
-  for (int d = tid; d < (1 << RB); d += RS2_NT) s_goff[d] = goff[(uint64_t)d * ntiles + blockIdx.x];  // used at the end
   __syncthreads();
-  const uint64_t base = (uint64_t)blockIdx.x * RS_TILE + (uint64_t)wid * (32 * RS2_IPT);
+  const uint64_t base = tile * RS_TILE + (uint64_t)wid * (32 * RS2_IPT);
   const uint32_t lt = (1u << lane) - 1;
   uint64_t key[RS2_IPT];
   uint32_t val[RS2_IPT];
@@ -186,7 +199,7 @@ __global__ void __launch_bounds__(RS2_NT, 2) k_rs_scatter2(const uint64_t* __res
     }
   }
   __syncthreads();
-  const uint32_t cnt = (uint32_t)min((uint64_t)RS_TILE, n - (uint64_t)blockIdx.x * RS_TILE);
+  const uint32_t cnt = (uint32_t)min((uint64_t)RS_TILE, n - tile * RS_TILE);
   for (uint32_t s = tid; s < cnt; s += RS2_NT) {
     const uint64_t kk = sk[s];
     const uint32_t d = (uint32_t)((kk & HASH_BITS_MASK) >> shift) & dmask;
@@ -194,6 +207,12 @@ __global__ void __launch_bounds__(RS2_NT, 2) k_rs_scatter2(const uint64_t* __res
     GOD_DCHECK(dst < n, "LSD scatter destination");
     kout[dst] = kk;
     vout[dst] = sv[s];
+  }
+  if constexpr (G > 1) {  // the next tile of this CTA continues each digit's run
+    __syncthreads();
+    if (tid < (1 << RB)) s_goff[tid] += acc;
+    // (the next round's first barrier orders this against its readers)
+  }
   }
 }
 
@@ -358,9 +377,9 @@ __global__ void __launch_bounds__(RS_NT) k_seg_assign(uint64_t* __restrict__ k, 
   for (int i = threadIdx.x; i < (1 << BIN_DIGIT); i += RS_NT) hh[i] = 0;
   __syncthreads();
   const uint64_t lmask = (1ull << L) - 1;
-  const uint64_t base = (uint64_t)blockIdx.x * RS_TILE;
+  const uint64_t base = (uint64_t)blockIdx.x * RS_TILE * RS_GROUP;
 #pragma unroll 4
-  for (int r = 0; r < RS_IPT; r++) {
+  for (int r = 0; r < RS_IPT * RS_GROUP; r++) {
     const uint64_t i = base + (uint64_t)r * RS_NT + threadIdx.x;
     if (i < n) {
       const uint64_t kk = k[i];
@@ -1686,30 +1705,33 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
     const uint32_t ntiles = (uint32_t)((n + RS_TILE - 1) / RS_TILE);
     uint32_t* hist = scr.alloc<uint32_t>((uint64_t)(1u << BIN_DIGIT) * ntiles);
     uint64_t* goff = scr.alloc<uint64_t>((uint64_t)(1u << BIN_DIGIT) * ntiles);
-    static bool attr = false;
-    if (!attr) {
+    static DeviceOnce attr_once;
+    attr_once.run([] {
       GOD_CUDA(cudaFuncSetAttribute(k_rs_scatter2<RS_BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize, RS_DYN_SMEM));
-      GOD_CUDA(cudaFuncSetAttribute(k_rs_scatter2<BIN_DIGIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, RS_DYN_SMEM));
-      GOD_CUDA(cudaFuncSetAttribute(k_rs_scatter2<BIN_DIGIT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      GOD_CUDA(cudaFuncSetAttribute(k_rs_scatter2<BIN_DIGIT, true, RS_GROUP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    RS_DYN_SMEM));
+      GOD_CUDA(cudaFuncSetAttribute(k_rs_scatter2<BIN_DIGIT, false, RS_GROUP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     RS_DYN_SMEM));
       GOD_CUDA(cudaFuncSetAttribute(k_bin_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, BS_SMEM));
       GOD_CUDA(cudaFuncSetAttribute(k_bin_build, cudaFuncAttributeMaxDynamicSharedMemorySize, BB_SMEM));
       GOD_CUDA(cudaFuncSetAttribute(k_bucket_sort_big, cudaFuncAttributeMaxDynamicSharedMemorySize, BS_SMEM));
-      attr = true;
-    }
+    });
     const int hbits = 2 * P.k;
-    auto lsd_pass = [&](auto rb, int shift, int bits, bool have_hist = false, const uint2* table = nullptr,
+    // gc: tiles per CTA / histogram column (RS_GROUP on the bin-sort path, 1 on the full LSD)
+    auto lsd_pass = [&](auto rb, auto gc, int shift, int bits, bool have_hist = false, const uint2* table = nullptr,
                         int L = 0, bool stable = true) {
       constexpr int RB = decltype(rb)::value;
+      constexpr int G = decltype(gc)::value;
       const uint32_t dmask = (1u << bits) - 1;
-      if (!have_hist) GOD_LAUNCH("k_rs_hist", k_rs_hist<RB>, ntiles, RS_NT, 0, st, k0, n, shift, dmask, hist, ntiles);
-      scan_exclusive_u32_to_u64(hist, goff, (uint64_t)(1u << RB) * ntiles, nullptr, st, scr, "scan_sort_hist");
+      const uint32_t ncols = (ntiles + G - 1) / G;
+      if (!have_hist) GOD_LAUNCH("k_rs_hist", (k_rs_hist<RB, G>), ncols, RS_NT, 0, st, k0, n, shift, dmask, hist, ncols);
+      scan_exclusive_u32_to_u64(hist, goff, (uint64_t)(1u << RB) * ncols, nullptr, st, scr, "scan_sort_hist");
       if (stable)
-        GOD_LAUNCH("k_rs_scatter", (k_rs_scatter2<RB, true>), ntiles, RS2_NT, RS_DYN_SMEM, st, k0, v0, k1, v1, n, shift,
-                   dmask, goff, ntiles, table, L, resident_ctas(k_rs_scatter2<RB, true>, RS2_NT, RS_DYN_SMEM));
+        GOD_LAUNCH("k_rs_scatter", (k_rs_scatter2<RB, true, G>), ncols, RS2_NT, RS_DYN_SMEM, st, k0, v0, k1, v1, n, shift,
+                   dmask, goff, ncols, table, L, resident_ctas(k_rs_scatter2<RB, true, G>, RS2_NT, RS_DYN_SMEM));
       else
-        GOD_LAUNCH("k_rs_scatter", (k_rs_scatter2<RB, false>), ntiles, RS2_NT, RS_DYN_SMEM, st, k0, v0, k1, v1, n, shift,
-                   dmask, goff, ntiles, table, L, resident_ctas(k_rs_scatter2<RB, false>, RS2_NT, RS_DYN_SMEM));
+        GOD_LAUNCH("k_rs_scatter", (k_rs_scatter2<RB, false, G>), ncols, RS2_NT, RS_DYN_SMEM, st, k0, v0, k1, v1, n, shift,
+                   dmask, goff, ncols, table, L, resident_ctas(k_rs_scatter2<RB, false, G>, RS2_NT, RS_DYN_SMEM));
       std::swap(k0, k1);
       std::swap(v0, v1);
     };
@@ -1729,16 +1751,28 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
       GOD_LAUNCH("k_seg_hist", k_seg_hist, 4u * num_sms(), 512, 0, st, k0, n, L, segc, seg_stride);
       const char* bt = getenv("GOD_BIN_TARGET");  // test hook: bin size (default BIN_TARGET)
       const uint64_t base_target = bt ? std::max(1, atoi(bt)) : BIN_TARGET;
+      // Two LSD passes order up to 2^18 bins.  An input that would need bins above the target for that
+      // (human '1': 517 M records) takes a third pass over the bin bits that fit above the hash instead:
+      // bins beyond the SMEM capacity fall to the bitonic / global paths (measured on human '1': stage 3
+      // 46 ms with 2 passes and 2125-record bins against the 2048 capacity).
+      const int bin_bits_max = std::min(3 * BIN_DIGIT, 63 - hbits);
+      const bool three = !getenv("GOD_BIN_2PASS") && bin_bits_max > 2 * BIN_DIGIT &&
+                         ((n + n / 16) / ((1u << (2 * BIN_DIGIT)) - (1u << SEG_BITS)) + 1 > base_target ||
+                          getenv("GOD_BIN_3PASS"));
+      const int bin_bits = three ? bin_bits_max : 2 * BIN_DIGIT;
       const uint32_t target =
-          (uint32_t)std::max<uint64_t>(base_target, (n + n / 16) / ((1u << (2 * BIN_DIGIT)) - (1u << SEG_BITS)) + 1);
+          (uint32_t)std::max<uint64_t>(base_target, (n + n / 16) / ((1ull << bin_bits) - (1u << SEG_BITS)) + 1);
       GOD_LAUNCH("k_seg_table", k_seg_table, 1, 1024, 0, st, segc, target, table, n_bins_d, seg_stride,
                  seg_stride > 1 ? 1u : 0u);
       // the first pass's tile histograms of the bins; the first scatter assigns the bins itself
-      GOD_LAUNCH("k_seg_assign", k_seg_assign, ntiles, RS_NT, 0, st, k0, n, L, hbits, table, (1u << BIN_DIGIT) - 1, hist,
-                 ntiles, 0);
+      const uint32_t ncols = (ntiles + RS_GROUP - 1) / RS_GROUP;
+      GOD_LAUNCH("k_seg_assign", k_seg_assign, ncols, RS_NT, 0, st, k0, n, L, hbits, table, (1u << BIN_DIGIT) - 1, hist,
+                 ncols, 0);
       // the first pass need not be stable: the records arrive from K1 in tile order
-      lsd_pass(std::integral_constant<int, BIN_DIGIT>(), hbits, BIN_DIGIT, true, table, L, getenv("GOD_RS_STABLE1") != nullptr);
-      lsd_pass(std::integral_constant<int, BIN_DIGIT>(), hbits + BIN_DIGIT, BIN_DIGIT);
+      using GC = std::integral_constant<int, RS_GROUP>;
+      lsd_pass(std::integral_constant<int, BIN_DIGIT>(), GC(), hbits, BIN_DIGIT, true, table, L, getenv("GOD_RS_STABLE1") != nullptr);
+      lsd_pass(std::integral_constant<int, BIN_DIGIT>(), GC(), hbits + BIN_DIGIT, BIN_DIGIT);
+      if (three) lsd_pass(std::integral_constant<int, BIN_DIGIT>(), GC(), hbits + 2 * BIN_DIGIT, bin_bits - 2 * BIN_DIGIT);
       const uint32_t nb = d2h_scalar(n_bins_d, st);
       uint64_t* bstart = scr.alloc<uint64_t>((uint64_t)nb + 1);
       uint32_t* big = scr.alloc<uint32_t>(nb ? nb : 1);
@@ -1778,7 +1812,7 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
     } else {
       // K2 full stable LSD over the 2k hash bits (position order kept within equal hashes)
       for (int shift = 0; shift < hbits; shift += RS_BITS)
-        lsd_pass(std::integral_constant<int, RS_BITS>(), shift, std::min(RS_BITS, hbits - shift));
+        lsd_pass(std::integral_constant<int, RS_BITS>(), std::integral_constant<int, 1>(), shift, std::min(RS_BITS, hbits - shift));
     }
   }
   // K3: runs (distinct hashes) + count histogram (unless the bin sort produced them); K4: tau

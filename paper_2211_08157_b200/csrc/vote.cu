@@ -744,17 +744,16 @@ uint64_t vote_reads(const god_index* ix, const uint8_t* reads, const uint64_t* r
   A.res = res;
   A.cnt = cnt;
   A.bad = ctr + 6;
-  static bool attr = false;
+  static DeviceOnce attr_once;
   constexpr int WPB1 = 8, WPB2 = 4;
   const size_t sm_wsm = WPB1 * group_bytes(VOTE_WSM), sm_wsm2 = WPB2 * group_bytes(VOTE_WSM2),
                sm_mid = group_bytes(VOTE_MID);
-  if (!attr) {
+  attr_once.run([&] {
     GOD_CUDA(cudaFuncSetAttribute(k_vote_wsm<VOTE_WSM, WPB1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_wsm));
     GOD_CUDA(cudaFuncSetAttribute(k_vote_wsm<VOTE_WSM2, WPB2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)sm_wsm2));
     GOD_CUDA(cudaFuncSetAttribute(k_vote_mid, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_mid));
-    attr = true;
-  }
+  });
   if (h[0])
     GOD_LAUNCH("k_vote_warp16", k_vote_warp<16>, grid_for((uint64_t)h[0] * 16, VOTE_NT), VOTE_NT, 0, st, A, lists, h[0]);
   if (h[1])

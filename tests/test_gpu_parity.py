@@ -214,12 +214,16 @@ def test_index_probe_every_hash(k, w, mode0, monkeypatch):
     assert (want > 6).sum() > 100  # frequent hashes present: long slots
 
 
-@pytest.mark.parametrize("env", [{}, {"GOD_BIN_TARGET": "6000"}, {"GOD_BIN_TARGET": "40"}, {"GOD_DIR_MODE0": "1"},
-                                 {"GOD_SORT_FULL": "1"}],
-                         ids=["default", "big-bins", "tiny-bins", "dir-mode0", "full-lsd"])
+@pytest.mark.parametrize("env", [{}, {"GOD_BIN_TARGET": "6000"}, {"GOD_BIN_TARGET": "3000"}, {"GOD_BIN_TARGET": "40"},
+                                 {"GOD_DIR_MODE0": "1"}, {"GOD_SORT_FULL": "1"},
+                                 {"GOD_BIN_TARGET": "40", "GOD_BIN_3PASS": "1"}, {"GOD_SEG_SAMPLE": "3"}],
+                         ids=["default", "big-bins", "mid-bins", "tiny-bins", "dir-mode0", "full-lsd", "three-pass",
+                              "sampled-seg-hist"])
 def test_index_parity_sort_and_directory_variants(env, monkeypatch):
     """k = 21 on a repeat-rich reference through every sort/directory path: bins above the SMEM
-    capacity (chunked global kernel), one-record bins, the top-bit directory, the full LSD."""
+    capacity (chunked global kernel), bins between one and two capacities (in-SMEM bitonic path),
+    one-record bins, the top-bit directory, the full LSD, a third LSD pass over the bin bits (what an
+    input of > 373 M records takes), a block-sampled segment histogram."""
     for kk, vv in env.items():
         monkeypatch.setenv(kk, vv)
     ref = synth.dup_genome(3_000_000, 31, dup_frac=0.35, lmin=200, lmax=4000)
