@@ -91,13 +91,19 @@ __global__ void __launch_bounds__(RS_NT) k_rs_hist(const uint64_t* __restrict__ 
 // plus per-warp digit counters (no block barrier per item round).  STABLE = false (the first LSD
 // pass over records that arrive in any order anyway: K1's tile-order output): one SMEM atomic per
 // item on the warp's digit counter gives its rank (the ballot peer masks were ~36% of the pass).
+#ifndef RS_UNSTABLE_MINB
+#define RS_UNSTABLE_MINB 2
+#endif
 template <int RB, bool STABLE = true, int G = 1>
-__global__ void __launch_bounds__(RS2_NT, 2) k_rs_scatter2(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin,
+__global__ void __launch_bounds__(RS2_NT, STABLE ? 2 : RS_UNSTABLE_MINB) k_rs_scatter2(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin,
                                                        uint64_t* __restrict__ kout, uint32_t* __restrict__ vout,
                                                        uint64_t n, int shift, uint32_t dmask,
                                                        const uint64_t* __restrict__ goff, uint32_t ntiles,
                                                        const uint2* __restrict__ table, int L, uint32_t ahead) {
-  __shared__ uint32_t wcnt[RS2_NT / 32][(1 << RB)];
+  // STABLE: one counter row per warp (ranks in (warp, item, lane) order).  Unstable: one row for the
+  // CTA — the atomic's return value is the item's rank in its digit, no prefix over warps
+  constexpr int NROW = STABLE ? RS2_NT / 32 : 1;
+  __shared__ __align__(16) uint32_t wcnt[NROW][(1 << RB)];
   __shared__ uint32_t dstart[(1 << RB) + 1];
   __shared__ uint32_t wsum[(1 << RB) / 32];
   __shared__ uint64_t s_goff[1 << RB];
@@ -118,7 +124,7 @@ __global__ void __launch_bounds__(RS2_NT, 2) k_rs_scatter2(const uint64_t* __res
       l2_prefetch_range(vin + t2 * RS_TILE, c2 * sizeof(uint32_t));
     }
   }
-  for (int i = tid; i < (RS2_NT / 32) * (1 << RB); i += RS2_NT) (&wcnt[0][0])[i] = 0;
+  for (int i = tid; i < NROW * (1 << RB) / 4; i += RS2_NT) reinterpret_cast<uint4*>(&wcnt[0][0])[i] = make_uint4(0, 0, 0, 0);
   __syncthreads();
   const uint64_t base = tile * RS_TILE + (uint64_t)wid * (32 * RS2_IPT);
   const uint32_t lt = (1u << lane) - 1;
@@ -148,7 +154,7 @@ __global__ void __launch_bounds__(RS2_NT, 2) k_rs_scatter2(const uint64_t* __res
     const bool ok = i < n;
     const uint32_t d = ok ? ((uint32_t)((key[j] & HASH_BITS_MASK) >> shift) & dmask) : (1 << RB);
     if constexpr (!STABLE) {
-      rk[j] = ok ? atomicAdd(&wcnt[wid][d], 1u) : 0u;
+      rk[j] = ok ? atomicAdd(&wcnt[0][d], 1u) : 0u;
       continue;
     }
     const uint32_t peers = warp_peers<RB>(d);
@@ -165,11 +171,15 @@ __global__ void __launch_bounds__(RS2_NT, 2) k_rs_scatter2(const uint64_t* __res
   // digit tid (< 256): exclusive prefix over warps, tile total
   uint32_t acc = 0;
   if (tid < (1 << RB)) {
+    if constexpr (STABLE) {
 #pragma unroll
-    for (int q = 0; q < RS2_NT / 32; q++) {
-      const uint32_t c = wcnt[q][tid];
-      wcnt[q][tid] = acc;
-      acc += c;
+      for (int q = 0; q < RS2_NT / 32; q++) {
+        const uint32_t c = wcnt[q][tid];
+        wcnt[q][tid] = acc;
+        acc += c;
+      }
+    } else {
+      acc = wcnt[0][tid];
     }
   }
   // exclusive scan of the tile totals over the 256 digits (warps 0..7)
@@ -193,7 +203,7 @@ __global__ void __launch_bounds__(RS2_NT, 2) k_rs_scatter2(const uint64_t* __res
     const uint64_t i = base + (uint64_t)j * 32 + lane;
     if (i < n) {
       const uint32_t d = (uint32_t)((key[j] & HASH_BITS_MASK) >> shift) & dmask;
-      const uint32_t slot = dstart[d] + wcnt[wid][d] + rk[j];
+      const uint32_t slot = dstart[d] + (STABLE ? wcnt[wid][d] : 0u) + rk[j];
       sk[slot] = key[j];
       sv[slot] = val[j];
     }

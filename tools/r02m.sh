@@ -1,0 +1,11 @@
+mkdir -p gpurun_out/r02c
+for v in "" u3; do
+export GOD_LIB_VARIANT=$v
+timeout 300 python -m pytest tests/test_gpu_parity.py -q -x -k "index or repeat or probe" > gpurun_out/r02c/parity_idx_$v.log 2>&1; tail -1 gpurun_out/r02c/parity_idx_$v.log
+timeout 300 python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline --no-vote > gpurun_out/r02c/bench_$v.json 2> gpurun_out/r02c/bench_$v.err
+python - <<PY
+import json
+d=json.loads(open('gpurun_out/r02c/bench_$v.json').read().strip().splitlines()[-1])
+print('$v', d['ms_per_step'], d['stage_ms'], {k:v['ms_per_step'] for k,v in d['kernels'].items() if k in ('k_rs_scatter','k_rs_hist','k_seg_assign','scan_sort_hist','k_bin_build')})
+PY
+done
