@@ -146,7 +146,7 @@ __global__ void k_read_anchor_counts1(const uint32_t* __restrict__ cnt, const ui
   for (uint64_t g = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / RG; g < n_reads;
        g += (uint64_t)gridDim.x * blockDim.x / RG) {
     const uint32_t r = (uint32_t)g;
-    const uint64_t j = (uint64_t)r * p + phases[r];
+    const uint64_t j = (uint64_t)r * p + (phases ? phases[r] : 0u);
     const uint64_t b = job_off[j], e = job_end[j];
     uint64_t acc = 0;
     for (uint64_t q = b + l; q < e; q += RG) acc += cnt[q] & CNT_MASK;
@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(256, GOD_AW_MINB) k_anchor_write1(IndexView v,
     const uint32_t r = (uint32_t)g;
     // the read's phase and the record ranges of all its phase jobs are loaded together (lane s holds
     // job s), then the chosen one is taken by shuffle: one dependent round trip less per read
-    const uint32_t a_ph = phases[r];
+    const uint32_t a_ph = phases ? phases[r] : 0u;
     uint64_t b, e;
     if (p <= (uint32_t)RG) {
       const uint64_t jl = (uint64_t)r * p + (l < p ? l : 0u);
@@ -515,28 +515,33 @@ uint64_t seed_reads(const god_index* ix, const uint8_t* reads, const uint64_t* o
     }
   }
   if (h3) probe_all(v, rec3, st, scr);
-  if (have_phase_records && nr == 0 && h3 == 0) {
-    // ---------------- S4 fast path: every read's PQ_a records are its phase-a job of S1
+  // ---------------- S4 fast path: every read's PQ_a records are one job of one extraction, (a) its
+  // phase-a job of S1 (short reads in SELECT mode), or (b) its job of the dedicated extraction when
+  // that covered every read in read order (p = 1, GIVEN mode) and reads are short (long reads keep the
+  // per-record writer, which balances their thousands of records over the threads)
+  auto fast_path = [&](const Records& rc, const uint8_t* ph, uint32_t pp, bool have_counts) -> uint64_t {
     uint64_t* total = scr.alloc<uint64_t>(1);
-    if (!counted)
+    if (!have_counts)
       GOD_LAUNCH("k_read_anchor_counts", k_read_anchor_counts1, grid_for((uint64_t)n_reads * RG, 256), 256, 0, st,
-                 rec1.cnt, rec1.job_off, rec1.job_end, phases, p, n_reads, anchor_offsets);
+                 rc.cnt, rc.job_off, rc.job_end, ph, pp, n_reads, anchor_offsets);
     scan_exclusive_u64(anchor_offsets, anchor_offsets, n_reads, total, st, scr, "scan_read_anchors");
     GOD_CUDA(cudaMemcpyAsync(anchor_offsets + n_reads, total, sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
     const uint64_t tot = d2h_scalar(total, st);
-    if (tot <= cap)
-    {
+    if (tot <= cap) {
       if ((reinterpret_cast<uintptr_t>(anchors) & 15u) == 0)
         GOD_LAUNCH("k_anchor_write", k_anchor_write1<true>, grid_for((uint64_t)n_reads * RG, 256), 256, 0, st, v,
-                   rec1.hz, rec1.pos, rec1.cnt, rec1.beg, rec1.job_off, rec1.job_end, phases, p, n_reads, anchor_offsets, anchors,
+                   rc.hz, rc.pos, rc.cnt, rc.beg, rc.job_off, rc.job_end, ph, pp, n_reads, anchor_offsets, anchors,
                    rid_base);
       else
         GOD_LAUNCH("k_anchor_write", k_anchor_write1<false>, grid_for((uint64_t)n_reads * RG, 256), 256, 0, st, v,
-                   rec1.hz, rec1.pos, rec1.cnt, rec1.beg, rec1.job_off, rec1.job_end, phases, p, n_reads, anchor_offsets, anchors,
+                   rc.hz, rc.pos, rc.cnt, rc.beg, rc.job_off, rc.job_end, ph, pp, n_reads, anchor_offsets, anchors,
                    rid_base);
     }
     return tot;
-  }
+  };
+  if (have_phase_records && nr == 0 && h3 == 0) return fast_path(rec1, phases, p, counted);
+  if (h3 == n_reads && nr == 0 && rec3.n <= 64ull * n_reads && !getenv("GOD_SEED_GENERAL"))
+    return fast_path(rec3, nullptr, 1, false);  // one job per read, in read order
   SeedSources S{};
   S.hz[0] = rec1.hz; S.pos[0] = rec1.pos; S.off[0] = rec1.job_off; S.cnt[0] = rec1.cnt; S.beg[0] = rec1.beg;
   S.hz[1] = rec2.hz; S.pos[1] = rec2.pos; S.off[1] = rec2.job_off; S.cnt[1] = rec2.cnt; S.beg[1] = rec2.beg;
