@@ -77,10 +77,24 @@ __global__ void __launch_bounds__(RS_NT) k_rs_hist(const uint64_t* __restrict__ 
   for (int i = threadIdx.x; i < (1 << RB); i += RS_NT) h[i] = 0;
   __syncthreads();
   const uint64_t base = (uint64_t)blockIdx.x * RS_TILE * G;
+  if (base + (uint64_t)RS_TILE * G <= n) {  // a full tile: two keys per 128-bit load, all loads in flight
+    const ulonglong2* k2 = reinterpret_cast<const ulonglong2*>(keys + base);
+    ulonglong2 kv[RS_IPT / 2];
+    for (int g = 0; g < G; g++) {
+#pragma unroll
+      for (int r = 0; r < RS_IPT / 2; r++) kv[r] = __ldcs(k2 + (size_t)g * (RS_TILE / 2) + r * RS_NT + threadIdx.x);
+#pragma unroll
+      for (int r = 0; r < RS_IPT / 2; r++) {
+        atomicAdd(&h[(uint32_t)((kv[r].x & HASH_BITS_MASK) >> shift) & dmask], 1u);
+        atomicAdd(&h[(uint32_t)((kv[r].y & HASH_BITS_MASK) >> shift) & dmask], 1u);
+      }
+    }
+  } else {
 #pragma unroll 4
-  for (int r = 0; r < RS_IPT * G; r++) {
-    uint64_t i = base + (uint64_t)r * RS_NT + threadIdx.x;
-    if (i < n) atomicAdd(&h[(uint32_t)((keys[i] & HASH_BITS_MASK) >> shift) & dmask], 1u);
+    for (int r = 0; r < RS_IPT * G; r++) {
+      uint64_t i = base + (uint64_t)r * RS_NT + threadIdx.x;
+      if (i < n) atomicAdd(&h[(uint32_t)((keys[i] & HASH_BITS_MASK) >> shift) & dmask], 1u);
+    }
   }
   __syncthreads();
   for (int d = threadIdx.x; d < (1 << RB); d += RS_NT) hist[(uint64_t)d * ntiles + blockIdx.x] = h[d];
@@ -388,16 +402,31 @@ __global__ void __launch_bounds__(RS_NT) k_seg_assign(uint64_t* __restrict__ k, 
   __syncthreads();
   const uint64_t lmask = (1ull << L) - 1;
   const uint64_t base = (uint64_t)blockIdx.x * RS_TILE * RS_GROUP;
+  auto one = [&](uint64_t i, uint64_t kk) {
+    const uint64_t h = kk & HASH_BITS_MASK;
+    const uint2 t = __ldg(table + (h >> L));
+    const uint64_t b = t.x + (((h & lmask) * t.y) >> L);
+    if (write_keys) k[i] = kk | (b << hbits);
+    atomicAdd(&hh[(uint32_t)b & dmask], 1u);
+  };
+  if (base + (uint64_t)RS_TILE * RS_GROUP <= n) {  // a full tile: two keys per 128-bit load, all loads in flight
+    const ulonglong2* k2 = reinterpret_cast<const ulonglong2*>(k + base);
+    ulonglong2 kv[RS_IPT / 2];
+    for (int g = 0; g < RS_GROUP; g++) {
+#pragma unroll
+      for (int r = 0; r < RS_IPT / 2; r++) kv[r] = __ldcs(k2 + (size_t)g * (RS_TILE / 2) + r * RS_NT + threadIdx.x);
+#pragma unroll
+      for (int r = 0; r < RS_IPT / 2; r++) {
+        const uint64_t i = base + (uint64_t)g * RS_TILE + 2 * ((uint64_t)r * RS_NT + threadIdx.x);
+        one(i, kv[r].x);
+        one(i + 1, kv[r].y);
+      }
+    }
+  } else {
 #pragma unroll 4
-  for (int r = 0; r < RS_IPT * RS_GROUP; r++) {
-    const uint64_t i = base + (uint64_t)r * RS_NT + threadIdx.x;
-    if (i < n) {
-      const uint64_t kk = k[i];
-      const uint64_t h = kk & HASH_BITS_MASK;
-      const uint2 t = __ldg(table + (h >> L));
-      const uint64_t b = t.x + (((h & lmask) * t.y) >> L);
-      if (write_keys) k[i] = kk | (b << hbits);
-      atomicAdd(&hh[(uint32_t)b & dmask], 1u);
+    for (int r = 0; r < RS_IPT * RS_GROUP; r++) {
+      const uint64_t i = base + (uint64_t)r * RS_NT + threadIdx.x;
+      if (i < n) one(i, k[i]);
     }
   }
   __syncthreads();

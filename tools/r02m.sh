@@ -1,5 +1,5 @@
 mkdir -p gpurun_out/r02c
-for v in "" u3; do
+for v in ""; do
 export GOD_LIB_VARIANT=$v
 timeout 300 python -m pytest tests/test_gpu_parity.py -q -x -k "index or repeat or probe" > gpurun_out/r02c/parity_idx_$v.log 2>&1; tail -1 gpurun_out/r02c/parity_idx_$v.log
 timeout 300 python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline --no-vote > gpurun_out/r02c/bench_$v.json 2> gpurun_out/r02c/bench_$v.err
