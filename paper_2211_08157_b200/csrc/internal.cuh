@@ -8,7 +8,7 @@ namespace god {
 // and a global position base for the reference).  Its k-mer starts occupy the global
 // position range [kb[j], kb[j] + nk] of the extraction index space; the last slot is a separator
 // (a window barrier) so that no window ever spans two jobs.
-struct Job {
+struct __align__(16) Job {  // 32 B: two 128-bit accesses
   uint64_t seq_off;   // first byte of the sequence
   uint64_t len;       // bytes
   uint64_t pos_base;  // added to output positions

@@ -22,11 +22,33 @@ __global__ void __launch_bounds__(SCAN_NT) k_scan(const TIn* in, uint64_t* out, 
   const uint64_t base = tile * SCAN_TILE + (uint64_t)threadIdx.x * SCAN_IPT;
   uint64_t v[SCAN_IPT];
   uint64_t sum = 0;
+  // a full tile of 16-B aligned arrays: 128-bit loads and stores (a thread's 16 items are contiguous)
+  const bool vec = base + SCAN_IPT <= n && ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15u) == 0;
+  if (vec) {
+    if constexpr (sizeof(TIn) == 4) {
+      const uint4* p4 = reinterpret_cast<const uint4*>(in + base);
 #pragma unroll
-  for (int i = 0; i < SCAN_IPT; i++) {
-    uint64_t idx = base + i;
-    v[i] = idx < n ? (uint64_t)in[idx] : 0;
-    sum += v[i];
+      for (int i = 0; i < SCAN_IPT / 4; i++) {
+        const uint4 q = p4[i];
+        v[4 * i] = q.x; v[4 * i + 1] = q.y; v[4 * i + 2] = q.z; v[4 * i + 3] = q.w;
+      }
+    } else {
+      const ulonglong2* p2 = reinterpret_cast<const ulonglong2*>(in + base);
+#pragma unroll
+      for (int i = 0; i < SCAN_IPT / 2; i++) {
+        const ulonglong2 q = p2[i];
+        v[2 * i] = q.x; v[2 * i + 1] = q.y;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < SCAN_IPT; i++) sum += v[i];
+  } else {
+#pragma unroll
+    for (int i = 0; i < SCAN_IPT; i++) {
+      uint64_t idx = base + i;
+      v[i] = idx < n ? (uint64_t)in[idx] : 0;
+      sum += v[i];
+    }
   }
   // block exclusive scan of per-thread sums
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -52,11 +74,21 @@ __global__ void __launch_bounds__(SCAN_NT) k_scan(const TIn* in, uint64_t* out, 
   }
   __syncthreads();
   uint64_t run = s_excl + (wid ? warp_sum[wid - 1] : 0) + x - sum;
+  if (vec) {
+    ulonglong2* o2 = reinterpret_cast<ulonglong2*>(out + base);
 #pragma unroll
-  for (int i = 0; i < SCAN_IPT; i++) {
-    uint64_t idx = base + i;
-    if (idx < n) out[idx] = run;
-    run += v[i];
+    for (int i = 0; i < SCAN_IPT / 2; i++) {
+      const uint64_t a = run, b = run + v[2 * i];
+      run = b + v[2 * i + 1];
+      o2[i] = make_ulonglong2(a, b);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < SCAN_IPT; i++) {
+      uint64_t idx = base + i;
+      if (idx < n) out[idx] = run;
+      run += v[i];
+    }
   }
   if (total && tile == (n + SCAN_TILE - 1) / SCAN_TILE - 1 && threadIdx.x == SCAN_NT - 1) *total = run;
 }
