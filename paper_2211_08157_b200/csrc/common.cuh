@@ -57,6 +57,10 @@ Params make_params(const god_params* prm);   // validates (GOD_EINVAL) and build
 __host__ __device__ inline uint64_t included_count(const Pattern& P, uint64_t L, uint32_t s) {
   if (L <= s) return 0;
   uint64_t n = L - s;
+  if (n <= 0xFFFFFFFFull) {  // 32-bit division (a 64-bit one is ~100 instructions on the device)
+    const uint32_t n32 = (uint32_t)n;
+    return (uint64_t)(n32 / P.p) * P.x + P.ones_before[n32 % P.p];
+  }
   return (n / P.p) * P.x + P.ones_before[n % P.p];
 }
 __host__ __device__ inline uint64_t orig_of(const Pattern& P, uint64_t q, uint32_t s) {

@@ -249,8 +249,9 @@ __global__ void k_make_jobs(Params P, const uint64_t* offsets, uint32_t n_seqs, 
   const uint64_t nj = p_all ? (uint64_t)n_seqs * p_all : n_seqs;
   uint64_t acc = 0, mxb = 0;
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < nj; j += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t sidx = p_all ? j / p_all : j;
-    const uint32_t s = p_all ? (uint32_t)(j % p_all) : (phases ? phases[sidx] : 0u);
+    const uint32_t j32 = (uint32_t)j;  // nj < 2^31 (make_jobs)
+    const uint64_t sidx = p_all ? j32 / p_all : j32;
+    const uint32_t s = p_all ? j32 % p_all : (phases ? phases[sidx] : 0u);
     Job jb;
     jb.seq_off = offsets[sidx];
     jb.len = offsets[sidx + 1] - offsets[sidx];
@@ -262,11 +263,12 @@ __global__ void k_make_jobs(Params P, const uint64_t* offsets, uint32_t n_seqs, 
     jb.nk = (uint32_t)nk;
     jobs[j] = jb;
     if (x2) {
-      const uint64_t W = (uint64_t)P.w;
-      nkp1[j] = (nk ? (nk + W - 1) / W : 1) * W;
+      const uint32_t W = (uint32_t)P.w, nk32 = (uint32_t)nk;  // nk fits 32 bits (Job::nk)
+      const uint32_t blocks = nk32 ? (nk32 - 1) / W + 1 : 1u;  // ceil(nk / W)
+      nkp1[j] = (uint64_t)blocks * W;
       cw[j] = nk ? (nk + P.k - 1 + 15) / 16 : 0;
       acc += nk;
-      mxb = max(mxb, nk ? (nk + W - 1) / W : 1);
+      mxb = max(mxb, (uint64_t)blocks);
     } else {
       nkp1[j] = nk + 1;
     }
@@ -276,14 +278,16 @@ __global__ void k_make_jobs(Params P, const uint64_t* offsets, uint32_t n_seqs, 
       acc += __shfl_xor_sync(0xffffffffu, acc, d);
       mxb = max(mxb, __shfl_xor_sync(0xffffffffu, mxb, d));
     }
-    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(nk_sum, (unsigned long long)acc);
-    // blocks of the longest job: one atomic per CTA (a per-warp atomicMax on one word serialised)
-    __shared__ unsigned long long s_mx;
-    if (threadIdx.x == 0) s_mx = 0;
+    // one atomic per CTA on each of the two words (a per-warp atomic on one global word serialises:
+    // 625 k of them for the 20 M read jobs of the human step)
+    __shared__ unsigned long long s_mx, s_acc;
+    if (threadIdx.x == 0) { s_mx = 0; s_acc = 0; }
     __syncthreads();
     if ((threadIdx.x & 31) == 0 && mxb) atomicMax(&s_mx, (unsigned long long)mxb);
+    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(&s_acc, (unsigned long long)acc);
     __syncthreads();
     if (threadIdx.x == 0 && s_mx) atomicMax(nk_sum + 1, s_mx);
+    if (threadIdx.x == 0 && s_acc) atomicAdd(nk_sum, s_acc);
   }
 }
 }  // namespace
