@@ -26,6 +26,26 @@ int num_sms() {  // of the current device
   return n;
 }
 
+cudaMemPool_t god_pool(PoolKind kind) {
+  static cudaMemPool_t pools[64][3] = {};
+  static std::mutex mu;
+  int dev = 0;
+  GOD_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> g(mu);
+  cudaMemPool_t& p = pools[dev & 63][kind];
+  if (!p) {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    GOD_CUDA(cudaMemPoolCreate(&p, &props));
+    uint64_t thr = ~0ull;  // keep freed memory mapped
+    GOD_CUDA(cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &thr));
+  }
+  return p;
+}
+
 // ---------------------------------------------------------------------------------- tracing
 namespace {
 struct ProfPending { const char* name; cudaEvent_t a, b; };

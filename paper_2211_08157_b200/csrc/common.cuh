@@ -181,10 +181,21 @@ struct DeviceOnce {
 
 // ------------------------------------------------------------------------------------ memory
 // Stream-ordered scratch allocation (cudaMallocAsync pool), freed in reverse at scope exit.
+// Memory pools of the current device beside its default pool (api.cu): the index build's scratch and
+// the index's own storage each get one, so that a build and a seeding call, whose multi-GB blocks have
+// different sizes, never recycle each other's memory (alternating them in one pool made the allocator
+// re-map physical memory every step: 40 ms of host-side gaps per human '1110' step, measured).
+enum PoolKind { POOL_DEFAULT = 0, POOL_BUILD = 1, POOL_INDEX = 2 };
+cudaMemPool_t god_pool(PoolKind kind);
+
 struct Scratch {
   cudaStream_t st;
+  cudaMemPool_t pool = nullptr;  // null: the device's default pool
   std::vector<void*> ptrs;
-  explicit Scratch(cudaStream_t s) : st(s) { keep_pool(); }
+  explicit Scratch(cudaStream_t s, PoolKind kind = POOL_DEFAULT) : st(s) {
+    keep_pool();
+    if (kind != POOL_DEFAULT) pool = god_pool(kind);
+  }
   // Keep freed pool memory mapped (release threshold = max): without this every synchronize
   // trims the pool and the next multi-GB cudaMallocAsync re-maps physical memory.
   static void keep_pool() {
@@ -204,7 +215,8 @@ struct Scratch {
     void* p = nullptr;
     size_t bytes = count * sizeof(T);
     if (bytes == 0) bytes = 16;
-    GOD_CUDA(cudaMallocAsync(&p, bytes, st));
+    if (pool) GOD_CUDA(cudaMallocFromPoolAsync(&p, bytes, pool, st));
+    else GOD_CUDA(cudaMallocAsync(&p, bytes, st));
     ptrs.push_back(p);
     return static_cast<T*>(p);
   }

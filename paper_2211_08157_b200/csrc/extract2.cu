@@ -1068,13 +1068,14 @@ __global__ void k_x2_sizes(const Job* __restrict__ jobs, uint32_t n, int K, int 
     acc += __shfl_xor_sync(0xffffffffu, acc, d);
     mxb = max(mxb, __shfl_xor_sync(0xffffffffu, mxb, d));
   }
-  if ((threadIdx.x & 31) == 0 && acc) atomicAdd(nk_sum, (unsigned long long)acc);
-  __shared__ unsigned long long s_mx;  // blocks of the longest job: one atomic per CTA
-  if (threadIdx.x == 0) s_mx = 0;
+  __shared__ unsigned long long s_mx, s_acc;  // one global atomic per CTA on each word
+  if (threadIdx.x == 0) { s_mx = 0; s_acc = 0; }
   __syncthreads();
   if ((threadIdx.x & 31) == 0 && mxb) atomicMax(&s_mx, (unsigned long long)mxb);
+  if ((threadIdx.x & 31) == 0 && acc) atomicAdd(&s_acc, (unsigned long long)acc);
   __syncthreads();
   if (threadIdx.x == 0 && s_mx) atomicMax(nk_sum + 1, s_mx);
+  if (threadIdx.x == 0 && s_acc) atomicAdd(nk_sum, s_acc);
 }
 
 template <int K, int W, int PP, int PX, bool ORDERED>

@@ -1697,7 +1697,7 @@ inline uint32_t floor_log2(uint64_t v) { return v ? 63u - (uint32_t)__builtin_cl
 
 void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offsets, uint32_t n_refs,
                  const god_cutoff& cut, god_index* ix, cudaStream_t st) {
-  Scratch scr(st);
+  Scratch scr(st, POOL_BUILD);
   ix->P = P;
   memset(&ix->st, 0, sizeof(ix->st));
   ix->st.k = P.k; ix->st.w = P.w; ix->st.p = P.pat.p; ix->st.x = P.pat.x;
@@ -1826,10 +1826,10 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
         S_dir = std::max(1u, std::min(S_MAX, target / DIR_TARGET));
         n_slots = (uint64_t)S_dir * nb;
         GOD_REQUIRE(n < 0xFFFFFFFFull, "index has >= 2^32 entries");
-        GOD_CUDA(cudaMallocAsync((void**)&seg, (1u << SEG_BITS) * sizeof(uint2), st));
+        GOD_CUDA(cudaMallocFromPoolAsync((void**)&seg, (1u << SEG_BITS) * sizeof(uint2), god_pool(POOL_INDEX), st));
         GOD_LAUNCH("k_seg_slots", k_seg_slots, (1u << SEG_BITS) / 256, 256, 0, st, table, S_dir, seg);
-        GOD_CUDA(cudaMallocAsync((void**)&ix->dir, std::max<uint64_t>(n_slots, 1) * sizeof(DirRec), st));
-        GOD_CUDA(cudaMallocAsync((void**)&ix->ent, n * sizeof(uint64_t), st));
+        GOD_CUDA(cudaMallocFromPoolAsync((void**)&ix->dir, std::max<uint64_t>(n_slots, 1) * sizeof(DirRec), god_pool(POOL_INDEX), st));
+        GOD_CUDA(cudaMallocFromPoolAsync((void**)&ix->ent, n * sizeof(uint64_t), god_pool(POOL_INDEX), st));
         GOD_LAUNCH("k_bin_build", k_bin_build, (unsigned)BS_MINB * num_sms(), BS_NT, BB_SMEM, st, k0, v0, bstart, n_bins_d, L, hbits,
                    big, n_big, ro, table, nullptr, S_dir, ix->ent, ix->dir, n_big + 3);
       } else {
@@ -1877,7 +1877,7 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
       GOD_CUDA(cudaMemsetAsync(segc, 0, (1u << SEG_BITS) * sizeof(uint32_t), st));
       if (n) GOD_LAUNCH("k_seg_hist", k_seg_hist, 4u * num_sms(), 512, 0, st, k0, n, (int)(hb - SEG_BITS), segc, 1u);
     }
-    GOD_CUDA(cudaMallocAsync((void**)&seg, (1u << SEG_BITS) * sizeof(uint2), st));
+    GOD_CUDA(cudaMallocFromPoolAsync((void**)&seg, (1u << SEG_BITS) * sizeof(uint2), god_pool(POOL_INDEX), st));
     uint32_t* ns_d = scr.alloc<uint32_t>(1);
     GOD_LAUNCH("k_seg_table", k_seg_table, 1, 1024, 0, st, segc, DIR_TARGET, seg, ns_d);
     n_slots = d2h_scalar(ns_d, st);
@@ -1915,9 +1915,9 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
   }
   ix->n_ent = n_kept;
   ix->tau_probe = 0xFFFFFFFFu;
-  GOD_CUDA(cudaMallocAsync((void**)&ix->dir, n_slots * sizeof(DirRec), st));
+  GOD_CUDA(cudaMallocFromPoolAsync((void**)&ix->dir, n_slots * sizeof(DirRec), god_pool(POOL_INDEX), st));
   uint32_t* dir1 = scr.alloc<uint32_t>(n_slots + 1);  // first entry per slot (+ n_kept), then pairs
-  GOD_CUDA(cudaMallocAsync((void**)&ix->ent, (n_kept ? n_kept : 1) * sizeof(uint64_t), st));
+  GOD_CUDA(cudaMallocFromPoolAsync((void**)&ix->ent, (n_kept ? n_kept : 1) * sizeof(uint64_t), god_pool(POOL_INDEX), st));
   const uint64_t nd1 = n_slots + 1;
   GOD_CUDA(cudaMemsetAsync(dir1, 0xFF, nd1 * sizeof(uint32_t), st));
   if (n) {  // K5: kept entries (+ K6a: the first entry of every non-empty slot)
