@@ -75,6 +75,11 @@ struct X2Args {
   uint32_t aligned;     // tiles are whole jobs (k_x2_tile_desc_aligned): no halo blocks
   uint64_t ntiles;
   uint32_t no_stage;    // developer toggle (GOD_X2_NO_STAGE): direct global loads in the sparsify stage
+  // slotted output (position order without inter-CTA waiting): tile t writes its records at t * X2_CAP
+  // and its count to tile_cnt[t]; a scan and k_x2_compact close the gaps.  A tile with more than X2_CAP
+  // records sets *overflow (the caller then runs the look-back kernel instead)
+  uint32_t* tile_cnt;
+  uint32_t* overflow;
 };
 
 __device__ __forceinline__ uint32_t find_job_le(const uint64_t* arr, uint32_t lo, uint32_t hi, uint64_t g) {
@@ -316,27 +321,44 @@ __device__ __forceinline__ uint32_t pat_delta(uint32_t r, uint32_t i) {
 __device__ __forceinline__ void lb_publish(uint64_t* status, uint64_t tile, uint64_t local) {
   lb_store(&status[tile], (tile == 0 ? LB_INC : LB_AGG) | local);
 }
-// ... and resolve the exclusive prefix later (whole warp), publishing the inclusive prefix
+// ... and resolve the exclusive prefix later (whole warp), publishing the inclusive prefix.
+// The resident CTAs reach this point almost in lock-step (each resolves tile t after computing its
+// next tile), so a tile's predecessors mostly carry aggregates, not inclusive prefixes, and the walk
+// back spans the whole resident window (~600 tiles on 148 SMs).  LB_R rounds of 32 predecessors are
+// therefore loaded at once: ~3 dependent L2 round trips instead of ~18 (measured on HiFi reads, whose
+// long jobs need position order: extract_seed 19.2 -> see DESIGN.md §6).
+constexpr int LB_R = 8;
 __device__ inline uint64_t lb_resolve_warp(uint64_t* status, uint64_t tile, uint64_t local) {
   const int lane = threadIdx.x & 31;
   if (tile == 0) return 0;
-  uint64_t excl = 0;
-  int64_t j = (int64_t)tile - 1 - lane;
-  while (true) {
-    uint64_t s = j >= 0 ? lb_load(&status[j]) : (LB_INC | 0ull);
-    while (__any_sync(0xffffffffu, (s & ~LB_VAL) == 0)) {
-      __nanosleep(32);  // back off: a spinning warp takes issue slots from the CTAs doing the work
-      if ((s & ~LB_VAL) == 0) s = lb_load(&status[j]);
-    }
-    const uint32_t inc = __ballot_sync(0xffffffffu, (s & ~LB_VAL) == LB_INC);
-    const int first = inc ? __ffs(inc) - 1 : 32;
-    uint64_t v = lane <= first ? (s & LB_VAL) : 0ull;
+  uint64_t part = 0;  // this lane's share of the exclusive prefix
+  int64_t j0 = (int64_t)tile - 1;
+  bool done = false;
+  while (!done) {
+    uint64_t s[LB_R];
 #pragma unroll
-    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    excl += v;
-    if (inc) break;
-    j -= 32;
+    for (int r = 0; r < LB_R; r++) {
+      const int64_t j = j0 - 32 * r - lane;
+      s[r] = j >= 0 ? lb_load(&status[j]) : (LB_INC | 0ull);
+    }
+#pragma unroll
+    for (int r = 0; r < LB_R; r++) {
+      if (done) break;
+      const int64_t j = j0 - 32 * r - lane;
+      while (__any_sync(0xffffffffu, (s[r] & ~LB_VAL) == 0)) {
+        __nanosleep(32);  // back off: a spinning warp takes issue slots from the CTAs doing the work
+        if ((s[r] & ~LB_VAL) == 0) s[r] = lb_load(&status[j]);
+      }
+      const uint32_t inc = __ballot_sync(0xffffffffu, (s[r] & ~LB_VAL) == LB_INC);
+      const int first = inc ? __ffs(inc) - 1 : 32;
+      if (lane <= first) part += s[r] & LB_VAL;
+      done = inc != 0;
+    }
+    j0 -= 32 * LB_R;
   }
+  uint64_t excl = part;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) excl += __shfl_xor_sync(0xffffffffu, excl, o);
   if (lane == 0) lb_store(&status[tile], LB_INC | (excl + local));
   return excl;
 }
@@ -894,7 +916,19 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract3(X2Args a) {
       HZ = (HZ == HZ0) ? HZ0 + POS : HZ0;
       continue;
     }
-    if (tid == 0) s_base = atomicAdd(reinterpret_cast<unsigned long long*>(a.total_out), (unsigned long long)total);
+    if (a.tile_cnt) {
+      if (tid == 0) {
+        s_base = (uint64_t)tile * X2_CAP;
+        a.tile_cnt[tile] = total <= (uint32_t)X2_CAP ? total : 0u;
+        if (total > (uint32_t)X2_CAP) *a.overflow = 1u;
+      }
+      if (total > (uint32_t)X2_CAP) {  // (uniform) nothing is written: the caller falls back
+        __syncthreads();
+        continue;
+      }
+    } else if (tid == 0) {
+      s_base = atomicAdd(reinterpret_cast<unsigned long long*>(a.total_out), (unsigned long long)total);
+    }
     uint32_t rank = before + incl - cnt;
     if (total <= (uint32_t)X2_CAP && !a.out_job) {
       // stage the tile-local indices of the selected positions (u16, position order), then one
@@ -1078,6 +1112,29 @@ __global__ void k_x2_sizes(const Job* __restrict__ jobs, uint32_t n, int K, int 
   if (threadIdx.x == 0 && s_acc) atomicAdd(nk_sum, s_acc);
 }
 
+// slotted output -> contiguous: one warp per tile copies its records to the tile's scanned offset
+__global__ void k_x2_compact(const uint64_t* __restrict__ shz, const uint32_t* __restrict__ spos,
+                             const uint32_t* __restrict__ tile_cnt, const uint64_t* __restrict__ toff, uint64_t ntiles,
+                             uint64_t* __restrict__ hz, uint32_t* __restrict__ pos) {
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint64_t t = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / 32; t < ntiles;
+       t += (uint64_t)gridDim.x * blockDim.x / 32) {
+    const uint32_t c = tile_cnt[t];
+    const uint64_t src = t * X2_CAP, dst = toff[t];
+    for (uint32_t i = lane; i < c; i += 32) {
+      hz[dst + i] = __ldcs(shz + src + i);
+      pos[dst + i] = __ldcs(spos + src + i);
+    }
+  }
+}
+// a job's first record: slot coordinate (tile * X2_CAP + rank) -> index in the compacted records
+__global__ void k_x2_job_off_fix(uint64_t* job_off, uint32_t n_jobs, const uint64_t* __restrict__ toff) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n_jobs; j += gridDim.x * blockDim.x) {
+    const uint64_t v = job_off[j];
+    job_off[j] = toff[v / X2_CAP] + v % X2_CAP;
+  }
+}
+
 template <int K, int W, int PP, int PX, bool ORDERED>
 size_t x2_smem_bytes() {
   return X2Cfg<K, W, PP, PX>::smem(ORDERED);
@@ -1164,7 +1221,8 @@ bool run_extract2(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const
   // position order through the decoupled look-back.  Unordered instances exist for 2k >= 36.
   const bool can_unordered = 2 * K >= 36 && !want_job && !getenv("GOD_X2_ORDERED");
   const bool aligned = can_unordered && order == ORDER_JOB && max_jb <= X2_NT / 4 && !getenv("GOD_X2_NO_ALIGN");
-  const bool ordered = !(can_unordered && (order == ORDER_NONE || aligned));
+  // GOD_X2_FORCE_UNORDERED: developer timing aid (records of a multi-tile job are then NOT contiguous)
+  const bool ordered = !(can_unordered && (order == ORDER_NONE || aligned || getenv("GOD_X2_FORCE_UNORDERED")));
   const uint32_t S_al = (uint32_t)(X2_NT + 1 - max_jb);  // tile stride (blocks) of the aligned layout
   const uint64_t ntiles = aligned ? (total_blocks + S_al - 1) / S_al : (total_blocks + X2_OUT_BLOCKS - 1) / X2_OUT_BLOCKS;
   GOD_REQUIRE(ntiles < 0x7FFFFFFFull, "input too large for one extraction launch");
@@ -1203,6 +1261,64 @@ bool run_extract2(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const
     const int kbits = atoi(dbg);
     if (kbits > 0 && kbits < 2 * K) key_shift = std::min(2 * K - kbits, 31);  // keys of >= 2k - 31 bits
   }
+  // launch the specialised kernel for (K, W, pattern); ordered_kernel: the look-back instance
+  auto launch = [&](const X2Args& a, bool ordered_kernel) {
+    auto by_pattern = [&](auto kc, auto wc) {
+      constexpr int KK = decltype(kc)::value, WW = decltype(wc)::value;
+      auto go = [&](auto oc) {
+        constexpr bool O = decltype(oc)::value;
+        if (PX == 1 && PP == 1) launch_x3<KK, WW, 1, 1, O>(a, ntiles, st, tag);
+        else if (PX == 1 && PP == 2) launch_x3<KK, WW, 2, 1, O>(a, ntiles, st, tag);
+        else if (PX == 1) launch_x3<KK, WW, 3, 1, O>(a, ntiles, st, tag);
+        else if (PX == 2) launch_x3<KK, WW, 3, 2, O>(a, ntiles, st, tag);
+        else launch_x3<KK, WW, 4, 3, O>(a, ntiles, st, tag);
+      };
+      if (!ordered_kernel) go(std::false_type());
+      else go(std::true_type());
+    };
+    if (K == 21 && W == 11) by_pattern(std::integral_constant<int, 21>(), std::integral_constant<int, 11>());
+    else if (K == 19 && W == 19) by_pattern(std::integral_constant<int, 19>(), std::integral_constant<int, 19>());
+    else if (K == 19 && W == 16) by_pattern(std::integral_constant<int, 19>(), std::integral_constant<int, 16>());
+    else by_pattern(std::integral_constant<int, 15>(), std::integral_constant<int, 10>());
+  };
+  // Position order for jobs that span tiles (long reads), without inter-CTA waiting: the unordered
+  // kernel writes tile t's records at slot t * X2_CAP and its count; a scan of the counts and one copy
+  // close the gaps.  (The look-back instance spent 56% of its stall samples waiting for predecessor
+  // tiles on the HiFi reads: extract_seed 19.2 ms; measured, round 2.)
+  if (ordered && order == ORDER_JOB && !want_job && ntiles && !getenv("GOD_X2_NO_SLOTS")) {
+    const uint64_t scap = ntiles * (uint64_t)X2_CAP;
+    uint64_t* shz = scr.alloc<uint64_t>(scap);
+    uint32_t* spos = scr.alloc<uint32_t>(scap);
+    uint32_t* tile_cnt = scr.alloc<uint32_t>(ntiles);
+    uint32_t* overflow = scr.alloc<uint32_t>(1);
+    GOD_CUDA(cudaMemsetAsync(ctr, 0, sizeof(uint32_t), st));
+    GOD_CUDA(cudaMemsetAsync(overflow, 0, sizeof(uint32_t), st));
+    X2Args a{seq, seq_bytes, jobs, kb, cw, n_jobs, total_blocks, P.pat.one[0], key_shift, status, ctr,
+             shz, spos, nullptr, rec.job_off, nullptr, scap, dtotal, dbg_flags,
+             dbg_counts, desc, 0u, ntiles, getenv("GOD_X2_NO_STAGE") ? 1u : 0u, tile_cnt, overflow};
+    launch(a, false);
+    const uint32_t over = d2h_scalar(overflow, st);
+    if (getenv("GOD_DEBUG_SLOTS")) fprintf(stderr, "[x2] %s slotted tiles=%llu overflow=%u\n", tag, (unsigned long long)ntiles, over);
+    if (over == 0) {
+      uint64_t* toff = scr.alloc<uint64_t>(ntiles + 1);  // [ntiles] = the total (a job starting past the last record)
+      scan_exclusive_u32_to_u64(tile_cnt, toff, ntiles, dtotal, st, scr, "scan_x2_tiles");
+      GOD_CUDA(cudaMemcpyAsync(toff + ntiles, dtotal, sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
+      const uint64_t n = d2h_scalar(dtotal, st);
+      rec.cap = n ? n : 1;
+      rec.hz = scr.alloc<uint64_t>(rec.cap);
+      rec.pos = scr.alloc<uint32_t>(rec.cap);
+      rec.job = nullptr;
+      GOD_LAUNCH("k_x2_compact", k_x2_compact, grid_for(ntiles * 32, 256), 256, 0, st, shz, spos, tile_cnt, toff, ntiles,
+                 rec.hz, rec.pos);
+      if (want_job_off) {
+        GOD_LAUNCH("k_x2_job_off_fix", k_x2_job_off_fix, grid_for(n_jobs, 256), 256, 0, st, rec.job_off, n_jobs, toff);
+        GOD_CUDA(cudaMemcpyAsync(rec.job_off + n_jobs, dtotal, sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
+      }
+      rec.n = n;
+      return true;
+    }
+    // a tile with more than X2_CAP minimizers (all-ties runs): the look-back kernel below
+  }
   for (int attempt = 0; attempt < 2; attempt++) {
     rec.cap = cap;
     rec.hz = scr.alloc<uint64_t>(cap);
@@ -1213,30 +1329,9 @@ bool run_extract2(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const
     GOD_CUDA(cudaMemsetAsync(dtotal, 0, sizeof(uint64_t), st));  // the unordered kernel's output counter
     X2Args a{seq, seq_bytes, jobs, kb, cw, n_jobs, total_blocks, P.pat.one[0], key_shift, status, ctr,
              rec.hz, rec.pos, rec.job, rec.job_off, aligned ? rec.job_end : nullptr, cap, dtotal, dbg_flags,
-             dbg_counts, desc, aligned ? 1u : 0u, ntiles, getenv("GOD_X2_NO_STAGE") ? 1u : 0u};
+             dbg_counts, desc, aligned ? 1u : 0u, ntiles, getenv("GOD_X2_NO_STAGE") ? 1u : 0u, nullptr, nullptr};
     if (ntiles) {
-      auto by_pattern = [&](auto kc, auto wc) {
-        constexpr int KK = decltype(kc)::value, WW = decltype(wc)::value;
-        auto go = [&](auto oc) {
-          constexpr bool O = decltype(oc)::value;
-          if (PX == 1 && PP == 1) launch_x3<KK, WW, 1, 1, O>(a, ntiles, st, tag);
-          else if (PX == 1 && PP == 2) launch_x3<KK, WW, 2, 1, O>(a, ntiles, st, tag);
-          else if (PX == 1) launch_x3<KK, WW, 3, 1, O>(a, ntiles, st, tag);
-          else if (PX == 2) launch_x3<KK, WW, 3, 2, O>(a, ntiles, st, tag);
-          else launch_x3<KK, WW, 4, 3, O>(a, ntiles, st, tag);
-        };
-        // unordered instances only where a caller may ask for them (the index path, 2k >= 36)
-        if constexpr (2 * KK >= 36) {
-          if (!ordered) go(std::false_type());
-          else go(std::true_type());
-        } else {
-          go(std::true_type());
-        }
-      };
-      if (K == 21 && W == 11) by_pattern(std::integral_constant<int, 21>(), std::integral_constant<int, 11>());
-      else if (K == 19 && W == 19) by_pattern(std::integral_constant<int, 19>(), std::integral_constant<int, 19>());
-      else if (K == 19 && W == 16) by_pattern(std::integral_constant<int, 19>(), std::integral_constant<int, 16>());
-      else by_pattern(std::integral_constant<int, 15>(), std::integral_constant<int, 10>());
+      launch(a, ordered);
     } else {
       GOD_CUDA(cudaMemsetAsync(dtotal, 0, sizeof(uint64_t), st));
     }

@@ -304,6 +304,33 @@ def test_seed_parity_mixed_reads(pattern, k, w, t):
     _seed_parity(ix, ox, rs, ro, phases=ph, t=t)
 
 
+@pytest.mark.parametrize("pattern,k,w", [("10", 21, 11), ("1", 15, 10), ("110", 19, 19)])
+def test_seed_long_reads_slotted_and_overflow(pattern, k, w, monkeypatch, capfd):
+    """Long reads through the specialised kernel's slotted position-ordered output (tile t at slot
+    t * 512, then scan + copy), and its fallback to the look-back kernel: a homopolymer run makes every
+    position of a tile a minimizer (more than the 512 records a slot holds)."""
+    rng = np.random.default_rng(23)
+    ref = synth.dup_genome(600_000, 13, dup_frac=0.2, lmin=300, lmax=3000)
+    ref = np.concatenate([ref, np.frombuffer(b"A" * 9000, np.uint8), synth.random_acgt(rng, 5000)])
+    roffs_ref = np.array([0, ref.size], np.uint64)
+    ix = god.god_build_index(cu(ref), cu(roffs_ref), pattern, k, w, cutoff=(1, 100))
+    ox = oracle.Index(ref, roffs_ref, pattern, k, w, cutoff=(1, 100))
+    reads = synth.simulate_reads(ref, 60, 7, mu=9.0, sigma=0.5, lmin=2000, lmax=30000, p_sub=0.005, p_ins=0.002,
+                                 p_del=0.002)
+    seqs = [reads.seq[int(reads.offsets[i]):int(reads.offsets[i + 1])] for i in range(reads.n)]
+    monkeypatch.setenv("GOD_DEBUG_SLOTS", "1")
+    _seed_parity(ix, ox, *synth.concat(seqs))  # slotted path only
+    err = capfd.readouterr().err
+    assert "extract_seed slotted" in err and "overflow=1" not in err
+    seqs.insert(20, np.concatenate([synth.random_acgt(rng, 4000), np.frombuffer(b"A" * 8000, np.uint8),
+                                    synth.random_acgt(rng, 3000)]))
+    rs, ro = synth.concat(seqs)
+    _seed_parity(ix, ox, rs, ro)  # a tile overflows its slot: the look-back kernel
+    assert "overflow=1" in capfd.readouterr().err
+    ph = rng.integers(0, len(pattern), size=len(ro) - 1).astype(np.uint8)
+    _seed_parity(ix, ox, rs, ro, phases=ph)
+
+
 def test_seed_host_pointer_path():
     cfg = synth.make_config("tiny", read_scale=0.1)
     ix = god.god_build_index(cfg.ref, cfg.ref_offsets, "10", 21, 11)
