@@ -329,6 +329,9 @@ def test_seed_long_reads_slotted_and_overflow(pattern, k, w, monkeypatch, capfd)
     assert "overflow=1" in capfd.readouterr().err
     ph = rng.integers(0, len(pattern), size=len(ro) - 1).astype(np.uint8)
     _seed_parity(ix, ox, rs, ro, phases=ph)
+    monkeypatch.setenv("GOD_SEED_GENERAL", "1")  # the per-record writer behind the read-ordered copy
+    _seed_parity(ix, ox, rs, ro, phases=ph)
+    _seed_parity(ix, ox, rs, ro)
 
 
 def test_seed_host_pointer_path():
