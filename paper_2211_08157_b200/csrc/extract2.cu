@@ -1285,7 +1285,7 @@ bool run_extract2(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const
   // kernel writes tile t's records at slot t * X2_CAP and its count; a scan of the counts and one copy
   // close the gaps.  (The look-back instance spent 56% of its stall samples waiting for predecessor
   // tiles on the HiFi reads: extract_seed 19.2 ms; measured, round 2.)
-  if (ordered && order == ORDER_JOB && !want_job && ntiles && !getenv("GOD_X2_NO_SLOTS")) {
+  if (ordered && !want_job && ntiles && !getenv("GOD_X2_NO_SLOTS")) {  // ORDER_JOB across tiles, ORDER_GLOBAL
     const uint64_t scap = ntiles * (uint64_t)X2_CAP;
     uint64_t* shz = scr.alloc<uint64_t>(scap);
     uint32_t* spos = scr.alloc<uint32_t>(scap);
