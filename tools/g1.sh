@@ -1,4 +1,5 @@
 set -x
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/g1_gather tools/g1_gather.cu
 mkdir -p gpurun_out/g1
 ./tools/g1_gather > gpurun_out/g1/g1.jsonl; cat gpurun_out/g1/g1.jsonl
 ./tools/g1_gather 32 > gpurun_out/g1/g1_lim32.jsonl; cat gpurun_out/g1/g1_lim32.jsonl
