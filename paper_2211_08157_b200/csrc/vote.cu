@@ -578,7 +578,41 @@ __device__ void vote_group(const VoteArgs& A, uint32_t r, const GroupArrays& S, 
   const uint32_t W = S.ctr[1];
   const bool rescue = W == 0;
   const uint32_t limit = rescue ? 1u : (A.mp ? min(A.mp, W) : W);
-  if (!rescue) {
+  if (!rescue && W > 64) {
+    // step (4), many winners (a long read with a small V): sort the winner list by (votes desc, diagonal
+    // asc), the same all-ascending bitonic network with a virtual worst element past W, O(W log^2 W)
+    // instead of the W^2 comparisons of the counting below; aux[rank] = cluster for rank < limit
+    auto worse = [&](uint32_t ca, uint32_t cb) {  // cluster ca ranks after cluster cb
+      return better(S.cv[cb], S.key[S.chead[cb]] >> 29, S.cv[ca], S.key[S.chead[ca]] >> 29);
+    };
+    uint32_t lg = 0;
+    while ((1u << lg) < W) ++lg;
+    const uint32_t N2 = 1u << lg;
+    for (uint32_t ls = 1; ls <= lg; ++ls) {
+      const uint32_t lh = ls - 1, half = 1u << lh;
+      for (uint32_t q = t; q < N2 / 2; q += NT) {
+        const uint32_t base = (q >> lh) << ls, off = q & (half - 1);
+        const uint32_t i = base + off, j = base + (2u * half) - 1 - off;
+        if (j < W) {
+          const uint32_t x = S.crank[i], y = S.crank[j];
+          if (worse(x, y)) { S.crank[i] = y; S.crank[j] = x; }
+        }
+      }
+      gsync<NT>();
+      for (int lstr = (int)lh - 1; lstr >= 0; --lstr) {
+        const uint32_t stride = 1u << lstr;
+        for (uint32_t q = t; q < N2 / 2; q += NT) {
+          const uint32_t i = ((q >> lstr) << (lstr + 1)) | (q & (stride - 1)), j = i + stride;
+          if (j < W) {
+            const uint32_t x = S.crank[i], y = S.crank[j];
+            if (worse(x, y)) { S.crank[i] = y; S.crank[j] = x; }
+          }
+        }
+        gsync<NT>();
+      }
+    }
+    for (uint32_t w = t; w < limit; w += NT) S.aux[w] = S.crank[w];
+  } else if (!rescue) {
     // step (4): rank the winners; aux[rank] = cluster for rank < limit
     for (uint32_t w = t; w < W; w += NT) {
       const uint32_t c = S.crank[w], v = S.cv[c];
