@@ -122,6 +122,37 @@ def test_hash_vs_independent_bigint():
             assert gv == wang_hash_bigint(int(xv), k)
 
 
+def _unxorshift(y, s, bits):
+    """x with x ^ (x >> s) == y (mod 2^bits): x = y ^ y>>s ^ y>>2s ^ ..."""
+    x, t = 0, y
+    while t:
+        x ^= t
+        t >>= s
+    return x & ((1 << bits) - 1)
+
+
+@pytest.mark.parametrize("k", [8, 11, 12, 14, 15, 16, 19, 21, 24, 28])
+def test_hash_is_undone_by_the_inverse_of_its_definition(k):
+    """P:370 calls the hash invertible.  The inverse is derived here step by step from the definition
+     with modular inverses of the three multipliers and un-xor-shifts, none of which
+    the oracle contains: a wrong shift or multiplier in the oracle (the constants that only act for
+    k >= 8..15) would still be a bijection but would not be undone by this inverse."""
+    bits = 2 * k
+    M = 1 << bits
+    rng = np.random.default_rng(100 + k)
+    xs = rng.integers(0, M, size=3000, dtype=np.uint64)
+    hs = oracle.hash_batch(xs, k)
+    i31, i21, i265, im = pow((1 << 31) + 1, -1, M), pow(21, -1, M), pow(265, -1, M), pow((1 << 21) - 1, -1, M)
+    for x, h in zip(xs.tolist(), hs.tolist()):
+        x6 = (h * i31) % M
+        x5 = _unxorshift(x6, 28, bits)
+        x4 = (x5 * i21) % M
+        x3 = _unxorshift(x4, 14, bits)
+        x2 = (x3 * i265) % M
+        x1 = _unxorshift(x2, 24, bits)
+        assert ((x1 + 1) * im) % M == x
+
+
 # ---------------------------------------------------------------------------- O4+O6 minimizers (P:294, P:370)
 def _mz_list(arr):
     return [(int(r["hash"]), int(r["pos"]), int(r["strand"])) for r in arr]
