@@ -1050,17 +1050,10 @@ __global__ void __launch_bounds__(BS_NT, BS_MINB) k_bin_build(const uint64_t* __
     }
     }  // !one
     }  // !mid
-    // K3 fused: runs never cross a bin (a hash lies in one bin).  Run heads mark NH[i] = i, a block
-    // suffix minimum gives every i the next head >= i, and a head's run length is NH[i + 1] - i.
-    // (A mid bin fills both buffers: its run heads gallop to their run's end instead.)
-    uint32_t* NH = reinterpret_cast<uint32_t*>(res == A ? Bf : A);  // [n + 1] (the non-result buffer)
-    if (!one && !mid) {
-      for (int i = threadIdx.x; i < n; i += BS_NT)
-        NH[i] = (i == 0 || (uint32_t)(res[i - 1] >> 33) != (uint32_t)(res[i] >> 33)) ? (uint32_t)i : (uint32_t)n;
-      if (threadIdx.x == 0) NH[n] = (uint32_t)n;
-      __syncthreads();
-      suffix_min_block(NH, (uint32_t)n + 1, wsum);
-    }
+    // K3 fused: runs never cross a bin (a hash lies in one bin).  A run head finds its run's end by
+    // galloping over the sorted records (almost every run has one record: one comparison); round 2's
+    // first version marked the heads in the other buffer and took a block suffix minimum (4 barriers
+    // more per bin).
     // K5 + K6 fused: entries in final position (all of them: a hash with count > tau is dropped at
     // probe time, reading O7), then the bin's S directory slots (bins are unions of whole slots)
     const uint2 tb = table[segv];                  // (first bin, bins) of the bin's segment
@@ -1076,7 +1069,7 @@ __global__ void __launch_bounds__(BS_NT, BS_MINB) k_bin_build(const uint64_t* __
       const bool head = i == 0 || (uint32_t)(res[i - 1] >> 33) != lo;
       if (one) {
         if (i == 0) run_emit(ro, rh, (uint64_t)n, racc);
-      } else if (head && mid) {
+      } else if (head) {
         int lo2 = i + 1, st = 1;  // gallop, then bisect, to the first record with another key
         while (lo2 + st <= n && (uint32_t)(res[lo2 + st - 1] >> 33) == lo) { lo2 += st; st <<= 1; }
         int hi2 = min(lo2 + st - 1, n);
@@ -1086,8 +1079,6 @@ __global__ void __launch_bounds__(BS_NT, BS_MINB) k_bin_build(const uint64_t* __
           else hi2 = m2;
         }
         run_emit(ro, rh, (uint64_t)(lo2 - i), racc);
-      } else if (head) {
-        run_emit(ro, rh, NH[i + 1] - (uint32_t)i, racc);
       }
       if (head) {  // a slot starts at a run head: its first record
         const uint32_t q = (uint32_t)((((uint64_t)lo * slots_t) >> L) - qbase);
