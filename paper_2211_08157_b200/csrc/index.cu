@@ -31,13 +31,22 @@ namespace god {
 
 namespace {
 constexpr int RS_NT = 256;
-constexpr int RS_IPT = 16;
+#ifndef RS_IPT_DEF
+#define RS_IPT_DEF 16
+#endif
+constexpr int RS_IPT = RS_IPT_DEF;
 constexpr int RS_TILE = RS_NT * RS_IPT;
 constexpr int RS_BITS = 8;
 constexpr int RS_BINS = 1 << RS_BITS;
 constexpr uint64_t HASH_BITS_MASK = (1ull << 63) - 1;
-constexpr int RS_DYN_SMEM = RS_TILE * (sizeof(uint64_t) + sizeof(uint32_t));
-constexpr int RS2_NT = 512, RS2_IPT = RS_TILE / RS2_NT;  // scatter: 16 warps, 8 items per thread
+#ifndef RS2_NT_DEF
+#define RS2_NT_DEF 512
+#endif
+constexpr int RS2_NT = RS2_NT_DEF, RS2_IPT = RS_TILE / RS2_NT;  // scatter: 8 items per thread
+// dynamic SMEM of the scatter: the staged tile (keys, values) + the digit counter rows
+constexpr int rs_dyn_smem(int rb, bool stable) {
+  return RS_TILE * (int)(sizeof(uint64_t) + sizeof(uint32_t)) + (stable ? RS2_NT / 32 : 1) * (1 << rb) * 4;
+}
 // tiles per histogram column of the bin-sort passes: one CTA can scatter RS_GROUP consecutive tiles,
 // carrying its digit offsets from tile to tile, so that the tile histograms and their scan are
 // RS_GROUP times smaller.  Measured (human, both passes): the scan falls 0.49 -> 0.27 / 0.15 / 0.09 ms
@@ -108,8 +117,11 @@ __global__ void __launch_bounds__(RS_NT) k_rs_hist(const uint64_t* __restrict__ 
 #ifndef RS_UNSTABLE_MINB
 #define RS_UNSTABLE_MINB 2
 #endif
-template <int RB, bool STABLE = true, int G = 1>
-__global__ void __launch_bounds__(RS2_NT, STABLE ? 2 : RS_UNSTABLE_MINB) k_rs_scatter2(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin,
+#ifndef RS_MINB_DEF
+#define RS_MINB_DEF 2
+#endif
+template <int RB, bool STABLE, int G>
+__global__ void __launch_bounds__(RS2_NT, STABLE ? RS_MINB_DEF : RS_UNSTABLE_MINB) k_rs_scatter2(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin,
                                                        uint64_t* __restrict__ kout, uint32_t* __restrict__ vout,
                                                        uint64_t n, int shift, uint32_t dmask,
                                                        const uint64_t* __restrict__ goff, uint32_t ntiles,
@@ -117,11 +129,11 @@ __global__ void __launch_bounds__(RS2_NT, STABLE ? 2 : RS_UNSTABLE_MINB) k_rs_sc
   // STABLE: one counter row per warp (ranks in (warp, item, lane) order).  Unstable: one row for the
   // CTA — the atomic's return value is the item's rank in its digit, no prefix over warps
   constexpr int NROW = STABLE ? RS2_NT / 32 : 1;
-  __shared__ __align__(16) uint32_t wcnt[NROW][(1 << RB)];
+  extern __shared__ __align__(16) unsigned char rs_dyn[];
+  uint32_t (*wcnt)[1 << RB] = reinterpret_cast<uint32_t (*)[1 << RB]>(rs_dyn + (size_t)RS_TILE * 12);
   __shared__ uint32_t dstart[(1 << RB) + 1];
   __shared__ uint32_t wsum[(1 << RB) / 32];
   __shared__ uint64_t s_goff[1 << RB];
-  extern __shared__ __align__(16) unsigned char rs_dyn[];
   uint64_t* sk = reinterpret_cast<uint64_t*>(rs_dyn);
   uint32_t* sv = reinterpret_cast<uint32_t*>(sk + RS_TILE);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -1737,11 +1749,12 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
     uint64_t* goff = scr.alloc<uint64_t>((uint64_t)(1u << BIN_DIGIT) * ntiles);
     static DeviceOnce attr_once;
     attr_once.run([] {
-      GOD_CUDA(cudaFuncSetAttribute(k_rs_scatter2<RS_BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize, RS_DYN_SMEM));
+      GOD_CUDA(cudaFuncSetAttribute(k_rs_scatter2<RS_BITS, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    rs_dyn_smem(RS_BITS, true)));
       GOD_CUDA(cudaFuncSetAttribute(k_rs_scatter2<BIN_DIGIT, true, RS_GROUP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    RS_DYN_SMEM));
+                                    rs_dyn_smem(BIN_DIGIT, true)));
       GOD_CUDA(cudaFuncSetAttribute(k_rs_scatter2<BIN_DIGIT, false, RS_GROUP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    RS_DYN_SMEM));
+                                    rs_dyn_smem(BIN_DIGIT, false)));
       GOD_CUDA(cudaFuncSetAttribute(k_bin_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, BS_SMEM));
       GOD_CUDA(cudaFuncSetAttribute(k_bin_build, cudaFuncAttributeMaxDynamicSharedMemorySize, BB_SMEM));
       GOD_CUDA(cudaFuncSetAttribute(k_bucket_sort_big, cudaFuncAttributeMaxDynamicSharedMemorySize, BS_SMEM));
@@ -1757,11 +1770,11 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
       if (!have_hist) GOD_LAUNCH("k_rs_hist", (k_rs_hist<RB, G>), ncols, RS_NT, 0, st, k0, n, shift, dmask, hist, ncols);
       scan_exclusive_u32_to_u64(hist, goff, (uint64_t)(1u << RB) * ncols, nullptr, st, scr, "scan_sort_hist");
       if (stable)
-        GOD_LAUNCH("k_rs_scatter", (k_rs_scatter2<RB, true, G>), ncols, RS2_NT, RS_DYN_SMEM, st, k0, v0, k1, v1, n, shift,
-                   dmask, goff, ncols, table, L, resident_ctas(k_rs_scatter2<RB, true, G>, RS2_NT, RS_DYN_SMEM));
+        GOD_LAUNCH("k_rs_scatter", (k_rs_scatter2<RB, true, G>), ncols, RS2_NT, rs_dyn_smem(RB, true), st, k0, v0, k1, v1, n,
+                   shift, dmask, goff, ncols, table, L, resident_ctas(k_rs_scatter2<RB, true, G>, RS2_NT, rs_dyn_smem(RB, true)));
       else
-        GOD_LAUNCH("k_rs_scatter", (k_rs_scatter2<RB, false, G>), ncols, RS2_NT, RS_DYN_SMEM, st, k0, v0, k1, v1, n, shift,
-                   dmask, goff, ncols, table, L, resident_ctas(k_rs_scatter2<RB, false, G>, RS2_NT, RS_DYN_SMEM));
+        GOD_LAUNCH("k_rs_scatter", (k_rs_scatter2<RB, false, G>), ncols, RS2_NT, rs_dyn_smem(RB, false), st, k0, v0, k1, v1, n,
+                   shift, dmask, goff, ncols, table, L, resident_ctas(k_rs_scatter2<RB, false, G>, RS2_NT, rs_dyn_smem(RB, false)));
       std::swap(k0, k1);
       std::swap(v0, v1);
     };
