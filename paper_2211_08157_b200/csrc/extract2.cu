@@ -734,6 +734,7 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract3(X2Args a) {
 
     // ------------------------------------------------------------------ C. selection on keys
     uint32_t selmask = 0;
+    uint32_t slow_flags = 0;  // 1: a run shorter than w, 2: a key tie (uniform: from the block-wide vote)
     if (!any_n) {
       bool need_slow = false;
       uint32_t PF[W], SF[W];
@@ -816,14 +817,12 @@ __global__ void __launch_bounds__(X2_NT, x2_minb<W>()) k_extract3(X2Args a) {
       }
       if (!aligned && (tid == 0 || tid == X2_NT - 1)) need_slow = false;  // halo blocks are not emitted
       if (a.dbg_flags & 2u) tie = false;
-      const int flags = __syncthreads_or((need_slow ? 1 : 0) | (tie ? 2 : 0));
-      if (tid == 0 && flags) T.slow = (uint32_t)flags;
-      __syncthreads();
+      slow_flags = (uint32_t)__syncthreads_or((need_slow ? 1 : 0) | (tie ? 2 : 0));
     }
 
     // ------------------------------------------------------------------ D. exact slow path (whole tile)
-    if (any_n || T.slow) {
-      if (tid == 0 && a.dbg_counts) atomicAdd(&a.dbg_counts[(T.slow & 2u) && !any_n ? 1 : 0], 1u);
+    if (any_n || slow_flags) {
+      if (tid == 0 && a.dbg_counts) atomicAdd(&a.dbg_counts[(slow_flags & 2u) && !any_n ? 1 : 0], 1u);
       uint32_t zmask = 0;
 #pragma unroll
       for (int i = 0; i < W; i++) zmask |= (uint32_t)(HZ[tid * W + i] >> 63) << i;
