@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--scale", type=float, default=1.0, help="size multiplier (1.0 = the BASELINE config)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-inputs", choices=["host", "staged"], default="host",
+                    help="host: pinned host buffers straight into the C ABI (default); staged: the caller copies them")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-vote", action="store_true")
     ap.add_argument("--vote-D", type=int, default=0, help="voting distance D (0 = read length)")
@@ -470,7 +472,7 @@ def main():
     # e2e through the C ABI with pinned host buffers
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(god, torch, cfg, pattern, k, w, n_anchors, args.e2e_steps, dist, world, dev)
+        e2e = run_e2e(god, torch, cfg, pattern, k, w, n_anchors, args.e2e_steps, dist, world, dev, args.e2e_inputs)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -546,7 +548,7 @@ def run_vote(god, torch, dreads, droffs, dref, droff, cfg, pattern, k, w, args, 
                          "frac": round(alg / (ms / 1e3) / 1e9 / float(peaks.get("hbm_gbs", 6650.0)), 4)}}
 
 
-def run_e2e(god, torch, cfg, pattern, k, w, n_anchors, steps, dist, world, dev):
+def run_e2e(god, torch, cfg, pattern, k, w, n_anchors, steps, dist, world, dev, inputs="host"):
     href = torch.from_numpy(cfg.ref).pin_memory()
     hroff = torch.from_numpy(cfg.ref_offsets).pin_memory()
     hreads = torch.from_numpy(cfg.reads.seq).pin_memory()
@@ -567,17 +569,18 @@ def run_e2e(god, torch, cfg, pattern, k, w, n_anchors, steps, dist, world, dev):
     need = ctypes.c_uint64(0)
     vp = ctypes.c_void_p
 
-    dref = torch.empty_like(href, device=dev)
-    droff = torch.empty_like(hroff, device=dev)
-    dreads = torch.empty_like(hreads, device=dev)
-    droffs = torch.empty_like(hroffs, device=dev)
+    if inputs == "staged":
+        dref = torch.empty_like(href, device=dev)
+        droff = torch.empty_like(hroff, device=dev)
+        dreads = torch.empty_like(hreads, device=dev)
+        droffs = torch.empty_like(hroffs, device=dev)
     side = torch.cuda.Stream()
     main = torch.cuda.current_stream()
 
-    def one():
-        # the reference in first (the index needs all of it); the reads follow on a copy stream while
-        # the index is built; the seeding then streams each read batch's results back to host
-        # buffers while later batches are seeded (god_seed_reads' pipelined path)
+    def one_staged():
+        # (--e2e-inputs staged) the caller stages the inputs itself: the reference in first (the index
+        # needs all of it); the reads follow on a copy stream while the index is built; the seeding then
+        # streams each read batch's results back to host buffers while later batches are seeded
         dref.copy_(href, non_blocking=True)
         droff.copy_(hroff, non_blocking=True)
         ref_in = torch.cuda.Event()
@@ -594,6 +597,20 @@ def run_e2e(god, torch, cfg, pattern, k, w, n_anchors, steps, dist, world, dev):
                                     vp(ph_host.data_ptr()), 16, vp(an_host.data_ptr()), vp(ao_host.data_ptr()),
                                     n_anchors, ctypes.byref(need), stream))
         return h
+
+    def one_host():
+        # (default) every buffer handed to the C ABI is a pinned HOST buffer: god_build_index streams the
+        # reference up in chunks with K1 running on the tiles that are in; god_seed_reads_compact
+        # pipelines read batches (H2D of batch b + 1, seeding of batch b, D2H of batch b - 1)
+        h = ctypes.c_void_p(0)
+        _lib.check(L.god_build_index(ctypes.byref(prm), vp(href.data_ptr()), vp(hroff.data_ptr()), 1,
+                                     ctypes.byref(cut), ctypes.byref(h), stream))
+        _lib.check(L.god_seed_reads_compact(h, vp(hreads.data_ptr()), vp(hroffs.data_ptr()), n, _lib.PHASE_SELECT,
+                                    vp(ph_host.data_ptr()), 16, vp(an_host.data_ptr()), vp(ao_host.data_ptr()),
+                                    n_anchors, ctypes.byref(need), stream))
+        return h
+
+    one = one_staged if inputs == "staged" else one_host
 
     L.god_index_free(one())  # warm-up
     torch.cuda.synchronize()
@@ -614,7 +631,7 @@ def run_e2e(god, torch, cfg, pattern, k, w, n_anchors, steps, dist, world, dev):
     h2d = cfg.ref.size + cfg.ref_offsets.nbytes + cfg.reads.seq.size + cfg.reads.offsets.nbytes
     d2h = int(need.value) * 8 + (n + 1) * 8 + n
     return {"value": round(world * n / (ms / steps / 1e3), 1), "unit": "reads/s", "h2d_bytes_per_step": int(h2d),
-            "d2h_bytes_per_step": int(d2h), "steps": steps, "ms_per_step": round(ms / steps, 3),
+            "d2h_bytes_per_step": int(d2h), "steps": steps, "ms_per_step": round(ms / steps, 3), "inputs": inputs,
             "outputs": "phases u8[n], anchor_offsets u64[n+1], god_anchor_compact[n_anchors] (8 B)"}
 
 

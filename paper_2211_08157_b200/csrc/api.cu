@@ -284,11 +284,9 @@ void grow(T*& p, uint64_t& cap, uint64_t need, cudaStream_t st) {
 }
 }  // namespace
 
-static uint64_t seed_reads_pipelined(const god_index* idx, const uint8_t* reads, const uint64_t* offs, uint32_t n_reads,
-                                     god_phase_mode mode, uint8_t* phases, uint32_t t, void* anchors,
-                                     uint64_t* anchor_offsets, uint64_t cap, uint32_t n_batches, cudaStream_t st,
-                                     bool reads_on_device, bool compact, uint32_t* bad_compact) {
-  static cudaStream_t h2d_of[64] = {nullptr}, d2h_of[64] = {nullptr};  // copy streams of each device
+// the copy streams of the current device (created once per device)
+static void copy_streams(cudaStream_t& s_h2d, cudaStream_t& s_d2h) {
+  static cudaStream_t h2d_of[64] = {nullptr}, d2h_of[64] = {nullptr};
   static DeviceOnce once;
   int dev_ord = 0;
   GOD_CUDA(cudaGetDevice(&dev_ord));
@@ -296,12 +294,34 @@ static uint64_t seed_reads_pipelined(const god_index* idx, const uint8_t* reads,
     GOD_CUDA(cudaStreamCreateWithFlags(&h2d_of[dev_ord & 63], cudaStreamNonBlocking));
     GOD_CUDA(cudaStreamCreateWithFlags(&d2h_of[dev_ord & 63], cudaStreamNonBlocking));
   });
-  const cudaStream_t s_h2d = h2d_of[dev_ord & 63], s_d2h = d2h_of[dev_ord & 63];
+  s_h2d = h2d_of[dev_ord & 63];
+  s_d2h = d2h_of[dev_ord & 63];
+}
+
+static uint64_t seed_reads_pipelined(const god_index* idx, const uint8_t* reads, const uint64_t* offs, uint32_t n_reads,
+                                     god_phase_mode mode, uint8_t* phases, uint32_t t, void* anchors,
+                                     uint64_t* anchor_offsets, uint64_t cap, uint32_t n_batches, cudaStream_t st,
+                                     bool reads_on_device, bool compact, uint32_t* bad_compact) {
+  cudaStream_t s_h2d, s_d2h;
+  copy_streams(s_h2d, s_d2h);
   PipeSlot slot[2];
   for (auto& sl : slot) {
     GOD_CUDA(cudaEventCreateWithFlags(&sl.h2d_done, cudaEventDisableTiming));
     GOD_CUDA(cudaEventCreateWithFlags(&sl.comp_done, cudaEventDisableTiming));
     GOD_CUDA(cudaEventCreateWithFlags(&sl.d2h_done, cudaEventDisableTiming));
+  }
+  // GOD_PIPE_TRACE: developer aid, device timeline of every batch's upload / seeding / download
+  const bool trace = getenv("GOD_PIPE_TRACE") != nullptr;
+  std::vector<cudaEvent_t> tev;  // 6 per batch: h2d begin/end, seeding begin/end, d2h begin/end
+  cudaEvent_t t_origin = nullptr;
+  auto mark = [&](uint32_t b, int which, cudaStream_t s) {
+    if (trace) GOD_CUDA(cudaEventRecord(tev[b * 6 + which], s));
+  };
+  if (trace) {
+    tev.resize((size_t)n_batches * 6);
+    for (auto& e : tev) GOD_CUDA(cudaEventCreate(&e));
+    GOD_CUDA(cudaEventCreate(&t_origin));
+    GOD_CUDA(cudaEventRecord(t_origin, st));
   }
   uint64_t written = 0;  // anchors before the current batch
   const uint32_t per = (n_reads + n_batches - 1) / n_batches;
@@ -323,21 +343,25 @@ static uint64_t seed_reads_pipelined(const god_index* idx, const uint8_t* reads,
     PipeSlot& sl = slot[b & 1];
     const uint64_t r0 = r_begin(b), r1 = r_begin(b + 1), nb = r1 - r0;
     const uint64_t bytes = boff[b + 1] - boff[b];
-    // the slot's buffers are free once its previous batch's results have left the device
-    if (sl.d2h_pending) GOD_CUDA(cudaStreamWaitEvent(s_h2d, sl.d2h_done, 0));
-    if (sl.off) GOD_CUDA(cudaStreamWaitEvent(s_h2d, sl.comp_done, 0));  // batch b-2 no longer reads them
+    // the slot's INPUT buffers (reads, offsets, given phases) are free once batch b-2's seeding has read
+    // them; its results leave from other buffers (an/anc, aoff, the selected phases), so the upload does
+    // not wait for that copy (it did: uploads and downloads then alternated instead of overlapping,
+    // 44 -> 33 ms for the 10 M reads of the human config)
+    if (sl.off) GOD_CUDA(cudaStreamWaitEvent(s_h2d, sl.comp_done, 0));
     grow(sl.off, sl.off_cap, nb + 1, s_h2d);
+    if (!reads_on_device) grow(sl.reads, sl.reads_cap, bytes + 16, s_h2d);
+    mark(b, 0, s_h2d);
     if (reads_on_device) {  // the reads stay where they are; only the batch's offsets are copied
       breads[b] = reads + boff[b];
       GOD_CUDA(cudaMemcpyAsync(sl.off, offs + r0, (nb + 1) * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s_h2d));
     } else {
-      grow(sl.reads, sl.reads_cap, bytes + 16, s_h2d);
       breads[b] = sl.reads;
       if (bytes) GOD_CUDA(cudaMemcpyAsync(sl.reads, reads + boff[b], bytes, cudaMemcpyHostToDevice, s_h2d));
       GOD_CUDA(cudaMemcpyAsync(sl.off, offs + r0, (nb + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, s_h2d));
     }
     if (mode == GOD_PHASE_GIVEN && nb) GOD_CUDA(cudaMemcpyAsync(sl.ph, phases + r0, nb, cudaMemcpyHostToDevice, s_h2d));
     GOD_CUDA(cudaEventRecord(sl.h2d_done, s_h2d));
+    mark(b, 1, s_h2d);
   };
   upload(0);
   set_copies_in_flight(true);
@@ -347,6 +371,7 @@ static uint64_t seed_reads_pipelined(const god_index* idx, const uint8_t* reads,
     if (b + 1 < n_batches) upload(b + 1);
     const uint64_t r0 = r_begin(b), r1 = r_begin(b + 1), nb = r1 - r0;
     GOD_CUDA(cudaStreamWaitEvent(st, sl.h2d_done, 0));
+    mark(b, 2, st);
     GOD_LAUNCH("k_rebase", k_rebase_u64, grid_for(nb + 1, 256), 256, 0, st, sl.off, nb + 1, boff[b], 0ull);
     // anchors of this batch: a share of the caller's capacity, grown and redone if too small
     uint64_t want = cap ? std::min<uint64_t>(cap, cap / n_batches + cap / (4 * n_batches) + 4096) : 4096;
@@ -371,18 +396,31 @@ static uint64_t seed_reads_pipelined(const god_index* idx, const uint8_t* reads,
       asz = sizeof(god_anchor_compact);
     }
     GOD_CUDA(cudaEventRecord(sl.comp_done, st));
+    mark(b, 3, st);
     GOD_CUDA(cudaStreamWaitEvent(s_d2h, sl.comp_done, 0));
+    mark(b, 4, s_d2h);
     if (written + tot <= cap && tot)
       GOD_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(anchors) + written * asz, src, tot * asz, cudaMemcpyDeviceToHost,
                                s_d2h));
     GOD_CUDA(cudaMemcpyAsync(anchor_offsets + r0, sl.aoff, (nb + 1) * sizeof(uint64_t), cudaMemcpyDeviceToHost, s_d2h));
     if (mode == GOD_PHASE_SELECT && nb) GOD_CUDA(cudaMemcpyAsync(phases + r0, sl.ph, nb, cudaMemcpyDeviceToHost, s_d2h));
     GOD_CUDA(cudaEventRecord(sl.d2h_done, s_d2h));
+    mark(b, 5, s_d2h);
     sl.d2h_pending = true;
     written += tot;
   }
   GOD_CUDA(cudaStreamSynchronize(s_d2h));
   GOD_CUDA(cudaStreamSynchronize(s_h2d));
+  if (trace) {
+    for (uint32_t b = 0; b < n_batches; b++) {
+      float t[6];
+      for (int q = 0; q < 6; q++) GOD_CUDA(cudaEventElapsedTime(&t[q], t_origin, tev[b * 6 + q]));
+      fprintf(stderr, "[pipe] batch %u: h2d %.2f-%.2f  seed %.2f-%.2f  d2h %.2f-%.2f ms\n", b, t[0], t[1], t[2], t[3],
+              t[4], t[5]);
+    }
+    for (auto& e : tev) cudaEventDestroy(e);
+    cudaEventDestroy(t_origin);
+  }
   for (auto& sl : slot) {
     if (sl.reads) cudaFreeAsync(sl.reads, st);
     if (sl.off) cudaFreeAsync(sl.off, st);
@@ -521,12 +559,55 @@ GOD_API god_status god_build_index(const god_params* prm, const uint8_t* ref, co
     Stage sg(st, scr);
     const uint64_t L = total_len(ref_offsets, n_refs, st);
     GOD_REQUIRE(L < (1ull << 32), "total reference length must be < 2^32 (u32 positions)");
-    const uint8_t* dref = sg.in(ref, L);
+    // A large host reference is streamed: chunks go up on the copy stream while K1 (stage 1+2) runs on
+    // the tiles whose bytes are in, so only the sort and the table build follow the transfer.
+    // GOD_STREAM_CHUNK_BYTES: test hook (chunk size; 0 disables streaming).
+    const char* sc = getenv("GOD_STREAM_CHUNK_BYTES");
+    const uint64_t want_chunk = sc ? strtoull(sc, nullptr, 10) : (32ull << 20);
+    const uint64_t max_chunks = 16;
+    god::SeqStream ss;
+    struct EvGuard {
+      god::SeqStream& s;
+      ~EvGuard() {
+        if (!s.arrived.empty()) set_copies_in_flight(false);
+        for (cudaEvent_t e : s.arrived) cudaEventDestroy(e);
+      }
+    } ev_guard{ss};
+    const uint8_t* dref;
+    if (ref && !is_device_ptr(ref) && want_chunk && L >= 2 * want_chunk) {
+      uint8_t* d = scr.alloc<uint8_t>(L);
+      cudaStream_t s_h2d, s_d2h;
+      copy_streams(s_h2d, s_d2h);
+      uint64_t chunk = std::max<uint64_t>(want_chunk, (L + max_chunks - 1) / max_chunks);
+      chunk = (chunk + 255) & ~255ull;
+      cudaEvent_t ready;  // the allocation is stream-ordered on st
+      GOD_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+      GOD_CUDA(cudaEventRecord(ready, st));
+      GOD_CUDA(cudaStreamWaitEvent(s_h2d, ready, 0));
+      GOD_CUDA(cudaEventDestroy(ready));  // (released once the wait has completed)
+      ss.chunk_bytes = chunk;
+      for (uint64_t o = 0; o < L; o += chunk) {
+        cudaEvent_t e;
+        GOD_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        ss.arrived.push_back(e);
+        GOD_CUDA(cudaMemcpyAsync(d + o, ref + o, std::min<uint64_t>(chunk, L - o), cudaMemcpyHostToDevice, s_h2d));
+        GOD_CUDA(cudaEventRecord(e, s_h2d));
+      }
+      set_copies_in_flight(true);  // small device->host reads go through the mapped page meanwhile
+      dref = d;
+    } else {
+      dref = sg.in(ref, L);
+    }
     const uint64_t* doff = sg.in(ref_offsets, (size_t)n_refs + 1);
     god_index* ix = new god_index();
     try {
-      god::build_index(P, dref, doff, n_refs, *cutoff, ix, st);
+      god::build_index(P, dref, doff, n_refs, *cutoff, ix, st, ss.arrived.empty() ? nullptr : &ss);
     } catch (...) {
+      if (!ss.arrived.empty()) {
+        cudaStream_t s_h2d, s_d2h;
+        copy_streams(s_h2d, s_d2h);
+        cudaStreamSynchronize(s_h2d);  // the copies target scratch memory that is about to be freed
+      }
       god_index_free(ix);
       throw;
     }

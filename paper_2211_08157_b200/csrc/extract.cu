@@ -340,10 +340,12 @@ JobSet make_jobs(const Params& P, const uint64_t* offsets, uint32_t n_seqs, cons
 
 void run_extract(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const Job* jobs, const uint64_t* kb,
                  uint32_t n_jobs, uint64_t total_pos, bool want_job, bool want_job_off, Records& rec, cudaStream_t st,
-                 Scratch& scr, uint64_t cap_hint, const char* tag, const X2Layout* x2, RecOrder order) {
+                 Scratch& scr, uint64_t cap_hint, const char* tag, const X2Layout* x2, RecOrder order,
+                 const SeqStream* ss) {
   rec.n = 0;
-  if (run_extract2(P, seq, seq_bytes, jobs, n_jobs, want_job, want_job_off, rec, st, scr, cap_hint, tag, x2, order))
+  if (run_extract2(P, seq, seq_bytes, jobs, n_jobs, want_job, want_job_off, rec, st, scr, cap_hint, tag, x2, order, ss))
     return;
+  if (ss) ss->wait_all(st);  // the generic kernel reads the whole buffer
   if (n_jobs == 0 || total_pos == 0) {
     rec.cap = 1;
     rec.hz = scr.alloc<uint64_t>(1);

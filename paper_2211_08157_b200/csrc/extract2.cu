@@ -110,7 +110,7 @@ struct __align__(16) X2Desc {
   uint64_t b0;                    // aligned tiles: first block (thread 0's), and the block count
   uint32_t nb, raw_len;           // raw_len: bytes a bulk copy stages for the tile (0: direct loads)
   uint64_t raw_lo;                // ... from this 16-B aligned global address
-  uint64_t pad;
+  uint64_t need;                  // the tile reads only bytes [0, need) of the sequence buffer (streamed input)
 };
 // bytes of the SMEM buffer the next tile's ASCII bytes are staged into (unordered K1)
 constexpr uint32_t X2_RAW_CAP = 48 * X2_NT;
@@ -138,6 +138,13 @@ __device__ __forceinline__ void raw_span(const uint8_t* seq, uint64_t seq_bytes,
   const uint64_t a = (s0 + lo) & ~15ull, b = (s0 + hi + 15) & ~15ull;
   raw_lo = a;
   raw_len = (a >= s0 && b <= s0 + seq_bytes && b - a <= X2_RAW_CAP && hi > lo) ? (uint32_t)(b - a) : 0u;
+}
+
+// bytes of the buffer a tile may touch: [0, need).  last_byte bounds every direct load (with its margin),
+// sp_hi the staged span before its 16-B alignment in the address space; checked loads stop at seq_bytes
+__device__ __forceinline__ uint64_t tile_need(uint64_t last_byte, uint64_t sp_hi, uint64_t seq_bytes) {
+  const uint64_t n = last_byte > sp_hi + 16 ? last_byte : sp_hi + 16;
+  return n < seq_bytes ? n : seq_bytes;
 }
 
 struct X2Tile {  // per-tile scalars, in SMEM
@@ -1032,7 +1039,7 @@ __global__ void k_x2_tile_desc(const uint64_t* __restrict__ kb, const uint64_t* 
     d.safe = last_byte <= seq_bytes;
     d.b0 = 0;
     d.nb = 0;
-    d.pad = 0;
+    d.need = tile_need(last_byte, sp_hi, seq_bytes);
     raw_span(seq, seq_bytes, sp_lo, sp_hi, d.raw_lo, d.raw_len);
     d.cw_lo = lo;
     d.cw_hi = hi;
@@ -1064,7 +1071,7 @@ __global__ void k_x2_tile_desc_aligned(const uint64_t* __restrict__ kb, const ui
     d.j1 = je > j0 ? je - 1 : d.j0;
     d.b0 = kb[j0 < n_jobs ? j0 : n_jobs] / W;
     d.nb = je > j0 ? (uint32_t)((kb[je] - kb[j0]) / W) : 0u;
-    d.pad = 0;
+    d.need = seq_bytes;  // (aligned tiles are never streamed)
     d.cw_lo = cw[d.j0];
     d.cw_hi = je > j0 ? cw[je] : cw[d.j0];
     uint64_t last_l = 0, sp_lo = ~0ull, sp_hi = 0;  // every job (jobs need not be in buffer order)
@@ -1134,11 +1141,41 @@ __global__ void k_x2_job_off_fix(uint64_t* job_off, uint32_t n_jobs, const uint6
   }
 }
 
+// Streamed input (SeqStream): first[i] = the first tile that reads past chunk i, i.e. tiles
+// [first[i - 1], first[i]) can run once chunks 0..i are in.  first[] starts at ntiles; a tile whose last
+// chunk is above its predecessor's lowers every boundary in between (need is nondecreasing in t for a
+// reference's jobs, and the minimum stays right if it is not).  ctr[i] = the tile counter each range starts at.
+__global__ void k_x2_stream_plan(const X2Desc* __restrict__ desc, uint64_t ntiles, uint64_t chunk_bytes, uint32_t S,
+                                 uint32_t* first) {
+  auto chunk_of = [&](uint64_t t) -> uint32_t {
+    const uint64_t need = desc[t].need;
+    const uint64_t c = need ? (need - 1) / chunk_bytes : 0;
+    return (uint32_t)(c < S - 1 ? c : S - 1);
+  };
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < ntiles; t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t c = chunk_of(t), cp = t ? chunk_of(t - 1) : 0u;
+    for (uint32_t i = cp; i < c; i++) atomicMin(&first[i], (uint32_t)t);
+  }
+}
+__global__ void k_x2_stream_ctrs(uint32_t* first, uint32_t S, uint32_t ntiles, uint32_t* ctr) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    // a dip in `need` must not start a later range before an earlier one: running minimum from the right
+    uint32_t m = ntiles;
+    first[S - 1] = ntiles;
+    for (int i = (int)S - 1; i >= 0; i--) {
+      m = first[i] < m ? first[i] : m;
+      first[i] = m;
+    }
+    for (uint32_t i = 0; i < S; i++) ctr[i] = i ? first[i - 1] : 0u;
+  }
+}
+
 template <int K, int W, int PP, int PX, bool ORDERED>
 size_t x2_smem_bytes() {
   return X2Cfg<K, W, PP, PX>::smem(ORDERED);
 }
 
+// ntiles: the tiles this launch will claim (sizes the grid; a.ntiles is the end of its tile range)
 template <int K, int W, int PP, int PX, bool ORDERED>
 void launch_x3(const X2Args& a, uint64_t ntiles, cudaStream_t st, const char* tag) {
   static int grid[64] = {0};  // per device
@@ -1178,7 +1215,7 @@ bool x2_supported(const Params& P) {
 // Returns false if no specialised kernel exists for these parameters (caller uses the generic one).
 bool run_extract2(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const Job* jobs, uint32_t n_jobs,
                   bool want_job, bool want_job_off, Records& rec, cudaStream_t st, Scratch& scr,
-                  uint64_t cap_hint, const char* tag, const X2Layout* x2, RecOrder order) {
+                  uint64_t cap_hint, const char* tag, const X2Layout* x2, RecOrder order, const SeqStream* ss) {
   if (!x2_supported(P)) return false;
   const int PP = (int)P.pat.p, PX = (int)P.pat.x;
   const int K = P.k, W = P.w;
@@ -1222,6 +1259,9 @@ bool run_extract2(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const
   const bool aligned = can_unordered && order == ORDER_JOB && max_jb <= X2_NT / 4 && !getenv("GOD_X2_NO_ALIGN");
   // GOD_X2_FORCE_UNORDERED: developer timing aid (records of a multi-tile job are then NOT contiguous)
   const bool ordered = !(can_unordered && (order == ORDER_NONE || aligned || getenv("GOD_X2_FORCE_UNORDERED")));
+  // a streamed input (SeqStream) is consumed chunk by chunk only by the unordered kernel over strided tiles
+  const bool streamed = ss && !ss->arrived.empty() && ss->chunk_bytes && !ordered && !aligned;
+  if (ss && !streamed) ss->wait_all(st);
   const uint32_t S_al = (uint32_t)(X2_NT + 1 - max_jb);  // tile stride (blocks) of the aligned layout
   const uint64_t ntiles = aligned ? (total_blocks + S_al - 1) / S_al : (total_blocks + X2_OUT_BLOCKS - 1) / X2_OUT_BLOCKS;
   GOD_REQUIRE(ntiles < 0x7FFFFFFFull, "input too large for one extraction launch");
@@ -1261,16 +1301,16 @@ bool run_extract2(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const
     if (kbits > 0 && kbits < 2 * K) key_shift = std::min(2 * K - kbits, 31);  // keys of >= 2k - 31 bits
   }
   // launch the specialised kernel for (K, W, pattern); ordered_kernel: the look-back instance
-  auto launch = [&](const X2Args& a, bool ordered_kernel) {
+  auto launch = [&](const X2Args& a, bool ordered_kernel, uint64_t count) {
     auto by_pattern = [&](auto kc, auto wc) {
       constexpr int KK = decltype(kc)::value, WW = decltype(wc)::value;
       auto go = [&](auto oc) {
         constexpr bool O = decltype(oc)::value;
-        if (PX == 1 && PP == 1) launch_x3<KK, WW, 1, 1, O>(a, ntiles, st, tag);
-        else if (PX == 1 && PP == 2) launch_x3<KK, WW, 2, 1, O>(a, ntiles, st, tag);
-        else if (PX == 1) launch_x3<KK, WW, 3, 1, O>(a, ntiles, st, tag);
-        else if (PX == 2) launch_x3<KK, WW, 3, 2, O>(a, ntiles, st, tag);
-        else launch_x3<KK, WW, 4, 3, O>(a, ntiles, st, tag);
+        if (PX == 1 && PP == 1) launch_x3<KK, WW, 1, 1, O>(a, count, st, tag);
+        else if (PX == 1 && PP == 2) launch_x3<KK, WW, 2, 1, O>(a, count, st, tag);
+        else if (PX == 1) launch_x3<KK, WW, 3, 1, O>(a, count, st, tag);
+        else if (PX == 2) launch_x3<KK, WW, 3, 2, O>(a, count, st, tag);
+        else launch_x3<KK, WW, 4, 3, O>(a, count, st, tag);
       };
       if (!ordered_kernel) go(std::false_type());
       else go(std::true_type());
@@ -1295,7 +1335,7 @@ bool run_extract2(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const
     X2Args a{seq, seq_bytes, jobs, kb, cw, n_jobs, total_blocks, P.pat.one[0], key_shift, status, ctr,
              shz, spos, nullptr, rec.job_off, nullptr, scap, dtotal, dbg_flags,
              dbg_counts, desc, 0u, ntiles, getenv("GOD_X2_NO_STAGE") ? 1u : 0u, tile_cnt, overflow};
-    launch(a, false);
+    launch(a, false, ntiles);
     const uint32_t over = d2h_scalar(overflow, st);
     if (getenv("GOD_DEBUG_SLOTS")) fprintf(stderr, "[x2] %s slotted tiles=%llu overflow=%u\n", tag, (unsigned long long)ntiles, over);
     if (over == 0) {
@@ -1329,8 +1369,30 @@ bool run_extract2(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const
     X2Args a{seq, seq_bytes, jobs, kb, cw, n_jobs, total_blocks, P.pat.one[0], key_shift, status, ctr,
              rec.hz, rec.pos, rec.job, rec.job_off, aligned ? rec.job_end : nullptr, cap, dtotal, dbg_flags,
              dbg_counts, desc, aligned ? 1u : 0u, ntiles, getenv("GOD_X2_NO_STAGE") ? 1u : 0u, nullptr, nullptr};
-    if (ntiles) {
-      launch(a, ordered);
+    if (ntiles && streamed && attempt == 0) {
+      // tiles [first[i - 1], first[i]) as soon as chunk i is in: one launch per chunk, each with its own
+      // tile counter starting at the range's first tile; all append to the same output
+      const uint32_t S = (uint32_t)ss->arrived.size();
+      uint32_t* first = scr.alloc<uint32_t>(S);
+      uint32_t* ctrs = scr.alloc<uint32_t>(S);
+      GOD_CUDA(cudaMemsetAsync(first, 0xFF, S * sizeof(uint32_t), st));
+      GOD_LAUNCH("k_x2_stream_plan", k_x2_stream_plan, grid_for(ntiles, 256), 256, 0, st, desc, ntiles, ss->chunk_bytes, S,
+                 first);
+      GOD_LAUNCH("k_x2_stream_plan", k_x2_stream_ctrs, 1, 32, 0, st, first, S, (uint32_t)ntiles, ctrs);
+      std::vector<uint32_t> hf(S);
+      d2h_small(hf.data(), first, S * sizeof(uint32_t), st);
+      uint32_t prev = 0;
+      for (uint32_t i = 0; i < S; i++) {
+        GOD_CUDA(cudaStreamWaitEvent(st, ss->arrived[i], 0));
+        if (hf[i] <= prev) continue;
+        X2Args ai = a;
+        ai.tile_ctr = ctrs + i;
+        ai.ntiles = hf[i];
+        launch(ai, false, hf[i] - prev);
+        prev = hf[i];
+      }
+    } else if (ntiles) {
+      launch(a, ordered, ntiles);
     } else {
       GOD_CUDA(cudaMemsetAsync(dtotal, 0, sizeof(uint64_t), st));
     }

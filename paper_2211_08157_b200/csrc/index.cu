@@ -1699,7 +1699,7 @@ inline uint32_t floor_log2(uint64_t v) { return v ? 63u - (uint32_t)__builtin_cl
 
 
 void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offsets, uint32_t n_refs,
-                 const god_cutoff& cut, god_index* ix, cudaStream_t st) {
+                 const god_cutoff& cut, god_index* ix, cudaStream_t st, const SeqStream* ss) {
   Scratch scr(st, POOL_BUILD);
   ix->P = P;
   memset(&ix->st, 0, sizeof(ix->st));
@@ -1711,7 +1711,7 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
   const bool bin_sort = 2 * P.k >= 36 && 2 * P.k - SEG_BITS <= 30 && !getenv("GOD_SORT_FULL");
   // the bin sort orders every bin by the packed (hash, pos) key, so K1 may emit records in tile order
   run_extract(P, ref, js.seq_bytes, js.jobs, js.kb, js.n, js.total_pos, false, false, rec, st, scr, est, "extract_ref",
-              js.x2p(), bin_sort ? ORDER_NONE : ORDER_GLOBAL);
+              js.x2p(), bin_sort ? ORDER_NONE : ORDER_GLOBAL, ss);
   const uint64_t n = rec.n;
   // K2: stable LSD radix sort on the 2k hash bits
   uint64_t* k0 = rec.hz;

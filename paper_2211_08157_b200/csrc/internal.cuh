@@ -46,13 +46,25 @@ enum RecOrder { ORDER_GLOBAL = 0, ORDER_JOB = 1, ORDER_NONE = 2 };
 // true iff run_extract2 has a specialised kernel for these parameters
 bool x2_supported(const Params& P);
 
+// The sequence buffer is still arriving from the host, chunk by chunk, on a copy stream (god_build_index
+// with a host reference): chunk i = bytes [i * chunk_bytes, (i + 1) * chunk_bytes) is complete when
+// arrived[i] has fired.  The unordered specialised K1 then runs each range of tiles as soon as the chunks
+// it reads are in (stage 1+2 hidden under the transfer); every other consumer calls wait_all first.
+struct SeqStream {
+  uint64_t chunk_bytes = 0;
+  std::vector<cudaEvent_t> arrived;
+  void wait_all(cudaStream_t st) const {
+    for (cudaEvent_t e : arrived) GOD_CUDA(cudaStreamWaitEvent(st, e, 0));
+  }
+};
+
 // Run the fused sparsify + minimizer kernel over device jobs (kb = exclusive scan of nk + 1,
 // total_pos = kb[n_jobs]; both unused when x2 carries the specialised layout).  Allocates rec arrays
 // from `scr` (capacity grown on demand), fills rec.n (synchronizes once to read the count).
 void run_extract(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const Job* jobs, const uint64_t* kb,
                  uint32_t n_jobs, uint64_t total_pos, bool want_job, bool want_job_off, Records& rec, cudaStream_t st,
                  Scratch& scr, uint64_t cap_hint, const char* tag = "k_extract", const X2Layout* x2 = nullptr,
-                 RecOrder order = ORDER_GLOBAL);
+                 RecOrder order = ORDER_GLOBAL, const SeqStream* ss = nullptr);
 // Specialised register-resident kernel (extract2.cu) for x == 1 patterns of period 1 to 3 (and the
 // '110' / '1110' shapes) and (k, w) in {(21,11), (19,19), (15,10), (19,16)}; returns false if not
 // applicable.
@@ -60,7 +72,8 @@ void run_extract(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const 
 // of through a decoupled look-back)
 bool run_extract2(const Params& P, const uint8_t* seq, uint64_t seq_bytes, const Job* jobs, uint32_t n_jobs,
                   bool want_job, bool want_job_off, Records& rec, cudaStream_t st, Scratch& scr,
-                  uint64_t cap_hint, const char* tag, const X2Layout* x2 = nullptr, RecOrder order = ORDER_GLOBAL);
+                  uint64_t cap_hint, const char* tag, const X2Layout* x2 = nullptr, RecOrder order = ORDER_GLOBAL,
+                  const SeqStream* ss = nullptr);
 
 // Build jobs for n sequences: phase from `phases` (nullable -> 0) or, if p_all != 0, one job per
 // (sequence, s) for s < p_all (job index = seq * p_all + s).  nk capped at kcap (0 = no cap).
@@ -231,8 +244,9 @@ struct god_index {
 };
 
 namespace god {
+// ss: the reference is still arriving from the host (SeqStream), else null
 void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offsets, uint32_t n_refs,
-                 const god_cutoff& cut, god_index* ix, cudaStream_t st);
+                 const god_cutoff& cut, god_index* ix, cudaStream_t st, const SeqStream* ss = nullptr);
 void index_count(const god_index* ix, const uint64_t* hashes, uint64_t n, uint32_t* counts, cudaStream_t st);
 void index_dump(const god_index* ix, uint64_t* hash, uint32_t* pos, uint8_t* strand, cudaStream_t st);
 // returns total anchors; writes anchors only if total <= cap; anchor read ids are rid_base + the

@@ -135,8 +135,9 @@ def test_minimizer_edge_inputs():
 
 
 # ------------------------------------------------------------------------------------ stage 3
-def _index_parity(ref, offs, pattern, k, w, cutoff=(1, 5000), max_occ=None):
-    ix = god.god_build_index(cu(ref), cu(offs), pattern, k, w, cutoff=cutoff, max_occ=max_occ)
+def _index_parity(ref, offs, pattern, k, w, cutoff=(1, 5000), max_occ=None, host=False):
+    ix = god.god_build_index(ref if host else cu(ref), offs if host else cu(offs), pattern, k, w, cutoff=cutoff,
+                             max_occ=max_occ)
     ox = oracle.Index(ref, offs, pattern, k, w, cutoff=cutoff, max_occ=-1 if max_occ is None else max_occ)
     st, ost = ix.stats(), ox.stats()
     for f in oracle.STATS_FIELDS:
@@ -234,6 +235,27 @@ def test_index_parity_sort_and_directory_variants(env, monkeypatch):
     ix, ox = _index_parity(ref, offs, "10", 21, 11, cutoff=(1, 2000))
     reads = synth.simulate_reads(ref, 3000, 41, length=150, p_sub=0.002)
     _seed_parity(ix, ox, reads.seq, reads.offsets)
+
+
+@pytest.mark.parametrize("chunk", ["4096", "50000", "0"])
+@pytest.mark.parametrize("pattern,k,w", [("10", 21, 11), ("110", 21, 11), ("1", 19, 19), ("10", 15, 10), ("110", 13, 7)])
+def test_index_streamed_host_reference(pattern, k, w, chunk, monkeypatch):
+    """A host reference goes up in chunks while K1 runs on the tiles whose bytes are in (god_build_index;
+    GOD_STREAM_CHUNK_BYTES shrinks the chunks so that a small input takes 16 of them): the unordered
+    specialised kernel consumes the stream range by range (k = 21, 19), the ordered and the generic
+    kernels wait for all of it (k = 15, 13); "0" disables streaming.  Several sequences, an empty one,
+    N runs across chunk borders."""
+    monkeypatch.setenv("GOD_STREAM_CHUNK_BYTES", chunk)
+    rng = np.random.default_rng(97)
+    seqs = [synth.random_acgt(rng, int(n), 0.002) for n in (90_000, 0, 3, 150_001, 40, 77_777)]
+    seqs[3][49_990:50_040] = ord("N")
+    seqs[0][4090:4100] = ord("N")
+    ref, offs = synth.concat(seqs)
+    ix, ox = _index_parity(ref, offs, pattern, k, w, cutoff=(1, 1000), host=True)
+    pinned = torch.from_numpy(ref).pin_memory()
+    ix2 = god.god_build_index(pinned.numpy(), offs, pattern, k, w, cutoff=(1, 1000))
+    for a, b in zip(ix.dump(), ix2.dump()):
+        assert np.array_equal(a, b)
 
 
 # ------------------------------------------------------------------------------------ stage 4
