@@ -58,8 +58,9 @@ def parse():
     ap.add_argument("--scale", type=float, default=1.0, help="size multiplier (1.0 = the BASELINE config)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-inputs", choices=["host", "staged"], default="host",
-                    help="host: pinned host buffers straight into the C ABI (default); staged: the caller copies them")
+    ap.add_argument("--e2e-inputs", choices=["host", "host2", "staged"], default="host",
+                    help="host: pinned host buffers into god_build_index_and_seed (default); host2: into the two "
+                         "separate calls; staged: the caller copies the inputs to the device itself")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-vote", action="store_true")
     ap.add_argument("--vote-D", type=int, default=0, help="voting distance D (0 = read length)")
@@ -599,9 +600,20 @@ def run_e2e(god, torch, cfg, pattern, k, w, n_anchors, steps, dist, world, dev, 
         return h
 
     def one_host():
-        # (default) every buffer handed to the C ABI is a pinned HOST buffer: god_build_index streams the
-        # reference up in chunks with K1 running on the tiles that are in; god_seed_reads_compact
-        # pipelines read batches (H2D of batch b + 1, seeding of batch b, D2H of batch b - 1)
+        # (default) every buffer handed to the C ABI is a pinned HOST buffer, one call:
+        # god_build_index_and_seed streams the reference up in chunks with K1 running on the tiles that
+        # are in, queues the first read batches right behind it (the link stays busy while the index is
+        # sorted) and pipelines the read batches (H2D ahead, seeding, D2H of the 8-B anchors behind)
+        h = ctypes.c_void_p(0)
+        _lib.check(L.god_build_index_and_seed(ctypes.byref(prm), vp(href.data_ptr()), vp(hroff.data_ptr()), 1,
+                                              ctypes.byref(cut), ctypes.byref(h), vp(hreads.data_ptr()),
+                                              vp(hroffs.data_ptr()), n, _lib.PHASE_SELECT, vp(ph_host.data_ptr()), 16, 1,
+                                              vp(an_host.data_ptr()), vp(ao_host.data_ptr()), n_anchors,
+                                              ctypes.byref(need), stream))
+        return h
+
+    def one_host2():
+        # (--e2e-inputs host2) the same buffers through the two separate calls
         h = ctypes.c_void_p(0)
         _lib.check(L.god_build_index(ctypes.byref(prm), vp(href.data_ptr()), vp(hroff.data_ptr()), 1,
                                      ctypes.byref(cut), ctypes.byref(h), stream))
@@ -610,7 +622,7 @@ def run_e2e(god, torch, cfg, pattern, k, w, n_anchors, steps, dist, world, dev, 
                                     n_anchors, ctypes.byref(need), stream))
         return h
 
-    one = one_staged if inputs == "staged" else one_host
+    one = {"staged": one_staged, "host": one_host, "host2": one_host2}[inputs]
 
     L.god_index_free(one())  # warm-up
     torch.cuda.synchronize()

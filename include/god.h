@@ -166,6 +166,22 @@ GOD_API god_status god_seed_reads_compact(const god_index* idx, const uint8_t* r
                                           god_anchor_compact* anchors, uint64_t* anchor_offsets, uint64_t cap,
                                           uint64_t* needed, god_stream stream);
 
+/* Index build and seeding in one call (the mapper's flow: P:286 (1)-(3) then P:298-308 on one reference
+ * and one read set), with the transfers overlapped across the two stages.  Same results as
+ * god_build_index(prm, ref, ref_offsets, n_refs, cutoff, out_index, stream) followed by god_seed_reads
+ * (compact == 0: anchors is god_anchor[cap]) or god_seed_reads_compact (compact != 0: anchors is
+ * god_anchor_compact[cap]) on *out_index; every argument as documented there.  With host buffers and
+ * >= 2^21 reads the first read batches are queued on the copy stream right behind the reference, so the
+ * host link stays busy while the index is sorted; otherwise it is exactly the two calls in sequence.
+ * *out_index is set as soon as the index is built, also when the seeding part then fails (GOD_ETRUNC
+ * with *needed, or an error): the caller owns it (god_index_free).  Synchronizes. */
+GOD_API god_status god_build_index_and_seed(const god_params* prm, const uint8_t* ref, const uint64_t* ref_offsets,
+                                            uint32_t n_refs, const god_cutoff* cutoff, god_index** out_index,
+                                            const uint8_t* reads, const uint64_t* read_offsets, uint32_t n_reads,
+                                            god_phase_mode mode, uint8_t* phases, uint32_t t, int compact,
+                                            void* anchors, uint64_t* anchor_offsets, uint64_t cap, uint64_t* needed,
+                                            god_stream stream);
+
 /* ---- location voting (section 3.4, Fig. 8; rescue P:398) ----
  * Consumes the anchors of god_seed_reads (same reads, same phases).  Readings (DESIGN.md §2,
  * V1-V6):

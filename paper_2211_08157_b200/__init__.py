@@ -250,6 +250,42 @@ def god_seed_reads(index: GodIndex, reads, read_offsets, phases=None, t: int = 1
     raise GodError(_lib.GOD_ETRUNC, "anchor capacity retry failed")
 
 
+def god_build_index_and_seed(ref, ref_offsets, reads, read_offsets, pattern: str, k: int, w: int, cutoff=(1, 5000),
+                             max_occ=None, phases=None, t: int = 16, cap: int | None = None, compact: bool = False):
+    """god_build_index + god_seed_reads in one call (include/god.h): with host inputs the first read
+    batches go up right behind the reference, while the index is sorted.  All inputs on the host, or all
+    on the device; outputs live where the inputs do.  -> (GodIndex, anchors, anchor_offsets, phases)."""
+    L = _lib.load()
+    dev = _is_cuda(ref)
+    if dev != _is_cuda(reads):
+        raise TypeError("ref and reads must both be CUDA tensors or both host arrays")
+    ref, ref_offsets = _prep(ref, np.uint8), _prep(ref_offsets, np.uint64)
+    reads, read_offsets = _prep(reads, np.uint8), _prep(read_offsets, np.uint64)
+    n_refs, n = int(ref_offsets.shape[0]) - 1, int(read_offsets.shape[0]) - 1
+    dv = reads.device if dev else None
+    prm = _params(pattern, k, w)
+    cut = _lib.GodCutoff(1, 0, 1, int(max_occ)) if max_occ is not None else _lib.GodCutoff(0, cutoff[0], cutoff[1], 0)
+    mode = _lib.PHASE_SELECT if phases is None else _lib.PHASE_GIVEN
+    ph = _empty(max(1, n), np.uint8, dev, dv) if phases is None else _prep(phases, np.uint8).clone() if dev \
+        else _prep(phases, np.uint8).copy()
+    ao = _empty(n + 1, np.uint64, dev, dv)
+    if cap is None:
+        cap = int(reads.shape[0]) // 4 + 1024
+    an = torch.empty((max(1, cap), 2 if compact else 4), dtype=torch.uint32, device=dv) if dev else \
+        np.zeros(max(1, cap), ANCHOR_COMPACT_DTYPE if compact else ANCHOR_DTYPE)
+    need = ctypes.c_uint64(0)
+    h = ctypes.c_void_p(0)
+    rc = L.god_build_index_and_seed(ctypes.byref(prm), _ptr(ref), _ptr(ref_offsets), n_refs, ctypes.byref(cut),
+                                    ctypes.byref(h), _ptr(reads), _ptr(read_offsets), n, mode, _ptr(ph), int(t),
+                                    1 if compact else 0, _ptr(an), _ptr(ao), cap, ctypes.byref(need), _stream(dev))
+    index = GodIndex(h, pattern, k, w) if h.value else None
+    if rc == _lib.GOD_ETRUNC and index is not None:  # the index stands; seed again with the capacity asked for
+        an, ao, ph = god_seed_reads(index, reads, read_offsets, phases=ph[:n], t=t, cap=need.value, compact=compact)
+        return index, an, ao, ph
+    _lib.check(rc)
+    return index, an[: need.value], ao, ph[:n]
+
+
 def expand_compact(anchors, anchor_offsets) -> np.ndarray:
     """god_anchor_compact (host or device) -> ANCHOR_DTYPE on the host (argument marshalling for
     callers and tests: the read id is the anchor's segment in anchor_offsets)."""
@@ -425,4 +461,4 @@ def launch_count() -> int:
 __all__ = ["god_sparsify", "god_minimizers", "god_build_index", "god_seed_reads", "god_vote_reads", "votes_numpy",
            "god_contain", "god_seed_harness",
            "god_harness_accepted",
-           "expand_compact", "GodIndex", "GodError", "ANCHOR_DTYPE", "ANCHOR_COMPACT_DTYPE", "VOTE_DTYPE", "version"]
+           "expand_compact", "god_build_index_and_seed", "GodIndex", "GodError", "ANCHOR_DTYPE", "ANCHOR_COMPACT_DTYPE", "VOTE_DTYPE", "version"]

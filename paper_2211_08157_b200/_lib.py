@@ -48,7 +48,7 @@ class GodIndexStats(ctypes.Structure):
 # every symbol include/god.h declares (tests/test_abi.py checks header <-> library agreement)
 EXPORTS = ("god_last_error", "god_version", "god_sparsify", "god_minimizers", "god_build_index",
            "god_index_get_stats", "god_index_dump", "god_index_count", "god_index_free", "god_seed_reads",
-           "god_seed_reads_compact",
+           "god_seed_reads_compact", "god_build_index_and_seed",
            "god_vote_reads", "god_contain", "god_seed_harness",
            "god_harness_accepted",
            "god_profile_enable", "god_profile_reset", "god_profile_query", "god_launch_count",
@@ -79,6 +79,8 @@ def load():
     L.god_index_free.restype = None
     L.god_seed_reads.argtypes = [vp, vp, vp, u32, i32, vp, u32, vp, vp, u64, P(ctypes.c_uint64), vp]
     L.god_seed_reads_compact.argtypes = L.god_seed_reads.argtypes
+    L.god_build_index_and_seed.argtypes = [P(GodParams), vp, vp, u32, P(GodCutoff), P(vp),
+                                           vp, vp, u32, i32, vp, u32, i32, vp, vp, u64, P(ctypes.c_uint64), vp]
     L.god_vote_reads.argtypes = [vp, vp, vp, u32, vp, vp, vp, P(GodVoteParams), vp, vp, u64, P(ctypes.c_uint64), vp]
     L.god_contain.argtypes = [P(GodParams), vp, vp, u32, P(GodCutoff), vp, vp, u32, u32, P(GodVoteParams),
                               P(GodContainParams), vp, vp, vp, vp]
@@ -95,7 +97,7 @@ def load():
     L.god_launch_count.argtypes = []
     L.god_launch_count.restype = u64
     for name in ("god_sparsify", "god_minimizers", "god_build_index", "god_index_get_stats", "god_index_dump",
-                 "god_index_count", "god_seed_reads", "god_seed_reads_compact"):
+                 "god_index_count", "god_seed_reads", "god_seed_reads_compact", "god_build_index_and_seed"):
         getattr(L, name).restype = i32
     _lib = L
     return L

@@ -2,6 +2,7 @@
 // api.cu — the C ABI (include/god.h): validation, host/device staging, dispatch to the kernels.
 #include <atomic>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <mutex>
 #include <string>
@@ -298,56 +299,100 @@ static void copy_streams(cudaStream_t& s_h2d, cudaStream_t& s_d2h) {
   s_d2h = d2h_of[dev_ord & 63];
 }
 
-static uint64_t seed_reads_pipelined(const god_index* idx, const uint8_t* reads, const uint64_t* offs, uint32_t n_reads,
-                                     god_phase_mode mode, uint8_t* phases, uint32_t t, void* anchors,
-                                     uint64_t* anchor_offsets, uint64_t cap, uint32_t n_batches, cudaStream_t st,
-                                     bool reads_on_device, bool compact, uint32_t* bad_compact) {
-  cudaStream_t s_h2d, s_d2h;
-  copy_streams(s_h2d, s_d2h);
-  PipeSlot slot[2];
-  for (auto& sl : slot) {
-    GOD_CUDA(cudaEventCreateWithFlags(&sl.h2d_done, cudaEventDisableTiming));
-    GOD_CUDA(cudaEventCreateWithFlags(&sl.comp_done, cudaEventDisableTiming));
-    GOD_CUDA(cudaEventCreateWithFlags(&sl.d2h_done, cudaEventDisableTiming));
-  }
+// Pipelined seeding of host (or device) reads with host outputs: read batches go up on the copy stream,
+// each is seeded on `st` when it is in, and its results go down on the other copy stream, through a ring
+// of PIPE_SLOTS device buffer sets (uploads run up to PIPE_SLOTS - 1 batches ahead of the seeding).
+// prefetch() needs no index: god_build_index_and_seed queues the first uploads right behind the
+// reference's chunks, so the link stays busy while the index is sorted.
+constexpr uint32_t PIPE_SLOTS = 4;
+struct SeedPipe {
+  const uint8_t* reads;
+  const uint64_t* offs;
+  uint32_t n_reads;
+  god_phase_mode mode;
+  uint8_t* phases;
+  uint32_t t;
+  void* anchors;
+  uint64_t* anchor_offsets;
+  uint64_t cap;
+  uint32_t n_batches;
+  cudaStream_t st, s_h2d, s_d2h;
+  bool reads_on_device, compact;
+  uint32_t* bad_compact;
+  PipeSlot slot[PIPE_SLOTS];
+  uint32_t per = 0, uploaded = 0;
+  std::vector<uint64_t> boff;
+  std::vector<const uint8_t*> breads;
   // GOD_PIPE_TRACE: developer aid, device timeline of every batch's upload / seeding / download
-  const bool trace = getenv("GOD_PIPE_TRACE") != nullptr;
+  bool trace = false;
   std::vector<cudaEvent_t> tev;  // 6 per batch: h2d begin/end, seeding begin/end, d2h begin/end
   cudaEvent_t t_origin = nullptr;
-  auto mark = [&](uint32_t b, int which, cudaStream_t s) {
+
+  SeedPipe(const uint8_t* reads_, const uint64_t* offs_, uint32_t n_reads_, god_phase_mode mode_, uint8_t* phases_,
+           uint32_t t_, void* anchors_, uint64_t* anchor_offsets_, uint64_t cap_, uint32_t n_batches_, cudaStream_t st_,
+           bool reads_on_device_, bool compact_, uint32_t* bad_compact_)
+      : reads(reads_), offs(offs_), n_reads(n_reads_), mode(mode_), phases(phases_), t(t_), anchors(anchors_),
+        anchor_offsets(anchor_offsets_), cap(cap_), n_batches(n_batches_), st(st_), reads_on_device(reads_on_device_),
+        compact(compact_), bad_compact(bad_compact_) {
+    copy_streams(s_h2d, s_d2h);
+    for (auto& sl : slot) {
+      GOD_CUDA(cudaEventCreateWithFlags(&sl.h2d_done, cudaEventDisableTiming));
+      GOD_CUDA(cudaEventCreateWithFlags(&sl.comp_done, cudaEventDisableTiming));
+      GOD_CUDA(cudaEventCreateWithFlags(&sl.d2h_done, cudaEventDisableTiming));
+    }
+    trace = getenv("GOD_PIPE_TRACE") != nullptr;
+    if (trace) {
+      tev.resize((size_t)n_batches * 6);
+      for (auto& e : tev) GOD_CUDA(cudaEventCreate(&e));
+      GOD_CUDA(cudaEventCreate(&t_origin));
+      GOD_CUDA(cudaEventRecord(t_origin, st));
+    }
+    per = (n_reads + n_batches - 1) / n_batches;
+    for (auto& sl : slot) {
+      GOD_CUDA(cudaMallocAsync((void**)&sl.ph, (uint64_t)per + 1, st));
+      GOD_CUDA(cudaMallocAsync((void**)&sl.aoff, ((uint64_t)per + 1) * sizeof(uint64_t), st));
+    }
+    // byte offset of each batch's first read (device-resident offsets: one small copy per batch start)
+    boff.resize(n_batches + 1);
+    for (uint32_t b = 0; b <= n_batches; b++) {
+      if (reads_on_device) d2h_small(&boff[b], offs + r_begin(b), 8, st);
+      else boff[b] = offs[r_begin(b)];
+    }
+    GOD_CUDA(cudaStreamSynchronize(st));  // the slots' phase / offset buffers exist before another stream uses them
+    breads.resize(n_batches);
+  }
+  SeedPipe(const SeedPipe&) = delete;
+  SeedPipe& operator=(const SeedPipe&) = delete;
+  ~SeedPipe() {
+    cudaStreamSynchronize(s_d2h);
+    cudaStreamSynchronize(s_h2d);
+    for (auto& sl : slot) {
+      if (sl.reads) cudaFreeAsync(sl.reads, st);
+      if (sl.off) cudaFreeAsync(sl.off, st);
+      if (sl.ph) cudaFreeAsync(sl.ph, st);
+      if (sl.aoff) cudaFreeAsync(sl.aoff, st);
+      if (sl.an) cudaFreeAsync(sl.an, st);
+      if (sl.anc) cudaFreeAsync(sl.anc, st);
+      cudaEventDestroy(sl.h2d_done);
+      cudaEventDestroy(sl.comp_done);
+      cudaEventDestroy(sl.d2h_done);
+    }
+    for (auto& e : tev) cudaEventDestroy(e);
+    if (t_origin) cudaEventDestroy(t_origin);
+    cudaStreamSynchronize(st);
+  }
+  uint64_t r_begin(uint32_t b) const { return std::min<uint64_t>((uint64_t)b * per, n_reads); }
+  void mark(uint32_t b, int which, cudaStream_t s) {
     if (trace) GOD_CUDA(cudaEventRecord(tev[b * 6 + which], s));
-  };
-  if (trace) {
-    tev.resize((size_t)n_batches * 6);
-    for (auto& e : tev) GOD_CUDA(cudaEventCreate(&e));
-    GOD_CUDA(cudaEventCreate(&t_origin));
-    GOD_CUDA(cudaEventRecord(t_origin, st));
   }
-  uint64_t written = 0;  // anchors before the current batch
-  const uint32_t per = (n_reads + n_batches - 1) / n_batches;
-  for (auto& sl : slot) {
-    GOD_CUDA(cudaMallocAsync((void**)&sl.ph, (uint64_t)per + 1, st));
-    GOD_CUDA(cudaMallocAsync((void**)&sl.aoff, ((uint64_t)per + 1) * sizeof(uint64_t), st));
-  }
-  GOD_CUDA(cudaStreamSynchronize(st));
-  auto r_begin = [&](uint32_t b) { return std::min<uint64_t>((uint64_t)b * per, n_reads); };
-  // byte offset of each batch's first read (device-resident offsets: one small copy per batch start)
-  std::vector<uint64_t> boff(n_batches + 1);
-  for (uint32_t b = 0; b <= n_batches; b++) {
-    if (reads_on_device) d2h_small(&boff[b], offs + r_begin(b), 8, st);
-    else boff[b] = offs[r_begin(b)];
-  }
-  GOD_CUDA(cudaStreamSynchronize(st));
-  std::vector<const uint8_t*> breads(n_batches);
-  auto upload = [&](uint32_t b) {
-    PipeSlot& sl = slot[b & 1];
+  // queue the upload of batch b into its slot (its previous user, batch b - PIPE_SLOTS, has been seeded:
+  // the slot's INPUT buffers are free then; the results leave from other buffers, so an upload never
+  // waits for a download)
+  void upload(uint32_t b) {
+    PipeSlot& sl = slot[b % PIPE_SLOTS];
     const uint64_t r0 = r_begin(b), r1 = r_begin(b + 1), nb = r1 - r0;
     const uint64_t bytes = boff[b + 1] - boff[b];
-    // the slot's INPUT buffers (reads, offsets, given phases) are free once batch b-2's seeding has read
-    // them; its results leave from other buffers (an/anc, aoff, the selected phases), so the upload does
-    // not wait for that copy (it did: uploads and downloads then alternated instead of overlapping,
-    // 44 -> 33 ms for the 10 M reads of the human config)
-    if (sl.off) GOD_CUDA(cudaStreamWaitEvent(s_h2d, sl.comp_done, 0));
+    if (b >= PIPE_SLOTS) GOD_CUDA(cudaStreamWaitEvent(s_h2d, sl.comp_done, 0));
     grow(sl.off, sl.off_cap, nb + 1, s_h2d);
     if (!reads_on_device) grow(sl.reads, sl.reads_cap, bytes + 16, s_h2d);
     mark(b, 0, s_h2d);
@@ -362,78 +407,86 @@ static uint64_t seed_reads_pipelined(const god_index* idx, const uint8_t* reads,
     if (mode == GOD_PHASE_GIVEN && nb) GOD_CUDA(cudaMemcpyAsync(sl.ph, phases + r0, nb, cudaMemcpyHostToDevice, s_h2d));
     GOD_CUDA(cudaEventRecord(sl.h2d_done, s_h2d));
     mark(b, 1, s_h2d);
-  };
-  upload(0);
-  set_copies_in_flight(true);
-  struct Reset { ~Reset() { set_copies_in_flight(false); } } reset_flag;
-  for (uint32_t b = 0; b < n_batches; b++) {
-    PipeSlot& sl = slot[b & 1];
-    if (b + 1 < n_batches) upload(b + 1);
-    const uint64_t r0 = r_begin(b), r1 = r_begin(b + 1), nb = r1 - r0;
-    GOD_CUDA(cudaStreamWaitEvent(st, sl.h2d_done, 0));
-    mark(b, 2, st);
-    GOD_LAUNCH("k_rebase", k_rebase_u64, grid_for(nb + 1, 256), 256, 0, st, sl.off, nb + 1, boff[b], 0ull);
-    // anchors of this batch: a share of the caller's capacity, grown and redone if too small
-    uint64_t want = cap ? std::min<uint64_t>(cap, cap / n_batches + cap / (4 * n_batches) + 4096) : 4096;
-    uint64_t tot = 0;
-    for (int attempt = 0; attempt < 2; attempt++) {
-      if (sl.d2h_pending) GOD_CUDA(cudaStreamWaitEvent(st, sl.d2h_done, 0));
-      grow(sl.an, sl.an_cap, want, st);
-      tot = god::seed_reads(idx, breads[b], sl.off, (uint32_t)nb, mode, sl.ph, t, sl.an, sl.aoff, sl.an_cap, st,
-                            (uint32_t)r0);
-      if (tot <= sl.an_cap) break;
-      want = tot;
-    }
-    // offsets of this batch -> global anchor offsets
-    GOD_LAUNCH("k_rebase", k_rebase_u64, grid_for(nb + 1, 256), 256, 0, st, sl.aoff, nb + 1, 0ull, written);
-    const void* src = sl.an;
-    size_t asz = sizeof(god_anchor);
-    if (compact && tot && tot <= sl.an_cap) {  // 8-B anchors leave the device: half the copy
-      grow(sl.anc, sl.anc_cap, tot, st);
-      GOD_LAUNCH("k_compact_anchors", k_compact_anchors, grid_for(tot, 256), 256, 0, st, sl.an, tot, sl.anc,
-                 bad_compact);
-      src = sl.anc;
-      asz = sizeof(god_anchor_compact);
-    }
-    GOD_CUDA(cudaEventRecord(sl.comp_done, st));
-    mark(b, 3, st);
-    GOD_CUDA(cudaStreamWaitEvent(s_d2h, sl.comp_done, 0));
-    mark(b, 4, s_d2h);
-    if (written + tot <= cap && tot)
-      GOD_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(anchors) + written * asz, src, tot * asz, cudaMemcpyDeviceToHost,
-                               s_d2h));
-    GOD_CUDA(cudaMemcpyAsync(anchor_offsets + r0, sl.aoff, (nb + 1) * sizeof(uint64_t), cudaMemcpyDeviceToHost, s_d2h));
-    if (mode == GOD_PHASE_SELECT && nb) GOD_CUDA(cudaMemcpyAsync(phases + r0, sl.ph, nb, cudaMemcpyDeviceToHost, s_d2h));
-    GOD_CUDA(cudaEventRecord(sl.d2h_done, s_d2h));
-    mark(b, 5, s_d2h);
-    sl.d2h_pending = true;
-    written += tot;
   }
-  GOD_CUDA(cudaStreamSynchronize(s_d2h));
-  GOD_CUDA(cudaStreamSynchronize(s_h2d));
-  if (trace) {
+  // uploads that fit the ring before any batch is seeded
+  void prefetch() {
+    while (uploaded < n_batches && uploaded < PIPE_SLOTS) upload(uploaded++);
+  }
+  // seed every batch against idx; returns the anchors in total (written while they fit cap)
+  uint64_t run(const god_index* idx) {
+    prefetch();
+    uint64_t written = 0;  // anchors before the current batch
+    const size_t asz_out = compact ? sizeof(god_anchor_compact) : sizeof(god_anchor);
+    set_copies_in_flight(true);
+    struct Reset { ~Reset() { set_copies_in_flight(false); } } reset_flag;
     for (uint32_t b = 0; b < n_batches; b++) {
-      float t[6];
-      for (int q = 0; q < 6; q++) GOD_CUDA(cudaEventElapsedTime(&t[q], t_origin, tev[b * 6 + q]));
-      fprintf(stderr, "[pipe] batch %u: h2d %.2f-%.2f  seed %.2f-%.2f  d2h %.2f-%.2f ms\n", b, t[0], t[1], t[2], t[3],
-              t[4], t[5]);
+      PipeSlot& sl = slot[b % PIPE_SLOTS];
+      const uint64_t r0 = r_begin(b), r1 = r_begin(b + 1), nb = r1 - r0;
+      GOD_CUDA(cudaStreamWaitEvent(st, sl.h2d_done, 0));
+      mark(b, 2, st);
+      GOD_LAUNCH("k_rebase", k_rebase_u64, grid_for(nb + 1, 256), 256, 0, st, sl.off, nb + 1, boff[b], 0ull);
+      // anchors of this batch: a share of the caller's capacity, grown and redone if too small
+      uint64_t want = cap ? std::min<uint64_t>(cap, cap / n_batches + cap / (4 * n_batches) + 4096) : 4096;
+      uint64_t tot = 0;
+      for (int attempt = 0; attempt < 2; attempt++) {
+        if (sl.d2h_pending) GOD_CUDA(cudaStreamWaitEvent(st, sl.d2h_done, 0));
+        grow(sl.an, sl.an_cap, want, st);
+        tot = god::seed_reads(idx, breads[b], sl.off, (uint32_t)nb, mode, sl.ph, t, sl.an, sl.aoff, sl.an_cap, st,
+                              (uint32_t)r0);
+        if (tot <= sl.an_cap) break;
+        want = tot;
+      }
+      // offsets of this batch -> global anchor offsets
+      GOD_LAUNCH("k_rebase", k_rebase_u64, grid_for(nb + 1, 256), 256, 0, st, sl.aoff, nb + 1, 0ull, written);
+      const void* src = sl.an;
+      if (compact && tot && tot <= sl.an_cap) {  // 8-B anchors leave the device: half the copy
+        grow(sl.anc, sl.anc_cap, tot, st);
+        GOD_LAUNCH("k_compact_anchors", k_compact_anchors, grid_for(tot, 256), 256, 0, st, sl.an, tot, sl.anc,
+                   bad_compact);
+        src = sl.anc;
+      }
+      GOD_CUDA(cudaEventRecord(sl.comp_done, st));
+      mark(b, 3, st);
+      if (uploaded < n_batches) upload(uploaded++);  // batch b + PIPE_SLOTS takes this slot's input buffers
+      GOD_CUDA(cudaStreamWaitEvent(s_d2h, sl.comp_done, 0));
+      mark(b, 4, s_d2h);
+      if (written + tot <= cap && tot)
+        GOD_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(anchors) + written * asz_out, src, tot * asz_out,
+                                 cudaMemcpyDeviceToHost, s_d2h));
+      GOD_CUDA(cudaMemcpyAsync(anchor_offsets + r0, sl.aoff, (nb + 1) * sizeof(uint64_t), cudaMemcpyDeviceToHost, s_d2h));
+      if (mode == GOD_PHASE_SELECT && nb) GOD_CUDA(cudaMemcpyAsync(phases + r0, sl.ph, nb, cudaMemcpyDeviceToHost, s_d2h));
+      GOD_CUDA(cudaEventRecord(sl.d2h_done, s_d2h));
+      mark(b, 5, s_d2h);
+      sl.d2h_pending = true;
+      written += tot;
     }
-    for (auto& e : tev) cudaEventDestroy(e);
-    cudaEventDestroy(t_origin);
+    GOD_CUDA(cudaStreamSynchronize(s_d2h));
+    GOD_CUDA(cudaStreamSynchronize(s_h2d));
+    if (trace) {
+      for (uint32_t b = 0; b < n_batches; b++) {
+        float tm[6];
+        for (int q = 0; q < 6; q++) GOD_CUDA(cudaEventElapsedTime(&tm[q], t_origin, tev[b * 6 + q]));
+        fprintf(stderr, "[pipe] batch %u: h2d %.2f-%.2f  seed %.2f-%.2f  d2h %.2f-%.2f ms\n", b, tm[0], tm[1], tm[2],
+                tm[3], tm[4], tm[5]);
+      }
+    }
+    return written;
   }
-  for (auto& sl : slot) {
-    if (sl.reads) cudaFreeAsync(sl.reads, st);
-    if (sl.off) cudaFreeAsync(sl.off, st);
-    if (sl.ph) cudaFreeAsync(sl.ph, st);
-    if (sl.aoff) cudaFreeAsync(sl.aoff, st);
-    if (sl.an) cudaFreeAsync(sl.an, st);
-    if (sl.anc) cudaFreeAsync(sl.anc, st);
-    cudaEventDestroy(sl.h2d_done);
-    cudaEventDestroy(sl.comp_done);
-    cudaEventDestroy(sl.d2h_done);
-  }
-  GOD_CUDA(cudaStreamSynchronize(st));
-  return written;
+};
+
+// whether a seeding call takes the pipelined path, and in how many batches (0: the plain path)
+static uint32_t pipe_batches(const void* reads, const void* read_offsets, uint32_t n_reads, const void* phases,
+                             const void* anchor_offsets, const void* anchors) {
+  const char* pm = getenv("GOD_PIPE_MIN_READS");  // test hook: smaller batches
+  const uint32_t pipe_min = pm ? (uint32_t)atoi(pm) : (1u << 20);  // reads per batch
+  const uint32_t n_batches = std::min<uint32_t>(8u, n_reads / (pipe_min ? pipe_min : 1u));
+  // reads and their offsets both on the host, or both on the device (then only the results are
+  // streamed back); phases, anchor offsets and anchors on the host
+  const bool rdev = is_device_ptr(reads), odev = is_device_ptr(read_offsets);
+  if (n_batches >= 2 && rdev == odev && !is_device_ptr(phases) && !is_device_ptr(anchor_offsets) &&
+      (!anchors || !is_device_ptr(anchors)))
+    return n_batches;
+  return 0;
 }
 
 extern "C" {
@@ -546,74 +599,89 @@ GOD_API god_status god_minimizers(const god_params* prm, const uint8_t* seq, con
   });
 }
 
-GOD_API god_status god_build_index(const god_params* prm, const uint8_t* ref, const uint64_t* ref_offsets,
-                                   uint32_t n_refs, const god_cutoff* cutoff, god_index** out, god_stream stream) {
-  return guarded([&] {
-    Params P = make_params(prm);
-    GOD_REQUIRE(ref_offsets && out && cutoff, "NULL argument");
-    GOD_REQUIRE(cutoff->mode <= 1, "cutoff mode must be 0 (fraction) or 1 (max_occ)");
-    GOD_REQUIRE(cutoff->mode == 1 || cutoff->frac_den > 0, "cutoff frac_den must be > 0");
-    *out = nullptr;
-    cudaStream_t st = (cudaStream_t)stream;
-    Scratch scr(st);
-    Stage sg(st, scr);
-    const uint64_t L = total_len(ref_offsets, n_refs, st);
-    GOD_REQUIRE(L < (1ull << 32), "total reference length must be < 2^32 (u32 positions)");
-    // A large host reference is streamed: chunks go up on the copy stream while K1 (stage 1+2) runs on
-    // the tiles whose bytes are in, so only the sort and the table build follow the transfer.
-    // GOD_STREAM_CHUNK_BYTES: test hook (chunk size; 0 disables streaming).
-    const char* sc = getenv("GOD_STREAM_CHUNK_BYTES");
-    const uint64_t want_chunk = sc ? strtoull(sc, nullptr, 10) : (32ull << 20);
-    const uint64_t max_chunks = 16;
-    god::SeqStream ss;
-    struct EvGuard {
-      god::SeqStream& s;
-      ~EvGuard() {
-        if (!s.arrived.empty()) set_copies_in_flight(false);
-        for (cudaEvent_t e : s.arrived) cudaEventDestroy(e);
-      }
-    } ev_guard{ss};
-    const uint8_t* dref;
-    if (ref && !is_device_ptr(ref) && want_chunk && L >= 2 * want_chunk) {
-      uint8_t* d = scr.alloc<uint8_t>(L);
+}  // extern "C"
+
+// god_build_index's body.  after_ref_queued (optional) runs once the reference's copies have been queued
+// on the copy stream (or started on `st` when it is not streamed): god_build_index_and_seed queues the
+// first read batches behind them there.
+static void build_index_entry(const god_params* prm, const uint8_t* ref, const uint64_t* ref_offsets, uint32_t n_refs,
+                              const god_cutoff* cutoff, god_index** out, god_stream stream,
+                              const std::function<void()>& after_ref_queued) {
+  Params P = make_params(prm);
+  GOD_REQUIRE(ref_offsets && out && cutoff, "NULL argument");
+  GOD_REQUIRE(cutoff->mode <= 1, "cutoff mode must be 0 (fraction) or 1 (max_occ)");
+  GOD_REQUIRE(cutoff->mode == 1 || cutoff->frac_den > 0, "cutoff frac_den must be > 0");
+  *out = nullptr;
+  cudaStream_t st = (cudaStream_t)stream;
+  Scratch scr(st);
+  Stage sg(st, scr);
+  const uint64_t L = total_len(ref_offsets, n_refs, st);
+  GOD_REQUIRE(L < (1ull << 32), "total reference length must be < 2^32 (u32 positions)");
+  // A large host reference is streamed: chunks go up on the copy stream while K1 (stage 1+2) runs on
+  // the tiles whose bytes are in, so only the sort and the table build follow the transfer.
+  // GOD_STREAM_CHUNK_BYTES: test hook (chunk size; 0 disables streaming).
+  const char* sc = getenv("GOD_STREAM_CHUNK_BYTES");
+  const uint64_t want_chunk = sc ? strtoull(sc, nullptr, 10) : (32ull << 20);
+  const uint64_t max_chunks = 16;
+  god::SeqStream ss;
+  struct EvGuard {
+    god::SeqStream& s;
+    ~EvGuard() {
+      if (!s.arrived.empty()) set_copies_in_flight(false);
+      for (cudaEvent_t e : s.arrived) cudaEventDestroy(e);
+    }
+  } ev_guard{ss};
+  const uint8_t* dref;
+  bool queued = false;
+  if (ref && !is_device_ptr(ref) && want_chunk && L >= 2 * want_chunk) {
+    uint8_t* d = scr.alloc<uint8_t>(L);
+    cudaStream_t s_h2d, s_d2h;
+    copy_streams(s_h2d, s_d2h);
+    uint64_t chunk = std::max<uint64_t>(want_chunk, (L + max_chunks - 1) / max_chunks);
+    chunk = (chunk + 255) & ~255ull;
+    cudaEvent_t ready;  // the allocation is stream-ordered on st
+    GOD_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    GOD_CUDA(cudaEventRecord(ready, st));
+    GOD_CUDA(cudaStreamWaitEvent(s_h2d, ready, 0));
+    GOD_CUDA(cudaEventDestroy(ready));  // (released once the wait has completed)
+    ss.chunk_bytes = chunk;
+    for (uint64_t o = 0; o < L; o += chunk) {
+      cudaEvent_t e;
+      GOD_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      ss.arrived.push_back(e);
+      GOD_CUDA(cudaMemcpyAsync(d + o, ref + o, std::min<uint64_t>(chunk, L - o), cudaMemcpyHostToDevice, s_h2d));
+      GOD_CUDA(cudaEventRecord(e, s_h2d));
+    }
+    set_copies_in_flight(true);  // small device->host reads go through the mapped page meanwhile
+    if (after_ref_queued) after_ref_queued();
+    queued = true;
+    dref = d;
+  } else {
+    dref = sg.in(ref, L);
+  }
+  if (!queued && after_ref_queued) after_ref_queued();
+  const uint64_t* doff = sg.in(ref_offsets, (size_t)n_refs + 1);
+  god_index* ix = new god_index();
+  try {
+    god::build_index(P, dref, doff, n_refs, *cutoff, ix, st, ss.arrived.empty() ? nullptr : &ss);
+  } catch (...) {
+    if (!ss.arrived.empty()) {
       cudaStream_t s_h2d, s_d2h;
       copy_streams(s_h2d, s_d2h);
-      uint64_t chunk = std::max<uint64_t>(want_chunk, (L + max_chunks - 1) / max_chunks);
-      chunk = (chunk + 255) & ~255ull;
-      cudaEvent_t ready;  // the allocation is stream-ordered on st
-      GOD_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
-      GOD_CUDA(cudaEventRecord(ready, st));
-      GOD_CUDA(cudaStreamWaitEvent(s_h2d, ready, 0));
-      GOD_CUDA(cudaEventDestroy(ready));  // (released once the wait has completed)
-      ss.chunk_bytes = chunk;
-      for (uint64_t o = 0; o < L; o += chunk) {
-        cudaEvent_t e;
-        GOD_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        ss.arrived.push_back(e);
-        GOD_CUDA(cudaMemcpyAsync(d + o, ref + o, std::min<uint64_t>(chunk, L - o), cudaMemcpyHostToDevice, s_h2d));
-        GOD_CUDA(cudaEventRecord(e, s_h2d));
-      }
-      set_copies_in_flight(true);  // small device->host reads go through the mapped page meanwhile
-      dref = d;
-    } else {
-      dref = sg.in(ref, L);
+      cudaStreamSynchronize(s_h2d);  // the copies target scratch memory that is about to be freed
     }
-    const uint64_t* doff = sg.in(ref_offsets, (size_t)n_refs + 1);
-    god_index* ix = new god_index();
-    try {
-      god::build_index(P, dref, doff, n_refs, *cutoff, ix, st, ss.arrived.empty() ? nullptr : &ss);
-    } catch (...) {
-      if (!ss.arrived.empty()) {
-        cudaStream_t s_h2d, s_d2h;
-        copy_streams(s_h2d, s_d2h);
-        cudaStreamSynchronize(s_h2d);  // the copies target scratch memory that is about to be freed
-      }
-      god_index_free(ix);
-      throw;
-    }
-    sg.finish();
-    *out = ix;
-  });
+    god_index_free(ix);
+    throw;
+  }
+  sg.finish();
+  *out = ix;
+}
+
+extern "C" {
+
+GOD_API god_status god_build_index(const god_params* prm, const uint8_t* ref, const uint64_t* ref_offsets,
+                                   uint32_t n_refs, const god_cutoff* cutoff, god_index** out, god_stream stream) {
+  return guarded([&] { build_index_entry(prm, ref, ref_offsets, n_refs, cutoff, out, stream, nullptr); });
 }
 
 GOD_API god_status god_index_get_stats(const god_index* idx, god_index_stats* out_host) {
@@ -678,20 +746,17 @@ static void seed_entry(const god_index* idx, const uint8_t* reads, const uint64_
     for (uint32_t i = 0; i < n_reads; i++) GOD_REQUIRE(phases[i] < idx->P.pat.p, "phase >= p");
   cudaStream_t st = (cudaStream_t)stream;
   const size_t asz = compact ? sizeof(god_anchor_compact) : sizeof(god_anchor);
-  // all-host buffers and a large batch: pipelined transfers (see seed_reads_pipelined)
-  const char* pm = getenv("GOD_PIPE_MIN_READS");  // test hook: smaller batches
-  const uint32_t pipe_min = pm ? (uint32_t)atoi(pm) : (1u << 20);  // reads per batch
-  const uint32_t n_batches = std::min<uint32_t>(8u, n_reads / (pipe_min ? pipe_min : 1u));
-  // reads and their offsets both on the host, or both on the device (then only the results are
-  // streamed back); phases, anchor offsets and anchors on the host
-  const bool rdev = is_device_ptr(reads), odev = is_device_ptr(read_offsets);
-  if (n_batches >= 2 && rdev == odev && !is_device_ptr(phases) && !is_device_ptr(anchor_offsets) &&
-      (!anchors || !is_device_ptr(anchors))) {
+  // all-host buffers and a large batch: pipelined transfers (SeedPipe)
+  if (const uint32_t n_batches = pipe_batches(reads, read_offsets, n_reads, phases, anchor_offsets, anchors)) {
     Scratch scr(st);
     uint32_t* bad = scr.alloc<uint32_t>(1);
     GOD_CUDA(cudaMemsetAsync(bad, 0, 4, st));
-    const uint64_t tot = seed_reads_pipelined(idx, reads, read_offsets, n_reads, mode, phases, t, anchors,
-                                              anchor_offsets, anchors ? cap : 0, n_batches, st, rdev, compact, bad);
+    uint64_t tot;
+    {
+      SeedPipe pipe(reads, read_offsets, n_reads, mode, phases, t, anchors, anchor_offsets, anchors ? cap : 0, n_batches,
+                    st, is_device_ptr(reads), compact, bad);
+      tot = pipe.run(idx);
+    }
     *needed = tot;
     if (compact) GOD_REQUIRE(d2h_scalar(bad, st) == 0, "compact anchors need read positions < 2^31");
     if (tot > cap) throw Fail{GOD_ETRUNC};
@@ -748,6 +813,46 @@ GOD_API god_status god_seed_reads_compact(const god_index* idx, const uint8_t* r
                                           uint64_t* needed, god_stream stream) {
   return guarded([&] {
     seed_entry(idx, reads, read_offsets, n_reads, mode, phases, t, anchors, true, anchor_offsets, cap, needed, stream);
+  });
+}
+
+GOD_API god_status god_build_index_and_seed(const god_params* prm, const uint8_t* ref, const uint64_t* ref_offsets,
+                                            uint32_t n_refs, const god_cutoff* cutoff, god_index** out_index,
+                                            const uint8_t* reads, const uint64_t* read_offsets, uint32_t n_reads,
+                                            god_phase_mode mode, uint8_t* phases, uint32_t t, int compact,
+                                            void* anchors, uint64_t* anchor_offsets, uint64_t cap, uint64_t* needed,
+                                            god_stream stream) {
+  return guarded([&] {
+    GOD_REQUIRE(out_index && read_offsets && phases && anchor_offsets && needed, "NULL argument");
+    GOD_REQUIRE(mode == GOD_PHASE_SELECT || mode == GOD_PHASE_GIVEN, "mode must be SELECT or GIVEN");
+    GOD_REQUIRE(t >= 1, "t must be >= 1");
+    GOD_REQUIRE(cap == 0 || anchors, "NULL anchors with nonzero capacity");
+    *out_index = nullptr;
+    const Params P = make_params(prm);
+    if (mode == GOD_PHASE_GIVEN && !is_device_ptr(phases))
+      for (uint32_t i = 0; i < n_reads; i++) GOD_REQUIRE(phases[i] < P.pat.p, "phase >= p");
+    cudaStream_t st = (cudaStream_t)stream;
+    const uint32_t n_batches = pipe_batches(reads, read_offsets, n_reads, phases, anchor_offsets, anchors);
+    if (!n_batches) {  // nothing to overlap: the two calls one after the other
+      build_index_entry(prm, ref, ref_offsets, n_refs, cutoff, out_index, stream, nullptr);
+      seed_entry(*out_index, reads, read_offsets, n_reads, mode, phases, t, anchors, compact != 0, anchor_offsets, cap,
+                 needed, stream);
+      return;
+    }
+    Scratch scr(st);
+    uint32_t* bad = scr.alloc<uint32_t>(1);
+    GOD_CUDA(cudaMemsetAsync(bad, 0, 4, st));
+    uint64_t tot;
+    {
+      SeedPipe pipe(reads, read_offsets, n_reads, mode, phases, t, anchors, anchor_offsets, anchors ? cap : 0, n_batches,
+                    st, is_device_ptr(reads), compact != 0, bad);
+      // the first read batches are queued on the copy stream right behind the reference
+      build_index_entry(prm, ref, ref_offsets, n_refs, cutoff, out_index, stream, [&] { pipe.prefetch(); });
+      tot = pipe.run(*out_index);
+    }
+    *needed = tot;
+    if (compact) GOD_REQUIRE(d2h_scalar(bad, st) == 0, "compact anchors need read positions < 2^31");
+    if (tot > cap) throw Fail{GOD_ETRUNC};
   });
 }
 

@@ -392,6 +392,48 @@ def test_seed_host_pipelined_batches(given, reads_dev, monkeypatch):
     assert np.array_equal(canon(an), canon(oan))
 
 
+@pytest.mark.parametrize("compact", [False, True])
+@pytest.mark.parametrize("where", ["host_overlapped", "host_plain", "device"])
+def test_build_index_and_seed(where, compact, monkeypatch):
+    """god_build_index_and_seed = god_build_index then god_seed_reads(_compact): with host buffers above the
+    batch threshold the first read batches are queued behind the streamed reference (both test hooks
+    shrink chunks and batches so that 16 chunks and 8 batches over a ring of 4 slots run here); below it,
+    and with device buffers, the two calls run in sequence.  Index, phases, offsets and anchors against the
+    oracle; a capacity that is too small keeps the index and reports the count."""
+    if where == "host_overlapped":
+        monkeypatch.setenv("GOD_PIPE_MIN_READS", "97")
+        monkeypatch.setenv("GOD_STREAM_CHUNK_BYTES", "20000")
+    rng = np.random.default_rng(29)
+    ref = synth.dup_genome(400_000, 17, dup_frac=0.2, lmin=300, lmax=2000)
+    roffs_ref = np.array([0, 150_000, 150_000, ref.size], np.uint64)
+    reads = synth.simulate_reads(ref, 800, 11, mu=5.5, sigma=1.0, lmin=1, lmax=4000, p_sub=0.01, p_ins=0.003,
+                                 p_del=0.003)
+    seqs = [reads.seq[int(reads.offsets[i]):int(reads.offsets[i + 1])] for i in range(reads.n)]
+    seqs[50:50] = [np.zeros(0, np.uint8), np.frombuffer(b"N" * 300, np.uint8)]
+    rs, ro = synth.concat(seqs)
+    ox = oracle.Index(ref, roffs_ref, "10", 21, 11, cutoff=(1, 500))
+    oan, oao, oph = ox.seed_reads(rs, ro)
+    conv = cu if where == "device" else (lambda a: a)
+    for cap in (None, 1000):
+        ix, an, ao, ph = god.god_build_index_and_seed(conv(ref), conv(roffs_ref), conv(rs), conv(ro), "10", 21, 11,
+                                                      cutoff=(1, 500), compact=compact, cap=cap)
+        for a, b in zip(ix.dump(), ox.dump()):
+            assert np.array_equal(np.asarray(a).astype(np.uint64), np.asarray(b).astype(np.uint64))
+        if where == "device":
+            an, ao, ph = np_(an), np_(ao), np_(ph)
+        assert np.array_equal(ph, oph) and np.array_equal(ao, oao)
+        full = god.expand_compact(an, ao) if compact else an
+        assert np.array_equal(canon(full), canon(oan))
+    ph_in = rng.integers(0, 2, size=len(ro) - 1).astype(np.uint8)
+    ix, an, ao, ph = god.god_build_index_and_seed(conv(ref), conv(roffs_ref), conv(rs), conv(ro), "10", 21, 11,
+                                                  cutoff=(1, 500), compact=compact, phases=conv(ph_in))
+    oan2, oao2, _ = ox.seed_reads(rs, ro, phases=ph_in)
+    if where == "device":
+        an, ao = np_(an), np_(ao)
+    assert np.array_equal(ao, oao2)
+    assert np.array_equal(canon(god.expand_compact(an, ao) if compact else an), canon(oan2))
+
+
 @pytest.mark.parametrize("where", ["device", "host", "host_pipelined", "reads_dev_pipelined"])
 def test_seed_compact_anchors(where, monkeypatch):
     """god_seed_reads_compact: the 8-byte anchors expand (read id from the offsets, strand from bit
