@@ -10,9 +10,11 @@ k=21, w=11, cutoff top 0.02%.  Inputs (3.1 GB + 1.5 GB) are larger than L2 (126 
 is needed between steps.
 
 value = reads seeded per second over the whole step (index build included), summed over ranks.
-e2e   = the same through the C ABI from pinned HOST buffers: every step copies the reference and
-        the reads in (the reads overlapped with the index build) and the anchors, offsets and
-        phases out (streamed back batch by batch while later batches are seeded).
+e2e   = the same through the C ABI from pinned HOST buffers, one god_build_index_and_seed call per
+        step: the reference goes up in chunks while K1 runs on the tiles that are in, the read
+        batches follow on the same copy stream while the index is sorted, and each batch's 8-B
+        anchors, offsets and phases stream back while later batches are seeded.  The last step's
+        host results are compared with the device-resident step's (e2e.equals_device_step).
 --impl reference: the CPU oracle (oracle/, plain single-threaded C) on a bounded sample of the
 same workload, extrapolated to the metric's unit (see cpu_baseline.sample).
 """
@@ -473,7 +475,8 @@ def main():
     # e2e through the C ABI with pinned host buffers
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(god, torch, cfg, pattern, k, w, n_anchors, args.e2e_steps, dist, world, dev, args.e2e_inputs)
+        e2e = run_e2e(god, torch, cfg, pattern, k, w, n_anchors, args.e2e_steps, dist, world, dev, args.e2e_inputs,
+                      outbuf)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -549,7 +552,7 @@ def run_vote(god, torch, dreads, droffs, dref, droff, cfg, pattern, k, w, args, 
                          "frac": round(alg / (ms / 1e3) / 1e9 / float(peaks.get("hbm_gbs", 6650.0)), 4)}}
 
 
-def run_e2e(god, torch, cfg, pattern, k, w, n_anchors, steps, dist, world, dev, inputs="host"):
+def run_e2e(god, torch, cfg, pattern, k, w, n_anchors, steps, dist, world, dev, inputs="host", device_out=None):
     href = torch.from_numpy(cfg.ref).pin_memory()
     hroff = torch.from_numpy(cfg.ref_offsets).pin_memory()
     hreads = torch.from_numpy(cfg.reads.seq).pin_memory()
@@ -642,8 +645,27 @@ def run_e2e(god, torch, cfg, pattern, k, w, n_anchors, steps, dist, world, dev, 
     ms = max_over_ranks(ms, dist, dev)
     h2d = cfg.ref.size + cfg.ref_offsets.nbytes + cfg.reads.seq.size + cfg.reads.offsets.nbytes
     d2h = int(need.value) * 8 + (n + 1) * 8 + n
+    # the host results of the last e2e step against the device-resident step's (untimed): same phases, same
+    # offsets, and every 8-B anchor = (ref_pos, read_pos | strand << 31) of the 16-B one, in the same order
+    same = None
+    if device_out and "an" in device_out:
+        try:
+            na = int(need.value)
+            dan, dao, dph = device_out["an"], device_out["ao"], device_out["ph"]
+            same = bool(int(dao.cpu()[n]) == na)
+            if same:
+                hc = an_host[: 2 * na].view(-1, 2).to(dev).to(torch.int64)
+                da = dan[:na].to(torch.int64)
+                same = bool(torch.equal(hc[:, 0], da[:, 0]) and torch.equal(hc[:, 1], da[:, 1] | (da[:, 3] << 31))
+                            and torch.equal(ao_host.to(dev).view(torch.int64), dao.view(torch.int64))
+                            and torch.equal(ph_host[:n].to(dev), dph[:n]))
+                del hc, da
+        except Exception as exc:  # never lose the bench line to the check itself
+            log(f"e2e result check did not run: {exc!r}")
+        log(f"e2e results equal the device-resident step's: {same}")
     return {"value": round(world * n / (ms / steps / 1e3), 1), "unit": "reads/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "steps": steps, "ms_per_step": round(ms / steps, 3), "inputs": inputs,
+            "equals_device_step": same,
             "outputs": "phases u8[n], anchor_offsets u64[n+1], god_anchor_compact[n_anchors] (8 B)"}
 
 

@@ -127,7 +127,9 @@ GOD_API god_status god_minimizers(const god_params* prm, const uint8_t* seq, con
  * Minimizers of every reference sequence (phase 0, global positions), sorted by (hash, pos),
  * counted per distinct hash, filtered by the cutoff, stored as a bucketed table: a directory over
  * the top B bits of the hash and, per kept entry, the remaining hash bits + strand and the
- * position.  *out receives a library-owned handle.  Synchronizes `stream`. */
+ * position.  *out receives a library-owned handle.  Synchronizes `stream`.
+ * A host reference of >= 64 MB (pinned memory for the overlap to be real) is streamed: it goes up in
+ * chunks on a copy stream while stage 1+2 runs on the parts that are in; the result is the same. */
 GOD_API god_status god_build_index(const god_params* prm, const uint8_t* ref, const uint64_t* ref_offsets,
                                    uint32_t n_refs, const god_cutoff* cutoff, god_index** out, god_stream stream);
 GOD_API god_status god_index_get_stats(const god_index* idx, god_index_stats* out_host);
