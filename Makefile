@@ -26,11 +26,11 @@ build/checked/%.o: $(PKG)/csrc/%.cu $(CU_HDRS)
 
 $(PKG)/lib/libgod_checked.so: $(CK_OBJS)
 	@mkdir -p $(PKG)/lib
-	$(NVCC) $(ARCH) -shared -Xcompiler -fPIC $(CK_OBJS) -o $@ -lcudart
+	$(NVCC) $(ARCH) -shared -Xcompiler -fPIC $(CK_OBJS) -o $@ -lcudart -ldl
 
 $(PKG)/lib/libgod.so: $(CU_OBJS)
 	@mkdir -p $(PKG)/lib
-	$(NVCC) $(ARCH) -shared -Xcompiler -fPIC $(CU_OBJS) -o $@ -lcudart
+	$(NVCC) $(ARCH) -shared -Xcompiler -fPIC $(CU_OBJS) -o $@ -lcudart -ldl
 
 oracle/liboracle.so: oracle/oracle.c oracle/oracle.h
 	gcc -O2 -std=c11 -shared -fPIC -Wall -Wextra -o $@ oracle/oracle.c

@@ -420,6 +420,7 @@ struct SeedPipe {
     set_copies_in_flight(true);
     struct Reset { ~Reset() { set_copies_in_flight(false); } } reset_flag;
     for (uint32_t b = 0; b < n_batches; b++) {
+      NvtxRange nvtx("seed batch");
       PipeSlot& sl = slot[b % PIPE_SLOTS];
       const uint64_t r0 = r_begin(b), r1 = r_begin(b + 1), nb = r1 - r0;
       GOD_CUDA(cudaStreamWaitEvent(st, sl.h2d_done, 0));
@@ -607,6 +608,7 @@ GOD_API god_status god_minimizers(const god_params* prm, const uint8_t* seq, con
 static void build_index_entry(const god_params* prm, const uint8_t* ref, const uint64_t* ref_offsets, uint32_t n_refs,
                               const god_cutoff* cutoff, god_index** out, god_stream stream,
                               const std::function<void()>& after_ref_queued) {
+  NvtxRange nvtx("god_build_index");
   Params P = make_params(prm);
   GOD_REQUIRE(ref_offsets && out && cutoff, "NULL argument");
   GOD_REQUIRE(cutoff->mode <= 1, "cutoff mode must be 0 (fraction) or 1 (max_occ)");
@@ -738,6 +740,7 @@ GOD_API void god_index_free(god_index* idx) {
 static void seed_entry(const god_index* idx, const uint8_t* reads, const uint64_t* read_offsets, uint32_t n_reads,
                        god_phase_mode mode, uint8_t* phases, uint32_t t, void* anchors, bool compact,
                        uint64_t* anchor_offsets, uint64_t cap, uint64_t* needed, god_stream stream) {
+  NvtxRange nvtx("god_seed_reads");
   GOD_REQUIRE(idx && read_offsets && phases && anchor_offsets && needed, "NULL argument");
   GOD_REQUIRE(mode == GOD_PHASE_SELECT || mode == GOD_PHASE_GIVEN, "mode must be SELECT or GIVEN");
   GOD_REQUIRE(t >= 1, "t must be >= 1");
@@ -823,6 +826,7 @@ GOD_API god_status god_build_index_and_seed(const god_params* prm, const uint8_t
                                             void* anchors, uint64_t* anchor_offsets, uint64_t cap, uint64_t* needed,
                                             god_stream stream) {
   return guarded([&] {
+    NvtxRange nvtx("god_build_index_and_seed");
     GOD_REQUIRE(out_index && read_offsets && phases && anchor_offsets && needed, "NULL argument");
     GOD_REQUIRE(mode == GOD_PHASE_SELECT || mode == GOD_PHASE_GIVEN, "mode must be SELECT or GIVEN");
     GOD_REQUIRE(t >= 1, "t must be >= 1");

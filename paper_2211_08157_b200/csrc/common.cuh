@@ -3,6 +3,7 @@
 #include <cstdio>
 #include <cuda_runtime.h>
 #include <cuda/atomic>
+#include <nvtx3/nvToolsExt.h>
 #include <stdint.h>
 #include <string>
 #include <mutex>
@@ -271,6 +272,14 @@ struct ProfScope {
 // Work units (e.g. k-mer start positions) processed by the launches named `name`, reported by
 // god_profile_units for the roofline of bench.py (recorded only while profiling is on).
 void prof_add_units(const char* name, uint64_t units);
+// NVTX range over a host scope (API entry points and the stages inside them; SURVEY §5 tracing): shows
+// up on the Nsight timeline, costs one predicted branch when no tool is attached
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 #define GOD_LAUNCH(NAME, KERNEL, GRID, BLOCK, SMEM, ST, ...)      \
   do {                                                           \
     ::god::ProfScope ps_(NAME, ST);                              \

@@ -1705,6 +1705,7 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
   memset(&ix->st, 0, sizeof(ix->st));
   ix->st.k = P.k; ix->st.w = P.w; ix->st.p = P.pat.p; ix->st.x = P.pat.x;
   // K1: reference minimizers, position order (phase 0, global positions)
+  NvtxRange nvtx12("stage 1+2: sparsify + minimizers (K1)");
   JobSet js = make_jobs(P, ref_offsets, n_refs, nullptr, 0, 0, true, st, scr);
   Records rec;
   const uint64_t est = js.total_pos / (uint64_t)(P.w + 1) * 2 + js.total_pos / 8 + 4096;
@@ -1713,6 +1714,8 @@ void build_index(const Params& P, const uint8_t* ref, const uint64_t* ref_offset
   run_extract(P, ref, js.seq_bytes, js.jobs, js.kb, js.n, js.total_pos, false, false, rec, st, scr, est, "extract_ref",
               js.x2p(), bin_sort ? ORDER_NONE : ORDER_GLOBAL, ss);
   const uint64_t n = rec.n;
+  nvtxRangePop();  // (nvtx12's destructor pops the range pushed next)
+  nvtxRangePushA("stage 3: sort, count, cutoff, table");
   // K2: stable LSD radix sort on the 2k hash bits
   uint64_t* k0 = rec.hz;
   uint32_t* v0 = rec.pos;

@@ -411,6 +411,7 @@ static void probe_all(const IndexView& v, Records& rec, cudaStream_t st, Scratch
 uint64_t seed_reads(const god_index* ix, const uint8_t* reads, const uint64_t* offsets, uint32_t n_reads,
                     god_phase_mode mode, uint8_t* phases, uint32_t t, god_anchor* anchors, uint64_t* anchor_offsets,
                     uint64_t cap, cudaStream_t st, uint32_t rid_base) {
+  NvtxRange nvtx("stage 4: phase selection + seeding");
   Scratch scr(st);
   const Params& P = ix->P;
   const uint32_t p = P.pat.p;
