@@ -201,3 +201,51 @@ def test_digest_parity(config, pattern):
           "n_reads": gold["n_reads"], "ref_bp": gold["ref_bp"], "seconds": round(time.time() - t0, 1)})
     assert not missing, f"digests not compared: {missing}"
     assert not fails, "; ".join(fails)
+
+
+@pytest.mark.parametrize("config,pattern", [("tiny", "10"), ("human", "10")], ids=["tiny-10", "human-10"])
+def test_digest_parity_host_call(config, pattern):
+    """The e2e launch configuration bench.py times: pinned HOST buffers through ONE
+    god_build_index_and_seed call (reference streamed up under K1, read batches queued behind it,
+    8-byte anchors streamed back).  The index dump, the SELECT phases, the anchor counts and the
+    canonically sorted anchors of all reads against the same oracle digests."""
+    gold = json.load(open(os.path.join(GOLD, f"{config}_{pattern}.json")))
+    D = gold["digests"]
+    chunk = D["anchors"]["chunk_records"]
+    t0 = time.time()
+    cfg = synth.make_config(config)
+    assert hashlib.sha256(cfg.ref.tobytes()).hexdigest() == gold["inputs"]["ref_sha256"]
+    assert hashlib.sha256(cfg.reads.seq.tobytes()).hexdigest() == gold["inputs"]["reads_sha256"]
+    pin = lambda a: torch.from_numpy(a).pin_memory().numpy()  # noqa: E731
+    ref, roff, rs, ro = pin(cfg.ref), pin(cfg.ref_offsets), pin(cfg.reads.seq), pin(cfg.reads.offsets)
+    fails, done = [], []
+
+    def check(name, sha):
+        if compare(name, sha, D[name], fails):
+            done.append(name)
+
+    ix, an, ao, ph = god.god_build_index_and_seed(ref, roff, rs, ro, pattern, gold["k"], gold["w"],
+                                                  cutoff=tuple(gold["cutoff"]), t=gold["t"], compact=True,
+                                                  cap=gold["n_anchors"] + 1024)
+    st = ix.stats()
+    for f, v in gold["index_stats"].items():
+        if st[f] != v:
+            fails.append(f"index_stats.{f}: {st[f]} vs oracle {v}")
+    h, p, z = ix.dump(device=True)
+    check("index_dump", sha_records17(h, p, z, chunk))
+    del h, p, z
+    ix.free()
+    torch.cuda.empty_cache()
+    check("phases", sha_array(np.asarray(ph), chunk))
+    cnts = np.diff(np.asarray(ao)).astype("<u8")
+    check("anchor_counts", sha_array(cnts, chunk))
+    # 8-B anchors -> (ref_pos, read_pos, read_id, strand) on the device (read id = the anchor's segment)
+    c = torch.from_numpy(np.ascontiguousarray(an).view(np.uint32).reshape(-1, 2).astype(np.int64)).cuda()
+    rid = torch.repeat_interleave(torch.arange(cnts.size, device="cuda"), torch.from_numpy(cnts.astype(np.int64)).cuda())
+    full = torch.stack([c[:, 0], c[:, 1] & 0x7FFFFFFF, rid, c[:, 1] >> 31], dim=1)
+    del c, rid
+    check("anchors", sha_anchors(full, chunk))
+    _log({"config": config, "pattern": pattern, "call": "god_build_index_and_seed (host buffers)", "bit_exact": not fails,
+          "compared": sorted(done), "failures": fails, "seconds": round(time.time() - t0, 1)})
+    assert not fails, "; ".join(fails)
+    assert sorted(done) == ["anchor_counts", "anchors", "index_dump", "phases"]
